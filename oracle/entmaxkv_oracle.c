@@ -1,0 +1,449 @@
+/*
+ * entmaxkv_oracle.c -- plain, slow, single-threaded CPU oracle for the EntmaxKV
+ * sparse alpha-entmax decode step (arxiv 2605.21649).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in the product path (paper_2605_21649_b200/,
+ * libentmaxkv.so) links, loads or calls this file.  Only tests/, bench.py's
+ * cpu_baseline / --impl reference leg and __graft_entry__.smoke() may use it.
+ * It shares no code, header, table or constant generator with the CUDA path.
+ *
+ * Citations: "P:L" = /root/reference/PAPER.md line L (paper LaTeX source),
+ * "S:L" = SPEC.md line L.  Readings of the paper where it is silent are listed in
+ * DESIGN.md section "Readings" and referenced here as R<n>.
+ *
+ * Precision (the paper fixes none):
+ *   - scores s_j, page bounds and Gaussian moments are fp32 with the canonical
+ *     summation order of DESIGN.md R1 ("dot16x8"), because they decide integers
+ *     (top-k membership, page selection) and both sides must take that decision
+ *     in the same precision (the kernel's);
+ *   - everything downstream of the scores (z = (alpha-1) s, tau, support, p, o,
+ *     delta, rho, tau_hat, truncated Gaussian moments) is fp64.
+ *
+ * Parity status: every exported function is pinned by tests/test_oracle_pins.py
+ * except where its comment says "parity unpinned".
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_D 128          /* head dim supported by the canonical order (R1) */
+
+/* ------------------------------------------------------------------------- */
+/* R1: canonical fp32 dot product over d = 128 ("dot16x8").                   */
+/*   partial[c] = fma-chain over x[8c..8c+7]*y[8c..8c+7], c = 0..15, from +0   */
+/*   then pairwise: level 1 c + (c+8) (c<8); level 2 c + (c+4) (c<4);          */
+/*   level 3 c + (c+2) (c<2); level 4 c0 + c1.                                 */
+/* This is one fixed evaluation order of  q^T k.       */
+/* ------------------------------------------------------------------------- */
+float orc_dot_canon(const float *x, const float *y)
+{
+    float part[16];
+    for (int c = 0; c < 16; ++c) {
+        float acc = 0.0f;
+        for (int i = 8 * c; i < 8 * c + 8; ++i)
+            acc = fmaf(x[i], y[i], acc);
+        part[c] = acc;
+    }
+    for (int c = 0; c < 8; ++c) part[c] = part[c] + part[c + 8];
+    for (int c = 0; c < 4; ++c) part[c] = part[c] + part[c + 4];
+    for (int c = 0; c < 2; ++c) part[c] = part[c] + part[c + 2];
+    return part[0] + part[1];
+}
+
+/* c_d = fl32(1/sqrt(d)); the score is fl32(dot * c_d) (R2: scale after the dot). */
+static float scale_cd(void) { return (float)(1.0 / sqrt((double)ORC_D)); }
+
+/* s_j = q^T k_j / sqrt(d) */
+float orc_token_score(const float *q, const float *k)
+{
+    return orc_dot_canon(q, k) * scale_cd();
+}
+
+/* ------------------------------------------------------------------------- */
+/* Page metadata (R5 clamp per S:175).                             */
+/* keys: [c][d] the page's tokens in append order.                            */
+/*   kmin/kmax: coordinate-wise min/max                           */
+/*   ksum = sum_t k_t (fp32, t ascending), ksumsq = sum_t k_t*k_t (fma chain)  */
+/*   kavg = ksum / c                                  */
+/*   kvar = max(0, ksumsq/c - kavg*kavg) = k_std^2                */
+/* ------------------------------------------------------------------------- */
+void orc_page_stats(const float *keys, int c, int d, float *kmin, float *kmax,
+                    float *ksum, float *ksumsq, float *kavg, float *kvar)
+{
+    for (int i = 0; i < d; ++i) {
+        float mn = keys[i], mx = keys[i], s = 0.0f, ss = 0.0f;
+        for (int t = 0; t < c; ++t) {
+            float v = keys[(size_t)t * d + i];
+            if (v < mn) mn = v;
+            if (v > mx) mx = v;
+            s = s + v;
+            ss = fmaf(v, v, ss);
+        }
+        float cf = (float)c;
+        float avg = s / cf;
+        float m2 = ss / cf;
+        float var = m2 - avg * avg;
+        if (!(var > 0.0f)) var = 0.0f;
+        kmin[i] = mn; kmax[i] = mx; ksum[i] = s; ksumsq[i] = ss;
+        kavg[i] = avg; kvar[i] = var;
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* Query-aware page scoring for ONE query head (kv head kvh) of one sequence. */
+/*  box  = (1/sqrt d) sum_i max(q_i kmin_i, q_i kmax_i)  Eq. box-page-bound    */
+/*         (P:321-333); evaluated as dot16x8(q, kext), kext_i = q_i>=0 ? kmax  */
+/*         : kmin (the max of the two products, Prop. B.1 proof P:815).        */
+/*  mu   = q^T kavg / sqrt d                     */
+/*  sig2 = (1/d) sum_i q_i^2 kstd_i^2                     */
+/* meta arrays: [n_phys][Hkv][d]; page_row: logical page -> physical page.    */
+/* modes: bit0 box, bit1 gaussian.                                            */
+/* ------------------------------------------------------------------------- */
+void orc_score_pages(const float *q, int kvh, int Hkv, const float *kmin,
+                     const float *kmax, const float *kavg, const float *kvar,
+                     const int32_t *page_row, int M, int modes,
+                     float *box, float *mu, float *sigma2)
+{
+    const int d = ORC_D;
+    float kext[ORC_D], q2[ORC_D];
+    for (int i = 0; i < d; ++i) q2[i] = q[i] * q[i];
+    for (int p = 0; p < M; ++p) {
+        size_t off = ((size_t)page_row[p] * Hkv + kvh) * d;
+        if (modes & 1) {
+            for (int i = 0; i < d; ++i)
+                kext[i] = (q[i] >= 0.0f) ? kmax[off + i] : kmin[off + i];
+            box[p] = orc_dot_canon(q, kext) * scale_cd();
+        }
+        if (modes & 2) {
+            mu[p] = orc_dot_canon(q, kavg + off) * scale_cd();
+            sigma2[p] = orc_dot_canon(q2, kvar + off) * (1.0f / (float)d);
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* Top-k page selection: the min(k,M) pages with the largest box   */
+/* score; tie -> lower page index (R3).  Output ascending page index.   */
+/* ------------------------------------------------------------------------- */
+typedef struct { double key; int32_t idx; } orc_kv;
+static int cmp_desc_then_idx(const void *a, const void *b)
+{
+    const orc_kv *x = a, *y = b;
+    if (x->key > y->key) return -1;
+    if (x->key < y->key) return 1;
+    return (x->idx < y->idx) ? -1 : (x->idx > y->idx);
+}
+static int cmp_i32(const void *a, const void *b)
+{
+    int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+    return (x < y) ? -1 : (x > y);
+}
+int orc_topk(const float *score, int M, int k, int32_t *out)
+{
+    if (k > M) k = M;
+    orc_kv *v = malloc(sizeof(orc_kv) * (size_t)(M > 0 ? M : 1));
+    for (int p = 0; p < M; ++p) { v[p].key = (double)score[p]; v[p].idx = p; }
+    qsort(v, (size_t)M, sizeof(orc_kv), cmp_desc_then_idx);
+    for (int i = 0; i < k; ++i) out[i] = v[i].idx;
+    qsort(out, (size_t)k, sizeof(int32_t), cmp_i32);
+    free(v);
+    return k;
+}
+
+/* ------------------------------------------------------------------------- */
+/* alpha-entmax (Eq. entmax-def, support Eq. P:137-148, App. A).    */
+/* z_i = (alpha-1) s_i is passed in.  beta = 1/(alpha-1).                      */
+/* Support by the threshold-free criterion (R9): with F(x) = sum_i (z_i-x)_+^b */
+/* strictly decreasing below max z and F(tau) = 1,  i in S  <=>  F(z_i) < 1.   */
+/* Evaluated on z sorted descending: F(z_(k)) = sum_{i<k} (z_(i)-z_(k))^beta,   */
+/* non-decreasing in k, so the support is the prefix before the first F >= 1.  */
+/* tau: beta=1 (sparsemax) (S1-1)/k; beta=2 m - sqrt((1-ss)/k); otherwise      */
+/* bisection on sum_{i in S}(z_i - tau)^beta = 1.  p_i = (z_i - tau)^beta.     */
+/* ------------------------------------------------------------------------- */
+static double powb(double x, double beta)
+{
+    if (beta == 1.0) return x;
+    if (beta == 2.0) return x * x;
+    if (beta == 3.0) return (x * x) * x;
+    if (beta == 4.0) { double x2 = x * x; return x2 * x2; }
+    return pow(x, beta);
+}
+static int cmp_desc_d(const void *a, const void *b)
+{
+    const orc_kv *x = a, *y = b;
+    if (x->key > y->key) return -1;
+    if (x->key < y->key) return 1;
+    return (x->idx < y->idx) ? -1 : (x->idx > y->idx);
+}
+
+int orc_entmax(const double *z, int n, double alpha, double *p, double *tau_out)
+{
+    const double beta = 1.0 / (alpha - 1.0);
+    if (n <= 0) { if (tau_out) *tau_out = NAN; return 0; }
+    orc_kv *v = malloc(sizeof(orc_kv) * (size_t)(n > 0 ? n : 1));
+    for (int i = 0; i < n; ++i) { v[i].key = z[i]; v[i].idx = i; }
+    qsort(v, (size_t)n, sizeof(orc_kv), cmp_desc_d);
+    int k;
+    for (k = 0; k < n; ++k) {
+        double x = v[k].key, F = 0.0;
+        for (int i = 0; i < k; ++i) F += powb(v[i].key - x, beta);
+        if (!(F < 1.0)) break;
+    }
+    double tau;
+    if (beta == 1.0) {
+        double s1 = 0.0;
+        for (int i = 0; i < k; ++i) s1 += v[i].key;
+        tau = (s1 - 1.0) / (double)k;
+    } else if (beta == 2.0) {
+        double s1 = 0.0, ss = 0.0;
+        for (int i = 0; i < k; ++i) s1 += v[i].key;
+        double m = s1 / (double)k;
+        for (int i = 0; i < k; ++i) ss += (v[i].key - m) * (v[i].key - m);
+        tau = m - sqrt((1.0 - ss) / (double)k);
+    } else {
+        double hi = v[k - 1].key, lo = v[0].key - 1.0;
+        for (int it = 0; it < 400; ++it) {
+            double mid = 0.5 * (lo + hi);
+            if (mid <= lo || mid >= hi) break;
+            double G = 0.0;
+            for (int i = 0; i < k; ++i) G += powb(v[i].key - mid, beta);
+            if (G >= 1.0) lo = mid; else hi = mid;
+        }
+        tau = 0.5 * (lo + hi);
+    }
+    for (int i = 0; i < n; ++i) p[i] = 0.0;
+    for (int i = 0; i < k; ++i) {
+        double x = v[i].key - tau;
+        p[v[i].idx] = x > 0.0 ? powb(x, beta) : 0.0;
+    }
+    free(v);
+    if (tau_out) *tau_out = tau;
+    return k;
+}
+
+/* softmax, fp64 with max subtraction. Returns log-normalizer. */
+double orc_softmax(const double *s, int n, double *p)
+{
+    double mx = s[0], sum = 0.0;
+    for (int i = 1; i < n; ++i) if (s[i] > mx) mx = s[i];
+    for (int i = 0; i < n; ++i) { p[i] = exp(s[i] - mx); sum += p[i]; }
+    for (int i = 0; i < n; ++i) p[i] /= sum;
+    return mx + log(sum);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Attention over a page set for ONE query head of one sequence              */
+/* (C_tok = union of the selected pages' tokens; p~ = transform of  */
+/* {s_j : j in C_tok}; o~ = sum_j p~_j v_j; p~_j = 0 outside C_tok).           */
+/* Kp, Vp: [n_phys][Hkv][P][d]; pages: logical page ids (any order, unique).   */
+/* transform: 0 = alpha-entmax, 1 = softmax.                                   */
+/* Outputs: o[dv] (fp64), *tau (entmax tau or softmax log-normalizer),         */
+/* p_tok[seq_len] (optional; dense over the sequence, 0 outside C_tok),        */
+/* s_tok[seq_len] (optional; fp32 scores of C_tok tokens, untouched elsewhere).*/
+/* Returns the support size (entmax) or |C_tok| (softmax).                      */
+/* ------------------------------------------------------------------------- */
+int orc_attend(const float *q, const float *Kp, const float *Vp,
+               const int32_t *page_row, int seq_len, int kvh, int Hkv, int P,
+               int dv, const int32_t *pages, int n_pages, double alpha,
+               int transform, double *o, double *tau, double *p_tok,
+               float *s_tok)
+{
+    const int d = ORC_D;
+    int cap = n_pages * P;
+    int32_t *tok = malloc(sizeof(int32_t) * (size_t)(cap > 0 ? cap : 1));
+    double *z = malloc(sizeof(double) * (size_t)(cap > 0 ? cap : 1));
+    double *pr = malloc(sizeof(double) * (size_t)(cap > 0 ? cap : 1));
+    int n = 0;
+    for (int ip = 0; ip < n_pages; ++ip) {
+        int lp = pages[ip];
+        for (int t = 0; t < P; ++t) {
+            int j = lp * P + t;
+            if (j >= seq_len) break;
+            size_t off = (((size_t)page_row[lp] * Hkv + kvh) * P + t) * d;
+            float s = orc_token_score(q, Kp + off);
+            if (s_tok) s_tok[j] = s;
+            tok[n] = j;
+            z[n] = (transform == 0) ? (alpha - 1.0) * (double)s : (double)s;
+            ++n;
+        }
+    }
+    int ret;
+    if (n == 0) ret = 0, *tau = NAN;
+    else if (transform == 0) ret = orc_entmax(z, n, alpha, pr, tau);
+    else { *tau = orc_softmax(z, n, pr); ret = n; }
+    for (int i = 0; i < dv; ++i) o[i] = 0.0;
+    if (p_tok) for (int j = 0; j < seq_len; ++j) p_tok[j] = 0.0;
+    for (int m = 0; m < n; ++m) {
+        int j = tok[m];
+        if (p_tok) p_tok[j] = pr[m];
+        if (pr[m] == 0.0) continue;
+        int lp = j / P, t = j % P;
+        size_t off = (((size_t)page_row[lp] * Hkv + kvh) * P + t) * dv;
+        for (int i = 0; i < dv; ++i) o[i] += pr[m] * (double)Vp[off + i];
+    }
+    free(tok); free(z); free(pr);
+    return ret;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Metrics (P:165-171 delta, P:220-232 rho).  p_full over all n tokens,        */
+/* in_keep[j] != 0 iff j in C_tok.  rho = 1 when the support is empty. */
+/* ------------------------------------------------------------------------- */
+void orc_metrics(const double *p_full, const uint8_t *in_keep, int n,
+                 double *delta, double *rho, int32_t *recovered, int32_t *full_supp)
+{
+    double dl = 0.0; int rec = 0, sup = 0;
+    for (int j = 0; j < n; ++j) {
+        if (!in_keep[j]) dl += p_full[j];
+        if (p_full[j] > 0.0) { ++sup; if (in_keep[j]) ++rec; }
+    }
+    *delta = dl;
+    *rho = sup ? (double)rec / (double)sup : 1.0;
+    *recovered = rec; *full_supp = sup;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Gaussian-aware selection (App. D).                   */
+/* ------------------------------------------------------------------------- */
+static double Phi(double t) { return 0.5 * erfc(-t / sqrt(2.0)); }
+static double phi(double t) { return exp(-0.5 * t * t) / sqrt(2.0 * M_PI); }
+
+/* E[(Y)_+^beta], Y ~ N(muY, sigY^2), t = muY/sigY.  Closed forms of App. D:   */
+/*   beta=1: muY Phi + sigY phi               */
+/*   beta=2: (muY^2+sigY^2) Phi + muY sigY phi               */
+/*   beta=3: (muY^3+3muY sigY^2) Phi + (muY^2 sigY + 2 sigY^3) phi*/
+/*   beta=4: not printed in the paper (R15): the same truncated-moment        */
+/*           recursion M_k = muY M_{k-1} + (k-1) sigY^2 M_{k-2}, M_0 = Phi,     */
+/*           M_1 = muY Phi + sigY phi, which reproduces the three above.       */
+/*   sigY = 0: point mass [muY]_+^beta.                               */
+double orc_trunc_moment(int beta, double muY, double sigY)
+{
+    if (!(sigY > 0.0)) {
+        double x = muY > 0.0 ? muY : 0.0;
+        double r = 1.0;
+        for (int i = 0; i < beta; ++i) r *= x;
+        return r;
+    }
+    double t = muY / sigY, Ph = Phi(t), ph = phi(t);
+    switch (beta) {
+    case 1: return muY * Ph + sigY * ph;
+    case 2: return (muY * muY + sigY * sigY) * Ph + muY * sigY * ph;
+    case 3: return (muY * muY * muY + 3.0 * muY * sigY * sigY) * Ph
+                 + (muY * muY * sigY + 2.0 * sigY * sigY * sigY) * ph;
+    default: {
+        double m0 = Ph, m1 = muY * Ph + sigY * ph, m2 = 0.0;
+        for (int k = 2; k <= beta; ++k) {
+            m2 = muY * m1 + (double)(k - 1) * sigY * sigY * m0;
+            m0 = m1; m1 = m2;
+        }
+        return m1;
+    }
+    }
+}
+
+/* Approximate normalization mass  sum_p |P_p| E[g_alpha(S^(p); tau)]          */
+/* (Eq. gaussian-threshold-main), S^(p) ~ N(mu_p, sigma_p^2),        */
+/* Y = a S - tau: muY = a mu - tau, sigY = a sigma.              */
+double orc_gauss_mass(const float *mu, const float *sigma2, const int32_t *counts,
+                      int M, double alpha, double tau)
+{
+    double a = alpha - 1.0;
+    int beta = (int)lround(1.0 / a);
+    double m = 0.0;
+    for (int p = 0; p < M; ++p) {
+        double s = sqrt((double)sigma2[p]);
+        m += (double)counts[p] * orc_trunc_moment(beta, a * (double)mu[p] - tau, a * s);
+    }
+    return m;
+}
+
+/* tau_hat: the root of mass(tau) = 1.  The mass is continuous,  */
+/* non-increasing in tau and strictly decreasing where positive.       */
+/* Plain bracketing + bisection to fp64 resolution (the paper's Newton/Halley */
+/* is a faster route to the same root).  Returns 0 on success, -1 on a bracket */
+/* failure.                                                                    */
+int orc_gauss_tau(const float *mu, const float *sigma2, const int32_t *counts,
+                  int M, double alpha, double *tau_hat)
+{
+    double a = alpha - 1.0, top = -INFINITY;
+    for (int p = 0; p < M; ++p) {
+        double v = a * ((double)mu[p] + 8.0 * sqrt((double)sigma2[p]));
+        if (v > top) top = v;
+    }
+    double hi = top, w = 1.0;
+    int guard = 0;
+    while (orc_gauss_mass(mu, sigma2, counts, M, alpha, hi) >= 1.0) {
+        hi += w; w *= 2.0;
+        if (++guard > 200) return -1;
+    }
+    double lo = hi - 1.0;
+    w = 1.0; guard = 0;
+    while (orc_gauss_mass(mu, sigma2, counts, M, alpha, lo) < 1.0) {
+        lo -= w; w *= 2.0;
+        if (++guard > 200) return -1;
+    }
+    for (int it = 0; it < 400; ++it) {
+        double mid = 0.5 * (lo + hi);
+        if (mid <= lo || mid >= hi) break;
+        if (orc_gauss_mass(mu, sigma2, counts, M, alpha, mid) >= 1.0) lo = mid;
+        else hi = mid;
+    }
+    *tau_hat = 0.5 * (lo + hi);
+    return 0;
+}
+
+/* Phi^{-1}(u) by bisection on Phi (u in (0,1)); used for the page-max        */
+/* quantile q_page^{1/|P_p|} of Eq. gaussian-page-bound-main.      */
+double orc_norm_ppf(double u)
+{
+    /* symmetry Phi^{-1}(u) = -Phi^{-1}(1-u): bisect in the lower tail, where Phi */
+    /* (via erfc) keeps full relative precision; 1-u is exact for u in [0.5, 1].  */
+    if (u > 0.5) return -orc_norm_ppf(1.0 - u);
+    double lo = -40.0, hi = 40.0;
+    for (int it = 0; it < 400; ++it) {
+        double mid = 0.5 * (lo + hi);
+        if (mid <= lo || mid >= hi) break;
+        if (Phi(mid) < u) lo = mid; else hi = mid;
+    }
+    return 0.5 * (lo + hi);
+}
+
+/* Page rule (Eq. gaussian-selector-main):                          */
+/*   keep p iff (alpha-1) * sbar_G(p) > tau_hat - Delta,                       */
+/*   sbar_G = mu + sigma * zq[c_p],  zq[c] = Phi^{-1}(q_page^{1/c})*/
+/* sbar_G is evaluated as fmaf(sqrtf(sigma2), (float)zq[c], mu) (R14) and the   */
+/* comparison in fp64.  Empty selection -> argmax mu, lower index on ties (R6).*/
+/* Output ascending.  Returns the count.                                       */
+int orc_gauss_select(const float *mu, const float *sigma2, const int32_t *counts,
+                     int M, double alpha, double tau_hat, double margin,
+                     const double *zq /* [P+1], zq[c] */, int32_t *out)
+{
+    double a = alpha - 1.0;
+    int n = 0;
+    for (int p = 0; p < M; ++p) {
+        float sg = fmaf(sqrtf(sigma2[p]), (float)zq[counts[p]], mu[p]);
+        if (a * (double)sg > tau_hat - margin) out[n++] = p;
+    }
+    if (n == 0 && M > 0) {
+        int best = 0;
+        for (int p = 1; p < M; ++p) if (mu[p] > mu[best]) best = p;
+        out[n++] = best;
+    }
+    return n;
+}
+
+/* Certified dropped-mass bound (R16): with z_j <= a*box_p     */
+/* (Prop. B.1) and tau >= tau~ (sparse tau is a lower bound of the  */
+/* full tau), delta <= sum_{p not selected} c_p [a*box_p - tau~]_+^beta.        */
+double orc_delta_bar(const float *box, const int32_t *counts, const uint8_t *sel,
+                     int M, double alpha, double tau_sparse)
+{
+    double a = alpha - 1.0, beta = 1.0 / a, s = 0.0;
+    for (int p = 0; p < M; ++p) {
+        if (sel[p]) continue;
+        double x = a * (double)box[p] - tau_sparse;
+        if (x > 0.0) s += (double)counts[p] * powb(x, beta);
+    }
+    return s;
+}
