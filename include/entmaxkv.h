@@ -1,0 +1,219 @@
+/*
+ * entmaxkv.h -- C ABI of libentmaxkv.so, the B200 (sm_100a) EntmaxKV sparse
+ * alpha-entmax decode step (arxiv 2605.21649).
+ *
+ * Citations: "P:L" = PAPER.md line L; "S:L" = SPEC.md line L; R<n> = reading n
+ * in DESIGN.md section 2.
+ *
+ * Conventions (every entry point):
+ *  - Returns ekv_status; EKV_OK = 0.  Never throws, never synchronises the
+ *    stream, never allocates device memory.  entmaxkv_last_error() returns a
+ *    thread-local message for the last non-OK status of the calling thread.
+ *  - All tensor arguments are DEVICE pointers owned by the caller; they must
+ *    stay valid until the work enqueued on `stream` completes.  Scratch comes
+ *    from a caller-owned device workspace of entmaxkv_workspace_size() bytes
+ *    (256-byte aligned); distinct concurrent calls need distinct workspaces.
+ *  - Work is enqueued on `stream` (a cudaStream_t passed as void*; NULL = the
+ *    legacy default stream).  Calls are CUDA-graph capturable.
+ *  - Layouts are row-major, innermost dimension last.  Supported shapes:
+ *    head_dim = value_dim = 128 (R1), page_size = 16, n_kv_heads in {1,2,4,8,16},
+ *    G = n_q_heads / n_kv_heads in {1,2,4,8}, max_pages_per_seq <= 65536.
+ *    Anything else -> EKV_ERR_UNSUPPORTED.
+ *  - Precondition (not checked): inputs are finite.
+ */
+#ifndef ENTMAXKV_H
+#define ENTMAXKV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    EKV_OK = 0,
+    EKV_ERR_INVALID_ARG = 1,  /* bad sizes, alpha <= 1, k < 1, q_page outside (0,1), NULL pointers */
+    EKV_ERR_UNSUPPORTED = 2,  /* shape outside the supported set; Gaussian with non-integer beta */
+    EKV_ERR_CAPACITY = 3,     /* a caller buffer is too small */
+    EKV_ERR_EMPTY = 4,        /* empty cache */
+    EKV_ERR_CUDA = 5          /* a CUDA launch failed (message has cudaGetErrorString) */
+} ekv_status;
+
+typedef enum { EKV_BF16 = 0, EKV_F32 = 1 } ekv_dtype;
+typedef enum { EKV_ENTMAX = 0, EKV_SOFTMAX = 1 } ekv_transform;     /* P:128-136 / P:121-124 */
+typedef enum { EKV_TOPK = 0, EKV_GAUSS = 1, EKV_ALL = 2 } ekv_policy;
+enum { EKV_SCORE_BOX = 1, EKV_SCORE_GAUSS = 2 };
+
+/*
+ * Paged KV cache (PagedAttention layout).  Caller-owned device buffers.
+ *   k_pages  [n_phys_pages][n_kv_heads][page_size][head_dim]   dtype
+ *   v_pages  [n_phys_pages][n_kv_heads][page_size][value_dim]  dtype
+ *   kmin,kmax[n_phys_pages][n_kv_heads][head_dim]              dtype (exact copies)
+ *   ksum, ksumsq, kavg, kvar [n_phys_pages][n_kv_heads][head_dim]  fp32 (R5)
+ *   page_table [batch][max_pages_per_seq] int32: logical page -> physical page
+ *   seq_lens   [batch] int32 (device; append_kv increments it)
+ * Token j of sequence b lives in physical page page_table[b][j / P], slot j % P.
+ */
+typedef struct {
+    int32_t dtype;             /* ekv_dtype of K, V, kmin, kmax */
+    int32_t batch;
+    int32_t n_kv_heads;
+    int32_t head_dim;
+    int32_t value_dim;
+    int32_t page_size;
+    int32_t max_pages_per_seq;
+    int32_t n_phys_pages;
+    void *k_pages, *v_pages;
+    void *kmin, *kmax;
+    float *ksum, *ksumsq, *kavg, *kvar;
+    const int32_t *page_table;
+    int32_t *seq_lens;
+} ekv_cache;
+
+/* alpha > 1; transform = ekv_transform (softmax ignores alpha). */
+typedef struct {
+    float alpha;
+    int32_t transform;
+} ekv_attn_params;
+
+/*
+ * policy TOPK: k_pages >= 1 pages per query head (R3 tie-break).
+ * policy GAUSS: q_page in (0,1) page-max confidence, margin = Delta >= 0
+ *   (Eq. gaussian-selector-main); needs integer beta = 1/(alpha-1) in
+ *   {1,2,3,4} (App. D, R15), else EKV_ERR_UNSUPPORTED.
+ * policy ALL: every page (the full cache).
+ */
+typedef struct {
+    int32_t policy;
+    int32_t k_pages;
+    double q_page;
+    double margin;
+} ekv_select_params;
+
+/*
+ * Per-(b, q-head) decode statistics, all [batch][n_q_heads], any may be NULL.
+ *   tau        f64  exact alpha-entmax threshold over C_tok (R9)
+ *   supp_count i32  |S~| support size within C_tok (softmax: |C_tok|)
+ *   n_sel      i32  |C_page|
+ *   delta_bar  f64  certified dropped-mass bound (R16; top-k and Gaussian)
+ *   tau_hat    f64  Gaussian threshold estimate (GAUSS only)
+ * eval_exact != 0 additionally runs a full-cache pass (all K; R16) and fills
+ *   delta f64 exact dropped mass (Eq. delta),
+ *   recovered i32 |S cap C_tok|, full_supp i32 |S| (Eq. rho),
+ *   tau_full f64.
+ */
+typedef struct {
+    double *tau;
+    int32_t *supp_count;
+    int32_t *n_sel;
+    double *delta_bar;
+    double *tau_hat;
+    int32_t eval_exact;
+    double *delta;
+    int32_t *recovered;
+    int32_t *full_supp;
+    double *tau_full;
+} ekv_decode_stats;
+
+/* Last error message of the calling thread ("" if none). */
+const char *entmaxkv_last_error(void);
+
+/* Library version string. */
+const char *entmaxkv_version(void);
+
+/*
+ * Workspace bytes needed by score/select/sparse_attend/full_attend/decode for
+ * this cache shape, n_q_heads and selection policy (sel may be NULL = ALL).
+ */
+size_t entmaxkv_workspace_size(const ekv_cache *cache, int32_t n_q_heads,
+                               const ekv_select_params *sel);
+
+/*
+ * Selection capacity (pages per query head) that page_idx buffers must hold:
+ * min(k_pages, max_pages) for TOPK, max_pages for GAUSS/ALL.
+ */
+int32_t entmaxkv_select_capacity(const ekv_cache *cache, const ekv_select_params *sel);
+
+/*
+ * a0: append n_tokens tokens per sequence.  k_new [batch][n_tokens][n_kv_heads][head_dim],
+ * v_new [batch][n_tokens][n_kv_heads][value_dim] (cache dtype).  Token t of
+ * sequence b goes to position seq_lens[b] + t; page_table[b][(seq_lens[b]+t)/P]
+ * must already map a physical page (precondition).  Updates kmin/kmax/ksum/ksumsq
+ * incrementally and rewrites kavg/kvar of the touched page (R5), then
+ * seq_lens[b] += n_tokens.
+ */
+ekv_status entmaxkv_append_kv(const ekv_cache *cache, const void *k_new, const void *v_new,
+                              int32_t n_tokens, void *stream);
+
+/*
+ * a0 (bulk): recompute kmin/kmax/ksum/ksumsq/kavg/kvar of every valid page of
+ * every sequence from the stored keys (identical bits to incremental appends).
+ */
+ekv_status entmaxkv_rebuild_page_stats(const ekv_cache *cache, void *stream);
+
+/*
+ * a1: page scores for every query head.  q [batch][n_q_heads][head_dim] (cache dtype).
+ * modes = EKV_SCORE_BOX and/or EKV_SCORE_GAUSS.  Outputs (NULL if not requested)
+ * [batch][n_q_heads][max_pages_per_seq] fp32; entries for pages >= ceil(seq_len/P)
+ * are left untouched.
+ *   box    = fl32(dot16x8(q, kext) * c_d), kext_i = q_i >= 0 ? kmax_i : kmin_i
+ *            (Eq. box-page-bound, R1, R2)
+ *   mu     = fl32(dot16x8(q, kavg) * c_d)
+ *   sigma2 = fl32(dot16x8(q*q, kvar) * (1/d))
+ */
+ekv_status entmaxkv_score_pages(const ekv_cache *cache, const void *q, int32_t n_q_heads,
+                                int32_t modes, float *box, float *mu, float *sigma2,
+                                void *workspace, void *stream);
+
+/*
+ * a2 / a2': page selection per (b, q-head).  Inputs are score_pages outputs
+ * (box for TOPK; mu, sigma2 for GAUSS).  Outputs:
+ *   page_idx [batch][n_q_heads][sel_stride] int32, ascending logical page ids;
+ *   n_sel    [batch][n_q_heads] int32;
+ *   tau_hat  [batch][n_q_heads] f64 (GAUSS; may be NULL).
+ * sel_stride >= entmaxkv_select_capacity(), else EKV_ERR_CAPACITY.
+ */
+ekv_status entmaxkv_select(const ekv_cache *cache, int32_t n_q_heads, const float *box,
+                           const float *mu, const float *sigma2, const ekv_select_params *sel,
+                           float alpha, int32_t *page_idx, int32_t *n_sel, int32_t sel_stride,
+                           double *tau_hat, void *workspace, void *stream);
+
+/*
+ * a3 (+a6): attention of every (b, q-head) over its own page list:
+ * C_tok = tokens of page_idx[b][h][0..n_sel) below seq_len; p~ = alpha-entmax (exact
+ * tau, R8/R9) or softmax of {s_j : j in C_tok}; out = sum p~_j v_j / sum p~_j (R12).
+ * K of the KV-group union is read once (R17); V only for support tokens.
+ *   out  [batch][n_q_heads][value_dim] fp32
+ *   tau  [batch][n_q_heads] f64 (softmax: log-normaliser)   (may be NULL)
+ *   supp [batch][n_q_heads] int32                            (may be NULL)
+ * page lists must be ascending and unique.
+ */
+ekv_status entmaxkv_sparse_attend(const ekv_cache *cache, const void *q, int32_t n_q_heads,
+                                  const int32_t *page_idx, const int32_t *n_sel,
+                                  int32_t sel_stride, const ekv_attn_params *attn,
+                                  float *out, double *tau, int32_t *supp,
+                                  void *workspace, void *stream);
+
+/* a5 (+a6): the dense baseline: the same attention over every page (all K read). */
+ekv_status entmaxkv_full_attend(const ekv_cache *cache, const void *q, int32_t n_q_heads,
+                                const ekv_attn_params *attn, float *out, double *tau,
+                                int32_t *supp, void *workspace, void *stream);
+
+/*
+ * Fused decode step: score_pages -> select -> sparse_attend (+ statistics a4),
+ * all enqueued on `stream` with no host synchronisation.
+ * out [batch][n_q_heads][value_dim] fp32.  stats may be NULL.
+ */
+ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_heads,
+                           const ekv_select_params *sel, const ekv_attn_params *attn,
+                           float *out, ekv_decode_stats *stats, void *workspace, void *stream);
+
+/* Number of kernels the last successful entmaxkv_decode / full_attend call on this
+ * thread enqueued (for launch accounting). */
+int32_t entmaxkv_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ENTMAXKV_H */

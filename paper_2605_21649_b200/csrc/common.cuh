@@ -1,0 +1,262 @@
+// common.cuh -- device helpers for libentmaxkv (sm_100a).
+// Numerics follow DESIGN.md section 2 (R1 canonical dot16x8, R5 metadata, R9 support).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace ekv {
+
+constexpr int kD = 128;   // head_dim = value_dim (R1)
+constexpr int kP = 16;    // page size
+constexpr float kCd = 0x1.6a09e6p-4f;   // fl32(1/sqrt(128)) (R2)
+
+struct CacheView {
+    int dtype, B, Hkv, maxp, nphys;
+    const void *K, *V;
+    void *Kw, *Vw;            // writable aliases (append)
+    void *kmin, *kmax;
+    float *ksum, *ksumsq, *kavg, *kvar;
+    const int32_t *page_table;
+    int32_t *seq_lens;
+};
+
+__device__ __forceinline__ int n_pages_of(int L) { return (L + kP - 1) / kP; }
+
+// ---------------------------------------------------------------- element access
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+template <typename T> struct Elem;
+template <> struct Elem<__nv_bfloat16> {
+    // 8 consecutive elements starting at p (16-byte aligned) -> fp32 (exact)
+    static __device__ __forceinline__ void load8(const __nv_bfloat16 *p, float (&x)[8]) {
+        uint4 v = *reinterpret_cast<const uint4 *>(p);
+        x[0] = bf_lo(v.x); x[1] = bf_hi(v.x); x[2] = bf_lo(v.y); x[3] = bf_hi(v.y);
+        x[4] = bf_lo(v.z); x[5] = bf_hi(v.z); x[6] = bf_lo(v.w); x[7] = bf_hi(v.w);
+    }
+    static __device__ __forceinline__ void load8_nc(const __nv_bfloat16 *p, float (&x)[8]) {
+        uint4 v = __ldg(reinterpret_cast<const uint4 *>(p));
+        x[0] = bf_lo(v.x); x[1] = bf_hi(v.x); x[2] = bf_lo(v.y); x[3] = bf_hi(v.y);
+        x[4] = bf_lo(v.z); x[5] = bf_hi(v.z); x[6] = bf_lo(v.w); x[7] = bf_hi(v.w);
+    }
+    static __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+    static __device__ __forceinline__ __nv_bfloat16 from_f(float f) { return __float2bfloat16_rn(f); }
+};
+template <> struct Elem<float> {
+    static __device__ __forceinline__ void load8(const float *p, float (&x)[8]) {
+        float4 a = *reinterpret_cast<const float4 *>(p);
+        float4 b = *reinterpret_cast<const float4 *>(p + 4);
+        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    }
+    static __device__ __forceinline__ void load8_nc(const float *p, float (&x)[8]) {
+        float4 a = __ldg(reinterpret_cast<const float4 *>(p));
+        float4 b = __ldg(reinterpret_cast<const float4 *>(p + 4));
+        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    }
+    static __device__ __forceinline__ float to_f(float v) { return v; }
+    static __device__ __forceinline__ float from_f(float f) { return f; }
+};
+
+// ---------------------------------------------------------------- R1: 16-lane reduce-scatter tree
+// Each lane of a 16-lane group holds the fma-chain partial of its 8-dim chunk
+// c = lane & 15 for G heads.  The tree pairs lanes (c, c^8), (c, c^4), (c, c^2),
+// (c, c^1) exactly like a butterfly; instead of reducing every head on every lane,
+// each split step keeps half of the heads (reduce-scatter), so G = 4 costs 5
+// shuffles instead of 16.  fp32 addition is commutative, so the result of head h is
+// bit-identical to the butterfly/oracle tree.
+template <int G, int O> struct RS {
+    static __device__ __forceinline__ void run(float *v, int lane) {
+        if constexpr (G > 1) {
+            const bool up = (lane & O) != 0;
+#pragma unroll
+            for (int i = 0; i < G / 2; ++i) {
+                float send = up ? v[i] : v[i + G / 2];
+                float keep = up ? v[i + G / 2] : v[i];
+                v[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, O));
+            }
+            if constexpr (O > 1) RS<G / 2, O / 2>::run(v, lane);
+        } else {
+            v[0] = __fadd_rn(v[0], __shfl_xor_sync(0xffffffffu, v[0], O));
+            if constexpr (O > 1) RS<1, O / 2>::run(v, lane);
+        }
+    }
+};
+template <int G> __device__ __forceinline__ float rs_reduce16(float (&v)[G], int lane) {
+    RS<G, 8>::run(v, lane);
+    return v[0];
+}
+// head index held by `lane` after rs_reduce16<G>
+template <int G> __device__ __forceinline__ int rs_head(int lane) {
+    int h = 0, n = G;
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) {
+        if (n > 1) { if (lane & o) h += n / 2; n >>= 1; }
+    }
+    return h;
+}
+// lanes that write (one per head per 16-lane group)
+template <int G> __device__ __forceinline__ bool rs_writer(int lane) {
+    return (lane & (16 / G - 1)) == 0;
+}
+
+// ---------------------------------------------------------------- ordered keys (R3)
+__device__ __forceinline__ uint32_t f2key(float f) {
+    uint32_t u = __float_as_uint(f);
+    if (u == 0x80000000u) u = 0u;             // -0 == +0
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ uint32_t ordered_f(float f) { return f2key(f); }
+__device__ __forceinline__ float key2f(uint32_t k) {
+    uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    return __uint_as_float(u);
+}
+
+// ---------------------------------------------------------------- powers (R9)
+__device__ __forceinline__ double powb(double x, double beta, int ib) {
+    switch (ib) {
+    case 1: return x;
+    case 2: return x * x;
+    case 3: return (x * x) * x;
+    case 4: { double x2 = x * x; return x2 * x2; }
+    default: return pow(x, beta);
+    }
+}
+__device__ __forceinline__ double powbm1(double x, double beta, int ib) {  // x^(beta-1)
+    switch (ib) {
+    case 1: return 1.0;
+    case 2: return x;
+    case 3: return x * x;
+    case 4: return (x * x) * x;
+    default: return pow(x, beta - 1.0);
+    }
+}
+
+// ---------------------------------------------------------------- block reductions (deterministic)
+template <int NT> __device__ __forceinline__ double block_sum_d(double v, double *sh) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (w == 0) {
+        r = (l < NT / 32) ? sh[l] : 0.0;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+        if (l == 0) sh[0] = r;
+    }
+    __syncthreads();
+    return sh[0];
+}
+template <int NT> __device__ __forceinline__ void block_sum2_d(double &a, double &b, double *sh) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) { sh[2 * w] = a; sh[2 * w + 1] = b; }
+    __syncthreads();
+    if (w == 0) {
+        double x = (l < NT / 32) ? sh[2 * l] : 0.0, y = (l < NT / 32) ? sh[2 * l + 1] : 0.0;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            x += __shfl_xor_sync(0xffffffffu, x, o);
+            y += __shfl_xor_sync(0xffffffffu, y, o);
+        }
+        if (l == 0) { sh[0] = x; sh[1] = y; }
+    }
+    __syncthreads();
+    a = sh[0]; b = sh[1];
+}
+template <int NT> __device__ __forceinline__ float block_max_f(float v, float *sh) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        float r = (l < NT / 32) ? sh[l] : -INFINITY;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) r = fmaxf(r, __shfl_xor_sync(0xffffffffu, r, o));
+        if (l == 0) sh[0] = r;
+    }
+    __syncthreads();
+    return sh[0];
+}
+template <int NT> __device__ __forceinline__ int block_sum_i(int v, int *sh) {
+    v = __reduce_add_sync(0xffffffffu, v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        int r = (l < NT / 32) ? sh[l] : 0;
+        r = __reduce_add_sync(0xffffffffu, r);
+        if (l == 0) sh[0] = r;
+    }
+    __syncthreads();
+    return sh[0];
+}
+// exclusive block scan of ints; returns exclusive prefix, total via *tot
+template <int NT> __device__ __forceinline__ int block_excl_scan(int v, int *sh, int *tot) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (l >= o) x += y;
+    }
+    __syncthreads();
+    if (l == 31) sh[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int s = (l < NT / 32) ? sh[l] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, s, o);
+            if (l >= o) s += y;
+        }
+        if (l < NT / 32) sh[l] = s;        // inclusive warp totals
+    }
+    __syncthreads();
+    int base = (w > 0) ? sh[w - 1] : 0;
+    *tot = sh[NT / 32 - 1];
+    return base + x - v;
+}
+
+// ---------------------------------------------------------------- TMA bulk copy + mbarrier (sm_90+/sm_100a)
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+}  // namespace ekv

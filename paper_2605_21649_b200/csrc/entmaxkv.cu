@@ -1,0 +1,482 @@
+// entmaxkv.cu -- host side of libentmaxkv.so: argument validation, workspace
+// carve-out and kernel launches behind the C ABI of include/entmaxkv.h.
+// Everything runs on the caller's stream; no allocation, no synchronisation.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "entmaxkv.h"
+#include "common.cuh"
+#include "kernels_meta.cuh"
+#include "kernels_select.cuh"
+#include "kernels_attend.cuh"
+
+using namespace ekv;
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+
+ekv_status fail(ekv_status st, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+ekv_status check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    ++g_launches;
+    return EKV_OK;
+}
+
+#define EKV_TRY(x)                       \
+    do {                                 \
+        ekv_status _s = (x);             \
+        if (_s != EKV_OK) return _s;     \
+    } while (0)
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+ekv_status check_cache(const ekv_cache *c, int Hq) {
+    if (!c) return fail(EKV_ERR_INVALID_ARG, "cache is NULL");
+    if (c->dtype != EKV_BF16 && c->dtype != EKV_F32) return fail(EKV_ERR_INVALID_ARG, "bad dtype %d", c->dtype);
+    if (c->head_dim != kD || c->value_dim != kD)
+        return fail(EKV_ERR_UNSUPPORTED, "head_dim/value_dim must be %d (got %d/%d)", kD, c->head_dim, c->value_dim);
+    if (c->page_size != kP) return fail(EKV_ERR_UNSUPPORTED, "page_size must be %d (got %d)", kP, c->page_size);
+    const int hk = c->n_kv_heads;
+    if (!(hk == 1 || hk == 2 || hk == 4 || hk == 8 || hk == 16))
+        return fail(EKV_ERR_UNSUPPORTED, "n_kv_heads must be 1,2,4,8,16 (got %d)", hk);
+    if (c->batch < 1 || c->max_pages_per_seq < 1 || c->n_phys_pages < 1)
+        return fail(EKV_ERR_INVALID_ARG, "batch/max_pages/n_phys must be >= 1");
+    if (c->max_pages_per_seq > 65536) return fail(EKV_ERR_UNSUPPORTED, "max_pages_per_seq > 65536");
+    if (Hq > 0) {
+        if (Hq % hk) return fail(EKV_ERR_INVALID_ARG, "n_q_heads %d not a multiple of n_kv_heads %d", Hq, hk);
+        const int G = Hq / hk;
+        if (!(G == 1 || G == 2 || G == 4 || G == 8)) return fail(EKV_ERR_UNSUPPORTED, "group size G=%d not in {1,2,4,8}", G);
+    }
+    if (!c->k_pages || !c->v_pages || !c->page_table || !c->seq_lens)
+        return fail(EKV_ERR_INVALID_ARG, "NULL cache buffer");
+    return EKV_OK;
+}
+
+CacheView view(const ekv_cache *c) {
+    CacheView v;
+    v.dtype = c->dtype; v.B = c->batch; v.Hkv = c->n_kv_heads; v.maxp = c->max_pages_per_seq;
+    v.nphys = c->n_phys_pages;
+    v.K = c->k_pages; v.V = c->v_pages; v.Kw = c->k_pages; v.Vw = c->v_pages;
+    v.kmin = c->kmin; v.kmax = c->kmax;
+    v.ksum = c->ksum; v.ksumsq = c->ksumsq; v.kavg = c->kavg; v.kvar = c->kvar;
+    v.page_table = c->page_table; v.seq_lens = c->seq_lens;
+    return v;
+}
+
+int sel_cap(const ekv_cache *c, const ekv_select_params *s) {
+    if (!s || s->policy != EKV_TOPK) return c->max_pages_per_seq;
+    return s->k_pages < c->max_pages_per_seq ? s->k_pages : c->max_pages_per_seq;
+}
+
+// ---------------------------------------------------------------- workspace layout
+struct Layout {
+    size_t box, mu, sigma2, page_idx, n_sel, tau_hat, upages, umask, ulen, scores, tok_list, p_list, n_list, full_out;
+    size_t sparse_total;   // end of the sparse region
+    size_t full_scores, total;
+    int cap, ucap, list_cap;
+};
+
+Layout layout(const ekv_cache *c, int Hq, const ekv_select_params *sel) {
+    Layout L;
+    const size_t B = c->batch, Hkv = c->n_kv_heads, maxp = c->max_pages_per_seq;
+    const int G = Hq / c->n_kv_heads;
+    L.cap = sel_cap(c, sel);
+    long long uc = (long long)G * L.cap;
+    L.ucap = (int)(uc < (long long)maxp ? uc : (long long)maxp);
+    L.list_cap = kCap;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o += align256(bytes); return r; };
+    L.box = take(B * Hq * maxp * 4);
+    L.mu = take(B * Hq * maxp * 4);
+    L.sigma2 = take(B * Hq * maxp * 4);
+    L.page_idx = take(B * Hq * (size_t)L.cap * 4);
+    L.n_sel = take(B * Hq * 4);
+    L.tau_hat = take(B * Hq * 8);
+    L.upages = take(B * Hkv * (size_t)L.ucap * 4);
+    L.umask = take(B * Hkv * (size_t)L.ucap);
+    L.ulen = take(B * Hkv * 4);
+    L.scores = take(B * Hq * (size_t)L.ucap * kP * 4);
+    L.tok_list = take(B * Hq * (size_t)L.list_cap * 4);
+    L.p_list = take(B * Hq * (size_t)L.list_cap * 8);
+    L.n_list = take(B * Hq * 4);
+    L.full_out = take(B * Hq * kD * 4);
+    L.sparse_total = o;
+    L.full_scores = take(B * Hq * maxp * kP * 4);
+    L.total = o;
+    return L;
+}
+
+template <typename P> P *at(void *ws, size_t off) { return reinterpret_cast<P *>(static_cast<char *>(ws) + off); }
+
+template <typename K> void set_smem(K kernel, int bytes) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+// ---------------------------------------------------------------- launch helpers
+template <typename T, int G>
+ekv_status launch_score_t(const CacheView &v, const void *q, int Hq, int modes, float *box, float *mu, float *s2,
+                          cudaStream_t st) {
+    const int ppc = 64;
+    dim3 grid((v.maxp + ppc - 1) / ppc, v.B);
+    const T *qq = static_cast<const T *>(q);
+    if (modes == 1) k_score<T, G, 1, 2><<<grid, 256, 0, st>>>(v, qq, Hq, ppc, box, mu, s2);
+    else if (modes == 2) k_score<T, G, 2, 2><<<grid, 256, 0, st>>>(v, qq, Hq, ppc, box, mu, s2);
+    else k_score<T, G, 3, 2><<<grid, 256, 0, st>>>(v, qq, Hq, ppc, box, mu, s2);
+    return check_launch("k_score");
+}
+template <typename T>
+ekv_status launch_score(const CacheView &v, const void *q, int Hq, int modes, float *box, float *mu, float *s2,
+                        cudaStream_t st) {
+    switch (Hq / v.Hkv) {
+    case 1: return launch_score_t<T, 1>(v, q, Hq, modes, box, mu, s2, st);
+    case 2: return launch_score_t<T, 2>(v, q, Hq, modes, box, mu, s2, st);
+    case 4: return launch_score_t<T, 4>(v, q, Hq, modes, box, mu, s2, st);
+    default: return launch_score_t<T, 8>(v, q, Hq, modes, box, mu, s2, st);
+    }
+}
+
+template <int NT, int KPT>
+void topk_go(const float *box, int Hq, int maxp, const int32_t *sl, int k, int32_t *pi, int32_t *ns, int stride,
+             int rows, cudaStream_t st) {
+    k_topk<NT, KPT><<<rows, NT, 0, st>>>(box, Hq, maxp, sl, k, pi, ns, stride);
+}
+ekv_status launch_topk(const float *box, int B, int Hq, int maxp, const int32_t *sl, int k, int32_t *pi, int32_t *ns,
+                       int stride, cudaStream_t st) {
+    const int rows = B * Hq;
+    if (maxp <= 256) topk_go<256, 1>(box, Hq, maxp, sl, k, pi, ns, stride, rows, st);
+    else if (maxp <= 1024) topk_go<256, 4>(box, Hq, maxp, sl, k, pi, ns, stride, rows, st);
+    else if (maxp <= 4096) topk_go<512, 8>(box, Hq, maxp, sl, k, pi, ns, stride, rows, st);
+    else if (maxp <= 16384) topk_go<1024, 16>(box, Hq, maxp, sl, k, pi, ns, stride, rows, st);
+    else if (maxp <= 32768) topk_go<1024, 32>(box, Hq, maxp, sl, k, pi, ns, stride, rows, st);
+    else topk_go<1024, 64>(box, Hq, maxp, sl, k, pi, ns, stride, rows, st);
+    return check_launch("k_topk");
+}
+
+ekv_status launch_union(const ekv_cache *c, int Hq, const int32_t *pi, const int32_t *ns, int stride, int32_t *up,
+                        uint8_t *um, int32_t *ul, int ucap, cudaStream_t st) {
+    const int G = Hq / c->n_kv_heads;
+    const int smem = 4 * ((c->max_pages_per_seq + 3) / 4);
+    static bool init = false;
+    if (!init) { set_smem(k_union<512>, 65536); init = true; }
+    k_union<512><<<c->batch * c->n_kv_heads, 512, smem, st>>>(c->n_kv_heads, G, c->max_pages_per_seq, c->seq_lens,
+                                                               pi, ns, stride, up, um, ul, ucap);
+    return check_launch("k_union");
+}
+
+template <typename T, int G>
+ekv_status launch_scores_t(const CacheView &v, const void *q, int Hq, const int32_t *up, const uint8_t *um,
+                           const int32_t *ul, int ucap, float *scores, int full, cudaStream_t st) {
+    constexpr int PPC = sizeof(T) == 2 ? 16 : 8;
+    constexpr int smem = PPC * kP * kD * (int)sizeof(T);
+    static bool init = false;
+    if (!init) { set_smem(k_attend_scores<T, G, PPC>, smem); init = true; }
+    dim3 grid((ucap + PPC - 1) / PPC, v.B * v.Hkv);
+    k_attend_scores<T, G, PPC><<<grid, 128, smem, st>>>(v, static_cast<const T *>(q), Hq, up, um, ul, ucap, scores,
+                                                        full);
+    return check_launch("k_attend_scores");
+}
+template <typename T>
+ekv_status launch_scores(const CacheView &v, const void *q, int Hq, const int32_t *up, const uint8_t *um,
+                         const int32_t *ul, int ucap, float *scores, int full, cudaStream_t st) {
+    switch (Hq / v.Hkv) {
+    case 1: return launch_scores_t<T, 1>(v, q, Hq, up, um, ul, ucap, scores, full, st);
+    case 2: return launch_scores_t<T, 2>(v, q, Hq, up, um, ul, ucap, scores, full, st);
+    case 4: return launch_scores_t<T, 4>(v, q, Hq, up, um, ul, ucap, scores, full, st);
+    default: return launch_scores_t<T, 8>(v, q, Hq, up, um, ul, ucap, scores, full, st);
+    }
+}
+
+template <typename T>
+ekv_status launch_tau(const CacheView &v, const TauArgs &A, int rows, cudaStream_t st) {
+    constexpr int smem = kCap * (int)(sizeof(float) + sizeof(int) + 1);
+    static bool init = false;
+    if (!init) { set_smem(k_tau_pv<T>, smem); init = true; }
+    k_tau_pv<T><<<rows, kTauNT, smem, st>>>(v, A);
+    return check_launch("k_tau_pv");
+}
+
+ekv_status check_attn(const ekv_attn_params *a) {
+    if (!a) return fail(EKV_ERR_INVALID_ARG, "attn params NULL");
+    if (a->transform != EKV_ENTMAX && a->transform != EKV_SOFTMAX) return fail(EKV_ERR_INVALID_ARG, "bad transform");
+    if (a->transform == EKV_ENTMAX && !(a->alpha > 1.0f)) return fail(EKV_ERR_INVALID_ARG, "alpha must be > 1");
+    return EKV_OK;
+}
+
+ekv_status check_sel(const ekv_select_params *s, float alpha) {
+    if (!s) return fail(EKV_ERR_INVALID_ARG, "select params NULL");
+    if (s->policy == EKV_TOPK) {
+        if (s->k_pages < 1) return fail(EKV_ERR_INVALID_ARG, "k_pages must be >= 1");
+    } else if (s->policy == EKV_GAUSS) {
+        if (!(s->q_page > 0.0 && s->q_page < 1.0)) return fail(EKV_ERR_INVALID_ARG, "q_page must be in (0,1)");
+        if (!(s->margin >= 0.0)) return fail(EKV_ERR_INVALID_ARG, "margin must be >= 0");
+        const double beta = 1.0 / ((double)alpha - 1.0);
+        const double rb = (double)(long long)(beta + 0.5);
+        if (!(alpha > 1.0f) || fabs(beta - rb) > 1e-9 || rb < 1 || rb > 4)
+            return fail(EKV_ERR_UNSUPPORTED, "Gaussian selector needs integer beta=1/(alpha-1) in {1,2,3,4} (alpha=%g)",
+                        (double)alpha);
+    } else if (s->policy != EKV_ALL) {
+        return fail(EKV_ERR_INVALID_ARG, "bad policy %d", s->policy);
+    }
+    return EKV_OK;
+}
+
+// sparse attention over given page lists (union + scores + tau/pv)
+ekv_status sparse_attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t *pi, const int32_t *ns,
+                              int stride, const ekv_attn_params *attn, float *out, double *tau, int32_t *supp,
+                              void *ws, const Layout &L, cudaStream_t st, TauArgs *extra) {
+    const CacheView v = view(c);
+    int32_t *up = at<int32_t>(ws, L.upages);
+    uint8_t *um = at<uint8_t>(ws, L.umask);
+    int32_t *ul = at<int32_t>(ws, L.ulen);
+    float *scores = at<float>(ws, L.scores);
+    EKV_TRY(launch_union(c, Hq, pi, ns, stride, up, um, ul, L.ucap, st));
+    if (c->dtype == EKV_BF16) EKV_TRY(launch_scores<__nv_bfloat16>(v, q, Hq, up, um, ul, L.ucap, scores, 0, st));
+    else EKV_TRY(launch_scores<float>(v, q, Hq, up, um, ul, L.ucap, scores, 0, st));
+    TauArgs A;
+    memset(&A, 0, sizeof(A));
+    if (extra) A = *extra;
+    A.scores = scores; A.ntok_stride = (size_t)L.ucap * kP;
+    A.union_pages = up; A.union_len = ul; A.ucap = L.ucap; A.full = 0;
+    A.Hq = Hq; A.G = Hq / c->n_kv_heads; A.alpha = attn->alpha; A.transform = attn->transform;
+    A.out = out; A.tau_out = tau; A.supp_out = supp;
+    if (c->dtype == EKV_BF16) return launch_tau<__nv_bfloat16>(v, A, c->batch * Hq, st);
+    return launch_tau<float>(v, A, c->batch * Hq, st);
+}
+
+ekv_status full_attend_impl(const ekv_cache *c, const void *q, int Hq, const ekv_attn_params *attn, float *out,
+                            double *tau, int32_t *supp, float *scores, cudaStream_t st, TauArgs *extra) {
+    const CacheView v = view(c);
+    const int maxp = c->max_pages_per_seq;
+    if (c->dtype == EKV_BF16) EKV_TRY(launch_scores<__nv_bfloat16>(v, q, Hq, nullptr, nullptr, nullptr, maxp, scores, 1, st));
+    else EKV_TRY(launch_scores<float>(v, q, Hq, nullptr, nullptr, nullptr, maxp, scores, 1, st));
+    TauArgs A;
+    memset(&A, 0, sizeof(A));
+    if (extra) A = *extra;
+    A.scores = scores; A.ntok_stride = (size_t)maxp * kP;
+    A.union_pages = nullptr; A.union_len = nullptr; A.ucap = maxp; A.full = 1;
+    A.Hq = Hq; A.G = Hq / c->n_kv_heads; A.alpha = attn->alpha; A.transform = attn->transform;
+    A.out = out; A.tau_out = tau; A.supp_out = supp;
+    if (c->dtype == EKV_BF16) return launch_tau<__nv_bfloat16>(v, A, c->batch * Hq, st);
+    return launch_tau<float>(v, A, c->batch * Hq, st);
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+extern "C" {
+
+const char *entmaxkv_last_error(void) { return g_err; }
+const char *entmaxkv_version(void) { return "entmaxkv-b200 0.1 (sm_100a)"; }
+int32_t entmaxkv_last_launch_count(void) { return g_launches; }
+
+size_t entmaxkv_workspace_size(const ekv_cache *cache, int32_t n_q_heads, const ekv_select_params *sel) {
+    if (check_cache(cache, n_q_heads) != EKV_OK) return 0;
+    Layout L = layout(cache, n_q_heads, sel);
+    if (!sel || sel->policy == EKV_ALL) return L.total - L.sparse_total + 256;
+    return L.sparse_total;
+}
+
+int32_t entmaxkv_select_capacity(const ekv_cache *cache, const ekv_select_params *sel) {
+    if (!cache) return 0;
+    return sel_cap(cache, sel);
+}
+
+ekv_status entmaxkv_append_kv(const ekv_cache *cache, const void *k_new, const void *v_new, int32_t n_tokens,
+                              void *stream) {
+    g_err[0] = 0;
+    EKV_TRY(check_cache(cache, 0));
+    if (!k_new || !v_new || n_tokens < 1) return fail(EKV_ERR_INVALID_ARG, "append: bad k/v or n_tokens");
+    if (!cache->kmin || !cache->kmax || !cache->ksum || !cache->ksumsq || !cache->kavg || !cache->kvar)
+        return fail(EKV_ERR_INVALID_ARG, "append: metadata buffers NULL");
+    g_launches = 0;
+    CacheView v = view(cache);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int nt = cache->n_kv_heads * kD;
+    if (nt > 1024) nt = 1024;
+    if (cache->dtype == EKV_BF16)
+        k_append<__nv_bfloat16><<<cache->batch, nt, 0, st>>>(v, static_cast<const __nv_bfloat16 *>(k_new),
+                                                             static_cast<const __nv_bfloat16 *>(v_new), n_tokens);
+    else
+        k_append<float><<<cache->batch, nt, 0, st>>>(v, static_cast<const float *>(k_new),
+                                                     static_cast<const float *>(v_new), n_tokens);
+    return check_launch("k_append");
+}
+
+ekv_status entmaxkv_rebuild_page_stats(const ekv_cache *cache, void *stream) {
+    g_err[0] = 0;
+    EKV_TRY(check_cache(cache, 0));
+    if (!cache->kmin || !cache->kmax || !cache->ksum || !cache->ksumsq || !cache->kavg || !cache->kvar)
+        return fail(EKV_ERR_INVALID_ARG, "rebuild: metadata buffers NULL");
+    g_launches = 0;
+    CacheView v = view(cache);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t per_seq = (size_t)cache->max_pages_per_seq * cache->n_kv_heads * kD;
+    dim3 grid((unsigned)((per_seq + 255) / 256), cache->batch);
+    if (cache->dtype == EKV_BF16) k_rebuild<__nv_bfloat16><<<grid, 256, 0, st>>>(v);
+    else k_rebuild<float><<<grid, 256, 0, st>>>(v);
+    return check_launch("k_rebuild");
+}
+
+ekv_status entmaxkv_score_pages(const ekv_cache *cache, const void *q, int32_t n_q_heads, int32_t modes, float *box,
+                                float *mu, float *sigma2, void *workspace, void *stream) {
+    (void)workspace;
+    g_err[0] = 0;
+    EKV_TRY(check_cache(cache, n_q_heads));
+    if (!q) return fail(EKV_ERR_INVALID_ARG, "q NULL");
+    if (modes < 1 || modes > 3) return fail(EKV_ERR_INVALID_ARG, "modes must be 1..3");
+    if ((modes & 1) && (!box || !cache->kmin || !cache->kmax)) return fail(EKV_ERR_INVALID_ARG, "box mode needs box/kmin/kmax");
+    if ((modes & 2) && (!mu || !sigma2 || !cache->kavg || !cache->kvar))
+        return fail(EKV_ERR_INVALID_ARG, "gauss mode needs mu/sigma2/kavg/kvar");
+    g_launches = 0;
+    CacheView v = view(cache);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cache->dtype == EKV_BF16) return launch_score<__nv_bfloat16>(v, q, n_q_heads, modes, box, mu, sigma2, st);
+    return launch_score<float>(v, q, n_q_heads, modes, box, mu, sigma2, st);
+}
+
+ekv_status entmaxkv_select(const ekv_cache *cache, int32_t n_q_heads, const float *box, const float *mu,
+                           const float *sigma2, const ekv_select_params *sel, float alpha, int32_t *page_idx,
+                           int32_t *n_sel, int32_t sel_stride, double *tau_hat, void *workspace, void *stream) {
+    (void)workspace;
+    g_err[0] = 0;
+    EKV_TRY(check_cache(cache, n_q_heads));
+    EKV_TRY(check_sel(sel, alpha));
+    if (!page_idx || !n_sel) return fail(EKV_ERR_INVALID_ARG, "page_idx/n_sel NULL");
+    if (sel_stride < sel_cap(cache, sel)) return fail(EKV_ERR_CAPACITY, "sel_stride %d < capacity %d", sel_stride, sel_cap(cache, sel));
+    g_launches = 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int maxp = cache->max_pages_per_seq;
+    if (sel->policy == EKV_TOPK) {
+        if (!box) return fail(EKV_ERR_INVALID_ARG, "top-k needs box scores");
+        return launch_topk(box, cache->batch, n_q_heads, maxp, cache->seq_lens, sel->k_pages, page_idx, n_sel, sel_stride, st);
+    }
+    if (sel->policy == EKV_ALL) {
+        return launch_topk(box ? box : nullptr, cache->batch, n_q_heads, maxp, cache->seq_lens, maxp, page_idx, n_sel,
+                           sel_stride, st);
+    }
+    if (!mu || !sigma2) return fail(EKV_ERR_INVALID_ARG, "Gaussian selector needs mu/sigma2");
+    k_gauss_select<256><<<cache->batch * n_q_heads, 256, 0, st>>>(mu, sigma2, n_q_heads, maxp, cache->seq_lens, alpha,
+                                                                  sel->margin, sel->q_page, page_idx, n_sel, sel_stride,
+                                                                  tau_hat);
+    return check_launch("k_gauss_select");
+}
+
+ekv_status entmaxkv_sparse_attend(const ekv_cache *cache, const void *q, int32_t n_q_heads, const int32_t *page_idx,
+                                  const int32_t *n_sel, int32_t sel_stride, const ekv_attn_params *attn, float *out,
+                                  double *tau, int32_t *supp, void *workspace, void *stream) {
+    g_err[0] = 0;
+    EKV_TRY(check_cache(cache, n_q_heads));
+    EKV_TRY(check_attn(attn));
+    if (!q || !page_idx || !n_sel || !out || !workspace) return fail(EKV_ERR_INVALID_ARG, "NULL argument");
+    if (sel_stride < 1) return fail(EKV_ERR_INVALID_ARG, "sel_stride < 1");
+    g_launches = 0;
+    ekv_select_params sp;
+    sp.policy = EKV_TOPK; sp.k_pages = sel_stride; sp.q_page = 0.99; sp.margin = 0.0;
+    Layout L = layout(cache, n_q_heads, &sp);
+    return sparse_attend_impl(cache, q, n_q_heads, page_idx, n_sel, sel_stride, attn, out, tau, supp, workspace, L,
+                              static_cast<cudaStream_t>(stream), nullptr);
+}
+
+ekv_status entmaxkv_full_attend(const ekv_cache *cache, const void *q, int32_t n_q_heads, const ekv_attn_params *attn,
+                                float *out, double *tau, int32_t *supp, void *workspace, void *stream) {
+    g_err[0] = 0;
+    EKV_TRY(check_cache(cache, n_q_heads));
+    EKV_TRY(check_attn(attn));
+    if (!q || !out || !workspace) return fail(EKV_ERR_INVALID_ARG, "NULL argument");
+    g_launches = 0;
+    return full_attend_impl(cache, q, n_q_heads, attn, out, tau, supp, static_cast<float *>(workspace),
+                            static_cast<cudaStream_t>(stream), nullptr);
+}
+
+ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_heads, const ekv_select_params *sel,
+                           const ekv_attn_params *attn, float *out, ekv_decode_stats *stats, void *workspace,
+                           void *stream) {
+    g_err[0] = 0;
+    EKV_TRY(check_cache(cache, n_q_heads));
+    EKV_TRY(check_attn(attn));
+    EKV_TRY(check_sel(sel, attn->alpha));
+    if (!q || !out || !workspace) return fail(EKV_ERR_INVALID_ARG, "NULL argument");
+    if (sel->policy == EKV_GAUSS && attn->transform != EKV_ENTMAX)
+        return fail(EKV_ERR_INVALID_ARG, "Gaussian selector is entmax-specific");
+    g_launches = 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const CacheView v = view(cache);
+    Layout L = layout(cache, n_q_heads, sel);
+    float *box = at<float>(workspace, L.box);
+    float *mu = at<float>(workspace, L.mu);
+    float *s2 = at<float>(workspace, L.sigma2);
+    int32_t *pi = at<int32_t>(workspace, L.page_idx);
+    int32_t *ns = at<int32_t>(workspace, L.n_sel);
+    double *th = at<double>(workspace, L.tau_hat);
+    const bool want_db = stats && stats->delta_bar;
+    // a1: page scores (box for top-k and for the certificate; mu/sigma2 for Gaussian)
+    int modes = 0;
+    if (sel->policy == EKV_TOPK || want_db) modes |= EKV_SCORE_BOX;
+    if (sel->policy == EKV_GAUSS) modes |= EKV_SCORE_GAUSS;
+    if (modes) {
+        if (cache->dtype == EKV_BF16) EKV_TRY(launch_score<__nv_bfloat16>(v, q, n_q_heads, modes, box, mu, s2, st));
+        else EKV_TRY(launch_score<float>(v, q, n_q_heads, modes, box, mu, s2, st));
+    }
+    // a2 / a2'
+    const int maxp = cache->max_pages_per_seq;
+    if (sel->policy == EKV_TOPK || sel->policy == EKV_ALL) {
+        const int k = sel->policy == EKV_TOPK ? sel->k_pages : maxp;
+        EKV_TRY(launch_topk(box, cache->batch, n_q_heads, maxp, cache->seq_lens, k, pi, ns, L.cap, st));
+    } else {
+        k_gauss_select<256><<<cache->batch * n_q_heads, 256, 0, st>>>(mu, s2, n_q_heads, maxp, cache->seq_lens,
+                                                                      attn->alpha, sel->margin, sel->q_page, pi, ns,
+                                                                      L.cap, th);
+        EKV_TRY(check_launch("k_gauss_select"));
+    }
+    // a3 (+a4 certificate)
+    TauArgs extra;
+    memset(&extra, 0, sizeof(extra));
+    if (want_db && attn->transform == EKV_ENTMAX) {
+        extra.box = box; extra.page_idx = pi; extra.n_sel = ns; extra.sel_stride = L.cap;
+        extra.delta_bar = stats->delta_bar;
+    }
+    EKV_TRY(sparse_attend_impl(cache, q, n_q_heads, pi, ns, L.cap, attn, out, stats ? stats->tau : nullptr,
+                               stats ? stats->supp_count : nullptr, workspace, L, st, &extra));
+    const int rows = cache->batch * n_q_heads;
+    if (stats) {
+        if (stats->n_sel) {
+            if (cudaMemcpyAsync(stats->n_sel, ns, rows * sizeof(int32_t), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+                return fail(EKV_ERR_CUDA, "n_sel copy");
+        }
+        if (stats->tau_hat && sel->policy == EKV_GAUSS) {
+            if (cudaMemcpyAsync(stats->tau_hat, th, rows * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+                return fail(EKV_ERR_CUDA, "tau_hat copy");
+        }
+        if (stats->eval_exact && attn->transform == EKV_ENTMAX) {
+            // a4 eval: full-cache pass with the support list, then delta / rho counts (R16)
+            float *fs = reinterpret_cast<float *>(static_cast<char *>(workspace) + L.sparse_total);
+            float *fout = at<float>(workspace, L.full_out);
+            TauArgs ex;
+            memset(&ex, 0, sizeof(ex));
+            ex.tok_list = at<int32_t>(workspace, L.tok_list);
+            ex.p_list = at<double>(workspace, L.p_list);
+            ex.n_list = at<int32_t>(workspace, L.n_list);
+            ex.list_cap = L.list_cap;
+            EKV_TRY(full_attend_impl(cache, q, n_q_heads, attn, fout, stats->tau_full, nullptr, fs, st, &ex));
+            k_eval_metrics<<<rows, 256, 0, st>>>(ex.tok_list, ex.p_list, ex.n_list, ex.list_cap, pi, ns, L.cap,
+                                                 stats->delta, stats->recovered, stats->full_supp);
+            EKV_TRY(check_launch("k_eval_metrics"));
+        }
+    }
+    return EKV_OK;
+}
+
+}  // extern "C"

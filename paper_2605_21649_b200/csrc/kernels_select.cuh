@@ -1,0 +1,274 @@
+// kernels_select.cuh -- a2 (top-k page selection), a2' (Gaussian-aware selection)
+// and the per-KV-group union of the selected pages (R17).
+#pragma once
+#include "common.cuh"
+
+namespace ekv {
+
+// ============================================================================ a2: top-k
+// One CTA (NT threads) per (b, q-head) row.  Thread t holds the KPT contiguous keys
+// [t*KPT, t*KPT+KPT) of the row in registers (ordered-int encoding of the fp32 box
+// score, -0 == +0).  The k-th largest key T* is found bit by bit (32 block-wide
+// counting rounds: T |= bit whenever count(key >= T|bit) >= k).  Every key > T* is
+// selected and the (k - count(key > T*)) lowest-index keys equal to T* (R3 tie-break).
+// Indices are written ascending via a block scan over the contiguous per-thread
+// blocks.  P:369-381.
+template <int NT, int KPT>
+__global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int Hq, int maxp,
+                                             const int32_t *__restrict__ seq_lens, int k,
+                                             int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
+                                             int sel_stride) {
+    __shared__ int sh[NT / 32 + 1];
+    const int row = blockIdx.x;
+    const int b = row / Hq;
+    const int M = n_pages_of(seq_lens[b]);
+    const int keff = min(k, M);
+    int32_t *out = page_idx + (size_t)row * sel_stride;
+    if (keff >= M) {
+        for (int p = threadIdx.x; p < M; p += NT) out[p] = p;
+        if (threadIdx.x == 0) n_sel[row] = M;
+        return;
+    }
+    const float *x = box + (size_t)row * maxp;
+    uint32_t key[KPT];
+    const int i0 = threadIdx.x * KPT;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) key[j] = (i0 + j < M) ? f2key(x[i0 + j]) : 0u;
+
+    uint32_t T = 0u;
+    for (int bit = 31; bit >= 0; --bit) {
+        const uint32_t Tt = T | (1u << bit);
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) cnt += (key[j] >= Tt) ? 1 : 0;
+        const int tot = block_sum_i<NT>(cnt, sh);
+        if (tot >= keff) T = Tt;
+    }
+    // selection flags
+    int ngt = 0;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) ngt += (key[j] > T) ? 1 : 0;
+    const int n_gt = block_sum_i<NT>(ngt, sh);
+    int neq = 0;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) neq += (key[j] == T && i0 + j < M) ? 1 : 0;
+    int tot_eq;
+    const int eq_before = block_excl_scan<NT>(neq, sh, &tot_eq);
+    const int need_eq = keff - n_gt;
+    // count selected in my block
+    int nsel = 0, e = eq_before;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+        const bool eq = (key[j] == T && i0 + j < M);
+        const bool s = (key[j] > T) || (eq && e < need_eq);
+        if (eq) ++e;
+        nsel += s ? 1 : 0;
+    }
+    int tot_sel;
+    int pos = block_excl_scan<NT>(nsel, sh, &tot_sel);
+    e = eq_before;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+        const bool eq = (key[j] == T && i0 + j < M);
+        const bool s = (key[j] > T) || (eq && e < need_eq);
+        if (eq) ++e;
+        if (s) out[pos++] = i0 + j;
+    }
+    if (threadIdx.x == 0) n_sel[row] = keff;
+}
+
+// ============================================================================ union per KV group
+// One CTA per (b, kv head): a shared-memory byte mask over the M pages (4 pages per
+// 32-bit word, bit g of a page's byte = selected by query head g of the group), then
+// an ordered compaction: union_pages ascending + per-page G-bit head mask (R17).
+template <int NT>
+__global__ void __launch_bounds__(NT) k_union(int Hkv, int G, int maxp, const int32_t *__restrict__ seq_lens,
+                                              const int32_t *__restrict__ page_idx,
+                                              const int32_t *__restrict__ n_sel, int sel_stride,
+                                              int32_t *__restrict__ union_pages,
+                                              uint8_t *__restrict__ union_mask,
+                                              int32_t *__restrict__ union_len, int ucap) {
+    extern __shared__ uint32_t wmask[];
+    __shared__ int sh[NT / 32 + 1];
+    const int unit = blockIdx.x;
+    const int b = unit / Hkv, kvh = unit % Hkv;
+    const int M = n_pages_of(seq_lens[b]);
+    const int W = (M + 3) / 4;
+    for (int w = threadIdx.x; w < W; w += NT) wmask[w] = 0u;
+    __syncthreads();
+    const int Hq = Hkv * G;
+    for (int g = 0; g < G; ++g) {
+        const int row = b * Hq + kvh * G + g;
+        const int n = n_sel[row];
+        const int32_t *pl = page_idx + (size_t)row * sel_stride;
+        for (int i = threadIdx.x; i < n; i += NT) {
+            const int p = pl[i];
+            atomicOr(&wmask[p >> 2], 1u << ((p & 3) * 8 + g));
+        }
+    }
+    __syncthreads();
+    const int wpt = (W + NT - 1) / NT;
+    const int w0 = threadIdx.x * wpt;
+    int cnt = 0;
+    for (int w = w0; w < min(W, w0 + wpt); ++w) {
+        const uint32_t v = wmask[w];
+        cnt += ((v & 0xffu) != 0) + ((v & 0xff00u) != 0) + ((v & 0xff0000u) != 0) + ((v & 0xff000000u) != 0);
+    }
+    int tot;
+    int pos = block_excl_scan<NT>(cnt, sh, &tot);
+    int32_t *up = union_pages + (size_t)unit * ucap;
+    uint8_t *um = union_mask + (size_t)unit * ucap;
+    for (int w = w0; w < min(W, w0 + wpt); ++w) {
+        const uint32_t v = wmask[w];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t m = (v >> (8 * j)) & 0xffu;
+            if (m) { up[pos] = 4 * w + j; um[pos] = (uint8_t)m; ++pos; }
+        }
+    }
+    if (threadIdx.x == 0) union_len[unit] = tot;
+}
+
+// ============================================================================ a2': Gaussian selector
+// One CTA per (b, q-head).  tau_hat solves  sum_p c_p E[(a S_p - tau)_+^beta] = 1
+// (Eq. gaussian-threshold-main) with the App. D closed forms in fp64
+// (beta = 4 by the truncated-moment recursion, R15).  Bracket [lo, hi] with
+// mass(lo) >= 1 > mass(hi), then safeguarded Newton (dE/dtau = -beta * M_{beta-1}),
+// falling back to bisection when a Newton step leaves the bracket.  Page rule
+// (Eq. gaussian-selector-main, R14): keep p iff
+// (double)a * fmaf(sqrtf(sigma2), zq[c], mu) > tau_hat - margin; empty -> argmax mu.
+struct GaussMoments { double m, dm; };   // M_beta and M_{beta-1}
+
+__device__ __forceinline__ GaussMoments trunc_moments(int beta, double muY, double sigY) {
+    if (!(sigY > 0.0)) {
+        const double x = muY > 0.0 ? muY : 0.0;
+        double r = 1.0, rm = 1.0;
+        for (int i = 0; i < beta; ++i) { rm = r; r *= x; }
+        if (beta == 0) rm = 0.0;
+        return {r, rm};
+    }
+    const double t = muY / sigY;
+    const double Ph = normcdf(t);
+    const double ph = exp(-0.5 * t * t) * 0.39894228040143267794;   // 1/sqrt(2 pi)
+    double m0 = Ph, m1 = muY * Ph + sigY * ph;
+    if (beta == 1) return {m1, m0};
+    double prev = m0, cur = m1;
+    for (int k = 2; k <= beta; ++k) {
+        const double nx = muY * cur + (double)(k - 1) * sigY * sigY * prev;
+        prev = cur; cur = nx;
+    }
+    return {cur, prev};
+}
+
+template <int NT>
+__device__ void gauss_mass(const float *mu, const float *s2, int M, int Lseq, double a, int beta,
+                           double tau, double &mass, double &dmass, double *shd) {
+    double m = 0.0, dm = 0.0;
+    for (int p = threadIdx.x; p < M; p += NT) {
+        const double cnt = (double)min(kP, Lseq - p * kP);
+        const double sg = sqrt((double)s2[p]);
+        GaussMoments g = trunc_moments(beta, a * (double)mu[p] - tau, a * sg);
+        m += cnt * g.m;
+        dm += cnt * (double)beta * g.dm;      // -d mass / d tau
+    }
+    block_sum2_d<NT>(m, dm, shd);
+    mass = m; dmass = dm;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_gauss_select(const float *__restrict__ mu, const float *__restrict__ sigma2,
+                                                     int Hq, int maxp, const int32_t *__restrict__ seq_lens,
+                                                     float alpha, double margin, double q_page,
+                                                     int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
+                                                     int sel_stride, double *__restrict__ tau_hat_out) {
+    __shared__ double shd[2 * (NT / 32) + 2];
+    __shared__ int shi[NT / 32 + 1];
+    __shared__ float shf[NT / 32 + 1];
+    __shared__ float zq[kP + 1];
+    // zq[c] = Phi^{-1}(q_page^{1/c}), fp64 normcdfinv rounded to fp32 (R14)
+    if (threadIdx.x >= 1 && threadIdx.x <= kP)
+        zq[threadIdx.x] = (float)normcdfinv(pow(q_page, 1.0 / (double)threadIdx.x));
+    const int row = blockIdx.x;
+    const int b = row / Hq;
+    const int Lseq = seq_lens[b];
+    const int M = n_pages_of(Lseq);
+    const float *m_ = mu + (size_t)row * maxp;
+    const float *s_ = sigma2 + (size_t)row * maxp;
+    const double a = (double)alpha - 1.0;
+    const int beta = (int)llrint(1.0 / a);
+    // bracket: top = a * max_p (mu + 8 sigma)
+    float tmax = -INFINITY;
+    for (int p = threadIdx.x; p < M; p += NT) tmax = fmaxf(tmax, m_[p] + 8.0f * sqrtf(s_[p]));
+    tmax = block_max_f<NT>(tmax, shf);
+    double hi = a * (double)tmax, w = 1.0, mass, dmass;
+    for (int it = 0; it < 200; ++it) {
+        gauss_mass<NT>(m_, s_, M, Lseq, a, beta, hi, mass, dmass, shd);
+        if (mass < 1.0) break;
+        hi += w; w *= 2.0;
+    }
+    double lo = hi - 1.0;
+    w = 1.0;
+    for (int it = 0; it < 200; ++it) {
+        gauss_mass<NT>(m_, s_, M, Lseq, a, beta, lo, mass, dmass, shd);
+        if (mass >= 1.0) break;
+        lo -= w; w *= 2.0;
+    }
+    // safeguarded Newton from lo (mass convex decreasing -> monotone from the left)
+    double tau = lo;
+    for (int it = 0; it < 200; ++it) {
+        gauss_mass<NT>(m_, s_, M, Lseq, a, beta, tau, mass, dmass, shd);
+        if (mass >= 1.0) lo = tau; else hi = tau;
+        double nt = (dmass > 0.0) ? tau + (mass - 1.0) / dmass : 0.5 * (lo + hi);
+        if (!(nt > lo && nt < hi)) nt = 0.5 * (lo + hi);
+        if (fabs(nt - tau) <= 1e-15 * fmax(1.0, fabs(tau)) || hi - lo <= 1e-15 * fmax(1.0, fabs(hi))) {
+            tau = nt;
+            break;
+        }
+        tau = nt;
+    }
+    // page rule + ordered compaction (NT pages per round)
+    int32_t *out = page_idx + (size_t)row * sel_stride;
+    int base = 0;
+    for (int r0 = 0; r0 < M; r0 += NT) {
+        const int p = r0 + threadIdx.x;
+        int keep = 0;
+        if (p < M) {
+            const int cnt = min(kP, Lseq - p * kP);
+            const float sg = __fmaf_rn(sqrtf(s_[p]), zq[cnt], m_[p]);
+            keep = (a * (double)sg > tau - margin) ? 1 : 0;
+        }
+        int tot;
+        const int pos = block_excl_scan<NT>(keep, shi, &tot);
+        if (keep) out[base + pos] = p;
+        base += tot;
+    }
+    if (base == 0 && M > 0) {
+        // argmax mu, lower index on ties (R6)
+        uint64_t best = 0;
+        for (int p = threadIdx.x; p < M; p += NT) {
+            const uint64_t k = ((uint64_t)f2key(m_[p]) << 32) | (uint32_t)(0xffffffffu - (uint32_t)p);
+            best = best > k ? best : k;
+        }
+        // block max of u64 via two passes on shared memory
+        __shared__ unsigned long long shb[NT / 32];
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            const uint64_t y = __shfl_xor_sync(0xffffffffu, best, o);
+            best = best > y ? best : y;
+        }
+        if ((threadIdx.x & 31) == 0) shb[threadIdx.x >> 5] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t r = 0;
+            for (int i = 0; i < NT / 32; ++i) r = r > shb[i] ? r : shb[i];
+            out[0] = (int)(0xffffffffu - (uint32_t)(r & 0xffffffffu));
+        }
+        base = 1;
+    }
+    if (threadIdx.x == 0) {
+        n_sel[row] = base;
+        if (tau_hat_out) tau_hat_out[row] = tau;
+    }
+}
+
+}  // namespace ekv

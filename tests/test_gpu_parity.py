@@ -1,0 +1,305 @@
+"""GPU parity: every C-ABI entry point against the CPU oracle on the same seeded
+inputs.  Bars (north star / SURVEY 8(c)): metadata, page scores, page sets and
+supports bit-exact; outputs max-abs <= 2e-3 (bf16 in) / 1e-5 (fp32 in);
+|tau_gpu - tau_cpu| <= 1e-6 max(1, |tau|)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2605_21649_b200 import binding as ekv
+from paper_2605_21649_b200.workload import make_workload, new_tokens
+from gpu_helpers import device_cache, host_cache, make_pair, q_host, tol_for
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # (B, seq_lens, Hq, Hkv, dtype)  -- several tiles, ragged tails, partial pages
+    (1, 4096, 4, 1, torch.float32),                 # config 1 shape (fp32)
+    (2, [1000, 777], 8, 2, torch.bfloat16),
+    (3, [33, 512, 1], 8, 8, torch.bfloat16),        # 1-token sequence, G = 1
+    (2, [2048, 1500], 32, 8, torch.bfloat16),       # Llama GQA-4 shape
+    (1, 300, 16, 2, torch.bfloat16),                # G = 8
+]
+
+
+def ids(c):
+    return f"B{c[0]}-{c[2]}q{c[3]}kv-{str(c[4]).split('.')[-1]}"
+
+
+@pytest.mark.parametrize("case", CASES, ids=ids)
+def test_page_stats_bit_exact(case):
+    B, sl, Hq, Hkv, dt = case
+    wl, dc, hc = make_pair(B, sl, Hq, Hkv, dtype=dt, seed=11)
+    torch.cuda.synchronize()
+    for name in ("kmin", "kmax", "ksum", "ksumsq", "kavg", "kvar"):
+        g = getattr(dc, name).float().cpu().numpy()
+        o = getattr(hc, name)
+        for b in range(B):
+            for lp in range(hc.n_pages(b)):
+                ph = int(hc.page_table[b, lp])
+                np.testing.assert_array_equal(g[ph], o[ph], err_msg=f"{name} b={b} page={lp}")
+
+
+def test_append_kv_matches_rebuild_and_oracle():
+    B, Hq, Hkv = 2, 8, 2
+    wl = make_workload(B, [40, 15], Hq, Hkv, seed=3, spare_tokens=40)
+    dc = device_cache(wl)
+    for step in range(20):
+        _, k, v = new_tokens(B, Hq, Hkv, seed=100 + step, device="cuda")
+        ekv.append_kv(dc, k, v)
+    # also a multi-token append
+    _, k, v = new_tokens(B * 3, Hq, Hkv, seed=999, device="cuda")
+    ekv.append_kv(dc, k.view(B, 3, Hkv, 128), v.view(B, 3, Hkv, 128))
+    torch.cuda.synchronize()
+    assert dc.seq_lens.cpu().tolist() == [63, 38]
+    hc = oracle.HostCache(dc.K.float().cpu().numpy(), dc.V.float().cpu().numpy(), dc.page_table.cpu().numpy(),
+                          dc.seq_lens.cpu().numpy())
+    hc.build_stats()
+    for name in ("kmin", "kmax", "ksum", "ksumsq", "kavg", "kvar"):
+        g = getattr(dc, name).float().cpu().numpy()
+        o = getattr(hc, name)
+        for b in range(B):
+            for lp in range(hc.n_pages(b)):
+                ph = int(hc.page_table[b, lp])
+                np.testing.assert_array_equal(g[ph], o[ph], err_msg=f"{name} b={b} page={lp}")
+
+
+@pytest.mark.parametrize("case", CASES, ids=ids)
+def test_score_pages_bit_exact(case):
+    B, sl, Hq, Hkv, dt = case
+    wl, dc, hc = make_pair(B, sl, Hq, Hkv, dtype=dt, seed=5)
+    G = Hq // Hkv
+    box, mu, s2 = ekv.score_pages(dc, wl.q.cuda(), modes=3)
+    torch.cuda.synchronize()
+    box, mu, s2 = box.cpu().numpy(), mu.cpu().numpy(), s2.cpu().numpy()
+    qh = q_host(wl)
+    for b in range(B):
+        M = hc.n_pages(b)
+        for h in range(Hq):
+            ob, om, os2 = hc.score_pages(qh[b, h], b, h // G, modes=3)
+            np.testing.assert_array_equal(box[b, h, :M], ob)
+            np.testing.assert_array_equal(mu[b, h, :M], om)
+            np.testing.assert_array_equal(s2[b, h, :M], os2)
+
+
+@pytest.mark.parametrize("case", CASES, ids=ids)
+@pytest.mark.parametrize("k", [1, 7, 64])
+def test_topk_select_bit_exact(case, k):
+    B, sl, Hq, Hkv, dt = case
+    wl, dc, hc = make_pair(B, sl, Hq, Hkv, dtype=dt, seed=7)
+    G = Hq // Hkv
+    box, _, _ = ekv.score_pages(dc, wl.q.cuda(), modes=1)
+    pi, ns, _ = ekv.select(dc, Hq, ekv.select_params("topk", k), box=box)
+    torch.cuda.synchronize()
+    pi, ns = pi.cpu().numpy(), ns.cpu().numpy()
+    qh = q_host(wl)
+    for b in range(B):
+        for h in range(Hq):
+            ob, _, _ = hc.score_pages(qh[b, h], b, h // G, modes=1)
+            ref = oracle.topk(ob, k)
+            assert ns[b, h] == len(ref)
+            assert pi[b, h, :ns[b, h]].tolist() == ref.tolist()
+
+
+def test_topk_ties_lower_index_wins():
+    # duplicate keys in every page -> many equal box scores; R3 tie-break
+    B, Hq, Hkv = 1, 4, 1
+    wl = make_workload(B, 1024, Hq, Hkv, seed=2)
+    base = wl.K[wl.page_table[0, 0]].clone()
+    for lp in range(0, 64, 2):
+        wl.K[wl.page_table[0, lp]] = base
+    dc, hc = device_cache(wl), host_cache(wl)
+    box, _, _ = ekv.score_pages(dc, wl.q.cuda(), modes=1)
+    pi, ns, _ = ekv.select(dc, Hq, ekv.select_params("topk", 5), box=box)
+    torch.cuda.synchronize()
+    qh = q_host(wl)
+    for h in range(Hq):
+        ob, _, _ = hc.score_pages(qh[0, h], 0, 0, modes=1)
+        assert pi[0, h, :ns[0, h]].cpu().tolist() == oracle.topk(ob, 5).tolist()
+
+
+def _check_attend(hc, qh, b, h, G, pages, alpha, transform, out, tau, supp, tol):
+    ref = hc.attend(qh[b, h], b, h // G, pages, alpha, transform)
+    np.testing.assert_allclose(out, ref["o"], atol=tol, rtol=0, err_msg=f"b={b} h={h}")
+    if transform == 0:
+        assert supp == ref["supp"], (b, h, supp, ref["supp"])
+        assert abs(tau - ref["tau"]) <= 1e-6 * max(1.0, abs(ref["tau"]))
+    return ref
+
+
+@pytest.mark.parametrize("case", CASES, ids=ids)
+@pytest.mark.parametrize("alpha", [1.5, 2.0, 1.25])
+def test_sparse_attend_oracle_pages(case, alpha):
+    """a3 on page lists chosen by the oracle (its own top-k) -> outputs within tolerance,
+    support sizes bit-exact."""
+    B, sl, Hq, Hkv, dt = case
+    wl, dc, hc = make_pair(B, sl, Hq, Hkv, dtype=dt, seed=13)
+    G = Hq // Hkv
+    qh = q_host(wl)
+    k = 9
+    lists = {}
+    cap = min(k, dc.max_pages)
+    pi = torch.full((B, Hq, cap), -1, dtype=torch.int32)
+    ns = torch.zeros(B, Hq, dtype=torch.int32)
+    for b in range(B):
+        for h in range(Hq):
+            ob, _, _ = hc.score_pages(qh[b, h], b, h // G, modes=1)
+            pl = oracle.topk(ob, k)
+            lists[b, h] = pl
+            pi[b, h, :len(pl)] = torch.from_numpy(pl)
+            ns[b, h] = len(pl)
+    out, tau, supp = ekv.sparse_attend(dc, wl.q.cuda(), pi.cuda(), ns.cuda(), ekv.attn_params(alpha))
+    torch.cuda.synchronize()
+    out, tau, supp = out.cpu().numpy(), tau.cpu().numpy(), supp.cpu().numpy()
+    for b in range(B):
+        for h in range(Hq):
+            _check_attend(hc, qh, b, h, G, lists[b, h], alpha, 0, out[b, h], tau[b, h], supp[b, h], tol_for(dt))
+
+
+@pytest.mark.parametrize("case", CASES[:4], ids=ids)
+def test_sparse_softmax_same_kernels(case):
+    B, sl, Hq, Hkv, dt = case
+    wl, dc, hc = make_pair(B, sl, Hq, Hkv, dtype=dt, seed=17)
+    G = Hq // Hkv
+    qh = q_host(wl)
+    box, _, _ = ekv.score_pages(dc, wl.q.cuda(), modes=1)
+    pi, ns, _ = ekv.select(dc, Hq, ekv.select_params("topk", 6), box=box)
+    out, tau, supp = ekv.sparse_attend(dc, wl.q.cuda(), pi, ns, ekv.attn_params(1.5, "softmax"))
+    torch.cuda.synchronize()
+    out, tau = out.cpu().numpy(), tau.cpu().numpy()
+    for b in range(B):
+        for h in range(Hq):
+            ob, _, _ = hc.score_pages(qh[b, h], b, h // G, modes=1)
+            ref = hc.attend(qh[b, h], b, h // G, oracle.topk(ob, 6), 1.5, transform=1)
+            np.testing.assert_allclose(out[b, h], ref["o"], atol=tol_for(dt), rtol=0)
+            assert abs(tau[b, h] - ref["tau"]) < 1e-5
+
+
+@pytest.mark.parametrize("case", CASES, ids=ids)
+@pytest.mark.parametrize("alpha", [1.5, 2.0, 1.25])
+def test_full_attend(case, alpha):
+    B, sl, Hq, Hkv, dt = case
+    wl, dc, hc = make_pair(B, sl, Hq, Hkv, dtype=dt, seed=19)
+    G = Hq // Hkv
+    qh = q_host(wl)
+    out, tau, supp = ekv.full_attend(dc, wl.q.cuda(), ekv.attn_params(alpha))
+    torch.cuda.synchronize()
+    out, tau, supp = out.cpu().numpy(), tau.cpu().numpy(), supp.cpu().numpy()
+    for b in range(B):
+        M = hc.n_pages(b)
+        for h in range(Hq):
+            _check_attend(hc, qh, b, h, G, np.arange(M, dtype=np.int32), alpha, 0, out[b, h], tau[b, h], supp[b, h],
+                          tol_for(dt))
+
+
+@pytest.mark.parametrize("case", CASES, ids=ids)
+@pytest.mark.parametrize("alpha,k", [(1.5, 32), (2.0, 8), (1.25, 16)])
+def test_decode_topk_end_to_end(case, alpha, k):
+    """Fused decode (score -> select -> attend + delta_bar) vs the oracle's step-by-step decode."""
+    B, sl, Hq, Hkv, dt = case
+    wl, dc, hc = make_pair(B, sl, Hq, Hkv, dtype=dt, seed=23, kind="planted" if B < 3 else "randn")
+    G = Hq // Hkv
+    qh = q_host(wl)
+    sel = ekv.select_params("topk", k)
+    ws = ekv.alloc_workspace(dc, Hq, sel, eval_exact=True)
+    st = ekv.DecodeStats(B, Hq, "cuda", delta_bar=True, eval_exact=True)
+    out = ekv.decode(dc, wl.q.cuda(), sel, ekv.attn_params(alpha), ws, stats=st)
+    torch.cuda.synchronize()
+    out = out.cpu().numpy()
+    for b in range(B):
+        for h in range(Hq):
+            ref = oracle.decode_head(hc, qh[b, h], b, h // G, alpha, k_pages=k, eval_exact=True)
+            np.testing.assert_allclose(out[b, h], ref["o"], atol=tol_for(dt), rtol=0)
+            assert int(st.n_sel[b, h]) == len(ref["pages"])
+            assert int(st.supp_count[b, h]) == ref["supp"]
+            assert abs(float(st.tau[b, h]) - ref["tau"]) <= 1e-6 * max(1, abs(ref["tau"]))
+            m = ref["metrics"]
+            assert int(st.full_supp[b, h]) == m["full_supp"]
+            assert int(st.recovered[b, h]) == m["recovered"]
+            assert abs(float(st.delta[b, h]) - m["delta"]) <= 1e-9
+            assert abs(float(st.tau_full[b, h]) - ref["full"]["tau"]) <= 1e-6 * max(1, abs(ref["full"]["tau"]))
+            db = oracle.delta_bar(ref["box"], hc.page_counts(b), ref["pages"], alpha, ref["tau"])
+            assert abs(float(st.delta_bar[b, h]) - db) <= 1e-9 * max(1.0, db)
+            assert float(st.delta[b, h]) <= float(st.delta_bar[b, h]) + 1e-12
+
+
+@pytest.mark.parametrize("case", CASES[1:4], ids=ids)
+@pytest.mark.parametrize("alpha", [1.5, 2.0, 1.25])
+def test_gaussian_select(case, alpha):
+    """a2': tau_hat within 1e-10 rel and the oracle's page set evaluated AT tau_hat_gpu equals
+    the GPU set bit-exactly (R14)."""
+    B, sl, Hq, Hkv, dt = case
+    wl, dc, hc = make_pair(B, sl, Hq, Hkv, dtype=dt, seed=29, kind="planted")
+    G = Hq // Hkv
+    qh = q_host(wl)
+    _, mu, s2 = ekv.score_pages(dc, wl.q.cuda(), modes=2)
+    sel = ekv.select_params("gauss", q_page=0.99, margin=0.05)
+    pi, ns, th = ekv.select(dc, Hq, sel, alpha=alpha, mu=mu, sigma2=s2)
+    torch.cuda.synchronize()
+    pi, ns, th = pi.cpu().numpy(), ns.cpu().numpy(), th.cpu().numpy()
+    zq = oracle.zq_table(0.99, 16)
+    for b in range(B):
+        counts = hc.page_counts(b)
+        for h in range(Hq):
+            _, om, os2 = hc.score_pages(qh[b, h], b, h // G, modes=2)
+            t_ref = oracle.gauss_tau(om, os2, counts, alpha)
+            assert abs(th[b, h] - t_ref) <= 1e-10 * max(1.0, abs(t_ref)), (b, h, th[b, h], t_ref)
+            ref = oracle.gauss_select(om, os2, counts, alpha, th[b, h], 0.05, zq)
+            assert pi[b, h, :ns[b, h]].tolist() == ref.tolist()
+
+
+def test_decode_gauss_end_to_end():
+    B, sl, Hq, Hkv = 2, [2048, 1333], 8, 2
+    wl, dc, hc = make_pair(B, sl, Hq, Hkv, seed=31, kind="planted")
+    G = Hq // Hkv
+    qh = q_host(wl)
+    sel = ekv.select_params("gauss", q_page=0.99, margin=0.1)
+    ws = ekv.alloc_workspace(dc, Hq, sel)
+    st = ekv.DecodeStats(B, Hq, "cuda", delta_bar=False, gauss=True)
+    out = ekv.decode(dc, wl.q.cuda(), sel, ekv.attn_params(1.5), ws, stats=st)
+    torch.cuda.synchronize()
+    out = out.cpu().numpy()
+    zq = oracle.zq_table(0.99, 16)
+    for b in range(B):
+        counts = hc.page_counts(b)
+        for h in range(Hq):
+            _, om, os2 = hc.score_pages(qh[b, h], b, h // G, modes=2)
+            pages = oracle.gauss_select(om, os2, counts, 1.5, float(st.tau_hat[b, h]), 0.1, zq)
+            assert int(st.n_sel[b, h]) == len(pages)
+            ref = hc.attend(qh[b, h], b, h // G, pages, 1.5)
+            np.testing.assert_allclose(out[b, h], ref["o"], atol=2e-3, rtol=0)
+            assert int(st.supp_count[b, h]) == ref["supp"]
+
+
+def test_prop2_exactness_on_gpu():
+    """Pages containing the full support -> sparse == full on the GPU path."""
+    B, Hq, Hkv = 1, 8, 2
+    wl, dc, hc = make_pair(B, 3000, Hq, Hkv, seed=37, kind="planted")
+    qh = q_host(wl)
+    out_f, tau_f, _ = ekv.full_attend(dc, wl.q.cuda(), ekv.attn_params(1.5))
+    cap = 40
+    pi = torch.full((B, Hq, cap), -1, dtype=torch.int32)
+    ns = torch.zeros(B, Hq, dtype=torch.int32)
+    M = hc.n_pages(0)
+    for h in range(Hq):
+        full = hc.attend(qh[0, h], 0, h // 4, np.arange(M, dtype=np.int32), 1.5, want_p=True)
+        pages = sorted({j // 16 for j in np.nonzero(full["p"])[0]} | {0, M - 1})[:cap]
+        pi[0, h, :len(pages)] = torch.tensor(pages, dtype=torch.int32)
+        ns[0, h] = len(pages)
+    out_s, tau_s, _ = ekv.sparse_attend(dc, wl.q.cuda(), pi.cuda(), ns.cuda(), ekv.attn_params(1.5))
+    torch.cuda.synchronize()
+    assert torch.max(torch.abs(out_s - out_f)).item() <= 2e-3
+    assert torch.max(torch.abs(tau_s - tau_f)).item() <= 1e-9
+
+
+def test_errors_fail_loudly():
+    wl = make_workload(1, 64, 4, 1, seed=1)
+    dc = device_cache(wl)
+    with pytest.raises(ekv.EkvError):
+        ekv.full_attend(dc, wl.q.cuda(), ekv.attn_params(1.0))         # alpha <= 1
+    with pytest.raises(ekv.EkvError):
+        ekv.select(dc, 4, ekv.select_params("topk", 0), box=torch.zeros(1, 4, dc.max_pages, device="cuda"))
+    box, mu, s2 = ekv.score_pages(dc, wl.q.cuda(), modes=3)
+    with pytest.raises(ekv.EkvError):
+        ekv.select(dc, 4, ekv.select_params("gauss"), alpha=1.7, mu=mu, sigma2=s2)   # non-integer beta
