@@ -183,8 +183,11 @@ def main():
     P = 16
     M = (n + P - 1) // P
     k_pages = max(1, math.ceil(args.budget * M))
-    spare = args.steps + args.warmup + 64
-    wl = make_workload(1, n, Hq, Hkv, seed=1000 + rank, device=dev, spare_tokens=spare)
+    # appended tokens grow the sequence; start slightly below n so that the context
+    # stays within the 65536-page table (n = 2^20 -> 1,048,576 - spare ... 1,048,576 tokens)
+    spare = args.steps + args.warmup + 64 + max(5, args.steps // 2) + 16
+    n0 = n - spare if (n + spare + P - 1) // P > 65536 else n
+    wl = make_workload(1, n0, Hq, Hkv, seed=1000 + rank, device=dev, spare_tokens=n - n0 if n0 < n else spare)
     cache = ekv.PagedCache.allocate_meta(wl.K, wl.V, wl.page_table, wl.seq_lens)
     ekv.rebuild_page_stats(cache)
     sel = ekv.select_params(args.policy, k_pages, 0.99, 0.0)
@@ -212,18 +215,20 @@ def main():
     stream.synchronize()
     launches_per_step = 1 + launches_decode
 
-    for _ in range(args.warmup):
-        g.replay()
+    with torch.cuda.stream(stream):        # replay() launches on the current stream
+        for _ in range(args.warmup):
+            g.replay()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(args.steps):
-            g.replay()
-        e1.record(stream)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(args.steps):
+                g.replay()
+            e1.record(stream)
         torch.cuda.synchronize()
     t_ms = e0.elapsed_time(e1)
     if world > 1:
@@ -243,14 +248,15 @@ def main():
         stream.synchronize()
         with torch.cuda.graph(gg, stream=stream):
             fn()
-        for _ in range(3):
-            gg.replay()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        a.record(stream)
-        for _ in range(reps):
-            gg.replay()
-        b.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                gg.replay()
+            torch.cuda.synchronize()
+            a.record(stream)
+            for _ in range(reps):
+                gg.replay()
+            b.record(stream)
         torch.cuda.synchronize()
         return a.elapsed_time(b) * 1e3 / reps
 

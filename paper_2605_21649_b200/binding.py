@@ -192,10 +192,9 @@ def select_capacity(cache: PagedCache, sel: ekv_select_params) -> int:
     return int(lib().entmaxkv_select_capacity(ctypes.byref(cs), ctypes.byref(sel)))
 
 
-def alloc_workspace(cache, n_q_heads, sel, eval_exact=False):
+def alloc_workspace(cache, n_q_heads, sel=None, eval_exact=False):
+    """One workspace serves decode (incl. eval_exact), select, sparse_attend and full_attend."""
     n = workspace_size(cache, n_q_heads, sel)
-    if eval_exact:
-        n += workspace_size(cache, n_q_heads, None)
     return torch.empty(n, dtype=torch.uint8, device=cache.K.device)
 
 

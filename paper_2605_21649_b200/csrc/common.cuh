@@ -260,3 +260,52 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
 }
 
 }  // namespace ekv
+
+namespace ekv {
+// ---------------------------------------------------------------- packed fp32x2 FMA (sm_100: FFMA2)
+// {a.x*b + c.x, a.y*b + c.y}, each an IEEE fma with round-to-nearest: bit-identical to two
+// __fmaf_rn; ptxas folds the broadcast of b into the FFMA2 operand.
+__device__ __forceinline__ float2 ffma2(float2 a, float b, float2 c) {
+    unsigned long long ra, rb, rc, rd;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1,%1};" : "=l"(rb) : "f"(b));
+    asm("mov.b64 %0, {%1,%2};" : "=l"(rc) : "f"(c.x), "f"(c.y));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(rb), "l"(rc));
+    float2 d;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
+    return d;
+}
+
+// bitonic sort of n (power of two) u64 keys in shared memory, ascending; all threads call.
+template <int NT> __device__ __forceinline__ void bitonic_sort_u64(unsigned long long *a, int n) {
+    for (int k = 2; k <= n; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n; i += NT) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const unsigned long long x = a[i], y = a[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((x > y) == up) { a[i] = y; a[ixj] = x; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+template <int NT> __device__ __forceinline__ void bitonic_sort_u32_desc(uint32_t *a, int n) {
+    for (int k = 2; k <= n; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n; i += NT) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const uint32_t x = a[i], y = a[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((x < y) == up) { a[i] = y; a[ixj] = x; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+__device__ __forceinline__ int next_pow2(int x) { int p = 1; while (p < x) p <<= 1; return p; }
+}  // namespace ekv

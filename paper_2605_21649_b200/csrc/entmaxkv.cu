@@ -76,45 +76,48 @@ CacheView view(const ekv_cache *c) {
     return v;
 }
 
+int c_max(const ekv_cache *c) { return c->max_pages_per_seq; }
+
 int sel_cap(const ekv_cache *c, const ekv_select_params *s) {
     if (!s || s->policy != EKV_TOPK) return c->max_pages_per_seq;
     return s->k_pages < c->max_pages_per_seq ? s->k_pages : c->max_pages_per_seq;
 }
 
 // ---------------------------------------------------------------- workspace layout
+// One layout serves decode (incl. eval_exact), select, sparse_attend and full_attend.
 struct Layout {
-    size_t box, mu, sigma2, page_idx, n_sel, tau_hat, upages, umask, ulen, scores, tok_list, p_list, n_list, full_out;
-    size_t sparse_total;   // end of the sparse region
-    size_t full_scores, total;
-    int cap, ucap, list_cap;
+    size_t box, mu, sigma2, page_idx, n_sel, tau_hat;
+    size_t zero, rowmax, ccount, umask, zero_bytes;   // zeroed per attention pass
+    size_t scores, cand_s, cand_j, tok_list, p_list, n_list, full_out, total;
+    int cap, W, list_cap;
 };
 
 Layout layout(const ekv_cache *c, int Hq, const ekv_select_params *sel) {
     Layout L;
     const size_t B = c->batch, Hkv = c->n_kv_heads, maxp = c->max_pages_per_seq;
-    const int G = Hq / c->n_kv_heads;
     L.cap = sel_cap(c, sel);
-    long long uc = (long long)G * L.cap;
-    L.ucap = (int)(uc < (long long)maxp ? uc : (long long)maxp);
+    L.W = (int)((maxp + 3) / 4);
     L.list_cap = kCap;
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o += align256(bytes); return r; };
     L.box = take(B * Hq * maxp * 4);
     L.mu = take(B * Hq * maxp * 4);
     L.sigma2 = take(B * Hq * maxp * 4);
-    L.page_idx = take(B * Hq * (size_t)L.cap * 4);
+    L.page_idx = take(B * Hq * maxp * 4);          // capacity max_pages: also serves the eval pass
     L.n_sel = take(B * Hq * 4);
     L.tau_hat = take(B * Hq * 8);
-    L.upages = take(B * Hkv * (size_t)L.ucap * 4);
-    L.umask = take(B * Hkv * (size_t)L.ucap);
-    L.ulen = take(B * Hkv * 4);
-    L.scores = take(B * Hq * (size_t)L.ucap * kP * 4);
+    L.zero = o;
+    L.rowmax = take(B * Hq * 4);
+    L.ccount = take(B * Hq * 4);
+    L.umask = take(B * Hkv * (size_t)L.W * 4);
+    L.zero_bytes = o - L.zero;
+    L.scores = take(B * Hq * maxp * kP * 4);
+    L.cand_s = take(B * Hq * (size_t)kCapG * 4);
+    L.cand_j = take(B * Hq * (size_t)kCapG * 4);
     L.tok_list = take(B * Hq * (size_t)L.list_cap * 4);
     L.p_list = take(B * Hq * (size_t)L.list_cap * 8);
     L.n_list = take(B * Hq * 4);
     L.full_out = take(B * Hq * kD * 4);
-    L.sparse_total = o;
-    L.full_scores = take(B * Hq * maxp * kP * 4);
     L.total = o;
     return L;
 }
@@ -165,43 +168,36 @@ ekv_status launch_topk(const float *box, int B, int Hq, int maxp, const int32_t 
     return check_launch("k_topk");
 }
 
-ekv_status launch_union(const ekv_cache *c, int Hq, const int32_t *pi, const int32_t *ns, int stride, int32_t *up,
-                        uint8_t *um, int32_t *ul, int ucap, cudaStream_t st) {
-    const int G = Hq / c->n_kv_heads;
-    const int smem = 4 * ((c->max_pages_per_seq + 3) / 4);
-    static bool init = false;
-    if (!init) { set_smem(k_union<512>, 65536); init = true; }
-    k_union<512><<<c->batch * c->n_kv_heads, 512, smem, st>>>(c->n_kv_heads, G, c->max_pages_per_seq, c->seq_lens,
-                                                               pi, ns, stride, up, um, ul, ucap);
-    return check_launch("k_union");
+ekv_status launch_mark(const ekv_cache *c, int Hq, const int32_t *pi, const int32_t *ns, int stride, uint32_t *um,
+                       int W, cudaStream_t st) {
+    k_mark<<<c->batch * Hq, 256, 0, st>>>(Hq, Hq / c->n_kv_heads, pi, ns, stride, um, W);
+    return check_launch("k_mark");
 }
 
 template <typename T, int G>
-ekv_status launch_scores_t(const CacheView &v, const void *q, int Hq, const int32_t *up, const uint8_t *um,
-                           const int32_t *ul, int ucap, float *scores, int full, cudaStream_t st) {
-    constexpr int PPC = sizeof(T) == 2 ? 16 : 8;
-    constexpr int smem = PPC * kP * kD * (int)sizeof(T);
+ekv_status launch_scores_t(const CacheView &v, const void *q, int Hq, const uint32_t *um, int W, float *scores,
+                           uint32_t *rowmax, int full, cudaStream_t st) {
+    constexpr int smem = 2 * 8 * kP * kD * (int)sizeof(T);
     static bool init = false;
-    if (!init) { set_smem(k_attend_scores<T, G, PPC>, smem); init = true; }
-    dim3 grid((ucap + PPC - 1) / PPC, v.B * v.Hkv);
-    k_attend_scores<T, G, PPC><<<grid, 128, smem, st>>>(v, static_cast<const T *>(q), Hq, up, um, ul, ucap, scores,
-                                                        full);
+    if (!init) { set_smem(k_attend_scores<T, G>, smem); init = true; }
+    dim3 grid((v.maxp + 127) / 128, v.B * v.Hkv);
+    k_attend_scores<T, G><<<grid, 256, smem, st>>>(v, static_cast<const T *>(q), Hq, um, W, scores, rowmax, full);
     return check_launch("k_attend_scores");
 }
 template <typename T>
-ekv_status launch_scores(const CacheView &v, const void *q, int Hq, const int32_t *up, const uint8_t *um,
-                         const int32_t *ul, int ucap, float *scores, int full, cudaStream_t st) {
+ekv_status launch_scores(const CacheView &v, const void *q, int Hq, const uint32_t *um, int W, float *scores,
+                         uint32_t *rowmax, int full, cudaStream_t st) {
     switch (Hq / v.Hkv) {
-    case 1: return launch_scores_t<T, 1>(v, q, Hq, up, um, ul, ucap, scores, full, st);
-    case 2: return launch_scores_t<T, 2>(v, q, Hq, up, um, ul, ucap, scores, full, st);
-    case 4: return launch_scores_t<T, 4>(v, q, Hq, up, um, ul, ucap, scores, full, st);
-    default: return launch_scores_t<T, 8>(v, q, Hq, up, um, ul, ucap, scores, full, st);
+    case 1: return launch_scores_t<T, 1>(v, q, Hq, um, W, scores, rowmax, full, st);
+    case 2: return launch_scores_t<T, 2>(v, q, Hq, um, W, scores, rowmax, full, st);
+    case 4: return launch_scores_t<T, 4>(v, q, Hq, um, W, scores, rowmax, full, st);
+    default: return launch_scores_t<T, 8>(v, q, Hq, um, W, scores, rowmax, full, st);
     }
 }
 
 template <typename T>
 ekv_status launch_tau(const CacheView &v, const TauArgs &A, int rows, cudaStream_t st) {
-    constexpr int smem = kCap * (int)(sizeof(float) + sizeof(int) + 1);
+    constexpr int smem = 8192 * 8 + kCap;
     static bool init = false;
     if (!init) { set_smem(k_tau_pv<T>, smem); init = true; }
     k_tau_pv<T><<<rows, kTauNT, smem, st>>>(v, A);
@@ -233,44 +229,39 @@ ekv_status check_sel(const ekv_select_params *s, float alpha) {
     return EKV_OK;
 }
 
-// sparse attention over given page lists (union + scores + tau/pv)
-ekv_status sparse_attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t *pi, const int32_t *ns,
-                              int stride, const ekv_attn_params *attn, float *out, double *tau, int32_t *supp,
-                              void *ws, const Layout &L, cudaStream_t st, TauArgs *extra) {
+// attention of every (b, q-head) over its page list (full: every page):
+// memset(rowmax, ccount, umask) -> [mark] -> K scores -> candidates -> tau/PV
+ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t *pi, const int32_t *ns, int stride,
+                       int full, const ekv_attn_params *attn, float *out, double *tau, int32_t *supp, void *ws,
+                       const Layout &L, cudaStream_t st, const TauArgs *extra) {
     const CacheView v = view(c);
-    int32_t *up = at<int32_t>(ws, L.upages);
-    uint8_t *um = at<uint8_t>(ws, L.umask);
-    int32_t *ul = at<int32_t>(ws, L.ulen);
+    uint32_t *rowmax = at<uint32_t>(ws, L.rowmax);
+    int *ccount = at<int>(ws, L.ccount);
+    uint32_t *um = at<uint32_t>(ws, L.umask);
     float *scores = at<float>(ws, L.scores);
-    EKV_TRY(launch_union(c, Hq, pi, ns, stride, up, um, ul, L.ucap, st));
-    if (c->dtype == EKV_BF16) EKV_TRY(launch_scores<__nv_bfloat16>(v, q, Hq, up, um, ul, L.ucap, scores, 0, st));
-    else EKV_TRY(launch_scores<float>(v, q, Hq, up, um, ul, L.ucap, scores, 0, st));
+    if (cudaMemsetAsync(at<char>(ws, L.zero), 0, L.zero_bytes, st) != cudaSuccess)
+        return fail(EKV_ERR_CUDA, "memset: %s", cudaGetErrorString(cudaGetLastError()));
+    if (!full) EKV_TRY(launch_mark(c, Hq, pi, ns, stride, um, L.W, st));
+    if (c->dtype == EKV_BF16) EKV_TRY(launch_scores<__nv_bfloat16>(v, q, Hq, um, L.W, scores, rowmax, full, st));
+    else EKV_TRY(launch_scores<float>(v, q, Hq, um, L.W, scores, rowmax, full, st));
+    const int rows = c->batch * Hq;
+    const size_t ntok = (size_t)c->max_pages_per_seq * kP;
+    float *cs = at<float>(ws, L.cand_s);
+    int32_t *cj = at<int32_t>(ws, L.cand_j);
+    const int list_len = full ? c->max_pages_per_seq : stride;
+    dim3 cg((list_len + 255) / 256, rows);
+    k_candidates<<<cg, 256, 0, st>>>(scores, ntok, rowmax, pi, ns, stride, c->seq_lens, Hq, full, attn->alpha,
+                                     attn->transform, ccount, cs, cj, kCapG);
+    EKV_TRY(check_launch("k_candidates"));
     TauArgs A;
     memset(&A, 0, sizeof(A));
     if (extra) A = *extra;
-    A.scores = scores; A.ntok_stride = (size_t)L.ucap * kP;
-    A.union_pages = up; A.union_len = ul; A.ucap = L.ucap; A.full = 0;
+    A.scores = scores; A.ntok = ntok; A.rowmax = rowmax; A.ccount = ccount; A.cand_s = cs; A.cand_j = cj;
+    A.capG = kCapG; A.page_idx = pi; A.n_sel = ns; A.sel_stride = stride; A.full = full;
     A.Hq = Hq; A.G = Hq / c->n_kv_heads; A.alpha = attn->alpha; A.transform = attn->transform;
     A.out = out; A.tau_out = tau; A.supp_out = supp;
-    if (c->dtype == EKV_BF16) return launch_tau<__nv_bfloat16>(v, A, c->batch * Hq, st);
-    return launch_tau<float>(v, A, c->batch * Hq, st);
-}
-
-ekv_status full_attend_impl(const ekv_cache *c, const void *q, int Hq, const ekv_attn_params *attn, float *out,
-                            double *tau, int32_t *supp, float *scores, cudaStream_t st, TauArgs *extra) {
-    const CacheView v = view(c);
-    const int maxp = c->max_pages_per_seq;
-    if (c->dtype == EKV_BF16) EKV_TRY(launch_scores<__nv_bfloat16>(v, q, Hq, nullptr, nullptr, nullptr, maxp, scores, 1, st));
-    else EKV_TRY(launch_scores<float>(v, q, Hq, nullptr, nullptr, nullptr, maxp, scores, 1, st));
-    TauArgs A;
-    memset(&A, 0, sizeof(A));
-    if (extra) A = *extra;
-    A.scores = scores; A.ntok_stride = (size_t)maxp * kP;
-    A.union_pages = nullptr; A.union_len = nullptr; A.ucap = maxp; A.full = 1;
-    A.Hq = Hq; A.G = Hq / c->n_kv_heads; A.alpha = attn->alpha; A.transform = attn->transform;
-    A.out = out; A.tau_out = tau; A.supp_out = supp;
-    if (c->dtype == EKV_BF16) return launch_tau<__nv_bfloat16>(v, A, c->batch * Hq, st);
-    return launch_tau<float>(v, A, c->batch * Hq, st);
+    if (c->dtype == EKV_BF16) return launch_tau<__nv_bfloat16>(v, A, rows, st);
+    return launch_tau<float>(v, A, rows, st);
 }
 
 }  // namespace
@@ -284,9 +275,7 @@ int32_t entmaxkv_last_launch_count(void) { return g_launches; }
 
 size_t entmaxkv_workspace_size(const ekv_cache *cache, int32_t n_q_heads, const ekv_select_params *sel) {
     if (check_cache(cache, n_q_heads) != EKV_OK) return 0;
-    Layout L = layout(cache, n_q_heads, sel);
-    if (!sel || sel->policy == EKV_ALL) return L.total - L.sparse_total + 256;
-    return L.sparse_total;
+    return layout(cache, n_q_heads, sel).total;
 }
 
 int32_t entmaxkv_select_capacity(const ekv_cache *cache, const ekv_select_params *sel) {
@@ -383,11 +372,9 @@ ekv_status entmaxkv_sparse_attend(const ekv_cache *cache, const void *q, int32_t
     if (!q || !page_idx || !n_sel || !out || !workspace) return fail(EKV_ERR_INVALID_ARG, "NULL argument");
     if (sel_stride < 1) return fail(EKV_ERR_INVALID_ARG, "sel_stride < 1");
     g_launches = 0;
-    ekv_select_params sp;
-    sp.policy = EKV_TOPK; sp.k_pages = sel_stride; sp.q_page = 0.99; sp.margin = 0.0;
-    Layout L = layout(cache, n_q_heads, &sp);
-    return sparse_attend_impl(cache, q, n_q_heads, page_idx, n_sel, sel_stride, attn, out, tau, supp, workspace, L,
-                              static_cast<cudaStream_t>(stream), nullptr);
+    Layout L = layout(cache, n_q_heads, nullptr);
+    return attend_impl(cache, q, n_q_heads, page_idx, n_sel, sel_stride, 0, attn, out, tau, supp, workspace, L,
+                       static_cast<cudaStream_t>(stream), nullptr);
 }
 
 ekv_status entmaxkv_full_attend(const ekv_cache *cache, const void *q, int32_t n_q_heads, const ekv_attn_params *attn,
@@ -397,8 +384,9 @@ ekv_status entmaxkv_full_attend(const ekv_cache *cache, const void *q, int32_t n
     EKV_TRY(check_attn(attn));
     if (!q || !out || !workspace) return fail(EKV_ERR_INVALID_ARG, "NULL argument");
     g_launches = 0;
-    return full_attend_impl(cache, q, n_q_heads, attn, out, tau, supp, static_cast<float *>(workspace),
-                            static_cast<cudaStream_t>(stream), nullptr);
+    Layout L = layout(cache, n_q_heads, nullptr);
+    return attend_impl(cache, q, n_q_heads, at<int32_t>(workspace, L.page_idx), at<int32_t>(workspace, L.n_sel),
+                       c_max(cache), 1, attn, out, tau, supp, workspace, L, static_cast<cudaStream_t>(stream), nullptr);
 }
 
 ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_heads, const ekv_select_params *sel,
@@ -421,7 +409,7 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
     int32_t *pi = at<int32_t>(workspace, L.page_idx);
     int32_t *ns = at<int32_t>(workspace, L.n_sel);
     double *th = at<double>(workspace, L.tau_hat);
-    const bool want_db = stats && stats->delta_bar;
+    const bool want_db = stats && stats->delta_bar && attn->transform == EKV_ENTMAX;
     // a1: page scores (box for top-k and for the certificate; mu/sigma2 for Gaussian)
     int modes = 0;
     if (sel->policy == EKV_TOPK || want_db) modes |= EKV_SCORE_BOX;
@@ -444,12 +432,9 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
     // a3 (+a4 certificate)
     TauArgs extra;
     memset(&extra, 0, sizeof(extra));
-    if (want_db && attn->transform == EKV_ENTMAX) {
-        extra.box = box; extra.page_idx = pi; extra.n_sel = ns; extra.sel_stride = L.cap;
-        extra.delta_bar = stats->delta_bar;
-    }
-    EKV_TRY(sparse_attend_impl(cache, q, n_q_heads, pi, ns, L.cap, attn, out, stats ? stats->tau : nullptr,
-                               stats ? stats->supp_count : nullptr, workspace, L, st, &extra));
+    if (want_db) { extra.box = box; extra.delta_bar = stats->delta_bar; }
+    EKV_TRY(attend_impl(cache, q, n_q_heads, pi, ns, L.cap, 0, attn, out, stats ? stats->tau : nullptr,
+                        stats ? stats->supp_count : nullptr, workspace, L, st, &extra));
     const int rows = cache->batch * n_q_heads;
     if (stats) {
         if (stats->n_sel) {
@@ -461,16 +446,16 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
                 return fail(EKV_ERR_CUDA, "tau_hat copy");
         }
         if (stats->eval_exact && attn->transform == EKV_ENTMAX) {
-            // a4 eval: full-cache pass with the support list, then delta / rho counts (R16)
-            float *fs = reinterpret_cast<float *>(static_cast<char *>(workspace) + L.sparse_total);
-            float *fout = at<float>(workspace, L.full_out);
+            // a4 eval: full-cache pass keeping the support list, then delta / rho counts (R16);
+            // the sparse page lists (pi, ns) stay untouched by the full pass.
             TauArgs ex;
             memset(&ex, 0, sizeof(ex));
             ex.tok_list = at<int32_t>(workspace, L.tok_list);
             ex.p_list = at<double>(workspace, L.p_list);
             ex.n_list = at<int32_t>(workspace, L.n_list);
             ex.list_cap = L.list_cap;
-            EKV_TRY(full_attend_impl(cache, q, n_q_heads, attn, fout, stats->tau_full, nullptr, fs, st, &ex));
+            EKV_TRY(attend_impl(cache, q, n_q_heads, pi, ns, L.cap, 1, attn, at<float>(workspace, L.full_out),
+                                stats->tau_full, nullptr, workspace, L, st, &ex));
             k_eval_metrics<<<rows, 256, 0, st>>>(ex.tok_list, ex.p_list, ex.n_list, ex.list_cap, pi, ns, L.cap,
                                                  stats->delta, stats->recovered, stats->full_supp);
             EKV_TRY(check_launch("k_eval_metrics"));

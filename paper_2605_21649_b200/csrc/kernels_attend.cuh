@@ -1,86 +1,110 @@
 // kernels_attend.cuh -- a3/a5/a6: token scores over the selected pages (TMA bulk
-// copies of K tiles into shared memory), exact alpha-entmax threshold + support,
-// and the weighted V sum over the support.
+// copies of K tiles into shared memory), candidate extraction, exact alpha-entmax
+// threshold + support, and the weighted V sum over the support.
 #pragma once
 #include "common.cuh"
 
 namespace ekv {
 
+// Score rows are indexed by token position: scores[b][h][j], j = page * P + t, over
+// the whole sequence capacity (max_pages * P); only tokens of pages selected by head h
+// are written.  rowmax[b][h] holds the ordered-int max score (atomicMax; 0 = empty).
+
 // ============================================================================ K scores
-// Grid (union-slot chunk of PPC pages, b * Hkv + kvh); 128 threads = 8 half-warps.
-// Thread 0 issues one cp.async.bulk (TMA, 1-D) per page tile K[phys][kvh][0..P)[0..d)
-// (4 KiB bf16 / 8 KiB fp32, contiguous in HBM) into its own shared-memory slot, each
-// with its own mbarrier, so all PPC tiles are in flight at once.  Half-warp hw then
-// scores tokens of pages hw, hw+8, ...: lane c reads the 16-byte chunk c of the token's
-// row (a contiguous 256-byte row per half-warp: conflict-free), runs the 8-element fma
-// chains for the G query heads of the group and the reduce-scatter tree (R1);
-// s = fl32(dot * c_d) (R2).  Tokens of pages that query head h did not select, and
-// tokens beyond seq_len, get -inf.  Output scores[b][h][slot * P + t] fp32.
-// full != 0: the union is every page of the sequence (a5).
-template <typename T, int G, int PPC>
-__global__ void __launch_bounds__(128) k_attend_scores(CacheView c, const T *__restrict__ q, int Hq,
-                                                       const int32_t *__restrict__ union_pages,
-                                                       const uint8_t *__restrict__ union_mask,
-                                                       const int32_t *__restrict__ union_len, int ucap,
-                                                       float *__restrict__ scores, int full) {
+// Grid (chunk of CH pages, b * Hkv + kvh); 256 threads = 16 half-warps.
+//  - The selected pages of the chunk (union mask byte != 0, or every page for the full
+//    baseline) are compacted ascending into shared memory.
+//  - They are processed in batches of BP pages through a 2-stage ring: thread 0 issues
+//    one cp.async.bulk (TMA, 1-D) per page tile K[phys][kvh][0..P)[0..d) (4 KiB bf16,
+//    contiguous in HBM) completing on the stage's mbarrier; batch i+1 is in flight
+//    while batch i is scored.
+//  - Two half-warps per page, 8 tokens each: lane c reads the 16-byte chunk c of the
+//    token row (contiguous 256-byte row per half-warp: conflict-free), runs the
+//    8-element fma chains for the G query heads (R1) and the reduce-scatter tree;
+//    s = fl32(dot * c_d) (R2).  Tokens past seq_len get -inf.
+//  - Per-head running max -> one atomicMax per (CTA, head) into rowmax.
+template <typename T, int G>
+__global__ void __launch_bounds__(256) k_attend_scores(CacheView c, const T *__restrict__ q, int Hq,
+                                                       const uint32_t *__restrict__ umask, int W,
+                                                       float *__restrict__ scores, uint32_t *__restrict__ rowmax,
+                                                       int full) {
+    constexpr int CH = 128;                 // pages per CTA
+    constexpr int BP = 8;                   // pages per batch (stage)
     constexpr int TILE = kP * kD * (int)sizeof(T);
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ uint64_t bars[PPC];
-    __shared__ int s_page[PPC];
-    __shared__ uint8_t s_mask[PPC];
+    extern __shared__ __align__(128) unsigned char smem[];   // [2][BP][TILE]
+    __shared__ uint64_t bars[2];
+    __shared__ int s_pages[CH];
+    __shared__ uint8_t s_mask[CH];
+    __shared__ int sh[9];
+    __shared__ uint32_t s_max[16][G];
     const int unit = blockIdx.y;
     const int b = unit / c.Hkv, kvh = unit % c.Hkv;
     const int L = c.seq_lens[b];
-    const int ulen = full ? n_pages_of(L) : union_len[unit];
-    const int u0 = blockIdx.x * PPC;
-    if (u0 >= ulen) return;
-    const int nu = min(PPC, ulen - u0);
-    if (threadIdx.x < nu) {
-        const int u = u0 + threadIdx.x;
-        s_page[threadIdx.x] = full ? u : union_pages[(size_t)unit * ucap + u];
-        s_mask[threadIdx.x] = full ? (uint8_t)0xff : union_mask[(size_t)unit * ucap + u];
+    const int M = n_pages_of(L);
+    const int p0 = blockIdx.x * CH;
+    if (p0 >= M) return;
+    const int tid = threadIdx.x;
+    // compact the selected pages of [p0, p0 + CH)
+    {
+        const int p = p0 + (tid & (CH - 1));
+        uint8_t m = 0;
+        if (tid < CH && p < M) {
+            m = full ? (uint8_t)((1u << G) - 1u)
+                     : (uint8_t)((umask[((size_t)b * c.Hkv + kvh) * W + (p >> 2)] >> ((p & 3) * 8)) & 0xffu);
+        }
+        int tot;
+        const int pos = block_excl_scan<256>(m ? 1 : 0, sh, &tot);
+        if (m) { s_pages[pos] = p; s_mask[pos] = m; }
+        if (tid == 0) sh[8] = tot;
     }
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < nu; ++i) mbar_init(&bars[i], 1);
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
         fence_mbar_init();
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned char *Kb = reinterpret_cast<const unsigned char *>(c.K);
-        for (int i = 0; i < nu; ++i) {
-            const int phys = c.page_table[(size_t)b * c.maxp + s_page[i]];
-            mbar_expect_tx(&bars[i], TILE);
-            bulk_g2s(smem + (size_t)i * TILE, Kb + ((size_t)phys * c.Hkv + kvh) * TILE, TILE, &bars[i]);
+    const int np = sh[8];
+    if (np == 0) return;
+    const int nb = (np + BP - 1) / BP;
+    const unsigned char *Kb = reinterpret_cast<const unsigned char *>(c.K);
+    auto issue = [&](int bi) {
+        const int st = bi & 1;
+        const int n = min(BP, np - bi * BP);
+        mbar_expect_tx(&bars[st], n * TILE);
+        for (int i = 0; i < n; ++i) {
+            const int phys = __ldg(c.page_table + (size_t)b * c.maxp + s_pages[bi * BP + i]);
+            bulk_g2s(smem + ((size_t)st * BP + i) * TILE, Kb + ((size_t)phys * c.Hkv + kvh) * TILE, TILE, &bars[st]);
         }
+    };
+    if (tid == 0) {
+        issue(0);
+        if (nb > 1) issue(1);
     }
-    const int lane = threadIdx.x & 31;
-    const int l16 = threadIdx.x & 15;
-    const int hw = threadIdx.x >> 4;
+    const int lane = tid & 31, l16 = tid & 15, hw = tid >> 4;
     float qr[G][8];
 #pragma unroll
-    for (int g = 0; g < G; ++g)
-        Elem<T>::load8(q + ((size_t)b * Hq + kvh * G + g) * kD + 8 * l16, qr[g]);
+    for (int g = 0; g < G; ++g) Elem<T>::load8(q + ((size_t)b * Hq + kvh * G + g) * kD + 8 * l16, qr[g]);
     const int hsel = rs_head<G>(lane);
     const bool writer = rs_writer<G>(lane);
-    const size_t ntok = (size_t)ucap * kP;
+    const size_t ntok = (size_t)c.maxp * kP;
     float *srow = scores + ((size_t)b * Hq + kvh * G + hsel) * ntok;
-    // warp-uniform loop: both half-warps of a warp iterate over the same i range
-    for (int ib = (hw & ~1); ib < nu + 1; ib += 8) {
-        const int i = ib + (hw & 1);
-        const bool active = i < nu;
-        if (ib >= nu) break;
-        if (active) mbar_wait(&bars[i], 0);
-        const int page = active ? s_page[i] : 0;
-        const bool hsel_ok = active && ((s_mask[active ? i : 0] >> hsel) & 1);
-        const T *tile = reinterpret_cast<const T *>(smem + (size_t)(active ? i : 0) * TILE);
+    float runmax = -INFINITY;
+    const int pi_local = hw >> 1;           // page within the batch (2 half-warps per page)
+    const int t0 = (hw & 1) * 8;            // first token of this half-warp
+    for (int bi = 0; bi < nb; ++bi) {
+        const int st = bi & 1;
+        mbar_wait(&bars[st], (bi >> 1) & 1);
+        const int n = min(BP, np - bi * BP);
+        const bool active = pi_local < n;
+        const int pidx = bi * BP + (active ? pi_local : 0);
+        const int page = s_pages[pidx];
+        const bool hok = active && ((s_mask[pidx] >> hsel) & 1);
+        const T *tile = reinterpret_cast<const T *>(smem + ((size_t)st * BP + (active ? pi_local : 0)) * TILE);
 #pragma unroll 4
-        for (int t = 0; t < kP; ++t) {
+        for (int tt = 0; tt < 8; ++tt) {
+            const int t = t0 + tt;
             float kx[8];
-            if (active) Elem<T>::load8(tile + t * kD + 8 * l16, kx);
-            else {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) kx[e] = 0.0f;
-            }
+            Elem<T>::load8(tile + t * kD + 8 * l16, kx);
             float acc[G];
 #pragma unroll
             for (int g = 0; g < G; ++g) {
@@ -91,102 +115,183 @@ __global__ void __launch_bounds__(128) k_attend_scores(CacheView c, const T *__r
             }
             const float s = __fmul_rn(rs_reduce16<G>(acc, lane), kCd);
             const int tok = page * kP + t;
-            if (writer && active) srow[(size_t)(u0 + i) * kP + t] = (hsel_ok && tok < L) ? s : -INFINITY;
+            if (writer && hok) {
+                const float v = tok < L ? s : -INFINITY;
+                srow[tok] = v;
+                runmax = fmaxf(runmax, v);
+            }
+        }
+        __syncthreads();                     // everyone is done with stage st
+        if (tid == 0 && bi + 2 < nb) issue(bi + 2);
+    }
+    // per-head max -> rowmax (one atomic per CTA and head)
+    if (writer) s_max[hw][hsel] = f2key(runmax);
+    __syncthreads();
+    if (tid < G) {
+        uint32_t m = 0u;
+        for (int w = 0; w < 16; ++w) m = max(m, s_max[w][tid]);
+        // -inf (key 0x007fffff) never beats an empty row's 0 sentinel... only real scores count
+        if (m > f2key(-INFINITY)) atomicMax(rowmax + (size_t)b * Hq + kvh * G + tid, m);
+    }
+}
+
+// ============================================================================ candidates
+// Grid (chunk of 256 page-list entries, b * Hq + h); thread = one selected page of the
+// row (sparse: page_idx[row][i]; full: page i).  A token is a candidate iff
+// z = (double)a * s > tau_lo = a * s_max - 1 (tau >= z_max - 1 since F(z_max - 1) >= 1,
+// R9).  Softmax rows take every valid token.  Per-CTA block scan + one atomicAdd for
+// the row offset; the order across CTAs is fixed later by sorting on the token index.
+__global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ scores, size_t ntok,
+                                                    const uint32_t *__restrict__ rowmax,
+                                                    const int32_t *__restrict__ page_idx,
+                                                    const int32_t *__restrict__ n_sel, int sel_stride,
+                                                    const int32_t *__restrict__ seq_lens, int Hq, int full,
+                                                    float alpha, int transform, int *__restrict__ ccount,
+                                                    float *__restrict__ cand_s, int32_t *__restrict__ cand_j,
+                                                    int capG) {
+    __shared__ int sh[9];
+    __shared__ int s_base;
+    const int row = blockIdx.y;
+    const int b = row / Hq;
+    const int L = seq_lens[b];
+    const int nlist = full ? n_pages_of(L) : n_sel[row];
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    if (blockIdx.x * 256 >= nlist) return;
+    const uint32_t mk = rowmax[row];
+    if (mk == 0u || transform == 1) return;     // softmax rows stream the row in k_tau_pv
+    const double a = (double)alpha - 1.0;
+    const double zmax = a * (double)key2f(mk);
+    const double tau_lo = zmax - 1.0 - 1e-12 * fmax(1.0, fabs(zmax));
+    float sv[kP];
+    int page = 0, cnt = 0;
+    const float *srow = scores + (size_t)row * ntok;
+    if (i < nlist) {
+        page = full ? i : page_idx[(size_t)row * sel_stride + i];
+        const float4 *p4 = reinterpret_cast<const float4 *>(srow + (size_t)page * kP);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const float4 x = p4[v];
+            sv[4 * v] = x.x; sv[4 * v + 1] = x.y; sv[4 * v + 2] = x.z; sv[4 * v + 3] = x.w;
+        }
+#pragma unroll
+        for (int t = 0; t < kP; ++t) {
+            const bool keep = (page * kP + t < L) && sv[t] != -INFINITY && a * (double)sv[t] > tau_lo;
+            cnt += keep ? 1 : 0;
+        }
+    }
+    int tot;
+    int pos = block_excl_scan<256>(cnt, sh, &tot);
+    if (threadIdx.x == 0) s_base = tot ? atomicAdd(ccount + row, tot) : 0;
+    __syncthreads();
+    pos += s_base;
+    if (i < nlist && cnt) {
+#pragma unroll
+        for (int t = 0; t < kP; ++t) {
+            const bool keep = (page * kP + t < L) && sv[t] != -INFINITY && a * (double)sv[t] > tau_lo;
+            if (keep) {
+                if (pos < capG) {
+                    cand_s[(size_t)row * capG + pos] = sv[t];
+                    cand_j[(size_t)row * capG + pos] = page * kP + t;
+                }
+                ++pos;
+            }
         }
     }
 }
 
 // ============================================================================ exact tau + PV
-// One CTA (NT = 256) per (b, q-head).  On the row of fp32 scores over the group's
-// union slots (-inf = not in C_tok(b,h)):
-//  1. s_max (block max);  z = (double)a * (double)s  (R9).
-//  2. tau_lo = z_max - 1 (F(z_max - 1) >= 1, so tau >= tau_lo).  Candidates
-//     {z > tau_lo} are compacted IN SLOT ORDER into shared memory (deterministic).  If
-//     more than CAP, the threshold of the first CAP candidates (a subset, so a lower
-//     bound of tau: F_subset <= F) raises tau_lo and the compaction repeats.
-//  3. Newton on g(tau) = ||(z - tau)_+||_beta - 1 (convex, decreasing -> monotone from
-//     the left, exact in one step for a single active token).
-//  4. Support by R9: z > tau_N + band -> in, z < tau_N - band -> out, otherwise decide
-//     by F(z_j) < 1 evaluated over all candidates (fp64).
-//  5. tau from the support: beta = 1: (S1 - 1)/k; beta = 2: m - sqrt((1 - ss)/k);
-//     otherwise one Newton polish of sum_S (z - tau)^beta = 1.
-//  6. p_j = (z_j - tau)^beta; out = sum p_j v_j / sum p_j (R12), V rows gathered only
-//     for support tokens (warp per token, lane = 4 dims).
-// Softmax (a6): p = exp(s - s_max) over every valid token, dense V.
+// One CTA (256 threads) per (b, q-head):
+//  1. the row's candidates are loaded into shared memory and bitonic-sorted by token
+//     index (deterministic order for every fp64 sum below);
+//  2. Newton on g(tau) = ||(z - tau)_+||_beta - 1 from tau_lo = z_max - 1 (convex and
+//     decreasing: monotone from the left, exact in one step for one active token);
+//  3. support by R9: z > tau_N + band -> in, z < tau_N - band -> out, else F(z_j) < 1;
+//  4. tau from the support: beta = 1: (S1 - 1)/k; beta = 2: m - sqrt((1 - ss)/k);
+//     otherwise one Newton polish on sum_S (z - tau)^beta = 1;
+//  5. p_j = (z_j - tau)^beta; out = sum p_j v_j / sum p_j (R12), V rows gathered for
+//     support tokens only (warp per token, lane = 4 dims).
+// Softmax rows (a6): p = exp(s - s_max) over every valid token (dense V).
+// Overflow (more candidates than fit in shared memory): Newton streamed over the
+// global candidate list / score row brings tau_lo just below tau, then re-extract.
 constexpr int kTauNT = 256;
-constexpr int kCap = 6144;
+constexpr int kCap = 6144;          // shared-memory candidate capacity
+constexpr int kCapG = 16384;        // global candidate capacity per row
 
 struct TauArgs {
-    const float *scores; size_t ntok_stride;
-    const int32_t *union_pages; const int32_t *union_len; int ucap; int full;
+    const float *scores; size_t ntok;
+    const uint32_t *rowmax; const int *ccount; const float *cand_s; const int32_t *cand_j; int capG;
+    const int32_t *page_idx; const int32_t *n_sel; int sel_stride; int full;
     int Hq, G; float alpha; int transform;
     float *out; double *tau_out; int32_t *supp_out;
-    // optional statistics
-    const float *box; const int32_t *page_idx; const int32_t *n_sel; int sel_stride;
-    double *delta_bar;
-    // eval: membership of each token in C_tok of the sparse selection (for full pass)
-    int32_t *tok_list; double *p_list; int32_t *n_list; int list_cap;
+    const float *box; double *delta_bar;                          // certificate (R16)
+    int32_t *tok_list; double *p_list; int32_t *n_list; int list_cap;   // eval list
 };
-
-__device__ __forceinline__ double zsafe_sub(double z, double t) { return z - t; }
 
 template <typename T>
 __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
     constexpr int NT = kTauNT;
     extern __shared__ __align__(16) unsigned char smem[];
-    float *cs = reinterpret_cast<float *>(smem);                 // candidate scores [kCap]
-    int *cj = reinterpret_cast<int *>(smem + sizeof(float) * kCap);   // candidate slots [kCap]
-    uint8_t *cin = reinterpret_cast<uint8_t *>(smem + (sizeof(float) + sizeof(int)) * kCap);
+    unsigned long long *ck = reinterpret_cast<unsigned long long *>(smem);   // [8192] (j << 32 | s bits)
+    uint8_t *cin = reinterpret_cast<uint8_t *>(smem + sizeof(unsigned long long) * 8192);   // [kCap]
+    uint32_t *selbits = reinterpret_cast<uint32_t *>(smem);   // reused after PV: [maxp/32]
     __shared__ double shd[2 * (NT / 32) + 2];
-    __shared__ float shf[NT / 32 + 1];
     __shared__ int shi[NT / 32 + 1];
     __shared__ float red[NT / 32][kD];
 
     const int row = blockIdx.x;
     const int b = row / A.Hq, h = row % A.Hq, kvh = h / A.G;
-    const int unit = b * c.Hkv + kvh;
     const int L = c.seq_lens[b];
-    const int ulen = A.full ? n_pages_of(L) : A.union_len[unit];
-    const int n = ulen * kP;
-    const float *s = A.scores + (size_t)row * A.ntok_stride;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-
-    float smax = -INFINITY;
-    for (int j = threadIdx.x; j < n; j += NT) smax = fmaxf(smax, s[j]);
-    smax = block_max_f<NT>(smax, shf);
-    if (smax == -INFINITY) {   // empty C_tok
+    const uint32_t mk = A.rowmax[row];
+    auto empty_out = [&]() {
         if (threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = 0.0f;
         if (threadIdx.x == 0) {
             if (A.tau_out) A.tau_out[row] = NAN;
             if (A.supp_out) A.supp_out[row] = 0;
+            if (A.n_list) A.n_list[row] = 0;
+            if (A.delta_bar) A.delta_bar[row] = NAN;
         }
-        return;
-    }
-    auto v_row = [&](int j) -> const T * {
-        const int u = j / kP, t = j % kP;
-        const int page = A.full ? u : A.union_pages[(size_t)unit * A.ucap + u];
-        const int phys = c.page_table[(size_t)b * c.maxp + page];
-        return reinterpret_cast<const T *>(c.V) + (((size_t)phys * c.Hkv + kvh) * kP + t) * kD;
     };
+    if (mk == 0u) { empty_out(); return; }
+    const float smax = key2f(mk);
+    auto v_row = [&](int j) -> const T * {
+        const int phys = c.page_table[(size_t)b * c.maxp + j / kP];
+        return reinterpret_cast<const T *>(c.V) + (((size_t)phys * c.Hkv + kvh) * kP + (j % kP)) * kD;
+    };
+    auto load_v4 = [&](const T *vr, float (&vx)[4]) {
+        if constexpr (sizeof(T) == 2) {
+            const uint2 w = *reinterpret_cast<const uint2 *>(vr);
+            vx[0] = bf_lo(w.x); vx[1] = bf_hi(w.x); vx[2] = bf_lo(w.y); vx[3] = bf_hi(w.y);
+        } else {
+            const float4 w = *reinterpret_cast<const float4 *>(vr);
+            vx[0] = w.x; vx[1] = w.y; vx[2] = w.z; vx[3] = w.w;
+        }
+    };
+    const int ncand_all = A.ccount[row];
+    const float *gs = A.cand_s + (size_t)row * A.capG;
+    const int32_t *gj = A.cand_j + (size_t)row * A.capG;
 
     if (A.transform == 1) {
-        // ---------------- softmax over C_tok (dense V)
+        // ---------------- softmax over C_tok: every valid token of the page list (dense V)
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         double zs = 0.0;
-        for (int j = warp; j < n; j += NT / 32) {
-            const float sj = s[j];
-            if (sj == -INFINITY) continue;
-            const float p = expf(sj - smax);
-            if (lane == 0) zs += (double)p;
-            const T *vr = v_row(j) + 4 * lane;
+        int cnt = 0;
+        const int nlist = A.full ? n_pages_of(L) : A.n_sel[row];
+        const float *srow = A.scores + (size_t)row * A.ntok;
+        for (int e = warp; e < nlist * kP; e += NT / 32) {
+            const int pg = A.full ? e / kP : A.page_idx[(size_t)row * A.sel_stride + e / kP];
+            const int j = pg * kP + e % kP;
+            if (j >= L) continue;
+            const float p = expf(srow[j] - smax);
+            if (lane == 0) { zs += (double)p; ++cnt; }
+            float vx[4];
+            load_v4(v_row(j) + 4 * lane, vx);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) acc[e] = __fmaf_rn(p, Elem<T>::to_f(vr[e]), acc[e]);
+            for (int e2 = 0; e2 < 4; ++e2) acc[e2] = __fmaf_rn(p, vx[e2], acc[e2]);
         }
 #pragma unroll
         for (int e = 0; e < 4; ++e) red[warp][4 * lane + e] = acc[e];
-        double zt = block_sum_d<NT>(zs, shd);
-        int cnt = 0;
-        for (int j = threadIdx.x; j < n; j += NT) cnt += (s[j] != -INFINITY);
+        const double zt = block_sum_d<NT>(zs, shd);
         cnt = block_sum_i<NT>(cnt, shi);
         if (threadIdx.x < kD) {
             float o = 0.f;
@@ -206,53 +311,33 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
     const int ib = (fabs(beta - rint(beta)) < 1e-12 && beta <= 4.5) ? (int)rint(beta) : 0;
     const double zmax = a * (double)smax;
     double tau_lo = zmax - 1.0 - 1e-12 * fmax(1.0, fabs(zmax));
-    int ncand = 0;
+    auto zof = [&](int k) -> double { return a * (double)__uint_as_float((uint32_t)(ck[k] & 0xffffffffu)); };
 
-    auto newton = [&](int nc, double tau0) -> double {
-        double tau = tau0;
-        for (int it = 0; it < 200; ++it) {
-            double F = 0.0, Fd = 0.0;
-            for (int k = threadIdx.x; k < nc; k += NT) {
-                const double d = a * (double)cs[k] - tau;
-                if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
-            }
-            block_sum2_d<NT>(F, Fd, shd);
-            if (!(Fd > 0.0)) break;
-            double root = (ib == 1) ? F : (ib == 2) ? sqrt(F) : (ib == 4) ? sqrt(sqrt(F)) : pow(F, 1.0 / beta);
-            // step = (F^{1/b} - 1) / (F^{1/b - 1} * Fd)
-            const double step = (root - 1.0) * F / (root * Fd);
-            const double nt = tau + step;
-            if (!(fabs(step) > 2e-16 * fmax(1.0, fabs(tau)))) { tau = nt; break; }
-            tau = nt;
-        }
-        return tau;
-    };
-
-    auto compact = [&](double tlo) -> int {
-        int base = 0;
-        for (int r0 = 0; r0 < n; r0 += NT) {
-            const int j = r0 + threadIdx.x;
-            const int keep = (j < n && s[j] != -INFINITY && a * (double)s[j] > tlo) ? 1 : 0;
-            int tot;
-            const int pos = block_excl_scan<NT>(keep, shi, &tot);
-            if (keep && base + pos < kCap) { cs[base + pos] = s[j]; cj[base + pos] = j; }
-            base += tot;
-        }
-        __syncthreads();
-        return base;
-    };
-    ncand = compact(tau_lo);
-    if (ncand > kCap) {
-        // overflow: Newton streamed over the whole row (global/L2) to approach tau from
-        // below, then re-compact just below it.
+    // candidate source: the global list (or, on overflow, a re-extraction) -> shared, sorted by j
+    int ncand = ncand_all;
+    if (ncand_all > kCap) {
+        // streamed Newton over the global candidates (or the whole row if the global list overflowed)
+        const bool use_list = ncand_all <= A.capG;
+        const int nlist = A.full ? n_pages_of(L) : A.n_sel[row];
+        const float *srow = A.scores + (size_t)row * A.ntok;
         double tau = tau_lo;
         for (int it = 0; it < 200; ++it) {
             double F = 0.0, Fd = 0.0;
-            for (int j = threadIdx.x; j < n; j += NT) {
-                const float sj = s[j];
-                if (sj == -INFINITY) continue;
-                const double d = a * (double)sj - tau;
-                if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
+            if (use_list) {
+                for (int k = threadIdx.x; k < ncand_all; k += NT) {
+                    const double d = a * (double)gs[k] - tau;
+                    if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
+                }
+            } else {
+                for (int e = threadIdx.x; e < nlist * kP; e += NT) {
+                    const int pg = A.full ? e / kP : A.page_idx[(size_t)row * A.sel_stride + e / kP];
+                    const int j = pg * kP + e % kP;
+                    if (j >= L) continue;
+                    const float sj = srow[j];
+                    if (sj == -INFINITY) continue;
+                    const double d = a * (double)sj - tau;
+                    if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
+                }
             }
             block_sum2_d<NT>(F, Fd, shd);
             if (!(Fd > 0.0)) break;
@@ -262,7 +347,29 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
             if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(tau)))) break;
         }
         tau_lo = fmax(tau_lo, tau - 1e-7 * fmax(1.0, fabs(tau)));
-        ncand = compact(tau_lo);
+        // ordered re-extraction of {z > tau_lo} (deterministic block scans)
+        int base = 0;
+        const int total_e = use_list ? ncand_all : nlist * kP;
+        for (int r0 = 0; r0 < total_e; r0 += NT) {
+            const int e = r0 + threadIdx.x;
+            float sj = -INFINITY;
+            int j = 0;
+            if (e < total_e) {
+                if (use_list) { sj = gs[e]; j = gj[e]; }
+                else {
+                    const int pg = A.full ? e / kP : A.page_idx[(size_t)row * A.sel_stride + e / kP];
+                    j = pg * kP + e % kP;
+                    if (j < L) sj = srow[j];
+                }
+            }
+            const int keep = (sj != -INFINITY && a * (double)sj > tau_lo) ? 1 : 0;
+            int tot;
+            const int pos = block_excl_scan<NT>(keep, shi, &tot);
+            if (keep && base + pos < kCap) ck[base + pos] = ((unsigned long long)j << 32) | __float_as_uint(sj);
+            base += tot;
+        }
+        __syncthreads();
+        ncand = base;
         if (ncand > kCap) {          // support larger than the shared-memory capacity
             if (threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = NAN;
             if (threadIdx.x == 0) {
@@ -271,28 +378,53 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
             }
             return;
         }
+    } else {
+        for (int k = threadIdx.x; k < ncand; k += NT)
+            ck[k] = ((unsigned long long)(uint32_t)gj[k] << 32) | __float_as_uint(gs[k]);
+        __syncthreads();
     }
-    const double tauN = newton(ncand, tau_lo);
+    {
+        const int n2 = next_pow2(max(ncand, 1));
+        for (int k = ncand + threadIdx.x; k < n2; k += NT) ck[k] = ~0ull;
+        __syncthreads();
+        bitonic_sort_u64<NT>(ck, n2);
+    }
+
+    // ---- Newton on the candidates
+    double tauN = tau_lo;
+    for (int it = 0; it < 200; ++it) {
+        double F = 0.0, Fd = 0.0;
+        for (int k = threadIdx.x; k < ncand; k += NT) {
+            const double d = zof(k) - tauN;
+            if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
+        }
+        block_sum2_d<NT>(F, Fd, shd);
+        if (!(Fd > 0.0)) break;
+        const double root = (ib == 1) ? F : (ib == 2) ? sqrt(F) : (ib == 4) ? sqrt(sqrt(F)) : pow(F, 1.0 / beta);
+        const double step = (root - 1.0) * F / (root * Fd);
+        tauN += step;
+        if (!(fabs(step) > 2e-16 * fmax(1.0, fabs(tauN)))) break;
+    }
     // ---- support (R9)
     const double band = 1e-9 * fmax(1.0, fabs(tauN));
     int amb = 0;
     for (int k = threadIdx.x; k < ncand; k += NT) {
-        const double z = a * (double)cs[k];
-        uint8_t f = (z > tauN + band) ? 1 : (z < tauN - band) ? 0 : 2;
+        const double z = zof(k);
+        const uint8_t f = (z > tauN + band) ? 1 : (z < tauN - band) ? 0 : 2;
         cin[k] = f;
         amb += (f == 2);
     }
     amb = block_sum_i<NT>(amb, shi);
     if (amb > 0) {
         for (int k0 = 0; k0 < ncand; ++k0) {
-            if (cin[k0] != 2) continue;           // uniform: cin is shared memory
-            const double zk = a * (double)cs[k0];
-            double F = 0.0, dummy = 0.0;
+            if (cin[k0] != 2) continue;
+            const double zk = zof(k0);
+            double F = 0.0, dz = 0.0;
             for (int k = threadIdx.x; k < ncand; k += NT) {
-                const double d = a * (double)cs[k] - zk;
+                const double d = zof(k) - zk;
                 if (d > 0.0) F += powb(d, beta, ib);
             }
-            block_sum2_d<NT>(F, dummy, shd);
+            block_sum2_d<NT>(F, dz, shd);
             if (threadIdx.x == 0) cin[k0] = (F < 1.0) ? 1 : 0;
             __syncthreads();
         }
@@ -300,7 +432,7 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
     // ---- tau from the support
     double S1 = 0.0, kk = 0.0;
     for (int k = threadIdx.x; k < ncand; k += NT)
-        if (cin[k]) { S1 += a * (double)cs[k]; kk += 1.0; }
+        if (cin[k]) { S1 += zof(k); kk += 1.0; }
     block_sum2_d<NT>(S1, kk, shd);
     double tau;
     if (ib == 1) {
@@ -309,13 +441,13 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
         const double m = S1 / kk;
         double ss = 0.0, dz = 0.0;
         for (int k = threadIdx.x; k < ncand; k += NT)
-            if (cin[k]) { const double d = a * (double)cs[k] - m; ss += d * d; }
+            if (cin[k]) { const double d = zof(k) - m; ss += d * d; }
         block_sum2_d<NT>(ss, dz, shd);
         tau = m - sqrt(fmax(0.0, 1.0 - ss) / kk);
     } else {
         double F = 0.0, Fd = 0.0;
         for (int k = threadIdx.x; k < ncand; k += NT)
-            if (cin[k]) { const double d = a * (double)cs[k] - tauN; F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
+            if (cin[k]) { const double d = zof(k) - tauN; F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
         block_sum2_d<NT>(F, Fd, shd);
         tau = tauN + (F - 1.0) / (beta * Fd);
     }
@@ -324,19 +456,12 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
     double psum = 0.0;
     for (int k = warp; k < ncand; k += NT / 32) {
         if (!cin[k]) continue;
-        const double d = a * (double)cs[k] - tau;
+        const double d = zof(k) - tau;
         const double pd = d > 0.0 ? powb(d, beta, ib) : 0.0;
         if (lane == 0) psum += pd;
         const float p = (float)pd;
-        const T *vr = v_row(cj[k]) + 4 * lane;
         float vx[4];
-        if constexpr (sizeof(T) == 2) {
-            const uint2 w = *reinterpret_cast<const uint2 *>(vr);
-            vx[0] = bf_lo(w.x); vx[1] = bf_hi(w.x); vx[2] = bf_lo(w.y); vx[3] = bf_hi(w.y);
-        } else {
-            const float4 w = *reinterpret_cast<const float4 *>(vr);
-            vx[0] = w.x; vx[1] = w.y; vx[2] = w.z; vx[3] = w.w;
-        }
+        load_v4(v_row((int)(ck[k] >> 32)) + 4 * lane, vx);
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[e] = __fmaf_rn(p, vx[e], acc[e]);
     }
@@ -352,7 +477,7 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
         if (A.tau_out) A.tau_out[row] = tau;
         if (A.supp_out) A.supp_out[row] = (int)kk;
     }
-    // ---- eval list: support tokens (slot index) and p, for exact delta / rho
+    // ---- eval list: support token positions and p (for exact delta / rho)
     if (A.tok_list) {
         int base = 0;
         for (int r0 = 0; r0 < ncand; r0 += NT) {
@@ -361,26 +486,29 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
             int tot;
             const int pos = block_excl_scan<NT>(keep, shi, &tot);
             if (keep && base + pos < A.list_cap) {
-                const double d = a * (double)cs[k] - tau;
-                A.tok_list[(size_t)row * A.list_cap + base + pos] = cj[k];
+                const double d = zof(k) - tau;
+                A.tok_list[(size_t)row * A.list_cap + base + pos] = (int32_t)(ck[k] >> 32);
                 A.p_list[(size_t)row * A.list_cap + base + pos] = d > 0.0 ? powb(d, beta, ib) : 0.0;
             }
             base += tot;
         }
         if (threadIdx.x == 0) A.n_list[row] = base;
     }
-    // ---- certified dropped-mass bound (R16): sum over unselected pages
+    // ---- certified dropped-mass bound (R16): sum over unselected pages, membership by bitmap
     if (A.delta_bar) {
+        __syncthreads();
         const int M = n_pages_of(L);
+        const int Wb = (M + 31) / 32;
+        for (int w = threadIdx.x; w < Wb; w += NT) selbits[w] = 0u;
+        __syncthreads();
         const int32_t *pl = A.page_idx + (size_t)row * A.sel_stride;
         const int ns = A.n_sel[row];
+        for (int i = threadIdx.x; i < ns; i += NT) atomicOr(&selbits[pl[i] >> 5], 1u << (pl[i] & 31));
+        __syncthreads();
         const float *bx = A.box + (size_t)row * c.maxp;
         double db = 0.0, dz = 0.0;
         for (int p = threadIdx.x; p < M; p += NT) {
-            // membership by binary search in the ascending page list
-            int lo = 0, hi = ns;
-            while (lo < hi) { const int mid = (lo + hi) >> 1; if (pl[mid] < p) lo = mid + 1; else hi = mid; }
-            if (lo < ns && pl[lo] == p) continue;
+            if ((selbits[p >> 5] >> (p & 31)) & 1u) continue;
             const double d = a * (double)bx[p] - tau;
             if (d > 0.0) db += (double)min(kP, L - p * kP) * powb(d, beta, ib);
         }
@@ -390,8 +518,8 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
 }
 
 // ============================================================================ eval: exact delta / rho
-// One CTA per (b, q-head): the full pass's support list (token positions j and p_j)
-// against the sparse selection (page list of head h): delta = sum of p_j over tokens
+// One CTA per (b, q-head): the full pass's support list (token positions j, p_j)
+// against the sparse selection (ascending page list of head h): delta = sum of p_j
 // whose page is not selected (Eq. delta), recovered = |S cap C_tok|,
 // full_supp = |S| (Eq. rho).
 __global__ void __launch_bounds__(256) k_eval_metrics(const int32_t *__restrict__ tok_list, const double *__restrict__ p_list,
@@ -408,7 +536,7 @@ __global__ void __launch_bounds__(256) k_eval_metrics(const int32_t *__restrict_
     int rec = 0;
     for (int i = threadIdx.x; i < n; i += 256) {
         const int j = tok_list[(size_t)row * list_cap + i];
-        const int p = j / kP;        // full pass: slot == token position
+        const int p = j / kP;
         int lo = 0, hi = ns;
         while (lo < hi) { const int mid = (lo + hi) >> 1; if (pl[mid] < p) lo = mid + 1; else hi = mid; }
         if (lo < ns && pl[lo] == p) ++rec;

@@ -6,19 +6,31 @@
 namespace ekv {
 
 // ============================================================================ a2: top-k
-// One CTA (NT threads) per (b, q-head) row.  Thread t holds the KPT contiguous keys
-// [t*KPT, t*KPT+KPT) of the row in registers (ordered-int encoding of the fp32 box
-// score, -0 == +0).  The k-th largest key T* is found bit by bit (32 block-wide
-// counting rounds: T |= bit whenever count(key >= T|bit) >= k).  Every key > T* is
-// selected and the (k - count(key > T*)) lowest-index keys equal to T* (R3 tie-break).
-// Indices are written ascending via a block scan over the contiguous per-thread
-// blocks.  P:369-381.
+// One CTA (NT threads) per (b, q-head) row; thread t holds the KPT keys {t + NT*j}
+// (ordered-int encoding of the fp32 box score, -0 == +0), loaded coalesced.
+//  1. Partition bound: L = the k-th largest of the NT per-thread maxima.  At least k
+//     keys are >= L (one per partition whose max is >= L), so the k-th largest key
+//     T* >= L and every selected key is a candidate {key >= L}.
+//  2. Candidates (key desc, index asc) are compacted into shared memory as u64
+//     (~key << 32 | index) and bitonic-sorted; the first k are the selection (R3
+//     tie-break: equal keys -> lower page index first).
+//  3. If the candidates overflow the shared buffer, an exact bit-by-bit search for T*
+//     (32 block-wide counting rounds) is used instead.
+//  4. Selected pages are marked in a shared bitmap and written ascending (block scan).
+// P:369-381.
+constexpr int kTopkCap = 4096;
+
 template <int NT, int KPT>
 __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int Hq, int maxp,
                                              const int32_t *__restrict__ seq_lens, int k,
                                              int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
                                              int sel_stride) {
+    constexpr int MAXP = NT * KPT;
     __shared__ int sh[NT / 32 + 1];
+    __shared__ uint32_t bits[MAXP / 32];
+    __shared__ uint32_t tmax[NT];
+    __shared__ unsigned long long cand[kTopkCap];
+    __shared__ int s_flag;
     const int row = blockIdx.x;
     const int b = row / Hq;
     const int M = n_pages_of(seq_lens[b]);
@@ -31,102 +43,118 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
     }
     const float *x = box + (size_t)row * maxp;
     uint32_t key[KPT];
-    const int i0 = threadIdx.x * KPT;
-#pragma unroll
-    for (int j = 0; j < KPT; ++j) key[j] = (i0 + j < M) ? f2key(x[i0 + j]) : 0u;
-
-    uint32_t T = 0u;
-    for (int bit = 31; bit >= 0; --bit) {
-        const uint32_t Tt = T | (1u << bit);
-        int cnt = 0;
-#pragma unroll
-        for (int j = 0; j < KPT; ++j) cnt += (key[j] >= Tt) ? 1 : 0;
-        const int tot = block_sum_i<NT>(cnt, sh);
-        if (tot >= keff) T = Tt;
-    }
-    // selection flags
-    int ngt = 0;
-#pragma unroll
-    for (int j = 0; j < KPT; ++j) ngt += (key[j] > T) ? 1 : 0;
-    const int n_gt = block_sum_i<NT>(ngt, sh);
-    int neq = 0;
-#pragma unroll
-    for (int j = 0; j < KPT; ++j) neq += (key[j] == T && i0 + j < M) ? 1 : 0;
-    int tot_eq;
-    const int eq_before = block_excl_scan<NT>(neq, sh, &tot_eq);
-    const int need_eq = keff - n_gt;
-    // count selected in my block
-    int nsel = 0, e = eq_before;
+    uint32_t mx = 0u;
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
-        const bool eq = (key[j] == T && i0 + j < M);
-        const bool s = (key[j] > T) || (eq && e < need_eq);
-        if (eq) ++e;
-        nsel += s ? 1 : 0;
+        const int i = threadIdx.x + NT * j;
+        key[j] = (i < M) ? f2key(__ldg(x + i)) : 0u;
+        mx = key[j] > mx ? key[j] : mx;
     }
-    int tot_sel;
-    int pos = block_excl_scan<NT>(nsel, sh, &tot_sel);
-    e = eq_before;
+    for (int w = threadIdx.x; w < MAXP / 32; w += NT) bits[w] = 0u;
+    // 1. partition bound
+    uint32_t Lb = 1u;
+    if (keff <= NT) {
+        tmax[threadIdx.x] = mx;
+        __syncthreads();
+        bitonic_sort_u32_desc<NT>(tmax, NT);
+        Lb = tmax[keff - 1];
+        if (Lb == 0u) Lb = 1u;
+    }
+    // 2. candidates
+    int c = 0;
 #pragma unroll
-    for (int j = 0; j < KPT; ++j) {
-        const bool eq = (key[j] == T && i0 + j < M);
-        const bool s = (key[j] > T) || (eq && e < need_eq);
-        if (eq) ++e;
-        if (s) out[pos++] = i0 + j;
+    for (int j = 0; j < KPT; ++j) c += (key[j] >= Lb) ? 1 : 0;
+    int ctot;
+    int pos = block_excl_scan<NT>(c, sh, &ctot);
+    if (ctot <= kTopkCap) {
+#pragma unroll
+        for (int j = 0; j < KPT; ++j)
+            if (key[j] >= Lb) cand[pos++] = ((unsigned long long)(~key[j]) << 32) | (uint32_t)(threadIdx.x + NT * j);
+        const int n2 = next_pow2(ctot);
+        for (int i = ctot + threadIdx.x; i < n2; i += NT) cand[i] = ~0ull;
+        __syncthreads();
+        bitonic_sort_u64<NT>(cand, n2);
+        for (int i = threadIdx.x; i < keff; i += NT) {
+            const uint32_t p = (uint32_t)(cand[i] & 0xffffffffu);
+            atomicOr(&bits[p >> 5], 1u << (p & 31));
+        }
+    } else {
+        // 3. exact fallback: T* bit by bit, then ties by lowest index
+        uint32_t T = 0u;
+        for (int bit = 31; bit >= 0; --bit) {
+            const uint32_t Tt = T | (1u << bit);
+            int cnt = 0;
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) cnt += (key[j] >= Tt) ? 1 : 0;
+            if (block_sum_i<NT>(cnt, sh) >= keff) T = Tt;
+        }
+        int ngt = 0;
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) ngt += (key[j] > T) ? 1 : 0;
+        const int need_eq = keff - block_sum_i<NT>(ngt, sh);
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            const int i = threadIdx.x + NT * j;
+            if (key[j] > T) atomicOr(&bits[i >> 5], 1u << (i & 31));
+        }
+        // equal keys: lowest indices first (sequential over the index order by warp 0)
+        if (threadIdx.x == 0) s_flag = 0;
+        __syncthreads();
+        for (int base = 0; base < M; base += NT) {
+            const int i = base + threadIdx.x;
+            // key of index i lives in thread i % NT, slot i / NT: re-read from global
+            const int eq = (i < M && f2key(__ldg(x + i)) == T) ? 1 : 0;
+            int tot;
+            const int r = block_excl_scan<NT>(eq, sh, &tot);
+            if (eq && s_flag + r < need_eq) atomicOr(&bits[i >> 5], 1u << (i & 31));
+            __syncthreads();
+            if (threadIdx.x == 0) s_flag += tot;
+            __syncthreads();
+        }
+    }
+    __syncthreads();
+    // 4. ascending output: thread t owns bitmap words [t*WPT, (t+1)*WPT)
+    constexpr int WPT = (MAXP / 32 + NT - 1) / NT;
+    int cnt = 0;
+#pragma unroll
+    for (int w = 0; w < WPT; ++w) {
+        const int wi = threadIdx.x * WPT + w;
+        if (wi < MAXP / 32) cnt += __popc(bits[wi]);
+    }
+    int tot;
+    int o = block_excl_scan<NT>(cnt, sh, &tot);
+#pragma unroll
+    for (int w = 0; w < WPT; ++w) {
+        const int wi = threadIdx.x * WPT + w;
+        if (wi >= MAXP / 32) break;
+        uint32_t v = bits[wi];
+        while (v) {
+            const int bpos = __ffs(v) - 1;
+            v &= v - 1;
+            out[o++] = wi * 32 + bpos;
+        }
     }
     if (threadIdx.x == 0) n_sel[row] = keff;
 }
 
 // ============================================================================ union per KV group
-// One CTA per (b, kv head): a shared-memory byte mask over the M pages (4 pages per
-// 32-bit word, bit g of a page's byte = selected by query head g of the group), then
-// an ordered compaction: union_pages ascending + per-page G-bit head mask (R17).
-template <int NT>
-__global__ void __launch_bounds__(NT) k_union(int Hkv, int G, int maxp, const int32_t *__restrict__ seq_lens,
-                                              const int32_t *__restrict__ page_idx,
+// The union of the G selections of a KV group as a byte mask per page (bit g = selected
+// by query head g of the group; R17): umask[b][kvh][page] bytes packed 4 per u32,
+// zeroed by the host (cudaMemsetAsync) and filled with atomicOr from the page lists.
+__global__ void __launch_bounds__(256) k_mark(int Hq, int G, const int32_t *__restrict__ page_idx,
                                               const int32_t *__restrict__ n_sel, int sel_stride,
-                                              int32_t *__restrict__ union_pages,
-                                              uint8_t *__restrict__ union_mask,
-                                              int32_t *__restrict__ union_len, int ucap) {
-    extern __shared__ uint32_t wmask[];
-    __shared__ int sh[NT / 32 + 1];
-    const int unit = blockIdx.x;
-    const int b = unit / Hkv, kvh = unit % Hkv;
-    const int M = n_pages_of(seq_lens[b]);
-    const int W = (M + 3) / 4;
-    for (int w = threadIdx.x; w < W; w += NT) wmask[w] = 0u;
-    __syncthreads();
-    const int Hq = Hkv * G;
-    for (int g = 0; g < G; ++g) {
-        const int row = b * Hq + kvh * G + g;
-        const int n = n_sel[row];
-        const int32_t *pl = page_idx + (size_t)row * sel_stride;
-        for (int i = threadIdx.x; i < n; i += NT) {
-            const int p = pl[i];
-            atomicOr(&wmask[p >> 2], 1u << ((p & 3) * 8 + g));
-        }
+                                              uint32_t *__restrict__ umask, int W) {
+    const int row = blockIdx.x;
+    const int b = row / Hq, h = row % Hq;
+    const int kvh = h / G, g = h % G;
+    const int Hkv = Hq / G;
+    const int n = n_sel[row];
+    const int32_t *pl = page_idx + (size_t)row * sel_stride;
+    uint32_t *um = umask + ((size_t)b * Hkv + kvh) * W;
+    for (int i = threadIdx.x; i < n; i += 256) {
+        const int p = pl[i];
+        atomicOr(um + (p >> 2), 1u << ((p & 3) * 8 + g));
     }
-    __syncthreads();
-    const int wpt = (W + NT - 1) / NT;
-    const int w0 = threadIdx.x * wpt;
-    int cnt = 0;
-    for (int w = w0; w < min(W, w0 + wpt); ++w) {
-        const uint32_t v = wmask[w];
-        cnt += ((v & 0xffu) != 0) + ((v & 0xff00u) != 0) + ((v & 0xff0000u) != 0) + ((v & 0xff000000u) != 0);
-    }
-    int tot;
-    int pos = block_excl_scan<NT>(cnt, sh, &tot);
-    int32_t *up = union_pages + (size_t)unit * ucap;
-    uint8_t *um = union_mask + (size_t)unit * ucap;
-    for (int w = w0; w < min(W, w0 + wpt); ++w) {
-        const uint32_t v = wmask[w];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t m = (v >> (8 * j)) & 0xffu;
-            if (m) { up[pos] = 4 * w + j; um[pos] = (uint8_t)m; ++pos; }
-        }
-    }
-    if (threadIdx.x == 0) union_len[unit] = tot;
 }
 
 // ============================================================================ a2': Gaussian selector
