@@ -87,7 +87,8 @@ int sel_cap(const ekv_cache *c, const ekv_select_params *s) {
 // One layout serves decode (incl. eval_exact), select, sparse_attend and full_attend.
 struct Layout {
     size_t box, mu, sigma2, page_idx, n_sel, tau_hat;
-    size_t zero, rowmax, ccount, umask, zero_bytes;   // zeroed per attention pass
+    size_t zero, rowmax, ccount, tickets, umask, zero_bytes;   // zeroed per attention pass
+    size_t db_partial, tau_int;
     size_t scores, cand_s, cand_j, tok_list, p_list, n_list, full_out, total;
     int cap, W, list_cap;
 };
@@ -109,6 +110,7 @@ Layout layout(const ekv_cache *c, int Hq, const ekv_select_params *sel) {
     L.zero = o;
     L.rowmax = take(B * Hq * 4);
     L.ccount = take(B * Hq * 4);
+    L.tickets = take(B * Hq * 4);
     L.umask = take(B * Hkv * (size_t)L.W * 4);
     L.zero_bytes = o - L.zero;
     L.scores = take(B * Hq * maxp * kP * 4);
@@ -118,6 +120,8 @@ Layout layout(const ekv_cache *c, int Hq, const ekv_select_params *sel) {
     L.p_list = take(B * Hq * (size_t)L.list_cap * 8);
     L.n_list = take(B * Hq * 4);
     L.full_out = take(B * Hq * kD * 4);
+    L.db_partial = take(B * Hq * (size_t)((maxp + kDbChunk - 1) / kDbChunk) * 8);
+    L.tau_int = take(B * Hq * 8);
     L.total = o;
     return L;
 }
@@ -129,15 +133,24 @@ template <typename K> void set_smem(K kernel, int bytes) {
 }
 
 // ---------------------------------------------------------------- launch helpers
+template <typename T, int G, int MODES>
+void score_go(const CacheView &v, const T *q, int Hq, float *box, float *mu, float *s2, cudaStream_t st) {
+    constexpr int PPC = ScoreCfg<MODES>::PPC;
+    const int HD = v.Hkv * kD;
+    const int per_page = ((MODES & 1) ? 2 * HD * (int)sizeof(T) : 0) + ((MODES & 2) ? 2 * HD * 4 : 0);
+    const int smem = PPC * per_page;
+    static int init = 0;
+    if (smem > init) { set_smem(k_score<T, G, MODES>, smem); init = smem; }
+    dim3 grid((v.maxp + PPC - 1) / PPC, v.B);
+    k_score<T, G, MODES><<<grid, 256, smem, st>>>(v, q, Hq, box, mu, s2);
+}
 template <typename T, int G>
 ekv_status launch_score_t(const CacheView &v, const void *q, int Hq, int modes, float *box, float *mu, float *s2,
                           cudaStream_t st) {
-    const int ppc = 64;
-    dim3 grid((v.maxp + ppc - 1) / ppc, v.B);
     const T *qq = static_cast<const T *>(q);
-    if (modes == 1) k_score<T, G, 1, 2><<<grid, 256, 0, st>>>(v, qq, Hq, ppc, box, mu, s2);
-    else if (modes == 2) k_score<T, G, 2, 2><<<grid, 256, 0, st>>>(v, qq, Hq, ppc, box, mu, s2);
-    else k_score<T, G, 3, 2><<<grid, 256, 0, st>>>(v, qq, Hq, ppc, box, mu, s2);
+    if (modes == 1) score_go<T, G, 1>(v, qq, Hq, box, mu, s2, st);
+    else if (modes == 2) score_go<T, G, 2>(v, qq, Hq, box, mu, s2, st);
+    else score_go<T, G, 3>(v, qq, Hq, box, mu, s2, st);
     return check_launch("k_score");
 }
 template <typename T>
@@ -151,20 +164,19 @@ ekv_status launch_score(const CacheView &v, const void *q, int Hq, int modes, fl
     }
 }
 
-template <int NT, int KPT>
+template <int NT>
 void topk_go(const float *box, int Hq, int maxp, const int32_t *sl, int k, int32_t *pi, int32_t *ns, int stride,
              int rows, cudaStream_t st) {
-    k_topk<NT, KPT><<<rows, NT, 0, st>>>(box, Hq, maxp, sl, k, pi, ns, stride);
+    const int smem = 8 * kTopkCap + 4 * ((maxp + 31) / 32);
+    static bool init = false;
+    if (!init) { set_smem(k_topk<NT>, 8 * kTopkCap + 4 * (131072 / 32)); init = true; }
+    k_topk<NT><<<rows, NT, smem, st>>>(box, Hq, maxp, sl, k, pi, ns, stride);
 }
 ekv_status launch_topk(const float *box, int B, int Hq, int maxp, const int32_t *sl, int k, int32_t *pi, int32_t *ns,
                        int stride, cudaStream_t st) {
     const int rows = B * Hq;
-    if (maxp <= 256) topk_go<256, 1>(box, Hq, maxp, sl, k, pi, ns, stride, rows, st);
-    else if (maxp <= 1024) topk_go<256, 4>(box, Hq, maxp, sl, k, pi, ns, stride, rows, st);
-    else if (maxp <= 4096) topk_go<512, 8>(box, Hq, maxp, sl, k, pi, ns, stride, rows, st);
-    else if (maxp <= 16384) topk_go<1024, 16>(box, Hq, maxp, sl, k, pi, ns, stride, rows, st);
-    else if (maxp <= 32768) topk_go<1024, 32>(box, Hq, maxp, sl, k, pi, ns, stride, rows, st);
-    else topk_go<1024, 64>(box, Hq, maxp, sl, k, pi, ns, stride, rows, st);
+    if (maxp <= 4096) topk_go<256>(box, Hq, maxp, sl, k, pi, ns, stride, rows, st);
+    else topk_go<1024>(box, Hq, maxp, sl, k, pi, ns, stride, rows, st);
     return check_launch("k_topk");
 }
 
@@ -180,7 +192,7 @@ ekv_status launch_scores_t(const CacheView &v, const void *q, int Hq, const uint
     constexpr int smem = 2 * 8 * kP * kD * (int)sizeof(T);
     static bool init = false;
     if (!init) { set_smem(k_attend_scores<T, G>, smem); init = true; }
-    dim3 grid((v.maxp + 127) / 128, v.B * v.Hkv);
+    dim3 grid((v.maxp + 511) / 512, v.B * v.Hkv);
     k_attend_scores<T, G><<<grid, 256, smem, st>>>(v, static_cast<const T *>(q), Hq, um, W, scores, rowmax, full);
     return check_launch("k_attend_scores");
 }
@@ -429,13 +441,20 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
                                                                       L.cap, th);
         EKV_TRY(check_launch("k_gauss_select"));
     }
-    // a3 (+a4 certificate)
-    TauArgs extra;
-    memset(&extra, 0, sizeof(extra));
-    if (want_db) { extra.box = box; extra.delta_bar = stats->delta_bar; }
-    EKV_TRY(attend_impl(cache, q, n_q_heads, pi, ns, L.cap, 0, attn, out, stats ? stats->tau : nullptr,
-                        stats ? stats->supp_count : nullptr, workspace, L, st, &extra));
+    // a3
+    double *tau_p = (stats && stats->tau) ? stats->tau : at<double>(workspace, L.tau_int);
+    EKV_TRY(attend_impl(cache, q, n_q_heads, pi, ns, L.cap, 0, attn, out, tau_p,
+                        stats ? stats->supp_count : nullptr, workspace, L, st, nullptr));
     const int rows = cache->batch * n_q_heads;
+    // a4: certified dropped-mass bound
+    if (want_db) {
+        const int nch = (maxp + kDbChunk - 1) / kDbChunk;
+        dim3 g(nch, rows);
+        k_delta_bar<<<g, 256, 0, st>>>(box, maxp, cache->seq_lens, n_q_heads, pi, ns, L.cap, tau_p, attn->alpha,
+                                       at<double>(workspace, L.db_partial), nch,
+                                       at<unsigned int>(workspace, L.tickets), stats->delta_bar);
+        EKV_TRY(check_launch("k_delta_bar"));
+    }
     if (stats) {
         if (stats->n_sel) {
             if (cudaMemcpyAsync(stats->n_sel, ns, rows * sizeof(int32_t), cudaMemcpyDeviceToDevice, st) != cudaSuccess)

@@ -28,13 +28,14 @@ __global__ void __launch_bounds__(256) k_attend_scores(CacheView c, const T *__r
                                                        const uint32_t *__restrict__ umask, int W,
                                                        float *__restrict__ scores, uint32_t *__restrict__ rowmax,
                                                        int full) {
-    constexpr int CH = 128;                 // pages per CTA
+    constexpr int CH = 512;                 // pages per CTA
     constexpr int BP = 8;                   // pages per batch (stage)
     constexpr int TILE = kP * kD * (int)sizeof(T);
     extern __shared__ __align__(128) unsigned char smem[];   // [2][BP][TILE]
     __shared__ uint64_t bars[2];
     __shared__ int s_pages[CH];
     __shared__ uint8_t s_mask[CH];
+    __shared__ int s_cnt;
     __shared__ int sh[9];
     __shared__ uint32_t s_max[16][G];
     const int unit = blockIdx.y;
@@ -44,17 +45,23 @@ __global__ void __launch_bounds__(256) k_attend_scores(CacheView c, const T *__r
     const int p0 = blockIdx.x * CH;
     if (p0 >= M) return;
     const int tid = threadIdx.x;
-    // compact the selected pages of [p0, p0 + CH)
+    // compact the selected pages of [p0, p0 + CH) in ascending order (2 pages per thread)
     {
-        const int p = p0 + (tid & (CH - 1));
-        uint8_t m = 0;
-        if (tid < CH && p < M) {
-            m = full ? (uint8_t)((1u << G) - 1u)
-                     : (uint8_t)((umask[((size_t)b * c.Hkv + kvh) * W + (p >> 2)] >> ((p & 3) * 8)) & 0xffu);
+        uint8_t m[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int p = p0 + 2 * tid + r;
+            m[r] = 0;
+            if (p < M) {
+                m[r] = full ? (uint8_t)((1u << G) - 1u)
+                            : (uint8_t)((umask[((size_t)b * c.Hkv + kvh) * W + (p >> 2)] >> ((p & 3) * 8)) & 0xffu);
+            }
         }
         int tot;
-        const int pos = block_excl_scan<256>(m ? 1 : 0, sh, &tot);
-        if (m) { s_pages[pos] = p; s_mask[pos] = m; }
+        int pos = block_excl_scan<256>((m[0] != 0) + (m[1] != 0), sh, &tot);
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+            if (m[r]) { s_pages[pos] = p0 + 2 * tid + r; s_mask[pos] = m[r]; ++pos; }
         if (tid == 0) sh[8] = tot;
     }
     if (tid == 0) {
@@ -223,7 +230,6 @@ struct TauArgs {
     const int32_t *page_idx; const int32_t *n_sel; int sel_stride; int full;
     int Hq, G; float alpha; int transform;
     float *out; double *tau_out; int32_t *supp_out;
-    const float *box; double *delta_bar;                          // certificate (R16)
     int32_t *tok_list; double *p_list; int32_t *n_list; int list_cap;   // eval list
 };
 
@@ -233,7 +239,6 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long *ck = reinterpret_cast<unsigned long long *>(smem);   // [8192] (j << 32 | s bits)
     uint8_t *cin = reinterpret_cast<uint8_t *>(smem + sizeof(unsigned long long) * 8192);   // [kCap]
-    uint32_t *selbits = reinterpret_cast<uint32_t *>(smem);   // reused after PV: [maxp/32]
     __shared__ double shd[2 * (NT / 32) + 2];
     __shared__ int shi[NT / 32 + 1];
     __shared__ float red[NT / 32][kD];
@@ -249,7 +254,6 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
             if (A.tau_out) A.tau_out[row] = NAN;
             if (A.supp_out) A.supp_out[row] = 0;
             if (A.n_list) A.n_list[row] = 0;
-            if (A.delta_bar) A.delta_bar[row] = NAN;
         }
     };
     if (mk == 0u) { empty_out(); return; }
@@ -494,26 +498,66 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
         }
         if (threadIdx.x == 0) A.n_list[row] = base;
     }
-    // ---- certified dropped-mass bound (R16): sum over unselected pages, membership by bitmap
-    if (A.delta_bar) {
-        __syncthreads();
-        const int M = n_pages_of(L);
-        const int Wb = (M + 31) / 32;
-        for (int w = threadIdx.x; w < Wb; w += NT) selbits[w] = 0u;
-        __syncthreads();
-        const int32_t *pl = A.page_idx + (size_t)row * A.sel_stride;
-        const int ns = A.n_sel[row];
-        for (int i = threadIdx.x; i < ns; i += NT) atomicOr(&selbits[pl[i] >> 5], 1u << (pl[i] & 31));
-        __syncthreads();
-        const float *bx = A.box + (size_t)row * c.maxp;
-        double db = 0.0, dz = 0.0;
-        for (int p = threadIdx.x; p < M; p += NT) {
-            if ((selbits[p >> 5] >> (p & 31)) & 1u) continue;
-            const double d = a * (double)bx[p] - tau;
+}
+
+// ============================================================================ a4: certified delta_bar
+// delta_bar = sum_{p not in C_page} c_p [a * box_p - tau~]_+^beta  (R16; Prop. B.1 gives
+// z_j <= a * box_p, and tau >= tau~).  Grid (chunk of 2048 pages, b * Hq + h): each CTA
+// marks its row's selected pages of the chunk in a shared bitmap, sums its chunk
+// (deterministic block tree) into partial[row][chunk]; the last CTA of a row (ticket
+// counter) adds the partials in chunk order, so the result is deterministic.
+constexpr int kDbChunk = 2048;
+__global__ void __launch_bounds__(256) k_delta_bar(const float *__restrict__ box, int maxp,
+                                                   const int32_t *__restrict__ seq_lens, int Hq,
+                                                   const int32_t *__restrict__ page_idx,
+                                                   const int32_t *__restrict__ n_sel, int sel_stride,
+                                                   const double *__restrict__ tau, float alpha,
+                                                   double *__restrict__ partial, int nchunks,
+                                                   unsigned int *__restrict__ tickets, double *__restrict__ out) {
+    __shared__ uint32_t bits[kDbChunk / 32];
+    __shared__ double shd[18];
+    __shared__ bool s_last;
+    const int row = blockIdx.y, b = row / Hq;
+    const int L = seq_lens[b];
+    const int M = n_pages_of(L);
+    const int p0 = blockIdx.x * kDbChunk;
+    const double t = tau[row];
+    const double a = (double)alpha - 1.0, beta = 1.0 / a;
+    const int ib = (fabs(beta - rint(beta)) < 1e-12 && beta <= 4.5) ? (int)rint(beta) : 0;
+    for (int w = threadIdx.x; w < kDbChunk / 32; w += 256) bits[w] = 0u;
+    __syncthreads();
+    const int32_t *pl = page_idx + (size_t)row * sel_stride;
+    const int ns = n_sel[row];
+    for (int i = threadIdx.x; i < ns; i += 256) {
+        const int p = pl[i] - p0;
+        if (p >= 0 && p < kDbChunk) atomicOr(&bits[p >> 5], 1u << (p & 31));
+    }
+    __syncthreads();
+    double db = 0.0, dz = 0.0;
+    const float *bx = box + (size_t)row * maxp;
+    if (t == t) {   // tau is NaN for an empty row
+#pragma unroll 4
+        for (int i = threadIdx.x; i < kDbChunk; i += 256) {
+            const int p = p0 + i;
+            if (p >= M || ((bits[i >> 5] >> (i & 31)) & 1u)) continue;
+            const double d = a * (double)__ldg(bx + p) - t;
             if (d > 0.0) db += (double)min(kP, L - p * kP) * powb(d, beta, ib);
         }
-        block_sum2_d<NT>(db, dz, shd);
-        if (threadIdx.x == 0) A.delta_bar[row] = db;
+    }
+    block_sum2_d<256>(db, dz, shd);
+    if (threadIdx.x == 0) {
+        partial[(size_t)row * nchunks + blockIdx.x] = db;
+        __threadfence();
+        const unsigned int tk = atomicAdd(tickets + row, 1u);
+        s_last = (tk == (unsigned)nchunks - 1);
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        __threadfence();
+        double s = 0.0;
+        for (int c2 = 0; c2 < nchunks; ++c2) s += ((volatile double *)partial)[(size_t)row * nchunks + c2];
+        out[row] = (t == t) ? s : NAN;
+        tickets[row] = 0u;                 // ready for the next call
     }
 }
 

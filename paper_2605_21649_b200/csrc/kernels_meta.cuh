@@ -94,105 +94,135 @@ __global__ void __launch_bounds__(256) k_rebuild(CacheView c) {
 }
 
 // ============================================================================ a1: score_pages
-// CTA = (chunk of PPC pages) x (sequence b), 256 threads = 16 half-warps.  Half-warp
-// hw serves kv head hw / (16/Hkv) and pages p0 + sub, p0 + sub + 16/Hkv, ...; lane c
-// of the half-warp owns dims [8c, 8c+8) and keeps q for the G query heads of its kv
-// group in registers.  kmin/kmax (and kavg/kvar) rows are read straight from HBM as
-// 16-byte loads (each half-warp reads one contiguous 256/512-byte row: coalesced);
-// the per-lane fma chains and the 16-lane reduce-scatter tree realise dot16x8 (R1).
-// Box: max(q_i kmin_i, q_i kmax_i) = q_i kext_i is evaluated as two fmas with
-// qneg = (q_i >= 0 ? 0 : q_i) and qpos = (q_i >= 0 ? q_i : 0); one of the two adds an
-// exact zero, so the chain equals the canonical fma(q_i, kext_i, acc).
-template <typename T, int G, int MODES, int UNR>
-__global__ void __launch_bounds__(256) k_score(CacheView c, const T *__restrict__ q, int Hq, int ppc,
+// CTA = (chunk of PPC pages) x (sequence b), 256 threads = 16 half-warps.
+//  - Thread 0 issues cp.async.bulk (TMA, 1-D) copies of each page's metadata blocks
+//    (kmin and kmax: Hkv*d elements each, contiguous in HBM; kavg/kvar for the
+//    Gaussian mode) into shared memory, one mbarrier per page, so the whole chunk is
+//    in flight at once and no registers hold loads.
+//  - Half-warp hw serves kv head hw / (16/Hkv) and pages sub, sub + 16/Hkv, ... of the
+//    chunk; lane c owns dims [8c, 8c+8) and keeps q for the G query heads of the group
+//    in registers (box: qpos/qneg per dim; Gaussian: q and q*q).  Reading one 256-byte
+//    metadata row per half-warp from shared memory is conflict-free.
+//  - dot16x8 (R1): per-lane fma chains (packed FFMA2 over head pairs, bit-identical to
+//    scalar fmas) + the 16-lane reduce-scatter tree.  Box: max(q_i kmin_i, q_i kmax_i)
+//    = q_i kext_i as two fmas with qneg = (q_i >= 0 ? 0 : q_i), qpos = (q_i >= 0 ? q_i
+//    : 0): one of the two adds an exact zero, so the chain equals fma(q_i, kext_i, acc).
+template <int MODES> struct ScoreCfg {
+    static constexpr int PPC = (MODES == 1) ? 16 : 8;
+};
+
+template <typename T, int G, int MODES>
+__global__ void __launch_bounds__(256) k_score(CacheView c, const T *__restrict__ q, int Hq,
                                                 float *__restrict__ box, float *__restrict__ mu,
                                                 float *__restrict__ sigma2) {
+    constexpr int PPC = ScoreCfg<MODES>::PPC;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bars[PPC];
     const int b = blockIdx.y;
     const int L = c.seq_lens[b];
     const int M = n_pages_of(L);
-    const int p0 = blockIdx.x * ppc;
+    const int p0 = blockIdx.x * PPC;
     if (p0 >= M) return;
+    const int np = min(PPC, M - p0);
+    const int HD = c.Hkv * kD;
+    const uint32_t bmm = (uint32_t)(HD * sizeof(T));          // kmin / kmax block bytes
+    const uint32_t bgs = (uint32_t)(HD * sizeof(float));      // kavg / kvar block bytes
+    const uint32_t per_page = ((MODES & 1) ? 2 * bmm : 0) + ((MODES & 2) ? 2 * bgs : 0);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < np; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+        for (int i = 0; i < np; ++i) {
+            const size_t phys = (size_t)__ldg(c.page_table + (size_t)b * c.maxp + p0 + i);
+            unsigned char *dst = smem + (size_t)i * per_page;
+            mbar_expect_tx(&bars[i], per_page);
+            if (MODES & 1) {
+                bulk_g2s(dst, reinterpret_cast<const T *>(c.kmin) + phys * HD, bmm, &bars[i]);
+                bulk_g2s(dst + bmm, reinterpret_cast<const T *>(c.kmax) + phys * HD, bmm, &bars[i]);
+                dst += 2 * bmm;
+            }
+            if (MODES & 2) {
+                bulk_g2s(dst, c.kavg + phys * HD, bgs, &bars[i]);
+                bulk_g2s(dst + bgs, c.kvar + phys * HD, bgs, &bars[i]);
+            }
+        }
+    }
     const int lane = threadIdx.x & 31;
     const int l16 = threadIdx.x & 15;
     const int hw = threadIdx.x >> 4;
     const int hwpk = 16 / c.Hkv;
     const int kvh = hw / hwpk, sub = hw % hwpk;
     const int hq0 = kvh * G;
-
-    float qp[G][8], qn[G][8], qa[G][8], q2[G][8];
+    constexpr int GP = (G + 1) / 2;          // head pairs
+    float2 qp[GP][8], qn[GP][8], qa[GP][8], q2[GP][8];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-        float x[8];
-        Elem<T>::load8(q + ((size_t)b * Hq + hq0 + g) * kD + 8 * l16, x);
+    for (int g = 0; g < GP; ++g) {
+        float x0[8], x1[8];
+        Elem<T>::load8(q + ((size_t)b * Hq + hq0 + 2 * g) * kD + 8 * l16, x0);
+        if (2 * g + 1 < G) Elem<T>::load8(q + ((size_t)b * Hq + hq0 + 2 * g + 1) * kD + 8 * l16, x1);
+        else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x1[i] = 0.0f;
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const bool nn = x[i] >= 0.0f;
-            qp[g][i] = nn ? x[i] : 0.0f;
-            qn[g][i] = nn ? 0.0f : x[i];
-            qa[g][i] = x[i];
-            q2[g][i] = __fmul_rn(x[i], x[i]);
+            qp[g][i] = make_float2(x0[i] >= 0.0f ? x0[i] : 0.0f, x1[i] >= 0.0f ? x1[i] : 0.0f);
+            qn[g][i] = make_float2(x0[i] >= 0.0f ? 0.0f : x0[i], x1[i] >= 0.0f ? 0.0f : x1[i]);
+            qa[g][i] = make_float2(x0[i], x1[i]);
+            q2[g][i] = make_float2(__fmul_rn(x0[i], x0[i]), __fmul_rn(x1[i], x1[i]));
         }
     }
-    const int pend = min(p0 + ppc, M);
-    const T *kmin = reinterpret_cast<const T *>(c.kmin);
-    const T *kmax = reinterpret_cast<const T *>(c.kmax);
+    __syncthreads();                         // mbarrier inits visible
     const int h_out = hq0 + rs_head<G>(lane);
     const bool writer = rs_writer<G>(lane);
     // warp-uniform trip count: both half-warps of a warp run the same iterations
-    for (int base = p0; base < pend; base += UNR * hwpk) {
-        float mn[UNR][8], mx[UNR][8], av[UNR][8], vr[UNR][8];
-        int pp[UNR];
+    for (int ib = 0; ib < np; ib += hwpk) {
+        const int i = ib + sub;
+        const bool valid = i < np;
+        const int ii = valid ? i : 0;
+        mbar_wait(&bars[ii], 0);
+        const unsigned char *pg = smem + (size_t)ii * per_page;
+        const int p = p0 + ii;
+        if (MODES & 1) {
+            float mn[8], mx[8];
+            Elem<T>::load8(reinterpret_cast<const T *>(pg) + kvh * kD + 8 * l16, mn);
+            Elem<T>::load8(reinterpret_cast<const T *>(pg + bmm) + kvh * kD + 8 * l16, mx);
+            float acc[G];
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            pp[u] = base + sub + u * hwpk;
-            const int p = min(pp[u], pend - 1);
-            const int page = __ldg(c.page_table + (size_t)b * c.maxp + p);
-            const size_t off = ((size_t)page * c.Hkv + kvh) * kD + 8 * l16;
-            if (MODES & 1) {
-                Elem<T>::load8_nc(kmin + off, mn[u]);
-                Elem<T>::load8_nc(kmax + off, mx[u]);
+            for (int g = 0; g < GP; ++g) {
+                float2 a2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    a2 = ffma2(qn[g][e], mn[e], a2);
+                    a2 = ffma2(qp[g][e], mx[e], a2);
+                }
+                acc[2 * g] = a2.x;
+                if (2 * g + 1 < G) acc[2 * g + 1] = a2.y;
             }
-            if (MODES & 2) {
-                Elem<float>::load8_nc(c.kavg + off, av[u]);
-                Elem<float>::load8_nc(c.kvar + off, vr[u]);
-            }
+            const float r = __fmul_rn(rs_reduce16<G>(acc, lane), kCd);
+            if (writer && valid) box[((size_t)b * Hq + h_out) * c.maxp + p] = r;
         }
+        if (MODES & 2) {
+            const unsigned char *pgs = pg + ((MODES & 1) ? 2 * bmm : 0);
+            float av[8], vr[8];
+            Elem<float>::load8(reinterpret_cast<const float *>(pgs) + kvh * kD + 8 * l16, av);
+            Elem<float>::load8(reinterpret_cast<const float *>(pgs + bgs) + kvh * kD + 8 * l16, vr);
+            float am[G], as[G];
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            const bool valid = pp[u] < pend;
-            if (MODES & 1) {
-                float acc[G];
+            for (int g = 0; g < GP; ++g) {
+                float2 m2 = make_float2(0.0f, 0.0f), s2 = make_float2(0.0f, 0.0f);
 #pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    float a = 0.0f;
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        a = __fmaf_rn(qn[g][i], mn[u][i], a);
-                        a = __fmaf_rn(qp[g][i], mx[u][i], a);
-                    }
-                    acc[g] = a;
+                for (int e = 0; e < 8; ++e) {
+                    m2 = ffma2(qa[g][e], av[e], m2);
+                    s2 = ffma2(q2[g][e], vr[e], s2);
                 }
-                const float r = __fmul_rn(rs_reduce16<G>(acc, lane), kCd);
-                if (writer && valid) box[((size_t)b * Hq + h_out) * c.maxp + pp[u]] = r;
+                am[2 * g] = m2.x; as[2 * g] = s2.x;
+                if (2 * g + 1 < G) { am[2 * g + 1] = m2.y; as[2 * g + 1] = s2.y; }
             }
-            if (MODES & 2) {
-                float am[G], as[G];
-#pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    float a = 0.0f, s = 0.0f;
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        a = __fmaf_rn(qa[g][i], av[u][i], a);
-                        s = __fmaf_rn(q2[g][i], vr[u][i], s);
-                    }
-                    am[g] = a; as[g] = s;
-                }
-                const float rm = __fmul_rn(rs_reduce16<G>(am, lane), kCd);
-                const float rs = __fmul_rn(rs_reduce16<G>(as, lane), 1.0f / (float)kD);
-                if (writer && valid) {
-                    mu[((size_t)b * Hq + h_out) * c.maxp + pp[u]] = rm;
-                    sigma2[((size_t)b * Hq + h_out) * c.maxp + pp[u]] = rs;
-                }
+            const float rm = __fmul_rn(rs_reduce16<G>(am, lane), kCd);
+            const float rs = __fmul_rn(rs_reduce16<G>(as, lane), 1.0f / (float)kD);
+            if (writer && valid) {
+                mu[((size_t)b * Hq + h_out) * c.maxp + p] = rm;
+                sigma2[((size_t)b * Hq + h_out) * c.maxp + p] = rs;
             }
         }
     }

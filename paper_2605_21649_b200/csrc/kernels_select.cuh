@@ -6,31 +6,30 @@
 namespace ekv {
 
 // ============================================================================ a2: top-k
-// One CTA (NT threads) per (b, q-head) row; thread t holds the KPT keys {t + NT*j}
-// (ordered-int encoding of the fp32 box score, -0 == +0), loaded coalesced.
-//  1. Partition bound: L = the k-th largest of the NT per-thread maxima.  At least k
-//     keys are >= L (one per partition whose max is >= L), so the k-th largest key
-//     T* >= L and every selected key is a candidate {key >= L}.
-//  2. Candidates (key desc, index asc) are compacted into shared memory as u64
-//     (~key << 32 | index) and bitonic-sorted; the first k are the selection (R3
-//     tie-break: equal keys -> lower page index first).
-//  3. If the candidates overflow the shared buffer, an exact bit-by-bit search for T*
-//     (32 block-wide counting rounds) is used instead.
-//  4. Selected pages are marked in a shared bitmap and written ascending (block scan).
-// P:369-381.
-constexpr int kTopkCap = 4096;
+// One CTA (NT threads) per (b, q-head) row (R3: key desc, then lower page
+// index).  Keys are the ordered-int encodings of the fp32 box scores (-0 == +0).
+//  1. Partition bound: thread t reads the keys {4(t + NT j) .. +3} (float4, coalesced)
+//     and keeps their max m_t.  L = the k-th largest m_t, found MSB-first with
+//     __syncthreads_count.  At least k keys are >= L, so T* (the k-th largest key) >= L.
+//  2. Candidates {key >= L} are compacted into shared memory (warp ballot).
+//  3. T* by an MSB-first search over the candidates; ties at T* are broken by the
+//     smallest page indices (a second MSB-first search over the index).
+//  4. The selection is marked in a shared bitmap and written ascending (block scan).
+// Overflow (more than kTopkCap candidates): the same searches run over all keys read
+// from global memory (L2) -- exact, slower.
+constexpr int kTopkCap = 8192;
 
-template <int NT, int KPT>
+template <int NT>
 __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int Hq, int maxp,
                                              const int32_t *__restrict__ seq_lens, int k,
                                              int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
                                              int sel_stride) {
-    constexpr int MAXP = NT * KPT;
+    extern __shared__ __align__(16) unsigned char tk_smem[];
+    uint32_t *ckey = reinterpret_cast<uint32_t *>(tk_smem);                 // [kTopkCap]
+    int32_t *cidx = reinterpret_cast<int32_t *>(tk_smem + 4 * kTopkCap);    // [kTopkCap]
+    uint32_t *bits = reinterpret_cast<uint32_t *>(tk_smem + 8 * kTopkCap);  // [maxp/32]
     __shared__ int sh[NT / 32 + 1];
-    __shared__ uint32_t bits[MAXP / 32];
-    __shared__ uint32_t tmax[NT];
-    __shared__ unsigned long long cand[kTopkCap];
-    __shared__ int s_flag;
+    __shared__ int s_cnt;
     const int row = blockIdx.x;
     const int b = row / Hq;
     const int M = n_pages_of(seq_lens[b]);
@@ -42,91 +41,103 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
         return;
     }
     const float *x = box + (size_t)row * maxp;
-    uint32_t key[KPT];
-    uint32_t mx = 0u;
-#pragma unroll
-    for (int j = 0; j < KPT; ++j) {
-        const int i = threadIdx.x + NT * j;
-        key[j] = (i < M) ? f2key(__ldg(x + i)) : 0u;
-        mx = key[j] > mx ? key[j] : mx;
-    }
-    for (int w = threadIdx.x; w < MAXP / 32; w += NT) bits[w] = 0u;
-    // 1. partition bound
-    uint32_t Lb = 1u;
-    if (keff <= NT) {
-        tmax[threadIdx.x] = mx;
-        __syncthreads();
-        bitonic_sort_u32_desc<NT>(tmax, NT);
-        Lb = tmax[keff - 1];
-        if (Lb == 0u) Lb = 1u;
-    }
-    // 2. candidates
-    int c = 0;
-#pragma unroll
-    for (int j = 0; j < KPT; ++j) c += (key[j] >= Lb) ? 1 : 0;
-    int ctot;
-    int pos = block_excl_scan<NT>(c, sh, &ctot);
-    if (ctot <= kTopkCap) {
-#pragma unroll
-        for (int j = 0; j < KPT; ++j)
-            if (key[j] >= Lb) cand[pos++] = ((unsigned long long)(~key[j]) << 32) | (uint32_t)(threadIdx.x + NT * j);
-        const int n2 = next_pow2(ctot);
-        for (int i = ctot + threadIdx.x; i < n2; i += NT) cand[i] = ~0ull;
-        __syncthreads();
-        bitonic_sort_u64<NT>(cand, n2);
-        for (int i = threadIdx.x; i < keff; i += NT) {
-            const uint32_t p = (uint32_t)(cand[i] & 0xffffffffu);
-            atomicOr(&bits[p >> 5], 1u << (p & 31));
-        }
-    } else {
-        // 3. exact fallback: T* bit by bit, then ties by lowest index
-        uint32_t T = 0u;
-        for (int bit = 31; bit >= 0; --bit) {
-            const uint32_t Tt = T | (1u << bit);
-            int cnt = 0;
-#pragma unroll
-            for (int j = 0; j < KPT; ++j) cnt += (key[j] >= Tt) ? 1 : 0;
-            if (block_sum_i<NT>(cnt, sh) >= keff) T = Tt;
-        }
-        int ngt = 0;
-#pragma unroll
-        for (int j = 0; j < KPT; ++j) ngt += (key[j] > T) ? 1 : 0;
-        const int need_eq = keff - block_sum_i<NT>(ngt, sh);
-#pragma unroll
-        for (int j = 0; j < KPT; ++j) {
-            const int i = threadIdx.x + NT * j;
-            if (key[j] > T) atomicOr(&bits[i >> 5], 1u << (i & 31));
-        }
-        // equal keys: lowest indices first (sequential over the index order by warp 0)
-        if (threadIdx.x == 0) s_flag = 0;
-        __syncthreads();
-        for (int base = 0; base < M; base += NT) {
-            const int i = base + threadIdx.x;
-            // key of index i lives in thread i % NT, slot i / NT: re-read from global
-            const int eq = (i < M && f2key(__ldg(x + i)) == T) ? 1 : 0;
-            int tot;
-            const int r = block_excl_scan<NT>(eq, sh, &tot);
-            if (eq && s_flag + r < need_eq) atomicOr(&bits[i >> 5], 1u << (i & 31));
-            __syncthreads();
-            if (threadIdx.x == 0) s_flag += tot;
-            __syncthreads();
+    const int W = (M + 31) / 32;
+    for (int w = threadIdx.x; w < W; w += NT) bits[w] = 0u;
+    if (threadIdx.x == 0) s_cnt = 0;
+    auto keyat = [&](int i) -> uint32_t { return i < M ? f2key(__ldg(x + i)) : 0u; };
+    // 1. partition maxima
+    uint32_t mt = 0u;
+    for (int i4 = 4 * threadIdx.x; i4 < M; i4 += 4 * NT) {
+        if (i4 + 3 < M && ((maxp & 3) == 0)) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(x + i4));
+            mt = max(mt, max(max(f2key(v.x), f2key(v.y)), max(f2key(v.z), f2key(v.w))));
+        } else {
+            for (int e = 0; e < 4; ++e) mt = max(mt, keyat(i4 + e));
         }
     }
     __syncthreads();
-    // 4. ascending output: thread t owns bitmap words [t*WPT, (t+1)*WPT)
-    constexpr int WPT = (MAXP / 32 + NT - 1) / NT;
+    uint32_t Lb = 1u;
+    if (keff <= NT) {
+        uint32_t T = 0u;
+        for (int bit = 31; bit >= 0; --bit) {
+            const uint32_t Tt = T | (1u << bit);
+            if (__syncthreads_count(mt >= Tt) >= keff) T = Tt;
+        }
+        Lb = T > 1u ? T : 1u;
+    }
+    // 2. candidates
+    for (int i0 = 0; i0 < M; i0 += NT) {
+        const int i = i0 + threadIdx.x;
+        const uint32_t kk = keyat(i);
+        const bool c = kk >= Lb;
+        const unsigned m = __ballot_sync(0xffffffffu, c);
+        int base = 0;
+        if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(&s_cnt, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (c) {
+            const int pos = base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u));
+            if (pos < kTopkCap) { ckey[pos] = kk; cidx[pos] = i; }
+        }
+    }
+    __syncthreads();
+    const int nc = s_cnt;
+    const bool ovf = nc > kTopkCap;
+    // 3. T* = k-th largest candidate key (or key, on overflow)
+    auto cnt_ge = [&](uint32_t Tt) -> int {
+        int c = 0;
+        if (!ovf) { for (int j = threadIdx.x; j < nc; j += NT) c += ckey[j] >= Tt; }
+        else { for (int i = threadIdx.x; i < M; i += NT) c += keyat(i) >= Tt; }
+        return block_sum_i<NT>(c, sh);
+    };
+    // largest T with #(key >= T) >= k; for T <= L the predicate holds by step 1
+    uint32_t T = 0u;
+    for (int bit = 31; bit >= 0; --bit) {
+        const uint32_t Tt = T | (1u << bit);
+        if (Tt <= Lb || cnt_ge(Tt) >= keff) T = Tt;
+    }
+    // keys > T are in; ties at T: the need smallest indices
+    const int n_gt = (T == 0xffffffffu) ? 0 : cnt_ge(T + 1u);
+    const int need = keff - n_gt;
+    auto cnt_eq_lt = [&](int I) -> int {       // #(key == T && idx < I)
+        int c = 0;
+        if (!ovf) { for (int j = threadIdx.x; j < nc; j += NT) c += (ckey[j] == T && cidx[j] < I); }
+        else { for (int i = threadIdx.x; i < min(M, I); i += NT) c += keyat(i) == T; }
+        return block_sum_i<NT>(c, sh);
+    };
+    int Ithr = M;                                    // select equal keys with idx < Ithr
+    if (cnt_eq_lt(M) > need) {
+        int I = 0;                                   // largest I with #(eq, idx < I) <= need
+        for (int bit = 17; bit >= 0; --bit) {
+            const int It = I + (1 << bit);
+            if (It <= M && cnt_eq_lt(It) <= need) I = It;
+        }
+        Ithr = I;
+    }
+    // 4. mark + ascending output
+    if (!ovf) {
+        for (int j = threadIdx.x; j < nc; j += NT) {
+            const uint32_t kk = ckey[j];
+            const int i = cidx[j];
+            if (kk > T || (kk == T && i < Ithr)) atomicOr(&bits[i >> 5], 1u << (i & 31));
+        }
+    } else {
+        for (int i = threadIdx.x; i < M; i += NT) {
+            const uint32_t kk = keyat(i);
+            if (kk > T || (kk == T && i < Ithr)) atomicOr(&bits[i >> 5], 1u << (i & 31));
+        }
+    }
+    __syncthreads();
+    const int wpt = (W + NT - 1) / NT;
     int cnt = 0;
-#pragma unroll
-    for (int w = 0; w < WPT; ++w) {
-        const int wi = threadIdx.x * WPT + w;
-        if (wi < MAXP / 32) cnt += __popc(bits[wi]);
+    for (int w = 0; w < wpt; ++w) {
+        const int wi = threadIdx.x * wpt + w;
+        if (wi < W) cnt += __popc(bits[wi]);
     }
     int tot;
     int o = block_excl_scan<NT>(cnt, sh, &tot);
-#pragma unroll
-    for (int w = 0; w < WPT; ++w) {
-        const int wi = threadIdx.x * WPT + w;
-        if (wi >= MAXP / 32) break;
+    for (int w = 0; w < wpt; ++w) {
+        const int wi = threadIdx.x * wpt + w;
+        if (wi >= W) break;
         uint32_t v = bits[wi];
         while (v) {
             const int bpos = __ffs(v) - 1;
