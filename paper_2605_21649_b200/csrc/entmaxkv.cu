@@ -109,13 +109,13 @@ Layout layout(const ekv_cache *c, int Hq, const ekv_select_params *sel) {
     L.tau_hat = take(B * Hq * 8);
     L.zero = o;
     L.rowmax = take(B * Hq * 4);
-    L.ccount = take(B * Hq * 4);
+    L.ccount = take(B * Hq * (size_t)((maxp + 255) / 256) * 4);
     L.tickets = take(B * Hq * 4);
     L.umask = take(B * Hkv * (size_t)L.W * 4);
     L.zero_bytes = o - L.zero;
     L.scores = take(B * Hq * maxp * kP * 4);
-    L.cand_s = take(B * Hq * (size_t)kCapG * 4);
-    L.cand_j = take(B * Hq * (size_t)kCapG * 4);
+    L.cand_s = take(B * Hq * (size_t)((maxp + 255) / 256) * kCpc * 4);
+    L.cand_j = take(B * Hq * (size_t)((maxp + 255) / 256) * kCpc * 4);
     L.tok_list = take(B * Hq * (size_t)L.list_cap * 4);
     L.p_list = take(B * Hq * (size_t)L.list_cap * 8);
     L.n_list = take(B * Hq * 4);
@@ -133,15 +133,31 @@ template <typename K> void set_smem(K kernel, int bytes) {
 }
 
 // ---------------------------------------------------------------- launch helpers
+int g_num_sms = 0;
+int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
 template <typename T, int G, int MODES>
 void score_go(const CacheView &v, const T *q, int Hq, float *box, float *mu, float *s2, cudaStream_t st) {
-    constexpr int PPC = ScoreCfg<MODES>::PPC;
+    constexpr int SP = ScoreCfg<MODES>::SP, NS = ScoreCfg<MODES>::NS;
     const int HD = v.Hkv * kD;
     const int per_page = ((MODES & 1) ? 2 * HD * (int)sizeof(T) : 0) + ((MODES & 2) ? 2 * HD * 4 : 0);
-    const int smem = PPC * per_page;
+    const int smem = NS * SP * per_page;
     static int init = 0;
     if (smem > init) { set_smem(k_score<T, G, MODES>, smem); init = smem; }
-    dim3 grid((v.maxp + PPC - 1) / PPC, v.B);
+    // persistent: ~2 CTAs per SM in total over the batch; at least 4 pages per CTA
+    const int per_b = (2 * num_sms() + v.B - 1) / v.B;
+    int gx = (v.maxp + 3) / 4;
+    if (gx > per_b) gx = per_b;
+    if (gx < 1) gx = 1;
+    dim3 grid(gx, v.B);
     k_score<T, G, MODES><<<grid, 256, smem, st>>>(v, q, Hq, box, mu, s2);
 }
 template <typename T, int G>
@@ -209,7 +225,7 @@ ekv_status launch_scores(const CacheView &v, const void *q, int Hq, const uint32
 
 template <typename T>
 ekv_status launch_tau(const CacheView &v, const TauArgs &A, int rows, cudaStream_t st) {
-    constexpr int smem = 8192 * 8 + kCap;
+    constexpr int smem = kCap * 8 + kCap;
     static bool init = false;
     if (!init) { set_smem(k_tau_pv<T>, smem); init = true; }
     k_tau_pv<T><<<rows, kTauNT, smem, st>>>(v, A);
@@ -261,15 +277,16 @@ ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t 
     float *cs = at<float>(ws, L.cand_s);
     int32_t *cj = at<int32_t>(ws, L.cand_j);
     const int list_len = full ? c->max_pages_per_seq : stride;
-    dim3 cg((list_len + 255) / 256, rows);
+    const int nch = (list_len + 255) / 256;
+    dim3 cg(nch, rows);
     k_candidates<<<cg, 256, 0, st>>>(scores, ntok, rowmax, pi, ns, stride, c->seq_lens, Hq, full, attn->alpha,
-                                     attn->transform, ccount, cs, cj, kCapG);
+                                     attn->transform, nch, ccount, cs, cj);
     EKV_TRY(check_launch("k_candidates"));
     TauArgs A;
     memset(&A, 0, sizeof(A));
     if (extra) A = *extra;
     A.scores = scores; A.ntok = ntok; A.rowmax = rowmax; A.ccount = ccount; A.cand_s = cs; A.cand_j = cj;
-    A.capG = kCapG; A.page_idx = pi; A.n_sel = ns; A.sel_stride = stride; A.full = full;
+    A.nch = nch; A.page_idx = pi; A.n_sel = ns; A.sel_stride = stride; A.full = full;
     A.Hq = Hq; A.G = Hq / c->n_kv_heads; A.alpha = attn->alpha; A.transform = attn->transform;
     A.out = out; A.tau_out = tau; A.supp_out = supp;
     if (c->dtype == EKV_BF16) return launch_tau<__nv_bfloat16>(v, A, rows, st);

@@ -146,18 +146,20 @@ __global__ void __launch_bounds__(256) k_attend_scores(CacheView c, const T *__r
 // Grid (chunk of 256 page-list entries, b * Hq + h); thread = one selected page of the
 // row (sparse: page_idx[row][i]; full: page i).  A token is a candidate iff
 // z = (double)a * s > tau_lo = a * s_max - 1 (tau >= z_max - 1 since F(z_max - 1) >= 1,
-// R9).  Softmax rows take every valid token.  Per-CTA block scan + one atomicAdd for
-// the row offset; the order across CTAs is fixed later by sorting on the token index.
+// R9).  Each chunk writes its candidates, in page-list order (block scan), into its own
+// region cand[row][chunk][0..kCpc) and its count into ccount[row][chunk]; the tau
+// kernel concatenates the chunks in order, so the candidate order is deterministic.
+// (max_pages <= 65536 -> at most 256 chunks per row.)
+constexpr int kCpc = 1024;          // candidates per chunk region
 __global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ scores, size_t ntok,
                                                     const uint32_t *__restrict__ rowmax,
                                                     const int32_t *__restrict__ page_idx,
                                                     const int32_t *__restrict__ n_sel, int sel_stride,
                                                     const int32_t *__restrict__ seq_lens, int Hq, int full,
-                                                    float alpha, int transform, int *__restrict__ ccount,
-                                                    float *__restrict__ cand_s, int32_t *__restrict__ cand_j,
-                                                    int capG) {
+                                                    float alpha, int transform, int nch,
+                                                    int *__restrict__ ccount, float *__restrict__ cand_s,
+                                                    int32_t *__restrict__ cand_j) {
     __shared__ int sh[9];
-    __shared__ int s_base;
     const int row = blockIdx.y;
     const int b = row / Hq;
     const int L = seq_lens[b];
@@ -181,25 +183,18 @@ __global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ sc
             sv[4 * v] = x.x; sv[4 * v + 1] = x.y; sv[4 * v + 2] = x.z; sv[4 * v + 3] = x.w;
         }
 #pragma unroll
-        for (int t = 0; t < kP; ++t) {
-            const bool keep = (page * kP + t < L) && sv[t] != -INFINITY && a * (double)sv[t] > tau_lo;
-            cnt += keep ? 1 : 0;
-        }
+        for (int t = 0; t < kP; ++t)
+            cnt += ((page * kP + t < L) && sv[t] != -INFINITY && a * (double)sv[t] > tau_lo) ? 1 : 0;
     }
     int tot;
     int pos = block_excl_scan<256>(cnt, sh, &tot);
-    if (threadIdx.x == 0) s_base = tot ? atomicAdd(ccount + row, tot) : 0;
-    __syncthreads();
-    pos += s_base;
+    const size_t reg = ((size_t)row * nch + blockIdx.x) * kCpc;
+    if (threadIdx.x == 0) ccount[(size_t)row * nch + blockIdx.x] = tot;
     if (i < nlist && cnt) {
 #pragma unroll
         for (int t = 0; t < kP; ++t) {
-            const bool keep = (page * kP + t < L) && sv[t] != -INFINITY && a * (double)sv[t] > tau_lo;
-            if (keep) {
-                if (pos < capG) {
-                    cand_s[(size_t)row * capG + pos] = sv[t];
-                    cand_j[(size_t)row * capG + pos] = page * kP + t;
-                }
+            if ((page * kP + t < L) && sv[t] != -INFINITY && a * (double)sv[t] > tau_lo) {
+                if (pos < kCpc) { cand_s[reg + pos] = sv[t]; cand_j[reg + pos] = page * kP + t; }
                 ++pos;
             }
         }
@@ -222,11 +217,10 @@ __global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ sc
 // global candidate list / score row brings tau_lo just below tau, then re-extract.
 constexpr int kTauNT = 256;
 constexpr int kCap = 6144;          // shared-memory candidate capacity
-constexpr int kCapG = 16384;        // global candidate capacity per row
 
 struct TauArgs {
     const float *scores; size_t ntok;
-    const uint32_t *rowmax; const int *ccount; const float *cand_s; const int32_t *cand_j; int capG;
+    const uint32_t *rowmax; const int *ccount; const float *cand_s; const int32_t *cand_j; int nch;
     const int32_t *page_idx; const int32_t *n_sel; int sel_stride; int full;
     int Hq, G; float alpha; int transform;
     float *out; double *tau_out; int32_t *supp_out;
@@ -237,8 +231,8 @@ template <typename T>
 __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
     constexpr int NT = kTauNT;
     extern __shared__ __align__(16) unsigned char smem[];
-    unsigned long long *ck = reinterpret_cast<unsigned long long *>(smem);   // [8192] (j << 32 | s bits)
-    uint8_t *cin = reinterpret_cast<uint8_t *>(smem + sizeof(unsigned long long) * 8192);   // [kCap]
+    unsigned long long *ck = reinterpret_cast<unsigned long long *>(smem);   // [kCap] (j << 32 | s bits)
+    uint8_t *cin = reinterpret_cast<uint8_t *>(smem + sizeof(unsigned long long) * kCap);   // [kCap]
     __shared__ double shd[2 * (NT / 32) + 2];
     __shared__ int shi[NT / 32 + 1];
     __shared__ float red[NT / 32][kD];
@@ -271,10 +265,17 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
             vx[0] = w.x; vx[1] = w.y; vx[2] = w.z; vx[3] = w.w;
         }
     };
-    const int ncand_all = A.ccount[row];
-    const float *gs = A.cand_s + (size_t)row * A.capG;
-    const int32_t *gj = A.cand_j + (size_t)row * A.capG;
-
+    // chunk counts -> offsets (deterministic concatenation in chunk order; nch <= NT)
+    int ccnt = 0, coff = 0, ncand_all = 0;
+    bool chunk_ovf = false;
+    if (threadIdx.x < A.nch) {
+        ccnt = A.ccount[(size_t)row * A.nch + threadIdx.x];
+        chunk_ovf = ccnt > kCpc;
+    }
+    coff = block_excl_scan<NT>(ccnt, shi, &ncand_all);
+    chunk_ovf = __syncthreads_or(chunk_ovf);
+    const float *gs = A.cand_s + (size_t)row * A.nch * kCpc;
+    const int32_t *gj = A.cand_j + (size_t)row * A.nch * kCpc;
     if (A.transform == 1) {
         // ---------------- softmax over C_tok: every valid token of the page list (dense V)
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -317,31 +318,23 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
     double tau_lo = zmax - 1.0 - 1e-12 * fmax(1.0, fabs(zmax));
     auto zof = [&](int k) -> double { return a * (double)__uint_as_float((uint32_t)(ck[k] & 0xffffffffu)); };
 
-    // candidate source: the global list (or, on overflow, a re-extraction) -> shared, sorted by j
+    // candidate source: the chunk regions concatenated in order (or, on overflow, an
+    // ordered re-extraction from the score row after a streamed Newton)
     int ncand = ncand_all;
-    if (ncand_all > kCap) {
-        // streamed Newton over the global candidates (or the whole row if the global list overflowed)
-        const bool use_list = ncand_all <= A.capG;
+    if (ncand_all > kCap || chunk_ovf) {
         const int nlist = A.full ? n_pages_of(L) : A.n_sel[row];
         const float *srow = A.scores + (size_t)row * A.ntok;
         double tau = tau_lo;
         for (int it = 0; it < 200; ++it) {
             double F = 0.0, Fd = 0.0;
-            if (use_list) {
-                for (int k = threadIdx.x; k < ncand_all; k += NT) {
-                    const double d = a * (double)gs[k] - tau;
-                    if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
-                }
-            } else {
-                for (int e = threadIdx.x; e < nlist * kP; e += NT) {
-                    const int pg = A.full ? e / kP : A.page_idx[(size_t)row * A.sel_stride + e / kP];
-                    const int j = pg * kP + e % kP;
-                    if (j >= L) continue;
-                    const float sj = srow[j];
-                    if (sj == -INFINITY) continue;
-                    const double d = a * (double)sj - tau;
-                    if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
-                }
+            for (int e = threadIdx.x; e < nlist * kP; e += NT) {
+                const int pg = A.full ? e / kP : A.page_idx[(size_t)row * A.sel_stride + e / kP];
+                const int j = pg * kP + e % kP;
+                if (j >= L) continue;
+                const float sj = srow[j];
+                if (sj == -INFINITY) continue;
+                const double d = a * (double)sj - tau;
+                if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
             }
             block_sum2_d<NT>(F, Fd, shd);
             if (!(Fd > 0.0)) break;
@@ -351,20 +344,16 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
             if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(tau)))) break;
         }
         tau_lo = fmax(tau_lo, tau - 1e-7 * fmax(1.0, fabs(tau)));
-        // ordered re-extraction of {z > tau_lo} (deterministic block scans)
         int base = 0;
-        const int total_e = use_list ? ncand_all : nlist * kP;
+        const int total_e = nlist * kP;
         for (int r0 = 0; r0 < total_e; r0 += NT) {
             const int e = r0 + threadIdx.x;
             float sj = -INFINITY;
             int j = 0;
             if (e < total_e) {
-                if (use_list) { sj = gs[e]; j = gj[e]; }
-                else {
-                    const int pg = A.full ? e / kP : A.page_idx[(size_t)row * A.sel_stride + e / kP];
-                    j = pg * kP + e % kP;
-                    if (j < L) sj = srow[j];
-                }
+                const int pg = A.full ? e / kP : A.page_idx[(size_t)row * A.sel_stride + e / kP];
+                j = pg * kP + e % kP;
+                if (j < L) sj = srow[j];
             }
             const int keep = (sj != -INFINITY && a * (double)sj > tau_lo) ? 1 : 0;
             int tot;
@@ -383,15 +372,13 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
             return;
         }
     } else {
-        for (int k = threadIdx.x; k < ncand; k += NT)
-            ck[k] = ((unsigned long long)(uint32_t)gj[k] << 32) | __float_as_uint(gs[k]);
+        // thread ch copies chunk ch to its prefix offset (chunk counts are small)
+        if (threadIdx.x < A.nch) {
+            const size_t g0 = (size_t)threadIdx.x * kCpc;
+            for (int k = 0; k < ccnt; ++k)
+                ck[coff + k] = ((unsigned long long)(uint32_t)gj[g0 + k] << 32) | __float_as_uint(gs[g0 + k]);
+        }
         __syncthreads();
-    }
-    {
-        const int n2 = next_pow2(max(ncand, 1));
-        for (int k = ncand + threadIdx.x; k < n2; k += NT) ck[k] = ~0ull;
-        __syncthreads();
-        bitonic_sort_u64<NT>(ck, n2);
     }
 
     // ---- Newton on the candidates
@@ -552,12 +539,16 @@ __global__ void __launch_bounds__(256) k_delta_bar(const float *__restrict__ box
         s_last = (tk == (unsigned)nchunks - 1);
     }
     __syncthreads();
-    if (s_last && threadIdx.x == 0) {
+    if (s_last && threadIdx.x < 32) {       // fixed lane -> chunk map and shuffle tree: deterministic
         __threadfence();
         double s = 0.0;
-        for (int c2 = 0; c2 < nchunks; ++c2) s += ((volatile double *)partial)[(size_t)row * nchunks + c2];
-        out[row] = (t == t) ? s : NAN;
-        tickets[row] = 0u;                 // ready for the next call
+        for (int c2 = threadIdx.x; c2 < nchunks; c2 += 32) s += ((volatile double *)partial)[(size_t)row * nchunks + c2];
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) {
+            out[row] = (t == t) ? s : NAN;
+            tickets[row] = 0u;             // ready for the next call
+        }
     }
 }
 

@@ -108,43 +108,53 @@ __global__ void __launch_bounds__(256) k_rebuild(CacheView c) {
 //    = q_i kext_i as two fmas with qneg = (q_i >= 0 ? 0 : q_i), qpos = (q_i >= 0 ? q_i
 //    : 0): one of the two adds an exact zero, so the chain equals fma(q_i, kext_i, acc).
 template <int MODES> struct ScoreCfg {
-    static constexpr int PPC = (MODES == 1) ? 16 : 8;
+    static constexpr int SP = (MODES == 1) ? 8 : 4;     // pages per stage
+    static constexpr int NS = 3;                        // ring stages
 };
 
+// Persistent: CTA k owns the contiguous page range [k*M/grid, (k+1)*M/grid) of every
+// sequence (grid.y = batch); stages of SP pages flow through an NS-deep ring.
 template <typename T, int G, int MODES>
-__global__ void __launch_bounds__(256) k_score(CacheView c, const T *__restrict__ q, int Hq,
-                                                float *__restrict__ box, float *__restrict__ mu,
-                                                float *__restrict__ sigma2) {
-    constexpr int PPC = ScoreCfg<MODES>::PPC;
+__global__ void __launch_bounds__(256, 2) k_score(CacheView c, const T *__restrict__ q, int Hq,
+                                                   float *__restrict__ box, float *__restrict__ mu,
+                                                   float *__restrict__ sigma2) {
+    constexpr int SP = ScoreCfg<MODES>::SP, NS = ScoreCfg<MODES>::NS;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ uint64_t bars[PPC];
+    __shared__ uint64_t bars[NS];
     const int b = blockIdx.y;
     const int L = c.seq_lens[b];
     const int M = n_pages_of(L);
-    const int p0 = blockIdx.x * PPC;
-    if (p0 >= M) return;
-    const int np = min(PPC, M - p0);
+    const int pa = (int)(((long long)M * blockIdx.x) / gridDim.x);
+    const int pz = (int)(((long long)M * (blockIdx.x + 1)) / gridDim.x);
+    if (pa >= pz) return;
+    const int nst = (pz - pa + SP - 1) / SP;
     const int HD = c.Hkv * kD;
     const uint32_t bmm = (uint32_t)(HD * sizeof(T));          // kmin / kmax block bytes
     const uint32_t bgs = (uint32_t)(HD * sizeof(float));      // kavg / kvar block bytes
     const uint32_t per_page = ((MODES & 1) ? 2 * bmm : 0) + ((MODES & 2) ? 2 * bgs : 0);
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < np; ++i) mbar_init(&bars[i], 1);
-        fence_mbar_init();
-        for (int i = 0; i < np; ++i) {
-            const size_t phys = (size_t)__ldg(c.page_table + (size_t)b * c.maxp + p0 + i);
-            unsigned char *dst = smem + (size_t)i * per_page;
-            mbar_expect_tx(&bars[i], per_page);
+    auto issue = [&](int si) {
+        const int slot = si % NS;
+        const int q0 = pa + si * SP;
+        const int n = min(SP, pz - q0);
+        mbar_expect_tx(&bars[slot], n * per_page);
+        for (int i = 0; i < n; ++i) {
+            const size_t phys = (size_t)__ldg(c.page_table + (size_t)b * c.maxp + q0 + i);
+            unsigned char *dst = smem + ((size_t)slot * SP + i) * per_page;
             if (MODES & 1) {
-                bulk_g2s(dst, reinterpret_cast<const T *>(c.kmin) + phys * HD, bmm, &bars[i]);
-                bulk_g2s(dst + bmm, reinterpret_cast<const T *>(c.kmax) + phys * HD, bmm, &bars[i]);
+                bulk_g2s(dst, reinterpret_cast<const T *>(c.kmin) + phys * HD, bmm, &bars[slot]);
+                bulk_g2s(dst + bmm, reinterpret_cast<const T *>(c.kmax) + phys * HD, bmm, &bars[slot]);
                 dst += 2 * bmm;
             }
             if (MODES & 2) {
-                bulk_g2s(dst, c.kavg + phys * HD, bgs, &bars[i]);
-                bulk_g2s(dst + bgs, c.kvar + phys * HD, bgs, &bars[i]);
+                bulk_g2s(dst, c.kavg + phys * HD, bgs, &bars[slot]);
+                bulk_g2s(dst + bgs, c.kvar + phys * HD, bgs, &bars[slot]);
             }
         }
+    };
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+        for (int si = 0; si < min(NS, nst); ++si) issue(si);
     }
     const int lane = threadIdx.x & 31;
     const int l16 = threadIdx.x & 15;
@@ -165,66 +175,76 @@ __global__ void __launch_bounds__(256) k_score(CacheView c, const T *__restrict_
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            qp[g][i] = make_float2(x0[i] >= 0.0f ? x0[i] : 0.0f, x1[i] >= 0.0f ? x1[i] : 0.0f);
-            qn[g][i] = make_float2(x0[i] >= 0.0f ? 0.0f : x0[i], x1[i] >= 0.0f ? 0.0f : x1[i]);
-            qa[g][i] = make_float2(x0[i], x1[i]);
-            q2[g][i] = make_float2(__fmul_rn(x0[i], x0[i]), __fmul_rn(x1[i], x1[i]));
+            if (MODES & 1) {
+                qp[g][i] = make_float2(x0[i] >= 0.0f ? x0[i] : 0.0f, x1[i] >= 0.0f ? x1[i] : 0.0f);
+                qn[g][i] = make_float2(x0[i] >= 0.0f ? 0.0f : x0[i], x1[i] >= 0.0f ? 0.0f : x1[i]);
+            }
+            if (MODES & 2) {
+                qa[g][i] = make_float2(x0[i], x1[i]);
+                q2[g][i] = make_float2(__fmul_rn(x0[i], x0[i]), __fmul_rn(x1[i], x1[i]));
+            }
         }
     }
     __syncthreads();                         // mbarrier inits visible
     const int h_out = hq0 + rs_head<G>(lane);
     const bool writer = rs_writer<G>(lane);
-    // warp-uniform trip count: both half-warps of a warp run the same iterations
-    for (int ib = 0; ib < np; ib += hwpk) {
-        const int i = ib + sub;
-        const bool valid = i < np;
-        const int ii = valid ? i : 0;
-        mbar_wait(&bars[ii], 0);
-        const unsigned char *pg = smem + (size_t)ii * per_page;
-        const int p = p0 + ii;
-        if (MODES & 1) {
-            float mn[8], mx[8];
-            Elem<T>::load8(reinterpret_cast<const T *>(pg) + kvh * kD + 8 * l16, mn);
-            Elem<T>::load8(reinterpret_cast<const T *>(pg + bmm) + kvh * kD + 8 * l16, mx);
-            float acc[G];
+    float *box_row = box + ((size_t)b * Hq + h_out) * c.maxp;
+    float *mu_row = mu + ((size_t)b * Hq + h_out) * c.maxp;
+    float *s2_row = sigma2 + ((size_t)b * Hq + h_out) * c.maxp;
+    for (int si = 0; si < nst; ++si) {
+        const int slot = si % NS;
+        mbar_wait(&bars[slot], (si / NS) & 1);
+        const int q0 = pa + si * SP;
+        const int n = min(SP, pz - q0);
+        // warp-uniform trip count: both half-warps of a warp run the same iterations
+        for (int ib = 0; ib < n; ib += hwpk) {
+            const int i = ib + sub;
+            const bool valid = i < n;
+            const unsigned char *pg = smem + ((size_t)slot * SP + (valid ? i : 0)) * per_page;
+            const int p = q0 + i;
+            if (MODES & 1) {
+                float mn[8], mx[8];
+                Elem<T>::load8(reinterpret_cast<const T *>(pg) + kvh * kD + 8 * l16, mn);
+                Elem<T>::load8(reinterpret_cast<const T *>(pg + bmm) + kvh * kD + 8 * l16, mx);
+                float acc[G];
 #pragma unroll
-            for (int g = 0; g < GP; ++g) {
-                float2 a2 = make_float2(0.0f, 0.0f);
+                for (int g = 0; g < GP; ++g) {
+                    float2 a2 = make_float2(0.0f, 0.0f);
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    a2 = ffma2(qn[g][e], mn[e], a2);
-                    a2 = ffma2(qp[g][e], mx[e], a2);
+                    for (int e = 0; e < 8; ++e) {
+                        a2 = ffma2(qn[g][e], mn[e], a2);
+                        a2 = ffma2(qp[g][e], mx[e], a2);
+                    }
+                    acc[2 * g] = a2.x;
+                    if (2 * g + 1 < G) acc[2 * g + 1] = a2.y;
                 }
-                acc[2 * g] = a2.x;
-                if (2 * g + 1 < G) acc[2 * g + 1] = a2.y;
+                const float r = __fmul_rn(rs_reduce16<G>(acc, lane), kCd);
+                if (writer && valid) box_row[p] = r;
             }
-            const float r = __fmul_rn(rs_reduce16<G>(acc, lane), kCd);
-            if (writer && valid) box[((size_t)b * Hq + h_out) * c.maxp + p] = r;
-        }
-        if (MODES & 2) {
-            const unsigned char *pgs = pg + ((MODES & 1) ? 2 * bmm : 0);
-            float av[8], vr[8];
-            Elem<float>::load8(reinterpret_cast<const float *>(pgs) + kvh * kD + 8 * l16, av);
-            Elem<float>::load8(reinterpret_cast<const float *>(pgs + bgs) + kvh * kD + 8 * l16, vr);
-            float am[G], as[G];
+            if (MODES & 2) {
+                const unsigned char *pgs = pg + ((MODES & 1) ? 2 * bmm : 0);
+                float av[8], vr[8];
+                Elem<float>::load8(reinterpret_cast<const float *>(pgs) + kvh * kD + 8 * l16, av);
+                Elem<float>::load8(reinterpret_cast<const float *>(pgs + bgs) + kvh * kD + 8 * l16, vr);
+                float am[G], as[G];
 #pragma unroll
-            for (int g = 0; g < GP; ++g) {
-                float2 m2 = make_float2(0.0f, 0.0f), s2 = make_float2(0.0f, 0.0f);
+                for (int g = 0; g < GP; ++g) {
+                    float2 m2 = make_float2(0.0f, 0.0f), s2 = make_float2(0.0f, 0.0f);
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    m2 = ffma2(qa[g][e], av[e], m2);
-                    s2 = ffma2(q2[g][e], vr[e], s2);
+                    for (int e = 0; e < 8; ++e) {
+                        m2 = ffma2(qa[g][e], av[e], m2);
+                        s2 = ffma2(q2[g][e], vr[e], s2);
+                    }
+                    am[2 * g] = m2.x; as[2 * g] = s2.x;
+                    if (2 * g + 1 < G) { am[2 * g + 1] = m2.y; as[2 * g + 1] = s2.y; }
                 }
-                am[2 * g] = m2.x; as[2 * g] = s2.x;
-                if (2 * g + 1 < G) { am[2 * g + 1] = m2.y; as[2 * g + 1] = s2.y; }
-            }
-            const float rm = __fmul_rn(rs_reduce16<G>(am, lane), kCd);
-            const float rs = __fmul_rn(rs_reduce16<G>(as, lane), 1.0f / (float)kD);
-            if (writer && valid) {
-                mu[((size_t)b * Hq + h_out) * c.maxp + p] = rm;
-                sigma2[((size_t)b * Hq + h_out) * c.maxp + p] = rs;
+                const float rm = __fmul_rn(rs_reduce16<G>(am, lane), kCd);
+                const float rs = __fmul_rn(rs_reduce16<G>(as, lane), 1.0f / (float)kD);
+                if (writer && valid) { mu_row[p] = rm; s2_row[p] = rs; }
             }
         }
+        __syncthreads();                     // stage consumed by every warp
+        if (threadIdx.x == 0 && si + NS < nst) issue(si + NS);
     }
 }
 

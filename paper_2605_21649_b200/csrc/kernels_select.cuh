@@ -8,12 +8,14 @@ namespace ekv {
 // ============================================================================ a2: top-k
 // One CTA (NT threads) per (b, q-head) row (R3: key desc, then lower page
 // index).  Keys are the ordered-int encodings of the fp32 box scores (-0 == +0).
-//  1. Partition bound: thread t reads the keys {4(t + NT j) .. +3} (float4, coalesced)
-//     and keeps their max m_t.  L = the k-th largest m_t, found MSB-first with
-//     __syncthreads_count.  At least k keys are >= L, so T* (the k-th largest key) >= L.
-//  2. Candidates {key >= L} are compacted into shared memory (warp ballot).
-//  3. T* by an MSB-first search over the candidates; ties at T* are broken by the
-//     smallest page indices (a second MSB-first search over the index).
+//  1. Partition bound: thread t reads the keys {4(t + NT j) .. +3} (float4, coalesced,
+//     4 loads in flight per thread) and keeps their max m_t.  L = the k-th largest
+//     m_t, found MSB-first with __syncthreads_count.  At least k keys are >= L, so the
+//     k-th largest key T* >= L and every selected key is a candidate {key >= L}.
+//  2. Candidates are compacted into shared memory (warp ballot + one shared atomic per
+//     warp; their order does not matter: the selection is defined by (key, index)).
+//  3. T* by an MSB-first search over the candidates (__syncthreads_count per slot);
+//     ties at T* are broken by the smallest page indices (MSB-first over the index).
 //  4. The selection is marked in a shared bitmap and written ascending (block scan).
 // Overflow (more than kTopkCap candidates): the same searches run over all keys read
 // from global memory (L2) -- exact, slower.
@@ -44,16 +46,29 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
     const int W = (M + 31) / 32;
     for (int w = threadIdx.x; w < W; w += NT) bits[w] = 0u;
     if (threadIdx.x == 0) s_cnt = 0;
-    auto keyat = [&](int i) -> uint32_t { return i < M ? f2key(__ldg(x + i)) : 0u; };
-    // 1. partition maxima
-    uint32_t mt = 0u;
-    for (int i4 = 4 * threadIdx.x; i4 < M; i4 += 4 * NT) {
-        if (i4 + 3 < M && ((maxp & 3) == 0)) {
+    const bool vec = (maxp & 3) == 0;
+    auto key4 = [&](int i4, uint32_t (&kk)[4]) {
+        if (vec && i4 + 3 < M) {
             const float4 v = __ldg(reinterpret_cast<const float4 *>(x + i4));
-            mt = max(mt, max(max(f2key(v.x), f2key(v.y)), max(f2key(v.z), f2key(v.w))));
+            kk[0] = f2key(v.x); kk[1] = f2key(v.y); kk[2] = f2key(v.z); kk[3] = f2key(v.w);
         } else {
-            for (int e = 0; e < 4; ++e) mt = max(mt, keyat(i4 + e));
+#pragma unroll
+            for (int e = 0; e < 4; ++e) kk[e] = (i4 + e < M) ? f2key(__ldg(x + i4 + e)) : 0u;
         }
+    };
+    // 1. partition maxima (4 float4 loads in flight per thread)
+    uint32_t mt = 0u;
+    for (int base = 0; base < M; base += 16 * NT) {
+        uint32_t kk[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i4 = base + 4 * (threadIdx.x + u * NT);
+            if (i4 < M) key4(i4, kk[u]);
+            else { kk[u][0] = kk[u][1] = kk[u][2] = kk[u][3] = 0u; }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            mt = max(mt, max(max(kk[u][0], kk[u][1]), max(kk[u][2], kk[u][3])));
     }
     __syncthreads();
     uint32_t Lb = 1u;
@@ -65,43 +80,68 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
         }
         Lb = T > 1u ? T : 1u;
     }
-    // 2. candidates
-    for (int i0 = 0; i0 < M; i0 += NT) {
-        const int i = i0 + threadIdx.x;
-        const uint32_t kk = keyat(i);
-        const bool c = kk >= Lb;
-        const unsigned m = __ballot_sync(0xffffffffu, c);
-        int base = 0;
-        if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(&s_cnt, __popc(m));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (c) {
-            const int pos = base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u));
-            if (pos < kTopkCap) { ckey[pos] = kk; cidx[pos] = i; }
+    // 2. candidates (second pass, same access pattern)
+    for (int base = 0; base < M; base += 16 * NT) {
+        uint32_t kk[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i4 = base + 4 * (threadIdx.x + u * NT);
+            if (i4 < M) key4(i4, kk[u]);
+            else { kk[u][0] = kk[u][1] = kk[u][2] = kk[u][3] = 0u; }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const bool c = kk[u][e] >= Lb;
+                const unsigned m = __ballot_sync(0xffffffffu, c);
+                if (!m) continue;
+                int pos = 0;
+                if ((threadIdx.x & 31) == 0) pos = atomicAdd(&s_cnt, __popc(m));
+                pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(m & ((1u << (threadIdx.x & 31)) - 1u));
+                if (c && pos < kTopkCap) {
+                    ckey[pos] = kk[u][e];
+                    cidx[pos] = base + 4 * (threadIdx.x + u * NT) + e;
+                }
+            }
         }
     }
     __syncthreads();
     const int nc = s_cnt;
     const bool ovf = nc > kTopkCap;
+    const int slots = (nc + NT - 1) / NT;
     // 3. T* = k-th largest candidate key (or key, on overflow)
     auto cnt_ge = [&](uint32_t Tt) -> int {
+        if (!ovf) {
+            int c = 0;
+            for (int s2 = 0; s2 < slots; ++s2) {
+                const int j = s2 * NT + threadIdx.x;
+                c += __syncthreads_count(j < nc && ckey[j] >= Tt);
+            }
+            return c;
+        }
         int c = 0;
-        if (!ovf) { for (int j = threadIdx.x; j < nc; j += NT) c += ckey[j] >= Tt; }
-        else { for (int i = threadIdx.x; i < M; i += NT) c += keyat(i) >= Tt; }
+        for (int i = threadIdx.x; i < M; i += NT) c += f2key(__ldg(x + i)) >= Tt;
         return block_sum_i<NT>(c, sh);
     };
-    // largest T with #(key >= T) >= k; for T <= L the predicate holds by step 1
-    uint32_t T = 0u;
+    uint32_t T = 0u;        // largest T with #(key >= T) >= k; holds for T <= L by step 1
     for (int bit = 31; bit >= 0; --bit) {
         const uint32_t Tt = T | (1u << bit);
         if (Tt <= Lb || cnt_ge(Tt) >= keff) T = Tt;
     }
-    // keys > T are in; ties at T: the need smallest indices
     const int n_gt = (T == 0xffffffffu) ? 0 : cnt_ge(T + 1u);
     const int need = keff - n_gt;
     auto cnt_eq_lt = [&](int I) -> int {       // #(key == T && idx < I)
+        if (!ovf) {
+            int c = 0;
+            for (int s2 = 0; s2 < slots; ++s2) {
+                const int j = s2 * NT + threadIdx.x;
+                c += __syncthreads_count(j < nc && ckey[j] == T && cidx[j] < I);
+            }
+            return c;
+        }
         int c = 0;
-        if (!ovf) { for (int j = threadIdx.x; j < nc; j += NT) c += (ckey[j] == T && cidx[j] < I); }
-        else { for (int i = threadIdx.x; i < min(M, I); i += NT) c += keyat(i) == T; }
+        for (int i = threadIdx.x; i < min(M, I); i += NT) c += f2key(__ldg(x + i)) == T;
         return block_sum_i<NT>(c, sh);
     };
     int Ithr = M;                                    // select equal keys with idx < Ithr
@@ -122,7 +162,7 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
         }
     } else {
         for (int i = threadIdx.x; i < M; i += NT) {
-            const uint32_t kk = keyat(i);
+            const uint32_t kk = f2key(__ldg(x + i));
             if (kk > T || (kk == T && i < Ithr)) atomicOr(&bits[i >> 5], 1u << (i & 31));
         }
     }
