@@ -309,3 +309,9 @@ template <int NT> __device__ __forceinline__ void bitonic_sort_u32_desc(uint32_t
 }
 __device__ __forceinline__ int next_pow2(int x) { int p = 1; while (p < x) p <<= 1; return p; }
 }  // namespace ekv
+
+namespace ekv {
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+}  // namespace ekv

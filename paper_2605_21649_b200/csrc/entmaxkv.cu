@@ -152,13 +152,11 @@ void score_go(const CacheView &v, const T *q, int Hq, float *box, float *mu, flo
     const int smem = NS * SP * per_page;
     static int init = 0;
     if (smem > init) { set_smem(k_score<T, G, MODES>, smem); init = smem; }
-    // persistent: ~2 CTAs per SM in total over the batch; at least 4 pages per CTA
-    const int per_b = (2 * num_sms() + v.B - 1) / v.B;
-    int gx = (v.maxp + 3) / 4;
-    if (gx > per_b) gx = per_b;
+    // persistent: 2 CTAs per SM over the flattened (b, page) space, >= 8 pages per CTA
+    long long gx = ((long long)v.B * v.maxp + 7) / 8;
+    if (gx > 2 * num_sms()) gx = 2 * num_sms();
     if (gx < 1) gx = 1;
-    dim3 grid(gx, v.B);
-    k_score<T, G, MODES><<<grid, 256, smem, st>>>(v, q, Hq, box, mu, s2);
+    k_score<T, G, MODES><<<(unsigned)gx, 288, smem, st>>>(v, q, Hq, box, mu, s2);
 }
 template <typename T, int G>
 ekv_status launch_score_t(const CacheView &v, const void *q, int Hq, int modes, float *box, float *mu, float *s2,
@@ -205,11 +203,15 @@ ekv_status launch_mark(const ekv_cache *c, int Hq, const int32_t *pi, const int3
 template <typename T, int G>
 ekv_status launch_scores_t(const CacheView &v, const void *q, int Hq, const uint32_t *um, int W, float *scores,
                            uint32_t *rowmax, int full, cudaStream_t st) {
-    constexpr int smem = 2 * 8 * kP * kD * (int)sizeof(T);
+    constexpr int smem = AttCfg<T>::SMEM;
     static bool init = false;
     if (!init) { set_smem(k_attend_scores<T, G>, smem); init = true; }
-    dim3 grid((v.maxp + 511) / 512, v.B * v.Hkv);
-    k_attend_scores<T, G><<<grid, 256, smem, st>>>(v, static_cast<const T *>(q), Hq, um, W, scores, rowmax, full);
+    const int per_sm = sizeof(T) == 2 ? 2 : 1;
+    long long gx = ((long long)v.B * v.Hkv * ((v.maxp + 3) / 4) + 15) / 16;   // >= 64 page slots per CTA
+    if (gx > per_sm * num_sms()) gx = per_sm * num_sms();
+    if (gx < 1) gx = 1;
+    k_attend_scores<T, G><<<(unsigned)gx, 288, smem, st>>>(v, static_cast<const T *>(q), Hq, um, W, scores, rowmax,
+                                                           full);
     return check_launch("k_attend_scores");
 }
 template <typename T>

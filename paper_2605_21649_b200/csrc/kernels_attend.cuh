@@ -11,135 +11,182 @@ namespace ekv {
 // are written.  rowmax[b][h] holds the ordered-int max score (atomicMax; 0 = empty).
 
 // ============================================================================ K scores
-// Grid (chunk of CH pages, b * Hkv + kvh); 256 threads = 16 half-warps.
-//  - The selected pages of the chunk (union mask byte != 0, or every page for the full
-//    baseline) are compacted ascending into shared memory.
-//  - They are processed in batches of BP pages through a 2-stage ring: thread 0 issues
-//    one cp.async.bulk (TMA, 1-D) per page tile K[phys][kvh][0..P)[0..d) (4 KiB bf16,
-//    contiguous in HBM) completing on the stage's mbarrier; batch i+1 is in flight
-//    while batch i is scored.
-//  - Two half-warps per page, 8 tokens each: lane c reads the 16-byte chunk c of the
-//    token row (contiguous 256-byte row per half-warp: conflict-free), runs the
-//    8-element fma chains for the G query heads (R1) and the reduce-scatter tree;
-//    s = fl32(dot * c_d) (R2).  Tokens past seq_len get -inf.
-//  - Per-head running max -> one atomicMax per (CTA, head) into rowmax.
+// Persistent, warp-specialised: grid = ~2 CTAs per SM, 288 threads = 8 consumer warps
+// (16 half-warps) + 1 producer warp.  The flattened (unit = b*Hkv + kvh, page) space
+// is split into equal contiguous ranges, one per CTA.
+//  - Producer warp: scans its range 32 pages at a time (ballot over the union mask
+//    byte, or every page for the full baseline), packs selected pages into ring stages
+//    of SP pages and issues one cp.async.bulk (TMA, 1-D) per page tile
+//    K[phys][kvh][0..P)[0..d) (4 KiB bf16, contiguous in HBM) completing on the
+//    stage's `full` mbarrier; it waits on the stage's `empty` mbarrier before reuse.
+//    A stage with n = -1 ends the stream.
+//  - Consumers: two half-warps per page, 8 tokens each: lane c reads the 16-byte chunk
+//    c of the token row from shared memory (contiguous 256-byte row per half-warp:
+//    conflict-free), runs the 8-element fma chains for the G query heads (R1; q is
+//    reloaded when the unit changes) and the reduce-scatter tree; s = fl32(dot * c_d)
+//    (R2).  Tokens past seq_len get -inf.  Running per-head max, flushed with one
+//    atomicMax per (half-warp, unit) into rowmax.
+template <typename T> struct AttCfg {
+    static constexpr int SP = 8, NS = 3;
+    static constexpr int TILE = kP * kD * (int)sizeof(T);
+    static constexpr int SMEM = NS * SP * TILE;
+};
+
 template <typename T, int G>
-__global__ void __launch_bounds__(256) k_attend_scores(CacheView c, const T *__restrict__ q, int Hq,
+__global__ void __launch_bounds__(288) k_attend_scores(CacheView c, const T *__restrict__ q, int Hq,
                                                        const uint32_t *__restrict__ umask, int W,
                                                        float *__restrict__ scores, uint32_t *__restrict__ rowmax,
                                                        int full) {
-    constexpr int CH = 512;                 // pages per CTA
-    constexpr int BP = 8;                   // pages per batch (stage)
-    constexpr int TILE = kP * kD * (int)sizeof(T);
-    extern __shared__ __align__(128) unsigned char smem[];   // [2][BP][TILE]
-    __shared__ uint64_t bars[2];
-    __shared__ int s_pages[CH];
-    __shared__ uint8_t s_mask[CH];
-    __shared__ int s_cnt;
-    __shared__ int sh[9];
-    __shared__ uint32_t s_max[16][G];
-    const int unit = blockIdx.y;
-    const int b = unit / c.Hkv, kvh = unit % c.Hkv;
-    const int L = c.seq_lens[b];
-    const int M = n_pages_of(L);
-    const int p0 = blockIdx.x * CH;
-    if (p0 >= M) return;
-    const int tid = threadIdx.x;
-    // compact the selected pages of [p0, p0 + CH) in ascending order (2 pages per thread)
-    {
-        uint8_t m[2];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const int p = p0 + 2 * tid + r;
-            m[r] = 0;
-            if (p < M) {
-                m[r] = full ? (uint8_t)((1u << G) - 1u)
-                            : (uint8_t)((umask[((size_t)b * c.Hkv + kvh) * W + (p >> 2)] >> ((p & 3) * 8)) & 0xffu);
-            }
-        }
-        int tot;
-        int pos = block_excl_scan<256>((m[0] != 0) + (m[1] != 0), sh, &tot);
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-            if (m[r]) { s_pages[pos] = p0 + 2 * tid + r; s_mask[pos] = m[r]; ++pos; }
-        if (tid == 0) sh[8] = tot;
-    }
-    if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+    constexpr int SP = AttCfg<T>::SP, NS = AttCfg<T>::NS, TILE = AttCfg<T>::TILE;
+    constexpr int NCW = 8;
+    extern __shared__ __align__(128) unsigned char smem[];   // [NS][SP][TILE]
+    __shared__ uint64_t fullb[NS], emptyb[NS];
+    __shared__ int d_page[NS][SP], d_unit[NS][SP], d_n[NS];
+    __shared__ uint8_t d_mask[NS][SP];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // flattened mask-word space (unit, word of 4 pages): one contiguous range per CTA
+    const long long W4 = (long long)c.B * c.Hkv * W;
+    const long long w0 = W4 * blockIdx.x / gridDim.x, w1 = W4 * (blockIdx.x + 1) / gridDim.x;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NS; ++i) { mbar_init(&fullb[i], 1); mbar_init(&emptyb[i], NCW); }
         fence_mbar_init();
     }
     __syncthreads();
-    const int np = sh[8];
-    if (np == 0) return;
-    const int nb = (np + BP - 1) / BP;
-    const unsigned char *Kb = reinterpret_cast<const unsigned char *>(c.K);
-    auto issue = [&](int bi) {
-        const int st = bi & 1;
-        const int n = min(BP, np - bi * BP);
-        mbar_expect_tx(&bars[st], n * TILE);
-        for (int i = 0; i < n; ++i) {
-            const int phys = __ldg(c.page_table + (size_t)b * c.maxp + s_pages[bi * BP + i]);
-            bulk_g2s(smem + ((size_t)st * BP + i) * TILE, Kb + ((size_t)phys * c.Hkv + kvh) * TILE, TILE, &bars[st]);
-        }
-    };
-    if (tid == 0) {
-        issue(0);
-        if (nb > 1) issue(1);
-    }
-    const int lane = tid & 31, l16 = tid & 15, hw = tid >> 4;
-    float qr[G][8];
+    if (warp == NCW) {
+        // ------------------------------------------------ producer
+        const unsigned char *Kb = reinterpret_cast<const unsigned char *>(c.K);
+        int si = 0, fill = 0;
+        auto open_stage = [&]() {
+            const int slot = si % NS;
+            if (si >= NS) mbar_wait(&emptyb[slot], ((si / NS) - 1) & 1);
+        };
+        auto close_stage = [&](int n) {           // lane 0 only
+            const int slot = si % NS;
+            d_n[slot] = n;
+            if (n > 0) {
+                mbar_expect_tx(&fullb[slot], (uint32_t)(n * TILE));
+                for (int i = 0; i < n; ++i) {
+                    const int u = d_unit[slot][i], bb = u / c.Hkv, kh = u % c.Hkv;
+                    const int phys = __ldg(c.page_table + (size_t)bb * c.maxp + d_page[slot][i]);
+                    bulk_g2s(smem + ((size_t)slot * SP + i) * TILE, Kb + ((size_t)phys * c.Hkv + kh) * TILE,
+                             TILE, &fullb[slot]);
+                }
+            } else {
+                mbar_arrive(&fullb[slot]);
+            }
+            ++si;
+        };
+        if (lane == 0) open_stage();
+        // scan the range one mask word (4 pages) per lane, 4 words in flight per lane
+        for (long long wb = w0; wb < w1; wb += 128) {
+            uint32_t wv[4];
+            int un[4], wj[4], Mu[4];
 #pragma unroll
-    for (int g = 0; g < G; ++g) Elem<T>::load8(q + ((size_t)b * Hq + kvh * G + g) * kD + 8 * l16, qr[g]);
+            for (int r = 0; r < 4; ++r) {
+                const long long wi = wb + r * 32 + lane;
+                wv[r] = 0u; un[r] = 0; wj[r] = 0; Mu[r] = 0;
+                if (wi < w1) {
+                    un[r] = (int)(wi / W);
+                    wj[r] = (int)(wi % W);
+                    Mu[r] = n_pages_of(__ldg(c.seq_lens + un[r] / c.Hkv));
+                    wv[r] = full ? 0xffffffffu : __ldg(umask + (size_t)un[r] * W + wj[r]);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int p = 4 * wj[r] + j;
+                    uint32_t m = (wv[r] >> (8 * j)) & 0xffu;
+                    if (full) m = (1u << G) - 1u;
+                    const bool sel = (wb + r * 32 + lane < w1) && p < Mu[r] && m != 0;
+                    unsigned bal = __ballot_sync(0xffffffffu, sel);
+                    while (bal) {
+                        const int src = __ffs(bal) - 1;
+                        bal &= bal - 1;
+                        const int up = __shfl_sync(0xffffffffu, un[r], src);
+                        const int pp = __shfl_sync(0xffffffffu, p, src);
+                        const int mm = __shfl_sync(0xffffffffu, (int)m, src);
+                        if (lane == 0) {
+                            const int slot = si % NS;
+                            d_unit[slot][fill] = up; d_page[slot][fill] = pp; d_mask[slot][fill] = (uint8_t)mm;
+                            if (++fill == SP) { close_stage(SP); fill = 0; open_stage(); }
+                        }
+                    }
+                }
+            }
+        }
+        if (lane == 0) {
+            if (fill > 0) { close_stage(fill); open_stage(); }
+            close_stage(-1);
+        }
+        return;
+    }
+    // ---------------------------------------------------- consumers
+    const int l16 = threadIdx.x & 15, hw = threadIdx.x >> 4;
     const int hsel = rs_head<G>(lane);
     const bool writer = rs_writer<G>(lane);
-    const size_t ntok = (size_t)c.maxp * kP;
-    float *srow = scores + ((size_t)b * Hq + kvh * G + hsel) * ntok;
-    float runmax = -INFINITY;
-    const int pi_local = hw >> 1;           // page within the batch (2 half-warps per page)
+    const int pi_local = hw >> 1;           // page within the stage (2 half-warps per page)
     const int t0 = (hw & 1) * 8;            // first token of this half-warp
-    for (int bi = 0; bi < nb; ++bi) {
-        const int st = bi & 1;
-        mbar_wait(&bars[st], (bi >> 1) & 1);
-        const int n = min(BP, np - bi * BP);
+    const size_t ntok = (size_t)c.maxp * kP;
+    float qr[G][8];
+    int cur_unit = -1, L = 0;
+    float runmax = -INFINITY;
+    float *srow = nullptr;
+    auto flush = [&]() {
+        if (cur_unit >= 0 && writer && runmax > -INFINITY) {
+            const int bb = cur_unit / c.Hkv, kh = cur_unit % c.Hkv;
+            atomicMax(rowmax + (size_t)bb * Hq + kh * G + hsel, f2key(runmax));
+        }
+        runmax = -INFINITY;
+    };
+    for (int si = 0;; ++si) {
+        const int slot = si % NS;
+        mbar_wait(&fullb[slot], (si / NS) & 1);
+        const int n = d_n[slot];
+        if (n < 0) break;
+        // both half-warps of a warp share pi_local's parity bit only; keep the warp converged
         const bool active = pi_local < n;
-        const int pidx = bi * BP + (active ? pi_local : 0);
-        const int page = s_pages[pidx];
-        const bool hok = active && ((s_mask[pidx] >> hsel) & 1);
-        const T *tile = reinterpret_cast<const T *>(smem + ((size_t)st * BP + (active ? pi_local : 0)) * TILE);
+        const int unit = d_unit[slot][active ? pi_local : 0];
+        if (active && unit != cur_unit) {
+            flush();
+            cur_unit = unit;
+            const int bb = unit / c.Hkv, kh = unit % c.Hkv;
+            L = c.seq_lens[bb];
+#pragma unroll
+            for (int g = 0; g < G; ++g) Elem<T>::load8(q + ((size_t)bb * Hq + kh * G + g) * kD + 8 * l16, qr[g]);
+            srow = scores + ((size_t)bb * Hq + kh * G + hsel) * ntok;
+        }
+        if (active) {
+            const int page = d_page[slot][pi_local];
+            const bool hok = (d_mask[slot][pi_local] >> hsel) & 1;
+            const T *tile = reinterpret_cast<const T *>(smem + ((size_t)slot * SP + pi_local) * TILE);
 #pragma unroll 4
-        for (int tt = 0; tt < 8; ++tt) {
-            const int t = t0 + tt;
-            float kx[8];
-            Elem<T>::load8(tile + t * kD + 8 * l16, kx);
-            float acc[G];
+            for (int tt = 0; tt < 8; ++tt) {
+                const int t = t0 + tt;
+                float kx[8];
+                Elem<T>::load8(tile + t * kD + 8 * l16, kx);
+                float acc[G];
 #pragma unroll
-            for (int g = 0; g < G; ++g) {
-                float a = 0.0f;
+                for (int g = 0; g < G; ++g) {
+                    float a = 0.0f;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) a = __fmaf_rn(qr[g][e], kx[e], a);
-                acc[g] = a;
-            }
-            const float s = __fmul_rn(rs_reduce16<G>(acc, lane), kCd);
-            const int tok = page * kP + t;
-            if (writer && hok) {
-                const float v = tok < L ? s : -INFINITY;
-                srow[tok] = v;
-                runmax = fmaxf(runmax, v);
+                    for (int e = 0; e < 8; ++e) a = __fmaf_rn(qr[g][e], kx[e], a);
+                    acc[g] = a;
+                }
+                const float s = __fmul_rn(rs_reduce16<G>(acc, lane), kCd);
+                const int tok = page * kP + t;
+                if (writer && hok) {
+                    const float v = tok < L ? s : -INFINITY;
+                    srow[tok] = v;
+                    runmax = fmaxf(runmax, v);
+                }
             }
         }
-        __syncthreads();                     // everyone is done with stage st
-        if (tid == 0 && bi + 2 < nb) issue(bi + 2);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyb[slot]);
     }
-    // per-head max -> rowmax (one atomic per CTA and head)
-    if (writer) s_max[hw][hsel] = f2key(runmax);
-    __syncthreads();
-    if (tid < G) {
-        uint32_t m = 0u;
-        for (int w = 0; w < 16; ++w) m = max(m, s_max[w][tid]);
-        // -inf (key 0x007fffff) never beats an empty row's 0 sentinel... only real scores count
-        if (m > f2key(-INFINITY)) atomicMax(rowmax + (size_t)b * Hq + kvh * G + tid, m);
-    }
+    flush();
 }
 
 // ============================================================================ candidates
@@ -372,11 +419,17 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
             return;
         }
     } else {
-        // thread ch copies chunk ch to its prefix offset (chunk counts are small)
-        if (threadIdx.x < A.nch) {
-            const size_t g0 = (size_t)threadIdx.x * kCpc;
-            for (int k = 0; k < ccnt; ++k)
-                ck[coff + k] = ((unsigned long long)(uint32_t)gj[g0 + k] << 32) | __float_as_uint(gs[g0 + k]);
+        // concatenate the chunk regions in order: chunk offsets/counts via shared memory,
+        // then every thread copies a strided share of each chunk (independent loads)
+        int *s_cnt = reinterpret_cast<int *>(cin);            // cin is free until the support pass
+        int *s_off = s_cnt + 256;
+        if (threadIdx.x < A.nch) { s_cnt[threadIdx.x] = ccnt; s_off[threadIdx.x] = coff; }
+        __syncthreads();
+        for (int ch = 0; ch < A.nch; ++ch) {
+            const int cc = s_cnt[ch], co = s_off[ch];
+            const size_t g0 = (size_t)ch * kCpc;
+            for (int k = threadIdx.x; k < cc; k += NT)
+                ck[co + k] = ((unsigned long long)(uint32_t)__ldg(gj + g0 + k) << 32) | __float_as_uint(__ldg(gs + g0 + k));
         }
         __syncthreads();
     }
@@ -523,11 +576,20 @@ __global__ void __launch_bounds__(256) k_delta_bar(const float *__restrict__ box
     double db = 0.0, dz = 0.0;
     const float *bx = box + (size_t)row * maxp;
     if (t == t) {   // tau is NaN for an empty row
-#pragma unroll 4
-        for (int i = threadIdx.x; i < kDbChunk; i += 256) {
+        // fp32 pre-test: a*box - tau > 0 needs box > tau/a; thr is rounded well below it
+        const float thr = (float)(t / a) - 1e-3f * fmaxf(1.0f, fabsf((float)(t / a)));
+        float bv[kDbChunk / 256];
+#pragma unroll
+        for (int r = 0; r < kDbChunk / 256; ++r) {
+            const int p = p0 + threadIdx.x + 256 * r;
+            bv[r] = p < M ? __ldg(bx + p) : -INFINITY;
+        }
+#pragma unroll
+        for (int r = 0; r < kDbChunk / 256; ++r) {
+            const int i = threadIdx.x + 256 * r;
             const int p = p0 + i;
-            if (p >= M || ((bits[i >> 5] >> (i & 31)) & 1u)) continue;
-            const double d = a * (double)__ldg(bx + p) - t;
+            if (!(bv[r] > thr) || ((bits[i >> 5] >> (i & 31)) & 1u)) continue;
+            const double d = a * (double)bv[r] - t;
             if (d > 0.0) db += (double)min(kP, L - p * kP) * powb(d, beta, ib);
         }
     }

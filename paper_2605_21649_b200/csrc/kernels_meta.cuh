@@ -112,51 +112,71 @@ template <int MODES> struct ScoreCfg {
     static constexpr int NS = 3;                        // ring stages
 };
 
-// Persistent: CTA k owns the contiguous page range [k*M/grid, (k+1)*M/grid) of every
-// sequence (grid.y = batch); stages of SP pages flow through an NS-deep ring.
+// Persistent, warp-specialised (288 threads = 8 consumer warps + 1 producer warp): the
+// flattened (b, page) space is split into equal contiguous ranges, one per CTA; the
+// producer streams the range's metadata through an NS-deep ring of SP-page stages
+// (full/empty mbarriers, no CTA-wide barrier in the loop).
 template <typename T, int G, int MODES>
-__global__ void __launch_bounds__(256, 2) k_score(CacheView c, const T *__restrict__ q, int Hq,
+__global__ void __launch_bounds__(288, 2) k_score(CacheView c, const T *__restrict__ q, int Hq,
                                                    float *__restrict__ box, float *__restrict__ mu,
                                                    float *__restrict__ sigma2) {
     constexpr int SP = ScoreCfg<MODES>::SP, NS = ScoreCfg<MODES>::NS;
+    constexpr int NCW = 8;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ uint64_t bars[NS];
-    const int b = blockIdx.y;
-    const int L = c.seq_lens[b];
-    const int M = n_pages_of(L);
-    const int pa = (int)(((long long)M * blockIdx.x) / gridDim.x);
-    const int pz = (int)(((long long)M * (blockIdx.x + 1)) / gridDim.x);
-    if (pa >= pz) return;
-    const int nst = (pz - pa + SP - 1) / SP;
+    __shared__ uint64_t fullb[NS], emptyb[NS];
+    __shared__ int d_b[NS], d_p0[NS], d_n[NS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long total = (long long)c.B * c.maxp;
+    const long long r0 = total * blockIdx.x / gridDim.x, r1 = total * (blockIdx.x + 1) / gridDim.x;
     const int HD = c.Hkv * kD;
     const uint32_t bmm = (uint32_t)(HD * sizeof(T));          // kmin / kmax block bytes
     const uint32_t bgs = (uint32_t)(HD * sizeof(float));      // kavg / kvar block bytes
     const uint32_t per_page = ((MODES & 1) ? 2 * bmm : 0) + ((MODES & 2) ? 2 * bgs : 0);
-    auto issue = [&](int si) {
-        const int slot = si % NS;
-        const int q0 = pa + si * SP;
-        const int n = min(SP, pz - q0);
-        mbar_expect_tx(&bars[slot], n * per_page);
-        for (int i = 0; i < n; ++i) {
-            const size_t phys = (size_t)__ldg(c.page_table + (size_t)b * c.maxp + q0 + i);
-            unsigned char *dst = smem + ((size_t)slot * SP + i) * per_page;
-            if (MODES & 1) {
-                bulk_g2s(dst, reinterpret_cast<const T *>(c.kmin) + phys * HD, bmm, &bars[slot]);
-                bulk_g2s(dst + bmm, reinterpret_cast<const T *>(c.kmax) + phys * HD, bmm, &bars[slot]);
-                dst += 2 * bmm;
-            }
-            if (MODES & 2) {
-                bulk_g2s(dst, c.kavg + phys * HD, bgs, &bars[slot]);
-                bulk_g2s(dst + bgs, c.kvar + phys * HD, bgs, &bars[slot]);
-            }
-        }
-    };
     if (threadIdx.x == 0) {
-        for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
+        for (int i = 0; i < NS; ++i) { mbar_init(&fullb[i], 1); mbar_init(&emptyb[i], NCW); }
         fence_mbar_init();
-        for (int si = 0; si < min(NS, nst); ++si) issue(si);
     }
-    const int lane = threadIdx.x & 31;
+    __syncthreads();
+    if (warp == NCW) {
+        // ------------------------------------------------ producer (lane 0)
+        if (lane != 0) return;
+        int si = 0;
+        long long g = r0;
+        while (true) {
+            const int slot = si % NS;
+            if (si >= NS) mbar_wait(&emptyb[slot], ((si / NS) - 1) & 1);
+            // next run of valid pages of one sequence
+            int n = 0, bb = 0, p0 = 0;
+            while (g < r1) {
+                bb = (int)(g / c.maxp);
+                p0 = (int)(g % c.maxp);
+                const int M = n_pages_of(c.seq_lens[bb]);
+                if (p0 >= M) { g = (long long)(bb + 1) * c.maxp; continue; }   // skip the sequence tail
+                n = (int)min((long long)min(SP, M - p0), r1 - g);
+                break;
+            }
+            if (n == 0) { d_n[slot] = -1; mbar_arrive(&fullb[slot]); break; }
+            d_b[slot] = bb; d_p0[slot] = p0; d_n[slot] = n;
+            mbar_expect_tx(&fullb[slot], n * per_page);
+            for (int i = 0; i < n; ++i) {
+                const size_t phys = (size_t)__ldg(c.page_table + (size_t)bb * c.maxp + p0 + i);
+                unsigned char *dst = smem + ((size_t)slot * SP + i) * per_page;
+                if (MODES & 1) {
+                    bulk_g2s(dst, reinterpret_cast<const T *>(c.kmin) + phys * HD, bmm, &fullb[slot]);
+                    bulk_g2s(dst + bmm, reinterpret_cast<const T *>(c.kmax) + phys * HD, bmm, &fullb[slot]);
+                    dst += 2 * bmm;
+                }
+                if (MODES & 2) {
+                    bulk_g2s(dst, c.kavg + phys * HD, bgs, &fullb[slot]);
+                    bulk_g2s(dst + bgs, c.kvar + phys * HD, bgs, &fullb[slot]);
+                }
+            }
+            g += n;
+            ++si;
+        }
+        return;
+    }
+    // ---------------------------------------------------- consumers
     const int l16 = threadIdx.x & 15;
     const int hw = threadIdx.x >> 4;
     const int hwpk = 16 / c.Hkv;
@@ -164,38 +184,42 @@ __global__ void __launch_bounds__(256, 2) k_score(CacheView c, const T *__restri
     const int hq0 = kvh * G;
     constexpr int GP = (G + 1) / 2;          // head pairs
     float2 qp[GP][8], qn[GP][8], qa[GP][8], q2[GP][8];
-#pragma unroll
-    for (int g = 0; g < GP; ++g) {
-        float x0[8], x1[8];
-        Elem<T>::load8(q + ((size_t)b * Hq + hq0 + 2 * g) * kD + 8 * l16, x0);
-        if (2 * g + 1 < G) Elem<T>::load8(q + ((size_t)b * Hq + hq0 + 2 * g + 1) * kD + 8 * l16, x1);
-        else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) x1[i] = 0.0f;
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            if (MODES & 1) {
-                qp[g][i] = make_float2(x0[i] >= 0.0f ? x0[i] : 0.0f, x1[i] >= 0.0f ? x1[i] : 0.0f);
-                qn[g][i] = make_float2(x0[i] >= 0.0f ? 0.0f : x0[i], x1[i] >= 0.0f ? 0.0f : x1[i]);
-            }
-            if (MODES & 2) {
-                qa[g][i] = make_float2(x0[i], x1[i]);
-                q2[g][i] = make_float2(__fmul_rn(x0[i], x0[i]), __fmul_rn(x1[i], x1[i]));
-            }
-        }
-    }
-    __syncthreads();                         // mbarrier inits visible
     const int h_out = hq0 + rs_head<G>(lane);
     const bool writer = rs_writer<G>(lane);
-    float *box_row = box + ((size_t)b * Hq + h_out) * c.maxp;
-    float *mu_row = mu + ((size_t)b * Hq + h_out) * c.maxp;
-    float *s2_row = sigma2 + ((size_t)b * Hq + h_out) * c.maxp;
-    for (int si = 0; si < nst; ++si) {
+    int cur_b = -1;
+    for (int si = 0;; ++si) {
         const int slot = si % NS;
-        mbar_wait(&bars[slot], (si / NS) & 1);
-        const int q0 = pa + si * SP;
-        const int n = min(SP, pz - q0);
+        mbar_wait(&fullb[slot], (si / NS) & 1);
+        const int n = d_n[slot];
+        if (n < 0) break;
+        const int bb = d_b[slot], q0 = d_p0[slot];
+        if (bb != cur_b) {
+            cur_b = bb;
+#pragma unroll
+            for (int g = 0; g < GP; ++g) {
+                float x0[8], x1[8];
+                Elem<T>::load8(q + ((size_t)bb * Hq + hq0 + 2 * g) * kD + 8 * l16, x0);
+                if (2 * g + 1 < G) Elem<T>::load8(q + ((size_t)bb * Hq + hq0 + 2 * g + 1) * kD + 8 * l16, x1);
+                else {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) x1[i] = 0.0f;
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (MODES & 1) {
+                        qp[g][i] = make_float2(x0[i] >= 0.0f ? x0[i] : 0.0f, x1[i] >= 0.0f ? x1[i] : 0.0f);
+                        qn[g][i] = make_float2(x0[i] >= 0.0f ? 0.0f : x0[i], x1[i] >= 0.0f ? 0.0f : x1[i]);
+                    }
+                    if (MODES & 2) {
+                        qa[g][i] = make_float2(x0[i], x1[i]);
+                        q2[g][i] = make_float2(__fmul_rn(x0[i], x0[i]), __fmul_rn(x1[i], x1[i]));
+                    }
+                }
+            }
+        }
+        float *box_row = box + ((size_t)bb * Hq + h_out) * c.maxp;
+        float *mu_row = mu + ((size_t)bb * Hq + h_out) * c.maxp;
+        float *s2_row = sigma2 + ((size_t)bb * Hq + h_out) * c.maxp;
         // warp-uniform trip count: both half-warps of a warp run the same iterations
         for (int ib = 0; ib < n; ib += hwpk) {
             const int i = ib + sub;
@@ -243,8 +267,8 @@ __global__ void __launch_bounds__(256, 2) k_score(CacheView c, const T *__restri
                 if (writer && valid) { mu_row[p] = rm; s2_row[p] = rs; }
             }
         }
-        __syncthreads();                     // stage consumed by every warp
-        if (threadIdx.x == 0 && si + NS < nst) issue(si + NS);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyb[slot]);
     }
 }
 

@@ -56,19 +56,31 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
             for (int e = 0; e < 4; ++e) kk[e] = (i4 + e < M) ? f2key(__ldg(x + i4 + e)) : 0u;
         }
     };
-    // 1. partition maxima (4 float4 loads in flight per thread)
+    // 1. partition maxima: thread t owns the float4 groups {t + NT*j}; the max of each
+    //    group is kept (fp32 max == key max: f2key is monotone) for the second pass.
+    constexpr int GPT = 16;                  // groups per thread (M <= 16 * 4 * NT)
+    float gmax[GPT];
     uint32_t mt = 0u;
-    for (int base = 0; base < M; base += 16 * NT) {
-        uint32_t kk[4][4];
+#pragma unroll
+    for (int j0 = 0; j0 < GPT; j0 += 4) {
+        float4 v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int i4 = base + 4 * (threadIdx.x + u * NT);
-            if (i4 < M) key4(i4, kk[u]);
-            else { kk[u][0] = kk[u][1] = kk[u][2] = kk[u][3] = 0u; }
+            const int i4 = 4 * (threadIdx.x + (j0 + u) * NT);
+            if (vec && i4 + 3 < M) v[u] = __ldg(reinterpret_cast<const float4 *>(x + i4));
+            else {
+                v[u].x = (i4 < M) ? __ldg(x + i4) : -INFINITY;
+                v[u].y = (i4 + 1 < M) ? __ldg(x + i4 + 1) : -INFINITY;
+                v[u].z = (i4 + 2 < M) ? __ldg(x + i4 + 2) : -INFINITY;
+                v[u].w = (i4 + 3 < M) ? __ldg(x + i4 + 3) : -INFINITY;
+            }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-            mt = max(mt, max(max(kk[u][0], kk[u][1]), max(kk[u][2], kk[u][3])));
+        for (int u = 0; u < 4; ++u) {
+            const int i4 = 4 * (threadIdx.x + (j0 + u) * NT);
+            gmax[j0 + u] = (i4 < M) ? fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)) : NAN;
+            if (i4 < M) mt = max(mt, f2key(gmax[j0 + u]));
+        }
     }
     __syncthreads();
     uint32_t Lb = 1u;
@@ -80,30 +92,23 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
         }
         Lb = T > 1u ? T : 1u;
     }
-    // 2. candidates (second pass, same access pattern)
-    for (int base = 0; base < M; base += 16 * NT) {
-        uint32_t kk[4][4];
+    // 2. candidates: only groups whose max reaches L are re-read
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int i4 = base + 4 * (threadIdx.x + u * NT);
-            if (i4 < M) key4(i4, kk[u]);
-            else { kk[u][0] = kk[u][1] = kk[u][2] = kk[u][3] = 0u; }
-        }
+    for (int j = 0; j < GPT; ++j) {
+        const int i4 = 4 * (threadIdx.x + j * NT);
+        const bool hit = (i4 < M) && f2key(gmax[j]) >= Lb;
+        if (__ballot_sync(0xffffffffu, hit) == 0u) continue;
+        uint32_t kk[4] = {0u, 0u, 0u, 0u};
+        if (hit) key4(i4, kk);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const bool c = kk[u][e] >= Lb;
-                const unsigned m = __ballot_sync(0xffffffffu, c);
-                if (!m) continue;
-                int pos = 0;
-                if ((threadIdx.x & 31) == 0) pos = atomicAdd(&s_cnt, __popc(m));
-                pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(m & ((1u << (threadIdx.x & 31)) - 1u));
-                if (c && pos < kTopkCap) {
-                    ckey[pos] = kk[u][e];
-                    cidx[pos] = base + 4 * (threadIdx.x + u * NT) + e;
-                }
-            }
+        for (int e = 0; e < 4; ++e) {
+            const bool c = hit && kk[e] >= Lb;
+            const unsigned m = __ballot_sync(0xffffffffu, c);
+            if (!m) continue;
+            int pos = 0;
+            if ((threadIdx.x & 31) == 0) pos = atomicAdd(&s_cnt, __popc(m));
+            pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(m & ((1u << (threadIdx.x & 31)) - 1u));
+            if (c && pos < kTopkCap) { ckey[pos] = kk[e]; cidx[pos] = i4 + e; }
         }
     }
     __syncthreads();
