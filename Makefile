@@ -3,7 +3,7 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 CSRC := paper_2605_21649_b200/csrc
 LIB := paper_2605_21649_b200/libentmaxkv.so
-NVFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -shared -Iinclude -I$(CSRC) --expt-relaxed-constexpr -Xptxas -v
+NVFLAGS := $(EXTRA) -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -shared -Iinclude -I$(CSRC) --expt-relaxed-constexpr -Xptxas -v
 
 all: $(LIB) oracle/liboracle.so
 

@@ -315,3 +315,29 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 }  // namespace ekv
+
+// ---------------------------------------------------------------- optional in-kernel phase stamps
+// Built with -DEKV_STAMPS: block 0 / thread 0 of an instrumented kernel writes %globaltimer
+// (ns) at checkpoints into ekv_stamps[kernel_slot][i]; read with entmaxkv_debug_stamps().
+namespace ekv {
+#ifdef EKV_STAMPS
+__device__ unsigned long long ekv_stamps[8][32];
+__device__ __forceinline__ void stamp(int k, int i) {
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        ekv_stamps[k][i] = t;
+    }
+}
+__device__ __forceinline__ void stamp_if(bool cond, int k, int i) {
+    if (cond && blockIdx.x == 0 && blockIdx.y == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        ekv_stamps[k][i] = t;
+    }
+}
+#else
+__device__ __forceinline__ void stamp(int, int) {}
+__device__ __forceinline__ void stamp_if(bool, int, int) {}
+#endif
+}  // namespace ekv

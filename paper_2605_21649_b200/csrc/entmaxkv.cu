@@ -87,7 +87,8 @@ int sel_cap(const ekv_cache *c, const ekv_select_params *s) {
 // One layout serves decode (incl. eval_exact), select, sparse_attend and full_attend.
 struct Layout {
     size_t box, mu, sigma2, page_idx, n_sel, tau_hat;
-    size_t zero, rowmax, ccount, tickets, umask, zero_bytes;   // zeroed per attention pass
+    size_t zero, rowmax, ccount, tickets, ucount, umask, zero_bytes;   // zeroed per attention pass
+    size_t ulist;
     size_t db_partial, tau_int;
     size_t scores, cand_s, cand_j, tok_list, p_list, n_list, full_out, total;
     int cap, W, list_cap;
@@ -111,8 +112,10 @@ Layout layout(const ekv_cache *c, int Hq, const ekv_select_params *sel) {
     L.rowmax = take(B * Hq * 4);
     L.ccount = take(B * Hq * (size_t)((maxp + 255) / 256) * 4);
     L.tickets = take(B * Hq * 4);
+    L.ucount = take(B * Hkv * 4);
     L.umask = take(B * Hkv * (size_t)L.W * 4);
     L.zero_bytes = o - L.zero;
+    L.ulist = take(B * Hkv * maxp * 4);
     L.scores = take(B * Hq * maxp * kP * 4);
     L.cand_s = take(B * Hq * (size_t)((maxp + 255) / 256) * kCpc * 4);
     L.cand_j = take(B * Hq * (size_t)((maxp + 255) / 256) * kCpc * 4);
@@ -195,33 +198,33 @@ ekv_status launch_topk(const float *box, int B, int Hq, int maxp, const int32_t 
 }
 
 ekv_status launch_mark(const ekv_cache *c, int Hq, const int32_t *pi, const int32_t *ns, int stride, uint32_t *um,
-                       int W, cudaStream_t st) {
-    k_mark<<<c->batch * Hq, 256, 0, st>>>(Hq, Hq / c->n_kv_heads, pi, ns, stride, um, W);
+                       int W, int32_t *ul, int32_t *uc, int ucap, cudaStream_t st) {
+    k_mark<<<c->batch * Hq, 256, 0, st>>>(Hq, Hq / c->n_kv_heads, pi, ns, stride, um, W, ul, uc, ucap);
     return check_launch("k_mark");
 }
 
 template <typename T, int G>
-ekv_status launch_scores_t(const CacheView &v, const void *q, int Hq, const uint32_t *um, int W, float *scores,
-                           uint32_t *rowmax, int full, cudaStream_t st) {
+ekv_status launch_scores_t(const CacheView &v, const void *q, int Hq, const uint32_t *um, int W, const int32_t *ul,
+                           const int32_t *uc, int ucap, float *scores, uint32_t *rowmax, int full, cudaStream_t st) {
     constexpr int smem = AttCfg<T>::SMEM;
     static bool init = false;
     if (!init) { set_smem(k_attend_scores<T, G>, smem); init = true; }
     const int per_sm = sizeof(T) == 2 ? 2 : 1;
-    long long gx = ((long long)v.B * v.Hkv * ((v.maxp + 3) / 4) + 15) / 16;   // >= 64 page slots per CTA
+    long long gx = ((long long)v.B * v.Hkv * ucap + 31) / 32;     // >= 32 work slots per CTA
     if (gx > per_sm * num_sms()) gx = per_sm * num_sms();
     if (gx < 1) gx = 1;
-    k_attend_scores<T, G><<<(unsigned)gx, 288, smem, st>>>(v, static_cast<const T *>(q), Hq, um, W, scores, rowmax,
-                                                           full);
+    k_attend_scores<T, G><<<(unsigned)gx, 288, smem, st>>>(v, static_cast<const T *>(q), Hq, um, W, ul, uc, ucap,
+                                                           scores, rowmax, full);
     return check_launch("k_attend_scores");
 }
 template <typename T>
-ekv_status launch_scores(const CacheView &v, const void *q, int Hq, const uint32_t *um, int W, float *scores,
-                         uint32_t *rowmax, int full, cudaStream_t st) {
+ekv_status launch_scores(const CacheView &v, const void *q, int Hq, const uint32_t *um, int W, const int32_t *ul,
+                         const int32_t *uc, int ucap, float *scores, uint32_t *rowmax, int full, cudaStream_t st) {
     switch (Hq / v.Hkv) {
-    case 1: return launch_scores_t<T, 1>(v, q, Hq, um, W, scores, rowmax, full, st);
-    case 2: return launch_scores_t<T, 2>(v, q, Hq, um, W, scores, rowmax, full, st);
-    case 4: return launch_scores_t<T, 4>(v, q, Hq, um, W, scores, rowmax, full, st);
-    default: return launch_scores_t<T, 8>(v, q, Hq, um, W, scores, rowmax, full, st);
+    case 1: return launch_scores_t<T, 1>(v, q, Hq, um, W, ul, uc, ucap, scores, rowmax, full, st);
+    case 2: return launch_scores_t<T, 2>(v, q, Hq, um, W, ul, uc, ucap, scores, rowmax, full, st);
+    case 4: return launch_scores_t<T, 4>(v, q, Hq, um, W, ul, uc, ucap, scores, rowmax, full, st);
+    default: return launch_scores_t<T, 8>(v, q, Hq, um, W, ul, uc, ucap, scores, rowmax, full, st);
     }
 }
 
@@ -271,9 +274,16 @@ ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t 
     float *scores = at<float>(ws, L.scores);
     if (cudaMemsetAsync(at<char>(ws, L.zero), 0, L.zero_bytes, st) != cudaSuccess)
         return fail(EKV_ERR_CUDA, "memset: %s", cudaGetErrorString(cudaGetLastError()));
-    if (!full) EKV_TRY(launch_mark(c, Hq, pi, ns, stride, um, L.W, st));
-    if (c->dtype == EKV_BF16) EKV_TRY(launch_scores<__nv_bfloat16>(v, q, Hq, um, L.W, scores, rowmax, full, st));
-    else EKV_TRY(launch_scores<float>(v, q, Hq, um, L.W, scores, rowmax, full, st));
+    int32_t *ul = at<int32_t>(ws, L.ulist);
+    int32_t *uc = at<int32_t>(ws, L.ucount);
+    // union capacity per KV group: min(G * list stride, max_pages); full: every page
+    const int G = Hq / c->n_kv_heads;
+    const long long uc_ll = (long long)G * stride;
+    const int ucap = full ? c->max_pages_per_seq : (int)(uc_ll < c->max_pages_per_seq ? uc_ll : c->max_pages_per_seq);
+    if (!full) EKV_TRY(launch_mark(c, Hq, pi, ns, stride, um, L.W, ul, uc, ucap, st));
+    if (c->dtype == EKV_BF16)
+        EKV_TRY(launch_scores<__nv_bfloat16>(v, q, Hq, um, L.W, ul, uc, ucap, scores, rowmax, full, st));
+    else EKV_TRY(launch_scores<float>(v, q, Hq, um, L.W, ul, uc, ucap, scores, rowmax, full, st));
     const int rows = c->batch * Hq;
     const size_t ntok = (size_t)c->max_pages_per_seq * kP;
     float *cs = at<float>(ws, L.cand_s);
@@ -303,6 +313,19 @@ extern "C" {
 const char *entmaxkv_last_error(void) { return g_err; }
 const char *entmaxkv_version(void) { return "entmaxkv-b200 0.1 (sm_100a)"; }
 int32_t entmaxkv_last_launch_count(void) { return g_launches; }
+
+/* Debug (not in the public header): copy in-kernel phase stamps (ns) and the last top-k
+ * candidate count; returns 0 when the library was built without -DEKV_STAMPS. */
+int entmaxkv_debug_stamps(unsigned long long *out /*[8*32]*/, int *nc) {
+#ifdef EKV_STAMPS
+    cudaMemcpyFromSymbol(out, ekv_stamps, sizeof(unsigned long long) * 8 * 32);
+    cudaMemcpyFromSymbol(nc, ekv_dbg_nc, sizeof(int));
+    return 1;
+#else
+    (void)out; (void)nc;
+    return 0;
+#endif
+}
 
 size_t entmaxkv_workspace_size(const ekv_cache *cache, int32_t n_q_heads, const ekv_select_params *sel) {
     if (check_cache(cache, n_q_heads) != EKV_OK) return 0;

@@ -35,18 +35,23 @@ template <typename T> struct AttCfg {
 template <typename T, int G>
 __global__ void __launch_bounds__(288) k_attend_scores(CacheView c, const T *__restrict__ q, int Hq,
                                                        const uint32_t *__restrict__ umask, int W,
+                                                       const int32_t *__restrict__ ulist,
+                                                       const int32_t *__restrict__ ucount, int ucap,
                                                        float *__restrict__ scores, uint32_t *__restrict__ rowmax,
                                                        int full) {
     constexpr int SP = AttCfg<T>::SP, NS = AttCfg<T>::NS, TILE = AttCfg<T>::TILE;
     constexpr int NCW = 8;
+    constexpr int CHK = 256;                // list entries per producer chunk (8 per lane)
     extern __shared__ __align__(128) unsigned char smem[];   // [NS][SP][TILE]
     __shared__ uint64_t fullb[NS], emptyb[NS];
-    __shared__ int d_page[NS][SP], d_unit[NS][SP], d_n[NS];
+    __shared__ int d_page[NS][SP], d_unit[NS][SP], d_phys[NS][SP], d_n[NS];
     __shared__ uint8_t d_mask[NS][SP];
+    __shared__ int l_unit[CHK], l_page[CHK], l_phys[CHK];
+    __shared__ uint8_t l_mask[CHK];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // flattened mask-word space (unit, word of 4 pages): one contiguous range per CTA
-    const long long W4 = (long long)c.B * c.Hkv * W;
-    const long long w0 = W4 * blockIdx.x / gridDim.x, w1 = W4 * (blockIdx.x + 1) / gridDim.x;
+    // flattened work space: (unit, slot), slot < ucap (sparse: union-list slots; full: pages)
+    const long long tot = (long long)c.B * c.Hkv * ucap;
+    const long long f0 = tot * blockIdx.x / gridDim.x, f1 = tot * (blockIdx.x + 1) / gridDim.x;
     if (threadIdx.x == 0) {
         for (int i = 0; i < NS; ++i) { mbar_init(&fullb[i], 1); mbar_init(&emptyb[i], NCW); }
         fence_mbar_init();
@@ -54,139 +59,177 @@ __global__ void __launch_bounds__(288) k_attend_scores(CacheView c, const T *__r
     __syncthreads();
     if (warp == NCW) {
         // ------------------------------------------------ producer
+        // Chunks of 256 work slots: 8 independent loads per lane (list entry / page), then
+        // the page-table and mask lookups in parallel, ballot compaction into a shared
+        // list, and lane 0 packs the list into ring stages of SP page tiles (TMA).
         const unsigned char *Kb = reinterpret_cast<const unsigned char *>(c.K);
         int si = 0, fill = 0;
-        auto open_stage = [&]() {
-            const int slot = si % NS;
-            if (si >= NS) mbar_wait(&emptyb[slot], ((si / NS) - 1) & 1);
-        };
-        auto close_stage = [&](int n) {           // lane 0 only
-            const int slot = si % NS;
-            d_n[slot] = n;
-            if (n > 0) {
-                mbar_expect_tx(&fullb[slot], (uint32_t)(n * TILE));
-                for (int i = 0; i < n; ++i) {
-                    const int u = d_unit[slot][i], bb = u / c.Hkv, kh = u % c.Hkv;
-                    const int phys = __ldg(c.page_table + (size_t)bb * c.maxp + d_page[slot][i]);
-                    bulk_g2s(smem + ((size_t)slot * SP + i) * TILE, Kb + ((size_t)phys * c.Hkv + kh) * TILE,
-                             TILE, &fullb[slot]);
-                }
-            } else {
-                mbar_arrive(&fullb[slot]);
-            }
-            ++si;
-        };
-        if (lane == 0) open_stage();
-        // scan the range one mask word (4 pages) per lane, 4 words in flight per lane
-        for (long long wb = w0; wb < w1; wb += 128) {
-            uint32_t wv[4];
-            int un[4], wj[4], Mu[4];
+        stamp_if(lane == 0, 2, 0);
+        int cu = (int)(f0 / ucap), cs = (int)(f0 % ucap);   // (unit, slot) of the chunk start
+        for (long long cb = f0; cb < f1; cb += CHK) {
+            int un[CHK / 32], pg[CHK / 32];
+            bool ok[CHK / 32];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const long long wi = wb + r * 32 + lane;
-                wv[r] = 0u; un[r] = 0; wj[r] = 0; Mu[r] = 0;
-                if (wi < w1) {
-                    un[r] = (int)(wi / W);
-                    wj[r] = (int)(wi % W);
-                    Mu[r] = n_pages_of(__ldg(c.seq_lens + un[r] / c.Hkv));
-                    wv[r] = full ? 0xffffffffu : __ldg(umask + (size_t)un[r] * W + wj[r]);
+            for (int r = 0; r < CHK / 32; ++r) {
+                int u = cu, sl = cs + r * 32 + lane;
+                while (sl >= ucap) { sl -= ucap; ++u; }
+                un[r] = u;
+                ok[r] = false;
+                pg[r] = 0;
+                if (cb + r * 32 + lane < f1) {
+                    const int M = n_pages_of(__ldg(c.seq_lens + u / c.Hkv));
+                    if (full) { pg[r] = sl; ok[r] = sl < M; }
+                    else if (sl < __ldg(ucount + u)) { pg[r] = __ldg(ulist + (size_t)u * ucap + sl); ok[r] = true; }
                 }
             }
+            cs += CHK;
+            while (cs >= ucap) { cs -= ucap; ++cu; }
+            int ph[CHK / 32];
+            uint8_t mk[CHK / 32];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
+            for (int r = 0; r < CHK / 32; ++r) {
+                ph[r] = 0; mk[r] = 0;
+                if (ok[r]) {
+                    ph[r] = __ldg(c.page_table + (size_t)(un[r] / c.Hkv) * c.maxp + pg[r]);
+                    mk[r] = full ? (uint8_t)((1u << G) - 1u)
+                                 : (uint8_t)((__ldg(umask + (size_t)un[r] * W + (pg[r] >> 2)) >> ((pg[r] & 3) * 8)) & 0xffu);
+                }
+            }
+            int nl = 0;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int p = 4 * wj[r] + j;
-                    uint32_t m = (wv[r] >> (8 * j)) & 0xffu;
-                    if (full) m = (1u << G) - 1u;
-                    const bool sel = (wb + r * 32 + lane < w1) && p < Mu[r] && m != 0;
-                    unsigned bal = __ballot_sync(0xffffffffu, sel);
-                    while (bal) {
-                        const int src = __ffs(bal) - 1;
-                        bal &= bal - 1;
-                        const int up = __shfl_sync(0xffffffffu, un[r], src);
-                        const int pp = __shfl_sync(0xffffffffu, p, src);
-                        const int mm = __shfl_sync(0xffffffffu, (int)m, src);
-                        if (lane == 0) {
-                            const int slot = si % NS;
-                            d_unit[slot][fill] = up; d_page[slot][fill] = pp; d_mask[slot][fill] = (uint8_t)mm;
-                            if (++fill == SP) { close_stage(SP); fill = 0; open_stage(); }
-                        }
+            for (int r = 0; r < CHK / 32; ++r) {
+                const unsigned bal = __ballot_sync(0xffffffffu, ok[r]);
+                if (ok[r]) {
+                    const int pos = nl + __popc(bal & ((1u << lane) - 1u));
+                    l_unit[pos] = un[r]; l_page[pos] = pg[r]; l_phys[pos] = ph[r]; l_mask[pos] = mk[r];
+                }
+                nl += __popc(bal);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                for (int i = 0; i < nl; ++i) {
+                    const int slot = si % NS;
+                    if (fill == 0 && si >= NS) mbar_wait(&emptyb[slot], ((si / NS) - 1) & 1);
+                    d_unit[slot][fill] = l_unit[i]; d_page[slot][fill] = l_page[i];
+                    d_mask[slot][fill] = l_mask[i]; d_phys[slot][fill] = l_phys[i];
+                    if (++fill == SP) {
+                        d_n[slot] = SP;
+                        mbar_expect_tx(&fullb[slot], (uint32_t)(SP * TILE));
+                        for (int k = 0; k < SP; ++k)
+                            bulk_g2s(smem + ((size_t)slot * SP + k) * TILE,
+                                     Kb + ((size_t)d_phys[slot][k] * c.Hkv + d_unit[slot][k] % c.Hkv) * TILE, TILE,
+                                     &fullb[slot]);
+                        ++si;
+                        fill = 0;
                     }
                 }
             }
+            __syncwarp();
         }
         if (lane == 0) {
-            if (fill > 0) { close_stage(fill); open_stage(); }
-            close_stage(-1);
+            if (fill > 0) {
+                const int slot = si % NS;
+                d_n[slot] = fill;
+                mbar_expect_tx(&fullb[slot], (uint32_t)(fill * TILE));
+                for (int k = 0; k < fill; ++k)
+                    bulk_g2s(smem + ((size_t)slot * SP + k) * TILE,
+                             Kb + ((size_t)d_phys[slot][k] * c.Hkv + d_unit[slot][k] % c.Hkv) * TILE, TILE,
+                             &fullb[slot]);
+                ++si;
+            }
+            const int slot = si % NS;           // end marker
+            if (si >= NS) mbar_wait(&emptyb[slot], ((si / NS) - 1) & 1);
+            d_n[slot] = -1;
+            mbar_arrive(&fullb[slot]);
         }
         return;
     }
     // ---------------------------------------------------- consumers
+    // Two tokens per iteration: the 2G partials (token-major) go through one 16-lane
+    // reduce-scatter (same pairing tree per value as rs_reduce16<G>: bit-identical).
+    constexpr int V = 2 * G;                // values reduced together
+    constexpr int GP = (G + 1) / 2;         // head pairs for FFMA2
     const int l16 = threadIdx.x & 15, hw = threadIdx.x >> 4;
-    const int hsel = rs_head<G>(lane);
-    const bool writer = rs_writer<G>(lane);
+    const int vsel = rs_head<V>(lane);
+    const int tsel = vsel / G, hsel = vsel % G;   // token (0/1) and head this lane reduces
+    const bool writer = rs_writer<V>(lane);
     const int pi_local = hw >> 1;           // page within the stage (2 half-warps per page)
     const int t0 = (hw & 1) * 8;            // first token of this half-warp
     const size_t ntok = (size_t)c.maxp * kP;
-    float qr[G][8];
+    float2 qr[GP][8];
     int cur_unit = -1, L = 0;
     float runmax = -INFINITY;
     float *srow = nullptr;
-    auto flush = [&]() {
-        if (cur_unit >= 0 && writer && runmax > -INFINITY) {
-            const int bb = cur_unit / c.Hkv, kh = cur_unit % c.Hkv;
-            atomicMax(rowmax + (size_t)bb * Hq + kh * G + hsel, f2key(runmax));
-        }
-        runmax = -INFINITY;
-    };
     for (int si = 0;; ++si) {
         const int slot = si % NS;
         mbar_wait(&fullb[slot], (si / NS) & 1);
         const int n = d_n[slot];
+        stamp_if(threadIdx.x == 0 && si < 16, 3, si);
         if (n < 0) break;
-        // both half-warps of a warp share pi_local's parity bit only; keep the warp converged
-        const bool active = pi_local < n;
+        const bool active = pi_local < n;   // warp-uniform (both half-warps share the page)
         const int unit = d_unit[slot][active ? pi_local : 0];
         if (active && unit != cur_unit) {
-            flush();
+            if (cur_unit >= 0 && writer && runmax > -INFINITY) {
+                const int bb = cur_unit / c.Hkv, kh = cur_unit % c.Hkv;
+                atomicMax(rowmax + (size_t)bb * Hq + kh * G + hsel, f2key(runmax));
+            }
+            runmax = -INFINITY;
             cur_unit = unit;
             const int bb = unit / c.Hkv, kh = unit % c.Hkv;
             L = c.seq_lens[bb];
 #pragma unroll
-            for (int g = 0; g < G; ++g) Elem<T>::load8(q + ((size_t)bb * Hq + kh * G + g) * kD + 8 * l16, qr[g]);
+            for (int g = 0; g < GP; ++g) {
+                float x0[8], x1[8];
+                Elem<T>::load8(q + ((size_t)bb * Hq + kh * G + 2 * g) * kD + 8 * l16, x0);
+                if (2 * g + 1 < G) Elem<T>::load8(q + ((size_t)bb * Hq + kh * G + 2 * g + 1) * kD + 8 * l16, x1);
+                else {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) x1[e] = 0.0f;
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) qr[g][e] = make_float2(x0[e], x1[e]);
+            }
             srow = scores + ((size_t)bb * Hq + kh * G + hsel) * ntok;
         }
         if (active) {
             const int page = d_page[slot][pi_local];
             const bool hok = (d_mask[slot][pi_local] >> hsel) & 1;
             const T *tile = reinterpret_cast<const T *>(smem + ((size_t)slot * SP + pi_local) * TILE);
-#pragma unroll 4
-            for (int tt = 0; tt < 8; ++tt) {
-                const int t = t0 + tt;
-                float kx[8];
-                Elem<T>::load8(tile + t * kD + 8 * l16, kx);
-                float acc[G];
+#pragma unroll 2
+            for (int tt = 0; tt < 8; tt += 2) {
+                const int ta = t0 + tt;
+                float ka[8], kb[8];
+                Elem<T>::load8(tile + ta * kD + 8 * l16, ka);
+                Elem<T>::load8(tile + (ta + 1) * kD + 8 * l16, kb);
+                float acc[V];
 #pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    float a = 0.0f;
+                for (int g = 0; g < GP; ++g) {
+                    float2 a2 = make_float2(0.0f, 0.0f), b2 = make_float2(0.0f, 0.0f);
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) a = __fmaf_rn(qr[g][e], kx[e], a);
-                    acc[g] = a;
+                    for (int e = 0; e < 8; ++e) {
+                        a2 = ffma2(qr[g][e], ka[e], a2);
+                        b2 = ffma2(qr[g][e], kb[e], b2);
+                    }
+                    acc[2 * g] = a2.x; acc[G + 2 * g] = b2.x;
+                    if (2 * g + 1 < G) { acc[2 * g + 1] = a2.y; acc[G + 2 * g + 1] = b2.y; }
                 }
-                const float s = __fmul_rn(rs_reduce16<G>(acc, lane), kCd);
-                const int tok = page * kP + t;
+                const float sres = __fmul_rn(rs_reduce16<V>(acc, lane), kCd);
+                const int tok = page * kP + ta + tsel;
                 if (writer && hok) {
-                    const float v = tok < L ? s : -INFINITY;
+                    const float v = tok < L ? sres : -INFINITY;
                     srow[tok] = v;
                     runmax = fmaxf(runmax, v);
                 }
             }
         }
         __syncwarp();
+        stamp_if(threadIdx.x == 0 && si < 16, 3, 16 + si);
         if (lane == 0) mbar_arrive(&emptyb[slot]);
     }
-    flush();
+    if (cur_unit >= 0 && writer && runmax > -INFINITY) {
+        const int bb = cur_unit / c.Hkv, kh = cur_unit % c.Hkv;
+        atomicMax(rowmax + (size_t)bb * Hq + kh * G + hsel, f2key(runmax));
+    }
 }
 
 // ============================================================================ candidates
@@ -233,6 +276,52 @@ __global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ sc
         for (int t = 0; t < kP; ++t)
             cnt += ((page * kP + t < L) && sv[t] != -INFINITY && a * (double)sv[t] > tau_lo) ? 1 : 0;
     }
+    // Local tightening: the chunk's own entmax threshold tau_c is a lower bound of tau
+    // (F_all >= F_chunk), so tokens with z <= tau_c can never be in the support.  Used when
+    // the chunk has many candidates (small alpha); Newton on ||(z - t)_+||_beta - 1 from the
+    // chunk's z_max - 1 (monotone from the left), deterministic block reductions.
+    __shared__ double shd[18];
+    __shared__ float shf[9];
+    double tcut = tau_lo;
+    int ctot = block_sum_i<256>(cnt, sh);
+    if (ctot > 64) {
+        const double beta = 1.0 / a;
+        const int ib = (fabs(beta - rint(beta)) < 1e-12 && beta <= 4.5) ? (int)rint(beta) : 0;
+        float lm = -INFINITY;
+        if (i < nlist) {
+#pragma unroll
+            for (int t = 0; t < kP; ++t) if (page * kP + t < L) lm = fmaxf(lm, sv[t]);
+        }
+        lm = block_max_f<256>(lm, shf);
+        double tc = a * (double)lm - 1.0;
+        for (int it = 0; it < 100; ++it) {
+            double F = 0.0, Fd = 0.0;
+            if (i < nlist) {
+#pragma unroll
+                for (int t = 0; t < kP; ++t) {
+                    if (page * kP + t >= L || sv[t] == -INFINITY) continue;
+                    const double d = a * (double)sv[t] - tc;
+                    if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
+                }
+            }
+            block_sum2_d<256>(F, Fd, shd);
+            if (!(Fd > 0.0)) break;
+            const double root = (ib == 1) ? F : (ib == 2) ? sqrt(F) : (ib == 4) ? sqrt(sqrt(F)) : pow(F, 1.0 / beta);
+            const double step = (root - 1.0) * F / (root * Fd);
+            tc += step;
+            if (!(fabs(step) > 1e-9 * fmax(1.0, fabs(tc)))) break;
+        }
+        tc -= 1e-7 * fmax(1.0, fabs(tc));      // margin: stay below the chunk threshold
+        if (tc > tcut) {
+            tcut = tc;
+            cnt = 0;
+            if (i < nlist) {
+#pragma unroll
+                for (int t = 0; t < kP; ++t)
+                    cnt += ((page * kP + t < L) && sv[t] != -INFINITY && a * (double)sv[t] > tcut) ? 1 : 0;
+            }
+        }
+    }
     int tot;
     int pos = block_excl_scan<256>(cnt, sh, &tot);
     const size_t reg = ((size_t)row * nch + blockIdx.x) * kCpc;
@@ -240,7 +329,7 @@ __global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ sc
     if (i < nlist && cnt) {
 #pragma unroll
         for (int t = 0; t < kP; ++t) {
-            if ((page * kP + t < L) && sv[t] != -INFINITY && a * (double)sv[t] > tau_lo) {
+            if ((page * kP + t < L) && sv[t] != -INFINITY && a * (double)sv[t] > tcut) {
                 if (pos < kCpc) { cand_s[reg + pos] = sv[t]; cand_j[reg + pos] = page * kP + t; }
                 ++pos;
             }
@@ -263,7 +352,7 @@ __global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ sc
 // Overflow (more candidates than fit in shared memory): Newton streamed over the
 // global candidate list / score row brings tau_lo just below tau, then re-extract.
 constexpr int kTauNT = 256;
-constexpr int kCap = 6144;          // shared-memory candidate capacity
+constexpr int kCap = 12288;         // shared-memory candidate capacity
 
 struct TauArgs {
     const float *scores; size_t ntok;
@@ -275,7 +364,7 @@ struct TauArgs {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
+__global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
     constexpr int NT = kTauNT;
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long *ck = reinterpret_cast<unsigned long long *>(smem);   // [kCap] (j << 32 | s bits)
@@ -284,6 +373,7 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
     __shared__ int shi[NT / 32 + 1];
     __shared__ float red[NT / 32][kD];
 
+    stamp(0, 0);
     const int row = blockIdx.x;
     const int b = row / A.Hq, h = row % A.Hq, kvh = h / A.G;
     const int L = c.seq_lens[b];
@@ -320,6 +410,7 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
         chunk_ovf = ccnt > kCpc;
     }
     coff = block_excl_scan<NT>(ccnt, shi, &ncand_all);
+    stamp(0, 1);
     chunk_ovf = __syncthreads_or(chunk_ovf);
     const float *gs = A.cand_s + (size_t)row * A.nch * kCpc;
     const int32_t *gj = A.cand_j + (size_t)row * A.nch * kCpc;
@@ -365,23 +456,43 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
     double tau_lo = zmax - 1.0 - 1e-12 * fmax(1.0, fabs(zmax));
     auto zof = [&](int k) -> double { return a * (double)__uint_as_float((uint32_t)(ck[k] & 0xffffffffu)); };
 
-    // candidate source: the chunk regions concatenated in order (or, on overflow, an
-    // ordered re-extraction from the score row after a streamed Newton)
+    // candidate source (all paths produce the candidates in ascending chunk order, so the
+    // fp64 sums below have a fixed order):
+    //  (a) chunk regions concatenated in order;
+    //  (b) too many candidates for shared memory: Newton streamed over the chunk regions
+    //      (thread t <-> chunk t) moves tau_lo just below tau, then re-extract;
+    //  (c) a chunk region overflowed: the same over the score row (thread t <-> segment t).
+    int *s_cnt = reinterpret_cast<int *>(cin);            // cin is free until the support pass
+    int *s_off = s_cnt + 256;
+    if (threadIdx.x < A.nch) { s_cnt[threadIdx.x] = ccnt; s_off[threadIdx.x] = coff; }
+    __syncthreads();
     int ncand = ncand_all;
     if (ncand_all > kCap || chunk_ovf) {
         const int nlist = A.full ? n_pages_of(L) : A.n_sel[row];
         const float *srow = A.scores + (size_t)row * A.ntok;
+        const int ntk = nlist * kP;
+        const int seg = (ntk + NT - 1) / NT;              // (c): contiguous segment per thread
         double tau = tau_lo;
         for (int it = 0; it < 200; ++it) {
             double F = 0.0, Fd = 0.0;
-            for (int e = threadIdx.x; e < nlist * kP; e += NT) {
-                const int pg = A.full ? e / kP : A.page_idx[(size_t)row * A.sel_stride + e / kP];
-                const int j = pg * kP + e % kP;
-                if (j >= L) continue;
-                const float sj = srow[j];
-                if (sj == -INFINITY) continue;
-                const double d = a * (double)sj - tau;
-                if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
+            if (!chunk_ovf) {
+                if (threadIdx.x < A.nch) {
+                    const size_t g0 = (size_t)threadIdx.x * kCpc;
+                    for (int k = 0; k < ccnt; ++k) {
+                        const double d = a * (double)__ldg(gs + g0 + k) - tau;
+                        if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
+                    }
+                }
+            } else {
+                for (int e = threadIdx.x * seg; e < min(ntk, (threadIdx.x + 1) * seg); ++e) {
+                    const int pg = A.full ? e / kP : A.page_idx[(size_t)row * A.sel_stride + e / kP];
+                    const int j = pg * kP + e % kP;
+                    if (j >= L) continue;
+                    const float sj = srow[j];
+                    if (sj == -INFINITY) continue;
+                    const double d = a * (double)sj - tau;
+                    if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
+                }
             }
             block_sum2_d<NT>(F, Fd, shd);
             if (!(Fd > 0.0)) break;
@@ -391,25 +502,23 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
             if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(tau)))) break;
         }
         tau_lo = fmax(tau_lo, tau - 1e-7 * fmax(1.0, fabs(tau)));
-        int base = 0;
-        const int total_e = nlist * kP;
-        for (int r0 = 0; r0 < total_e; r0 += NT) {
-            const int e = r0 + threadIdx.x;
-            float sj = -INFINITY;
-            int j = 0;
-            if (e < total_e) {
-                const int pg = A.full ? e / kP : A.page_idx[(size_t)row * A.sel_stride + e / kP];
-                j = pg * kP + e % kP;
-                if (j < L) sj = srow[j];
+        // deterministic re-extraction: count per thread, block scan, write in order
+        int mine = 0;
+        if (!chunk_ovf) {
+            if (threadIdx.x < A.nch) {
+                const size_t g0 = (size_t)threadIdx.x * kCpc;
+                for (int k = 0; k < ccnt; ++k) mine += a * (double)__ldg(gs + g0 + k) > tau_lo;
             }
-            const int keep = (sj != -INFINITY && a * (double)sj > tau_lo) ? 1 : 0;
-            int tot;
-            const int pos = block_excl_scan<NT>(keep, shi, &tot);
-            if (keep && base + pos < kCap) ck[base + pos] = ((unsigned long long)j << 32) | __float_as_uint(sj);
-            base += tot;
+        } else {
+            for (int e = threadIdx.x * seg; e < min(ntk, (threadIdx.x + 1) * seg); ++e) {
+                const int pg = A.full ? e / kP : A.page_idx[(size_t)row * A.sel_stride + e / kP];
+                const int j = pg * kP + e % kP;
+                if (j < L && srow[j] != -INFINITY && a * (double)srow[j] > tau_lo) ++mine;
+            }
         }
-        __syncthreads();
-        ncand = base;
+        int tot;
+        int pos = block_excl_scan<NT>(mine, shi, &tot);
+        ncand = tot;
         if (ncand > kCap) {          // support larger than the shared-memory capacity
             if (threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = NAN;
             if (threadIdx.x == 0) {
@@ -418,18 +527,33 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
             }
             return;
         }
-    } else {
-        // concatenate the chunk regions in order: chunk offsets/counts via shared memory,
-        // then every thread copies a strided share of each chunk (independent loads)
-        int *s_cnt = reinterpret_cast<int *>(cin);            // cin is free until the support pass
-        int *s_off = s_cnt + 256;
-        if (threadIdx.x < A.nch) { s_cnt[threadIdx.x] = ccnt; s_off[threadIdx.x] = coff; }
+        if (!chunk_ovf) {
+            if (threadIdx.x < A.nch) {
+                const size_t g0 = (size_t)threadIdx.x * kCpc;
+                for (int k = 0; k < ccnt; ++k) {
+                    const float sj = __ldg(gs + g0 + k);
+                    if (a * (double)sj > tau_lo)
+                        ck[pos++] = ((unsigned long long)(uint32_t)__ldg(gj + g0 + k) << 32) | __float_as_uint(sj);
+                }
+            }
+        } else {
+            for (int e = threadIdx.x * seg; e < min(ntk, (threadIdx.x + 1) * seg); ++e) {
+                const int pg = A.full ? e / kP : A.page_idx[(size_t)row * A.sel_stride + e / kP];
+                const int j = pg * kP + e % kP;
+                if (j < L && srow[j] != -INFINITY && a * (double)srow[j] > tau_lo)
+                    ck[pos++] = ((unsigned long long)j << 32) | __float_as_uint(srow[j]);
+            }
+        }
         __syncthreads();
-        for (int ch = 0; ch < A.nch; ++ch) {
-            const int cc = s_cnt[ch], co = s_off[ch];
-            const size_t g0 = (size_t)ch * kCpc;
-            for (int k = threadIdx.x; k < cc; k += NT)
-                ck[co + k] = ((unsigned long long)(uint32_t)__ldg(gj + g0 + k) << 32) | __float_as_uint(__ldg(gs + g0 + k));
+    } else {
+        // (a) flattened parallel copy: element e lives in chunk ch(e) (binary search on offsets)
+#pragma unroll 4
+        for (int e = threadIdx.x; e < ncand; e += NT) {
+            int lo = 0, hi = A.nch - 1;
+            while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (s_off[mid] <= e) lo = mid; else hi = mid - 1; }
+            // skip empty chunks sharing the same offset: the last chunk with off <= e holds e
+            const size_t g = (size_t)lo * kCpc + (e - s_off[lo]);
+            ck[e] = ((unsigned long long)(uint32_t)__ldg(gj + g) << 32) | __float_as_uint(__ldg(gs + g));
         }
         __syncthreads();
     }
@@ -449,6 +573,7 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
         tauN += step;
         if (!(fabs(step) > 2e-16 * fmax(1.0, fabs(tauN)))) break;
     }
+    stamp(0, 3);
     // ---- support (R9)
     const double band = 1e-9 * fmax(1.0, fabs(tauN));
     int amb = 0;
@@ -473,6 +598,7 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
             __syncthreads();
         }
     }
+    stamp(0, 4);
     // ---- tau from the support
     double S1 = 0.0, kk = 0.0;
     for (int k = threadIdx.x; k < ncand; k += NT)
@@ -495,6 +621,7 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
         block_sum2_d<NT>(F, Fd, shd);
         tau = tauN + (F - 1.0) / (beta * Fd);
     }
+    stamp(0, 5);
     // ---- p and PV (warp per support token, lane = 4 dims)
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     double psum = 0.0;
@@ -521,6 +648,7 @@ __global__ void __launch_bounds__(kTauNT) k_tau_pv(CacheView c, TauArgs A) {
         if (A.tau_out) A.tau_out[row] = tau;
         if (A.supp_out) A.supp_out[row] = (int)kk;
     }
+    stamp(0, 6);
     // ---- eval list: support token positions and p (for exact delta / rho)
     if (A.tok_list) {
         int base = 0;

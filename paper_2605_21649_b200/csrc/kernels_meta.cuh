@@ -12,7 +12,7 @@ namespace ekv {
 // explicit round-to-nearest intrinsics (no contraction).  seq_lens[b] is bumped after
 // a CTA barrier.
 template <typename T>
-__global__ void __launch_bounds__(1024) k_append(CacheView c, const T *__restrict__ k_new,
+__global__ void __launch_bounds__(1024, 1) k_append(CacheView c, const T *__restrict__ k_new,
                                                  const T *__restrict__ v_new, int n_tokens) {
     const int b = blockIdx.x;
     const int L = c.seq_lens[b];
@@ -117,7 +117,7 @@ template <int MODES> struct ScoreCfg {
 // producer streams the range's metadata through an NS-deep ring of SP-page stages
 // (full/empty mbarriers, no CTA-wide barrier in the loop).
 template <typename T, int G, int MODES>
-__global__ void __launch_bounds__(288, 2) k_score(CacheView c, const T *__restrict__ q, int Hq,
+__global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(CacheView c, const T *__restrict__ q, int Hq,
                                                    float *__restrict__ box, float *__restrict__ mu,
                                                    float *__restrict__ sigma2) {
     constexpr int SP = ScoreCfg<MODES>::SP, NS = ScoreCfg<MODES>::NS;
@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(288, 2) k_score(CacheView c, const T *__restri
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t fullb[NS], emptyb[NS];
     __shared__ int d_b[NS], d_p0[NS], d_n[NS];
+    __shared__ int l_phys[512];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long total = (long long)c.B * c.maxp;
     const long long r0 = total * blockIdx.x / gridDim.x, r1 = total * (blockIdx.x + 1) / gridDim.x;
@@ -138,41 +139,64 @@ __global__ void __launch_bounds__(288, 2) k_score(CacheView c, const T *__restri
     }
     __syncthreads();
     if (warp == NCW) {
-        // ------------------------------------------------ producer (lane 0)
-        if (lane != 0) return;
+        // ------------------------------------------------ producer
+        // The range is processed in chunks of 512 (b, page) slots: the warp first loads the
+        // chunk's page-table entries into shared memory (16 independent loads per lane),
+        // then lane 0 packs runs of valid pages (one sequence at a time) into ring stages.
         int si = 0;
-        long long g = r0;
-        while (true) {
-            const int slot = si % NS;
+        // (b, page) of the chunk start, advanced incrementally (no 64-bit divisions in the loop)
+        int cb_b = (int)(r0 / c.maxp), cb_p = (int)(r0 % c.maxp);
+        for (long long cb = r0; cb < r1; cb += 512) {
+            const int nchk = (int)min((long long)512, r1 - cb);
+#pragma unroll 4
+            for (int i = lane; i < nchk; i += 32) {
+                int bb = cb_b, p = cb_p + i;
+                while (p >= c.maxp) { p -= c.maxp; ++bb; }
+                l_phys[i] = (p < n_pages_of(__ldg(c.seq_lens + bb))) ? __ldg(c.page_table + (size_t)bb * c.maxp + p) : -1;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                int i = 0, bb = cb_b, p0 = cb_p;           // (bb, p0) tracks chunk slot i
+                while (i < nchk) {
+                    if (l_phys[i] < 0) {                   // past the sequence end
+                        ++i;
+                        if (++p0 == c.maxp) { p0 = 0; ++bb; }
+                        continue;
+                    }
+                    int n = 1;
+                    while (n < SP && i + n < nchk && l_phys[i + n] >= 0 && p0 + n < c.maxp) ++n;
+                    const int slot = si % NS;
+                    if (si >= NS) mbar_wait(&emptyb[slot], ((si / NS) - 1) & 1);
+                    d_b[slot] = bb; d_p0[slot] = p0; d_n[slot] = n;
+                    mbar_expect_tx(&fullb[slot], n * per_page);
+                    for (int k = 0; k < n; ++k) {
+                        const size_t phys = (size_t)l_phys[i + k];
+                        unsigned char *dst = smem + ((size_t)slot * SP + k) * per_page;
+                        if (MODES & 1) {
+                            bulk_g2s(dst, reinterpret_cast<const T *>(c.kmin) + phys * HD, bmm, &fullb[slot]);
+                            bulk_g2s(dst + bmm, reinterpret_cast<const T *>(c.kmax) + phys * HD, bmm, &fullb[slot]);
+                            dst += 2 * bmm;
+                        }
+                        if (MODES & 2) {
+                            bulk_g2s(dst, c.kavg + phys * HD, bgs, &fullb[slot]);
+                            bulk_g2s(dst + bgs, c.kvar + phys * HD, bgs, &fullb[slot]);
+                        }
+                    }
+                    ++si;
+                    i += n;
+                    p0 += n;
+                    if (p0 >= c.maxp) { p0 -= c.maxp; ++bb; }
+                }
+            }
+            __syncwarp();
+            cb_p += nchk;
+            while (cb_p >= c.maxp) { cb_p -= c.maxp; ++cb_b; }
+        }
+        if (lane == 0) {
+            const int slot = si % NS;           // end marker
             if (si >= NS) mbar_wait(&emptyb[slot], ((si / NS) - 1) & 1);
-            // next run of valid pages of one sequence
-            int n = 0, bb = 0, p0 = 0;
-            while (g < r1) {
-                bb = (int)(g / c.maxp);
-                p0 = (int)(g % c.maxp);
-                const int M = n_pages_of(c.seq_lens[bb]);
-                if (p0 >= M) { g = (long long)(bb + 1) * c.maxp; continue; }   // skip the sequence tail
-                n = (int)min((long long)min(SP, M - p0), r1 - g);
-                break;
-            }
-            if (n == 0) { d_n[slot] = -1; mbar_arrive(&fullb[slot]); break; }
-            d_b[slot] = bb; d_p0[slot] = p0; d_n[slot] = n;
-            mbar_expect_tx(&fullb[slot], n * per_page);
-            for (int i = 0; i < n; ++i) {
-                const size_t phys = (size_t)__ldg(c.page_table + (size_t)bb * c.maxp + p0 + i);
-                unsigned char *dst = smem + ((size_t)slot * SP + i) * per_page;
-                if (MODES & 1) {
-                    bulk_g2s(dst, reinterpret_cast<const T *>(c.kmin) + phys * HD, bmm, &fullb[slot]);
-                    bulk_g2s(dst + bmm, reinterpret_cast<const T *>(c.kmax) + phys * HD, bmm, &fullb[slot]);
-                    dst += 2 * bmm;
-                }
-                if (MODES & 2) {
-                    bulk_g2s(dst, c.kavg + phys * HD, bgs, &fullb[slot]);
-                    bulk_g2s(dst + bgs, c.kvar + phys * HD, bgs, &fullb[slot]);
-                }
-            }
-            g += n;
-            ++si;
+            d_n[slot] = -1;
+            mbar_arrive(&fullb[slot]);
         }
         return;
     }
@@ -184,13 +208,12 @@ __global__ void __launch_bounds__(288, 2) k_score(CacheView c, const T *__restri
     const int hq0 = kvh * G;
     constexpr int GP = (G + 1) / 2;          // head pairs
     float2 qp[GP][8], qn[GP][8], qa[GP][8], q2[GP][8];
-    const int h_out = hq0 + rs_head<G>(lane);
-    const bool writer = rs_writer<G>(lane);
     int cur_b = -1;
     for (int si = 0;; ++si) {
         const int slot = si % NS;
         mbar_wait(&fullb[slot], (si / NS) & 1);
         const int n = d_n[slot];
+        stamp_if(threadIdx.x == 0 && si < 16, 4, si);
         if (n < 0) break;
         const int bb = d_b[slot], q0 = d_p0[slot];
         if (bb != cur_b) {
@@ -217,57 +240,78 @@ __global__ void __launch_bounds__(288, 2) k_score(CacheView c, const T *__restri
                 }
             }
         }
-        float *box_row = box + ((size_t)bb * Hq + h_out) * c.maxp;
-        float *mu_row = mu + ((size_t)bb * Hq + h_out) * c.maxp;
-        float *s2_row = sigma2 + ((size_t)bb * Hq + h_out) * c.maxp;
-        // warp-uniform trip count: both half-warps of a warp run the same iterations
-        for (int ib = 0; ib < n; ib += hwpk) {
-            const int i = ib + sub;
-            const bool valid = i < n;
-            const unsigned char *pg = smem + ((size_t)slot * SP + (valid ? i : 0)) * per_page;
-            const int p = q0 + i;
+        // two items (pages) per iteration, interleaved; the 2G partials go through one
+        // 16-lane reduce-scatter (same pairing tree per value: bit-identical to per-item)
+        for (int ib = 0; ib < n; ib += 2 * hwpk) {
+            const int i0 = ib + sub, i1 = ib + sub + hwpk;
+            const bool v0 = i0 < n, v1 = i1 < n;
+            const unsigned char *pg0 = smem + ((size_t)slot * SP + (v0 ? i0 : 0)) * per_page;
+            const unsigned char *pg1 = smem + ((size_t)slot * SP + (v1 ? i1 : 0)) * per_page;
             if (MODES & 1) {
-                float mn[8], mx[8];
-                Elem<T>::load8(reinterpret_cast<const T *>(pg) + kvh * kD + 8 * l16, mn);
-                Elem<T>::load8(reinterpret_cast<const T *>(pg + bmm) + kvh * kD + 8 * l16, mx);
-                float acc[G];
+                float mn0[8], mx0[8], mn1[8], mx1[8];
+                Elem<T>::load8(reinterpret_cast<const T *>(pg0) + kvh * kD + 8 * l16, mn0);
+                Elem<T>::load8(reinterpret_cast<const T *>(pg0 + bmm) + kvh * kD + 8 * l16, mx0);
+                Elem<T>::load8(reinterpret_cast<const T *>(pg1) + kvh * kD + 8 * l16, mn1);
+                Elem<T>::load8(reinterpret_cast<const T *>(pg1 + bmm) + kvh * kD + 8 * l16, mx1);
+                float acc[2 * G];
 #pragma unroll
                 for (int g = 0; g < GP; ++g) {
-                    float2 a2 = make_float2(0.0f, 0.0f);
+                    float2 a0 = make_float2(0.0f, 0.0f), a1 = make_float2(0.0f, 0.0f);
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
-                        a2 = ffma2(qn[g][e], mn[e], a2);
-                        a2 = ffma2(qp[g][e], mx[e], a2);
+                        a0 = ffma2(qn[g][e], mn0[e], a0);
+                        a1 = ffma2(qn[g][e], mn1[e], a1);
+                        a0 = ffma2(qp[g][e], mx0[e], a0);
+                        a1 = ffma2(qp[g][e], mx1[e], a1);
                     }
-                    acc[2 * g] = a2.x;
-                    if (2 * g + 1 < G) acc[2 * g + 1] = a2.y;
+                    acc[2 * g] = a0.x; acc[G + 2 * g] = a1.x;
+                    if (2 * g + 1 < G) { acc[2 * g + 1] = a0.y; acc[G + 2 * g + 1] = a1.y; }
                 }
-                const float r = __fmul_rn(rs_reduce16<G>(acc, lane), kCd);
-                if (writer && valid) box_row[p] = r;
+                const float r = __fmul_rn(rs_reduce16<2 * G>(acc, lane), kCd);
+                const int vv = rs_head<2 * G>(lane);
+                const int it = vv / G, hh = vv % G;
+                if (rs_writer<2 * G>(lane) && (it ? v1 : v0))
+                    box[((size_t)bb * Hq + hq0 + hh) * c.maxp + q0 + (it ? i1 : i0)] = r;
             }
             if (MODES & 2) {
-                const unsigned char *pgs = pg + ((MODES & 1) ? 2 * bmm : 0);
-                float av[8], vr[8];
-                Elem<float>::load8(reinterpret_cast<const float *>(pgs) + kvh * kD + 8 * l16, av);
-                Elem<float>::load8(reinterpret_cast<const float *>(pgs + bgs) + kvh * kD + 8 * l16, vr);
-                float am[G], as[G];
+                const unsigned char *ps0 = pg0 + ((MODES & 1) ? 2 * bmm : 0);
+                const unsigned char *ps1 = pg1 + ((MODES & 1) ? 2 * bmm : 0);
+                float av0[8], vr0[8], av1[8], vr1[8];
+                Elem<float>::load8(reinterpret_cast<const float *>(ps0) + kvh * kD + 8 * l16, av0);
+                Elem<float>::load8(reinterpret_cast<const float *>(ps0 + bgs) + kvh * kD + 8 * l16, vr0);
+                Elem<float>::load8(reinterpret_cast<const float *>(ps1) + kvh * kD + 8 * l16, av1);
+                Elem<float>::load8(reinterpret_cast<const float *>(ps1 + bgs) + kvh * kD + 8 * l16, vr1);
+                float am[2 * G], as[2 * G];
 #pragma unroll
                 for (int g = 0; g < GP; ++g) {
-                    float2 m2 = make_float2(0.0f, 0.0f), s2 = make_float2(0.0f, 0.0f);
+                    float2 m0 = make_float2(0.0f, 0.0f), s0 = make_float2(0.0f, 0.0f);
+                    float2 m1 = make_float2(0.0f, 0.0f), s1 = make_float2(0.0f, 0.0f);
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
-                        m2 = ffma2(qa[g][e], av[e], m2);
-                        s2 = ffma2(q2[g][e], vr[e], s2);
+                        m0 = ffma2(qa[g][e], av0[e], m0);
+                        s0 = ffma2(q2[g][e], vr0[e], s0);
+                        m1 = ffma2(qa[g][e], av1[e], m1);
+                        s1 = ffma2(q2[g][e], vr1[e], s1);
                     }
-                    am[2 * g] = m2.x; as[2 * g] = s2.x;
-                    if (2 * g + 1 < G) { am[2 * g + 1] = m2.y; as[2 * g + 1] = s2.y; }
+                    am[2 * g] = m0.x; as[2 * g] = s0.x; am[G + 2 * g] = m1.x; as[G + 2 * g] = s1.x;
+                    if (2 * g + 1 < G) {
+                        am[2 * g + 1] = m0.y; as[2 * g + 1] = s0.y;
+                        am[G + 2 * g + 1] = m1.y; as[G + 2 * g + 1] = s1.y;
+                    }
                 }
-                const float rm = __fmul_rn(rs_reduce16<G>(am, lane), kCd);
-                const float rs = __fmul_rn(rs_reduce16<G>(as, lane), 1.0f / (float)kD);
-                if (writer && valid) { mu_row[p] = rm; s2_row[p] = rs; }
+                const float rm = __fmul_rn(rs_reduce16<2 * G>(am, lane), kCd);
+                const float rs = __fmul_rn(rs_reduce16<2 * G>(as, lane), 1.0f / (float)kD);
+                const int vv = rs_head<2 * G>(lane);
+                const int it = vv / G, hh = vv % G;
+                if (rs_writer<2 * G>(lane) && (it ? v1 : v0)) {
+                    const size_t o = ((size_t)bb * Hq + hq0 + hh) * c.maxp + q0 + (it ? i1 : i0);
+                    mu[o] = rm;
+                    sigma2[o] = rs;
+                }
             }
         }
         __syncwarp();
+        stamp_if(threadIdx.x == 0 && si < 16, 4, 16 + si);
         if (lane == 0) mbar_arrive(&emptyb[slot]);
     }
 }

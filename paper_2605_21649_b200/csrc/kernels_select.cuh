@@ -20,9 +20,52 @@ namespace ekv {
 // Overflow (more than kTopkCap candidates): the same searches run over all keys read
 // from global memory (L2) -- exact, slower.
 constexpr int kTopkCap = 8192;
+__device__ int ekv_dbg_nc;
+
+__device__ __forceinline__ void topk_key4(const float *x, int i4, int M, bool vec, uint32_t (&kk)[4]) {
+    if (vec && i4 + 3 < M) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(x + i4));
+        kk[0] = f2key(v.x); kk[1] = f2key(v.y); kk[2] = f2key(v.z); kk[3] = f2key(v.w);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) kk[e] = (i4 + e < M) ? f2key(__ldg(x + i4 + e)) : 0u;
+    }
+}
+// #(candidates with key >= Tt) (or over all keys on overflow), block-wide
+template <int NT>
+__device__ __forceinline__ int topk_cnt_ge(uint32_t Tt, bool ovf, int nc, int slots, const uint32_t *ckey,
+                                           const float *x, int M, int *sh) {
+    if (!ovf) {
+        int c = 0;
+        for (int s2 = 0; s2 < slots; ++s2) {
+            const int j = s2 * NT + threadIdx.x;
+            c += __syncthreads_count(j < nc && ckey[j] >= Tt);
+        }
+        return c;
+    }
+    int c = 0;
+    for (int i = threadIdx.x; i < M; i += NT) c += f2key(__ldg(x + i)) >= Tt;
+    return block_sum_i<NT>(c, sh);
+}
+// #(key == T && idx < I), block-wide
+template <int NT>
+__device__ __forceinline__ int topk_cnt_eq_lt(uint32_t T, int I, bool ovf, int nc, int slots, const uint32_t *ckey,
+                                              const int32_t *cidx, const float *x, int M, int *sh) {
+    if (!ovf) {
+        int c = 0;
+        for (int s2 = 0; s2 < slots; ++s2) {
+            const int j = s2 * NT + threadIdx.x;
+            c += __syncthreads_count(j < nc && ckey[j] == T && cidx[j] < I);
+        }
+        return c;
+    }
+    int c = 0;
+    for (int i = threadIdx.x; i < min(M, I); i += NT) c += f2key(__ldg(x + i)) == T;
+    return block_sum_i<NT>(c, sh);
+}
 
 template <int NT>
-__global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int Hq, int maxp,
+__global__ void __launch_bounds__(NT, 1) k_topk(const float *__restrict__ box, int Hq, int maxp,
                                              const int32_t *__restrict__ seq_lens, int k,
                                              int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
                                              int sel_stride) {
@@ -42,20 +85,12 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
         if (threadIdx.x == 0) n_sel[row] = M;
         return;
     }
+    stamp(1, 0);
     const float *x = box + (size_t)row * maxp;
     const int W = (M + 31) / 32;
     for (int w = threadIdx.x; w < W; w += NT) bits[w] = 0u;
     if (threadIdx.x == 0) s_cnt = 0;
     const bool vec = (maxp & 3) == 0;
-    auto key4 = [&](int i4, uint32_t (&kk)[4]) {
-        if (vec && i4 + 3 < M) {
-            const float4 v = __ldg(reinterpret_cast<const float4 *>(x + i4));
-            kk[0] = f2key(v.x); kk[1] = f2key(v.y); kk[2] = f2key(v.z); kk[3] = f2key(v.w);
-        } else {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) kk[e] = (i4 + e < M) ? f2key(__ldg(x + i4 + e)) : 0u;
-        }
-    };
     // 1. partition maxima: thread t owns the float4 groups {t + NT*j}; the max of each
     //    group is kept (fp32 max == key max: f2key is monotone) for the second pass.
     constexpr int GPT = 16;                  // groups per thread (M <= 16 * 4 * NT)
@@ -83,6 +118,7 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
         }
     }
     __syncthreads();
+    stamp(1, 1);
     uint32_t Lb = 1u;
     if (keff <= NT) {
         uint32_t T = 0u;
@@ -92,6 +128,7 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
         }
         Lb = T > 1u ? T : 1u;
     }
+    stamp(1, 2);
     // 2. candidates: only groups whose max reaches L are re-read
 #pragma unroll
     for (int j = 0; j < GPT; ++j) {
@@ -99,7 +136,7 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
         const bool hit = (i4 < M) && f2key(gmax[j]) >= Lb;
         if (__ballot_sync(0xffffffffu, hit) == 0u) continue;
         uint32_t kk[4] = {0u, 0u, 0u, 0u};
-        if (hit) key4(i4, kk);
+        if (hit) topk_key4(x, i4, M, vec, kk);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const bool c = hit && kk[e] >= Lb;
@@ -114,50 +151,28 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
     __syncthreads();
     const int nc = s_cnt;
     const bool ovf = nc > kTopkCap;
+    stamp(1, 3);
+    if (threadIdx.x == 0 && blockIdx.x == 0) ekv_dbg_nc = nc;
     const int slots = (nc + NT - 1) / NT;
     // 3. T* = k-th largest candidate key (or key, on overflow)
-    auto cnt_ge = [&](uint32_t Tt) -> int {
-        if (!ovf) {
-            int c = 0;
-            for (int s2 = 0; s2 < slots; ++s2) {
-                const int j = s2 * NT + threadIdx.x;
-                c += __syncthreads_count(j < nc && ckey[j] >= Tt);
-            }
-            return c;
-        }
-        int c = 0;
-        for (int i = threadIdx.x; i < M; i += NT) c += f2key(__ldg(x + i)) >= Tt;
-        return block_sum_i<NT>(c, sh);
-    };
     uint32_t T = 0u;        // largest T with #(key >= T) >= k; holds for T <= L by step 1
     for (int bit = 31; bit >= 0; --bit) {
         const uint32_t Tt = T | (1u << bit);
-        if (Tt <= Lb || cnt_ge(Tt) >= keff) T = Tt;
+        if (Tt <= Lb || topk_cnt_ge<NT>(Tt, ovf, nc, slots, ckey, x, M, sh) >= keff) T = Tt;
     }
-    const int n_gt = (T == 0xffffffffu) ? 0 : cnt_ge(T + 1u);
+    const int n_gt = (T == 0xffffffffu) ? 0 : topk_cnt_ge<NT>(T + 1u, ovf, nc, slots, ckey, x, M, sh);
     const int need = keff - n_gt;
-    auto cnt_eq_lt = [&](int I) -> int {       // #(key == T && idx < I)
-        if (!ovf) {
-            int c = 0;
-            for (int s2 = 0; s2 < slots; ++s2) {
-                const int j = s2 * NT + threadIdx.x;
-                c += __syncthreads_count(j < nc && ckey[j] == T && cidx[j] < I);
-            }
-            return c;
-        }
-        int c = 0;
-        for (int i = threadIdx.x; i < min(M, I); i += NT) c += f2key(__ldg(x + i)) == T;
-        return block_sum_i<NT>(c, sh);
-    };
+    stamp(1, 4);
     int Ithr = M;                                    // select equal keys with idx < Ithr
-    if (cnt_eq_lt(M) > need) {
+    if (topk_cnt_eq_lt<NT>(T, M, ovf, nc, slots, ckey, cidx, x, M, sh) > need) {
         int I = 0;                                   // largest I with #(eq, idx < I) <= need
         for (int bit = 17; bit >= 0; --bit) {
             const int It = I + (1 << bit);
-            if (It <= M && cnt_eq_lt(It) <= need) I = It;
+            if (It <= M && topk_cnt_eq_lt<NT>(T, It, ovf, nc, slots, ckey, cidx, x, M, sh) <= need) I = It;
         }
         Ithr = I;
     }
+    stamp(1, 5);
     // 4. mark + ascending output
     if (!ovf) {
         for (int j = threadIdx.x; j < nc; j += NT) {
@@ -191,25 +206,34 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
         }
     }
     if (threadIdx.x == 0) n_sel[row] = keff;
+    stamp(1, 6);
 }
 
 // ============================================================================ union per KV group
-// The union of the G selections of a KV group as a byte mask per page (bit g = selected
-// by query head g of the group; R17): umask[b][kvh][page] bytes packed 4 per u32,
-// zeroed by the host (cudaMemsetAsync) and filled with atomicOr from the page lists.
+// The union of the G selections of a KV group (R17): umask[b][kvh][page] bytes (4 per
+// u32, bit g = selected by query head g of the group), zeroed by the host and filled
+// with atomicOr from the page lists; the head that sets a page's first bit also appends
+// the page to the group's compact list ulist[b][kvh][0..ucount) (order irrelevant: the
+// K-score kernel's result does not depend on the order in which pages are processed).
 __global__ void __launch_bounds__(256) k_mark(int Hq, int G, const int32_t *__restrict__ page_idx,
                                               const int32_t *__restrict__ n_sel, int sel_stride,
-                                              uint32_t *__restrict__ umask, int W) {
+                                              uint32_t *__restrict__ umask, int W, int32_t *__restrict__ ulist,
+                                              int32_t *__restrict__ ucount, int ucap) {
     const int row = blockIdx.x;
     const int b = row / Hq, h = row % Hq;
     const int kvh = h / G, g = h % G;
     const int Hkv = Hq / G;
+    const int unit = b * Hkv + kvh;
     const int n = n_sel[row];
     const int32_t *pl = page_idx + (size_t)row * sel_stride;
-    uint32_t *um = umask + ((size_t)b * Hkv + kvh) * W;
+    uint32_t *um = umask + (size_t)unit * W;
     for (int i = threadIdx.x; i < n; i += 256) {
         const int p = pl[i];
-        atomicOr(um + (p >> 2), 1u << ((p & 3) * 8 + g));
+        const uint32_t old = atomicOr(um + (p >> 2), 1u << ((p & 3) * 8 + g));
+        if (((old >> ((p & 3) * 8)) & 0xffu) == 0u) {
+            const int pos = atomicAdd(ucount + unit, 1);
+            if (pos < ucap) ulist[(size_t)unit * ucap + pos] = p;
+        }
     }
 }
 

@@ -1,0 +1,19 @@
+import ctypes, torch, sys, math
+sys.path.insert(0,'.')
+from paper_2605_21649_b200 import binding as ekv
+from paper_2605_21649_b200.workload import make_workload, new_tokens
+dev=torch.device('cuda')
+n=(1<<20)-200; Hq,Hkv=32,8
+wl=make_workload(1,n,Hq,Hkv,seed=1,device=dev,spare_tokens=200)
+c=ekv.PagedCache.allocate_meta(wl.K,wl.V,wl.page_table,wl.seq_lens); ekv.rebuild_page_stats(c)
+sel=ekv.select_params('topk',656); attn=ekv.attn_params(1.5); ws=ekv.alloc_workspace(c,Hq,sel)
+st=ekv.DecodeStats(1,Hq,dev)
+L=ekv.lib(); L.entmaxkv_debug_stamps.argtypes=[ctypes.c_void_p, ctypes.c_void_p]
+buf=(ctypes.c_ulonglong*256)(); nc=ctypes.c_int()
+for it in range(5):
+    ekv.decode(c,wl.q,sel,attn,ws,stats=st); torch.cuda.synchronize()
+L.entmaxkv_debug_stamps(buf, ctypes.byref(nc))
+for k,name in [(0,'tau'),(1,'topk')]:
+    v=[buf[k*32+i] for i in range(8)]
+    print(name, [ (v[i]-v[0])/1000 for i in range(8) if v[i]])
+print('topk nc', nc.value)
