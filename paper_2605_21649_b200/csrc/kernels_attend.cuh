@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ sc
     __shared__ float shf[9];
     double tcut = tau_lo;
     int ctot = block_sum_i<256>(cnt, sh);
-    if (ctot > 64) {
+    if (ctot > 256) {
         const double beta = 1.0 / a;
         const int ib = (fabs(beta - rint(beta)) < 1e-12 && beta <= 4.5) ? (int)rint(beta) : 0;
         float lm = -INFINITY;
