@@ -327,6 +327,7 @@ __device__ __forceinline__ void stamp(int k, int i) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         ekv_stamps[k][i] = t;
+        ekv_stamps[k][16 + i] = clock64();
     }
 }
 __device__ __forceinline__ void stamp_if(bool cond, int k, int i) {
@@ -340,4 +341,94 @@ __device__ __forceinline__ void stamp_if(bool cond, int k, int i) {
 __device__ __forceinline__ void stamp(int, int) {}
 __device__ __forceinline__ void stamp_if(bool, int, int) {}
 #endif
+}  // namespace ekv
+
+namespace ekv {
+// Block sum of two doubles with ONE barrier: warp shuffle tree, per-warp partials in a
+// double-buffered shared slot (buf[2][2*NW]), then every thread adds the NW partials in
+// the same fixed order (deterministic; no second barrier needed before the next call
+// because the next call writes the other buffer).
+template <int NT> struct BlockRed2 {
+    double *buf;   // [2][2 * NT/32]
+    int ph;
+    __device__ __forceinline__ void sum(double &a, double &b) {
+        constexpr int NW = NT / 32;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        double *s = buf + ph * 2 * NW;
+        ph ^= 1;
+        if ((threadIdx.x & 31) == 0) { s[2 * (threadIdx.x >> 5)] = a; s[2 * (threadIdx.x >> 5) + 1] = b; }
+        __syncthreads();
+        double x = 0.0, y = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) { x += s[2 * w]; y += s[2 * w + 1]; }
+        a = x; b = y;
+    }
+};
+}  // namespace ekv
+
+namespace ekv {
+// Block-wide k-th largest of per-thread uint32 keys (CPT slots per thread, 0 = no key):
+// MSB-first radix select with 8-bit digits; each round builds a 256-bin shared histogram
+// of the digits of the keys that match the prefix found so far (warp-aggregated with
+// __match_any_sync), and warp 0 locates the digit holding the k-th key with a suffix scan.
+// Returns T* = the k-th largest key; *n_gt = number of keys > T*.  Requires
+// 1 <= k <= number of keys.  hist: 256 words of shared memory; sh: >= 2 ints.
+template <int NT, int CPT>
+__device__ uint32_t block_kth_largest(const uint32_t (&key)[CPT], int k, uint32_t *hist, int *sh, int *n_gt) {
+    uint32_t prefix = 0u, pmask = 0u;
+    int kk = k, above = 0;
+    const int lane = threadIdx.x & 31;
+#pragma unroll 1
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += NT) hist[i] = 0u;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+            const uint32_t x = key[j];
+            const bool act = x != 0u && (x & pmask) == prefix;
+            if (__ballot_sync(0xffffffffu, act) == 0u) continue;      // warp-uniform skip
+            const uint32_t d = act ? ((x >> shift) & 255u) : (256u + lane);
+            const unsigned peers = __match_any_sync(0xffffffffu, d);
+            if (act && lane == __ffs(peers) - 1) atomicAdd(&hist[d], (uint32_t)__popc(peers));
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            int v[8], s = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) { v[e] = (int)hist[255 - 8 * lane - e]; s += v[e]; }
+            int incl = s;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int excl = incl - s;
+            int D = -1, cab = 0, cum = excl;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                if (D < 0 && cum + v[e] >= kk) { D = 255 - 8 * lane - e; cab = cum; }
+                cum += v[e];
+            }
+            const unsigned bm = __ballot_sync(0xffffffffu, D >= 0 && excl < kk);
+            const int src = __ffs(bm) - 1;
+            D = __shfl_sync(0xffffffffu, D, src);
+            cab = __shfl_sync(0xffffffffu, cab, src);
+            if (lane == 0) { sh[0] = D; sh[1] = cab; }
+        }
+        __syncthreads();
+        const uint32_t D = (uint32_t)sh[0];
+        const int cab = sh[1];
+        prefix |= D << shift;
+        pmask |= 255u << shift;
+        above += cab;
+        kk -= cab;
+        __syncthreads();
+    }
+    *n_gt = above;
+    return prefix;
+}
 }  // namespace ekv

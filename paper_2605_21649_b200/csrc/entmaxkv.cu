@@ -181,56 +181,61 @@ ekv_status launch_score(const CacheView &v, const void *q, int Hq, int modes, fl
     }
 }
 
+struct UnionOut {            // optional union marks done by the selection kernel
+    uint32_t *umask; int W;
+};
+
 template <int NT>
 void topk_go(const float *box, int Hq, int maxp, const int32_t *sl, int k, int32_t *pi, int32_t *ns, int stride,
-             int rows, cudaStream_t st) {
-    const int smem = 8 * kTopkCap + 4 * ((maxp + 31) / 32);
+             int rows, int G, const UnionOut &u, cudaStream_t st) {
+    const int smem = 8 * kTopkCap;
     static bool init = false;
-    if (!init) { set_smem(k_topk<NT>, 8 * kTopkCap + 4 * (131072 / 32)); init = true; }
-    k_topk<NT><<<rows, NT, smem, st>>>(box, Hq, maxp, sl, k, pi, ns, stride);
+    if (!init) { set_smem(k_topk<NT>, smem); init = true; }
+    k_topk<NT><<<rows, NT, smem, st>>>(box, Hq, maxp, sl, k, pi, ns, stride, G, u.umask, u.W);
 }
 ekv_status launch_topk(const float *box, int B, int Hq, int maxp, const int32_t *sl, int k, int32_t *pi, int32_t *ns,
-                       int stride, cudaStream_t st) {
+                       int stride, int G, const UnionOut &u, cudaStream_t st) {
     const int rows = B * Hq;
-    if (maxp <= 4096) topk_go<256>(box, Hq, maxp, sl, k, pi, ns, stride, rows, st);
-    else topk_go<1024>(box, Hq, maxp, sl, k, pi, ns, stride, rows, st);
+    if (maxp <= 4096) topk_go<256>(box, Hq, maxp, sl, k, pi, ns, stride, rows, G, u, st);
+    else topk_go<1024>(box, Hq, maxp, sl, k, pi, ns, stride, rows, G, u, st);
     return check_launch("k_topk");
 }
 
 ekv_status launch_mark(const ekv_cache *c, int Hq, const int32_t *pi, const int32_t *ns, int stride, uint32_t *um,
-                       int W, int32_t *ul, int32_t *uc, int ucap, cudaStream_t st) {
-    k_mark<<<c->batch * Hq, 256, 0, st>>>(Hq, Hq / c->n_kv_heads, pi, ns, stride, um, W, ul, uc, ucap);
+                       int W, cudaStream_t st) {
+    k_mark<<<c->batch * Hq, 256, 0, st>>>(Hq, Hq / c->n_kv_heads, pi, ns, stride, um, W);
     return check_launch("k_mark");
 }
 
 template <typename T, int G>
-ekv_status launch_scores_t(const CacheView &v, const void *q, int Hq, const uint32_t *um, int W, const int32_t *ul,
-                           const int32_t *uc, int ucap, float *scores, uint32_t *rowmax, int full, cudaStream_t st) {
+ekv_status launch_scores_t(const CacheView &v, const void *q, int Hq, const uint32_t *um, int W, const int32_t *pi,
+                           const int32_t *ns, int stride, float *scores, uint32_t *rowmax, int full, cudaStream_t st) {
     constexpr int smem = AttCfg<T>::SMEM;
     static bool init = false;
     if (!init) { set_smem(k_attend_scores<T, G>, smem); init = true; }
     const int per_sm = sizeof(T) == 2 ? 2 : 1;
-    long long gx = ((long long)v.B * v.Hkv * ucap + 31) / 32;     // >= 32 work slots per CTA
+    const long long slots = full ? (long long)v.B * v.Hkv * v.maxp : (long long)v.B * Hq * stride;
+    long long gx = (slots + 31) / 32;                                // >= 32 work slots per CTA
     if (gx > per_sm * num_sms()) gx = per_sm * num_sms();
     if (gx < 1) gx = 1;
-    k_attend_scores<T, G><<<(unsigned)gx, 288, smem, st>>>(v, static_cast<const T *>(q), Hq, um, W, ul, uc, ucap,
+    k_attend_scores<T, G><<<(unsigned)gx, 288, smem, st>>>(v, static_cast<const T *>(q), Hq, um, W, pi, ns, stride,
                                                            scores, rowmax, full);
     return check_launch("k_attend_scores");
 }
 template <typename T>
-ekv_status launch_scores(const CacheView &v, const void *q, int Hq, const uint32_t *um, int W, const int32_t *ul,
-                         const int32_t *uc, int ucap, float *scores, uint32_t *rowmax, int full, cudaStream_t st) {
+ekv_status launch_scores(const CacheView &v, const void *q, int Hq, const uint32_t *um, int W, const int32_t *pi,
+                         const int32_t *ns, int stride, float *scores, uint32_t *rowmax, int full, cudaStream_t st) {
     switch (Hq / v.Hkv) {
-    case 1: return launch_scores_t<T, 1>(v, q, Hq, um, W, ul, uc, ucap, scores, rowmax, full, st);
-    case 2: return launch_scores_t<T, 2>(v, q, Hq, um, W, ul, uc, ucap, scores, rowmax, full, st);
-    case 4: return launch_scores_t<T, 4>(v, q, Hq, um, W, ul, uc, ucap, scores, rowmax, full, st);
-    default: return launch_scores_t<T, 8>(v, q, Hq, um, W, ul, uc, ucap, scores, rowmax, full, st);
+    case 1: return launch_scores_t<T, 1>(v, q, Hq, um, W, pi, ns, stride, scores, rowmax, full, st);
+    case 2: return launch_scores_t<T, 2>(v, q, Hq, um, W, pi, ns, stride, scores, rowmax, full, st);
+    case 4: return launch_scores_t<T, 4>(v, q, Hq, um, W, pi, ns, stride, scores, rowmax, full, st);
+    default: return launch_scores_t<T, 8>(v, q, Hq, um, W, pi, ns, stride, scores, rowmax, full, st);
     }
 }
 
 template <typename T>
 ekv_status launch_tau(const CacheView &v, const TauArgs &A, int rows, cudaStream_t st) {
-    constexpr int smem = kCap * 8 + kCap;
+    constexpr int smem = kCap * (8 + 1 + 4);   // ck, cin, cphys (+ ~29 KB static)
     static bool init = false;
     if (!init) { set_smem(k_tau_pv<T>, smem); init = true; }
     k_tau_pv<T><<<rows, kTauNT, smem, st>>>(v, A);
@@ -266,34 +271,31 @@ ekv_status check_sel(const ekv_select_params *s, float alpha) {
 // memset(rowmax, ccount, umask) -> [mark] -> K scores -> candidates -> tau/PV
 ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t *pi, const int32_t *ns, int stride,
                        int full, const ekv_attn_params *attn, float *out, double *tau, int32_t *supp, void *ws,
-                       const Layout &L, cudaStream_t st, const TauArgs *extra) {
+                       const Layout &L, cudaStream_t st, const TauArgs *extra, bool marked = false) {
     const CacheView v = view(c);
     uint32_t *rowmax = at<uint32_t>(ws, L.rowmax);
     int *ccount = at<int>(ws, L.ccount);
     uint32_t *um = at<uint32_t>(ws, L.umask);
     float *scores = at<float>(ws, L.scores);
-    if (cudaMemsetAsync(at<char>(ws, L.zero), 0, L.zero_bytes, st) != cudaSuccess)
+    if (!marked && cudaMemsetAsync(at<char>(ws, L.zero), 0, L.zero_bytes, st) != cudaSuccess)
         return fail(EKV_ERR_CUDA, "memset: %s", cudaGetErrorString(cudaGetLastError()));
-    int32_t *ul = at<int32_t>(ws, L.ulist);
-    int32_t *uc = at<int32_t>(ws, L.ucount);
-    // union capacity per KV group: min(G * list stride, max_pages); full: every page
-    const int G = Hq / c->n_kv_heads;
-    const long long uc_ll = (long long)G * stride;
-    const int ucap = full ? c->max_pages_per_seq : (int)(uc_ll < c->max_pages_per_seq ? uc_ll : c->max_pages_per_seq);
-    if (!full) EKV_TRY(launch_mark(c, Hq, pi, ns, stride, um, L.W, ul, uc, ucap, st));
+    if (!full && !marked) EKV_TRY(launch_mark(c, Hq, pi, ns, stride, um, L.W, st));
     if (c->dtype == EKV_BF16)
-        EKV_TRY(launch_scores<__nv_bfloat16>(v, q, Hq, um, L.W, ul, uc, ucap, scores, rowmax, full, st));
-    else EKV_TRY(launch_scores<float>(v, q, Hq, um, L.W, ul, uc, ucap, scores, rowmax, full, st));
+        EKV_TRY(launch_scores<__nv_bfloat16>(v, q, Hq, um, L.W, pi, ns, stride, scores, rowmax, full, st));
+    else EKV_TRY(launch_scores<float>(v, q, Hq, um, L.W, pi, ns, stride, scores, rowmax, full, st));
     const int rows = c->batch * Hq;
     const size_t ntok = (size_t)c->max_pages_per_seq * kP;
     float *cs = at<float>(ws, L.cand_s);
     int32_t *cj = at<int32_t>(ws, L.cand_j);
-    const int list_len = full ? c->max_pages_per_seq : stride;
-    const int nch = (list_len + 255) / 256;
-    dim3 cg(nch, rows);
-    k_candidates<<<cg, 256, 0, st>>>(scores, ntok, rowmax, pi, ns, stride, c->seq_lens, Hq, full, attn->alpha,
-                                     attn->transform, nch, ccount, cs, cj);
-    EKV_TRY(check_launch("k_candidates"));
+    // full rows are long: candidates extracted by a wide kernel; sparse rows are read by
+    // the tau kernel directly from the score row (one launch less)
+    const int nch = full ? (c->max_pages_per_seq + 255) / 256 : 0;
+    if (full && attn->transform == EKV_ENTMAX) {
+        dim3 cg(nch, rows);
+        k_candidates<<<cg, 256, 0, st>>>(scores, ntok, rowmax, pi, ns, stride, c->seq_lens, Hq, full, attn->alpha,
+                                         attn->transform, nch, ccount, cs, cj);
+        EKV_TRY(check_launch("k_candidates"));
+    }
     TauArgs A;
     memset(&A, 0, sizeof(A));
     if (extra) A = *extra;
@@ -404,11 +406,12 @@ ekv_status entmaxkv_select(const ekv_cache *cache, int32_t n_q_heads, const floa
     const int maxp = cache->max_pages_per_seq;
     if (sel->policy == EKV_TOPK) {
         if (!box) return fail(EKV_ERR_INVALID_ARG, "top-k needs box scores");
-        return launch_topk(box, cache->batch, n_q_heads, maxp, cache->seq_lens, sel->k_pages, page_idx, n_sel, sel_stride, st);
+        return launch_topk(box, cache->batch, n_q_heads, maxp, cache->seq_lens, sel->k_pages, page_idx, n_sel, sel_stride,
+                           n_q_heads / cache->n_kv_heads, UnionOut{nullptr, 0}, st);
     }
     if (sel->policy == EKV_ALL) {
         return launch_topk(box ? box : nullptr, cache->batch, n_q_heads, maxp, cache->seq_lens, maxp, page_idx, n_sel,
-                           sel_stride, st);
+                           sel_stride, n_q_heads / cache->n_kv_heads, UnionOut{nullptr, 0}, st);
     }
     if (!mu || !sigma2) return fail(EKV_ERR_INVALID_ARG, "Gaussian selector needs mu/sigma2");
     k_gauss_select<256><<<cache->batch * n_q_heads, 256, 0, st>>>(mu, sigma2, n_q_heads, maxp, cache->seq_lens, alpha,
@@ -464,6 +467,11 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
     int32_t *ns = at<int32_t>(workspace, L.n_sel);
     double *th = at<double>(workspace, L.tau_hat);
     const bool want_db = stats && stats->delta_bar && attn->transform == EKV_ENTMAX;
+    // zero the per-step counters / union mask once; the selection kernel merges the union
+    if (cudaMemsetAsync(at<char>(workspace, L.zero), 0, L.zero_bytes, st) != cudaSuccess)
+        return fail(EKV_ERR_CUDA, "memset: %s", cudaGetErrorString(cudaGetLastError()));
+    const int Gq = n_q_heads / cache->n_kv_heads;
+    const UnionOut uo{at<uint32_t>(workspace, L.umask), L.W};
     // a1: page scores (box for top-k and for the certificate; mu/sigma2 for Gaussian)
     int modes = 0;
     if (sel->policy == EKV_TOPK || want_db) modes |= EKV_SCORE_BOX;
@@ -476,19 +484,20 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
     const int maxp = cache->max_pages_per_seq;
     if (sel->policy == EKV_TOPK || sel->policy == EKV_ALL) {
         const int k = sel->policy == EKV_TOPK ? sel->k_pages : maxp;
-        EKV_TRY(launch_topk(box, cache->batch, n_q_heads, maxp, cache->seq_lens, k, pi, ns, L.cap, st));
+        EKV_TRY(launch_topk(box, cache->batch, n_q_heads, maxp, cache->seq_lens, k, pi, ns, L.cap, Gq, uo, st));
     } else {
         k_gauss_select<256><<<cache->batch * n_q_heads, 256, 0, st>>>(mu, s2, n_q_heads, maxp, cache->seq_lens,
                                                                       attn->alpha, sel->margin, sel->q_page, pi, ns,
                                                                       L.cap, th);
         EKV_TRY(check_launch("k_gauss_select"));
+        EKV_TRY(launch_mark(cache, n_q_heads, pi, ns, L.cap, uo.umask, L.W, st));
     }
     // a3
     double *tau_p = (stats && stats->tau) ? stats->tau : at<double>(workspace, L.tau_int);
     EKV_TRY(attend_impl(cache, q, n_q_heads, pi, ns, L.cap, 0, attn, out, tau_p,
-                        stats ? stats->supp_count : nullptr, workspace, L, st, nullptr));
+                        stats ? stats->supp_count : nullptr, workspace, L, st, nullptr, /*marked=*/true));
     const int rows = cache->batch * n_q_heads;
-    // a4: certified dropped-mass bound
+    // a4: certified dropped-mass bound (wide kernel; deterministic ticketed final sum)
     if (want_db) {
         const int nch = (maxp + kDbChunk - 1) / kDbChunk;
         dim3 g(nch, rows);
@@ -497,6 +506,7 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
                                        at<unsigned int>(workspace, L.tickets), stats->delta_bar);
         EKV_TRY(check_launch("k_delta_bar"));
     }
+
     if (stats) {
         if (stats->n_sel) {
             if (cudaMemcpyAsync(stats->n_sel, ns, rows * sizeof(int32_t), cudaMemcpyDeviceToDevice, st) != cudaSuccess)

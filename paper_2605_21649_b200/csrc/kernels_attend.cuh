@@ -35,8 +35,8 @@ template <typename T> struct AttCfg {
 template <typename T, int G>
 __global__ void __launch_bounds__(288) k_attend_scores(CacheView c, const T *__restrict__ q, int Hq,
                                                        const uint32_t *__restrict__ umask, int W,
-                                                       const int32_t *__restrict__ ulist,
-                                                       const int32_t *__restrict__ ucount, int ucap,
+                                                       const int32_t *__restrict__ page_idx,
+                                                       const int32_t *__restrict__ n_sel, int stride,
                                                        float *__restrict__ scores, uint32_t *__restrict__ rowmax,
                                                        int full) {
     constexpr int SP = AttCfg<T>::SP, NS = AttCfg<T>::NS, TILE = AttCfg<T>::TILE;
@@ -49,8 +49,11 @@ __global__ void __launch_bounds__(288) k_attend_scores(CacheView c, const T *__r
     __shared__ int l_unit[CHK], l_page[CHK], l_phys[CHK];
     __shared__ uint8_t l_mask[CHK];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // flattened work space: (unit, slot), slot < ucap (sparse: union-list slots; full: pages)
-    const long long tot = (long long)c.B * c.Hkv * ucap;
+    // flattened work space.  sparse: (row = b*Hq + h, i < stride) over the page lists; a page
+    // is kept only from its lowest selecting head of the group (union mask byte).  full:
+    // (unit = b*Hkv + kvh, page).
+    const int ucap = full ? c.maxp : stride;
+    const long long tot = full ? (long long)c.B * c.Hkv * c.maxp : (long long)c.B * Hq * stride;
     const long long f0 = tot * blockIdx.x / gridDim.x, f1 = tot * (blockIdx.x + 1) / gridDim.x;
     if (threadIdx.x == 0) {
         for (int i = 0; i < NS; ++i) { mbar_init(&fullb[i], 1); mbar_init(&emptyb[i], NCW); }
@@ -65,21 +68,23 @@ __global__ void __launch_bounds__(288) k_attend_scores(CacheView c, const T *__r
         const unsigned char *Kb = reinterpret_cast<const unsigned char *>(c.K);
         int si = 0, fill = 0;
         stamp_if(lane == 0, 2, 0);
-        int cu = (int)(f0 / ucap), cs = (int)(f0 % ucap);   // (unit, slot) of the chunk start
+        int cu = (int)(f0 / ucap), cs = (int)(f0 % ucap);   // (row or unit, slot) of the chunk start
         for (long long cb = f0; cb < f1; cb += CHK) {
-            int un[CHK / 32], pg[CHK / 32];
+            int un[CHK / 32], pg[CHK / 32], hg[CHK / 32];
             bool ok[CHK / 32];
 #pragma unroll
             for (int r = 0; r < CHK / 32; ++r) {
                 int u = cu, sl = cs + r * 32 + lane;
                 while (sl >= ucap) { sl -= ucap; ++u; }
-                un[r] = u;
+                // u: full -> unit; sparse -> row (b*Hq + h)
+                const int bb = full ? u / c.Hkv : u / Hq;
+                un[r] = full ? u : bb * c.Hkv + (u % Hq) / G;
+                hg[r] = full ? 0 : (u % Hq) % G;
                 ok[r] = false;
                 pg[r] = 0;
                 if (cb + r * 32 + lane < f1) {
-                    const int M = n_pages_of(__ldg(c.seq_lens + u / c.Hkv));
-                    if (full) { pg[r] = sl; ok[r] = sl < M; }
-                    else if (sl < __ldg(ucount + u)) { pg[r] = __ldg(ulist + (size_t)u * ucap + sl); ok[r] = true; }
+                    if (full) { pg[r] = sl; ok[r] = sl < n_pages_of(__ldg(c.seq_lens + bb)); }
+                    else if (sl < __ldg(n_sel + u)) { pg[r] = __ldg(page_idx + (size_t)u * stride + sl); ok[r] = true; }
                 }
             }
             cs += CHK;
@@ -95,6 +100,9 @@ __global__ void __launch_bounds__(288) k_attend_scores(CacheView c, const T *__r
                                  : (uint8_t)((__ldg(umask + (size_t)un[r] * W + (pg[r] >> 2)) >> ((pg[r] & 3) * 8)) & 0xffu);
                 }
             }
+#pragma unroll
+            for (int r = 0; r < CHK / 32; ++r)      // keep each union page once: lowest selecting head
+                if (ok[r] && !full && (__ffs((int)mk[r]) - 1) != hg[r]) ok[r] = false;
             int nl = 0;
 #pragma unroll
             for (int r = 0; r < CHK / 32; ++r) {
@@ -306,8 +314,8 @@ __global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ sc
             }
             block_sum2_d<256>(F, Fd, shd);
             if (!(Fd > 0.0)) break;
-            const double root = (ib == 1) ? F : (ib == 2) ? sqrt(F) : (ib == 4) ? sqrt(sqrt(F)) : pow(F, 1.0 / beta);
-            const double step = (root - 1.0) * F / (root * Fd);
+            const float Ff = (float)F, rootf = (ib == 1) ? Ff : (ib == 2) ? sqrtf(Ff) : (ib == 4) ? sqrtf(sqrtf(Ff)) : powf(Ff, (float)(1.0 / beta));
+            const double step = (double)((rootf - 1.0f) * Ff / (rootf * (float)Fd));
             tc += step;
             if (!(fabs(step) > 1e-9 * fmax(1.0, fabs(tc)))) break;
         }
@@ -339,18 +347,20 @@ __global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ sc
 
 // ============================================================================ exact tau + PV
 // One CTA (256 threads) per (b, q-head):
-//  1. the row's candidates are loaded into shared memory and bitonic-sorted by token
-//     index (deterministic order for every fp64 sum below);
-//  2. Newton on g(tau) = ||(z - tau)_+||_beta - 1 from tau_lo = z_max - 1 (convex and
-//     decreasing: monotone from the left, exact in one step for one active token);
+//  1. candidates {z > tau_lo = z_max - 1} in a FIXED order (fp64 sums below are then
+//     deterministic): sparse rows are read directly from the score row over the head's
+//     page list (block scan per round of 4 pages per thread); full rows come from the
+//     k_candidates chunk regions concatenated in chunk order.  Overflow -> Newton
+//     streamed over the source moves tau_lo just below tau, then an ordered re-extraction.
+//  2. Newton on g(tau) = ||(z - tau)_+||_beta - 1 from tau_lo (convex, decreasing:
+//     monotone from the left, exact in one step for one active token);
 //  3. support by R9: z > tau_N + band -> in, z < tau_N - band -> out, else F(z_j) < 1;
 //  4. tau from the support: beta = 1: (S1 - 1)/k; beta = 2: m - sqrt((1 - ss)/k);
 //     otherwise one Newton polish on sum_S (z - tau)^beta = 1;
-//  5. p_j = (z_j - tau)^beta; out = sum p_j v_j / sum p_j (R12), V rows gathered for
-//     support tokens only (warp per token, lane = 4 dims).
+//  5. p_j = (z_j - tau)^beta; out = sum p_j v_j / sum p_j (R12): support tokens are
+//     compacted NT at a time, their page-table entries fetched in parallel, then warps
+//     gather the V rows (4 in flight per warp; lane = 4 dims);
 // Softmax rows (a6): p = exp(s - s_max) over every valid token (dense V).
-// Overflow (more candidates than fit in shared memory): Newton streamed over the
-// global candidate list / score row brings tau_lo just below tau, then re-extract.
 constexpr int kTauNT = 256;
 constexpr int kCap = 12288;         // shared-memory candidate capacity
 
@@ -360,18 +370,49 @@ struct TauArgs {
     const int32_t *page_idx; const int32_t *n_sel; int sel_stride; int full;
     int Hq, G; float alpha; int transform;
     float *out; double *tau_out; int32_t *supp_out;
-    int32_t *tok_list; double *p_list; int32_t *n_list; int list_cap;   // eval list
+    int32_t *tok_list; double *p_list; int32_t *n_list; int list_cap;     // eval list
 };
+
+template <typename T>
+__device__ __forceinline__ void ldv4(const T *vr, float (&vx)[4]) {
+    if constexpr (sizeof(T) == 2) {
+        const uint2 w = *reinterpret_cast<const uint2 *>(vr);
+        vx[0] = bf_lo(w.x); vx[1] = bf_hi(w.x); vx[2] = bf_lo(w.y); vx[3] = bf_hi(w.y);
+    } else {
+        const float4 w = *reinterpret_cast<const float4 *>(vr);
+        vx[0] = w.x; vx[1] = w.y; vx[2] = w.z; vx[3] = w.w;
+    }
+}
+__device__ __forceinline__ double lbeta_step(double F, double Fd, double beta, int ib) {
+    // Newton step on g(tau) = ||(z - tau)_+||_beta - 1:  (F^{1/b} - 1) / (F^{1/b - 1} Fd).
+    // F and Fd are fp64 sums; the step itself only steers the iteration (its fixed point is
+    // F(tau) = 1 whatever the step's rounding), so it is evaluated in fp32, with F^{1/b} - 1
+    // formed from the accurate F - 1 to keep full relative precision near convergence.
+    const float dF = (float)(F - 1.0), Ff = (float)F, Fdf = (float)Fd;
+    float root, rm1;
+    if (ib == 1) { root = Ff; rm1 = dF; }
+    else if (ib == 2) { root = sqrtf(Ff); rm1 = dF / (root + 1.0f); }
+    else if (ib == 4) { root = sqrtf(sqrtf(Ff)); rm1 = dF / ((1.0f + root) * (1.0f + root * root)); }
+    else { rm1 = expm1f(log1pf(dF) / (float)beta); root = 1.0f + rm1; }
+    return (double)(rm1 * Ff / (root * Fdf));
+}
 
 template <typename T>
 __global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
     constexpr int NT = kTauNT;
+    constexpr int NW = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long *ck = reinterpret_cast<unsigned long long *>(smem);   // [kCap] (j << 32 | s bits)
     uint8_t *cin = reinterpret_cast<uint8_t *>(smem + sizeof(unsigned long long) * kCap);   // [kCap]
-    __shared__ double shd[2 * (NT / 32) + 2];
-    __shared__ int shi[NT / 32 + 1];
-    __shared__ float red[NT / 32][kD];
+    int *cphys = reinterpret_cast<int *>(smem + (sizeof(unsigned long long) + 1) * kCap);    // [kCap] (direct path)
+    __shared__ double rbuf[2 * 2 * NW];
+    __shared__ double shd[2 * NW + 2];
+    __shared__ int shi[NW + 1];
+    __shared__ float red[NW][kD];
+    constexpr int kSup = 2048;
+    __shared__ int sup_j[kSup], sup_phys[kSup];
+    __shared__ float sup_p[kSup];
+    BlockRed2<NT> R{rbuf, 0};
 
     stamp(0, 0);
     const int row = blockIdx.x;
@@ -379,70 +420,49 @@ __global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
     const int L = c.seq_lens[b];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t mk = A.rowmax[row];
-    auto empty_out = [&]() {
+    if (mk == 0u) {   // empty C_tok
         if (threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = 0.0f;
         if (threadIdx.x == 0) {
             if (A.tau_out) A.tau_out[row] = NAN;
             if (A.supp_out) A.supp_out[row] = 0;
             if (A.n_list) A.n_list[row] = 0;
         }
-    };
-    if (mk == 0u) { empty_out(); return; }
-    const float smax = key2f(mk);
-    auto v_row = [&](int j) -> const T * {
-        const int phys = c.page_table[(size_t)b * c.maxp + j / kP];
-        return reinterpret_cast<const T *>(c.V) + (((size_t)phys * c.Hkv + kvh) * kP + (j % kP)) * kD;
-    };
-    auto load_v4 = [&](const T *vr, float (&vx)[4]) {
-        if constexpr (sizeof(T) == 2) {
-            const uint2 w = *reinterpret_cast<const uint2 *>(vr);
-            vx[0] = bf_lo(w.x); vx[1] = bf_hi(w.x); vx[2] = bf_lo(w.y); vx[3] = bf_hi(w.y);
-        } else {
-            const float4 w = *reinterpret_cast<const float4 *>(vr);
-            vx[0] = w.x; vx[1] = w.y; vx[2] = w.z; vx[3] = w.w;
-        }
-    };
-    // chunk counts -> offsets (deterministic concatenation in chunk order; nch <= NT)
-    int ccnt = 0, coff = 0, ncand_all = 0;
-    bool chunk_ovf = false;
-    if (threadIdx.x < A.nch) {
-        ccnt = A.ccount[(size_t)row * A.nch + threadIdx.x];
-        chunk_ovf = ccnt > kCpc;
+        return;
     }
-    coff = block_excl_scan<NT>(ccnt, shi, &ncand_all);
-    stamp(0, 1);
-    chunk_ovf = __syncthreads_or(chunk_ovf);
-    const float *gs = A.cand_s + (size_t)row * A.nch * kCpc;
-    const int32_t *gj = A.cand_j + (size_t)row * A.nch * kCpc;
+    const float smax = key2f(mk);
+    const int nlist = A.full ? n_pages_of(L) : A.n_sel[row];
+    const int32_t *plist = A.page_idx + (size_t)row * A.sel_stride;
+    const float *srow = A.scores + (size_t)row * A.ntok;
+    const T *Vb = reinterpret_cast<const T *>(c.V);
+
     if (A.transform == 1) {
         // ---------------- softmax over C_tok: every valid token of the page list (dense V)
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        double zs = 0.0;
+        double zs = 0.0, dz = 0.0;
         int cnt = 0;
-        const int nlist = A.full ? n_pages_of(L) : A.n_sel[row];
-        const float *srow = A.scores + (size_t)row * A.ntok;
-        for (int e = warp; e < nlist * kP; e += NT / 32) {
-            const int pg = A.full ? e / kP : A.page_idx[(size_t)row * A.sel_stride + e / kP];
+        for (int e = warp; e < nlist * kP; e += NW) {
+            const int pg = A.full ? e / kP : plist[e / kP];
             const int j = pg * kP + e % kP;
             if (j >= L) continue;
             const float p = expf(srow[j] - smax);
             if (lane == 0) { zs += (double)p; ++cnt; }
+            const int phys = c.page_table[(size_t)b * c.maxp + pg];
             float vx[4];
-            load_v4(v_row(j) + 4 * lane, vx);
+            ldv4<T>(Vb + (((size_t)phys * c.Hkv + kvh) * kP + (j % kP)) * kD + 4 * lane, vx);
 #pragma unroll
             for (int e2 = 0; e2 < 4; ++e2) acc[e2] = __fmaf_rn(p, vx[e2], acc[e2]);
         }
 #pragma unroll
         for (int e = 0; e < 4; ++e) red[warp][4 * lane + e] = acc[e];
-        const double zt = block_sum_d<NT>(zs, shd);
+        R.sum(zs, dz);
         cnt = block_sum_i<NT>(cnt, shi);
         if (threadIdx.x < kD) {
             float o = 0.f;
-            for (int w = 0; w < NT / 32; ++w) o = __fadd_rn(o, red[w][threadIdx.x]);
-            A.out[(size_t)row * kD + threadIdx.x] = (float)((double)o / zt);
+            for (int w = 0; w < NW; ++w) o = __fadd_rn(o, red[w][threadIdx.x]);
+            A.out[(size_t)row * kD + threadIdx.x] = (float)((double)o / zs);
         }
         if (threadIdx.x == 0) {
-            if (A.tau_out) A.tau_out[row] = (double)smax + log(zt);
+            if (A.tau_out) A.tau_out[row] = (double)smax + log(zs);
             if (A.supp_out) A.supp_out[row] = cnt;
         }
         return;
@@ -454,28 +474,85 @@ __global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
     const int ib = (fabs(beta - rint(beta)) < 1e-12 && beta <= 4.5) ? (int)rint(beta) : 0;
     const double zmax = a * (double)smax;
     double tau_lo = zmax - 1.0 - 1e-12 * fmax(1.0, fabs(zmax));
-    auto zof = [&](int k) -> double { return a * (double)__uint_as_float((uint32_t)(ck[k] & 0xffffffffu)); };
+    int ncand = 0;
+    bool overflow = false;
+    bool have_phys = false;                 // cphys[] valid (direct extraction without overflow)
 
-    // candidate source (all paths produce the candidates in ascending chunk order, so the
-    // fp64 sums below have a fixed order):
-    //  (a) chunk regions concatenated in order;
-    //  (b) too many candidates for shared memory: Newton streamed over the chunk regions
-    //      (thread t <-> chunk t) moves tau_lo just below tau, then re-extract;
-    //  (c) a chunk region overflowed: the same over the score row (thread t <-> segment t).
-    int *s_cnt = reinterpret_cast<int *>(cin);            // cin is free until the support pass
-    int *s_off = s_cnt + 256;
-    if (threadIdx.x < A.nch) { s_cnt[threadIdx.x] = ccnt; s_off[threadIdx.x] = coff; }
-    __syncthreads();
-    int ncand = ncand_all;
-    if (ncand_all > kCap || chunk_ovf) {
-        const int nlist = A.full ? n_pages_of(L) : A.n_sel[row];
-        const float *srow = A.scores + (size_t)row * A.ntok;
-        const int ntk = nlist * kP;
-        const int seg = (ntk + NT - 1) / NT;              // (c): contiguous segment per thread
-        double tau = tau_lo;
-        for (int it = 0; it < 200; ++it) {
-            double F = 0.0, Fd = 0.0;
-            if (!chunk_ovf) {
+    if (!A.full) {
+        // (direct) rounds of up to 4 list pages per thread: loads in flight, count, scan, write
+        for (int r0 = 0; r0 < nlist; r0 += 4 * NT) {
+            float sv[4][kP];
+            int pgs[4], phs[4];
+            int cnt = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int li = r0 + threadIdx.x + u * NT;
+                pgs[u] = li < nlist ? plist[li] : -1;
+                phs[u] = 0;
+                if (pgs[u] >= 0) {
+                    phs[u] = __ldg(c.page_table + (size_t)b * c.maxp + pgs[u]);
+                    const float4 *p4 = reinterpret_cast<const float4 *>(srow + (size_t)pgs[u] * kP);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const float4 x = p4[v];
+                        sv[u][4 * v] = x.x; sv[u][4 * v + 1] = x.y; sv[u][4 * v + 2] = x.z; sv[u][4 * v + 3] = x.w;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (pgs[u] >= 0) {
+#pragma unroll
+                    for (int t = 0; t < kP; ++t)
+                        cnt += (pgs[u] * kP + t < L && sv[u][t] != -INFINITY && a * (double)sv[u][t] > tau_lo);
+                }
+            int tot;
+            int pos = ncand + block_excl_scan<NT>(cnt, shi, &tot);
+            if (ncand + tot > kCap) { overflow = true; break; }   // uniform
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (pgs[u] >= 0) {
+#pragma unroll
+                    for (int t = 0; t < kP; ++t)
+                        if (pgs[u] * kP + t < L && sv[u][t] != -INFINITY && a * (double)sv[u][t] > tau_lo) {
+                            cphys[pos] = phs[u];
+                            ck[pos++] = ((unsigned long long)(uint32_t)(pgs[u] * kP + t) << 32) | __float_as_uint(sv[u][t]);
+                        }
+                }
+            ncand += tot;
+        }
+        have_phys = !overflow;
+        __syncthreads();
+    } else {
+        // (full) chunk regions from k_candidates, concatenated in chunk order (nch <= NT)
+        int ccnt = 0, tot = 0;
+        bool chunk_ovf = false;
+        if (threadIdx.x < A.nch) {
+            ccnt = A.ccount[(size_t)row * A.nch + threadIdx.x];
+            chunk_ovf = ccnt > kCpc;
+        }
+        const int coff = block_excl_scan<NT>(ccnt, shi, &tot);
+        chunk_ovf = __syncthreads_or(chunk_ovf);
+        const float *gs = A.cand_s + (size_t)row * A.nch * kCpc;
+        const int32_t *gj = A.cand_j + (size_t)row * A.nch * kCpc;
+        if (!chunk_ovf && tot <= kCap) {
+            int *s_off = reinterpret_cast<int *>(cin);       // cin is free until the support pass
+            if (threadIdx.x < A.nch) s_off[threadIdx.x] = coff;
+            __syncthreads();
+#pragma unroll 4
+            for (int e = threadIdx.x; e < tot; e += NT) {
+                int lo = 0, hi = A.nch - 1;               // last chunk with offset <= e
+                while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (s_off[mid] <= e) lo = mid; else hi = mid - 1; }
+                const size_t g = (size_t)lo * kCpc + (e - s_off[lo]);
+                ck[e] = ((unsigned long long)(uint32_t)__ldg(gj + g) << 32) | __float_as_uint(__ldg(gs + g));
+            }
+            ncand = tot;
+            __syncthreads();
+        } else if (!chunk_ovf) {
+            // too many for shared memory: Newton over the chunk regions (thread t <-> chunk t)
+            double tau = tau_lo;
+            for (int it = 0; it < 200; ++it) {
+                double F = 0.0, Fd = 0.0;
                 if (threadIdx.x < A.nch) {
                     const size_t g0 = (size_t)threadIdx.x * kCpc;
                     for (int k = 0; k < ccnt; ++k) {
@@ -483,102 +560,114 @@ __global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
                         if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
                     }
                 }
-            } else {
-                for (int e = threadIdx.x * seg; e < min(ntk, (threadIdx.x + 1) * seg); ++e) {
-                    const int pg = A.full ? e / kP : A.page_idx[(size_t)row * A.sel_stride + e / kP];
-                    const int j = pg * kP + e % kP;
-                    if (j >= L) continue;
-                    const float sj = srow[j];
-                    if (sj == -INFINITY) continue;
-                    const double d = a * (double)sj - tau;
-                    if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
-                }
+                R.sum(F, Fd);
+                if (!(Fd > 0.0)) break;
+                const double step = lbeta_step(F, Fd, beta, ib);
+                tau += step;
+                if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(tau)))) break;
             }
-            block_sum2_d<NT>(F, Fd, shd);
-            if (!(Fd > 0.0)) break;
-            const double root = (ib == 1) ? F : (ib == 2) ? sqrt(F) : (ib == 4) ? sqrt(sqrt(F)) : pow(F, 1.0 / beta);
-            const double step = (root - 1.0) * F / (root * Fd);
-            tau += step;
-            if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(tau)))) break;
-        }
-        tau_lo = fmax(tau_lo, tau - 1e-7 * fmax(1.0, fabs(tau)));
-        // deterministic re-extraction: count per thread, block scan, write in order
-        int mine = 0;
-        if (!chunk_ovf) {
+            tau_lo = fmax(tau_lo, tau - 1e-7 * fmax(1.0, fabs(tau)));
+            int mine = 0;
             if (threadIdx.x < A.nch) {
                 const size_t g0 = (size_t)threadIdx.x * kCpc;
                 for (int k = 0; k < ccnt; ++k) mine += a * (double)__ldg(gs + g0 + k) > tau_lo;
             }
+            int tt;
+            int pos = block_excl_scan<NT>(mine, shi, &tt);
+            if (tt > kCap) overflow = true;
+            else {
+                if (threadIdx.x < A.nch) {
+                    const size_t g0 = (size_t)threadIdx.x * kCpc;
+                    for (int k = 0; k < ccnt; ++k) {
+                        const float sj = __ldg(gs + g0 + k);
+                        if (a * (double)sj > tau_lo)
+                            ck[pos++] = ((unsigned long long)(uint32_t)__ldg(gj + g0 + k) << 32) | __float_as_uint(sj);
+                    }
+                }
+                ncand = tt;
+            }
+            __syncthreads();
         } else {
-            for (int e = threadIdx.x * seg; e < min(ntk, (threadIdx.x + 1) * seg); ++e) {
-                const int pg = A.full ? e / kP : A.page_idx[(size_t)row * A.sel_stride + e / kP];
+            overflow = true;
+        }
+    }
+    if (overflow) {
+        // Newton streamed over the whole score row (coalesced, fixed thread mapping), then
+        // an ordered re-extraction by contiguous per-thread segments of the page list.
+        const int ntk = nlist * kP;
+        double tau = tau_lo;
+        for (int it = 0; it < 200; ++it) {
+            double F = 0.0, Fd = 0.0;
+            for (int e = threadIdx.x; e < ntk; e += NT) {
+                const int pg = A.full ? e / kP : plist[e / kP];
                 const int j = pg * kP + e % kP;
+                if (j >= L) continue;
+                const float sj = srow[j];
+                if (sj == -INFINITY) continue;
+                const double d = a * (double)sj - tau;
+                if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
+            }
+            R.sum(F, Fd);
+            if (!(Fd > 0.0)) break;
+            const double step = lbeta_step(F, Fd, beta, ib);
+            tau += step;
+            if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(tau)))) break;
+        }
+        tau_lo = fmax(tau_lo, tau - 1e-7 * fmax(1.0, fabs(tau)));
+        const int seg = (nlist + NT - 1) / NT;            // pages per thread, contiguous in list order
+        int mine = 0;
+        for (int li = threadIdx.x * seg; li < min(nlist, (threadIdx.x + 1) * seg); ++li) {
+            const int pg = A.full ? li : plist[li];
+            for (int t = 0; t < kP; ++t) {
+                const int j = pg * kP + t;
                 if (j < L && srow[j] != -INFINITY && a * (double)srow[j] > tau_lo) ++mine;
             }
         }
-        int tot;
-        int pos = block_excl_scan<NT>(mine, shi, &tot);
-        ncand = tot;
-        if (ncand > kCap) {          // support larger than the shared-memory capacity
+        int tt;
+        int pos = block_excl_scan<NT>(mine, shi, &tt);
+        if (tt > kCap) {             // support larger than the shared-memory capacity
             if (threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = NAN;
             if (threadIdx.x == 0) {
                 if (A.tau_out) A.tau_out[row] = NAN;
-                if (A.supp_out) A.supp_out[row] = -ncand;
+                if (A.supp_out) A.supp_out[row] = -tt;
             }
             return;
         }
-        if (!chunk_ovf) {
-            if (threadIdx.x < A.nch) {
-                const size_t g0 = (size_t)threadIdx.x * kCpc;
-                for (int k = 0; k < ccnt; ++k) {
-                    const float sj = __ldg(gs + g0 + k);
-                    if (a * (double)sj > tau_lo)
-                        ck[pos++] = ((unsigned long long)(uint32_t)__ldg(gj + g0 + k) << 32) | __float_as_uint(sj);
-                }
-            }
-        } else {
-            for (int e = threadIdx.x * seg; e < min(ntk, (threadIdx.x + 1) * seg); ++e) {
-                const int pg = A.full ? e / kP : A.page_idx[(size_t)row * A.sel_stride + e / kP];
-                const int j = pg * kP + e % kP;
+        for (int li = threadIdx.x * seg; li < min(nlist, (threadIdx.x + 1) * seg); ++li) {
+            const int pg = A.full ? li : plist[li];
+            for (int t = 0; t < kP; ++t) {
+                const int j = pg * kP + t;
                 if (j < L && srow[j] != -INFINITY && a * (double)srow[j] > tau_lo)
-                    ck[pos++] = ((unsigned long long)j << 32) | __float_as_uint(srow[j]);
+                    ck[pos++] = ((unsigned long long)(uint32_t)j << 32) | __float_as_uint(srow[j]);
             }
         }
-        __syncthreads();
-    } else {
-        // (a) flattened parallel copy: element e lives in chunk ch(e) (binary search on offsets)
-#pragma unroll 4
-        for (int e = threadIdx.x; e < ncand; e += NT) {
-            int lo = 0, hi = A.nch - 1;
-            while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (s_off[mid] <= e) lo = mid; else hi = mid - 1; }
-            // skip empty chunks sharing the same offset: the last chunk with off <= e holds e
-            const size_t g = (size_t)lo * kCpc + (e - s_off[lo]);
-            ck[e] = ((unsigned long long)(uint32_t)__ldg(gj + g) << 32) | __float_as_uint(__ldg(gs + g));
-        }
+        ncand = tt;
         __syncthreads();
     }
-
+    stamp(0, 2);
+#define ZOF(k) (a * (double)__uint_as_float((uint32_t)(ck[k] & 0xffffffffu)))
     // ---- Newton on the candidates
     double tauN = tau_lo;
     for (int it = 0; it < 200; ++it) {
         double F = 0.0, Fd = 0.0;
         for (int k = threadIdx.x; k < ncand; k += NT) {
-            const double d = zof(k) - tauN;
+            const double d = ZOF(k) - tauN;
             if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
         }
-        block_sum2_d<NT>(F, Fd, shd);
+        R.sum(F, Fd);
         if (!(Fd > 0.0)) break;
-        const double root = (ib == 1) ? F : (ib == 2) ? sqrt(F) : (ib == 4) ? sqrt(sqrt(F)) : pow(F, 1.0 / beta);
-        const double step = (root - 1.0) * F / (root * Fd);
+        const double step = lbeta_step(F, Fd, beta, ib);
         tauN += step;
-        if (!(fabs(step) > 2e-16 * fmax(1.0, fabs(tauN)))) break;
+        // 1e-14 relative is far inside the support band (R9) and the final tau is
+        // recomputed from the support; a tighter test can oscillate at the ulp level
+        if (!(fabs(step) > 1e-14 * fmax(1.0, fabs(tauN))) || it >= 63) break;
     }
     stamp(0, 3);
     // ---- support (R9)
     const double band = 1e-9 * fmax(1.0, fabs(tauN));
     int amb = 0;
     for (int k = threadIdx.x; k < ncand; k += NT) {
-        const double z = zof(k);
+        const double z = ZOF(k);
         const uint8_t f = (z > tauN + band) ? 1 : (z < tauN - band) ? 0 : 2;
         cin[k] = f;
         amb += (f == 2);
@@ -587,23 +676,22 @@ __global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
     if (amb > 0) {
         for (int k0 = 0; k0 < ncand; ++k0) {
             if (cin[k0] != 2) continue;
-            const double zk = zof(k0);
+            const double zk = ZOF(k0);
             double F = 0.0, dz = 0.0;
             for (int k = threadIdx.x; k < ncand; k += NT) {
-                const double d = zof(k) - zk;
+                const double d = ZOF(k) - zk;
                 if (d > 0.0) F += powb(d, beta, ib);
             }
-            block_sum2_d<NT>(F, dz, shd);
+            R.sum(F, dz);
             if (threadIdx.x == 0) cin[k0] = (F < 1.0) ? 1 : 0;
             __syncthreads();
         }
     }
-    stamp(0, 4);
     // ---- tau from the support
     double S1 = 0.0, kk = 0.0;
     for (int k = threadIdx.x; k < ncand; k += NT)
-        if (cin[k]) { S1 += zof(k); kk += 1.0; }
-    block_sum2_d<NT>(S1, kk, shd);
+        if (cin[k]) { S1 += ZOF(k); kk += 1.0; }
+    R.sum(S1, kk);
     double tau;
     if (ib == 1) {
         tau = (S1 - 1.0) / kk;
@@ -611,44 +699,80 @@ __global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
         const double m = S1 / kk;
         double ss = 0.0, dz = 0.0;
         for (int k = threadIdx.x; k < ncand; k += NT)
-            if (cin[k]) { const double d = zof(k) - m; ss += d * d; }
-        block_sum2_d<NT>(ss, dz, shd);
+            if (cin[k]) { const double d = ZOF(k) - m; ss += d * d; }
+        R.sum(ss, dz);
         tau = m - sqrt(fmax(0.0, 1.0 - ss) / kk);
     } else {
         double F = 0.0, Fd = 0.0;
         for (int k = threadIdx.x; k < ncand; k += NT)
-            if (cin[k]) { const double d = zof(k) - tauN; F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
-        block_sum2_d<NT>(F, Fd, shd);
+            if (cin[k]) { const double d = ZOF(k) - tauN; F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
+        R.sum(F, Fd);
         tau = tauN + (F - 1.0) / (beta * Fd);
     }
-    stamp(0, 5);
-    // ---- p and PV (warp per support token, lane = 4 dims)
+    stamp(0, 4);
+    // ---- p and PV: support compacted in candidate order (rounds of kSup entries), page-table
+    // entries fetched in parallel, then warp w gathers entries w, w + NW, ... (4 V rows in flight)
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     double psum = 0.0;
-    for (int k = warp; k < ncand; k += NT / 32) {
-        if (!cin[k]) continue;
-        const double d = zof(k) - tau;
-        const double pd = d > 0.0 ? powb(d, beta, ib) : 0.0;
-        if (lane == 0) psum += pd;
-        const float p = (float)pd;
-        float vx[4];
-        load_v4(v_row((int)(ck[k] >> 32)) + 4 * lane, vx);
+    for (int r0 = 0; r0 < ncand;) {
+        // take candidates [r0, r1) whose support count fits kSup (r1 multiple of NT)
+        int nsup = 0, r1 = r0;
+        while (r1 < ncand) {
+            const int k = r1 + threadIdx.x;
+            const bool in = k < ncand && cin[k];
+            int tot;
+            const int pos = nsup + block_excl_scan<NT>(in ? 1 : 0, shi, &tot);
+            if (nsup + tot > kSup) break;             // uniform
+            if (in) {
+                const int j = (int)(ck[k] >> 32);
+                const double d = ZOF(k) - tau;
+                const double pd = d > 0.0 ? powb(d, beta, ib) : 0.0;
+                sup_j[pos] = j;
+                sup_p[pos] = (float)pd;
+                sup_phys[pos] = have_phys ? cphys[k] : __ldg(c.page_table + (size_t)b * c.maxp + j / kP);
+                psum += pd;
+            }
+            nsup += tot;
+            r1 += NT;
+        }
+        __syncthreads();
+        for (int e0 = warp; e0 < nsup; e0 += 4 * NW) {
+            float vx[4][4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[e] = __fmaf_rn(p, vx[e], acc[e]);
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * NW;
+                if (e < nsup) {
+                    const int j = sup_j[e];
+                    ldv4<T>(Vb + (((size_t)sup_phys[e] * c.Hkv + kvh) * kP + (j % kP)) * kD + 4 * lane, vx[u]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * NW;
+                if (e < nsup) {
+                    const float p = sup_p[e];
+#pragma unroll
+                    for (int q2 = 0; q2 < 4; ++q2) acc[q2] = __fmaf_rn(p, vx[u][q2], acc[q2]);
+                }
+            }
+        }
+        __syncthreads();
+        r0 = r1;
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) red[warp][4 * lane + e] = acc[e];
-    const double pt = block_sum_d<NT>(psum, shd);
+    double pz = 0.0;
+    R.sum(psum, pz);
     if (threadIdx.x < kD) {
         float o = 0.f;
-        for (int w = 0; w < NT / 32; ++w) o = __fadd_rn(o, red[w][threadIdx.x]);
-        A.out[(size_t)row * kD + threadIdx.x] = (float)((double)o / pt);
+        for (int w = 0; w < NW; ++w) o = __fadd_rn(o, red[w][threadIdx.x]);
+        A.out[(size_t)row * kD + threadIdx.x] = (float)((double)o / psum);
     }
     if (threadIdx.x == 0) {
         if (A.tau_out) A.tau_out[row] = tau;
         if (A.supp_out) A.supp_out[row] = (int)kk;
     }
-    stamp(0, 6);
+    stamp(0, 5);
     // ---- eval list: support token positions and p (for exact delta / rho)
     if (A.tok_list) {
         int base = 0;
@@ -658,7 +782,7 @@ __global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
             int tot;
             const int pos = block_excl_scan<NT>(keep, shi, &tot);
             if (keep && base + pos < A.list_cap) {
-                const double d = zof(k) - tau;
+                const double d = ZOF(k) - tau;
                 A.tok_list[(size_t)row * A.list_cap + base + pos] = (int32_t)(ck[k] >> 32);
                 A.p_list[(size_t)row * A.list_cap + base + pos] = d > 0.0 ? powb(d, beta, ib) : 0.0;
             }
@@ -666,6 +790,8 @@ __global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
         }
         if (threadIdx.x == 0) A.n_list[row] = base;
     }
+#undef ZOF
+    stamp(0, 6);
 }
 
 // ============================================================================ a4: certified delta_bar

@@ -8,17 +8,18 @@ namespace ekv {
 // ============================================================================ a2: top-k
 // One CTA (NT threads) per (b, q-head) row (R3: key desc, then lower page
 // index).  Keys are the ordered-int encodings of the fp32 box scores (-0 == +0).
-//  1. Partition bound: thread t reads the keys {4(t + NT j) .. +3} (float4, coalesced,
-//     4 loads in flight per thread) and keeps their max m_t.  L = the k-th largest
-//     m_t, found MSB-first with __syncthreads_count.  At least k keys are >= L, so the
-//     k-th largest key T* >= L and every selected key is a candidate {key >= L}.
-//  2. Candidates are compacted into shared memory (warp ballot + one shared atomic per
-//     warp; their order does not matter: the selection is defined by (key, index)).
-//  3. T* by an MSB-first search over the candidates (__syncthreads_count per slot);
-//     ties at T* are broken by the smallest page indices (MSB-first over the index).
-//  4. The selection is marked in a shared bitmap and written ascending (block scan).
-// Overflow (more than kTopkCap candidates): the same searches run over all keys read
-// from global memory (L2) -- exact, slower.
+//  1. Partition bound: thread t reads the float4 groups {t + NT j} (coalesced, 8 loads in
+//     flight) and keeps each group's max; L = the k-th largest per-thread max (MSB-first
+//     with __syncthreads_count).  At least k keys are >= L, so T* (the k-th largest key)
+//     >= L and every selected key is a candidate {key >= L}.
+//  2. Groups whose max reaches L are listed in shared memory and re-read in parallel; the
+//     keys >= L are compacted into shared memory (order irrelevant: the selection is
+//     defined by (key, index)).
+//  3. T* and the tie cut (smallest indices first) by MSB-first searches run by warp 0
+//     alone over the shared candidates (warp reductions, no block barriers).
+//  4. The selection is marked in a shared bitmap, written ascending (block scan), and --
+//     if umask != NULL -- merged into the KV-group union (mask bits + compact list).
+// Overflow (more than kTopkCap candidates): exact block-wide searches over all keys.
 constexpr int kTopkCap = 8192;
 __device__ int ekv_dbg_nc;
 
@@ -31,76 +32,53 @@ __device__ __forceinline__ void topk_key4(const float *x, int i4, int M, bool ve
         for (int e = 0; e < 4; ++e) kk[e] = (i4 + e < M) ? f2key(__ldg(x + i4 + e)) : 0u;
     }
 }
-// #(candidates with key >= Tt) (or over all keys on overflow), block-wide
-template <int NT>
-__device__ __forceinline__ int topk_cnt_ge(uint32_t Tt, bool ovf, int nc, int slots, const uint32_t *ckey,
-                                           const float *x, int M, int *sh) {
-    if (!ovf) {
-        int c = 0;
-        for (int s2 = 0; s2 < slots; ++s2) {
-            const int j = s2 * NT + threadIdx.x;
-            c += __syncthreads_count(j < nc && ckey[j] >= Tt);
-        }
-        return c;
-    }
-    int c = 0;
-    for (int i = threadIdx.x; i < M; i += NT) c += f2key(__ldg(x + i)) >= Tt;
-    return block_sum_i<NT>(c, sh);
-}
-// #(key == T && idx < I), block-wide
-template <int NT>
-__device__ __forceinline__ int topk_cnt_eq_lt(uint32_t T, int I, bool ovf, int nc, int slots, const uint32_t *ckey,
-                                              const int32_t *cidx, const float *x, int M, int *sh) {
-    if (!ovf) {
-        int c = 0;
-        for (int s2 = 0; s2 < slots; ++s2) {
-            const int j = s2 * NT + threadIdx.x;
-            c += __syncthreads_count(j < nc && ckey[j] == T && cidx[j] < I);
-        }
-        return c;
-    }
-    int c = 0;
-    for (int i = threadIdx.x; i < min(M, I); i += NT) c += f2key(__ldg(x + i)) == T;
-    return block_sum_i<NT>(c, sh);
+
+// union mark of one selected page: bit g of the page's byte (fire-and-forget atomic)
+__device__ __forceinline__ void union_mark(uint32_t *um, int p, int g) {
+    atomicOr(um + (p >> 2), 1u << ((p & 3) * 8 + g));
 }
 
 template <int NT>
 __global__ void __launch_bounds__(NT, 1) k_topk(const float *__restrict__ box, int Hq, int maxp,
-                                             const int32_t *__restrict__ seq_lens, int k,
-                                             int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
-                                             int sel_stride) {
+                                                const int32_t *__restrict__ seq_lens, int k,
+                                                int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
+                                                int sel_stride, int G, uint32_t *__restrict__ umask, int W) {
+    constexpr int CPT = kTopkCap / NT;       // candidate slots per thread
     extern __shared__ __align__(16) unsigned char tk_smem[];
     uint32_t *ckey = reinterpret_cast<uint32_t *>(tk_smem);                 // [kTopkCap]
     int32_t *cidx = reinterpret_cast<int32_t *>(tk_smem + 4 * kTopkCap);    // [kTopkCap]
-    uint32_t *bits = reinterpret_cast<uint32_t *>(tk_smem + 8 * kTopkCap);  // [maxp/32]
-    __shared__ int sh[NT / 32 + 1];
-    __shared__ int s_cnt;
+    __shared__ uint32_t bits[2048];
+    __shared__ uint32_t hist[256];
+    __shared__ int sh[NT / 32 + 2];
     const int row = blockIdx.x;
     const int b = row / Hq;
     const int M = n_pages_of(seq_lens[b]);
     const int keff = min(k, M);
     int32_t *out = page_idx + (size_t)row * sel_stride;
+    const int unit = b * (Hq / G) + (row % Hq) / G, gh = (row % Hq) % G;
+    uint32_t *um = umask ? umask + (size_t)unit * W : nullptr;
+    stamp(1, 0);
     if (keff >= M) {
-        for (int p = threadIdx.x; p < M; p += NT) out[p] = p;
+        for (int p = threadIdx.x; p < M; p += NT) {
+            out[p] = p;
+            if (um) union_mark(um, p, gh);
+        }
         if (threadIdx.x == 0) n_sel[row] = M;
         return;
     }
-    stamp(1, 0);
     const float *x = box + (size_t)row * maxp;
-    const int W = (M + 31) / 32;
-    for (int w = threadIdx.x; w < W; w += NT) bits[w] = 0u;
-    if (threadIdx.x == 0) s_cnt = 0;
+    const int Wb = (M + 31) / 32;
+    for (int w = threadIdx.x; w < Wb; w += NT) bits[w] = 0u;
     const bool vec = (maxp & 3) == 0;
-    // 1. partition maxima: thread t owns the float4 groups {t + NT*j}; the max of each
-    //    group is kept (fp32 max == key max: f2key is monotone) for the second pass.
-    constexpr int GPT = 16;                  // groups per thread (M <= 16 * 4 * NT)
-    float gmax[GPT];
+    // 1. partition maxima: thread t owns the float4 groups {t + NT j}, j < GPT
+    constexpr int GPT = 16;                  // groups per thread (M <= 64 NT)
+    uint32_t gkey[GPT];
     uint32_t mt = 0u;
 #pragma unroll
-    for (int j0 = 0; j0 < GPT; j0 += 4) {
-        float4 v[4];
+    for (int j0 = 0; j0 < GPT; j0 += 8) {
+        float4 v[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
             const int i4 = 4 * (threadIdx.x + (j0 + u) * NT);
             if (vec && i4 + 3 < M) v[u] = __ldg(reinterpret_cast<const float4 *>(x + i4));
             else {
@@ -111,98 +89,135 @@ __global__ void __launch_bounds__(NT, 1) k_topk(const float *__restrict__ box, i
             }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
             const int i4 = 4 * (threadIdx.x + (j0 + u) * NT);
-            gmax[j0 + u] = (i4 < M) ? fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)) : NAN;
-            if (i4 < M) mt = max(mt, f2key(gmax[j0 + u]));
+            gkey[j0 + u] = (i4 < M) ? f2key(fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w))) : 0u;
+            mt = max(mt, gkey[j0 + u]);
         }
     }
-    __syncthreads();
     stamp(1, 1);
     uint32_t Lb = 1u;
-    if (keff <= NT) {
-        uint32_t T = 0u;
-        for (int bit = 31; bit >= 0; --bit) {
-            const uint32_t Tt = T | (1u << bit);
-            if (__syncthreads_count(mt >= Tt) >= keff) T = Tt;
-        }
-        Lb = T > 1u ? T : 1u;
+    int dummy;
+    // the bound needs at least k non-empty partitions (block_kth_largest requires k <= #keys)
+    if (keff <= NT && __syncthreads_count(mt != 0u) >= keff) {
+        const uint32_t km[1] = {mt};
+        Lb = block_kth_largest<NT, 1>(km, keff, hist, sh, &dummy);
+        if (Lb == 0u) Lb = 1u;
     }
     stamp(1, 2);
-    // 2. candidates: only groups whose max reaches L are re-read
+    // 2. candidates {key >= L}: re-read the hit groups (8 in flight), block-scan compaction
+    int nc = 0;
+    bool ovf = false;
 #pragma unroll
-    for (int j = 0; j < GPT; ++j) {
-        const int i4 = 4 * (threadIdx.x + j * NT);
-        const bool hit = (i4 < M) && f2key(gmax[j]) >= Lb;
-        if (__ballot_sync(0xffffffffu, hit) == 0u) continue;
-        uint32_t kk[4] = {0u, 0u, 0u, 0u};
-        if (hit) topk_key4(x, i4, M, vec, kk);
+    for (int j0 = 0; j0 < GPT; j0 += 8) {
+        uint32_t kk[8][4];
+        int cnt = 0;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const bool c = hit && kk[e] >= Lb;
-            const unsigned m = __ballot_sync(0xffffffffu, c);
-            if (!m) continue;
-            int pos = 0;
-            if ((threadIdx.x & 31) == 0) pos = atomicAdd(&s_cnt, __popc(m));
-            pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(m & ((1u << (threadIdx.x & 31)) - 1u));
-            if (c && pos < kTopkCap) { ckey[pos] = kk[e]; cidx[pos] = i4 + e; }
+        for (int u = 0; u < 8; ++u) {
+            const int i4 = 4 * (threadIdx.x + (j0 + u) * NT);
+            if (gkey[j0 + u] >= Lb) topk_key4(x, i4, M, vec, kk[u]);
+            else { kk[u][0] = kk[u][1] = kk[u][2] = kk[u][3] = 0u; }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) cnt += kk[u][e] >= Lb;
         }
+        int tot;
+        int pos = nc + block_excl_scan<NT>(cnt, sh, &tot);
+        if (nc + tot > kTopkCap) { ovf = true; break; }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (kk[u][e] >= Lb) { ckey[pos] = kk[u][e]; cidx[pos] = 4 * (threadIdx.x + (j0 + u) * NT) + e; ++pos; }
+        nc += tot;
     }
     __syncthreads();
-    const int nc = s_cnt;
-    const bool ovf = nc > kTopkCap;
     stamp(1, 3);
     if (threadIdx.x == 0 && blockIdx.x == 0) ekv_dbg_nc = nc;
-    const int slots = (nc + NT - 1) / NT;
-    // 3. T* = k-th largest candidate key (or key, on overflow)
-    uint32_t T = 0u;        // largest T with #(key >= T) >= k; holds for T <= L by step 1
-    for (int bit = 31; bit >= 0; --bit) {
-        const uint32_t Tt = T | (1u << bit);
-        if (Tt <= Lb || topk_cnt_ge<NT>(Tt, ovf, nc, slots, ckey, x, M, sh) >= keff) T = Tt;
-    }
-    const int n_gt = (T == 0xffffffffu) ? 0 : topk_cnt_ge<NT>(T + 1u, ovf, nc, slots, ckey, x, M, sh);
-    const int need = keff - n_gt;
-    stamp(1, 4);
-    int Ithr = M;                                    // select equal keys with idx < Ithr
-    if (topk_cnt_eq_lt<NT>(T, M, ovf, nc, slots, ckey, cidx, x, M, sh) > need) {
-        int I = 0;                                   // largest I with #(eq, idx < I) <= need
-        for (int bit = 17; bit >= 0; --bit) {
-            const int It = I + (1 << bit);
-            if (It <= M && topk_cnt_eq_lt<NT>(T, It, ovf, nc, slots, ckey, cidx, x, M, sh) <= need) I = It;
-        }
-        Ithr = I;
-    }
-    stamp(1, 5);
-    // 4. mark + ascending output
+    uint32_t T;
+    int n_gt, Ithr = M;
     if (!ovf) {
-        for (int j = threadIdx.x; j < nc; j += NT) {
-            const uint32_t kk = ckey[j];
-            const int i = cidx[j];
-            if (kk > T || (kk == T && i < Ithr)) atomicOr(&bits[i >> 5], 1u << (i & 31));
+        // 3. T* = k-th largest candidate (radix select), then the tie cut by index
+        uint32_t ck[CPT];
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+            const int e = j * NT + threadIdx.x;
+            ck[j] = e < nc ? ckey[e] : 0u;
+        }
+        T = block_kth_largest<NT, CPT>(ck, keff, hist, sh, &n_gt);
+        const int need = keff - n_gt;
+        int ceq = 0;
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) ceq += ck[j] == T;
+        if (block_sum_i<NT>(ceq, sh) > need) {
+            int I = 0;                       // largest I with #(eq, idx < I) <= need
+            for (int bit = 17; bit >= 0; --bit) {
+                const int It = I + (1 << bit);
+                if (It > M) continue;
+                int c = 0;
+#pragma unroll
+                for (int j = 0; j < CPT; ++j) {
+                    const int e = j * NT + threadIdx.x;
+                    c += (ck[j] == T && e < nc && cidx[e] < It);
+                }
+                if (block_sum_i<NT>(c, sh) <= need) I = It;
+            }
+            Ithr = I;
+        }
+        for (int e = threadIdx.x; e < nc; e += NT) {
+            const uint32_t kv = ckey[e];
+            const int i = cidx[e];
+            if (kv > T || (kv == T && i < Ithr)) atomicOr(&bits[i >> 5], 1u << (i & 31));
         }
     } else {
+        // exact fallback over all keys (bitwise threshold search, block-wide counts)
+        T = 0u;
+        for (int bit = 31; bit >= 0; --bit) {
+            const uint32_t Tt = T | (1u << bit);
+            int c = 0;
+            for (int i = threadIdx.x; i < M; i += NT) c += f2key(__ldg(x + i)) >= Tt;
+            if (block_sum_i<NT>(c, sh) >= keff) T = Tt;
+        }
+        int c = 0;
+        for (int i = threadIdx.x; i < M; i += NT) c += f2key(__ldg(x + i)) > T;
+        const int need = keff - block_sum_i<NT>(c, sh);
+        c = 0;
+        for (int i = threadIdx.x; i < M; i += NT) c += f2key(__ldg(x + i)) == T;
+        if (block_sum_i<NT>(c, sh) > need) {
+            int I = 0;
+            for (int bit = 17; bit >= 0; --bit) {
+                const int It = I + (1 << bit);
+                if (It > M) continue;
+                int c2 = 0;
+                for (int i = threadIdx.x; i < It; i += NT) c2 += f2key(__ldg(x + i)) == T;
+                if (block_sum_i<NT>(c2, sh) <= need) I = It;
+            }
+            Ithr = I;
+        }
         for (int i = threadIdx.x; i < M; i += NT) {
-            const uint32_t kk = f2key(__ldg(x + i));
-            if (kk > T || (kk == T && i < Ithr)) atomicOr(&bits[i >> 5], 1u << (i & 31));
+            const uint32_t kv = f2key(__ldg(x + i));
+            if (kv > T || (kv == T && i < Ithr)) atomicOr(&bits[i >> 5], 1u << (i & 31));
         }
     }
     __syncthreads();
-    const int wpt = (W + NT - 1) / NT;
+    stamp(1, 5);
+    // 4. ascending output (+ union marks)
+    const int wpt = (Wb + NT - 1) / NT;
     int cnt = 0;
     for (int w = 0; w < wpt; ++w) {
         const int wi = threadIdx.x * wpt + w;
-        if (wi < W) cnt += __popc(bits[wi]);
+        if (wi < Wb) cnt += __popc(bits[wi]);
     }
     int tot;
     int o = block_excl_scan<NT>(cnt, sh, &tot);
     for (int w = 0; w < wpt; ++w) {
         const int wi = threadIdx.x * wpt + w;
-        if (wi >= W) break;
+        if (wi >= Wb) break;
         uint32_t v = bits[wi];
         while (v) {
             const int bpos = __ffs(v) - 1;
             v &= v - 1;
             out[o++] = wi * 32 + bpos;
+            if (um) union_mark(um, wi * 32 + bpos, gh);
         }
     }
     if (threadIdx.x == 0) n_sel[row] = keff;
@@ -212,29 +227,18 @@ __global__ void __launch_bounds__(NT, 1) k_topk(const float *__restrict__ box, i
 // ============================================================================ union per KV group
 // The union of the G selections of a KV group (R17): umask[b][kvh][page] bytes (4 per
 // u32, bit g = selected by query head g of the group), zeroed by the host and filled
-// with atomicOr from the page lists; the head that sets a page's first bit also appends
-// the page to the group's compact list ulist[b][kvh][0..ucount) (order irrelevant: the
-// K-score kernel's result does not depend on the order in which pages are processed).
+// with atomicOr from the page lists.  The K-score kernel walks the G page lists of a
+// group and keeps a page only from its lowest selecting head (one read per union page).
 __global__ void __launch_bounds__(256) k_mark(int Hq, int G, const int32_t *__restrict__ page_idx,
                                               const int32_t *__restrict__ n_sel, int sel_stride,
-                                              uint32_t *__restrict__ umask, int W, int32_t *__restrict__ ulist,
-                                              int32_t *__restrict__ ucount, int ucap) {
+                                              uint32_t *__restrict__ umask, int W) {
     const int row = blockIdx.x;
     const int b = row / Hq, h = row % Hq;
-    const int kvh = h / G, g = h % G;
-    const int Hkv = Hq / G;
-    const int unit = b * Hkv + kvh;
+    const int unit = b * (Hq / G) + h / G, g = h % G;
     const int n = n_sel[row];
     const int32_t *pl = page_idx + (size_t)row * sel_stride;
     uint32_t *um = umask + (size_t)unit * W;
-    for (int i = threadIdx.x; i < n; i += 256) {
-        const int p = pl[i];
-        const uint32_t old = atomicOr(um + (p >> 2), 1u << ((p & 3) * 8 + g));
-        if (((old >> ((p & 3) * 8)) & 0xffu) == 0u) {
-            const int pos = atomicAdd(ucount + unit, 1);
-            if (pos < ucap) ulist[(size_t)unit * ucap + pos] = p;
-        }
-    }
+    for (int i = threadIdx.x; i < n; i += 256) union_mark(um, pl[i], g);
 }
 
 // ============================================================================ a2': Gaussian selector

@@ -25,3 +25,6 @@ print('K4 consumer stage done    ', [ (x-v[0])/1000 if x else None for x in w[16
 w=[buf[4*32+i] for i in range(32)]
 print('score consumer arrivals', [ (x-w[0])/1000 if x else None for x in w[:16]])
 print('score consumer done    ', [ (x-w[0])/1000 if x else None for x in w[16:32]])
+v=[buf[0*32+i] for i in range(8)]; cl=[buf[0*32+16+i] for i in range(8)]
+i0=0; i1=max(i for i in range(8) if v[i])
+print('tau kernel SM clock MHz ~', (cl[i1]-cl[i0])/((v[i1]-v[i0])/1e3)/1e6*1e6/1e6 if v[i1]>v[i0] else None, 'cycles per phase', [cl[i]-cl[i0] for i in range(8) if v[i]])
