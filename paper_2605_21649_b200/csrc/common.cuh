@@ -337,9 +337,23 @@ __device__ __forceinline__ void stamp_if(bool cond, int k, int i) {
         ekv_stamps[k][i] = t;
     }
 }
+// per-CTA timeline of one instrumented kernel: [0] start, [1] first data, [2] end, [3] count
+__device__ unsigned long long ekv_cta[4][1024];
+__device__ __forceinline__ void stamp_cta(bool cond, int which) {
+    if (cond && blockIdx.x < 1024) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        ekv_cta[which][blockIdx.x] = t;
+    }
+}
+__device__ __forceinline__ void count_cta(bool cond, unsigned long long v) {
+    if (cond && blockIdx.x < 1024) ekv_cta[3][blockIdx.x] = v;
+}
 #else
 __device__ __forceinline__ void stamp(int, int) {}
 __device__ __forceinline__ void stamp_if(bool, int, int) {}
+__device__ __forceinline__ void stamp_cta(bool, int) {}
+__device__ __forceinline__ void count_cta(bool, unsigned long long) {}
 #endif
 }  // namespace ekv
 
@@ -430,5 +444,18 @@ __device__ uint32_t block_kth_largest(const uint32_t (&key)[CPT], int k, uint32_
     }
     *n_gt = above;
     return prefix;
+}
+}  // namespace ekv
+
+namespace ekv {
+// packed fp32x2 add (sm_100: FADD2): two independent IEEE round-to-nearest adds
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    unsigned long long ra, rb, rd;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1,%2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(rd) : "l"(ra), "l"(rb));
+    float2 d;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
+    return d;
 }
 }  // namespace ekv

@@ -218,7 +218,7 @@ ekv_status launch_scores_t(const CacheView &v, const void *q, int Hq, const uint
     long long gx = (slots + 31) / 32;                                // >= 32 work slots per CTA
     if (gx > per_sm * num_sms()) gx = per_sm * num_sms();
     if (gx < 1) gx = 1;
-    k_attend_scores<T, G><<<(unsigned)gx, 288, smem, st>>>(v, static_cast<const T *>(q), Hq, um, W, pi, ns, stride,
+    k_attend_scores<T, G><<<(unsigned)gx, 32 * (AttCfg<T>::NCW + 1), smem, st>>>(v, static_cast<const T *>(q), Hq, um, W, pi, ns, stride,
                                                            scores, rowmax, full);
     return check_launch("k_attend_scores");
 }
@@ -318,6 +318,15 @@ int32_t entmaxkv_last_launch_count(void) { return g_launches; }
 
 /* Debug (not in the public header): copy in-kernel phase stamps (ns) and the last top-k
  * candidate count; returns 0 when the library was built without -DEKV_STAMPS. */
+int entmaxkv_debug_cta(unsigned long long *out /*[4*1024]*/) {
+#ifdef EKV_STAMPS
+    cudaMemcpyFromSymbol(out, ekv::ekv_cta, sizeof(unsigned long long) * 4 * 1024);
+    return 1;
+#else
+    (void)out;
+    return 0;
+#endif
+}
 int entmaxkv_debug_stamps(unsigned long long *out /*[8*32]*/, int *nc) {
 #ifdef EKV_STAMPS
     cudaMemcpyFromSymbol(out, ekv_stamps, sizeof(unsigned long long) * 8 * 32);
@@ -501,8 +510,8 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
     if (want_db) {
         const int nch = (maxp + kDbChunk - 1) / kDbChunk;
         dim3 g(nch, rows);
-        k_delta_bar<<<g, 256, 0, st>>>(box, maxp, cache->seq_lens, n_q_heads, pi, ns, L.cap, tau_p, attn->alpha,
-                                       at<double>(workspace, L.db_partial), nch,
+        k_delta_bar<<<g, 256, 0, st>>>(box, maxp, cache->seq_lens, n_q_heads, Gq, uo.umask, L.W, tau_p,
+                                       attn->alpha, at<double>(workspace, L.db_partial), nch,
                                        at<unsigned int>(workspace, L.tickets), stats->delta_bar);
         EKV_TRY(check_launch("k_delta_bar"));
     }

@@ -11,47 +11,54 @@ namespace ekv {
 // are written.  rowmax[b][h] holds the ordered-int max score (atomicMax; 0 = empty).
 
 // ============================================================================ K scores
-// Persistent, warp-specialised: grid = ~2 CTAs per SM, 288 threads = 8 consumer warps
-// (16 half-warps) + 1 producer warp.  The flattened (unit = b*Hkv + kvh, page) space
-// is split into equal contiguous ranges, one per CTA.
-//  - Producer warp: scans its range 32 pages at a time (ballot over the union mask
-//    byte, or every page for the full baseline), packs selected pages into ring stages
-//    of SP pages and issues one cp.async.bulk (TMA, 1-D) per page tile
-//    K[phys][kvh][0..P)[0..d) (4 KiB bf16, contiguous in HBM) completing on the
-//    stage's `full` mbarrier; it waits on the stage's `empty` mbarrier before reuse.
-//    A stage with n = -1 ends the stream.
-//  - Consumers: two half-warps per page, 8 tokens each: lane c reads the 16-byte chunk
-//    c of the token row from shared memory (contiguous 256-byte row per half-warp:
-//    conflict-free), runs the 8-element fma chains for the G query heads (R1; q is
-//    reloaded when the unit changes) and the reduce-scatter tree; s = fl32(dot * c_d)
-//    (R2).  Tokens past seq_len get -inf.  Running per-head max, flushed with one
-//    atomicMax per (half-warp, unit) into rowmax.
+// Persistent, warp-specialised: 160 threads = 4 consumer warps + 1 producer warp,
+// 2 CTAs per SM (bf16).  The flattened work space (sparse: (row, i) over the page lists,
+// each union page kept once -- from its lowest selecting head; full: (unit, page)) is
+// split into equal contiguous ranges, one per CTA.
+//  - Producer warp: collects the range's pages (page-table and union-mask lookups in
+//    parallel), packs them into ring stages of SP = 8 pages and issues one
+//    cp.async.bulk (TMA, 1-D) copy per page of the contiguous tile K[phys][kvh][0..P)[0..d)
+//    completing on the stage's `full` mbarrier; it waits on the stage's `empty` mbarrier
+//    before reuse.  n = -1 ends.  (Per-row copies into a padded layout were tried: 16
+//    small copies per page are TMA-issue bound, ~2x slower.)
+//  - Consumers: warp w scores pages 2w, 2w+1 of the stage, lane = token t: the lane
+//    computes dot16x8 (R1) for the G query heads entirely in registers -- 16 chunk
+//    partials per head (fma chains, packed FFMA2 over head pairs; 64 independent chains
+//    of ILP) and the pairwise tree c+(c+8), c+(c+4), c+(c+2), c0+c1 with packed adds --
+//    q is read from shared memory.  Bank conflicts: lane t handles chunk c ^ (t & 7) in
+//    register slot c, so 8 consecutive lanes (rows 256 B apart) read 8 distinct 16-byte
+//    bank groups; XOR-relabelling with s < 8 maps the butterfly's pairs (x, x+2^j) onto
+//    themselves and fp add commutes, so slot 0 ends bit-identical to R1's tree.  q rows
+//    are padded by 16 B per chunk for the same reason.  s = fl32(dot * c_d) (R2); -inf
+//    past seq_len; stores of 32 consecutive tokens per head are coalesced.  Per-head
+//    running max, flushed with one atomicMax per (warp, unit) into rowmax.
 template <typename T> struct AttCfg {
-    static constexpr int SP = 8, NS = 3;
+    static constexpr int NCW = 4;                          // consumer warps
+    static constexpr int SP = 2 * NCW;                     // pages per stage
+    static constexpr int NS = 3;                           // ring stages
     static constexpr int TILE = kP * kD * (int)sizeof(T);
     static constexpr int SMEM = NS * SP * TILE;
 };
 
 template <typename T, int G>
-__global__ void __launch_bounds__(288) k_attend_scores(CacheView c, const T *__restrict__ q, int Hq,
-                                                       const uint32_t *__restrict__ umask, int W,
-                                                       const int32_t *__restrict__ page_idx,
-                                                       const int32_t *__restrict__ n_sel, int stride,
-                                                       float *__restrict__ scores, uint32_t *__restrict__ rowmax,
-                                                       int full) {
+__global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1)) k_attend_scores(
+    CacheView c, const T *__restrict__ q, int Hq, const uint32_t *__restrict__ umask, int W,
+    const int32_t *__restrict__ page_idx, const int32_t *__restrict__ n_sel, int stride,
+    float *__restrict__ scores, uint32_t *__restrict__ rowmax, int full) {
     constexpr int SP = AttCfg<T>::SP, NS = AttCfg<T>::NS, TILE = AttCfg<T>::TILE;
-    constexpr int NCW = 8;
-    constexpr int CHK = 256;                // list entries per producer chunk (8 per lane)
+    constexpr int NCW = AttCfg<T>::NCW;
+    constexpr int CHK = 256;                // work slots per producer chunk (8 per lane)
+    constexpr int GP = (G + 1) / 2;         // head pairs
     extern __shared__ __align__(128) unsigned char smem[];   // [NS][SP][TILE]
     __shared__ uint64_t fullb[NS], emptyb[NS];
     __shared__ int d_page[NS][SP], d_unit[NS][SP], d_phys[NS][SP], d_n[NS];
     __shared__ uint8_t d_mask[NS][SP];
     __shared__ int l_unit[CHK], l_page[CHK], l_phys[CHK];
     __shared__ uint8_t l_mask[CHK];
+    constexpr int QCH = 8 * GP + 2;         // float2 per q chunk row (8 dims x GP pairs + 16 B pad)
+    __shared__ __align__(16) float2 qs[NCW][16 * QCH];      // per-warp copy of q (head pairs)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // flattened work space.  sparse: (row = b*Hq + h, i < stride) over the page lists; a page
-    // is kept only from its lowest selecting head of the group (union mask byte).  full:
-    // (unit = b*Hkv + kvh, page).
+    stamp_cta(threadIdx.x == 0, 0);
     const int ucap = full ? c.maxp : stride;
     const long long tot = full ? (long long)c.B * c.Hkv * c.maxp : (long long)c.B * Hq * stride;
     const long long f0 = tot * blockIdx.x / gridDim.x, f1 = tot * (blockIdx.x + 1) / gridDim.x;
@@ -62,12 +69,8 @@ __global__ void __launch_bounds__(288) k_attend_scores(CacheView c, const T *__r
     __syncthreads();
     if (warp == NCW) {
         // ------------------------------------------------ producer
-        // Chunks of 256 work slots: 8 independent loads per lane (list entry / page), then
-        // the page-table and mask lookups in parallel, ballot compaction into a shared
-        // list, and lane 0 packs the list into ring stages of SP page tiles (TMA).
         const unsigned char *Kb = reinterpret_cast<const unsigned char *>(c.K);
         int si = 0, fill = 0;
-        stamp_if(lane == 0, 2, 0);
         int cu = (int)(f0 / ucap), cs = (int)(f0 % ucap);   // (row or unit, slot) of the chunk start
         for (long long cb = f0; cb < f1; cb += CHK) {
             int un[CHK / 32], pg[CHK / 32], hg[CHK / 32];
@@ -76,8 +79,7 @@ __global__ void __launch_bounds__(288) k_attend_scores(CacheView c, const T *__r
             for (int r = 0; r < CHK / 32; ++r) {
                 int u = cu, sl = cs + r * 32 + lane;
                 while (sl >= ucap) { sl -= ucap; ++u; }
-                // u: full -> unit; sparse -> row (b*Hq + h)
-                const int bb = full ? u / c.Hkv : u / Hq;
+                const int bb = full ? u / c.Hkv : u / Hq;      // u: full -> unit; sparse -> row
                 un[r] = full ? u : bb * c.Hkv + (u % Hq) / G;
                 hg[r] = full ? 0 : (u % Hq) % G;
                 ok[r] = false;
@@ -114,37 +116,42 @@ __global__ void __launch_bounds__(288) k_attend_scores(CacheView c, const T *__r
                 nl += __popc(bal);
             }
             __syncwarp();
-            if (lane == 0) {
-                for (int i = 0; i < nl; ++i) {
-                    const int slot = si % NS;
-                    if (fill == 0 && si >= NS) mbar_wait(&emptyb[slot], ((si / NS) - 1) & 1);
+            for (int i = 0; i < nl; ++i) {          // warp-uniform
+                const int slot = si % NS;
+                if (fill == 0) {
+                    if (lane == 0 && si >= NS) mbar_wait(&emptyb[slot], ((si / NS) - 1) & 1);
+                    __syncwarp();
+                }
+                if (lane == 0) {
                     d_unit[slot][fill] = l_unit[i]; d_page[slot][fill] = l_page[i];
                     d_mask[slot][fill] = l_mask[i]; d_phys[slot][fill] = l_phys[i];
-                    if (++fill == SP) {
-                        d_n[slot] = SP;
-                        mbar_expect_tx(&fullb[slot], (uint32_t)(SP * TILE));
-                        for (int k = 0; k < SP; ++k)
-                            bulk_g2s(smem + ((size_t)slot * SP + k) * TILE,
-                                     Kb + ((size_t)d_phys[slot][k] * c.Hkv + d_unit[slot][k] % c.Hkv) * TILE, TILE,
-                                     &fullb[slot]);
-                        ++si;
-                        fill = 0;
-                    }
+                }
+                if (++fill == SP) {
+                    __syncwarp();
+                    if (lane == 0) { d_n[slot] = SP; mbar_expect_tx(&fullb[slot], (uint32_t)(SP * TILE)); }
+                    __syncwarp();
+                    if (lane < SP)
+                        bulk_g2s(smem + ((size_t)slot * SP + lane) * TILE,
+                                 Kb + ((size_t)d_phys[slot][lane] * c.Hkv + d_unit[slot][lane] % c.Hkv) * TILE,
+                                 TILE, &fullb[slot]);
+                    ++si;
+                    fill = 0;
                 }
             }
             __syncwarp();
         }
+        if (fill > 0) {
+            const int slot = si % NS;
+            __syncwarp();
+            if (lane == 0) { d_n[slot] = fill; mbar_expect_tx(&fullb[slot], (uint32_t)(fill * TILE)); }
+            __syncwarp();
+            if (lane < fill)
+                bulk_g2s(smem + ((size_t)slot * SP + lane) * TILE,
+                         Kb + ((size_t)d_phys[slot][lane] * c.Hkv + d_unit[slot][lane] % c.Hkv) * TILE,
+                         TILE, &fullb[slot]);
+            ++si;
+        }
         if (lane == 0) {
-            if (fill > 0) {
-                const int slot = si % NS;
-                d_n[slot] = fill;
-                mbar_expect_tx(&fullb[slot], (uint32_t)(fill * TILE));
-                for (int k = 0; k < fill; ++k)
-                    bulk_g2s(smem + ((size_t)slot * SP + k) * TILE,
-                             Kb + ((size_t)d_phys[slot][k] * c.Hkv + d_unit[slot][k] % c.Hkv) * TILE, TILE,
-                             &fullb[slot]);
-                ++si;
-            }
             const int slot = si % NS;           // end marker
             if (si >= NS) mbar_wait(&emptyb[slot], ((si / NS) - 1) & 1);
             d_n[slot] = -1;
@@ -152,81 +159,98 @@ __global__ void __launch_bounds__(288) k_attend_scores(CacheView c, const T *__r
         }
         return;
     }
-    // ---------------------------------------------------- consumers
-    // Two tokens per iteration: the 2G partials (token-major) go through one 16-lane
-    // reduce-scatter (same pairing tree per value as rs_reduce16<G>: bit-identical).
-    constexpr int V = 2 * G;                // values reduced together
-    constexpr int GP = (G + 1) / 2;         // head pairs for FFMA2
-    const int l16 = threadIdx.x & 15, hw = threadIdx.x >> 4;
-    const int vsel = rs_head<V>(lane);
-    const int tsel = vsel / G, hsel = vsel % G;   // token (0/1) and head this lane reduces
-    const bool writer = rs_writer<V>(lane);
-    const int pi_local = hw >> 1;           // page within the stage (2 half-warps per page)
-    const int t0 = (hw & 1) * 8;            // first token of this half-warp
+    // ---------------------------------------------------- consumers (lane = token)
     const size_t ntok = (size_t)c.maxp * kP;
-    float2 qr[GP][8];
+    const int pp = lane >> 4, t = lane & 15;      // page (0/1) of the warp's pair, token in page
     int cur_unit = -1, L = 0;
-    float runmax = -INFINITY;
-    float *srow = nullptr;
+    float runmax[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) runmax[g] = -INFINITY;
+    auto flush = [](const float (&rm)[G], int unit, const CacheView &cv, int Hq_, uint32_t *rmx) {
+        int bb = unit / cv.Hkv, kh = unit % cv.Hkv;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            float m = rm[g];
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if ((threadIdx.x & 31) == 0 && m > -INFINITY)
+                atomicMax(rmx + (size_t)bb * Hq_ + kh * G + g, f2key(m));
+        }
+    };
     for (int si = 0;; ++si) {
         const int slot = si % NS;
         mbar_wait(&fullb[slot], (si / NS) & 1);
         const int n = d_n[slot];
+        stamp_cta(threadIdx.x == 0 && si == 0, 1);
         stamp_if(threadIdx.x == 0 && si < 16, 3, si);
-        if (n < 0) break;
-        const bool active = pi_local < n;   // warp-uniform (both half-warps share the page)
-        const int unit = d_unit[slot][active ? pi_local : 0];
-        if (active && unit != cur_unit) {
-            if (cur_unit >= 0 && writer && runmax > -INFINITY) {
-                const int bb = cur_unit / c.Hkv, kh = cur_unit % c.Hkv;
-                atomicMax(rowmax + (size_t)bb * Hq + kh * G + hsel, f2key(runmax));
-            }
-            runmax = -INFINITY;
-            cur_unit = unit;
-            const int bb = unit / c.Hkv, kh = unit % c.Hkv;
-            L = c.seq_lens[bb];
+        if (n < 0) { stamp_cta(threadIdx.x == 0, 2); count_cta(threadIdx.x == 0, si); break; }
+        const int k = 2 * warp + pp;              // page of this lane within the stage
+        if (2 * warp < n) {                       // warp-uniform
+            const bool act = k < n;
+            const int unitA = d_unit[slot][2 * warp];
+            const int unitB = d_unit[slot][act ? k : 2 * warp];
+            const int unitB16 = __shfl_sync(0xffffffffu, unitB, 16);
+            const bool split = unitB16 != unitA;  // warp-uniform
+            // both pages of a warp normally share the unit; if not, process them one at a time
+            for (int part = 0; part < (split ? 2 : 1); ++part) {
+                const int u_here = part == 0 ? unitA : unitB16;
+                const bool mine = act && (!split || pp == part);
+                if (u_here != cur_unit) {                                      // warp-uniform
+                    if (cur_unit >= 0) flush(runmax, cur_unit, c, Hq, rowmax);
 #pragma unroll
-            for (int g = 0; g < GP; ++g) {
-                float x0[8], x1[8];
-                Elem<T>::load8(q + ((size_t)bb * Hq + kh * G + 2 * g) * kD + 8 * l16, x0);
-                if (2 * g + 1 < G) Elem<T>::load8(q + ((size_t)bb * Hq + kh * G + 2 * g + 1) * kD + 8 * l16, x1);
-                else {
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) x1[e] = 0.0f;
+                    for (int g = 0; g < G; ++g) runmax[g] = -INFINITY;
+                    cur_unit = u_here;
+                    const int bb = u_here / c.Hkv, kh = u_here % c.Hkv;
+                    L = c.seq_lens[bb];
+                    __syncwarp();
+                    for (int e = lane; e < kD * G; e += 32) {       // q -> shared (head pairs)
+                        const int i = e / G, g = e % G;
+                        const float v = Elem<T>::to_f(q[((size_t)bb * Hq + kh * G + g) * kD + i]);
+                        float2 &dst = qs[warp][(i >> 3) * QCH + (i & 7) * GP + (g >> 1)];
+                        if (g & 1) dst.y = v; else dst.x = v;
+                        if ((G & 1) && g == G - 1) dst.y = 0.0f;
+                    }
+                    __syncwarp();
                 }
+                if (!mine) continue;
+                const int page = d_page[slot][k];
+                const uint8_t msk = d_mask[slot][k];
+                const T *row = reinterpret_cast<const T *>(smem + ((size_t)slot * SP + k) * TILE) + t * kD;
+                const int sw = t & 7;
+                float2 acc[16][GP];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) qr[g][e] = make_float2(x0[e], x1[e]);
-            }
-            srow = scores + ((size_t)bb * Hq + kh * G + hsel) * ntok;
-        }
-        if (active) {
-            const int page = d_page[slot][pi_local];
-            const bool hok = (d_mask[slot][pi_local] >> hsel) & 1;
-            const T *tile = reinterpret_cast<const T *>(smem + ((size_t)slot * SP + pi_local) * TILE);
-#pragma unroll 2
-            for (int tt = 0; tt < 8; tt += 2) {
-                const int ta = t0 + tt;
-                float ka[8], kb[8];
-                Elem<T>::load8(tile + ta * kD + 8 * l16, ka);
-                Elem<T>::load8(tile + (ta + 1) * kD + 8 * l16, kb);
-                float acc[V];
+                for (int cch = 0; cch < 16; ++cch) {
+                    const int ch = cch ^ sw;              // chunk held in register slot cch
+                    float kx[8];
+                    Elem<T>::load8(row + 8 * ch, kx);
+                    const float2 *qc = &qs[warp][ch * QCH];
 #pragma unroll
-                for (int g = 0; g < GP; ++g) {
-                    float2 a2 = make_float2(0.0f, 0.0f), b2 = make_float2(0.0f, 0.0f);
+                    for (int hp = 0; hp < GP; ++hp) acc[cch][hp] = make_float2(0.0f, 0.0f);
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
-                        a2 = ffma2(qr[g][e], ka[e], a2);
-                        b2 = ffma2(qr[g][e], kb[e], b2);
+#pragma unroll
+                        for (int hp = 0; hp < GP; ++hp) acc[cch][hp] = ffma2(qc[e * GP + hp], kx[e], acc[cch][hp]);
                     }
-                    acc[2 * g] = a2.x; acc[G + 2 * g] = b2.x;
-                    if (2 * g + 1 < G) { acc[2 * g + 1] = a2.y; acc[G + 2 * g + 1] = b2.y; }
                 }
-                const float sres = __fmul_rn(rs_reduce16<V>(acc, lane), kCd);
-                const int tok = page * kP + ta + tsel;
-                if (writer && hok) {
-                    const float v = tok < L ? sres : -INFINITY;
-                    srow[tok] = v;
-                    runmax = fmaxf(runmax, v);
+#pragma unroll
+                for (int hp = 0; hp < GP; ++hp) {
+#pragma unroll
+                    for (int cch = 0; cch < 8; ++cch) acc[cch][hp] = fadd2(acc[cch][hp], acc[cch + 8][hp]);
+#pragma unroll
+                    for (int cch = 0; cch < 4; ++cch) acc[cch][hp] = fadd2(acc[cch][hp], acc[cch + 4][hp]);
+#pragma unroll
+                    for (int cch = 0; cch < 2; ++cch) acc[cch][hp] = fadd2(acc[cch][hp], acc[cch + 2][hp]);
+                    acc[0][hp] = fadd2(acc[0][hp], acc[1][hp]);
+                }
+                const int tok = page * kP + t;
+                const int bb = u_here / c.Hkv, kh = u_here % c.Hkv;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    if (!((msk >> g) & 1)) continue;
+                    const float sv = __fmul_rn((g & 1) ? acc[0][g >> 1].y : acc[0][g >> 1].x, kCd);
+                    const float v = tok < L ? sv : -INFINITY;
+                    scores[((size_t)bb * Hq + kh * G + g) * ntok + tok] = v;
+                    runmax[g] = fmaxf(runmax[g], v);
                 }
             }
         }
@@ -234,10 +258,7 @@ __global__ void __launch_bounds__(288) k_attend_scores(CacheView c, const T *__r
         stamp_if(threadIdx.x == 0 && si < 16, 3, 16 + si);
         if (lane == 0) mbar_arrive(&emptyb[slot]);
     }
-    if (cur_unit >= 0 && writer && runmax > -INFINITY) {
-        const int bb = cur_unit / c.Hkv, kh = cur_unit % c.Hkv;
-        atomicMax(rowmax + (size_t)bb * Hq + kh * G + hsel, f2key(runmax));
-    }
+    if (cur_unit >= 0) flush(runmax, cur_unit, c, Hq, rowmax);
 }
 
 // ============================================================================ candidates
@@ -802,52 +823,54 @@ __global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
 // counter) adds the partials in chunk order, so the result is deterministic.
 constexpr int kDbChunk = 2048;
 __global__ void __launch_bounds__(256) k_delta_bar(const float *__restrict__ box, int maxp,
-                                                   const int32_t *__restrict__ seq_lens, int Hq,
-                                                   const int32_t *__restrict__ page_idx,
-                                                   const int32_t *__restrict__ n_sel, int sel_stride,
+                                                   const int32_t *__restrict__ seq_lens, int Hq, int G,
+                                                   const uint32_t *__restrict__ umask, int W,
                                                    const double *__restrict__ tau, float alpha,
                                                    double *__restrict__ partial, int nchunks,
                                                    unsigned int *__restrict__ tickets, double *__restrict__ out) {
-    __shared__ uint32_t bits[kDbChunk / 32];
-    __shared__ double shd[18];
+    __shared__ double rbuf[2 * 2 * 8];
     __shared__ bool s_last;
-    const int row = blockIdx.y, b = row / Hq;
+    BlockRed2<256> R{rbuf, 0};
+    const int row = blockIdx.y, b = row / Hq, h = row % Hq;
+    const int unit = b * (Hq / G) + h / G, g = h % G;
     const int L = seq_lens[b];
     const int M = n_pages_of(L);
     const int p0 = blockIdx.x * kDbChunk;
+    // all loads first: 8 box scores (2 float4) and 2 mask words per thread
+    const float *bx = box + (size_t)row * maxp;
+    float bv[8];
+    uint32_t mw[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int p = p0 + 4 * (threadIdx.x + 256 * r);
+        if (p + 3 < M && (maxp & 3) == 0) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(bx + p));
+            bv[4 * r] = v.x; bv[4 * r + 1] = v.y; bv[4 * r + 2] = v.z; bv[4 * r + 3] = v.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) bv[4 * r + e] = (p + e < M) ? __ldg(bx + p + e) : -INFINITY;
+        }
+        mw[r] = (p < M) ? __ldg(umask + (size_t)unit * W + (p >> 2)) : 0u;
+    }
     const double t = tau[row];
     const double a = (double)alpha - 1.0, beta = 1.0 / a;
     const int ib = (fabs(beta - rint(beta)) < 1e-12 && beta <= 4.5) ? (int)rint(beta) : 0;
-    for (int w = threadIdx.x; w < kDbChunk / 32; w += 256) bits[w] = 0u;
-    __syncthreads();
-    const int32_t *pl = page_idx + (size_t)row * sel_stride;
-    const int ns = n_sel[row];
-    for (int i = threadIdx.x; i < ns; i += 256) {
-        const int p = pl[i] - p0;
-        if (p >= 0 && p < kDbChunk) atomicOr(&bits[p >> 5], 1u << (p & 31));
-    }
-    __syncthreads();
     double db = 0.0, dz = 0.0;
-    const float *bx = box + (size_t)row * maxp;
     if (t == t) {   // tau is NaN for an empty row
         // fp32 pre-test: a*box - tau > 0 needs box > tau/a; thr is rounded well below it
         const float thr = (float)(t / a) - 1e-3f * fmaxf(1.0f, fabsf((float)(t / a)));
-        float bv[kDbChunk / 256];
 #pragma unroll
-        for (int r = 0; r < kDbChunk / 256; ++r) {
-            const int p = p0 + threadIdx.x + 256 * r;
-            bv[r] = p < M ? __ldg(bx + p) : -INFINITY;
-        }
+        for (int r = 0; r < 2; ++r)
 #pragma unroll
-        for (int r = 0; r < kDbChunk / 256; ++r) {
-            const int i = threadIdx.x + 256 * r;
-            const int p = p0 + i;
-            if (!(bv[r] > thr) || ((bits[i >> 5] >> (i & 31)) & 1u)) continue;
-            const double d = a * (double)bv[r] - t;
-            if (d > 0.0) db += (double)min(kP, L - p * kP) * powb(d, beta, ib);
-        }
+            for (int e = 0; e < 4; ++e) {
+                const int p = p0 + 4 * (threadIdx.x + 256 * r) + e;
+                const bool sel = (mw[r] >> (8 * e + g)) & 1u;      // page selected by head h
+                if (p >= M || sel || !(bv[4 * r + e] > thr)) continue;
+                const double d = a * (double)bv[4 * r + e] - t;
+                if (d > 0.0) db += (double)min(kP, L - p * kP) * powb(d, beta, ib);
+            }
     }
-    block_sum2_d<256>(db, dz, shd);
+    R.sum(db, dz);
     if (threadIdx.x == 0) {
         partial[(size_t)row * nchunks + blockIdx.x] = db;
         __threadfence();
@@ -857,12 +880,12 @@ __global__ void __launch_bounds__(256) k_delta_bar(const float *__restrict__ box
     __syncthreads();
     if (s_last && threadIdx.x < 32) {       // fixed lane -> chunk map and shuffle tree: deterministic
         __threadfence();
-        double s = 0.0;
-        for (int c2 = threadIdx.x; c2 < nchunks; c2 += 32) s += ((volatile double *)partial)[(size_t)row * nchunks + c2];
+        double sum = 0.0;
+        for (int c2 = threadIdx.x; c2 < nchunks; c2 += 32) sum += ((volatile double *)partial)[(size_t)row * nchunks + c2];
 #pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        for (int o = 16; o >= 1; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
         if (threadIdx.x == 0) {
-            out[row] = (t == t) ? s : NAN;
+            out[row] = (t == t) ? sum : NAN;
             tickets[row] = 0u;             // ready for the next call
         }
     }
