@@ -15,7 +15,8 @@
  *    (256-byte aligned); distinct concurrent calls need distinct workspaces.
  *  - Work is enqueued on `stream` (a cudaStream_t passed as void*; NULL = the
  *    legacy default stream).  Calls are CUDA-graph capturable.
- *  - Layouts are row-major, innermost dimension last.  Supported shapes:
+ *  - Layouts are row-major, innermost dimension last; q, k_pages and v_pages must be
+ *    16-byte aligned (else EKV_ERR_INVALID_ARG).  Supported shapes:
  *    head_dim = value_dim = 128 (R1), page_size = 16, n_kv_heads in {1,2,4,8,16},
  *    G = n_q_heads / n_kv_heads in {1,2,4,8}, max_pages_per_seq <= 65536.
  *    Anything else -> EKV_ERR_UNSUPPORTED.

@@ -250,13 +250,26 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+#ifndef EKV_MBAR_HINT
+#define EKV_MBAR_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+#if EKV_MBAR_HINT
+    // try_wait with a suspend-time hint (ns): the warp may sleep until the phase completes
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase), "r"((unsigned)EKV_MBAR_HINT)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
         "r"(phase)
         : "memory");
+#endif
 }
 
 }  // namespace ekv
@@ -337,23 +350,27 @@ __device__ __forceinline__ void stamp_if(bool cond, int k, int i) {
         ekv_stamps[k][i] = t;
     }
 }
-// per-CTA timeline of one instrumented kernel: [0] start, [1] first data, [2] end, [3] count
+// per-CTA timeline of one instrumented kernel (id EKV_CTA_KERNEL: 1 = K-score, 2 = score_pages):
+// [0] start, [1] first data, [2] end, [3] count
+#ifndef EKV_CTA_KERNEL
+#define EKV_CTA_KERNEL 1
+#endif
 __device__ unsigned long long ekv_cta[4][1024];
-__device__ __forceinline__ void stamp_cta(bool cond, int which) {
-    if (cond && blockIdx.x < 1024) {
+template <int KID> __device__ __forceinline__ void stamp_cta(bool cond, int which) {
+    if (KID == EKV_CTA_KERNEL && cond && blockIdx.x < 1024) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         ekv_cta[which][blockIdx.x] = t;
     }
 }
-__device__ __forceinline__ void count_cta(bool cond, unsigned long long v) {
-    if (cond && blockIdx.x < 1024) ekv_cta[3][blockIdx.x] = v;
+template <int KID> __device__ __forceinline__ void count_cta(bool cond, unsigned long long v) {
+    if (KID == EKV_CTA_KERNEL && cond && blockIdx.x < 1024) ekv_cta[3][blockIdx.x] = v;
 }
 #else
 __device__ __forceinline__ void stamp(int, int) {}
 __device__ __forceinline__ void stamp_if(bool, int, int) {}
-__device__ __forceinline__ void stamp_cta(bool, int) {}
-__device__ __forceinline__ void count_cta(bool, unsigned long long) {}
+template <int KID> __device__ __forceinline__ void stamp_cta(bool, int) {}
+template <int KID> __device__ __forceinline__ void count_cta(bool, unsigned long long) {}
 #endif
 }  // namespace ekv
 
@@ -448,6 +465,29 @@ __device__ uint32_t block_kth_largest(const uint32_t (&key)[CPT], int k, uint32_
 }  // namespace ekv
 
 namespace ekv {
+// fp32 accumulate of a bf16 x bf16 product (sm_100: FHFMA.BF16, half selectors folded):
+// both operands widen exactly to fp32 and their product is exact in fp32, so this is
+// bit-identical to fmaf(float(a), float(b), c) -- the R1 chain step.
+__device__ __forceinline__ float fma_bf16lo(uint32_t a, uint32_t b, float c) {
+    unsigned short al, ah, bl, bh;
+    asm("mov.b32 {%0,%1}, %2;" : "=h"(al), "=h"(ah) : "r"(a));
+    asm("mov.b32 {%0,%1}, %2;" : "=h"(bl), "=h"(bh) : "r"(b));
+    asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(c) : "h"(al), "h"(bl));
+    return c;
+}
+__device__ __forceinline__ float fma_bf16hi(uint32_t a, uint32_t b, float c) {
+    unsigned short al, ah, bl, bh;
+    asm("mov.b32 {%0,%1}, %2;" : "=h"(al), "=h"(ah) : "r"(a));
+    asm("mov.b32 {%0,%1}, %2;" : "=h"(bl), "=h"(bh) : "r"(b));
+    asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(c) : "h"(ah), "h"(bh));
+    return c;
+}
+// PRMT byte select: bytes 0-3 of a, 4-7 of b (selector nibbles in the low 16 bits)
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
 // packed fp32x2 add (sm_100: FADD2): two independent IEEE round-to-nearest adds
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
     unsigned long long ra, rb, rd;

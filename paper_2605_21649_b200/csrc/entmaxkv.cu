@@ -62,6 +62,14 @@ ekv_status check_cache(const ekv_cache *c, int Hq) {
     }
     if (!c->k_pages || !c->v_pages || !c->page_table || !c->seq_lens)
         return fail(EKV_ERR_INVALID_ARG, "NULL cache buffer");
+    if (((uintptr_t)c->k_pages | (uintptr_t)c->v_pages) & 15)
+        return fail(EKV_ERR_INVALID_ARG, "k_pages/v_pages must be 16-byte aligned");
+    return EKV_OK;
+}
+
+ekv_status check_q(const void *q) {
+    if (!q) return fail(EKV_ERR_INVALID_ARG, "q is NULL");
+    if ((uintptr_t)q & 15) return fail(EKV_ERR_INVALID_ARG, "q must be 16-byte aligned");
     return EKV_OK;
 }
 
@@ -133,6 +141,13 @@ template <typename P> P *at(void *ws, size_t off) { return reinterpret_cast<P *>
 
 template <typename K> void set_smem(K kernel, int bytes) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
+// resident CTAs per SM of a persistent kernel (>= 1): grids are sized to one wave
+template <typename K> int resident_per_sm(K kernel, int threads, int smem) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess || n < 1) n = 1;
+    return n;
 }
 
 // ---------------------------------------------------------------- launch helpers
@@ -153,11 +168,16 @@ void score_go(const CacheView &v, const T *q, int Hq, float *box, float *mu, flo
     const int HD = v.Hkv * kD;
     const int per_page = ((MODES & 1) ? 2 * HD * (int)sizeof(T) : 0) + ((MODES & 2) ? 2 * HD * 4 : 0);
     const int smem = NS * SP * per_page;
-    static int init = 0;
-    if (smem > init) { set_smem(k_score<T, G, MODES>, smem); init = smem; }
-    // persistent: 2 CTAs per SM over the flattened (b, page) space, >= 8 pages per CTA
+    static int init = 0, per_sm = 1;
+    if (smem > init) {
+        set_smem(k_score<T, G, MODES>, smem);
+        init = smem;
+    }
+    static int occ_for = -1;
+    if (occ_for != smem) { per_sm = resident_per_sm(k_score<T, G, MODES>, 288, smem); occ_for = smem; }
+    // persistent: one wave of resident CTAs over the flattened (b, page) space, >= 8 pages per CTA
     long long gx = ((long long)v.B * v.maxp + 7) / 8;
-    if (gx > 2 * num_sms()) gx = 2 * num_sms();
+    if (gx > per_sm * num_sms()) gx = per_sm * num_sms();
     if (gx < 1) gx = 1;
     k_score<T, G, MODES><<<(unsigned)gx, 288, smem, st>>>(v, q, Hq, box, mu, s2);
 }
@@ -210,10 +230,12 @@ ekv_status launch_mark(const ekv_cache *c, int Hq, const int32_t *pi, const int3
 template <typename T, int G>
 ekv_status launch_scores_t(const CacheView &v, const void *q, int Hq, const uint32_t *um, int W, const int32_t *pi,
                            const int32_t *ns, int stride, float *scores, uint32_t *rowmax, int full, cudaStream_t st) {
-    constexpr int smem = AttCfg<T>::SMEM;
-    static bool init = false;
-    if (!init) { set_smem(k_attend_scores<T, G>, smem); init = true; }
-    const int per_sm = sizeof(T) == 2 ? 2 : 1;
+    constexpr int smem = AttCfg<T>::template smem<G>();
+    static int per_sm = 0;
+    if (!per_sm) {
+        set_smem(k_attend_scores<T, G>, smem);
+        per_sm = resident_per_sm(k_attend_scores<T, G>, 32 * (AttCfg<T>::NCW + 1), smem);
+    }
     const long long slots = full ? (long long)v.B * v.Hkv * v.maxp : (long long)v.B * Hq * stride;
     long long gx = (slots + 31) / 32;                                // >= 32 work slots per CTA
     if (gx > per_sm * num_sms()) gx = per_sm * num_sms();
@@ -389,7 +411,7 @@ ekv_status entmaxkv_score_pages(const ekv_cache *cache, const void *q, int32_t n
     (void)workspace;
     g_err[0] = 0;
     EKV_TRY(check_cache(cache, n_q_heads));
-    if (!q) return fail(EKV_ERR_INVALID_ARG, "q NULL");
+    EKV_TRY(check_q(q));
     if (modes < 1 || modes > 3) return fail(EKV_ERR_INVALID_ARG, "modes must be 1..3");
     if ((modes & 1) && (!box || !cache->kmin || !cache->kmax)) return fail(EKV_ERR_INVALID_ARG, "box mode needs box/kmin/kmax");
     if ((modes & 2) && (!mu || !sigma2 || !cache->kavg || !cache->kvar))
@@ -436,6 +458,7 @@ ekv_status entmaxkv_sparse_attend(const ekv_cache *cache, const void *q, int32_t
     EKV_TRY(check_cache(cache, n_q_heads));
     EKV_TRY(check_attn(attn));
     if (!q || !page_idx || !n_sel || !out || !workspace) return fail(EKV_ERR_INVALID_ARG, "NULL argument");
+    EKV_TRY(check_q(q));
     if (sel_stride < 1) return fail(EKV_ERR_INVALID_ARG, "sel_stride < 1");
     g_launches = 0;
     Layout L = layout(cache, n_q_heads, nullptr);
@@ -449,6 +472,7 @@ ekv_status entmaxkv_full_attend(const ekv_cache *cache, const void *q, int32_t n
     EKV_TRY(check_cache(cache, n_q_heads));
     EKV_TRY(check_attn(attn));
     if (!q || !out || !workspace) return fail(EKV_ERR_INVALID_ARG, "NULL argument");
+    EKV_TRY(check_q(q));
     g_launches = 0;
     Layout L = layout(cache, n_q_heads, nullptr);
     return attend_impl(cache, q, n_q_heads, at<int32_t>(workspace, L.page_idx), at<int32_t>(workspace, L.n_sel),
@@ -463,6 +487,7 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
     EKV_TRY(check_attn(attn));
     EKV_TRY(check_sel(sel, attn->alpha));
     if (!q || !out || !workspace) return fail(EKV_ERR_INVALID_ARG, "NULL argument");
+    EKV_TRY(check_q(q));
     if (sel->policy == EKV_GAUSS && attn->transform != EKV_ENTMAX)
         return fail(EKV_ERR_INVALID_ARG, "Gaussian selector is entmax-specific");
     g_launches = 0;
@@ -510,8 +535,13 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
     if (want_db) {
         const int nch = (maxp + kDbChunk - 1) / kDbChunk;
         dim3 g(nch, rows);
+        DbConst kc;
+        kc.a = (double)attn->alpha - 1.0;
+        kc.beta = 1.0 / kc.a;
+        kc.inv_a = kc.beta;
+        kc.ib = (std::fabs(kc.beta - std::rint(kc.beta)) < 1e-12 && kc.beta <= 4.5) ? (int)std::rint(kc.beta) : 0;
         k_delta_bar<<<g, 256, 0, st>>>(box, maxp, cache->seq_lens, n_q_heads, Gq, uo.umask, L.W, tau_p,
-                                       attn->alpha, at<double>(workspace, L.db_partial), nch,
+                                       kc, at<double>(workspace, L.db_partial), nch,
                                        at<unsigned int>(workspace, L.tickets), stats->delta_bar);
         EKV_TRY(check_launch("k_delta_bar"));
     }

@@ -11,54 +11,60 @@ namespace ekv {
 // are written.  rowmax[b][h] holds the ordered-int max score (atomicMax; 0 = empty).
 
 // ============================================================================ K scores
-// Persistent, warp-specialised: 160 threads = 4 consumer warps + 1 producer warp,
+// Persistent, warp-specialised: 288 threads = 8 consumer warps + 1 producer warp,
 // 2 CTAs per SM (bf16).  The flattened work space (sparse: (row, i) over the page lists,
 // each union page kept once -- from its lowest selecting head; full: (unit, page)) is
 // split into equal contiguous ranges, one per CTA.
 //  - Producer warp: collects the range's pages (page-table and union-mask lookups in
 //    parallel), packs them into ring stages of SP = 8 pages and issues one
 //    cp.async.bulk (TMA, 1-D) copy per page of the contiguous tile K[phys][kvh][0..P)[0..d)
-//    completing on the stage's `full` mbarrier; it waits on the stage's `empty` mbarrier
-//    before reuse.  n = -1 ends.  (Per-row copies into a padded layout were tried: 16
-//    small copies per page are TMA-issue bound, ~2x slower.)
-//  - Consumers: warp w scores pages 2w, 2w+1 of the stage, lane = token t: the lane
-//    computes dot16x8 (R1) for the G query heads entirely in registers -- 16 chunk
-//    partials per head (fma chains, packed FFMA2 over head pairs; 64 independent chains
-//    of ILP) and the pairwise tree c+(c+8), c+(c+4), c+(c+2), c0+c1 with packed adds --
-//    q is read from shared memory.  Bank conflicts: lane t handles chunk c ^ (t & 7) in
-//    register slot c, so 8 consecutive lanes (rows 256 B apart) read 8 distinct 16-byte
+//    completing on the stage's `full` mbarrier, after writing the stage's work items:
+//    one (page, head) item per head of the unit whose union-mask bit is set (sparse:
+//    ~1.1 items per page -- only heads that selected the page are scored; full: G).
+//    It waits on the stage's `empty` mbarrier before reuse.  n = -1 ends.  (Per-row
+//    copies into a padded layout were tried: 16 small copies per page are TMA-issue
+//    bound, ~2x slower.)
+//  - Consumers: a half-warp scores one item, lane = token t, computing dot16x8 (R1)
+//    in registers: 16 independent chunk chains (bf16: FHFMA.BF16 straight from the
+//    packed K and q words, no unpacking -- exact, see fma_bf16lo) and the pairwise tree
+//    c+(c+8), c+(c+4), c+(c+2), c0+c1.  Bank conflicts: lane t handles chunk c ^ (t & 7)
+//    in register slot c, so 8 consecutive lanes (rows 256 B apart) read 8 distinct 16-byte
 //    bank groups; XOR-relabelling with s < 8 maps the butterfly's pairs (x, x+2^j) onto
-//    themselves and fp add commutes, so slot 0 ends bit-identical to R1's tree.  q rows
-//    are padded by 16 B per chunk for the same reason.  s = fl32(dot * c_d) (R2); -inf
-//    past seq_len; stores of 32 consecutive tokens per head are coalesced.  Per-head
-//    running max, flushed with one atomicMax per (warp, unit) into rowmax.
+//    themselves and fp add commutes, so slot 0 ends bit-identical to R1's tree.  q of the
+//    item's unit (G heads) is cached per half-warp in shared memory.  s = fl32(dot * c_d)
+//    (R2); -inf past seq_len; a half-warp stores 16 consecutive scores (64 B); one
+//    atomicMax per item into rowmax.
+#ifndef EKV_ATT_NCW
+#define EKV_ATT_NCW 8
+#endif
+#ifndef EKV_ATT_NS
+#define EKV_ATT_NS 3
+#endif
 template <typename T> struct AttCfg {
-    static constexpr int NCW = 4;                          // consumer warps
-    static constexpr int SP = 2 * NCW;                     // pages per stage
-    static constexpr int NS = 3;                           // ring stages
+    static constexpr int NCW = EKV_ATT_NCW;                // consumer warps (16 half-warps >= items per stage, usually)
+    static constexpr int SP = 8;                           // pages per stage (item code: 3 bits)
+    static constexpr int NS = sizeof(T) == 2 ? EKV_ATT_NS : 2;   // ring stages
     static constexpr int TILE = kP * kD * (int)sizeof(T);
-    static constexpr int SMEM = NS * SP * TILE;
+    static constexpr int RING = NS * SP * TILE;
+    template <int G> static constexpr int smem() { return RING + NCW * G * kD * (int)sizeof(T); }  // + q cache
 };
 
 template <typename T, int G>
-__global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1)) k_attend_scores(
+__global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 : 1) k_attend_scores(
     CacheView c, const T *__restrict__ q, int Hq, const uint32_t *__restrict__ umask, int W,
     const int32_t *__restrict__ page_idx, const int32_t *__restrict__ n_sel, int stride,
     float *__restrict__ scores, uint32_t *__restrict__ rowmax, int full) {
     constexpr int SP = AttCfg<T>::SP, NS = AttCfg<T>::NS, TILE = AttCfg<T>::TILE;
     constexpr int NCW = AttCfg<T>::NCW;
     constexpr int CHK = 256;                // work slots per producer chunk (8 per lane)
-    constexpr int GP = (G + 1) / 2;         // head pairs
     extern __shared__ __align__(128) unsigned char smem[];   // [NS][SP][TILE]
     __shared__ uint64_t fullb[NS], emptyb[NS];
-    __shared__ int d_page[NS][SP], d_unit[NS][SP], d_phys[NS][SP], d_n[NS];
-    __shared__ uint8_t d_mask[NS][SP];
+    __shared__ int d_page[NS][SP], d_unit[NS][SP], d_phys[NS][SP], d_n[NS], d_ni[NS];
+    __shared__ uint8_t d_mask[NS][SP], d_items[NS][SP * G];
     __shared__ int l_unit[CHK], l_page[CHK], l_phys[CHK];
     __shared__ uint8_t l_mask[CHK];
-    constexpr int QCH = 8 * GP + 2;         // float2 per q chunk row (8 dims x GP pairs + 16 B pad)
-    __shared__ __align__(16) float2 qs[NCW][16 * QCH];      // per-warp copy of q (head pairs)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    stamp_cta(threadIdx.x == 0, 0);
+    stamp_cta<1>(threadIdx.x == 0, 0);
     const int ucap = full ? c.maxp : stride;
     const long long tot = full ? (long long)c.B * c.Hkv * c.maxp : (long long)c.B * Hq * stride;
     const long long f0 = tot * blockIdx.x / gridDim.x, f1 = tot * (blockIdx.x + 1) / gridDim.x;
@@ -128,7 +134,14 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1)) k_attend_scores(
                 }
                 if (++fill == SP) {
                     __syncwarp();
-                    if (lane == 0) { d_n[slot] = SP; mbar_expect_tx(&fullb[slot], (uint32_t)(SP * TILE)); }
+                    if (lane == 0) {
+                        d_n[slot] = SP;
+                        int ni = 0;
+                        for (int kk = 0; kk < SP; ++kk)
+                            for (unsigned m = d_mask[slot][kk]; m; m &= m - 1u) d_items[slot][ni++] = (uint8_t)(kk * 8 + __ffs((int)m) - 1);
+                        d_ni[slot] = ni;
+                        mbar_expect_tx(&fullb[slot], (uint32_t)(SP * TILE));
+                    }
                     __syncwarp();
                     if (lane < SP)
                         bulk_g2s(smem + ((size_t)slot * SP + lane) * TILE,
@@ -143,7 +156,14 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1)) k_attend_scores(
         if (fill > 0) {
             const int slot = si % NS;
             __syncwarp();
-            if (lane == 0) { d_n[slot] = fill; mbar_expect_tx(&fullb[slot], (uint32_t)(fill * TILE)); }
+            if (lane == 0) {
+                d_n[slot] = fill;
+                int ni = 0;
+                for (int kk = 0; kk < fill; ++kk)
+                    for (unsigned m = d_mask[slot][kk]; m; m &= m - 1u) d_items[slot][ni++] = (uint8_t)(kk * 8 + __ffs((int)m) - 1);
+                d_ni[slot] = ni;
+                mbar_expect_tx(&fullb[slot], (uint32_t)(fill * TILE));
+            }
             __syncwarp();
             if (lane < fill)
                 bulk_g2s(smem + ((size_t)slot * SP + lane) * TILE,
@@ -159,106 +179,91 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1)) k_attend_scores(
         }
         return;
     }
-    // ---------------------------------------------------- consumers (lane = token)
+    // ---------------------------------------------------- consumers (half-warp = item, lane = token)
     const size_t ntok = (size_t)c.maxp * kP;
-    const int pp = lane >> 4, t = lane & 15;      // page (0/1) of the warp's pair, token in page
-    int cur_unit = -1, L = 0;
-    float runmax[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) runmax[g] = -INFINITY;
-    auto flush = [](const float (&rm)[G], int unit, const CacheView &cv, int Hq_, uint32_t *rmx) {
-        int bb = unit / cv.Hkv, kh = unit % cv.Hkv;
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            float m = rm[g];
-#pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-            if ((threadIdx.x & 31) == 0 && m > -INFINITY)
-                atomicMax(rmx + (size_t)bb * Hq_ + kh * G + g, f2key(m));
-        }
-    };
+    const int half = lane >> 4, t = lane & 15, sw = t & 7;
+    const unsigned hm = 0xffffu << (16 * half);
+    T *qsh = reinterpret_cast<T *>(smem + AttCfg<T>::RING) + warp * G * kD;   // q cache of the warp
+    int cu = -1, L = 0;                           // unit whose q is in qsh
     for (int si = 0;; ++si) {
         const int slot = si % NS;
         mbar_wait(&fullb[slot], (si / NS) & 1);
         const int n = d_n[slot];
-        stamp_cta(threadIdx.x == 0 && si == 0, 1);
+        stamp_cta<1>(threadIdx.x == 0 && si == 0, 1);
         stamp_if(threadIdx.x == 0 && si < 16, 3, si);
-        if (n < 0) { stamp_cta(threadIdx.x == 0, 2); count_cta(threadIdx.x == 0, si); break; }
-        const int k = 2 * warp + pp;              // page of this lane within the stage
-        if (2 * warp < n) {                       // warp-uniform
-            const bool act = k < n;
-            const int unitA = d_unit[slot][2 * warp];
-            const int unitB = d_unit[slot][act ? k : 2 * warp];
-            const int unitB16 = __shfl_sync(0xffffffffu, unitB, 16);
-            const bool split = unitB16 != unitA;  // warp-uniform
-            // both pages of a warp normally share the unit; if not, process them one at a time
-            for (int part = 0; part < (split ? 2 : 1); ++part) {
-                const int u_here = part == 0 ? unitA : unitB16;
-                const bool mine = act && (!split || pp == part);
-                if (u_here != cur_unit) {                                      // warp-uniform
-                    if (cur_unit >= 0) flush(runmax, cur_unit, c, Hq, rowmax);
-#pragma unroll
-                    for (int g = 0; g < G; ++g) runmax[g] = -INFINITY;
-                    cur_unit = u_here;
-                    const int bb = u_here / c.Hkv, kh = u_here % c.Hkv;
-                    L = c.seq_lens[bb];
+        if (n < 0) { stamp_cta<1>(threadIdx.x == 0, 2); count_cta<1>(threadIdx.x == 0, si); break; }
+        const int ni = d_ni[slot];
+        for (int base = 2 * warp; base < ni; base += 2 * NCW) {            // warp-uniform
+            const int it = base + half;
+            const bool act = it < ni;
+            const int code = d_items[slot][act ? it : base];
+            const int k = code >> 3, g = code & 7;
+            const int unit = d_unit[slot][k];
+            const int unitA = __shfl_sync(0xffffffffu, unit, 0), unitB = __shfl_sync(0xffffffffu, unit, 16);
+            for (int pass = 0; pass < (unitA != unitB ? 2 : 1); ++pass) {  // warp-uniform
+                const int u = pass ? unitB : unitA;
+                if (u != cu) {                                             // warp-uniform
+                    const int bb = u / c.Hkv, kh = u % c.Hkv;
                     __syncwarp();
-                    for (int e = lane; e < kD * G; e += 32) {       // q -> shared (head pairs)
-                        const int i = e / G, g = e % G;
-                        const float v = Elem<T>::to_f(q[((size_t)bb * Hq + kh * G + g) * kD + i]);
-                        float2 &dst = qs[warp][(i >> 3) * QCH + (i & 7) * GP + (g >> 1)];
-                        if (g & 1) dst.y = v; else dst.x = v;
-                        if ((G & 1) && g == G - 1) dst.y = 0.0f;
-                    }
+                    const uint4 *src = reinterpret_cast<const uint4 *>(q + ((size_t)bb * Hq + kh * G) * kD);
+                    uint4 *dst = reinterpret_cast<uint4 *>(qsh);
+                    for (int e = lane; e < G * kD * (int)sizeof(T) / 16; e += 32) dst[e] = __ldg(src + e);
                     __syncwarp();
+                    cu = u;
+                    L = __ldg(c.seq_lens + bb);
                 }
-                if (!mine) continue;
-                const int page = d_page[slot][k];
-                const uint8_t msk = d_mask[slot][k];
-                const T *row = reinterpret_cast<const T *>(smem + ((size_t)slot * SP + k) * TILE) + t * kD;
-                const int sw = t & 7;
-                float2 acc[16][GP];
+                if (!act || unit != u) continue;                            // half-warp-uniform
+            const unsigned char *tile = smem + ((size_t)slot * SP + k) * TILE;
+            float acc[16];
+            if constexpr (sizeof(T) == 2) {
+                const uint4 *krow = reinterpret_cast<const uint4 *>(tile) + t * (kD / 8);
+                const uint4 *qrow = reinterpret_cast<const uint4 *>(qsh) + g * (kD / 8);
 #pragma unroll
-                for (int cch = 0; cch < 16; ++cch) {
-                    const int ch = cch ^ sw;              // chunk held in register slot cch
-                    float kx[8];
-                    Elem<T>::load8(row + 8 * ch, kx);
-                    const float2 *qc = &qs[warp][ch * QCH];
-#pragma unroll
-                    for (int hp = 0; hp < GP; ++hp) acc[cch][hp] = make_float2(0.0f, 0.0f);
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-#pragma unroll
-                        for (int hp = 0; hp < GP; ++hp) acc[cch][hp] = ffma2(qc[e * GP + hp], kx[e], acc[cch][hp]);
-                    }
+                for (int cc = 0; cc < 16; ++cc) {
+                    const int ch = cc ^ sw;
+                    const uint4 kv = krow[ch], qv = qrow[ch];
+                    float a = 0.0f;
+                    a = fma_bf16lo(qv.x, kv.x, a); a = fma_bf16hi(qv.x, kv.x, a);
+                    a = fma_bf16lo(qv.y, kv.y, a); a = fma_bf16hi(qv.y, kv.y, a);
+                    a = fma_bf16lo(qv.z, kv.z, a); a = fma_bf16hi(qv.z, kv.z, a);
+                    a = fma_bf16lo(qv.w, kv.w, a); a = fma_bf16hi(qv.w, kv.w, a);
+                    acc[cc] = a;
                 }
+            } else {
+                const float4 *krow = reinterpret_cast<const float4 *>(tile) + t * (kD / 4);
+                const float4 *qrow = reinterpret_cast<const float4 *>(qsh) + g * (kD / 4);
 #pragma unroll
-                for (int hp = 0; hp < GP; ++hp) {
-#pragma unroll
-                    for (int cch = 0; cch < 8; ++cch) acc[cch][hp] = fadd2(acc[cch][hp], acc[cch + 8][hp]);
-#pragma unroll
-                    for (int cch = 0; cch < 4; ++cch) acc[cch][hp] = fadd2(acc[cch][hp], acc[cch + 4][hp]);
-#pragma unroll
-                    for (int cch = 0; cch < 2; ++cch) acc[cch][hp] = fadd2(acc[cch][hp], acc[cch + 2][hp]);
-                    acc[0][hp] = fadd2(acc[0][hp], acc[1][hp]);
+                for (int cc = 0; cc < 16; ++cc) {
+                    const int ch = cc ^ sw;
+                    const float4 k0 = krow[2 * ch], k1 = krow[2 * ch + 1], q0 = qrow[2 * ch], q1 = qrow[2 * ch + 1];
+                    float a = 0.0f;
+                    a = fmaf(q0.x, k0.x, a); a = fmaf(q0.y, k0.y, a); a = fmaf(q0.z, k0.z, a); a = fmaf(q0.w, k0.w, a);
+                    a = fmaf(q1.x, k1.x, a); a = fmaf(q1.y, k1.y, a); a = fmaf(q1.z, k1.z, a); a = fmaf(q1.w, k1.w, a);
+                    acc[cc] = a;
                 }
-                const int tok = page * kP + t;
-                const int bb = u_here / c.Hkv, kh = u_here % c.Hkv;
+            }
 #pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    if (!((msk >> g) & 1)) continue;
-                    const float sv = __fmul_rn((g & 1) ? acc[0][g >> 1].y : acc[0][g >> 1].x, kCd);
-                    const float v = tok < L ? sv : -INFINITY;
-                    scores[((size_t)bb * Hq + kh * G + g) * ntok + tok] = v;
-                    runmax[g] = fmaxf(runmax[g], v);
-                }
+            for (int cc = 0; cc < 8; ++cc) acc[cc] = __fadd_rn(acc[cc], acc[cc + 8]);
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) acc[cc] = __fadd_rn(acc[cc], acc[cc + 4]);
+            acc[0] = __fadd_rn(acc[0], acc[2]);
+            acc[1] = __fadd_rn(acc[1], acc[3]);
+            const float sv = __fmul_rn(__fadd_rn(acc[0], acc[1]), kCd);
+            const int page = d_page[slot][k];
+            const int tok = page * kP + t;
+            const int bb = unit / c.Hkv, row = bb * Hq + (unit % c.Hkv) * G + g;
+            const float v = tok < L ? sv : -INFINITY;
+            scores[(size_t)row * ntok + tok] = v;
+            float m = v;
+#pragma unroll
+            for (int o = 8; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(hm, m, o));
+            if (t == 0 && m > -INFINITY) atomicMax(rowmax + row, f2key(m));
             }
         }
         __syncwarp();
         stamp_if(threadIdx.x == 0 && si < 16, 3, 16 + si);
         if (lane == 0) mbar_arrive(&emptyb[slot]);
     }
-    if (cur_unit >= 0) flush(runmax, cur_unit, c, Hq, rowmax);
 }
 
 // ============================================================================ candidates
@@ -821,56 +826,69 @@ __global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
 // marks its row's selected pages of the chunk in a shared bitmap, sums its chunk
 // (deterministic block tree) into partial[row][chunk]; the last CTA of a row (ticket
 // counter) adds the partials in chunk order, so the result is deterministic.
-constexpr int kDbChunk = 2048;
+constexpr int kDbChunk = 8192;   // pages per CTA: 256 threads x 8 groups of 4 pages
+struct DbConst {                 // per-call constants of alpha (host-computed)
+    double a, beta, inv_a;       // a = alpha - 1, beta = 1/a
+    int ib;                      // integer beta in 1..4, else 0
+};
+// delta_bar (R16, P:409-420 certificate): per (b, q-head) row, sum over the UNSELECTED
+// valid pages p of n_p * ((alpha-1) * box_p - tau)_+^beta.  Grid (chunks, rows); every
+// thread issues its 8 float4 box loads and 8 union-mask words first (union-mask bit
+// (page, g) = page selected by head g of the unit), then the fp64 terms; partial sums
+// per CTA, deterministic ticketed final sum per row.
 __global__ void __launch_bounds__(256) k_delta_bar(const float *__restrict__ box, int maxp,
                                                    const int32_t *__restrict__ seq_lens, int Hq, int G,
                                                    const uint32_t *__restrict__ umask, int W,
-                                                   const double *__restrict__ tau, float alpha,
+                                                   const double *__restrict__ tau, DbConst k,
                                                    double *__restrict__ partial, int nchunks,
                                                    unsigned int *__restrict__ tickets, double *__restrict__ out) {
+    constexpr int R = kDbChunk / 1024;
     __shared__ double rbuf[2 * 2 * 8];
     __shared__ bool s_last;
-    BlockRed2<256> R{rbuf, 0};
-    const int row = blockIdx.y, b = row / Hq, h = row % Hq;
-    const int unit = b * (Hq / G) + h / G, g = h % G;
-    const int L = seq_lens[b];
+    BlockRed2<256> Rd{rbuf, 0};
+    const int row = blockIdx.y, b = row / Hq, h = row - b * Hq;
+    const int unit = b * (Hq / G) + h / G, g = h - (h / G) * G;
+    const int L = __ldg(seq_lens + b);
     const int M = n_pages_of(L);
     const int p0 = blockIdx.x * kDbChunk;
-    // all loads first: 8 box scores (2 float4) and 2 mask words per thread
+    const double t = __ldg(tau + row);
     const float *bx = box + (size_t)row * maxp;
-    float bv[8];
-    uint32_t mw[2];
+    const uint32_t *um = umask + (size_t)unit * W;
+    float bv[4 * R];
+    uint32_t mw[R];
+    const bool vec = (maxp & 3) == 0;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < R; ++r) {
         const int p = p0 + 4 * (threadIdx.x + 256 * r);
-        if (p + 3 < M && (maxp & 3) == 0) {
+        if (vec && p + 3 < M) {
             const float4 v = __ldg(reinterpret_cast<const float4 *>(bx + p));
             bv[4 * r] = v.x; bv[4 * r + 1] = v.y; bv[4 * r + 2] = v.z; bv[4 * r + 3] = v.w;
         } else {
 #pragma unroll
             for (int e = 0; e < 4; ++e) bv[4 * r + e] = (p + e < M) ? __ldg(bx + p + e) : -INFINITY;
         }
-        mw[r] = (p < M) ? __ldg(umask + (size_t)unit * W + (p >> 2)) : 0u;
+        mw[r] = (p < M) ? __ldg(um + (p >> 2)) : 0u;
     }
-    const double t = tau[row];
-    const double a = (double)alpha - 1.0, beta = 1.0 / a;
-    const int ib = (fabs(beta - rint(beta)) < 1e-12 && beta <= 4.5) ? (int)rint(beta) : 0;
     double db = 0.0, dz = 0.0;
     if (t == t) {   // tau is NaN for an empty row
         // fp32 pre-test: a*box - tau > 0 needs box > tau/a; thr is rounded well below it
-        const float thr = (float)(t / a) - 1e-3f * fmaxf(1.0f, fabsf((float)(t / a)));
+        const float tf = (float)(t * k.inv_a);
+        const float thr = tf - 1e-3f * fmaxf(1.0f, fabsf(tf));
 #pragma unroll
-        for (int r = 0; r < 2; ++r)
+        for (int r = 0; r < R; ++r)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int p = p0 + 4 * (threadIdx.x + 256 * r) + e;
                 const bool sel = (mw[r] >> (8 * e + g)) & 1u;      // page selected by head h
-                if (p >= M || sel || !(bv[4 * r + e] > thr)) continue;
-                const double d = a * (double)bv[4 * r + e] - t;
-                if (d > 0.0) db += (double)min(kP, L - p * kP) * powb(d, beta, ib);
+                if (sel || !(bv[4 * r + e] > thr)) continue;        // also skips p >= M (-inf)
+                const double d = k.a * (double)bv[4 * r + e] - t;
+                if (d > 0.0) {
+                    const double w = powb(d, k.beta, k.ib);
+                    db += (p == M - 1) ? (double)(L - p * kP) * w : (double)kP * w;
+                }
             }
     }
-    R.sum(db, dz);
+    Rd.sum(db, dz);
     if (threadIdx.x == 0) {
         partial[(size_t)row * nchunks + blockIdx.x] = db;
         __threadfence();

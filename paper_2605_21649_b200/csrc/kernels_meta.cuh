@@ -107,9 +107,15 @@ __global__ void __launch_bounds__(256) k_rebuild(CacheView c) {
 //    scalar fmas) + the 16-lane reduce-scatter tree.  Box: max(q_i kmin_i, q_i kmax_i)
 //    = q_i kext_i as two fmas with qneg = (q_i >= 0 ? 0 : q_i), qpos = (q_i >= 0 ? q_i
 //    : 0): one of the two adds an exact zero, so the chain equals fma(q_i, kext_i, acc).
+#ifndef EKV_SCORE_SP
+#define EKV_SCORE_SP 8
+#endif
+#ifndef EKV_SCORE_NS
+#define EKV_SCORE_NS 3
+#endif
 template <int MODES> struct ScoreCfg {
-    static constexpr int SP = (MODES == 1) ? 8 : 4;     // pages per stage
-    static constexpr int NS = 3;                        // ring stages
+    static constexpr int SP = (MODES == 1) ? EKV_SCORE_SP : 4;   // pages per stage
+    static constexpr int NS = EKV_SCORE_NS;                      // ring stages
 };
 
 // Persistent, warp-specialised (288 threads = 8 consumer warps + 1 producer warp): the
@@ -129,6 +135,7 @@ __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(C
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long total = (long long)c.B * c.maxp;
     const long long r0 = total * blockIdx.x / gridDim.x, r1 = total * (blockIdx.x + 1) / gridDim.x;
+    stamp_cta<2>(threadIdx.x == 0, 0);
     const int HD = c.Hkv * kD;
     const uint32_t bmm = (uint32_t)(HD * sizeof(T));          // kmin / kmax block bytes
     const uint32_t bgs = (uint32_t)(HD * sizeof(float));      // kavg / kvar block bytes
@@ -155,7 +162,10 @@ __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(C
                 l_phys[i] = (p < n_pages_of(__ldg(c.seq_lens + bb))) ? __ldg(c.page_table + (size_t)bb * c.maxp + p) : -1;
             }
             __syncwarp();
-            if (lane == 0) {
+            {
+                // every lane walks the same runs (l_phys reads are broadcasts); lane 0 owns
+                // the mbarrier protocol, and the stage's copies are issued one per lane
+                constexpr int CPP = ((MODES & 1) ? 2 : 0) + ((MODES & 2) ? 2 : 0);   // copies per page
                 int i = 0, bb = cb_b, p0 = cb_p;           // (bb, p0) tracks chunk slot i
                 while (i < nchk) {
                     if (l_phys[i] < 0) {                   // past the sequence end
@@ -166,20 +176,25 @@ __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(C
                     int n = 1;
                     while (n < SP && i + n < nchk && l_phys[i + n] >= 0 && p0 + n < c.maxp) ++n;
                     const int slot = si % NS;
-                    if (si >= NS) mbar_wait(&emptyb[slot], ((si / NS) - 1) & 1);
-                    d_b[slot] = bb; d_p0[slot] = p0; d_n[slot] = n;
-                    mbar_expect_tx(&fullb[slot], n * per_page);
-                    for (int k = 0; k < n; ++k) {
+                    if (lane == 0) {
+                        if (si >= NS) mbar_wait(&emptyb[slot], ((si / NS) - 1) & 1);
+                        d_b[slot] = bb; d_p0[slot] = p0; d_n[slot] = n;
+                        mbar_expect_tx(&fullb[slot], n * per_page);
+                    }
+                    __syncwarp();
+                    for (int e = lane; e < n * CPP; e += 32) {
+                        const int k = e / CPP, w = e - k * CPP;
                         const size_t phys = (size_t)l_phys[i + k];
                         unsigned char *dst = smem + ((size_t)slot * SP + k) * per_page;
                         if (MODES & 1) {
-                            bulk_g2s(dst, reinterpret_cast<const T *>(c.kmin) + phys * HD, bmm, &fullb[slot]);
-                            bulk_g2s(dst + bmm, reinterpret_cast<const T *>(c.kmax) + phys * HD, bmm, &fullb[slot]);
+                            if (w == 0) bulk_g2s(dst, reinterpret_cast<const T *>(c.kmin) + phys * HD, bmm, &fullb[slot]);
+                            if (w == 1) bulk_g2s(dst + bmm, reinterpret_cast<const T *>(c.kmax) + phys * HD, bmm, &fullb[slot]);
                             dst += 2 * bmm;
                         }
                         if (MODES & 2) {
-                            bulk_g2s(dst, c.kavg + phys * HD, bgs, &fullb[slot]);
-                            bulk_g2s(dst + bgs, c.kvar + phys * HD, bgs, &fullb[slot]);
+                            const int w2 = w - ((MODES & 1) ? 2 : 0);
+                            if (w2 == 0) bulk_g2s(dst, c.kavg + phys * HD, bgs, &fullb[slot]);
+                            if (w2 == 1) bulk_g2s(dst + bgs, c.kvar + phys * HD, bgs, &fullb[slot]);
                         }
                     }
                     ++si;
@@ -206,6 +221,87 @@ __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(C
     const int hwpk = 16 / c.Hkv;
     const int kvh = hw / hwpk, sub = hw % hwpk;
     const int hq0 = kvh * G;
+    if constexpr (MODES == 1 && sizeof(T) == 2) {
+        // Box, bf16: lane c keeps q's 4 bf16x2 words of its chunk per head and the PRMT
+        // selectors picking kext_i = (q_i >= 0 ? kmax_i : kmin_i) bytewise from the packed
+        // kmax/kmin words (R1's kext exactly, -0 counted as >= 0); the chain is FHFMA.BF16
+        // on packed words (exact widening, fma_bf16lo).  IPR items per 16-lane reduce-scatter.
+        constexpr int IPR = (16 / G) < 4 ? 16 / G : 4;
+        constexpr int V = IPR * G;
+        uint32_t qw[G][4], sel[G][4];
+        int cur_b = -1;
+        for (int si = 0;; ++si) {
+            const int slot = si % NS;
+            mbar_wait(&fullb[slot], (si / NS) & 1);
+            const int n = d_n[slot];
+            stamp_cta<2>(threadIdx.x == 0 && si == 0, 1);
+            stamp_if(threadIdx.x == 0 && si < 16, 4, si);
+            if (n < 0) { stamp_cta<2>(threadIdx.x == 0, 2); count_cta<2>(threadIdx.x == 0, si); break; }
+            const int bb = d_b[slot], q0 = d_p0[slot];
+            if (bb != cur_b) {
+                cur_b = bb;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const uint4 w = __ldg(reinterpret_cast<const uint4 *>(q + ((size_t)bb * Hq + hq0 + g) * kD + 8 * l16));
+                    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        qw[g][j] = ws[j];
+                        const bool plo = __uint_as_float(ws[j] << 16) >= 0.0f;
+                        const bool phi = __uint_as_float(ws[j] & 0xffff0000u) >= 0.0f;
+                        sel[g][j] = (plo ? 0x10u : 0x54u) | ((phi ? 0x32u : 0x76u) << 8);
+                    }
+                }
+            }
+            bool released = false;
+            for (int ib = 0; ib < n; ib += IPR * hwpk) {
+                // all of the group's metadata words to registers first; the last group of
+                // the stage then releases the ring slot before computing, so the producer
+                // refills it while the FHFMA chains run
+                uint32_t wn[IPR][4], wx[IPR][4];
+#pragma unroll
+                for (int j = 0; j < IPR; ++j) {
+                    const int it = ib + sub + j * hwpk;
+                    const unsigned char *pg = smem + ((size_t)slot * SP + (it < n ? it : 0)) * per_page;
+                    const uint4 mn = *reinterpret_cast<const uint4 *>(pg + (size_t)(kvh * kD + 8 * l16) * 2);
+                    const uint4 mx = *reinterpret_cast<const uint4 *>(pg + bmm + (size_t)(kvh * kD + 8 * l16) * 2);
+                    wn[j][0] = mn.x; wn[j][1] = mn.y; wn[j][2] = mn.z; wn[j][3] = mn.w;
+                    wx[j][0] = mx.x; wx[j][1] = mx.y; wx[j][2] = mx.z; wx[j][3] = mx.w;
+                }
+                if (ib + IPR * hwpk >= n) {                  // warp-uniform
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&emptyb[slot]);
+                    released = true;
+                }
+                float acc[V];
+#pragma unroll
+                for (int j = 0; j < IPR; ++j) {
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        float a = 0.0f;
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const uint32_t ke = prmt(wx[j][e], wn[j][e], sel[g][e]);
+                            a = fma_bf16lo(qw[g][e], ke, a);
+                            a = fma_bf16hi(qw[g][e], ke, a);
+                        }
+                        acc[j * G + g] = a;
+                    }
+                }
+                const float r = __fmul_rn(rs_reduce16<V>(acc, lane), kCd);
+                const int vv = rs_head<V>(lane);
+                const int it = ib + sub + (vv / G) * hwpk, hh = vv % G;
+                if (rs_writer<V>(lane) && it < n)
+                    box[((size_t)bb * Hq + hq0 + hh) * c.maxp + q0 + it] = r;
+            }
+            if (!released) {                                 // no group (n <= sub): release now
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&emptyb[slot]);
+            }
+            stamp_if(threadIdx.x == 0 && si < 16, 4, 16 + si);
+        }
+        return;
+    }
     constexpr int GP = (G + 1) / 2;          // head pairs
     float2 qp[GP][8], qn[GP][8], qa[GP][8], q2[GP][8];
     int cur_b = -1;

@@ -1,9 +1,11 @@
-"""Per-CTA timeline of the instrumented kernel (library built with EXTRA=-DEKV_STAMPS)."""
+"""Per-CTA timeline of the instrumented kernel (library built with
+EXTRA='-DEKV_STAMPS -DEKV_CTA_KERNEL=k', k = 1 K-score, 2 score_pages)."""
 import ctypes, sys
 import numpy as np, torch
 sys.path.insert(0, '.')
 from paper_2605_21649_b200 import binding as ekv
 from paper_2605_21649_b200.workload import make_workload
+slot = int(sys.argv[1]) if len(sys.argv) > 1 else 3     # block-0 stage stamps: 3 K-score, 4 score_pages
 dev = torch.device('cuda')
 n = (1 << 20) - 200; Hq, Hkv = 32, 8
 wl = make_workload(1, n, Hq, Hkv, seed=1, device=dev, spare_tokens=200)
@@ -15,7 +17,9 @@ L.entmaxkv_debug_stamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 buf = (ctypes.c_ulonglong * 4096)(); sb = (ctypes.c_ulonglong * 256)(); nc = ctypes.c_int()
 for it in range(5):
     ekv.decode(c, wl.q, sel, attn, ws, stats=st); torch.cuda.synchronize()
-L.entmaxkv_debug_cta(buf); L.entmaxkv_debug_stamps(sb, ctypes.byref(nc))
+if not L.entmaxkv_debug_cta(buf):
+    sys.exit('library built without -DEKV_STAMPS')
+L.entmaxkv_debug_stamps(sb, ctypes.byref(nc))
 a = np.array(buf[:], dtype=np.float64).reshape(4, 1024)
 m = a[0] > 0
 s0 = a[0][m].min()
@@ -27,6 +31,7 @@ print('first data ', q(fd))
 print('end        ', q(en))
 print('stages     ', q(cnt))
 print('dur/stage  ', q((en - fd) / np.maximum(cnt, 1)))
-w = [sb[3 * 32 + i] for i in range(32)]
-print('blk0 arrivals', [round((x - s0) / 1e3, 2) if x else None for x in w[:16]])
-print('blk0 done    ', [round((x - s0) / 1e3, 2) if x else None for x in w[16:32]])
+w = [sb[slot * 32 + i] for i in range(32)]
+b0 = a[0][0]
+print('blk0 arrivals', [round((x - b0) / 1e3, 2) if x else None for x in w[:16]])
+print('blk0 done    ', [round((x - b0) / 1e3, 2) if x else None for x in w[16:32]])
