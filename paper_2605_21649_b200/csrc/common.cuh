@@ -132,6 +132,26 @@ __device__ __forceinline__ double powbm1(double x, double beta, int ib) {  // x^
     }
 }
 
+// fp32 versions (steering iterations only; never decide support or tau)
+__device__ __forceinline__ float powbf(float x, float beta, int ib) {
+    switch (ib) {
+    case 1: return x;
+    case 2: return x * x;
+    case 3: return (x * x) * x;
+    case 4: { float x2 = x * x; return x2 * x2; }
+    default: return __powf(x, beta);
+    }
+}
+__device__ __forceinline__ float powbm1f(float x, float beta, int ib) {
+    switch (ib) {
+    case 1: return 1.0f;
+    case 2: return x;
+    case 3: return x * x;
+    case 4: return (x * x) * x;
+    default: return __powf(x, beta - 1.0f);
+    }
+}
+
 // ---------------------------------------------------------------- block reductions (deterministic)
 template <int NT> __device__ __forceinline__ double block_sum_d(double v, double *sh) {
 #pragma unroll
@@ -366,7 +386,25 @@ template <int KID> __device__ __forceinline__ void stamp_cta(bool cond, int whic
 template <int KID> __device__ __forceinline__ void count_cta(bool cond, unsigned long long v) {
     if (KID == EKV_CTA_KERNEL && cond && blockIdx.x < 1024) ekv_cta[3][blockIdx.x] = v;
 }
+// whole-kernel trace: first CTA start (min) and last CTA end (max, thread 0 of each CTA)
+__device__ unsigned long long ekv_trace[16][2];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+struct TraceScope {
+    int k;
+    __device__ __forceinline__ explicit TraceScope(int kid) : k(kid) {
+        if (threadIdx.x == 0 && threadIdx.y == 0) atomicMin(&ekv_trace[k][0], gtimer());
+    }
+    __device__ __forceinline__ ~TraceScope() {
+        if (threadIdx.x == 0 && threadIdx.y == 0) atomicMax(&ekv_trace[k][1], gtimer());
+    }
+};
+#define EKV_TRACE(kid) ::ekv::TraceScope ekv_trace_scope_(kid)
 #else
+#define EKV_TRACE(kid) do {} while (0)
 __device__ __forceinline__ void stamp(int, int) {}
 __device__ __forceinline__ void stamp_if(bool, int, int) {}
 template <int KID> __device__ __forceinline__ void stamp_cta(bool, int) {}

@@ -12,6 +12,7 @@
 #include "kernels_meta.cuh"
 #include "kernels_select.cuh"
 #include "kernels_attend.cuh"
+#include "kernels_tau.cuh"
 
 using namespace ekv;
 
@@ -205,19 +206,27 @@ struct UnionOut {            // optional union marks done by the selection kerne
     uint32_t *umask; int W;
 };
 
-template <int NT>
-void topk_go(const float *box, int Hq, int maxp, const int32_t *sl, int k, int32_t *pi, int32_t *ns, int stride,
-             int rows, int G, const UnionOut &u, cudaStream_t st) {
-    const int smem = 8 * kTopkCap;
-    static bool init = false;
-    if (!init) { set_smem(k_topk<NT>, smem); init = true; }
-    k_topk<NT><<<rows, NT, smem, st>>>(box, Hq, maxp, sl, k, pi, ns, stride, G, u.umask, u.W);
-}
+// top-k: one cluster of CL CTAs per row, CL = pages / 8192 rounded up to a power of two
 ekv_status launch_topk(const float *box, int B, int Hq, int maxp, const int32_t *sl, int k, int32_t *pi, int32_t *ns,
                        int stride, int G, const UnionOut &u, cudaStream_t st) {
-    const int rows = B * Hq;
-    if (maxp <= 4096) topk_go<256>(box, Hq, maxp, sl, k, pi, ns, stride, rows, G, u, st);
-    else topk_go<1024>(box, Hq, maxp, sl, k, pi, ns, stride, rows, G, u, st);
+    int CL = 1;
+    while (CL * kTkPerCta < maxp) CL *= 2;
+    if (CL > 8) return fail(EKV_ERR_UNSUPPORTED, "top-k supports at most %d pages", 8 * kTkPerCta);
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3((unsigned)(B * Hq * CL));
+    cfg.blockDim = dim3(kTkNT);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_topk, box, Hq, maxp, sl, k, pi, ns, stride, G, u.umask, u.W);
+    if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "k_topk: %s", cudaGetErrorString(e));
     return check_launch("k_topk");
 }
 
@@ -257,11 +266,32 @@ ekv_status launch_scores(const CacheView &v, const void *q, int Hq, const uint32
 
 template <typename T>
 ekv_status launch_tau(const CacheView &v, const TauArgs &A, int rows, cudaStream_t st) {
-    constexpr int smem = kCap * (8 + 1 + 4);   // ck, cin, cphys (+ ~29 KB static)
+    constexpr int smem = kTauSmem;   // ck, cin, cphys, pruned list (+ ~29 KB static)
     static bool init = false;
     if (!init) { set_smem(k_tau_pv<T>, smem); init = true; }
     k_tau_pv<T><<<rows, kTauNT, smem, st>>>(v, A);
     return check_launch("k_tau_pv");
+}
+
+template <typename T, int IB>
+ekv_status launch_tau_sparse_ib(const CacheView &v, const TauArgs &A, int rows, cudaStream_t st) {
+    static bool init = false;
+    if (!init) { set_smem(k_tau_sparse<T, IB>, kTsSmem); init = true; }
+    k_tau_sparse<T, IB><<<rows, kTsNT, kTsSmem, st>>>(v, A);
+    return check_launch("k_tau_sparse");
+}
+// integer beta = 1/(alpha-1) in 1..4 is a template constant; any other alpha -> IB = 0
+template <typename T>
+ekv_status launch_tau_sparse(const CacheView &v, const TauArgs &A, int rows, cudaStream_t st) {
+    const double beta = 1.0 / ((double)A.alpha - 1.0);
+    const int ib = (std::fabs(beta - std::rint(beta)) < 1e-12 && beta <= 4.5) ? (int)std::rint(beta) : 0;
+    switch (ib) {
+    case 1: return launch_tau_sparse_ib<T, 1>(v, A, rows, st);
+    case 2: return launch_tau_sparse_ib<T, 2>(v, A, rows, st);
+    case 3: return launch_tau_sparse_ib<T, 3>(v, A, rows, st);
+    case 4: return launch_tau_sparse_ib<T, 4>(v, A, rows, st);
+    default: return launch_tau_sparse_ib<T, 0>(v, A, rows, st);
+    }
 }
 
 ekv_status check_attn(const ekv_attn_params *a) {
@@ -325,6 +355,10 @@ ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t 
     A.nch = nch; A.page_idx = pi; A.n_sel = ns; A.sel_stride = stride; A.full = full;
     A.Hq = Hq; A.G = Hq / c->n_kv_heads; A.alpha = attn->alpha; A.transform = attn->transform;
     A.out = out; A.tau_out = tau; A.supp_out = supp;
+    if (!full && attn->transform == EKV_ENTMAX && !A.tok_list) {
+        if (c->dtype == EKV_BF16) return launch_tau_sparse<__nv_bfloat16>(v, A, rows, st);
+        return launch_tau_sparse<float>(v, A, rows, st);
+    }
     if (c->dtype == EKV_BF16) return launch_tau<__nv_bfloat16>(v, A, rows, st);
     return launch_tau<float>(v, A, rows, st);
 }
@@ -349,10 +383,27 @@ int entmaxkv_debug_cta(unsigned long long *out /*[4*1024]*/) {
     return 0;
 #endif
 }
+/* Debug: whole-kernel trace [16][2] (first CTA start, last CTA end; ns of %globaltimer);
+ * reset != 0 re-arms it.  Returns 0 without -DEKV_STAMPS. */
+int entmaxkv_debug_trace(unsigned long long *out, int reset) {
+#ifdef EKV_STAMPS
+    if (reset) {
+        unsigned long long init[16][2];
+        for (int i = 0; i < 16; ++i) { init[i][0] = ~0ull; init[i][1] = 0ull; }
+        cudaMemcpyToSymbol(ekv::ekv_trace, init, sizeof(init));
+    } else {
+        cudaMemcpyFromSymbol(out, ekv::ekv_trace, sizeof(unsigned long long) * 32);
+    }
+    return 1;
+#else
+    (void)out; (void)reset;
+    return 0;
+#endif
+}
 int entmaxkv_debug_stamps(unsigned long long *out /*[8*32]*/, int *nc) {
 #ifdef EKV_STAMPS
     cudaMemcpyFromSymbol(out, ekv_stamps, sizeof(unsigned long long) * 8 * 32);
-    cudaMemcpyFromSymbol(nc, ekv_dbg_nc, sizeof(int));
+    *nc = 0;
     return 1;
 #else
     (void)out; (void)nc;

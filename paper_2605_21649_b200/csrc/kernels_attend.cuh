@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
     CacheView c, const T *__restrict__ q, int Hq, const uint32_t *__restrict__ umask, int W,
     const int32_t *__restrict__ page_idx, const int32_t *__restrict__ n_sel, int stride,
     float *__restrict__ scores, uint32_t *__restrict__ rowmax, int full) {
+    EKV_TRACE(4);
     constexpr int SP = AttCfg<T>::SP, NS = AttCfg<T>::NS, TILE = AttCfg<T>::TILE;
     constexpr int NCW = AttCfg<T>::NCW;
     constexpr int CHK = 256;                // work slots per producer chunk (8 per lane)
@@ -283,6 +284,7 @@ __global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ sc
                                                     float alpha, int transform, int nch,
                                                     int *__restrict__ ccount, float *__restrict__ cand_s,
                                                     int32_t *__restrict__ cand_j) {
+    EKV_TRACE(5);
     __shared__ int sh[9];
     const int row = blockIdx.y;
     const int b = row / Hq;
@@ -389,6 +391,8 @@ __global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ sc
 // Softmax rows (a6): p = exp(s - s_max) over every valid token (dense V).
 constexpr int kTauNT = 256;
 constexpr int kCap = 12288;         // shared-memory candidate capacity
+constexpr int kPr = 2048;           // pruned-list capacity (tau solver)
+constexpr int kTauSmem = (8 + 1 + 4) * kCap + (8 + 4) * kPr;
 
 struct TauArgs {
     const float *scores; size_t ntok;
@@ -425,6 +429,7 @@ __device__ __forceinline__ double lbeta_step(double F, double Fd, double beta, i
 
 template <typename T>
 __global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
+    EKV_TRACE(6);
     constexpr int NT = kTauNT;
     constexpr int NW = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -506,6 +511,9 @@ __global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
 
     if (!A.full) {
         // (direct) rounds of up to 4 list pages per thread: loads in flight, count, scan, write
+        // fp32 pre-test (conservative: a * s > tau_lo needs s > tau_lo / a; -inf never passes)
+        const float thr_c = (float)(tau_lo / a);
+        const float thr_f = thr_c - 1e-6f * fmaxf(1.0f, fabsf(thr_c));
         for (int r0 = 0; r0 < nlist; r0 += 4 * NT) {
             float sv[4][kP];
             int pgs[4], phs[4];
@@ -530,7 +538,7 @@ __global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
                 if (pgs[u] >= 0) {
 #pragma unroll
                     for (int t = 0; t < kP; ++t)
-                        cnt += (pgs[u] * kP + t < L && sv[u][t] != -INFINITY && a * (double)sv[u][t] > tau_lo);
+                        cnt += (pgs[u] * kP + t < L && sv[u][t] >= thr_f && a * (double)sv[u][t] > tau_lo);
                 }
             int tot;
             int pos = ncand + block_excl_scan<NT>(cnt, shi, &tot);
@@ -540,7 +548,7 @@ __global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
                 if (pgs[u] >= 0) {
 #pragma unroll
                     for (int t = 0; t < kP; ++t)
-                        if (pgs[u] * kP + t < L && sv[u][t] != -INFINITY && a * (double)sv[u][t] > tau_lo) {
+                        if (pgs[u] * kP + t < L && sv[u][t] >= thr_f && a * (double)sv[u][t] > tau_lo) {
                             cphys[pos] = phs[u];
                             ck[pos++] = ((unsigned long long)(uint32_t)(pgs[u] * kP + t) << 32) | __float_as_uint(sv[u][t]);
                         }
@@ -671,97 +679,247 @@ __global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
         __syncthreads();
     }
     stamp(0, 2);
+#ifdef EKV_STAMPS
+    if (blockIdx.x == 0 && threadIdx.x == 0) ekv_stamps[0][14] = (unsigned long long)ncand;
+#endif
 #define ZOF(k) (a * (double)__uint_as_float((uint32_t)(ck[k] & 0xffffffffu)))
-    // ---- Newton on the candidates
-    double tauN = tau_lo;
-    for (int it = 0; it < 200; ++it) {
-        double F = 0.0, Fd = 0.0;
-        for (int k = threadIdx.x; k < ncand; k += NT) {
-            const double d = ZOF(k) - tauN;
-            if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
+    // ---- tau and support by warp 0 alone (warp-shuffle sums, no block barriers; the xor
+    // butterfly leaves the same value on every lane, so every result is deterministic):
+    //  (a) fp32 Newton on the candidates (cheap; only steers),
+    //  (b) certified lower bound lo2 = tau32 - 1e-3 max(1, |tau32|) if F(lo2) >= 1 in fp64
+    //      (F decreasing -> tau >= lo2; else lo2 = tau_lo), and the list {z > lo2} in fp64
+    //      compacted into shared memory (every token outside it has F(z) >= 1: not in S),
+    //  (c) fp64 Newton on the list from lo2, R9 support, tau from the support (closed forms),
+    //  (d) the support's p_j and V addresses for the PV gather.
+    double *zp = reinterpret_cast<double *>(smem + (sizeof(unsigned long long) + 1 + 4) * kCap);   // [kPr]
+    int *ip = reinterpret_cast<int *>(smem + (sizeof(unsigned long long) + 1 + 4) * kCap + 8 * kPr); // [kPr]
+    __shared__ double s_tau, s_kk, s_psum;
+    __shared__ int s_nsup, s_mode;
+    if (warp == 0) {
+        const float af = (float)a;
+        const float betaf = (float)beta;
+        float tf = (float)tau_lo;
+        // a few fp32 Newton steps from the left: only a pruning point, not a result
+        for (int it = 0; it < 6; ++it) {
+            float F0 = 0.f, F1 = 0.f, D0 = 0.f, D1 = 0.f;
+            for (int k = lane; k < ncand; k += 64) {
+                const float d0 = af * __uint_as_float((uint32_t)ck[k]) - tf;
+                if (d0 > 0.f) { F0 += powbf(d0, betaf, ib); D0 += powbm1f(d0, betaf, ib); }
+                if (k + 32 < ncand) {
+                    const float d1 = af * __uint_as_float((uint32_t)ck[k + 32]) - tf;
+                    if (d1 > 0.f) { F1 += powbf(d1, betaf, ib); D1 += powbm1f(d1, betaf, ib); }
+                }
+            }
+            float F = F0 + F1, D = D0 + D1;
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+                F += __shfl_xor_sync(0xffffffffu, F, o);
+                D += __shfl_xor_sync(0xffffffffu, D, o);
+            }
+            if (!(D > 0.f)) break;
+            const float step = (float)lbeta_step((double)F, (double)D, beta, ib);
+            tf += step;
+            if (!(fabsf(step) > 1e-4f * fmaxf(1.0f, fabsf(tf)))) break;
         }
-        R.sum(F, Fd);
-        if (!(Fd > 0.0)) break;
-        const double step = lbeta_step(F, Fd, beta, ib);
-        tauN += step;
-        // 1e-14 relative is far inside the support band (R9) and the final tau is
-        // recomputed from the support; a tighter test can oscillate at the ulp level
-        if (!(fabs(step) > 1e-14 * fmax(1.0, fabs(tauN))) || it >= 63) break;
+        stamp(6, 1);
+        auto wsum2 = [&](double &x, double &y) {
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+                x += __shfl_xor_sync(0xffffffffu, x, o);
+                y += __shfl_xor_sync(0xffffffffu, y, o);
+            }
+        };
+        // (b) list {z > base} with the fp64 mass F(base); an fp32 pre-test skips the
+        // fp64 work of tokens far below base (conservative margin)
+        auto build = [&](double base, double &F) -> int {
+            int np = 0;
+            double f = 0.0, dz = 0.0;
+            const float bf = (float)base;
+            const float bpre = bf - 1e-3f * fmaxf(1.0f, fabsf(bf));
+            for (int k0 = 0; k0 < ncand; k0 += 32) {
+                const int k = k0 + lane;
+                const bool pre = k < ncand && af * __uint_as_float((uint32_t)ck[k]) > bpre;
+                if (!__any_sync(0xffffffffu, pre)) continue;
+                double z = 0.0;
+                bool in = false;
+                if (pre) {
+                    z = ZOF(k);
+                    const double d = z - base;
+                    if (d > 0.0) { f += powb(d, beta, ib); in = true; }
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, in);
+                const int pos = np + __popc(bal & ((1u << lane) - 1u));
+                if (in && pos < kPr) { zp[pos] = z; ip[pos] = k; }
+                np += __popc(bal);
+            }
+            wsum2(f, dz);
+            F = f;
+            return np;
+        };
+        double base = (double)tf - 1e-4 * fmax(1.0, fabs((double)tf));
+        double Fb = 0.0;
+        int np = -1;
+        if (base > tau_lo && tf == tf) {
+            np = build(base, Fb);
+            if (!(Fb >= 1.0)) np = -1;
+        }
+        if (np < 0) { base = tau_lo; np = build(base, Fb); }
+        stamp(6, 2);
+        const bool listed = np <= kPr;      // else: work on the whole candidate array
+        const int nl = listed ? np : ncand;
+#define ZL(i) (listed ? zp[i] : ZOF(i))
+        for (int k = lane; k < ncand; k += 32) cin[k] = 0;
+        __syncwarp();
+        double tauN = base;
+        int n_it = 0, amb = 0;
+        if (listed && np <= 64) {
+            // (c1) short list: the R9 criterion itself, F(z_j) = sum_i (z_i - z_j)_+^beta < 1,
+            // for every entry (all pairs; z_i broadcast from shared memory)
+            for (int i = lane; i < nl; i += 32) {
+                const double zj = zp[i];
+                double F = 0.0;
+                for (int i2 = 0; i2 < nl; ++i2) {
+                    const double d = zp[i2] - zj;
+                    if (d > 0.0) F += powb(d, beta, ib);
+                }
+                cin[ip[i]] = (F < 1.0) ? 1 : 0;
+            }
+            __syncwarp();
+            if (ib != 1 && ib != 2) {
+                // Newton polish start for the general-beta tau below: the largest listed z
+                // outside the support (or base) has F >= 1, i.e. lies left of tau
+                double t0 = base, dz = 0.0;
+                for (int i = lane; i < nl; i += 32)
+                    if (!cin[ip[i]]) t0 = fmax(t0, zp[i]);
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) t0 = fmax(t0, __shfl_xor_sync(0xffffffffu, t0, o));
+                tauN = t0;
+                for (int it = 0; it < 60; ++it) {
+                    double F = 0.0, Fd = 0.0;
+                    for (int i = lane; i < nl; i += 32)
+                        if (cin[ip[i]]) { const double d = zp[i] - tauN; F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
+                    wsum2(F, Fd);
+                    if (!(Fd > 0.0)) break;
+                    const double step = lbeta_step(F, Fd, beta, ib);
+                    tauN += step;
+                    if (!(fabs(step) > 1e-15 * fmax(1.0, fabs(tauN)))) break;
+                }
+                (void)dz;
+            }
+        } else {
+            // (c2) fp64 Newton from base (monotone from the left), then R9 with a band
+            for (int it = 0; it < 200; ++it) {
+                n_it = it + 1;
+                double F = 0.0, Fd = 0.0;
+                for (int i = lane; i < nl; i += 32) {
+                    const double d = ZL(i) - tauN;
+                    if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
+                }
+                wsum2(F, Fd);
+                if (!(Fd > 0.0)) break;
+                const double step = lbeta_step(F, Fd, beta, ib);
+                tauN += step;
+                // 1e-14 relative is far inside the support band (R9) and the final tau is
+                // recomputed from the support; a tighter test can oscillate at the ulp level
+                if (!(fabs(step) > 1e-14 * fmax(1.0, fabs(tauN))) || it >= 63) break;
+            }
+            stamp(6, 3);
+            // support (R9): z > tau_N + band -> in, z < tau_N - band -> out, else F(z_j) < 1
+            // (list entries only: every other candidate has z <= base <= tau)
+            const double band = 1e-9 * fmax(1.0, fabs(tauN));
+            for (int i = lane; i < nl; i += 32) {
+                const double z = ZL(i);
+                const uint8_t f = (z > tauN + band) ? 1 : (z < tauN - band) ? 0 : 2;
+                cin[listed ? ip[i] : i] = f;
+                amb += (f == 2);
+            }
+            amb = __reduce_add_sync(0xffffffffu, amb);
+            __syncwarp();
+            if (amb > 0) {
+                for (int i0 = 0; i0 < nl; ++i0) {
+                    const int k0 = listed ? ip[i0] : i0;
+                    if (cin[k0] != 2) continue;
+                    const double zk = ZL(i0);
+                    double F = 0.0, dz = 0.0;
+                    for (int i = lane; i < nl; i += 32) {
+                        const double d = ZL(i) - zk;
+                        if (d > 0.0) F += powb(d, beta, ib);
+                    }
+                    wsum2(F, dz);
+                    __syncwarp();
+                    if (lane == 0) cin[k0] = (F < 1.0) ? 1 : 0;
+                    __syncwarp();
+                }
+            }
+        }
+#ifdef EKV_STAMPS
+        if (blockIdx.x == 0 && lane == 0) {
+            ekv_stamps[0][13] = (unsigned long long)n_it; ekv_stamps[0][12] = (unsigned long long)amb;
+            ekv_stamps[0][11] = (unsigned long long)np;
+        }
+#endif
+        stamp(6, 4);
+        // tau from the support
+        double S1 = 0.0, kk = 0.0;
+        for (int i = lane; i < nl; i += 32)
+            if (cin[listed ? ip[i] : i]) { S1 += ZL(i); kk += 1.0; }
+        wsum2(S1, kk);
+        double tau;
+        if (ib == 1) {
+            tau = (S1 - 1.0) / kk;
+        } else if (ib == 2) {
+            const double m = S1 / kk;
+            double ss = 0.0, dz = 0.0;
+            for (int i = lane; i < nl; i += 32)
+                if (cin[listed ? ip[i] : i]) { const double d = ZL(i) - m; ss += d * d; }
+            wsum2(ss, dz);
+            tau = m - sqrt(fmax(0.0, 1.0 - ss) / kk);
+        } else {
+            double F = 0.0, Fd = 0.0;
+            for (int i = lane; i < nl; i += 32)
+                if (cin[listed ? ip[i] : i]) { const double d = ZL(i) - tauN; F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
+            wsum2(F, Fd);
+            tau = tauN + (F - 1.0) / (beta * Fd);
+        }
+        stamp(6, 5);
+        // (d) support entries (list order) with p_j, if they fit the shared support arrays
+        int nsup = 0;
+        double psum = 0.0, dz = 0.0;
+        if (listed && kk <= (double)kSup) {
+            for (int i0 = 0; i0 < nl; i0 += 32) {
+                const int i = i0 + lane;
+                const int k = i < nl ? ip[i] : 0;
+                const bool in = i < nl && cin[k];
+                const unsigned bal = __ballot_sync(0xffffffffu, in);
+                const int pos = nsup + __popc(bal & ((1u << lane) - 1u));
+                if (in) {
+                    const int j = (int)(ck[k] >> 32);
+                    const double d = zp[i] - tau;
+                    const double pd = d > 0.0 ? powb(d, beta, ib) : 0.0;
+                    sup_j[pos] = j;
+                    sup_p[pos] = (float)pd;
+                    sup_phys[pos] = have_phys ? cphys[k] : __ldg(c.page_table + (size_t)b * c.maxp + j / kP);
+                    psum += pd;
+                }
+                nsup += __popc(bal);
+            }
+            wsum2(psum, dz);
+        }
+#undef ZL
+        stamp(6, 6);
+        if (lane == 0) {
+            s_tau = tau; s_kk = kk; s_psum = psum; s_nsup = nsup;
+            s_mode = (listed && kk <= (double)kSup) ? 1 : 0;
+        }
     }
     stamp(0, 3);
-    // ---- support (R9)
-    const double band = 1e-9 * fmax(1.0, fabs(tauN));
-    int amb = 0;
-    for (int k = threadIdx.x; k < ncand; k += NT) {
-        const double z = ZOF(k);
-        const uint8_t f = (z > tauN + band) ? 1 : (z < tauN - band) ? 0 : 2;
-        cin[k] = f;
-        amb += (f == 2);
-    }
-    amb = block_sum_i<NT>(amb, shi);
-    if (amb > 0) {
-        for (int k0 = 0; k0 < ncand; ++k0) {
-            if (cin[k0] != 2) continue;
-            const double zk = ZOF(k0);
-            double F = 0.0, dz = 0.0;
-            for (int k = threadIdx.x; k < ncand; k += NT) {
-                const double d = ZOF(k) - zk;
-                if (d > 0.0) F += powb(d, beta, ib);
-            }
-            R.sum(F, dz);
-            if (threadIdx.x == 0) cin[k0] = (F < 1.0) ? 1 : 0;
-            __syncthreads();
-        }
-    }
-    // ---- tau from the support
-    double S1 = 0.0, kk = 0.0;
-    for (int k = threadIdx.x; k < ncand; k += NT)
-        if (cin[k]) { S1 += ZOF(k); kk += 1.0; }
-    R.sum(S1, kk);
-    double tau;
-    if (ib == 1) {
-        tau = (S1 - 1.0) / kk;
-    } else if (ib == 2) {
-        const double m = S1 / kk;
-        double ss = 0.0, dz = 0.0;
-        for (int k = threadIdx.x; k < ncand; k += NT)
-            if (cin[k]) { const double d = ZOF(k) - m; ss += d * d; }
-        R.sum(ss, dz);
-        tau = m - sqrt(fmax(0.0, 1.0 - ss) / kk);
-    } else {
-        double F = 0.0, Fd = 0.0;
-        for (int k = threadIdx.x; k < ncand; k += NT)
-            if (cin[k]) { const double d = ZOF(k) - tauN; F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
-        R.sum(F, Fd);
-        tau = tauN + (F - 1.0) / (beta * Fd);
-    }
+    __syncthreads();
+    const double tau = s_tau, kk = s_kk;
     stamp(0, 4);
-    // ---- p and PV: support compacted in candidate order (rounds of kSup entries), page-table
-    // entries fetched in parallel, then warp w gathers entries w, w + NW, ... (4 V rows in flight)
+    // ---- PV: warp w gathers support entries w, w + NW, ... (4 V rows in flight per warp)
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     double psum = 0.0;
-    for (int r0 = 0; r0 < ncand;) {
-        // take candidates [r0, r1) whose support count fits kSup (r1 multiple of NT)
-        int nsup = 0, r1 = r0;
-        while (r1 < ncand) {
-            const int k = r1 + threadIdx.x;
-            const bool in = k < ncand && cin[k];
-            int tot;
-            const int pos = nsup + block_excl_scan<NT>(in ? 1 : 0, shi, &tot);
-            if (nsup + tot > kSup) break;             // uniform
-            if (in) {
-                const int j = (int)(ck[k] >> 32);
-                const double d = ZOF(k) - tau;
-                const double pd = d > 0.0 ? powb(d, beta, ib) : 0.0;
-                sup_j[pos] = j;
-                sup_p[pos] = (float)pd;
-                sup_phys[pos] = have_phys ? cphys[k] : __ldg(c.page_table + (size_t)b * c.maxp + j / kP);
-                psum += pd;
-            }
-            nsup += tot;
-            r1 += NT;
-        }
-        __syncthreads();
+    auto gather = [&](int nsup) {
         for (int e0 = warp; e0 < nsup; e0 += 4 * NW) {
             float vx[4][4];
 #pragma unroll
@@ -782,8 +940,37 @@ __global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
                 }
             }
         }
-        __syncthreads();
-        r0 = r1;
+    };
+    if (s_mode == 1) {
+        gather(s_nsup);
+        if (threadIdx.x == 0) psum = s_psum;
+    } else {
+        // large support: compacted in candidate order, rounds of kSup entries
+        for (int r0 = 0; r0 < ncand;) {
+            int nsup = 0, r1 = r0;
+            while (r1 < ncand) {
+                const int k = r1 + threadIdx.x;
+                const bool in = k < ncand && cin[k];
+                int tot;
+                const int pos = nsup + block_excl_scan<NT>(in ? 1 : 0, shi, &tot);
+                if (nsup + tot > kSup) break;             // uniform
+                if (in) {
+                    const int j = (int)(ck[k] >> 32);
+                    const double d = ZOF(k) - tau;
+                    const double pd = d > 0.0 ? powb(d, beta, ib) : 0.0;
+                    sup_j[pos] = j;
+                    sup_p[pos] = (float)pd;
+                    sup_phys[pos] = have_phys ? cphys[k] : __ldg(c.page_table + (size_t)b * c.maxp + j / kP);
+                    psum += pd;
+                }
+                nsup += tot;
+                r1 += NT;
+            }
+            __syncthreads();
+            gather(nsup);
+            __syncthreads();
+            r0 = r1;
+        }
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) red[warp][4 * lane + e] = acc[e];
@@ -842,6 +1029,7 @@ __global__ void __launch_bounds__(256) k_delta_bar(const float *__restrict__ box
                                                    const double *__restrict__ tau, DbConst k,
                                                    double *__restrict__ partial, int nchunks,
                                                    unsigned int *__restrict__ tickets, double *__restrict__ out) {
+    EKV_TRACE(7);
     constexpr int R = kDbChunk / 1024;
     __shared__ double rbuf[2 * 2 * 8];
     __shared__ bool s_last;
@@ -918,6 +1106,7 @@ __global__ void __launch_bounds__(256) k_eval_metrics(const int32_t *__restrict_
                                                       const int32_t *__restrict__ n_list, int list_cap,
                                                       const int32_t *__restrict__ page_idx, const int32_t *__restrict__ n_sel,
                                                       int sel_stride, double *delta, int32_t *recovered, int32_t *full_supp) {
+    EKV_TRACE(9);
     __shared__ double shd[2 * 8 + 2];
     __shared__ int shi[9];
     const int row = blockIdx.x;

@@ -14,6 +14,7 @@ namespace ekv {
 template <typename T>
 __global__ void __launch_bounds__(1024, 1) k_append(CacheView c, const T *__restrict__ k_new,
                                                  const T *__restrict__ v_new, int n_tokens) {
+    EKV_TRACE(0);
     const int b = blockIdx.x;
     const int L = c.seq_lens[b];
     T *K = reinterpret_cast<T *>(c.Kw);
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(1024, 1) k_append(CacheView c, const T *__rest
 // identical arithmetic to the incremental append (R5).
 template <typename T>
 __global__ void __launch_bounds__(256) k_rebuild(CacheView c) {
+    EKV_TRACE(10);
     const int b = blockIdx.y;
     const int L = c.seq_lens[b];
     const int M = n_pages_of(L);
@@ -126,6 +128,7 @@ template <typename T, int G, int MODES>
 __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(CacheView c, const T *__restrict__ q, int Hq,
                                                    float *__restrict__ box, float *__restrict__ mu,
                                                    float *__restrict__ sigma2) {
+    EKV_TRACE(1);
     constexpr int SP = ScoreCfg<MODES>::SP, NS = ScoreCfg<MODES>::NS;
     constexpr int NCW = 8;
     extern __shared__ __align__(128) unsigned char smem[];

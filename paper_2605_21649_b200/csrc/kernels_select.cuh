@@ -2,226 +2,234 @@
 // and the per-KV-group union of the selected pages (R17).
 #pragma once
 #include "common.cuh"
+#include <cooperative_groups.h>
 
 namespace ekv {
 
 // ============================================================================ a2: top-k
-// One CTA (NT threads) per (b, q-head) row (R3: key desc, then lower page
-// index).  Keys are the ordered-int encodings of the fp32 box scores (-0 == +0).
-//  1. Partition bound: thread t reads the float4 groups {t + NT j} (coalesced, 8 loads in
-//     flight) and keeps each group's max; L = the k-th largest per-thread max (MSB-first
-//     with __syncthreads_count).  At least k keys are >= L, so T* (the k-th largest key)
-//     >= L and every selected key is a candidate {key >= L}.
-//  2. Groups whose max reaches L are listed in shared memory and re-read in parallel; the
-//     keys >= L are compacted into shared memory (order irrelevant: the selection is
-//     defined by (key, index)).
-//  3. T* and the tie cut (smallest indices first) by MSB-first searches run by warp 0
-//     alone over the shared candidates (warp reductions, no block barriers).
-//  4. The selection is marked in a shared bitmap, written ascending (block scan), and --
-//     if umask != NULL -- merged into the KV-group union (mask bits + compact list).
-// Overflow (more than kTopkCap candidates): exact block-wide searches over all keys.
-constexpr int kTopkCap = 8192;
-__device__ int ekv_dbg_nc;
-
-__device__ __forceinline__ void topk_key4(const float *x, int i4, int M, bool vec, uint32_t (&kk)[4]) {
-    if (vec && i4 + 3 < M) {
-        const float4 v = __ldg(reinterpret_cast<const float4 *>(x + i4));
-        kk[0] = f2key(v.x); kk[1] = f2key(v.y); kk[2] = f2key(v.z); kk[3] = f2key(v.w);
-    } else {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) kk[e] = (i4 + e < M) ? f2key(__ldg(x + i4 + e)) : 0u;
-    }
-}
+// A thread-block cluster of CL CTAs (CL = 1, 2, 4 or 8) per (b, q-head) row (
+// R3: key desc, then lower page index).  Keys are the ordered-int encodings of the fp32
+// box scores (-0 == +0; pages past the sequence end get key 0, below every real key).
+// CTA r of the cluster owns pages [8192 r, 8192 (r + 1)); thread t holds the 32 keys of
+// pages 8192 r + 4 (t + 256 j) + e (j < 8, e < 4: coalesced float4 loads) in registers.
+//  1. MSB-first radix select of T* = the k-th largest key with 8-bit digits: each CTA
+//     histograms the digit of its keys that match the prefix so far (warp-aggregated
+//     shared atomics), the cluster barrier publishes the histograms, every CTA sums the CL
+//     histograms through distributed shared memory and locates the digit holding the k-th
+//     key (warp suffix scan).  Two alternating histogram buffers: one cluster barrier per
+//     digit.  A digit whose whole bin is taken ends the search early (no tie cut needed).
+//  2. Ties at T* (only if the bin of T* is split): CTA r takes the first
+//     clamp(need - #eq in CTAs < r, 0, #eq in r) equal keys in page order.
+//  3. Selection bitmap (bit = page), one word per thread, block scan + cluster offsets:
+//     ascending page ids, and -- if umask != NULL -- the KV-group union marks.
+constexpr int kTkNT = 256;
+constexpr int kTkKPT = 32;
+constexpr int kTkPerCta = kTkNT * kTkKPT;   // 8192 pages per CTA, <= 8 CTAs -> 65536 pages
 
 // union mark of one selected page: bit g of the page's byte (fire-and-forget atomic)
 __device__ __forceinline__ void union_mark(uint32_t *um, int p, int g) {
     atomicOr(um + (p >> 2), 1u << ((p & 3) * 8 + g));
 }
 
-template <int NT>
-__global__ void __launch_bounds__(NT, 1) k_topk(const float *__restrict__ box, int Hq, int maxp,
+// bitmap word of the CTA-local pages 1024 j + 4 t + e (e < 4) of a 4-bit nibble per thread:
+// 8 consecutive lanes share a word; lane t % 8 == 0 returns it
+__device__ __forceinline__ uint32_t nibble_word(uint32_t nib, int lane) {
+    uint32_t w = nib << (4 * (lane & 7));
+    w |= __shfl_xor_sync(0xffffffffu, w, 1);
+    w |= __shfl_xor_sync(0xffffffffu, w, 2);
+    w |= __shfl_xor_sync(0xffffffffu, w, 4);
+    return w;
+}
+
+__global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, int Hq, int maxp,
                                                 const int32_t *__restrict__ seq_lens, int k,
                                                 int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
                                                 int sel_stride, int G, uint32_t *__restrict__ umask, int W) {
-    constexpr int CPT = kTopkCap / NT;       // candidate slots per thread
-    extern __shared__ __align__(16) unsigned char tk_smem[];
-    uint32_t *ckey = reinterpret_cast<uint32_t *>(tk_smem);                 // [kTopkCap]
-    int32_t *cidx = reinterpret_cast<int32_t *>(tk_smem + 4 * kTopkCap);    // [kTopkCap]
-    __shared__ uint32_t bits[2048];
-    __shared__ uint32_t hist[256];
-    __shared__ int sh[NT / 32 + 2];
-    const int row = blockIdx.x;
+    EKV_TRACE(2);
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int CL = (int)cl.num_blocks(), r = (int)cl.block_rank();
+    const int row = blockIdx.x / CL;
+    const int t = threadIdx.x, lane = t & 31;
+    __shared__ uint32_t hist[2][256];
+    __shared__ uint32_t bits[256];
+    __shared__ int xch[2];                   // published to the cluster: [0] #eq, [1] #selected
+    __shared__ int sh[(kTkNT / 32 + 2)];
     const int b = row / Hq;
-    const int M = n_pages_of(seq_lens[b]);
+    const int M = n_pages_of(__ldg(seq_lens + b));
     const int keff = min(k, M);
     int32_t *out = page_idx + (size_t)row * sel_stride;
     const int unit = b * (Hq / G) + (row % Hq) / G, gh = (row % Hq) % G;
     uint32_t *um = umask ? umask + (size_t)unit * W : nullptr;
+    const int base = r * kTkPerCta;
     stamp(1, 0);
-    if (keff >= M) {
-        for (int p = threadIdx.x; p < M; p += NT) {
+    if (keff >= M) {                         // every page (uniform over the cluster)
+        for (int p = base + t; p < min(M, base + kTkPerCta); p += kTkNT) {
             out[p] = p;
             if (um) union_mark(um, p, gh);
         }
-        if (threadIdx.x == 0) n_sel[row] = M;
+        if (r == 0 && t == 0) n_sel[row] = M;
         return;
     }
     const float *x = box + (size_t)row * maxp;
-    const int Wb = (M + 31) / 32;
-    for (int w = threadIdx.x; w < Wb; w += NT) bits[w] = 0u;
     const bool vec = (maxp & 3) == 0;
-    // 1. partition maxima: thread t owns the float4 groups {t + NT j}, j < GPT
-    constexpr int GPT = 16;                  // groups per thread (M <= 64 NT)
-    uint32_t gkey[GPT];
-    uint32_t mt = 0u;
+    uint32_t key[kTkKPT];
 #pragma unroll
-    for (int j0 = 0; j0 < GPT; j0 += 8) {
-        float4 v[8];
+    for (int j = 0; j < kTkKPT / 4; ++j) {
+        const int i4 = base + 4 * (t + kTkNT * j);
+        float4 v;
+        if (vec && i4 + 3 < M) v = __ldg(reinterpret_cast<const float4 *>(x + i4));
+        else {
+            v.x = (i4 < M) ? __ldg(x + i4) : 0.f;
+            v.y = (i4 + 1 < M) ? __ldg(x + i4 + 1) : 0.f;
+            v.z = (i4 + 2 < M) ? __ldg(x + i4 + 2) : 0.f;
+            v.w = (i4 + 3 < M) ? __ldg(x + i4 + 3) : 0.f;
+        }
+        key[4 * j] = (i4 < M) ? f2key(v.x) : 0u;
+        key[4 * j + 1] = (i4 + 1 < M) ? f2key(v.y) : 0u;
+        key[4 * j + 2] = (i4 + 2 < M) ? f2key(v.z) : 0u;
+        key[4 * j + 3] = (i4 + 3 < M) ? f2key(v.w) : 0u;
+    }
+    hist[0][t] = 0u;
+    hist[1][t] = 0u;
+    __syncthreads();
+    stamp(1, 1);
+    // 1. radix select over the cluster
+    uint32_t prefix = 0u, pmask = 0u;
+    int kk = keff;                           // keys still to take among those matching prefix
+    bool whole = false;                      // the last digit's bin is taken entirely
+#pragma unroll 1
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        uint32_t *hb = hist[pass & 1];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int i4 = 4 * (threadIdx.x + (j0 + u) * NT);
-            if (vec && i4 + 3 < M) v[u] = __ldg(reinterpret_cast<const float4 *>(x + i4));
-            else {
-                v[u].x = (i4 < M) ? __ldg(x + i4) : -INFINITY;
-                v[u].y = (i4 + 1 < M) ? __ldg(x + i4 + 1) : -INFINITY;
-                v[u].z = (i4 + 2 < M) ? __ldg(x + i4 + 2) : -INFINITY;
-                v[u].w = (i4 + 3 < M) ? __ldg(x + i4 + 3) : -INFINITY;
+        for (int j = 0; j < kTkKPT; ++j) {
+            const uint32_t v = key[j];
+            const bool act = v != 0u && (v & pmask) == prefix;
+            const unsigned bal = __ballot_sync(0xffffffffu, act);
+            if (bal == 0u) continue;                                   // warp-uniform skip
+            // the common case (every active lane in one bin) costs one atomic; otherwise the
+            // lanes add one each (shared atomics serialise only equal addresses)
+            const uint32_t d = (v >> shift) & 255u;
+            const int leader = __ffs(bal) - 1;
+            const uint32_t dl = __shfl_sync(0xffffffffu, d, leader);
+            const unsigned same = __ballot_sync(0xffffffffu, act && d == dl);
+            if (same == bal) {
+                if (lane == leader) atomicAdd(&hb[dl], (uint32_t)__popc(bal));
+            } else if (act) {
+                atomicAdd(&hb[d], 1u);
             }
         }
+        cl.sync();                           // histograms of this digit visible cluster-wide
+        // the other buffer was last read remotely before this barrier: clear it for the next digit
+        if (pass + 1 < 4 && pass >= 1) hist[(pass + 1) & 1][t] = 0u;
+        uint32_t g = 0u;
+        for (int q = 0; q < CL; ++q) g += cl.map_shared_rank(hb, q)[t];
+        bits[t] = g;                         // global histogram (bits[] is free until step 3)
+        __syncthreads();
+        if (t < 32) {
+            int v[8], s = 0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int i4 = 4 * (threadIdx.x + (j0 + u) * NT);
-            gkey[j0 + u] = (i4 < M) ? f2key(fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w))) : 0u;
-            mt = max(mt, gkey[j0 + u]);
+            for (int e = 0; e < 8; ++e) { v[e] = (int)bits[255 - 8 * lane - e]; s += v[e]; }
+            int incl = s;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int excl = incl - s;
+            int D = -1, cab = 0, cum = excl, cnt = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                if (D < 0 && cum + v[e] >= kk) { D = 255 - 8 * lane - e; cab = cum; cnt = v[e]; }
+                cum += v[e];
+            }
+            const unsigned bm = __ballot_sync(0xffffffffu, D >= 0 && excl < kk);
+            const int src = __ffs(bm) - 1;
+            D = __shfl_sync(0xffffffffu, D, src);
+            cab = __shfl_sync(0xffffffffu, cab, src);
+            cnt = __shfl_sync(0xffffffffu, cnt, src);
+            if (lane == 0) { sh[0] = D; sh[1] = cab; sh[2] = cnt; }
         }
-    }
-    stamp(1, 1);
-    uint32_t Lb = 1u;
-    int dummy;
-    // the bound needs at least k non-empty partitions (block_kth_largest requires k <= #keys)
-    if (keff <= NT && __syncthreads_count(mt != 0u) >= keff) {
-        const uint32_t km[1] = {mt};
-        Lb = block_kth_largest<NT, 1>(km, keff, hist, sh, &dummy);
-        if (Lb == 0u) Lb = 1u;
+        __syncthreads();
+        prefix |= (uint32_t)sh[0] << shift;
+        pmask |= 255u << shift;
+        kk -= sh[1];
+        const int cnt = sh[2];
+        if (kk == cnt) { whole = true; break; }
     }
     stamp(1, 2);
-    // 2. candidates {key >= L}: re-read the hit groups (8 in flight), block-scan compaction
-    int nc = 0;
-    bool ovf = false;
-#pragma unroll
-    for (int j0 = 0; j0 < GPT; j0 += 8) {
-        uint32_t kk[8][4];
-        int cnt = 0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int i4 = 4 * (threadIdx.x + (j0 + u) * NT);
-            if (gkey[j0 + u] >= Lb) topk_key4(x, i4, M, vec, kk[u]);
-            else { kk[u][0] = kk[u][1] = kk[u][2] = kk[u][3] = 0u; }
-#pragma unroll
-            for (int e = 0; e < 4; ++e) cnt += kk[u][e] >= Lb;
-        }
-        int tot;
-        int pos = nc + block_excl_scan<NT>(cnt, sh, &tot);
-        if (nc + tot > kTopkCap) { ovf = true; break; }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if (kk[u][e] >= Lb) { ckey[pos] = kk[u][e]; cidx[pos] = 4 * (threadIdx.x + (j0 + u) * NT) + e; ++pos; }
-        nc += tot;
-    }
-    __syncthreads();
-    stamp(1, 3);
-    if (threadIdx.x == 0 && blockIdx.x == 0) ekv_dbg_nc = nc;
-    uint32_t T;
-    int n_gt, Ithr = M;
-    if (!ovf) {
-        // 3. T* = k-th largest candidate (radix select), then the tie cut by index
-        uint32_t ck[CPT];
-#pragma unroll
-        for (int j = 0; j < CPT; ++j) {
-            const int e = j * NT + threadIdx.x;
-            ck[j] = e < nc ? ckey[e] : 0u;
-        }
-        T = block_kth_largest<NT, CPT>(ck, keff, hist, sh, &n_gt);
-        const int need = keff - n_gt;
+    // selected: (key & pmask) > prefix, or (key & pmask) == prefix and (whole, or one of the
+    // first kk equal keys in page order)
+    int take = 0;
+    if (!whole) {
         int ceq = 0;
 #pragma unroll
-        for (int j = 0; j < CPT; ++j) ceq += ck[j] == T;
-        if (block_sum_i<NT>(ceq, sh) > need) {
-            int I = 0;                       // largest I with #(eq, idx < I) <= need
-            for (int bit = 17; bit >= 0; --bit) {
-                const int It = I + (1 << bit);
-                if (It > M) continue;
-                int c = 0;
+        for (int j = 0; j < kTkKPT; ++j) ceq += key[j] == prefix;
+        ceq = block_sum_i<kTkNT>(ceq, sh);
+        if (t == 0) xch[0] = ceq;
+        cl.sync();
+        int before = 0;
+        for (int q = 0; q < r; ++q) before += *cl.map_shared_rank(&xch[0], q);
+        take = min(max(kk - before, 0), ceq);
+        // equal keys of this CTA in page order: bitmap, word t = pages 32 t .. 32 t + 31
 #pragma unroll
-                for (int j = 0; j < CPT; ++j) {
-                    const int e = j * NT + threadIdx.x;
-                    c += (ck[j] == T && e < nc && cidx[e] < It);
-                }
-                if (block_sum_i<NT>(c, sh) <= need) I = It;
-            }
-            Ithr = I;
+        for (int j = 0; j < kTkKPT / 4; ++j) {
+            uint32_t nib = 0u;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) nib |= (key[4 * j + e] == prefix ? 1u : 0u) << e;
+            const uint32_t w = nibble_word(nib, lane);
+            if ((lane & 7) == 0) bits[32 * j + (t >> 3)] = w;
         }
-        for (int e = threadIdx.x; e < nc; e += NT) {
-            const uint32_t kv = ckey[e];
-            const int i = cidx[e];
-            if (kv > T || (kv == T && i < Ithr)) atomicOr(&bits[i >> 5], 1u << (i & 31));
+        __syncthreads();
+        uint32_t w = bits[t];
+        int tot;
+        int rank = block_excl_scan<kTkNT>(__popc(w), sh, &tot);
+        uint32_t keep = 0u;
+        while (w) {
+            const uint32_t lb = w & (0u - w);
+            if (rank < take) keep |= lb;
+            ++rank;
+            w ^= lb;
         }
-    } else {
-        // exact fallback over all keys (bitwise threshold search, block-wide counts)
-        T = 0u;
-        for (int bit = 31; bit >= 0; --bit) {
-            const uint32_t Tt = T | (1u << bit);
-            int c = 0;
-            for (int i = threadIdx.x; i < M; i += NT) c += f2key(__ldg(x + i)) >= Tt;
-            if (block_sum_i<NT>(c, sh) >= keff) T = Tt;
+        __syncthreads();
+        bits[t] = keep;                      // chosen equal keys
+        __syncthreads();
+    }
+    // 3. selection bitmap and ascending output
+#pragma unroll
+    for (int j = 0; j < kTkKPT / 4; ++j) {
+        uint32_t nib = 0u;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t v = key[4 * j + e] & pmask;
+            const bool s = v > prefix || (whole && v == prefix);
+            nib |= (s ? 1u : 0u) << e;
         }
-        int c = 0;
-        for (int i = threadIdx.x; i < M; i += NT) c += f2key(__ldg(x + i)) > T;
-        const int need = keff - block_sum_i<NT>(c, sh);
-        c = 0;
-        for (int i = threadIdx.x; i < M; i += NT) c += f2key(__ldg(x + i)) == T;
-        if (block_sum_i<NT>(c, sh) > need) {
-            int I = 0;
-            for (int bit = 17; bit >= 0; --bit) {
-                const int It = I + (1 << bit);
-                if (It > M) continue;
-                int c2 = 0;
-                for (int i = threadIdx.x; i < It; i += NT) c2 += f2key(__ldg(x + i)) == T;
-                if (block_sum_i<NT>(c2, sh) <= need) I = It;
-            }
-            Ithr = I;
-        }
-        for (int i = threadIdx.x; i < M; i += NT) {
-            const uint32_t kv = f2key(__ldg(x + i));
-            if (kv > T || (kv == T && i < Ithr)) atomicOr(&bits[i >> 5], 1u << (i & 31));
+        const uint32_t w = nibble_word(nib, lane);
+        if ((lane & 7) == 0) {
+            const int wi = 32 * j + (t >> 3);
+            bits[wi] = whole ? w : (w | bits[wi]);
         }
     }
     __syncthreads();
-    stamp(1, 5);
-    // 4. ascending output (+ union marks)
-    const int wpt = (Wb + NT - 1) / NT;
-    int cnt = 0;
-    for (int w = 0; w < wpt; ++w) {
-        const int wi = threadIdx.x * wpt + w;
-        if (wi < Wb) cnt += __popc(bits[wi]);
-    }
+    const uint32_t w = bits[t];
     int tot;
-    int o = block_excl_scan<NT>(cnt, sh, &tot);
-    for (int w = 0; w < wpt; ++w) {
-        const int wi = threadIdx.x * wpt + w;
-        if (wi >= Wb) break;
-        uint32_t v = bits[wi];
-        while (v) {
-            const int bpos = __ffs(v) - 1;
-            v &= v - 1;
-            out[o++] = wi * 32 + bpos;
-            if (um) union_mark(um, wi * 32 + bpos, gh);
-        }
+    const int pos = block_excl_scan<kTkNT>(__popc(w), sh, &tot);
+    if (t == 0) xch[1] = tot;
+    cl.sync();
+    int o = pos;
+    for (int q = 0; q < r; ++q) o += *cl.map_shared_rank(&xch[1], q);
+    uint32_t v = w;
+    while (v) {
+        const int p = base + 32 * t + __ffs(v) - 1;
+        v &= v - 1;
+        out[o++] = p;
+        if (um) union_mark(um, p, gh);
     }
-    if (threadIdx.x == 0) n_sel[row] = keff;
+    if (r == 0 && t == 0) n_sel[row] = keff;
     stamp(1, 6);
+    cl.sync();                               // keep shared memory alive for remote readers
 }
 
 // ============================================================================ union per KV group
@@ -232,6 +240,7 @@ __global__ void __launch_bounds__(NT, 1) k_topk(const float *__restrict__ box, i
 __global__ void __launch_bounds__(256) k_mark(int Hq, int G, const int32_t *__restrict__ page_idx,
                                               const int32_t *__restrict__ n_sel, int sel_stride,
                                               uint32_t *__restrict__ umask, int W) {
+    EKV_TRACE(3);
     const int row = blockIdx.x;
     const int b = row / Hq, h = row % Hq;
     const int unit = b * (Hq / G) + h / G, g = h % G;
@@ -293,6 +302,7 @@ __global__ void __launch_bounds__(NT) k_gauss_select(const float *__restrict__ m
                                                      float alpha, double margin, double q_page,
                                                      int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
                                                      int sel_stride, double *__restrict__ tau_hat_out) {
+    EKV_TRACE(8);
     __shared__ double shd[2 * (NT / 32) + 2];
     __shared__ int shi[NT / 32 + 1];
     __shared__ float shf[NT / 32 + 1];

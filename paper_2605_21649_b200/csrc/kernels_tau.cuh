@@ -1,0 +1,483 @@
+// kernels_tau.cuh -- a3 hot path: exact alpha-entmax threshold, support and weighted V
+// sum of one (b, q-head) row over its selected pages (sparse decode, R8-R12).
+// The general kernel k_tau_pv (kernels_attend.cuh) serves full rows, softmax rows and the
+// eval lists; this lean kernel serves the decode step's sparse entmax rows, with the
+// integer beta = 1/(alpha-1) a compile-time constant (IB in 1..4; 0 = any other alpha).
+//
+// One CTA (256 threads) per row.  Work is shaped around latency (one CTA per row, few
+// rows): every pass over the candidates is block-parallel, and only the short exact phase
+// runs on one warp.
+//  1. Candidates {j in C_tok : z_j > tau_lo = z_max - 1} (tau >= z_max - 1 since
+//     F(z_max - 1) >= 1): items of 4 consecutive scores (float4) of the page list,
+//     8 items per thread in flight, fp32 pre-test then the fp64 test, block-scan
+//     compaction (fixed order: deterministic sums below).
+//  2. fp32 Newton steps on ||(z - t)_+||_beta - 1 from tau_lo (block sums): a pruning
+//     point t32 only -- nothing is decided in fp32.
+//  3. base = t32 - 1e-4 max(1, |t32|) is kept iff F(base) >= 1 in fp64 (then tau >= base
+//     because F decreases); else base = tau_lo.  The list {z > base} (z in fp64) is
+//     compacted in candidate order.  Every candidate outside it has z <= base <= tau,
+//     i.e. F(z) >= 1: not in the support (R9).
+//  4. Warp 0: support by R9 itself on the list -- short lists (<= 64): F(z_j) < 1 for every
+//     entry, all pairs; longer lists: fp64 Newton from base, then z > tau_N + band in,
+//     z < tau_N - band out, F(z_j) < 1 in between.  tau from the support (closed forms for
+//     beta = 1, 2; Newton on the support otherwise), p_j = (z_j - tau)^beta.
+//  5. PV: warps gather the V rows of the support (4 in flight per warp, lane = 4 dims);
+//     out = sum p_j v_j / sum p_j (R12).
+// Overflow (more candidates than shared memory): fp64 Newton streamed over the score row
+// raises tau_lo to just below tau, then the extraction is repeated.
+#pragma once
+#include "kernels_attend.cuh"
+
+namespace ekv {
+
+template <int IB> __device__ __forceinline__ double powB(double x, double beta) {
+    if constexpr (IB == 1) return x;
+    else if constexpr (IB == 2) return x * x;
+    else if constexpr (IB == 3) return (x * x) * x;
+    else if constexpr (IB == 4) { const double x2 = x * x; return x2 * x2; }
+    else return pow(x, beta);
+}
+template <int IB> __device__ __forceinline__ double powBm1(double x, double beta) {
+    if constexpr (IB == 1) return 1.0;
+    else if constexpr (IB == 2) return x;
+    else if constexpr (IB == 3) return x * x;
+    else if constexpr (IB == 4) return (x * x) * x;
+    else return pow(x, beta - 1.0);
+}
+template <int IB> __device__ __forceinline__ float powBf(float x, float beta) {
+    if constexpr (IB == 1) return x;
+    else if constexpr (IB == 2) return x * x;
+    else if constexpr (IB == 3) return (x * x) * x;
+    else if constexpr (IB == 4) { const float x2 = x * x; return x2 * x2; }
+    else return __powf(x, beta);
+}
+template <int IB> __device__ __forceinline__ float powBm1f(float x, float beta) {
+    if constexpr (IB == 1) return 1.0f;
+    else if constexpr (IB == 2) return x;
+    else if constexpr (IB == 3) return x * x;
+    else if constexpr (IB == 4) return (x * x) * x;
+    else return __powf(x, beta - 1.0f);
+}
+
+// deterministic block sum of two floats (fixed order; alternating buffers: one barrier)
+template <int NT> struct BlockRed2f {
+    float *buf;   // [2][2 * NT/32]
+    int ph;
+    __device__ __forceinline__ void sum(float &a, float &b) {
+        constexpr int NW = NT / 32;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        float *s = buf + ph * 2 * NW;
+        ph ^= 1;
+        if ((threadIdx.x & 31) == 0) { s[2 * (threadIdx.x >> 5)] = a; s[2 * (threadIdx.x >> 5) + 1] = b; }
+        __syncthreads();
+        float x = 0.f, y = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) { x += s[2 * w]; y += s[2 * w + 1]; }
+        a = x; b = y;
+    }
+};
+
+constexpr int kTsNT = 256;
+constexpr int kTsCap = 12288;                                         // candidates in shared memory
+constexpr int kTsSup = 2048;                                          // support entries per gather round
+constexpr int kTsSmem = (4 + 4 + 4 + 1) * kTsCap + (8 + 4) * kPr;     // zs, cj, cph, cin + list
+
+template <typename T, int IB>
+__global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A) {
+    EKV_TRACE(6);
+    constexpr int NT = kTsNT, NW = NT / 32;
+    extern __shared__ __align__(16) unsigned char smem[];
+    float *zs = reinterpret_cast<float *>(smem);                           // raw scores s
+    int *cj = reinterpret_cast<int *>(smem + 4 * kTsCap);                  // token positions
+    int *cph = reinterpret_cast<int *>(smem + 8 * kTsCap);                 // physical pages
+    double *zp = reinterpret_cast<double *>(smem + 12 * kTsCap);           // list z (fp64)
+    int *ip = reinterpret_cast<int *>(smem + 12 * kTsCap + 8 * kPr);       // list -> candidate slot
+    uint8_t *cin = reinterpret_cast<uint8_t *>(smem + 12 * kTsCap + 12 * kPr);   // support flags
+    __shared__ float red[NW][kD];
+    __shared__ int sup_j[kTsSup], sup_phys[kTsSup];
+    __shared__ float sup_p[kTsSup];
+    __shared__ double rbuf[2 * 2 * NW];
+    __shared__ float rbuff[2 * 2 * NW];
+    __shared__ int shi[NW + 1];
+    __shared__ double s_tau, s_kk, s_psum;
+    __shared__ int s_nsup, s_mode;
+    BlockRed2<NT> Rd{rbuf, 0};
+    BlockRed2f<NT> Rf{rbuff, 0};
+
+    const int row = blockIdx.x;
+    const int b = row / A.Hq, h = row % A.Hq, kvh = h / A.G;
+    const int L = c.seq_lens[b];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t mk = A.rowmax[row];
+    if (mk == 0u) {   // empty C_tok
+        if (threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = 0.0f;
+        if (threadIdx.x == 0) {
+            if (A.tau_out) A.tau_out[row] = NAN;
+            if (A.supp_out) A.supp_out[row] = 0;
+        }
+        return;
+    }
+    const float smax = key2f(mk);
+    const int nlist = A.n_sel[row];
+    const int32_t *plist = A.page_idx + (size_t)row * A.sel_stride;
+    const float *srow = A.scores + (size_t)row * A.ntok;
+    const int32_t *ptab = c.page_table + (size_t)b * c.maxp;
+    const T *Vb = reinterpret_cast<const T *>(c.V);
+    const double a = (double)A.alpha - 1.0;
+    const double beta = 1.0 / a;
+    const float af = (float)a, betaf = (float)beta;
+    const double zmax = a * (double)smax;
+    double tau_lo = zmax - 1.0 - 1e-12 * fmax(1.0, fabs(zmax));
+
+    // ---- 1. candidates {z > tau_lo} (returns -1 on overflow; uniform)
+    auto extract = [&](double tlo) -> int {
+        const float thr_c = (float)(tlo / a);
+        const float thr_f = thr_c - 1e-6f * fmaxf(1.0f, fabsf(thr_c));   // conservative fp32 pre-test
+        const int nitems = nlist * 4;
+        int n = 0;
+        for (int r0 = 0; r0 < nitems; r0 += 8 * NT) {
+            float4 v[8];
+            int pg[8], ph[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = r0 + threadIdx.x + NT * u;
+                pg[u] = e < nitems ? __ldg(plist + (e >> 2)) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = r0 + threadIdx.x + NT * u;
+                if (pg[u] >= 0) {
+                    v[u] = *reinterpret_cast<const float4 *>(srow + (size_t)pg[u] * kP + 4 * (e & 3));
+                    ph[u] = __ldg(ptab + pg[u]);
+                }
+            }
+            uint32_t bits = 0u;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (pg[u] < 0) continue;
+                const int e = r0 + threadIdx.x + NT * u;
+                const int j0 = pg[u] * kP + 4 * (e & 3);
+                const float sv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (j0 + q < L && sv[q] >= thr_f && a * (double)sv[q] > tlo) bits |= 1u << (4 * u + q);
+            }
+            int tot;
+            int pos = n + block_excl_scan<NT>(__popc(bits), shi, &tot);
+            if (n + tot > kTsCap) return -1;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = r0 + threadIdx.x + NT * u;
+                const float sv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (bits & (1u << (4 * u + q))) {
+                        zs[pos] = sv[q];
+                        cj[pos] = pg[u] * kP + 4 * (e & 3) + q;
+                        cph[pos] = ph[u];
+                        ++pos;
+                    }
+            }
+            n += tot;
+        }
+        return n;
+    };
+    int ncand = extract(tau_lo);
+    if (ncand < 0) {
+        // overflow: fp64 Newton streamed over the whole row moves tau_lo just below tau
+        const int ntk = nlist * kP;
+        double t = tau_lo;
+        for (int it = 0; it < 200; ++it) {
+            double F = 0.0, Fd = 0.0;
+            for (int e = threadIdx.x; e < ntk; e += NT) {
+                const int j = __ldg(plist + e / kP) * kP + e % kP;
+                if (j >= L) continue;
+                const double d = a * (double)srow[j] - t;
+                if (d > 0.0) { F += powB<IB>(d, beta); Fd += powBm1<IB>(d, beta); }
+            }
+            Rd.sum(F, Fd);
+            if (!(Fd > 0.0)) break;
+            const double step = lbeta_step(F, Fd, beta, IB);
+            t += step;
+            if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(t)))) break;
+        }
+        tau_lo = fmax(tau_lo, t - 1e-7 * fmax(1.0, fabs(t)));
+        ncand = extract(tau_lo);
+        if (ncand < 0) {             // support larger than the shared-memory capacity
+            if (threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = NAN;
+            if (threadIdx.x == 0) {
+                if (A.tau_out) A.tau_out[row] = NAN;
+                if (A.supp_out) A.supp_out[row] = -1;
+            }
+            return;
+        }
+    }
+    __syncthreads();
+
+    // ---- 2. fp32 Newton steps (pruning point only)
+    float tf = (float)tau_lo;
+    for (int it = 0; it < 8; ++it) {
+        float F = 0.f, D = 0.f;
+        for (int k = threadIdx.x; k < ncand; k += NT) {
+            const float d = af * zs[k] - tf;
+            if (d > 0.f) { F += powBf<IB>(d, betaf); D += powBm1f<IB>(d, betaf); }
+        }
+        Rf.sum(F, D);
+        if (!(D > 0.f)) break;
+        const float step = (float)lbeta_step((double)F, (double)D, beta, IB);
+        tf += step;
+        if (!(fabsf(step) > 1e-4f * fmaxf(1.0f, fabsf(tf)))) break;
+    }
+
+    // ---- 3. certified base and the list {z > base}
+    auto build = [&](double base, double &Fb) -> int {
+        const float bf = (float)base;
+        const float bpre = bf - 1e-3f * fmaxf(1.0f, fabsf(bf));
+        int np = 0;
+        double f = 0.0, dz = 0.0;
+        for (int r0 = 0; r0 < ncand; r0 += NT) {
+            const int k = r0 + threadIdx.x;
+            bool in = false;
+            double z = 0.0;
+            if (k < ncand && af * zs[k] > bpre) {
+                z = a * (double)zs[k];
+                if (z > base) { in = true; f += powB<IB>(z - base, beta); }
+            }
+            int tot;
+            const int pos = np + block_excl_scan<NT>(in ? 1 : 0, shi, &tot);
+            if (in && pos < kPr) { zp[pos] = z; ip[pos] = k; }
+            np += tot;
+        }
+        Rd.sum(f, dz);
+        Fb = f;
+        return np;
+    };
+    double base = (double)tf - 1e-4 * fmax(1.0, fabs((double)tf));
+    double Fb = 0.0;
+    int np = -1;
+    if (base > tau_lo && tf == tf) {
+        np = build(base, Fb);
+        if (!(Fb >= 1.0)) np = -1;
+    }
+    if (np < 0) { base = tau_lo; np = build(base, Fb); }
+    for (int k = threadIdx.x; k < ncand; k += NT) cin[k] = 0;
+    __syncthreads();
+
+    // ---- 4. support and tau (warp 0)
+    if (warp == 0) {
+        auto wsum2 = [&](double &x, double &y) {
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+                x += __shfl_xor_sync(0xffffffffu, x, o);
+                y += __shfl_xor_sync(0xffffffffu, y, o);
+            }
+        };
+        const bool listed = np <= kPr;
+        const int nl = listed ? np : ncand;
+#define ZL(i) (listed ? zp[i] : a * (double)zs[i])
+#define SL(i) (listed ? ip[i] : (i))
+        double tauN = base;
+        if (listed && np <= 64) {
+            // short list: R9 itself, F(z_j) = sum_i (z_i - z_j)_+^beta < 1, all pairs
+            for (int i = lane; i < nl; i += 32) {
+                const double zj = zp[i];
+                double F0 = 0.0, F1 = 0.0;
+                int i2 = 0;
+                for (; i2 + 1 < nl; i2 += 2) {
+                    const double d0 = zp[i2] - zj, d1 = zp[i2 + 1] - zj;
+                    if (d0 > 0.0) F0 += powB<IB>(d0, beta);
+                    if (d1 > 0.0) F1 += powB<IB>(d1, beta);
+                }
+                if (i2 < nl) { const double d0 = zp[i2] - zj; if (d0 > 0.0) F0 += powB<IB>(d0, beta); }
+                cin[ip[i]] = (F0 + F1 < 1.0) ? 1 : 0;
+            }
+            __syncwarp();
+            if constexpr (IB != 1 && IB != 2) {
+                // Newton start for the tau polish: the largest listed z outside the support
+                // (or base) has F >= 1, i.e. lies left of tau
+                double t0 = base;
+                for (int i = lane; i < nl; i += 32)
+                    if (!cin[ip[i]]) t0 = fmax(t0, zp[i]);
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) t0 = fmax(t0, __shfl_xor_sync(0xffffffffu, t0, o));
+                tauN = t0;
+                for (int it = 0; it < 60; ++it) {
+                    double F = 0.0, Fd = 0.0;
+                    for (int i = lane; i < nl; i += 32)
+                        if (cin[ip[i]]) { const double d = zp[i] - tauN; F += powB<IB>(d, beta); Fd += powBm1<IB>(d, beta); }
+                    wsum2(F, Fd);
+                    if (!(Fd > 0.0)) break;
+                    const double step = lbeta_step(F, Fd, beta, IB);
+                    tauN += step;
+                    if (!(fabs(step) > 1e-15 * fmax(1.0, fabs(tauN)))) break;
+                }
+            }
+        } else {
+            for (int it = 0; it < 64; ++it) {
+                double F = 0.0, Fd = 0.0;
+                for (int i = lane; i < nl; i += 32) {
+                    const double d = ZL(i) - tauN;
+                    if (d > 0.0) { F += powB<IB>(d, beta); Fd += powBm1<IB>(d, beta); }
+                }
+                wsum2(F, Fd);
+                if (!(Fd > 0.0)) break;
+                const double step = lbeta_step(F, Fd, beta, IB);
+                tauN += step;
+                // 1e-14 relative is far inside the support band (R9) and the final tau is
+                // recomputed from the support; a tighter test can oscillate at the ulp level
+                if (!(fabs(step) > 1e-14 * fmax(1.0, fabs(tauN)))) break;
+            }
+            const double band = 1e-9 * fmax(1.0, fabs(tauN));
+            int amb = 0;
+            for (int i = lane; i < nl; i += 32) {
+                const double z = ZL(i);
+                const uint8_t f = (z > tauN + band) ? 1 : (z < tauN - band) ? 0 : 2;
+                cin[SL(i)] = f;
+                amb += (f == 2);
+            }
+            amb = __reduce_add_sync(0xffffffffu, amb);
+            __syncwarp();
+            if (amb > 0) {
+                for (int i0 = 0; i0 < nl; ++i0) {
+                    const int k0 = SL(i0);
+                    if (cin[k0] != 2) continue;
+                    const double zk = ZL(i0);
+                    double F = 0.0, dz = 0.0;
+                    for (int i = lane; i < nl; i += 32) {
+                        const double d = ZL(i) - zk;
+                        if (d > 0.0) F += powB<IB>(d, beta);
+                    }
+                    wsum2(F, dz);
+                    __syncwarp();
+                    if (lane == 0) cin[k0] = (F < 1.0) ? 1 : 0;
+                    __syncwarp();
+                }
+            }
+        }
+        // tau from the support
+        double S1 = 0.0, kk = 0.0;
+        for (int i = lane; i < nl; i += 32)
+            if (cin[SL(i)]) { S1 += ZL(i); kk += 1.0; }
+        wsum2(S1, kk);
+        double tau;
+        if constexpr (IB == 1) {
+            tau = (S1 - 1.0) / kk;
+        } else if constexpr (IB == 2) {
+            const double m = S1 / kk;
+            double ss = 0.0, dz = 0.0;
+            for (int i = lane; i < nl; i += 32)
+                if (cin[SL(i)]) { const double d = ZL(i) - m; ss += d * d; }
+            wsum2(ss, dz);
+            tau = m - sqrt(fmax(0.0, 1.0 - ss) / kk);
+        } else {
+            double F = 0.0, Fd = 0.0;
+            for (int i = lane; i < nl; i += 32)
+                if (cin[SL(i)]) { const double d = ZL(i) - tauN; F += powB<IB>(d, beta); Fd += powBm1<IB>(d, beta); }
+            wsum2(F, Fd);
+            tau = tauN + (F - 1.0) / (beta * Fd);
+        }
+        // support entries (list order) with p_j, if they fit one gather round
+        int nsup = 0;
+        double psum = 0.0, dz = 0.0;
+        const bool one_round = listed && kk <= (double)kTsSup;
+        if (one_round) {
+            for (int i0 = 0; i0 < nl; i0 += 32) {
+                const int i = i0 + lane;
+                const int k = i < nl ? ip[i] : 0;
+                const bool in = i < nl && cin[k];
+                const unsigned bal = __ballot_sync(0xffffffffu, in);
+                const int pos = nsup + __popc(bal & ((1u << lane) - 1u));
+                if (in) {
+                    const double d = zp[i] - tau;
+                    const double pd = d > 0.0 ? powB<IB>(d, beta) : 0.0;
+                    sup_j[pos] = cj[k];
+                    sup_p[pos] = (float)pd;
+                    sup_phys[pos] = cph[k];
+                    psum += pd;
+                }
+                nsup += __popc(bal);
+            }
+            wsum2(psum, dz);
+        }
+#undef ZL
+#undef SL
+        if (lane == 0) { s_tau = tau; s_kk = kk; s_psum = psum; s_nsup = nsup; s_mode = one_round ? 1 : 0; }
+    }
+    __syncthreads();
+    const double tau = s_tau, kk = s_kk;
+
+    // ---- 5. PV
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    double psum = 0.0;
+    auto gather = [&](int nsup) {
+        for (int e0 = warp; e0 < nsup; e0 += 4 * NW) {
+            float vx[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * NW;
+                if (e < nsup) {
+                    const int j = sup_j[e];
+                    ldv4<T>(Vb + (((size_t)sup_phys[e] * c.Hkv + kvh) * kP + (j % kP)) * kD + 4 * lane, vx[u]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * NW;
+                if (e < nsup) {
+                    const float p = sup_p[e];
+#pragma unroll
+                    for (int q2 = 0; q2 < 4; ++q2) acc[q2] = __fmaf_rn(p, vx[u][q2], acc[q2]);
+                }
+            }
+        }
+    };
+    if (s_mode == 1) {
+        gather(s_nsup);
+        if (threadIdx.x == 0) psum = s_psum;
+    } else {
+        // large support: compacted in candidate order, rounds of kTsSup entries
+        for (int r0 = 0; r0 < ncand;) {
+            int nsup = 0, r1 = r0;
+            while (r1 < ncand) {
+                const int k = r1 + threadIdx.x;
+                const bool in = k < ncand && cin[k];
+                int tot;
+                const int pos = nsup + block_excl_scan<NT>(in ? 1 : 0, shi, &tot);
+                if (nsup + tot > kTsSup) break;             // uniform
+                if (in) {
+                    const double d = a * (double)zs[k] - tau;
+                    const double pd = d > 0.0 ? powB<IB>(d, beta) : 0.0;
+                    sup_j[pos] = cj[k];
+                    sup_p[pos] = (float)pd;
+                    sup_phys[pos] = cph[k];
+                    psum += pd;
+                }
+                nsup += tot;
+                r1 += NT;
+            }
+            __syncthreads();
+            gather(nsup);
+            __syncthreads();
+            r0 = r1;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) red[warp][4 * lane + e] = acc[e];
+    double pz = 0.0;
+    Rd.sum(psum, pz);
+    if (threadIdx.x < kD) {
+        float o = 0.f;
+        for (int w = 0; w < NW; ++w) o = __fadd_rn(o, red[w][threadIdx.x]);
+        A.out[(size_t)row * kD + threadIdx.x] = (float)((double)o / psum);
+    }
+    if (threadIdx.x == 0) {
+        if (A.tau_out) A.tau_out[row] = tau;
+        if (A.supp_out) A.supp_out[row] = (int)kk;
+    }
+}
+
+}  // namespace ekv

@@ -119,6 +119,35 @@ def test_topk_ties_lower_index_wins():
         assert pi[0, h, :ns[0, h]].cpu().tolist() == oracle.topk(ob, 5).tolist()
 
 
+@pytest.mark.parametrize("M", [8193, 16391, 40000, 65536])
+def test_topk_large_rows_clusters(M):
+    """Rows of up to 65536 pages: top-k runs as a cluster of 2/4/8 CTAs (8192 pages each).
+    Box scores are fed directly (select reads only seq_lens and the scores); one row has
+    coarse-quantised scores so equal keys straddle CTA boundaries (R3 tie cut)."""
+    dev = torch.device("cuda")
+    B, Hq, Hkv = 3, 2, 1
+    K = torch.zeros(1, Hkv, 16, 128, dtype=torch.bfloat16, device=dev)
+    pt = torch.zeros(B, M, dtype=torch.int32, device=dev)
+    lens = [M * 16, M * 16 - 15, (M // 3) * 16 + 1]
+    dc = ekv.PagedCache.allocate_meta(K, K.clone(), pt, torch.tensor(lens, dtype=torch.int32, device=dev))
+    g = torch.Generator().manual_seed(M)
+    box = torch.randn(B, Hq, M, generator=g)
+    box[0, 1] = torch.round(box[0, 1] * 2) / 2          # ~13 distinct values: massive ties
+    box[1, 0, ::7] = -0.0                                 # -0 == +0 (R3)
+    box[2, 1] = 1.0                                       # all equal
+    boxd = box.to(dev)
+    for k in (1, 656, 4097, M - 1):
+        pi, ns, _ = ekv.select(dc, Hq, ekv.select_params("topk", k), box=boxd)
+        torch.cuda.synchronize()
+        pi, ns = pi.cpu().numpy(), ns.cpu().numpy()
+        for b in range(B):
+            Mb = (lens[b] + 15) // 16
+            for h in range(Hq):
+                ref = oracle.topk(box[b, h, :Mb].numpy(), k)
+                assert ns[b, h] == len(ref), (k, b, h)
+                assert np.array_equal(pi[b, h, :ns[b, h]], ref), (k, b, h)
+
+
 def _check_attend(hc, qh, b, h, G, pages, alpha, transform, out, tau, supp, tol):
     ref = hc.attend(qh[b, h], b, h // G, pages, alpha, transform)
     np.testing.assert_allclose(out, ref["o"], atol=tol, rtol=0, err_msg=f"b={b} h={h}")

@@ -13,10 +13,11 @@ buf=(ctypes.c_ulonglong*256)(); nc=ctypes.c_int()
 for it in range(5):
     ekv.decode(c,wl.q,sel,attn,ws,stats=st); torch.cuda.synchronize()
 L.entmaxkv_debug_stamps(buf, ctypes.byref(nc))
-for k,name in [(0,'tau'),(1,'topk')]:
+for k,name in [(0,'tau'),(1,'topk'),(6,'tau-solver')]:
     v=[buf[k*32+i] for i in range(8)]
-    print(name, [ (v[i]-v[0])/1000 for i in range(8) if v[i]])
-print('topk nc', nc.value)
+    b0=buf[0*32+2] if k==6 else v[0]
+    print(name, [ (v[i]-b0)/1000 if v[i] else None for i in range(8)])
+print('tau ncand (block 0)', buf[14], 'newton its', buf[13], 'amb', buf[12], 'listed', buf[11])
 v=[buf[2*32+i] for i in range(16)]
 print('K4 producer', [ (x-v[0])/1000 if x else None for x in v[:13]])
 w=[buf[3*32+i] for i in range(32)]

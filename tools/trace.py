@@ -1,0 +1,65 @@
+"""In-graph kernel timeline of one decode step (library built with EXTRA=-DEKV_STAMPS):
+first-CTA start / last-CTA end of every kernel, from %globaltimer.
+usage: python tools/trace.py [n_tokens] [policy] [k_pages]"""
+import ctypes, sys
+import torch
+sys.path.insert(0, '.')
+from paper_2605_21649_b200 import binding as ekv
+from paper_2605_21649_b200.workload import make_workload, new_tokens
+NAMES = ['append', 'score', 'topk', 'mark', 'attend_scores', 'candidates', 'tau_pv', 'delta_bar', 'gauss_select',
+         'eval_metrics', 'rebuild']
+n = int(sys.argv[1]) if len(sys.argv) > 1 else (1 << 20) - 200
+policy = sys.argv[2] if len(sys.argv) > 2 else 'topk'
+dev = torch.device('cuda')
+Hq, Hkv = 32, 8
+M = (n + 15) // 16
+k = int(sys.argv[3]) if len(sys.argv) > 3 else max(1, -(-M // 100))
+wl = make_workload(1, n, Hq, Hkv, seed=1, device=dev, spare_tokens=200)
+c = ekv.PagedCache.allocate_meta(wl.K, wl.V, wl.page_table, wl.seq_lens)
+ekv.rebuild_page_stats(c)
+sel = ekv.select_params(policy, k)
+attn = ekv.attn_params(1.5)
+ws = ekv.alloc_workspace(c, Hq, sel)
+st = ekv.DecodeStats(1, Hq, dev, delta_bar=True, gauss=policy == 'gauss')
+q, kn, vn = new_tokens(1, Hq, Hkv, seed=7, device=dev)
+out = torch.empty(1, Hq, 128, dtype=torch.float32, device=dev)
+s = torch.cuda.Stream()
+L = ekv.lib()
+L.entmaxkv_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
+
+
+def step():
+    ekv.append_kv(c, kn, vn, stream=s)
+    ekv.decode(c, q, sel, attn, ws, out=out, stats=st, stream=s)
+
+
+with torch.cuda.stream(s):
+    for _ in range(3):
+        step()
+s.synchronize()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=s):
+    step()
+buf = (ctypes.c_ulonglong * 32)()
+for rep in range(3):
+    with torch.cuda.stream(s):
+        g.replay()
+    torch.cuda.synchronize()
+    if not L.entmaxkv_debug_trace(buf, 1):
+        sys.exit('library built without -DEKV_STAMPS')
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        a.record(s)
+        g.replay()
+        b.record(s)
+    torch.cuda.synchronize()
+    L.entmaxkv_debug_trace(buf, 0)
+    ev = [(buf[2 * i], buf[2 * i + 1], NAMES[i]) for i in range(len(NAMES)) if buf[2 * i + 1]]
+    ev.sort()
+    t0 = ev[0][0]
+    print(f'--- replay {rep}: event time {a.elapsed_time(b) * 1e3:.1f} us, traced span {(max(e[1] for e in ev) - t0) / 1e3:.1f} us')
+    prev = t0
+    for st_, en, nm in ev:
+        print(f'  {nm:14s} start {(st_ - t0) / 1e3:7.2f}  dur {(en - st_) / 1e3:7.2f}  gap {(st_ - prev) / 1e3:6.2f}')
+        prev = en
