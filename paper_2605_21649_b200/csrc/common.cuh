@@ -386,6 +386,23 @@ template <int KID> __device__ __forceinline__ void stamp_cta(bool cond, int whic
 template <int KID> __device__ __forceinline__ void count_cta(bool cond, unsigned long long v) {
     if (KID == EKV_CTA_KERNEL && cond && blockIdx.x < 1024) ekv_cta[3][blockIdx.x] = v;
 }
+// per-CTA phase times of one kernel (id EKV_PH_KERNEL: 6 = tau_sparse, 2 = topk) and two
+// per-CTA counters: ekv_ph[phase][cta] (ns), ekv_phc[which][cta]
+#ifndef EKV_PH_KERNEL
+#define EKV_PH_KERNEL 6
+#endif
+__device__ unsigned long long ekv_ph[8][1024];
+__device__ long long ekv_phc[2][1024];
+template <int KID> __device__ __forceinline__ void ph_stamp(int phase) {
+    if (KID == EKV_PH_KERNEL && threadIdx.x == 0 && blockIdx.x < 1024) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        ekv_ph[phase][blockIdx.x] = t;
+    }
+}
+template <int KID> __device__ __forceinline__ void ph_count(int which, long long v) {
+    if (KID == EKV_PH_KERNEL && threadIdx.x == 0 && blockIdx.x < 1024) ekv_phc[which][blockIdx.x] = v;
+}
 // whole-kernel trace: first CTA start (min) and last CTA end (max, thread 0 of each CTA)
 __device__ unsigned long long ekv_trace[16][2];
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -405,6 +422,8 @@ struct TraceScope {
 #define EKV_TRACE(kid) ::ekv::TraceScope ekv_trace_scope_(kid)
 #else
 #define EKV_TRACE(kid) do {} while (0)
+template <int KID> __device__ __forceinline__ void ph_stamp(int) {}
+template <int KID> __device__ __forceinline__ void ph_count(int, long long) {}
 __device__ __forceinline__ void stamp(int, int) {}
 __device__ __forceinline__ void stamp_if(bool, int, int) {}
 template <int KID> __device__ __forceinline__ void stamp_cta(bool, int) {}

@@ -276,8 +276,9 @@ ekv_status launch_tau(const CacheView &v, const TauArgs &A, int rows, cudaStream
 template <typename T, int IB>
 ekv_status launch_tau_sparse_ib(const CacheView &v, const TauArgs &A, int rows, cudaStream_t st) {
     static bool init = false;
-    if (!init) { set_smem(k_tau_sparse<T, IB>, kTsSmem); init = true; }
-    k_tau_sparse<T, IB><<<rows, kTsNT, kTsSmem, st>>>(v, A);
+    constexpr int smem = ts_smem<T>();
+    if (!init) { set_smem(k_tau_sparse<T, IB>, smem); init = true; }
+    k_tau_sparse<T, IB><<<rows, kTsNT, smem, st>>>(v, A);
     return check_launch("k_tau_sparse");
 }
 // integer beta = 1/(alpha-1) in 1..4 is a template constant; any other alpha -> IB = 0
@@ -397,6 +398,17 @@ int entmaxkv_debug_trace(unsigned long long *out, int reset) {
     return 1;
 #else
     (void)out; (void)reset;
+    return 0;
+#endif
+}
+/* Debug: per-CTA phase stamps [8][1024] ns and counters [2][1024]. */
+int entmaxkv_debug_phases(unsigned long long *ph, long long *cnt) {
+#ifdef EKV_STAMPS
+    cudaMemcpyFromSymbol(ph, ekv::ekv_ph, sizeof(unsigned long long) * 8 * 1024);
+    cudaMemcpyFromSymbol(cnt, ekv::ekv_phc, sizeof(long long) * 2 * 1024);
+    return 1;
+#else
+    (void)ph; (void)cnt;
     return 0;
 #endif
 }

@@ -10,20 +10,24 @@ namespace ekv {
 // A thread-block cluster of CL CTAs (CL = 1, 2, 4 or 8) per (b, q-head) row (
 // R3: key desc, then lower page index).  Keys are the ordered-int encodings of the fp32
 // box scores (-0 == +0; pages past the sequence end get key 0, below every real key).
-// CTA r of the cluster owns pages [8192 r, 8192 (r + 1)); thread t holds the 32 keys of
-// pages 8192 r + 4 (t + 256 j) + e (j < 8, e < 4: coalesced float4 loads) in registers.
+// CTA r of the cluster owns pages [8192 r, 8192 (r + 1)); thread t (of 512) holds the 16
+// keys of pages 8192 r + 4 (t + 512 j) + e (j < 4, e < 4: coalesced float4 loads, issued
+// together with the sequence-length load) in registers.  Many threads per CTA: every
+// step below is a chain of dependent warp-synchronous instructions, hidden only by TLP.
 //  1. MSB-first radix select of T* = the k-th largest key with 8-bit digits: each CTA
-//     histograms the digit of its keys that match the prefix so far (warp-aggregated
-//     shared atomics), the cluster barrier publishes the histograms, every CTA sums the CL
-//     histograms through distributed shared memory and locates the digit holding the k-th
-//     key (warp suffix scan).  Two alternating histogram buffers: one cluster barrier per
-//     digit.  A digit whose whole bin is taken ends the search early (no tie cut needed).
+//     histograms the digit of its keys that match the prefix so far (per-warp private
+//     shared histograms, one atomic per warp when the active lanes agree -- the usual case
+//     for the leading digits -- then summed), the cluster barrier publishes the CTA
+//     histograms, every CTA sums the CL histograms through distributed shared memory and
+//     locates the digit holding the k-th key (warp suffix scan).  The CTA histogram buffers
+//     alternate: one cluster barrier per digit.  A digit whose whole bin is taken ends the search early (no tie cut needed).
 //  2. Ties at T* (only if the bin of T* is split): CTA r takes the first
 //     clamp(need - #eq in CTAs < r, 0, #eq in r) equal keys in page order.
-//  3. Selection bitmap (bit = page), one word per thread, block scan + cluster offsets:
-//     ascending page ids, and -- if umask != NULL -- the KV-group union marks.
-constexpr int kTkNT = 256;
-constexpr int kTkKPT = 32;
+//  3. Selection bitmap (bit = page), one word per thread (t < 256), block scan + cluster
+//     offsets: ascending page ids, and -- if umask != NULL -- the KV-group union marks.
+//     (512 threads, 2 CTAs per SM: the 256 CTAs of a 32-row, 65536-page launch are one wave.)
+constexpr int kTkNT = 512;
+constexpr int kTkKPT = 16;
 constexpr int kTkPerCta = kTkNT * kTkKPT;   // 8192 pages per CTA, <= 8 CTAs -> 65536 pages
 
 // union mark of one selected page: bit g of the page's byte (fire-and-forget atomic)
@@ -31,8 +35,8 @@ __device__ __forceinline__ void union_mark(uint32_t *um, int p, int g) {
     atomicOr(um + (p >> 2), 1u << ((p & 3) * 8 + g));
 }
 
-// bitmap word of the CTA-local pages 1024 j + 4 t + e (e < 4) of a 4-bit nibble per thread:
-// 8 consecutive lanes share a word; lane t % 8 == 0 returns it
+// bitmap word of the CTA-local pages 2048 j + 4 t + e (e < 4) of a 4-bit nibble per thread:
+// 8 consecutive lanes share a word (index 64 j + t / 8); lane t % 8 == 0 returns it
 __device__ __forceinline__ uint32_t nibble_word(uint32_t nib, int lane) {
     uint32_t w = nib << (4 * (lane & 7));
     w |= __shfl_xor_sync(0xffffffffu, w, 1);
@@ -51,18 +55,37 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
     const int CL = (int)cl.num_blocks(), r = (int)cl.block_rank();
     const int row = blockIdx.x / CL;
     const int t = threadIdx.x, lane = t & 31;
-    __shared__ uint32_t hist[2][256];
+    constexpr int NWp = kTkNT / 32;
+    __shared__ uint32_t whist[NWp][256];     // per-warp private histograms (no cross-warp contention)
+    __shared__ uint32_t hist[2][256];        // the CTA's histogram of the current digit (published)
     __shared__ uint32_t bits[256];
     __shared__ int xch[2];                   // published to the cluster: [0] #eq, [1] #selected
     __shared__ int sh[(kTkNT / 32 + 2)];
     const int b = row / Hq;
-    const int M = n_pages_of(__ldg(seq_lens + b));
+    const int base = r * kTkPerCta;
+    const float *x = box + (size_t)row * maxp;
+    const bool vec = (maxp & 3) == 0;
+    // keys and the sequence length in one round trip (masked below)
+    const int Lb = __ldg(seq_lens + b);
+    float4 kv[kTkKPT / 4];
+#pragma unroll
+    for (int j = 0; j < kTkKPT / 4; ++j) {
+        const int i4 = base + 4 * (t + kTkNT * j);
+        if (vec && i4 + 3 < maxp) kv[j] = __ldg(reinterpret_cast<const float4 *>(x + i4));
+        else {
+            kv[j].x = (i4 < maxp) ? __ldg(x + i4) : 0.f;
+            kv[j].y = (i4 + 1 < maxp) ? __ldg(x + i4 + 1) : 0.f;
+            kv[j].z = (i4 + 2 < maxp) ? __ldg(x + i4 + 2) : 0.f;
+            kv[j].w = (i4 + 3 < maxp) ? __ldg(x + i4 + 3) : 0.f;
+        }
+    }
+    const int M = n_pages_of(Lb);
     const int keff = min(k, M);
     int32_t *out = page_idx + (size_t)row * sel_stride;
     const int unit = b * (Hq / G) + (row % Hq) / G, gh = (row % Hq) % G;
     uint32_t *um = umask ? umask + (size_t)unit * W : nullptr;
-    const int base = r * kTkPerCta;
     stamp(1, 0);
+    ph_stamp<2>(0);
     if (keff >= M) {                         // every page (uniform over the cluster)
         for (int p = base + t; p < min(M, base + kTkPerCta); p += kTkNT) {
             out[p] = p;
@@ -71,29 +94,19 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
         if (r == 0 && t == 0) n_sel[row] = M;
         return;
     }
-    const float *x = box + (size_t)row * maxp;
-    const bool vec = (maxp & 3) == 0;
     uint32_t key[kTkKPT];
 #pragma unroll
     for (int j = 0; j < kTkKPT / 4; ++j) {
         const int i4 = base + 4 * (t + kTkNT * j);
-        float4 v;
-        if (vec && i4 + 3 < M) v = __ldg(reinterpret_cast<const float4 *>(x + i4));
-        else {
-            v.x = (i4 < M) ? __ldg(x + i4) : 0.f;
-            v.y = (i4 + 1 < M) ? __ldg(x + i4 + 1) : 0.f;
-            v.z = (i4 + 2 < M) ? __ldg(x + i4 + 2) : 0.f;
-            v.w = (i4 + 3 < M) ? __ldg(x + i4 + 3) : 0.f;
-        }
-        key[4 * j] = (i4 < M) ? f2key(v.x) : 0u;
-        key[4 * j + 1] = (i4 + 1 < M) ? f2key(v.y) : 0u;
-        key[4 * j + 2] = (i4 + 2 < M) ? f2key(v.z) : 0u;
-        key[4 * j + 3] = (i4 + 3 < M) ? f2key(v.w) : 0u;
+        key[4 * j] = (i4 < M) ? f2key(kv[j].x) : 0u;
+        key[4 * j + 1] = (i4 + 1 < M) ? f2key(kv[j].y) : 0u;
+        key[4 * j + 2] = (i4 + 2 < M) ? f2key(kv[j].z) : 0u;
+        key[4 * j + 3] = (i4 + 3 < M) ? f2key(kv[j].w) : 0u;
     }
-    hist[0][t] = 0u;
-    hist[1][t] = 0u;
+    for (int i = t; i < NWp * 256; i += kTkNT) (&whist[0][0])[i] = 0u;
     __syncthreads();
     stamp(1, 1);
+    ph_stamp<2>(1);
     // 1. radix select over the cluster
     uint32_t prefix = 0u, pmask = 0u;
     int kk = keff;                           // keys still to take among those matching prefix
@@ -102,6 +115,7 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
     for (int pass = 0; pass < 4; ++pass) {
         const int shift = 24 - 8 * pass;
         uint32_t *hb = hist[pass & 1];
+        uint32_t *wh = whist[t >> 5];
 #pragma unroll
         for (int j = 0; j < kTkKPT; ++j) {
             const uint32_t v = key[j];
@@ -115,17 +129,26 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
             const uint32_t dl = __shfl_sync(0xffffffffu, d, leader);
             const unsigned same = __ballot_sync(0xffffffffu, act && d == dl);
             if (same == bal) {
-                if (lane == leader) atomicAdd(&hb[dl], (uint32_t)__popc(bal));
+                if (lane == leader) atomicAdd(&wh[dl], (uint32_t)__popc(bal));
             } else if (act) {
-                atomicAdd(&hb[d], 1u);
+                atomicAdd(&wh[d], 1u);
             }
         }
+        __syncthreads();
+        if (t < 256) {                       // CTA histogram = sum of the warp histograms (then cleared)
+            uint32_t sum = 0u;
+#pragma unroll
+            for (int w = 0; w < NWp; ++w) { sum += whist[w][t]; whist[w][t] = 0u; }
+            hb[t] = sum;
+        }
+        ph_stamp<2>(2 + pass);
         cl.sync();                           // histograms of this digit visible cluster-wide
         // the other buffer was last read remotely before this barrier: clear it for the next digit
-        if (pass + 1 < 4 && pass >= 1) hist[(pass + 1) & 1][t] = 0u;
-        uint32_t g = 0u;
-        for (int q = 0; q < CL; ++q) g += cl.map_shared_rank(hb, q)[t];
-        bits[t] = g;                         // global histogram (bits[] is free until step 3)
+        if (t < 256) {
+            uint32_t g = 0u;
+            for (int q = 0; q < CL; ++q) g += cl.map_shared_rank(hb, q)[t];
+            bits[t] = g;                     // global histogram (bits[] is free until step 3)
+        }
         __syncthreads();
         if (t < 32) {
             int v[8], s = 0;
@@ -159,6 +182,7 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
         if (kk == cnt) { whole = true; break; }
     }
     stamp(1, 2);
+    ph_stamp<2>(6);
     // selected: (key & pmask) > prefix, or (key & pmask) == prefix and (whole, or one of the
     // first kk equal keys in page order)
     int take = 0;
@@ -172,17 +196,17 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
         int before = 0;
         for (int q = 0; q < r; ++q) before += *cl.map_shared_rank(&xch[0], q);
         take = min(max(kk - before, 0), ceq);
-        // equal keys of this CTA in page order: bitmap, word t = pages 32 t .. 32 t + 31
+        // equal keys of this CTA in page order: bitmap, word w = pages 32 w .. 32 w + 31
 #pragma unroll
         for (int j = 0; j < kTkKPT / 4; ++j) {
             uint32_t nib = 0u;
 #pragma unroll
             for (int e = 0; e < 4; ++e) nib |= (key[4 * j + e] == prefix ? 1u : 0u) << e;
             const uint32_t w = nibble_word(nib, lane);
-            if ((lane & 7) == 0) bits[32 * j + (t >> 3)] = w;
+            if ((lane & 7) == 0) bits[64 * j + (t >> 3)] = w;
         }
         __syncthreads();
-        uint32_t w = bits[t];
+        uint32_t w = t < 256 ? bits[t] : 0u;
         int tot;
         int rank = block_excl_scan<kTkNT>(__popc(w), sh, &tot);
         uint32_t keep = 0u;
@@ -193,7 +217,7 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
             w ^= lb;
         }
         __syncthreads();
-        bits[t] = keep;                      // chosen equal keys
+        if (t < 256) bits[t] = keep;         // chosen equal keys
         __syncthreads();
     }
     // 3. selection bitmap and ascending output
@@ -208,12 +232,12 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
         }
         const uint32_t w = nibble_word(nib, lane);
         if ((lane & 7) == 0) {
-            const int wi = 32 * j + (t >> 3);
+            const int wi = 64 * j + (t >> 3);
             bits[wi] = whole ? w : (w | bits[wi]);
         }
     }
     __syncthreads();
-    const uint32_t w = bits[t];
+    const uint32_t w = t < 256 ? bits[t] : 0u;
     int tot;
     const int pos = block_excl_scan<kTkNT>(__popc(w), sh, &tot);
     if (t == 0) xch[1] = tot;
@@ -229,6 +253,7 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
     }
     if (r == 0 && t == 0) n_sel[row] = keff;
     stamp(1, 6);
+    ph_stamp<2>(7);
     cl.sync();                               // keep shared memory alive for remote readers
 }
 

@@ -7,21 +7,27 @@
 // One CTA (256 threads) per row.  Work is shaped around latency (one CTA per row, few
 // rows): every pass over the candidates is block-parallel, and only the short exact phase
 // runs on one warp.
+// Global-memory round trips dominate (~1 us each), so the kernel issues every independent
+// load up front: row max, list length and the page list of the first round (12 items of
+// 4 scores per thread: 768 pages) go out together, then the scores and page-table entries.
 //  1. Candidates {j in C_tok : z_j > tau_lo = z_max - 1} (tau >= z_max - 1 since
-//     F(z_max - 1) >= 1): items of 4 consecutive scores (float4) of the page list,
-//     8 items per thread in flight, fp32 pre-test then the fp64 test, block-scan
-//     compaction (fixed order: deterministic sums below).
+//     F(z_max - 1) >= 1): fp32 pre-test then the fp64 test, block-scan compaction (fixed
+//     order: deterministic sums below).
 //  2. fp32 Newton steps on ||(z - t)_+||_beta - 1 from tau_lo (block sums): a pruning
 //     point t32 only -- nothing is decided in fp32.
 //  3. base = t32 - 1e-4 max(1, |t32|) is kept iff F(base) >= 1 in fp64 (then tau >= base
 //     because F decreases); else base = tau_lo.  The list {z > base} (z in fp64) is
 //     compacted in candidate order.  Every candidate outside it has z <= base <= tau,
 //     i.e. F(z) >= 1: not in the support (R9).
-//  4. Warp 0: support by R9 itself on the list -- short lists (<= 64): F(z_j) < 1 for every
-//     entry, all pairs; longer lists: fp64 Newton from base, then z > tau_N + band in,
-//     z < tau_N - band out, F(z_j) < 1 in between.  tau from the support (closed forms for
-//     beta = 1, 2; Newton on the support otherwise), p_j = (z_j - tau)^beta.
-//  5. PV: warps gather the V rows of the support (4 in flight per warp, lane = 4 dims);
+//     The V rows of a short list (<= 64 entries) are copied to shared memory now
+//     (cp.async), overlapping step 4.
+//  4. Support by R9 itself: short lists (<= 32, beta = 1 or 2): F(z_j) = sum_i (z_i -
+//     z_j)_+^beta < 1 for every entry, all pairs over the whole block (8 threads per entry),
+//     tau from the support's closed form by block sums.  Otherwise warp 0: all pairs (<= 64)
+//     or fp64 Newton from base, then z > tau_N + band in, z < tau_N - band out, F(z_j) < 1
+//     in between; tau by the closed forms (beta = 1, 2) or Newton on the support.
+//  5. PV: p_j = (z_j - tau)^beta; warps accumulate p_j v_j (V from shared memory for short
+//     lists, else gathered, 4 rows in flight per warp; lane = 4 dims);
 //     out = sum p_j v_j / sum p_j (R12).
 // Overflow (more candidates than shared memory): fp64 Newton streamed over the score row
 // raises tau_lo to just below tau, then the extraction is repeated.
@@ -82,9 +88,21 @@ template <int NT> struct BlockRed2f {
 };
 
 constexpr int kTsNT = 256;
-constexpr int kTsCap = 12288;                                         // candidates in shared memory
-constexpr int kTsSup = 2048;                                          // support entries per gather round
-constexpr int kTsSmem = (4 + 4 + 4 + 1) * kTsCap + (8 + 4) * kPr;     // zs, cj, cph, cin + list
+constexpr int kTsCap = 10240;                                         // candidates in shared memory
+constexpr int kTsSup = 1024;                                          // support entries per gather round
+constexpr int kTsVpre = 64;                                           // V rows staged for short lists
+constexpr int kTsU = 12;                                              // float4 items per thread per round
+template <typename T> constexpr int ts_smem() {
+    return (4 + 4 + 4 + 1) * kTsCap + (8 + 4) * kPr + kTsVpre * kD * (int)sizeof(T);
+}
+
+__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 
 template <typename T, int IB>
 __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A) {
@@ -96,9 +114,10 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
     int *cph = reinterpret_cast<int *>(smem + 8 * kTsCap);                 // physical pages
     double *zp = reinterpret_cast<double *>(smem + 12 * kTsCap);           // list z (fp64)
     int *ip = reinterpret_cast<int *>(smem + 12 * kTsCap + 8 * kPr);       // list -> candidate slot
-    uint8_t *cin = reinterpret_cast<uint8_t *>(smem + 12 * kTsCap + 12 * kPr);   // support flags
+    T *vpre = reinterpret_cast<T *>(smem + 12 * kTsCap + 12 * kPr);        // [kTsVpre][kD] staged V rows
+    uint8_t *cin = reinterpret_cast<uint8_t *>(smem + 12 * kTsCap + 12 * kPr + kTsVpre * kD * sizeof(T));
     __shared__ float red[NW][kD];
-    __shared__ int sup_j[kTsSup], sup_phys[kTsSup];
+    __shared__ int sup_j[kTsSup], sup_phys[kTsSup];   // (staged path: sup_j = list index)
     __shared__ float sup_p[kTsSup];
     __shared__ double rbuf[2 * 2 * NW];
     __shared__ float rbuff[2 * 2 * NW];
@@ -110,9 +129,20 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
 
     const int row = blockIdx.x;
     const int b = row / A.Hq, h = row % A.Hq, kvh = h / A.G;
-    const int L = c.seq_lens[b];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t mk = A.rowmax[row];
+    const int32_t *plist = A.page_idx + (size_t)row * A.sel_stride;
+    // independent loads first (one round trip): row max, list length, sequence length and
+    // the first round's page list
+    const uint32_t mk = __ldg(A.rowmax + row);
+    const int nlist = __ldg(A.n_sel + row);
+    const int L = __ldg(c.seq_lens + b);
+    int pg[kTsU];
+#pragma unroll
+    for (int u = 0; u < kTsU; ++u) {
+        const int i = (threadIdx.x + NT * u) >> 2;
+        pg[u] = i < A.sel_stride ? __ldg(plist + i) : -1;
+    }
+    ph_stamp<6>(0);
     if (mk == 0u) {   // empty C_tok
         if (threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = 0.0f;
         if (threadIdx.x == 0) {
@@ -122,8 +152,6 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
         return;
     }
     const float smax = key2f(mk);
-    const int nlist = A.n_sel[row];
-    const int32_t *plist = A.page_idx + (size_t)row * A.sel_stride;
     const float *srow = A.scores + (size_t)row * A.ntok;
     const int32_t *ptab = c.page_table + (size_t)b * c.maxp;
     const T *Vb = reinterpret_cast<const T *>(c.V);
@@ -134,59 +162,66 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
     double tau_lo = zmax - 1.0 - 1e-12 * fmax(1.0, fabs(zmax));
 
     // ---- 1. candidates {z > tau_lo} (returns -1 on overflow; uniform)
-    auto extract = [&](double tlo) -> int {
+    auto extract = [&](double tlo, bool have_pg) -> int {
         const float thr_c = (float)(tlo / a);
         const float thr_f = thr_c - 1e-6f * fmaxf(1.0f, fabsf(thr_c));   // conservative fp32 pre-test
         const int nitems = nlist * 4;
         int n = 0;
-        for (int r0 = 0; r0 < nitems; r0 += 8 * NT) {
-            float4 v[8];
-            int pg[8], ph[8];
+        for (int r0 = 0; r0 < nitems; r0 += kTsU * NT) {
+            if (r0 > 0 || !have_pg) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int e = r0 + threadIdx.x + NT * u;
-                pg[u] = e < nitems ? __ldg(plist + (e >> 2)) : -1;
+                for (int u = 0; u < kTsU; ++u) {
+                    const int e = r0 + threadIdx.x + NT * u;
+                    pg[u] = e < nitems ? __ldg(plist + (e >> 2)) : -1;
+                }
             }
+            float4 v[kTsU];
+            int ph[kTsU];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < kTsU; ++u) {
                 const int e = r0 + threadIdx.x + NT * u;
+                if (e >= nitems) pg[u] = -1;
                 if (pg[u] >= 0) {
                     v[u] = *reinterpret_cast<const float4 *>(srow + (size_t)pg[u] * kP + 4 * (e & 3));
                     ph[u] = __ldg(ptab + pg[u]);
                 }
             }
-            uint32_t bits = 0u;
+            uint64_t bits = 0ull;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < kTsU; ++u) {
                 if (pg[u] < 0) continue;
                 const int e = r0 + threadIdx.x + NT * u;
                 const int j0 = pg[u] * kP + 4 * (e & 3);
                 const float sv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
-                    if (j0 + q < L && sv[q] >= thr_f && a * (double)sv[q] > tlo) bits |= 1u << (4 * u + q);
+                    if (j0 + q < L && sv[q] >= thr_f && a * (double)sv[q] > tlo) bits |= 1ull << (4 * u + q);
             }
             int tot;
-            int pos = n + block_excl_scan<NT>(__popc(bits), shi, &tot);
+            int pos = n + block_excl_scan<NT>(__popcll(bits), shi, &tot);
             if (n + tot > kTsCap) return -1;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            while (bits) {
+                const int bi = __ffsll(bits) - 1;
+                bits &= bits - 1;
+                const int u = bi >> 2, q = bi & 3;
                 const int e = r0 + threadIdx.x + NT * u;
-                const float sv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+                float sv = 0.f;
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (bits & (1u << (4 * u + q))) {
-                        zs[pos] = sv[q];
-                        cj[pos] = pg[u] * kP + 4 * (e & 3) + q;
-                        cph[pos] = ph[u];
-                        ++pos;
-                    }
+                for (int uu = 0; uu < kTsU; ++uu)        // register select (no local memory)
+                    if (uu == u) sv = q == 0 ? v[uu].x : q == 1 ? v[uu].y : q == 2 ? v[uu].z : v[uu].w;
+                int pgu = 0, phu = 0;
+#pragma unroll
+                for (int uu = 0; uu < kTsU; ++uu) if (uu == u) { pgu = pg[uu]; phu = ph[uu]; }
+                zs[pos] = sv;
+                cj[pos] = pgu * kP + 4 * (e & 3) + q;
+                cph[pos] = phu;
+                ++pos;
             }
             n += tot;
         }
         return n;
     };
-    int ncand = extract(tau_lo);
+    int ncand = extract(tau_lo, true);
     if (ncand < 0) {
         // overflow: fp64 Newton streamed over the whole row moves tau_lo just below tau
         const int ntk = nlist * kP;
@@ -206,7 +241,7 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
             if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(t)))) break;
         }
         tau_lo = fmax(tau_lo, t - 1e-7 * fmax(1.0, fabs(t)));
-        ncand = extract(tau_lo);
+        ncand = extract(tau_lo, false);
         if (ncand < 0) {             // support larger than the shared-memory capacity
             if (threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = NAN;
             if (threadIdx.x == 0) {
@@ -217,10 +252,12 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
         }
     }
     __syncthreads();
+    ph_stamp<6>(1);
+    ph_count<6>(0, ncand);
 
     // ---- 2. fp32 Newton steps (pruning point only)
     float tf = (float)tau_lo;
-    for (int it = 0; it < 8; ++it) {
+    for (int it = 0; it < 6; ++it) {
         float F = 0.f, D = 0.f;
         for (int k = threadIdx.x; k < ncand; k += NT) {
             const float d = af * zs[k] - tf;
@@ -230,8 +267,9 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
         if (!(D > 0.f)) break;
         const float step = (float)lbeta_step((double)F, (double)D, beta, IB);
         tf += step;
-        if (!(fabsf(step) > 1e-4f * fmaxf(1.0f, fabsf(tf)))) break;
+        if (!(fabsf(step) > 1e-3f * fmaxf(1.0f, fabsf(tf)))) break;
     }
+    ph_stamp<6>(2);
 
     // ---- 3. certified base and the list {z > base}
     auto build = [&](double base, double &Fb) -> int {
@@ -264,11 +302,69 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
         if (!(Fb >= 1.0)) np = -1;
     }
     if (np < 0) { base = tau_lo; np = build(base, Fb); }
-    for (int k = threadIdx.x; k < ncand; k += NT) cin[k] = 0;
-    __syncthreads();
+    const bool listed = np <= kPr;
+    const bool staged = np <= kTsVpre;
+    if (staged) {
+        // V rows of the list entries -> shared memory, in flight during step 4
+        constexpr int CH = kD * (int)sizeof(T) / 16;          // 16-byte chunks per row
+        for (int e = threadIdx.x; e < np * CH; e += NT) {
+            const int i = e / CH, ch = e - i * CH;
+            const int k = ip[i];
+            const int j = cj[k];
+            const T *src = Vb + (((size_t)cph[k] * c.Hkv + kvh) * kP + (j % kP)) * kD;
+            cp_async16(reinterpret_cast<char *>(vpre + (size_t)i * kD) + 16 * ch,
+                       reinterpret_cast<const char *>(src) + 16 * ch);
+        }
+        cp_async_commit();
+    }
+    if (!listed) for (int k = threadIdx.x; k < ncand; k += NT) cin[k] = 0;
+    ph_stamp<6>(3);
+    ph_count<6>(1, np);
 
-    // ---- 4. support and tau (warp 0)
-    if (warp == 0) {
+    // ---- 4. support and tau
+    const bool block_path = (IB == 1 || IB == 2) && np <= 32;
+    if (block_path) {
+        // R9 on every list entry: thread t -> entry t / 8, partial sum over i = t % 8 (mod 8)
+        const int jj = threadIdx.x >> 3, cc = threadIdx.x & 7;
+        double F = 0.0, zj = 0.0;
+        if (jj < np) {
+            zj = zp[jj];
+            for (int i2 = cc; i2 < np; i2 += 8) {
+                const double d = zp[i2] - zj;
+                if (d > 0.0) F += powB<IB>(d, beta);
+            }
+        }
+        F += __shfl_xor_sync(0xffffffffu, F, 1);
+        F += __shfl_xor_sync(0xffffffffu, F, 2);
+        F += __shfl_xor_sync(0xffffffffu, F, 4);
+        const bool in = jj < np && cc == 0 && F < 1.0;
+        double S1 = in ? zj : 0.0, kk = in ? 1.0 : 0.0;
+        Rd.sum(S1, kk);
+        double tau;
+        if constexpr (IB == 1) {
+            tau = (S1 - 1.0) / kk;
+        } else {
+            const double m = S1 / kk;
+            double ss = in ? (zj - m) * (zj - m) : 0.0, dz = 0.0;
+            Rd.sum(ss, dz);
+            tau = m - sqrt(fmax(0.0, 1.0 - ss) / kk);
+        }
+        // support entries in list order (warp 0 holds entries 0..3 of each lane group: use a
+        // block scan over the entry owners)
+        int tot;
+        const int pos = block_excl_scan<NT>(in ? 1 : 0, shi, &tot);
+        double pd = 0.0;
+        if (in) {
+            const double d = zj - tau;
+            pd = d > 0.0 ? powB<IB>(d, beta) : 0.0;
+            sup_j[pos] = jj;                       // list index (V staged)
+            sup_p[pos] = (float)pd;
+        }
+        if (threadIdx.x == 0) { s_tau = tau; s_kk = kk; s_nsup = tot; s_mode = 2; }
+        double psum = pd, dz = 0.0;
+        Rd.sum(psum, dz);                          // (barrier: sup_* and s_* visible)
+        if (threadIdx.x == 0) s_psum = psum;
+    } else if (warp == 0) {
         auto wsum2 = [&](double &x, double &y) {
 #pragma unroll
             for (int o = 16; o >= 1; o >>= 1) {
@@ -276,7 +372,6 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
                 y += __shfl_xor_sync(0xffffffffu, y, o);
             }
         };
-        const bool listed = np <= kPr;
         const int nl = listed ? np : ncand;
 #define ZL(i) (listed ? zp[i] : a * (double)zs[i])
 #define SL(i) (listed ? ip[i] : (i))
@@ -394,7 +489,7 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
                 if (in) {
                     const double d = zp[i] - tau;
                     const double pd = d > 0.0 ? powB<IB>(d, beta) : 0.0;
-                    sup_j[pos] = cj[k];
+                    sup_j[pos] = staged ? i : cj[k];
                     sup_p[pos] = (float)pd;
                     sup_phys[pos] = cph[k];
                     psum += pd;
@@ -405,9 +500,14 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
         }
 #undef ZL
 #undef SL
-        if (lane == 0) { s_tau = tau; s_kk = kk; s_psum = psum; s_nsup = nsup; s_mode = one_round ? 1 : 0; }
+        if (lane == 0) {
+            s_tau = tau; s_kk = kk; s_psum = psum; s_nsup = nsup;
+            s_mode = one_round ? (staged ? 2 : 1) : 0;
+        }
     }
+    if (staged) cp_async_commit_wait_all();
     __syncthreads();
+    ph_stamp<6>(4);
     const double tau = s_tau, kk = s_kk;
 
     // ---- 5. PV
@@ -435,7 +535,18 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
             }
         }
     };
-    if (s_mode == 1) {
+    if (s_mode == 2) {
+        // staged V rows: warp w takes entries w, w + NW, ...
+        const int nsup = s_nsup;
+        for (int e = warp; e < nsup; e += NW) {
+            float vx[4];
+            ldv4<T>(vpre + (size_t)sup_j[e] * kD + 4 * lane, vx);
+            const float p = sup_p[e];
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2) acc[q2] = __fmaf_rn(p, vx[q2], acc[q2]);
+        }
+        if (threadIdx.x == 0) psum = s_psum;
+    } else if (s_mode == 1) {
         gather(s_nsup);
         if (threadIdx.x == 0) psum = s_psum;
     } else {
@@ -478,6 +589,7 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
         if (A.tau_out) A.tau_out[row] = tau;
         if (A.supp_out) A.supp_out[row] = (int)kk;
     }
+    ph_stamp<6>(5);
 }
 
 }  // namespace ekv

@@ -63,3 +63,22 @@ for rep in range(3):
     for st_, en, nm in ev:
         print(f'  {nm:14s} start {(st_ - t0) / 1e3:7.2f}  dur {(en - st_) / 1e3:7.2f}  gap {(st_ - prev) / 1e3:6.2f}')
         prev = en
+
+# per-CTA phases of the EKV_PH_KERNEL kernel (last replay)
+import numpy as np
+L.entmaxkv_debug_phases.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+ph = np.zeros((8, 1024), dtype=np.uint64)
+cn = np.zeros((2, 1024), dtype=np.int64)
+L.entmaxkv_debug_phases(ph.ctypes.data, cn.ctypes.data)
+used = [i for i in range(8) if ph[i].any()]
+if used:
+    m = ph[0] > 0
+    t0 = ph[0][m].min()
+    print('per-CTA phases (us from first CTA start): p10 / p50 / p90 / max')
+    for i in used:
+        x = (ph[i][m].astype(np.float64) - t0) / 1e3
+        print(f'  phase {i}: ' + ' / '.join(f'{v:7.2f}' for v in np.percentile(x, [10, 50, 90, 100])))
+    last = int(np.argmax(ph[max(used)] * m))
+    print('slowest CTA', last, 'phases', [round((int(ph[i][last]) - int(ph[0][last])) / 1e3, 2) for i in used],
+          'counters', cn[0][last], cn[1][last])
+    print('counters p50/max', np.percentile(cn[0][m], [50, 100]), np.percentile(cn[1][m], [50, 100]))
