@@ -596,16 +596,33 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
     const int rows = cache->batch * n_q_heads;
     // a4: certified dropped-mass bound (wide kernel; deterministic ticketed final sum)
     if (want_db) {
-        const int nch = (maxp + kDbChunk - 1) / kDbChunk;
-        dim3 g(nch, rows);
+        const int nch = (maxp + kDbChunk - 1) / kDbChunk;   // <= 8 (max_pages <= 65536)
         DbConst kc;
         kc.a = (double)attn->alpha - 1.0;
         kc.beta = 1.0 / kc.a;
         kc.inv_a = kc.beta;
         kc.ib = (std::fabs(kc.beta - std::rint(kc.beta)) < 1e-12 && kc.beta <= 4.5) ? (int)std::rint(kc.beta) : 0;
-        k_delta_bar<<<g, 256, 0, st>>>(box, maxp, cache->seq_lens, n_q_heads, Gq, uo.umask, L.W, tau_p,
-                                       kc, at<double>(workspace, L.db_partial), nch,
-                                       at<unsigned int>(workspace, L.tickets), stats->delta_bar);
+        cudaLaunchConfig_t cfg;
+        memset(&cfg, 0, sizeof(cfg));
+        cfg.gridDim = dim3((unsigned)nch, (unsigned)rows);
+        cfg.blockDim = dim3(256);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)nch;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaError_t ce;
+        switch (kc.ib) {
+        case 1: ce = cudaLaunchKernelEx(&cfg, k_delta_bar<1>, (const float *)box, maxp, (const int32_t *)cache->seq_lens, n_q_heads, Gq, (const uint32_t *)uo.umask, L.W, (const double *)tau_p, kc, stats->delta_bar); break;
+        case 2: ce = cudaLaunchKernelEx(&cfg, k_delta_bar<2>, (const float *)box, maxp, (const int32_t *)cache->seq_lens, n_q_heads, Gq, (const uint32_t *)uo.umask, L.W, (const double *)tau_p, kc, stats->delta_bar); break;
+        case 3: ce = cudaLaunchKernelEx(&cfg, k_delta_bar<3>, (const float *)box, maxp, (const int32_t *)cache->seq_lens, n_q_heads, Gq, (const uint32_t *)uo.umask, L.W, (const double *)tau_p, kc, stats->delta_bar); break;
+        case 4: ce = cudaLaunchKernelEx(&cfg, k_delta_bar<4>, (const float *)box, maxp, (const int32_t *)cache->seq_lens, n_q_heads, Gq, (const uint32_t *)uo.umask, L.W, (const double *)tau_p, kc, stats->delta_bar); break;
+        default: ce = cudaLaunchKernelEx(&cfg, k_delta_bar<0>, (const float *)box, maxp, (const int32_t *)cache->seq_lens, n_q_heads, Gq, (const uint32_t *)uo.umask, L.W, (const double *)tau_p, kc, stats->delta_bar); break;
+        }
+        if (ce != cudaSuccess) return fail(EKV_ERR_CUDA, "k_delta_bar: %s", cudaGetErrorString(ce));
         EKV_TRY(check_launch("k_delta_bar"));
     }
 

@@ -3,6 +3,7 @@
 // threshold + support, and the weighted V sum over the support.
 #pragma once
 #include "common.cuh"
+#include <cooperative_groups.h>
 
 namespace ekv {
 
@@ -1019,44 +1020,48 @@ struct DbConst {                 // per-call constants of alpha (host-computed)
     int ib;                      // integer beta in 1..4, else 0
 };
 // delta_bar (R16, P:409-420 certificate): per (b, q-head) row, sum over the UNSELECTED
-// valid pages p of n_p * ((alpha-1) * box_p - tau)_+^beta.  Grid (chunks, rows); every
-// thread issues its 8 float4 box loads and 8 union-mask words first (union-mask bit
-// (page, g) = page selected by head g of the unit), then the fp64 terms; partial sums
-// per CTA, deterministic ticketed final sum per row.
+// valid pages p of n_p * ((alpha-1) * box_p - tau)_+^beta.  Grid (chunks, rows), the
+// chunks of a row form one thread-block cluster (<= 8).  Every thread issues its 8 float4
+// box loads, 8 union-mask words (bit (page, g) = page selected by head g of the unit), the
+// row's tau and sequence length together, then the fp64 terms (integer beta IB is a
+// template constant: no pow); the CTA partials are summed in fixed order by rank 0 through
+// distributed shared memory (deterministic, no global ticket).
+template <int IB>
 __global__ void __launch_bounds__(256) k_delta_bar(const float *__restrict__ box, int maxp,
                                                    const int32_t *__restrict__ seq_lens, int Hq, int G,
                                                    const uint32_t *__restrict__ umask, int W,
                                                    const double *__restrict__ tau, DbConst k,
-                                                   double *__restrict__ partial, int nchunks,
-                                                   unsigned int *__restrict__ tickets, double *__restrict__ out) {
+                                                   double *__restrict__ out) {
     EKV_TRACE(7);
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
     constexpr int R = kDbChunk / 1024;
     __shared__ double rbuf[2 * 2 * 8];
-    __shared__ bool s_last;
+    __shared__ double part;
     BlockRed2<256> Rd{rbuf, 0};
     const int row = blockIdx.y, b = row / Hq, h = row - b * Hq;
     const int unit = b * (Hq / G) + h / G, g = h - (h / G) * G;
-    const int L = __ldg(seq_lens + b);
-    const int M = n_pages_of(L);
     const int p0 = blockIdx.x * kDbChunk;
-    const double t = __ldg(tau + row);
     const float *bx = box + (size_t)row * maxp;
     const uint32_t *um = umask + (size_t)unit * W;
+    const bool vec = (maxp & 3) == 0;
+    const int L = __ldg(seq_lens + b);
+    const double t = __ldg(tau + row);
     float bv[4 * R];
     uint32_t mw[R];
-    const bool vec = (maxp & 3) == 0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int p = p0 + 4 * (threadIdx.x + 256 * r);
-        if (vec && p + 3 < M) {
+        if (vec && p + 3 < maxp) {
             const float4 v = __ldg(reinterpret_cast<const float4 *>(bx + p));
             bv[4 * r] = v.x; bv[4 * r + 1] = v.y; bv[4 * r + 2] = v.z; bv[4 * r + 3] = v.w;
         } else {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) bv[4 * r + e] = (p + e < M) ? __ldg(bx + p + e) : -INFINITY;
+            for (int e = 0; e < 4; ++e) bv[4 * r + e] = (p + e < maxp) ? __ldg(bx + p + e) : -INFINITY;
         }
-        mw[r] = (p < M) ? __ldg(um + (p >> 2)) : 0u;
+        mw[r] = (p < maxp) ? __ldg(um + (p >> 2)) : 0u;
     }
+    const int M = n_pages_of(L);
     double db = 0.0, dz = 0.0;
     if (t == t) {   // tau is NaN for an empty row
         // fp32 pre-test: a*box - tau > 0 needs box > tau/a; thr is rounded well below it
@@ -1068,33 +1073,28 @@ __global__ void __launch_bounds__(256) k_delta_bar(const float *__restrict__ box
             for (int e = 0; e < 4; ++e) {
                 const int p = p0 + 4 * (threadIdx.x + 256 * r) + e;
                 const bool sel = (mw[r] >> (8 * e + g)) & 1u;      // page selected by head h
-                if (sel || !(bv[4 * r + e] > thr)) continue;        // also skips p >= M (-inf)
+                if (p >= M || sel || !(bv[4 * r + e] > thr)) continue;
                 const double d = k.a * (double)bv[4 * r + e] - t;
                 if (d > 0.0) {
-                    const double w = powb(d, k.beta, k.ib);
+                    double w;
+                    if constexpr (IB == 1) w = d;
+                    else if constexpr (IB == 2) w = d * d;
+                    else if constexpr (IB == 3) w = d * d * d;
+                    else if constexpr (IB == 4) { const double d2 = d * d; w = d2 * d2; }
+                    else w = pow(d, k.beta);
                     db += (p == M - 1) ? (double)(L - p * kP) * w : (double)kP * w;
                 }
             }
     }
     Rd.sum(db, dz);
-    if (threadIdx.x == 0) {
-        partial[(size_t)row * nchunks + blockIdx.x] = db;
-        __threadfence();
-        const unsigned int tk = atomicAdd(tickets + row, 1u);
-        s_last = (tk == (unsigned)nchunks - 1);
-    }
-    __syncthreads();
-    if (s_last && threadIdx.x < 32) {       // fixed lane -> chunk map and shuffle tree: deterministic
-        __threadfence();
+    if (threadIdx.x == 0) part = db;
+    cl.sync();
+    if (cl.block_rank() == 0 && threadIdx.x == 0) {
         double sum = 0.0;
-        for (int c2 = threadIdx.x; c2 < nchunks; c2 += 32) sum += ((volatile double *)partial)[(size_t)row * nchunks + c2];
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        if (threadIdx.x == 0) {
-            out[row] = (t == t) ? sum : NAN;
-            tickets[row] = 0u;             // ready for the next call
-        }
+        for (int q = 0; q < (int)cl.num_blocks(); ++q) sum += *cl.map_shared_rank(&part, q);
+        out[row] = (t == t) ? sum : NAN;
     }
+    cl.sync();                               // keep shared memory alive for rank 0's reads
 }
 
 // ============================================================================ eval: exact delta / rho
