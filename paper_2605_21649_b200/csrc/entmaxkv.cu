@@ -277,8 +277,29 @@ template <typename T, int IB>
 ekv_status launch_tau_sparse_ib(const CacheView &v, const TauArgs &A, int rows, cudaStream_t st) {
     static bool init = false;
     constexpr int smem = ts_smem<T>();
-    if (!init) { set_smem(k_tau_sparse<T, IB>, smem); init = true; }
-    k_tau_sparse<T, IB><<<rows, kTsNT, smem, st>>>(v, A);
+    if (!init) {
+        set_smem(k_tau_sparse<T, IB>, smem);
+        cudaFuncSetAttribute(k_tau_sparse<T, IB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        init = true;
+    }
+    // a cluster of up to 4 CTAs per row splits the candidate extraction (page-list reads are
+    // latency bound per SM); rank 0 then finishes the row
+    const int CL = A.sel_stride > 384 ? 4 : A.sel_stride > 128 ? 2 : 1;
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3((unsigned)(rows * CL));
+    cfg.blockDim = dim3(kTsNT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_tau_sparse<T, IB>, v, A);
+    if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "k_tau_sparse: %s", cudaGetErrorString(e));
     return check_launch("k_tau_sparse");
 }
 // integer beta = 1/(alpha-1) in 1..4 is a template constant; any other alpha -> IB = 0

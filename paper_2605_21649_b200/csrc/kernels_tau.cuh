@@ -32,6 +32,7 @@
 // Overflow (more candidates than shared memory): fp64 Newton streamed over the score row
 // raises tau_lo to just below tau, then the extraction is repeated.
 #pragma once
+#include <cooperative_groups.h>
 #include "kernels_attend.cuh"
 
 namespace ekv {
@@ -127,25 +128,30 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
     BlockRed2<NT> Rd{rbuf, 0};
     BlockRed2f<NT> Rf{rbuff, 0};
 
-    const int row = blockIdx.x;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int CL = (int)cl.num_blocks(), rk = (int)cl.block_rank();
+    const int row = blockIdx.x / CL;
     const int b = row / A.Hq, h = row % A.Hq, kvh = h / A.G;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int32_t *plist = A.page_idx + (size_t)row * A.sel_stride;
     // independent loads first (one round trip): row max, list length, sequence length and
-    // the first round's page list
+    // this rank's first-round page list
     const uint32_t mk = __ldg(A.rowmax + row);
     const int nlist = __ldg(A.n_sel + row);
     const int L = __ldg(c.seq_lens + b);
+    // rank rk extracts the items [rk S, (rk + 1) S) (item = 4 scores), S from the list capacity
+    const int S = ((A.sel_stride * 4 + CL - 1) / CL + 3) & ~3;
     int pg[kTsU];
 #pragma unroll
     for (int u = 0; u < kTsU; ++u) {
-        const int i = (threadIdx.x + NT * u) >> 2;
-        pg[u] = i < A.sel_stride ? __ldg(plist + i) : -1;
+        const int e = rk * S + threadIdx.x + NT * u;
+        pg[u] = (e < (rk + 1) * S && (e >> 2) < A.sel_stride) ? __ldg(plist + (e >> 2)) : -1;
     }
     ph_stamp<6>(0);
-    if (mk == 0u) {   // empty C_tok
-        if (threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = 0.0f;
-        if (threadIdx.x == 0) {
+    if (mk == 0u) {   // empty C_tok (uniform over the cluster)
+        if (rk == 0 && threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = 0.0f;
+        if (rk == 0 && threadIdx.x == 0) {
             if (A.tau_out) A.tau_out[row] = NAN;
             if (A.supp_out) A.supp_out[row] = 0;
         }
@@ -162,13 +168,14 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
     double tau_lo = zmax - 1.0 - 1e-12 * fmax(1.0, fabs(zmax));
 
     // ---- 1. candidates {z > tau_lo} (returns -1 on overflow; uniform)
-    auto extract = [&](double tlo, bool have_pg) -> int {
+    // items [lo, min(hi, 4 nlist)) in rounds of U * NT; candidates compacted in item order
+    auto extract = [&](double tlo, bool have_pg, int lo, int hi) -> int {
         const float thr_c = (float)(tlo / a);
         const float thr_f = thr_c - 1e-6f * fmaxf(1.0f, fabsf(thr_c));   // conservative fp32 pre-test
-        const int nitems = nlist * 4;
+        const int nitems = min(nlist * 4, hi);
         int n = 0;
-        for (int r0 = 0; r0 < nitems; r0 += kTsU * NT) {
-            if (r0 > 0 || !have_pg) {
+        for (int r0 = lo; r0 < nitems; r0 += kTsU * NT) {
+            if (r0 > lo || !have_pg) {
 #pragma unroll
                 for (int u = 0; u < kTsU; ++u) {
                     const int e = r0 + threadIdx.x + NT * u;
@@ -221,7 +228,34 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
         }
         return n;
     };
-    int ncand = extract(tau_lo, true);
+    int ncand = extract(tau_lo, true, rk * S, (rk + 1) * S);
+    if (CL > 1) {
+        // merge: ranks publish their counts; if everything fits, ranks >= 1 store their
+        // candidates into rank 0's arrays (rank order: deterministic) and leave
+        __shared__ int s_cnt;
+        if (threadIdx.x == 0) s_cnt = ncand;
+        cl.sync();
+        int tot = 0, off = 0;
+        bool ovf = false;
+        for (int q = 0; q < CL; ++q) {
+            const int nq = *cl.map_shared_rank(&s_cnt, q);
+            if (nq < 0) ovf = true;
+            if (q < rk) off += nq;
+            tot += nq;
+        }
+        if (tot > kTsCap) ovf = true;
+        if (!ovf && rk > 0 && ncand > 0) {
+            float *zs0 = cl.map_shared_rank(zs, 0);
+            int *cj0 = cl.map_shared_rank(cj, 0), *cph0 = cl.map_shared_rank(cph, 0);
+            for (int i = threadIdx.x; i < ncand; i += NT) {
+                zs0[off + i] = zs[i]; cj0[off + i] = cj[i]; cph0[off + i] = cph[i];
+            }
+        }
+        cl.sync();
+        if (rk > 0) return;
+        ncand = ovf ? -1 : tot;
+        if (ovf) ncand = extract(tau_lo, false, 0, 1 << 30);   // rank 0 alone (may overflow again)
+    }
     if (ncand < 0) {
         // overflow: fp64 Newton streamed over the whole row moves tau_lo just below tau
         const int ntk = nlist * kP;
@@ -241,7 +275,7 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
             if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(t)))) break;
         }
         tau_lo = fmax(tau_lo, t - 1e-7 * fmax(1.0, fabs(t)));
-        ncand = extract(tau_lo, false);
+        ncand = extract(tau_lo, false, 0, 1 << 30);
         if (ncand < 0) {             // support larger than the shared-memory capacity
             if (threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = NAN;
             if (threadIdx.x == 0) {
@@ -317,52 +351,85 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
         }
         cp_async_commit();
     }
-    if (!listed) for (int k = threadIdx.x; k < ncand; k += NT) cin[k] = 0;
+    for (int k = threadIdx.x; k < ncand; k += NT) cin[k] = 0;
     ph_stamp<6>(3);
     ph_count<6>(1, np);
 
     // ---- 4. support and tau
-    const bool block_path = (IB == 1 || IB == 2) && np <= 32;
+    const bool block_path = listed && np <= NT;
     if (block_path) {
-        // R9 on every list entry: thread t -> entry t / 8, partial sum over i = t % 8 (mod 8)
-        const int jj = threadIdx.x >> 3, cc = threadIdx.x & 7;
+        // R9 on every list entry: TPE threads per entry (npad = np rounded up to a power of
+        // two >= 8), partial sums over i = lane-in-group (mod TPE), xor-shuffle combine
+        int npad = 8;
+        while (npad < np) npad <<= 1;
+        const int TPE = NT / npad;                // 1..32
+        const int jj = threadIdx.x / TPE, cc = threadIdx.x % TPE;
         double F = 0.0, zj = 0.0;
         if (jj < np) {
             zj = zp[jj];
-            for (int i2 = cc; i2 < np; i2 += 8) {
+            for (int i2 = cc; i2 < np; i2 += TPE) {
                 const double d = zp[i2] - zj;
                 if (d > 0.0) F += powB<IB>(d, beta);
             }
         }
-        F += __shfl_xor_sync(0xffffffffu, F, 1);
-        F += __shfl_xor_sync(0xffffffffu, F, 2);
-        F += __shfl_xor_sync(0xffffffffu, F, 4);
-        const bool in = jj < np && cc == 0 && F < 1.0;
+        for (int o = 1; o < TPE; o <<= 1) F += __shfl_xor_sync(0xffffffffu, F, o);
+        const bool own = jj < np && cc == 0;
+        const bool in = own && F < 1.0;
         double S1 = in ? zj : 0.0, kk = in ? 1.0 : 0.0;
         Rd.sum(S1, kk);
         double tau;
         if constexpr (IB == 1) {
             tau = (S1 - 1.0) / kk;
-        } else {
+        } else if constexpr (IB == 2) {
             const double m = S1 / kk;
             double ss = in ? (zj - m) * (zj - m) : 0.0, dz = 0.0;
             Rd.sum(ss, dz);
             tau = m - sqrt(fmax(0.0, 1.0 - ss) / kk);
+        } else {
+            // Newton on sum_S (z - t)^beta = 1 from the largest listed z outside S (or base):
+            // F >= 1 there, so the iteration is monotone from the left
+            double t0 = (own && !in) ? zj : base, dz = 0.0;
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) t0 = fmax(t0, __shfl_xor_sync(0xffffffffu, t0, o));
+            __shared__ double s_mx[NW];
+            if (lane == 0) s_mx[warp] = t0;
+            __syncthreads();
+            t0 = base;
+            for (int w = 0; w < NW; ++w) t0 = fmax(t0, s_mx[w]);
+            tau = t0;
+            for (int it = 0; it < 60; ++it) {
+                double Fs = 0.0, Fd = 0.0;
+                if (in) { const double d = zj - tau; Fs = powB<IB>(d, beta); Fd = powBm1<IB>(d, beta); }
+                Rd.sum(Fs, Fd);
+                if (!(Fd > 0.0)) break;
+                const double step = lbeta_step(Fs, Fd, beta, IB);
+                tau += step;
+                if (!(fabs(step) > 1e-15 * fmax(1.0, fabs(tau)))) break;
+            }
+            // final polish on the support sum itself (as the warp path)
+            double Fs = 0.0, Fd = 0.0;
+            if (in) { const double d = zj - tau; Fs = powB<IB>(d, beta); Fd = powBm1<IB>(d, beta); }
+            Rd.sum(Fs, Fd);
+            if (Fd > 0.0) tau += (Fs - 1.0) / (beta * Fd);
+            (void)dz;
         }
-        // support entries in list order (warp 0 holds entries 0..3 of each lane group: use a
-        // block scan over the entry owners)
+        // support entries in list order (block scan over the entry owners)
         int tot;
         const int pos = block_excl_scan<NT>(in ? 1 : 0, shi, &tot);
         double pd = 0.0;
-        if (in) {
+        const bool fits = tot <= kTsSup;
+        if (in && fits) {
             const double d = zj - tau;
             pd = d > 0.0 ? powB<IB>(d, beta) : 0.0;
-            sup_j[pos] = jj;                       // list index (V staged)
+            const int k = ip[jj];
+            sup_j[pos] = staged ? jj : cj[k];     // list index (V staged) or token position
+            sup_phys[pos] = cph[k];
             sup_p[pos] = (float)pd;
         }
-        if (threadIdx.x == 0) { s_tau = tau; s_kk = kk; s_nsup = tot; s_mode = 2; }
-        double psum = pd, dz = 0.0;
-        Rd.sum(psum, dz);                          // (barrier: sup_* and s_* visible)
+        if (own) cin[ip[jj]] = in ? 1 : 0;       // (large-support fallback reads the flags)
+        if (threadIdx.x == 0) { s_tau = tau; s_kk = kk; s_nsup = tot; s_mode = fits ? (staged ? 2 : 1) : 0; }
+        double psum = pd, dz2 = 0.0;
+        Rd.sum(psum, dz2);                         // (barrier: sup_*, cin and s_* visible)
         if (threadIdx.x == 0) s_psum = psum;
     } else if (warp == 0) {
         auto wsum2 = [&](double &x, double &y) {

@@ -253,6 +253,31 @@ def test_decode_topk_end_to_end(case, alpha, k):
             assert float(st.delta[b, h]) <= float(st.delta_bar[b, h]) + 1e-12
 
 
+@pytest.mark.parametrize("k", [200, 500, 700])
+@pytest.mark.parametrize("alpha", [1.5, 2.0, 1.25, 1.75])
+def test_decode_large_budgets(k, alpha):
+    """Budgets of hundreds of pages: the tau kernel splits the candidate extraction over a
+    cluster of 2/4 CTAs (k > 128 / > 384); alpha = 1.75 exercises the non-integer beta path.
+    Ragged second sequence (its list is shorter than the capacity)."""
+    B, Hq, Hkv = 2, 8, 2
+    wl, dc, hc = make_pair(B, [12000, 7001], Hq, Hkv, dtype=torch.bfloat16, seed=31, kind="planted")
+    G = Hq // Hkv
+    qh = q_host(wl)
+    sel = ekv.select_params("topk", k)
+    ws = ekv.alloc_workspace(dc, Hq, sel)
+    st = ekv.DecodeStats(B, Hq, "cuda", delta_bar=True)
+    out = ekv.decode(dc, wl.q.cuda(), sel, ekv.attn_params(alpha), ws, stats=st)
+    torch.cuda.synchronize()
+    out = out.cpu().numpy()
+    for b in range(B):
+        for h in range(Hq):
+            ref = oracle.decode_head(hc, qh[b, h], b, h // G, alpha, k_pages=k)
+            np.testing.assert_allclose(out[b, h], ref["o"], atol=2e-3, rtol=0, err_msg=f"b={b} h={h}")
+            assert int(st.n_sel[b, h]) == len(ref["pages"])
+            assert int(st.supp_count[b, h]) == ref["supp"], (b, h)
+            assert abs(float(st.tau[b, h]) - ref["tau"]) <= 1e-6 * max(1, abs(ref["tau"]))
+
+
 @pytest.mark.parametrize("case", CASES[1:4], ids=ids)
 @pytest.mark.parametrize("alpha", [1.5, 2.0, 1.25])
 def test_gaussian_select(case, alpha):
