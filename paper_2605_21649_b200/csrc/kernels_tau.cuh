@@ -207,22 +207,21 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
             int tot;
             int pos = n + block_excl_scan<NT>(__popcll(bits), shi, &tot);
             if (n + tot > kTsCap) return -1;
-            while (bits) {
-                const int bi = __ffsll(bits) - 1;
-                bits &= bits - 1;
-                const int u = bi >> 2, q = bi & 3;
-                const int e = r0 + threadIdx.x + NT * u;
-                float sv = 0.f;
+            if (bits) {
 #pragma unroll
-                for (int uu = 0; uu < kTsU; ++uu)        // register select (no local memory)
-                    if (uu == u) sv = q == 0 ? v[uu].x : q == 1 ? v[uu].y : q == 2 ? v[uu].z : v[uu].w;
-                int pgu = 0, phu = 0;
+                for (int u = 0; u < kTsU; ++u) {
+                    if (!((bits >> (4 * u)) & 15ull)) continue;
+                    const int e = r0 + threadIdx.x + NT * u;
+                    const float sv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
-                for (int uu = 0; uu < kTsU; ++uu) if (uu == u) { pgu = pg[uu]; phu = ph[uu]; }
-                zs[pos] = sv;
-                cj[pos] = pgu * kP + 4 * (e & 3) + q;
-                cph[pos] = phu;
-                ++pos;
+                    for (int q = 0; q < 4; ++q)
+                        if ((bits >> (4 * u + q)) & 1ull) {
+                            zs[pos] = sv[q];
+                            cj[pos] = pg[u] * kP + 4 * (e & 3) + q;
+                            cph[pos] = ph[u];
+                            ++pos;
+                        }
+                }
             }
             n += tot;
         }
@@ -291,7 +290,7 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
 
     // ---- 2. fp32 Newton steps (pruning point only)
     float tf = (float)tau_lo;
-    for (int it = 0; it < 6; ++it) {
+    for (int it = 0; it < 3; ++it) {      // Newton from the left: every iterate is below tau
         float F = 0.f, D = 0.f;
         for (int k = threadIdx.x; k < ncand; k += NT) {
             const float d = af * zs[k] - tf;
