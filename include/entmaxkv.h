@@ -38,7 +38,8 @@ typedef enum {
     EKV_ERR_UNSUPPORTED = 2,  /* shape outside the supported set; Gaussian with non-integer beta */
     EKV_ERR_CAPACITY = 3,     /* a caller buffer is too small */
     EKV_ERR_EMPTY = 4,        /* empty cache */
-    EKV_ERR_CUDA = 5          /* a CUDA launch failed (message has cudaGetErrorString) */
+    EKV_ERR_CUDA = 5,         /* a CUDA launch failed (message has cudaGetErrorString) */
+    EKV_ERR_COMM = 6          /* a communicator callback returned non-zero (sharded decode) */
 } ekv_status;
 
 typedef enum { EKV_BF16 = 0, EKV_F32 = 1 } ekv_dtype;
@@ -209,6 +210,58 @@ ekv_status entmaxkv_full_attend(const ekv_cache *cache, const void *q, int32_t n
 ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_heads,
                            const ekv_select_params *sel, const ekv_attn_params *attn,
                            float *out, ekv_decode_stats *stats, void *workspace, void *stream);
+
+/*
+ * Sequence sharding (north star: "sequence sharding of the page cache across
+ * 2/4/8 GPUs over NVLink with NCCL allreduce of per-head partial sum (z - tau)_+^beta during
+ * tau bisection and of partial numerator/denominator outputs").
+ *
+ * Striping: rank r of `world` holds the global pages p = r + i * world as its local pages
+ * i = 0, 1, ... (its own ekv_cache: local page table, local seq_lens = the number of tokens
+ * in those pages; only the global last page can be partial and it is the owner's last local
+ * page).  Every rank calls entmaxkv_decode_sharded with the same q and parameters; each gets
+ * the full output (replicated).
+ *
+ * The library never talks to a network itself: collectives go through the caller's
+ * callbacks (e.g. NCCL via torch.distributed), enqueued on `stream`, in the same order on
+ * every rank.  Both callbacks return 0 on success.  Buffers passed to them lie inside the
+ * caller's workspace.
+ *   allreduce(buf, count, dtype, op): in place; dtype 0 = f32, 1 = f64; op 0 = sum, 1 = max.
+ *   allgather(send, recv, bytes): rank r's `bytes` bytes from send land at recv + r * bytes.
+ */
+typedef struct {
+    int32_t rank, world;
+    int32_t (*allreduce)(void *buf, size_t count, int32_t dtype, int32_t op, void *user, void *stream);
+    int32_t (*allgather)(const void *send, void *recv, size_t bytes, void *user, void *stream);
+    void *user;
+} ekv_comm;
+
+/* Workspace bytes for entmaxkv_decode_sharded on this local cache shape. */
+size_t entmaxkv_shard_workspace_size(const ekv_cache *local, int32_t n_q_heads, const ekv_select_params *sel,
+                                     int32_t world);
+
+/*
+ * One sequence-sharded decode step (top-k selection, exact entmax):
+ *   1. local box scores + local top-k; (score, global page) lists all-gathered; the global
+ *      top-k (R3 tie-break on the global page index, i.e. identical to the 1-GPU selection)
+ *      is merged on every rank, which keeps its own pages;
+ *   2. K scores of the local share; all-reduce(max) of the row maxima;
+ *   3. local candidates z > z_max - 1;
+ *   4. multisection rounds on F(x) = sum (z - x)_+^beta: per round an all-reduce(sum) of
+ *      F, #{z > x}, #{z >= x} at 32 probes per row, until no z lies strictly inside the
+ *      bracket (the support is then exact, R9); one device->host read per round;
+ *   5. all-reduce(sum) of the support's power sums -> tau (closed form / polynomial Newton);
+ *   6. all-reduce(sum) of the numerator sum p_j v_j and denominator sum p_j -> out.
+ * global_seq_lens: device [batch] int32, the unsharded sequence lengths.
+ * Supported: policy TOPK, transform ENTMAX, integer beta = 1/(alpha-1) in {1,2,3,4}, world * k
+ * <= 16384, <= 8192 candidates per row and rank (else the row's tau/out are NaN).
+ * stats may be NULL; fills tau, supp_count (global |S~|) and n_sel (global |C_page|).
+ * Not graph-capturable (one small synchronous read per multisection round).
+ */
+ekv_status entmaxkv_decode_sharded(const ekv_cache *local, const int32_t *global_seq_lens, const void *q,
+                                   int32_t n_q_heads, const ekv_select_params *sel, const ekv_attn_params *attn,
+                                   const ekv_comm *comm, float *out, ekv_decode_stats *stats, void *workspace,
+                                   void *stream);
 
 /* Number of kernels the last successful entmaxkv_decode / full_attend call on this
  * thread enqueued (for launch accounting). */

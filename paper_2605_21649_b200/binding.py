@@ -16,7 +16,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libentmaxkv.so")
 
-EKV_OK, EKV_ERR_INVALID_ARG, EKV_ERR_UNSUPPORTED, EKV_ERR_CAPACITY, EKV_ERR_EMPTY, EKV_ERR_CUDA = range(6)
+EKV_OK, EKV_ERR_INVALID_ARG, EKV_ERR_UNSUPPORTED, EKV_ERR_CAPACITY, EKV_ERR_EMPTY, EKV_ERR_CUDA, EKV_ERR_COMM = range(7)
 EKV_BF16, EKV_F32 = 0, 1
 EKV_ENTMAX, EKV_SOFTMAX = 0, 1
 EKV_TOPK, EKV_GAUSS, EKV_ALL = 0, 1, 2
@@ -26,6 +26,7 @@ EXPORTED = [
     "entmaxkv_last_error", "entmaxkv_version", "entmaxkv_workspace_size", "entmaxkv_select_capacity",
     "entmaxkv_append_kv", "entmaxkv_rebuild_page_stats", "entmaxkv_score_pages", "entmaxkv_select",
     "entmaxkv_sparse_attend", "entmaxkv_full_attend", "entmaxkv_decode", "entmaxkv_last_launch_count",
+    "entmaxkv_shard_workspace_size", "entmaxkv_decode_sharded",
 ]
 
 
@@ -61,6 +62,17 @@ class ekv_decode_stats(ctypes.Structure):
                 ("tau_full", ctypes.c_void_p)]
 
 
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32, ctypes.c_int32,
+                                ctypes.c_void_p, ctypes.c_void_p)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                                ctypes.c_void_p)
+
+
+class ekv_comm(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("allreduce", ALLREDUCE_FN),
+                ("allgather", ALLGATHER_FN), ("user", ctypes.c_void_p)]
+
+
 _lib = None
 
 
@@ -88,7 +100,11 @@ def lib():
         L.entmaxkv_decode.argtypes = [P(ekv_cache), vp, i32, P(ekv_select_params), P(ekv_attn_params), vp,
                                       P(ekv_decode_stats), vp, vp]
         L.entmaxkv_last_launch_count.restype = i32
-        for name in ("entmaxkv_append_kv", "entmaxkv_rebuild_page_stats", "entmaxkv_score_pages", "entmaxkv_select",
+        L.entmaxkv_shard_workspace_size.argtypes = [P(ekv_cache), i32, P(ekv_select_params), i32]
+        L.entmaxkv_shard_workspace_size.restype = ctypes.c_size_t
+        L.entmaxkv_decode_sharded.argtypes = [P(ekv_cache), vp, vp, i32, P(ekv_select_params), P(ekv_attn_params),
+                                              P(ekv_comm), vp, P(ekv_decode_stats), vp, vp]
+        for name in ("entmaxkv_decode_sharded", "entmaxkv_append_kv", "entmaxkv_rebuild_page_stats", "entmaxkv_score_pages", "entmaxkv_select",
                      "entmaxkv_sparse_attend", "entmaxkv_full_attend", "entmaxkv_decode"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
@@ -317,3 +333,37 @@ def select_into(cache: PagedCache, n_q_heads, sel: ekv_select_params, alpha, box
     _check(lib().entmaxkv_select(ctypes.byref(cs), int(n_q_heads), _ptr(box), _ptr(mu), _ptr(sigma2),
                                  ctypes.byref(sel), float(alpha), _ptr(page_idx), _ptr(n_sel), int(page_idx.shape[2]),
                                  _ptr(tau_hat), None, _stream(stream)))
+
+
+# ----------------------------------------------------------------------------- sequence sharding
+def shard_workspace(cache: PagedCache, n_q_heads, sel: ekv_select_params, world: int):
+    n = lib().entmaxkv_shard_workspace_size(ctypes.byref(cache.c_struct()), int(n_q_heads), ctypes.byref(sel),
+                                            int(world))
+    if n == 0:
+        raise EkvError(EKV_ERR_INVALID_ARG, lib().entmaxkv_last_error().decode())
+    return torch.empty(int(n), dtype=torch.uint8, device=cache.K.device)
+
+
+def decode_sharded(cache: PagedCache, global_seq_lens, q, sel: ekv_select_params, attn: ekv_attn_params, comm,
+                   workspace, out=None, stats: DecodeStats | None = None, stream=None):
+    """One sequence-sharded decode step on this rank's local cache (include/entmaxkv.h).
+    `comm` provides rank, world and the collectives (see paper_2605_21649_b200.sharding); the
+    library calls them back between its kernels.  Returns out [B][Hq][dv] fp32 (replicated)."""
+    B, Hq, _ = q.shape
+    if out is None:
+        out = torch.empty(B, Hq, cache.V.shape[3], dtype=torch.float32, device=q.device)
+    s = stream if stream is not None else torch.cuda.current_stream(q.device)
+    comm.bind(workspace, s)
+    cm = ekv_comm(int(comm.rank), int(comm.world), comm.c_allreduce, comm.c_allgather, None)
+    cs = cache.c_struct()
+    st = stats.c_struct() if stats is not None else None
+    try:
+        _check(lib().entmaxkv_decode_sharded(ctypes.byref(cs), _ptr(global_seq_lens), _ptr(q), Hq, ctypes.byref(sel),
+                                             ctypes.byref(attn), ctypes.byref(cm), _ptr(out),
+                                             None if st is None else ctypes.byref(st), _ptr(workspace),
+                                             ctypes.c_void_p(s.cuda_stream)))
+    finally:
+        comm.unbind()
+    if comm.error is not None:
+        raise comm.error
+    return out
