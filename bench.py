@@ -158,6 +158,51 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- sequence sharding (N > 1)
+def run_seq_sharded(args, rank, world, dev, k_pages):
+    """configs[3]'s multi-GPU form: ONE 1M-token sequence whose pages are striped over the N
+    ranks (page p on rank p mod N); every step = local scoring + top-k, all-gather merge,
+    K scores, z_max all-reduce, multisection tau rounds (all-reduce of the partial
+    sum (z - x)_+^beta), power-sum tau, numerator/denominator all-reduce (NCCL through
+    torch.distributed).  Timed with CUDA events per rank, max over ranks (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_21649_b200 import binding as ekv
+    from paper_2605_21649_b200 import sharding
+    from paper_2605_21649_b200.workload import make_workload
+    Hq, Hkv = 32, 8
+    wl = make_workload(1, args.n, Hq, Hkv, seed=1000, device=dev)     # same sequence on every rank
+    cache = sharding.shard_cache(wl.K, wl.V, wl.page_table, wl.seq_lens, rank, world)
+    gl = wl.seq_lens.to(torch.int32).to(dev)
+    q = wl.q.to(dev)
+    del wl
+    torch.cuda.empty_cache()
+    sel = ekv.select_params("topk", k_pages)
+    attn = ekv.attn_params(args.alpha)
+    ws = ekv.shard_workspace(cache, Hq, sel, world)
+    st = ekv.DecodeStats(1, Hq, dev, delta_bar=False)
+    out = torch.empty(1, Hq, 128, dtype=torch.float32, device=dev)
+    comm = sharding.TorchComm()
+    s = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(s):
+        for _ in range(max(3, args.warmup)):
+            ekv.decode_sharded(cache, gl, q, sel, attn, comm, ws, out=out, stats=st, stream=s)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        e0.record(s)
+        for _ in range(args.steps):
+            ekv.decode_sharded(cache, gl, q, sel, attn, comm, ws, out=out, stats=st, stream=s)
+        e1.record(s)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) * 1e3 / args.steps], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ok = bool(torch.isfinite(out).all().item())
+    return {"us_per_step": float(t.item()), "local_pages": int(cache.page_table.shape[1]),
+            "outputs_finite": ok, "supp_mean": float(st.supp_count.float().mean().item())}
+
+
 # ----------------------------------------------------------------------------- our arm
 def main():
     args = parse()
@@ -166,8 +211,11 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     import torch
     import torch.distributed as dist
+    same = os.environ.get("EKV_SAME_DEVICE") == "1"     # test knob: N ranks on cuda:0 over gloo
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group("gloo" if same else "nccl", init_method="env://")
+    if same:
+        local = 0
     torch.cuda.set_device(local)
     if args.impl == "reference":
         run_reference(args, rank, world)
@@ -329,6 +377,12 @@ def main():
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "us", "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
 
+    seq = None
+    if world > 1:
+        try:
+            seq = run_seq_sharded(args, rank, world, dev, k_pages)
+        except Exception as e:  # reported, the batch-sharded line stands
+            seq = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": us_step, "unit": "us", "n_gpus": world, "steps": args.steps,
@@ -353,6 +407,21 @@ def main():
             "clocks": clk.summary(),
             "support_per_head_mean": supp / Hq, "union_pages": union,
         }
+        if seq is not None:
+            line["batch_sharded"] = {"us_per_step": us_step, "scaling": "weak",
+                                     "parallelism": f"batch-sharded x{world} (one 1M sequence per GPU)"}
+            line["seq_sharded"] = seq
+            if "us_per_step" in seq:
+                # headline at N > 1: the one 1M sequence sequence-sharded over the N GPUs (configs[3])
+                line["value"] = seq["us_per_step"]
+                line["ms_per_step"] = seq["us_per_step"] / 1e3
+                line["scaling"] = "strong"
+                line["config"]["workload"] = (f"C4: ONE {args.n}-token sequence, pages striped over {world} GPUs, "
+                                              f"32q/8kv, d=128, P=16, bf16, alpha={args.alpha}, top-k "
+                                              f"{args.budget:.0%} (k={k_pages}); step = local score + top-k, "
+                                              f"all-gather merge, K scores, NCCL multisection tau, num/den "
+                                              f"all-reduce")
+                line["config"]["parallelism"] = f"sequence-sharded x{world} (NCCL via torch.distributed)"
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

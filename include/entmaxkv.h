@@ -248,8 +248,9 @@ size_t entmaxkv_shard_workspace_size(const ekv_cache *local, int32_t n_q_heads, 
  *   2. K scores of the local share; all-reduce(max) of the row maxima;
  *   3. local candidates z > z_max - 1;
  *   4. multisection rounds on F(x) = sum (z - x)_+^beta: per round an all-reduce(sum) of
- *      F, #{z > x}, #{z >= x} at 32 probes per row, until no z lies strictly inside the
- *      bracket (the support is then exact, R9); one device->host read per round;
+ *      F, #{z > x}, #{z >= x} at 64 probes per row, until no z lies strictly inside the
+ *      bracket (the support is then exact, R9); one device->host read per round from the
+ *      second round on;
  *   5. all-reduce(sum) of the support's power sums -> tau (closed form / polynomial Newton);
  *   6. all-reduce(sum) of the numerator sum p_j v_j and denominator sum p_j -> out.
  * global_seq_lens: device [batch] int32, the unsharded sequence lengths.

@@ -809,6 +809,7 @@ ekv_status entmaxkv_decode_sharded(const ekv_cache *cache, const int32_t *global
     for (int round = 0; round < 13; ++round) {
         EKV_TRY(comm_allreduce(comm, part, (size_t)rows * kShP * 3, 1, 0, st));
         EKV_TRY(probe(part));
+        if (round < 1) continue;              // two rounds (12 bits) before the first check
         k_shard_open<<<1, 256, 0, st>>>(rst, rows, openp);
         EKV_TRY(check_launch("k_shard_open"));
         int open = 0;

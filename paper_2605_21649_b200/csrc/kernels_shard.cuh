@@ -29,7 +29,7 @@
 
 namespace ekv {
 
-constexpr int kShT = 30;                 // interior probes per multisection round
+constexpr int kShT = 62;                 // interior probes per multisection round (6 bits)
 constexpr int kShP = kShT + 2;           // probe points incl. the bracket ends
 constexpr int kShCap = 8192;             // local candidates per row
 constexpr int kShSums = 5;               // S_0 .. S_4
@@ -243,11 +243,13 @@ __global__ void __launch_bounds__(256) k_shard_probe(const double *__restrict__ 
     __syncthreads();
     const int n = min(ncand[row], kShCap);
     const bool live = !s.done;
-    // thread-private partials per probe, then a fixed-order block sum (deterministic)
-    for (int t = 0; t < kShP && live; ++t) {
+    // warp w evaluates probes w, w + 8, ...: lanes stride over the candidates, fixed-order
+    // xor-shuffle sums (deterministic); no block barrier per probe
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int t = warp; t < kShP && live; t += 8) {
         const double x = probe_x(s.lo, s.hi, t);
         double f = 0.0, cg = 0.0, ce = 0.0;
-        for (int i = threadIdx.x; i < n; i += 256) {
+        for (int i = lane; i < n; i += 32) {
             const double z = cz[(size_t)row * kShCap + i];
             const double d = z - x;
             if (d > 0.0) { f += sh_pow<IB>(d, beta); cg += 1.0; }
@@ -259,16 +261,9 @@ __global__ void __launch_bounds__(256) k_shard_probe(const double *__restrict__ 
             cg += __shfl_xor_sync(0xffffffffu, cg, o);
             ce += __shfl_xor_sync(0xffffffffu, ce, o);
         }
-        __shared__ double wp[8][3];
-        if ((threadIdx.x & 31) == 0) { wp[threadIdx.x >> 5][0] = f; wp[threadIdx.x >> 5][1] = cg; wp[threadIdx.x >> 5][2] = ce; }
-        __syncthreads();
-        if (threadIdx.x < 3) {
-            double v = 0.0;
-            for (int w = 0; w < 8; ++w) v += wp[w][threadIdx.x];
-            acc[t][threadIdx.x] = v;
-        }
-        __syncthreads();
+        if (lane == 0) { acc[t][0] = f; acc[t][1] = cg; acc[t][2] = ce; }
     }
+    __syncthreads();
     for (int i = threadIdx.x; i < kShP * 3; i += 256) part[(size_t)row * kShP * 3 + i] = (&acc[0][0])[i];
 }
 

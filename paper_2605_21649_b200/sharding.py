@@ -112,12 +112,31 @@ class TorchComm(_CommBase):
         self.dist, self.group = dist, group
         super().__init__(dist.get_rank(group), dist.get_world_size(group))
 
+    def _host_staged(self):
+        # gloo (tests: several ranks sharing one GPU) has no device all-gather: stage on the host
+        return self.dist.get_backend(self.group) == "gloo"
+
     def all_reduce(self, t, op):
         d = self.dist
+        rop = d.ReduceOp.MAX if op == 1 else d.ReduceOp.SUM
+        if self._host_staged():
+            self.stream.synchronize()
+            h = t.cpu()
+            d.all_reduce(h, op=rop, group=self.group)
+            t.copy_(h)
+            torch.cuda.synchronize()
+            return
         with torch.cuda.stream(self.stream):
-            d.all_reduce(t, op=d.ReduceOp.MAX if op == 1 else d.ReduceOp.SUM, group=self.group)
+            d.all_reduce(t, op=rop, group=self.group)
 
     def all_gather(self, send, recv):
+        if self._host_staged():
+            self.stream.synchronize()
+            parts = [torch.empty_like(send, device="cpu") for _ in range(self.world)]
+            self.dist.all_gather(parts, send.cpu(), group=self.group)
+            recv.copy_(torch.cat(parts))
+            torch.cuda.synchronize()
+            return
         with torch.cuda.stream(self.stream):
             self.dist.all_gather_into_tensor(recv, send, group=self.group)
 

@@ -84,3 +84,24 @@ def test_sharded_rejects_non_integer_beta():
         ekv.decode_sharded(c, wl.seq_lens.to(torch.int32).cuda(), wl.q.cuda(), sel, ekv.attn_params(1.7),
                            sharding.LoopbackGroup(1).comm(0), ws)
     assert ei.value.status == ekv.EKV_ERR_UNSUPPORTED
+
+
+def test_torchcomm_two_processes_share_one_gpu():
+    """The multi-process path (torchrun, TorchComm callbacks, one process per rank) on the
+    one available GPU: gloo with host-staged collectives, compared with the 1-GPU decode."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ, EKV_SAME_DEVICE="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(root, "tools", "shard_check.py"), "40000", "100", "1.5"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "-> OK" in r.stdout

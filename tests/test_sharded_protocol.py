@@ -19,7 +19,7 @@ import oracle
 from paper_2605_21649_b200.sharding import local_pages
 from paper_2605_21649_b200.workload import make_workload
 
-T_PROBES = 30            # interior probes per round (kernels_shard.cuh kShT)
+T_PROBES = 62            # interior probes per round (kernels_shard.cuh kShT)
 NP = T_PROBES + 2
 
 
