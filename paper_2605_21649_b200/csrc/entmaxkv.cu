@@ -99,7 +99,8 @@ struct Layout {
     size_t box, mu, sigma2, page_idx, n_sel, tau_hat;
     size_t zero, rowmax, ccount, tickets, ucount, umask, zero_bytes;   // zeroed per attention pass
     size_t ulist;
-    size_t db_partial, tau_int;
+    size_t db_partial, tau_int, smx_acc, smx_l, smx_cnt;
+    int smx_nch;
     size_t scores, cand_s, cand_j, tok_list, p_list, n_list, full_out, total;
     int cap, W, list_cap;
 };
@@ -135,6 +136,10 @@ Layout layout(const ekv_cache *c, int Hq, const ekv_select_params *sel) {
     L.full_out = take(B * Hq * kD * 4);
     L.db_partial = take(B * Hq * (size_t)((maxp + kDbChunk - 1) / kDbChunk) * 8);
     L.tau_int = take(B * Hq * 8);
+    L.smx_nch = (int)((maxp + kSmxPages - 1) / kSmxPages);
+    L.smx_acc = take(B * Hq * (size_t)L.smx_nch * kD * 4);
+    L.smx_l = take(B * Hq * (size_t)L.smx_nch * 8);
+    L.smx_cnt = take(B * Hq * (size_t)L.smx_nch * 4);
     L.total = o;
     return L;
 }
@@ -378,6 +383,23 @@ ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t 
     A.nch = nch; A.page_idx = pi; A.n_sel = ns; A.sel_stride = stride; A.full = full;
     A.Hq = Hq; A.G = Hq / c->n_kv_heads; A.alpha = attn->alpha; A.transform = attn->transform;
     A.out = out; A.tau_out = tau; A.supp_out = supp;
+    if (attn->transform == EKV_SOFTMAX) {
+        // a6: split dense-V softmax (flash-decoding chunks) + ordered combine
+        const int nch = full ? (c->max_pages_per_seq + kSmxPages - 1) / kSmxPages : (stride + kSmxPages - 1) / kSmxPages;
+        dim3 g(nch, rows);
+        float *pacc = at<float>(ws, L.smx_acc);
+        double *pl = at<double>(ws, L.smx_l);
+        int32_t *pc = at<int32_t>(ws, L.smx_cnt);
+        if (c->dtype == EKV_BF16)
+            k_softmax_partial<__nv_bfloat16><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, pi, ns, stride, full, Hq,
+                                                                 Hq / c->n_kv_heads, nch, pacc, pl, pc);
+        else
+            k_softmax_partial<float><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, pi, ns, stride, full, Hq,
+                                                        Hq / c->n_kv_heads, nch, pacc, pl, pc);
+        EKV_TRY(check_launch("k_softmax_partial"));
+        k_softmax_combine<<<rows, 128, 0, st>>>(pacc, pl, pc, rowmax, nch, out, tau, supp);
+        return check_launch("k_softmax_combine");
+    }
     if (!full && attn->transform == EKV_ENTMAX && !A.tok_list) {
         if (c->dtype == EKV_BF16) return launch_tau_sparse<__nv_bfloat16>(v, A, rows, st);
         return launch_tau_sparse<float>(v, A, rows, st);

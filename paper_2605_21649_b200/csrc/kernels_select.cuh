@@ -306,16 +306,46 @@ __device__ __forceinline__ GaussMoments trunc_moments(int beta, double muY, doub
     return {cur, prev};
 }
 
-template <int NT>
-__device__ void gauss_mass(const float *mu, const float *s2, int M, int Lseq, double a, int beta,
-                           double tau, double &mass, double &dmass, double *shd) {
+// mass(tau) = sum_p c_p M_beta(a mu_p - tau, a sigma_p) and -d mass / d tau, in fp64 (FP64 = 1)
+// or fp32 (steering only).  Pages whose standardised t = (a mu - tau) / (a sigma) < -9 are
+// skipped: their terms are below Phi(-9) ~ 1e-19 relative (the fp64 sum's own rounding is
+// ~1e-16), decided by a conservative fp32 pre-test.
+template <int NT, bool FP64>
+__device__ void gauss_mass2(const float *mu, const float *s2, int M, int Lseq, float af, int beta, double tau,
+                            double &mass, double &dmass, double *shd) {
     double m = 0.0, dm = 0.0;
+    const float tf = (float)tau;
     for (int p = threadIdx.x; p < M; p += NT) {
+        const float mp = __ldg(mu + p), sp = sqrtf(__ldg(s2 + p));
+        const float num = af * mp - tf, den = af * sp;
+        if (den > 0.f ? (num < -9.5f * den) : (num <= 0.f)) continue;
         const double cnt = (double)min(kP, Lseq - p * kP);
-        const double sg = sqrt((double)s2[p]);
-        GaussMoments g = trunc_moments(beta, a * (double)mu[p] - tau, a * sg);
-        m += cnt * g.m;
-        dm += cnt * (double)beta * g.dm;      // -d mass / d tau
+        if constexpr (FP64) {
+            const double a = (double)af;
+            const double sg = sqrt((double)s2[p]);
+            GaussMoments g = trunc_moments(beta, a * (double)mp - tau, a * sg);
+            m += cnt * g.m;
+            dm += cnt * (double)beta * g.dm;
+        } else {
+            float r, rm;
+            if (!(den > 0.f)) {
+                const float x = num > 0.f ? num : 0.f;
+                r = 1.f; rm = 1.f;
+                for (int i = 0; i < beta; ++i) { rm = r; r *= x; }
+            } else {
+                const float t = num / den;
+                const float Ph = normcdff(t), ph = __expf(-0.5f * t * t) * 0.39894228f;
+                float m0 = Ph, m1 = num * Ph + den * ph;
+                if (beta == 1) { r = m1; rm = m0; }
+                else {
+                    float pr = m0, cu = m1;
+                    for (int k = 2; k <= beta; ++k) { const float nx = num * cu + (float)(k - 1) * den * den * pr; pr = cu; cu = nx; }
+                    r = cu; rm = pr;
+                }
+            }
+            m += cnt * (double)r;
+            dm += cnt * (double)beta * (double)rm;
+        }
     }
     block_sum2_d<NT>(m, dm, shd);
     mass = m; dmass = dm;
@@ -342,28 +372,53 @@ __global__ void __launch_bounds__(NT) k_gauss_select(const float *__restrict__ m
     const float *m_ = mu + (size_t)row * maxp;
     const float *s_ = sigma2 + (size_t)row * maxp;
     const double a = (double)alpha - 1.0;
+    const float af = (float)a;
     const int beta = (int)llrint(1.0 / a);
-    // bracket: top = a * max_p (mu + 8 sigma)
+    // (1) fp32 steering: bracket from a max_p (mu + 8 sigma), then safeguarded Newton
     float tmax = -INFINITY;
     for (int p = threadIdx.x; p < M; p += NT) tmax = fmaxf(tmax, m_[p] + 8.0f * sqrtf(s_[p]));
     tmax = block_max_f<NT>(tmax, shf);
     double hi = a * (double)tmax, w = 1.0, mass, dmass;
     for (int it = 0; it < 200; ++it) {
-        gauss_mass<NT>(m_, s_, M, Lseq, a, beta, hi, mass, dmass, shd);
+        gauss_mass2<NT, false>(m_, s_, M, Lseq, af, beta, hi, mass, dmass, shd);
         if (mass < 1.0) break;
         hi += w; w *= 2.0;
     }
     double lo = hi - 1.0;
     w = 1.0;
     for (int it = 0; it < 200; ++it) {
-        gauss_mass<NT>(m_, s_, M, Lseq, a, beta, lo, mass, dmass, shd);
+        gauss_mass2<NT, false>(m_, s_, M, Lseq, af, beta, lo, mass, dmass, shd);
         if (mass >= 1.0) break;
         lo -= w; w *= 2.0;
     }
-    // safeguarded Newton from lo (mass convex decreasing -> monotone from the left)
     double tau = lo;
+    for (int it = 0; it < 60; ++it) {
+        gauss_mass2<NT, false>(m_, s_, M, Lseq, af, beta, tau, mass, dmass, shd);
+        if (mass >= 1.0) lo = tau; else hi = tau;
+        double nt = (dmass > 0.0) ? tau + (mass - 1.0) / dmass : 0.5 * (lo + hi);
+        if (!(nt > lo && nt < hi)) nt = 0.5 * (lo + hi);
+        const bool stop = fabs(nt - tau) <= 1e-6 * fmax(1.0, fabs(tau)) || hi - lo <= 1e-6 * fmax(1.0, fabs(hi));
+        tau = nt;
+        if (stop) break;
+    }
+    // (2) fp64: a verified bracket around the fp32 root, then safeguarded Newton to fp64
+    double dl = 1e-4 * fmax(1.0, fabs(tau));
+    lo = tau - dl;
     for (int it = 0; it < 200; ++it) {
-        gauss_mass<NT>(m_, s_, M, Lseq, a, beta, tau, mass, dmass, shd);
+        gauss_mass2<NT, true>(m_, s_, M, Lseq, af, beta, lo, mass, dmass, shd);
+        if (mass >= 1.0) break;
+        dl *= 4.0; lo = tau - dl;
+    }
+    double dh = 1e-4 * fmax(1.0, fabs(tau));
+    hi = tau + dh;
+    for (int it = 0; it < 200; ++it) {
+        gauss_mass2<NT, true>(m_, s_, M, Lseq, af, beta, hi, mass, dmass, shd);
+        if (mass < 1.0) break;
+        dh *= 4.0; hi = tau + dh;
+    }
+    tau = fmin(fmax(tau, lo), hi);
+    for (int it = 0; it < 100; ++it) {
+        gauss_mass2<NT, true>(m_, s_, M, Lseq, af, beta, tau, mass, dmass, shd);
         if (mass >= 1.0) lo = tau; else hi = tau;
         double nt = (dmass > 0.0) ? tau + (mass - 1.0) / dmass : 0.5 * (lo + hi);
         if (!(nt > lo && nt < hi)) nt = 0.5 * (lo + hi);

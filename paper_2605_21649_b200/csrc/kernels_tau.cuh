@@ -659,3 +659,96 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
 }
 
 }  // namespace ekv
+
+namespace ekv {
+// ============================================================================ a6: softmax rows
+// Softmax over C_tok (the Quest-style baseline on the same kernels): dense
+// V over every valid token of the page list, split flash-decoding style.  The row maximum is
+// already known (the K-score pass's rowmax), so the chunk partials need no rescaling:
+// p_j = exp(s_j - s_max); chunk c of kSmxPages list pages -> acc[c][dv] = sum p_j v_j (fp32),
+// l[c] = sum p_j (fp64); k_softmax_combine adds the chunks in order (deterministic).
+constexpr int kSmxPages = 32;            // list pages per CTA (512 tokens)
+template <typename T>
+__global__ void __launch_bounds__(256) k_softmax_partial(CacheView c, const float *__restrict__ scores, size_t ntok,
+                                                         const uint32_t *__restrict__ rowmax,
+                                                         const int32_t *__restrict__ page_idx,
+                                                         const int32_t *__restrict__ n_sel, int stride, int full,
+                                                         int Hq, int G, int nch, float *__restrict__ pacc,
+                                                         double *__restrict__ pl, int32_t *__restrict__ pcnt) {
+    __shared__ float red[8][kD];
+    __shared__ double wl[8];
+    __shared__ int wc[8];
+    const int row = blockIdx.y, ch = blockIdx.x;
+    const int b = row / Hq, kvh = (row % Hq) / G;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int L = __ldg(c.seq_lens + b);
+    const int nlist = full ? n_pages_of(L) : __ldg(n_sel + row);
+    const uint32_t mk = __ldg(rowmax + row);
+    const float smax = mk ? key2f(mk) : 0.f;
+    const float *srow = scores + (size_t)row * ntok;
+    const T *Vb = reinterpret_cast<const T *>(c.V);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    double l = 0.0;
+    int cnt = 0;
+    const int i0 = ch * kSmxPages;
+    if (mk && i0 < nlist) {
+        // warp w: list pages i0 + w, i0 + w + 8, ...; the 16 tokens of a page, 4 V rows in flight
+        for (int ii = i0 + warp; ii < min(nlist, i0 + kSmxPages); ii += 8) {
+            const int pg = full ? ii : __ldg(page_idx + (size_t)row * stride + ii);
+            const int phys = __ldg(c.page_table + (size_t)b * c.maxp + pg);
+            const float sv = (lane < kP) ? srow[(size_t)pg * kP + lane] : -INFINITY;
+            const T *vp = Vb + ((size_t)phys * c.Hkv + kvh) * kP * kD + 4 * lane;
+#pragma unroll 4
+            for (int t = 0; t < kP; ++t) {
+                const float s = __shfl_sync(0xffffffffu, sv, t);
+                if (pg * kP + t >= L || s == -INFINITY) continue;        // warp-uniform
+                const float p = expf(s - smax);
+                float vx[4];
+                ldv4<T>(vp + (size_t)t * kD, vx);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] = __fmaf_rn(p, vx[q], acc[q]);
+                if (lane == 0) { l += (double)p; ++cnt; }
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) red[warp][4 * lane + q] = acc[q];
+    if (lane == 0) { wl[warp] = l; wc[warp] = cnt; }
+    __syncthreads();
+    const size_t o = (size_t)row * nch + ch;
+    if (threadIdx.x < kD) {
+        float s = 0.f;
+        for (int w = 0; w < 8; ++w) s = __fadd_rn(s, red[w][threadIdx.x]);
+        pacc[o * kD + threadIdx.x] = s;
+    }
+    if (threadIdx.x == 0) {
+        double sl = 0.0;
+        int sc = 0;
+        for (int w = 0; w < 8; ++w) { sl += wl[w]; sc += wc[w]; }
+        pl[o] = sl;
+        pcnt[o] = sc;
+    }
+}
+
+__global__ void __launch_bounds__(128) k_softmax_combine(const float *__restrict__ pacc, const double *__restrict__ pl,
+                                                         const int32_t *__restrict__ pcnt, const uint32_t *__restrict__ rowmax,
+                                                         int nch, float *__restrict__ out, double *__restrict__ tau,
+                                                         int32_t *__restrict__ supp) {
+    const int row = blockIdx.x;
+    const uint32_t mk = rowmax[row];
+    float o = 0.f;
+    double l = 0.0;
+    int cnt = 0;
+    for (int ch = 0; ch < nch; ++ch) {
+        const size_t i = (size_t)row * nch + ch;
+        o = __fadd_rn(o, pacc[i * kD + threadIdx.x]);
+        l += pl[i];
+        cnt += pcnt[i];
+    }
+    out[(size_t)row * kD + threadIdx.x] = (mk && l > 0.0) ? (float)((double)o / l) : 0.0f;
+    if (threadIdx.x == 0) {
+        if (tau) tau[row] = mk ? (double)key2f(mk) + log(l) : NAN;
+        if (supp) supp[row] = cnt;
+    }
+}
+}  // namespace ekv
