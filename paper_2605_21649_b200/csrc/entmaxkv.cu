@@ -589,7 +589,7 @@ ekv_status entmaxkv_select(const ekv_cache *cache, int32_t n_q_heads, const floa
                            sel_stride, n_q_heads / cache->n_kv_heads, UnionOut{nullptr, 0}, st);
     }
     if (!mu || !sigma2) return fail(EKV_ERR_INVALID_ARG, "Gaussian selector needs mu/sigma2");
-    k_gauss_select<256><<<cache->batch * n_q_heads, 256, 0, st>>>(mu, sigma2, n_q_heads, maxp, cache->seq_lens, alpha,
+    k_gauss_select<1024><<<cache->batch * n_q_heads, 1024, 0, st>>>(mu, sigma2, n_q_heads, maxp, cache->seq_lens, alpha,
                                                                   sel->margin, sel->q_page, page_idx, n_sel, sel_stride,
                                                                   tau_hat);
     return check_launch("k_gauss_select");
@@ -664,7 +664,7 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
         const int k = sel->policy == EKV_TOPK ? sel->k_pages : maxp;
         EKV_TRY(launch_topk(box, cache->batch, n_q_heads, maxp, cache->seq_lens, k, pi, ns, L.cap, Gq, uo, st));
     } else {
-        k_gauss_select<256><<<cache->batch * n_q_heads, 256, 0, st>>>(mu, s2, n_q_heads, maxp, cache->seq_lens,
+        k_gauss_select<1024><<<cache->batch * n_q_heads, 1024, 0, st>>>(mu, s2, n_q_heads, maxp, cache->seq_lens,
                                                                       attn->alpha, sel->margin, sel->q_page, pi, ns,
                                                                       L.cap, th);
         EKV_TRY(check_launch("k_gauss_select"));

@@ -68,7 +68,30 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     stamp_cta<1>(threadIdx.x == 0, 0);
     const int ucap = full ? c.maxp : stride;
-    const long long tot = full ? (long long)c.B * c.Hkv * c.maxp : (long long)c.B * Hq * stride;
+    // sparse rows: the work space is the concatenation of the rows' actual lists (prefix sums
+    // of n_sel, computed by every producer), so CTAs get equal numbers of pages whatever the
+    // list lengths (Gaussian selection: variable, often far below the capacity)
+    constexpr int kMaxRowsBal = 1024;
+    __shared__ int pref[kMaxRowsBal + 1];
+    const int nrows = c.B * Hq;
+    const bool bal = !full && nrows <= kMaxRowsBal;
+    long long tot = full ? (long long)c.B * c.Hkv * c.maxp : (long long)c.B * Hq * stride;
+    if (bal && warp == NCW) {
+        const int per = (nrows + 31) / 32;
+        int run = 0;
+        for (int i = 0; i < per; ++i) { const int r = lane * per + i; run += r < nrows ? __ldg(n_sel + r) : 0; }
+        int incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += y; }
+        int acc = incl - run;
+        for (int i = 0; i < per; ++i) {
+            const int r = lane * per + i;
+            if (r < nrows) { pref[r] = acc; acc += __ldg(n_sel + r); }
+        }
+        if (lane == 31) pref[nrows] = incl;
+        __syncwarp();
+        tot = pref[nrows];
+    }
     const long long f0 = tot * blockIdx.x / gridDim.x, f1 = tot * (blockIdx.x + 1) / gridDim.x;
     if (threadIdx.x == 0) {
         for (int i = 0; i < NS; ++i) { mbar_init(&fullb[i], 1); mbar_init(&emptyb[i], NCW); }
@@ -80,13 +103,23 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
         const unsigned char *Kb = reinterpret_cast<const unsigned char *>(c.K);
         int si = 0, fill = 0;
         int cu = (int)(f0 / ucap), cs = (int)(f0 % ucap);   // (row or unit, slot) of the chunk start
+        int brow = 0;                                        // balanced: row of the chunk start
+        if (bal) { while (brow + 1 < nrows && pref[brow + 1] <= f0) ++brow; }
         for (long long cb = f0; cb < f1; cb += CHK) {
             int un[CHK / 32], pg[CHK / 32], hg[CHK / 32];
             bool ok[CHK / 32];
+            if (bal) { while (brow + 1 < nrows && pref[brow + 1] <= cb) ++brow; }
 #pragma unroll
             for (int r = 0; r < CHK / 32; ++r) {
                 int u = cu, sl = cs + r * 32 + lane;
-                while (sl >= ucap) { sl -= ucap; ++u; }
+                if (bal) {
+                    const int e = (int)(cb + r * 32 + lane);
+                    u = brow;
+                    while (u + 1 < nrows && pref[u + 1] <= e) ++u;
+                    sl = e - pref[u];
+                } else {
+                    while (sl >= ucap) { sl -= ucap; ++u; }
+                }
                 const int bb = full ? u / c.Hkv : u / Hq;      // u: full -> unit; sparse -> row
                 un[r] = full ? u : bb * c.Hkv + (u % Hq) / G;
                 hg[r] = full ? 0 : (u % Hq) % G;
