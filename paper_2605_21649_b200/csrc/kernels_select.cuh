@@ -397,12 +397,28 @@ __global__ void __launch_bounds__(NT) k_gauss_select(const float *__restrict__ m
         if (mass >= 1.0) lo = tau; else hi = tau;
         double nt = (dmass > 0.0) ? tau + (mass - 1.0) / dmass : 0.5 * (lo + hi);
         if (!(nt > lo && nt < hi)) nt = 0.5 * (lo + hi);
-        const bool stop = fabs(nt - tau) <= 1e-6 * fmax(1.0, fabs(tau)) || hi - lo <= 1e-6 * fmax(1.0, fabs(hi));
+        const bool stop = fabs(nt - tau) <= 2e-7 * fmax(1.0, fabs(tau)) || hi - lo <= 2e-7 * fmax(1.0, fabs(hi));
         tau = nt;
         if (stop) break;
     }
-    // (2) fp64: a verified bracket around the fp32 root, then safeguarded Newton to fp64
+    // (2) fp64 Newton straight from the fp32 root (mass is convex and decreasing: quadratic
+    // convergence from ~1e-6 takes two or three passes); any large or non-finite step falls
+    // back to a verified bracket + safeguarded Newton
+    bool done64 = false;
+    {
+        double t = tau;
+        for (int it = 0; it < 4; ++it) {
+            gauss_mass2<NT, true>(m_, s_, M, Lseq, af, beta, t, mass, dmass, shd);
+            if (!(dmass > 0.0)) break;
+            const double step = (mass - 1.0) / dmass;
+            if (!(fabs(step) <= 1e-3 * fmax(1.0, fabs(t)))) break;
+            t += step;
+            if (fabs(step) <= 1e-14 * fmax(1.0, fabs(t))) { done64 = true; break; }
+        }
+        if (done64) tau = t;
+    }
     double dl = 1e-4 * fmax(1.0, fabs(tau));
+    if (!done64) {
     lo = tau - dl;
     for (int it = 0; it < 200; ++it) {
         gauss_mass2<NT, true>(m_, s_, M, Lseq, af, beta, lo, mass, dmass, shd);
@@ -427,6 +443,7 @@ __global__ void __launch_bounds__(NT) k_gauss_select(const float *__restrict__ m
             break;
         }
         tau = nt;
+    }
     }
     // page rule + ordered compaction (NT pages per round)
     int32_t *out = page_idx + (size_t)row * sel_stride;
