@@ -335,7 +335,7 @@ def main():
     full_bytes = n_tok * Hkv * 2 * d * 2
 
     # ---- full-cache entmax baseline (a5)
-    full_us = None
+    full_us = full_dense_us = None
     if not args.no_full:
         wsf = ekv.alloc_workspace(cache, Hq, None)
         fo = torch.empty(1, Hq, d, dtype=torch.float32, device=dev)
@@ -343,6 +343,9 @@ def main():
         fsu = torch.empty(1, Hq, dtype=torch.int32, device=dev)
         full_us = time_graph(lambda: ekv.full_attend(cache, q, attn, workspace=wsf, out=fo, tau=ft, supp=fsu,
                                                      stream=stream), max(5, reps // 5))
+        attn_d = ekv.attn_params(args.alpha, dense_v=True)
+        full_dense_us = time_graph(lambda: ekv.full_attend(cache, q, attn_d, workspace=wsf, out=fo, tau=ft,
+                                                           supp=fsu, stream=stream), max(5, reps // 5))
         del wsf
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
@@ -399,8 +402,12 @@ def main():
             "phases_us": phases,
             "step_bytes": step_bytes, "step_gbs": step_bytes / (us_step * 1e-6) / 1e9,
             "bytes_read_vs_full": step_bytes / full_bytes,
-            "full_entmax_us": full_us,
-            "speedup_vs_full_entmax": (full_us / us_step) if full_us else None,
+            # a5 baseline (SURVEY 8(c) reading 17): dense-V full-cache entmax (all K and all V, the
+            # paper's reference P:1343); the support-V variant (all K, V of the support) beside it
+            "full_entmax_us": full_dense_us,
+            "speedup_vs_full_entmax": (full_dense_us / us_step) if full_dense_us else None,
+            "full_entmax_support_v_us": full_us,
+            "speedup_vs_full_entmax_support_v": (full_us / us_step) if full_us else None,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_us, "unit": "us", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches_per_step * args.steps,

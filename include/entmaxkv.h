@@ -73,10 +73,15 @@ typedef struct {
     int32_t *seq_lens;
 } ekv_cache;
 
-/* alpha > 1; transform = ekv_transform (softmax ignores alpha). */
+/* alpha > 1; transform = ekv_transform (softmax ignores alpha).
+ * flags: EKV_ATTN_DENSE_V -- entmaxkv_full_attend streams EVERY V row (weights p_j, zero
+ * outside the support), the paper's full-cache reference that reads all scores and V
+ * (P:1343); without it the full path reads V of the support only.  Ignored elsewhere. */
+enum { EKV_ATTN_DENSE_V = 1 };
 typedef struct {
     float alpha;
     int32_t transform;
+    int32_t flags;
 } ekv_attn_params;
 
 /*

@@ -46,8 +46,11 @@ class ekv_cache(ctypes.Structure):
                 ("kvar", ctypes.c_void_p), ("page_table", ctypes.c_void_p), ("seq_lens", ctypes.c_void_p)]
 
 
+EKV_ATTN_DENSE_V = 1
+
+
 class ekv_attn_params(ctypes.Structure):
-    _fields_ = [("alpha", ctypes.c_float), ("transform", ctypes.c_int32)]
+    _fields_ = [("alpha", ctypes.c_float), ("transform", ctypes.c_int32), ("flags", ctypes.c_int32)]
 
 
 class ekv_select_params(ctypes.Structure):
@@ -191,8 +194,9 @@ def select_params(policy="topk", k_pages=64, q_page=0.99, margin=0.0) -> ekv_sel
     return ekv_select_params(pol, int(k_pages), float(q_page), float(margin))
 
 
-def attn_params(alpha=1.5, transform="entmax") -> ekv_attn_params:
-    return ekv_attn_params(float(alpha), {"entmax": EKV_ENTMAX, "softmax": EKV_SOFTMAX}[transform])
+def attn_params(alpha=1.5, transform="entmax", dense_v=False) -> ekv_attn_params:
+    return ekv_attn_params(float(alpha), {"entmax": EKV_ENTMAX, "softmax": EKV_SOFTMAX}[transform],
+                           EKV_ATTN_DENSE_V if dense_v else 0)
 
 
 def workspace_size(cache: PagedCache, n_q_heads: int, sel: ekv_select_params | None) -> int:

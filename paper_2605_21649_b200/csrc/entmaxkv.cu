@@ -270,15 +270,6 @@ ekv_status launch_scores(const CacheView &v, const void *q, int Hq, const uint32
     }
 }
 
-template <typename T>
-ekv_status launch_tau(const CacheView &v, const TauArgs &A, int rows, cudaStream_t st) {
-    constexpr int smem = kTauSmem;   // ck, cin, cphys, pruned list (+ ~29 KB static)
-    static bool init = false;
-    if (!init) { set_smem(k_tau_pv<T>, smem); init = true; }
-    k_tau_pv<T><<<rows, kTauNT, smem, st>>>(v, A);
-    return check_launch("k_tau_pv");
-}
-
 template <typename T, int IB>
 ekv_status launch_tau_sparse_ib(const CacheView &v, const TauArgs &A, int rows, cudaStream_t st) {
     static bool init = false;
@@ -290,7 +281,7 @@ ekv_status launch_tau_sparse_ib(const CacheView &v, const TauArgs &A, int rows, 
     }
     // a cluster of up to 4 CTAs per row splits the candidate extraction (page-list reads are
     // latency bound per SM); rank 0 then finishes the row
-    const int CL = A.sel_stride > 384 ? 4 : A.sel_stride > 128 ? 2 : 1;
+    const int CL = A.full ? 1 : A.sel_stride > 384 ? 4 : A.sel_stride > 128 ? 2 : 1;
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3((unsigned)(rows * CL));
@@ -392,20 +383,38 @@ ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t 
         int32_t *pc = at<int32_t>(ws, L.smx_cnt);
         if (c->dtype == EKV_BF16)
             k_softmax_partial<__nv_bfloat16><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, pi, ns, stride, full, Hq,
-                                                                 Hq / c->n_kv_heads, nch, pacc, pl, pc);
+                                                                 Hq / c->n_kv_heads, nch, pacc, pl, pc, nullptr, 0.f);
         else
             k_softmax_partial<float><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, pi, ns, stride, full, Hq,
-                                                        Hq / c->n_kv_heads, nch, pacc, pl, pc);
+                                                        Hq / c->n_kv_heads, nch, pacc, pl, pc, nullptr, 0.f);
         EKV_TRY(check_launch("k_softmax_partial"));
         k_softmax_combine<<<rows, 128, 0, st>>>(pacc, pl, pc, rowmax, nch, out, tau, supp);
         return check_launch("k_softmax_combine");
     }
-    if (!full && attn->transform == EKV_ENTMAX && !A.tok_list) {
-        if (c->dtype == EKV_BF16) return launch_tau_sparse<__nv_bfloat16>(v, A, rows, st);
-        return launch_tau_sparse<float>(v, A, rows, st);
+    const bool dense = full && (attn->flags & EKV_ATTN_DENSE_V) && !A.tok_list;
+    if (dense) {
+        // dense-V baseline: exact tau first (no PV), then every V row streamed with p_j
+        A.no_pv = 1;
+        if (!tau) A.tau_out = at<double>(ws, L.tau_int);
     }
-    if (c->dtype == EKV_BF16) return launch_tau<__nv_bfloat16>(v, A, rows, st);
-    return launch_tau<float>(v, A, rows, st);
+    if (c->dtype == EKV_BF16) EKV_TRY(launch_tau_sparse<__nv_bfloat16>(v, A, rows, st));
+    else EKV_TRY(launch_tau_sparse<float>(v, A, rows, st));
+    if (!dense) return EKV_OK;
+    const int dch = (c->max_pages_per_seq + kSmxPages - 1) / kSmxPages;
+    dim3 g(dch, rows);
+    float *pacc = at<float>(ws, L.smx_acc);
+    double *pl = at<double>(ws, L.smx_l);
+    int32_t *pc = at<int32_t>(ws, L.smx_cnt);
+    if (c->dtype == EKV_BF16)
+        k_softmax_partial<__nv_bfloat16><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, pi, ns, stride, full, Hq,
+                                                             Hq / c->n_kv_heads, dch, pacc, pl, pc, A.tau_out,
+                                                             attn->alpha);
+    else
+        k_softmax_partial<float><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, pi, ns, stride, full, Hq,
+                                                    Hq / c->n_kv_heads, dch, pacc, pl, pc, A.tau_out, attn->alpha);
+    EKV_TRY(check_launch("k_softmax_partial"));
+    k_softmax_combine<<<rows, 128, 0, st>>>(pacc, pl, pc, rowmax, dch, out, nullptr, nullptr);
+    return check_launch("k_softmax_combine");
 }
 
 

@@ -220,13 +220,33 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
     const unsigned hm = 0xffffu << (16 * half);
     T *qsh = reinterpret_cast<T *>(smem + AttCfg<T>::RING) + warp * G * kD;   // q cache of the warp
     int cu = -1, L = 0;                           // unit whose q is in qsh
+    // running row maxima of the current unit (lanes 0 and 16: their half-warp's items),
+    // flushed with one atomicMax per (head, half-warp) when the unit changes and at the end
+    // (one atomic per item would serialise on the few rowmax words in full mode)
+    float hmax[G];
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) hmax[gg] = -INFINITY;
+    auto flush = [&](int u) {
+        if (u >= 0 && t == 0) {
+            const int row0 = (u / c.Hkv) * Hq + (u % c.Hkv) * G;
+#pragma unroll
+            for (int gg = 0; gg < G; ++gg)
+                if (hmax[gg] > -INFINITY) atomicMax(rowmax + row0 + gg, f2key(hmax[gg]));
+        }
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) hmax[gg] = -INFINITY;
+    };
     for (int si = 0;; ++si) {
         const int slot = si % NS;
         mbar_wait(&fullb[slot], (si / NS) & 1);
         const int n = d_n[slot];
         stamp_cta<1>(threadIdx.x == 0 && si == 0, 1);
         stamp_if(threadIdx.x == 0 && si < 16, 3, si);
-        if (n < 0) { stamp_cta<1>(threadIdx.x == 0, 2); count_cta<1>(threadIdx.x == 0, si); break; }
+        if (n < 0) {
+            flush(cu);
+            stamp_cta<1>(threadIdx.x == 0, 2); count_cta<1>(threadIdx.x == 0, si);
+            break;
+        }
         const int ni = d_ni[slot];
         for (int base = 2 * warp; base < ni; base += 2 * NCW) {            // warp-uniform
             const int it = base + half;
@@ -238,6 +258,7 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
             for (int pass = 0; pass < (unitA != unitB ? 2 : 1); ++pass) {  // warp-uniform
                 const int u = pass ? unitB : unitA;
                 if (u != cu) {                                             // warp-uniform
+                    flush(cu);
                     const int bb = u / c.Hkv, kh = u % c.Hkv;
                     __syncwarp();
                     const uint4 *src = reinterpret_cast<const uint4 *>(q + ((size_t)bb * Hq + kh * G) * kD);
@@ -292,7 +313,9 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
             float m = v;
 #pragma unroll
             for (int o = 8; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(hm, m, o));
-            if (t == 0 && m > -INFINITY) atomicMax(rowmax + row, f2key(m));
+            (void)row;
+#pragma unroll
+            for (int gg = 0; gg < G; ++gg) if (gg == g) hmax[gg] = fmaxf(hmax[gg], m);
             }
         }
         __syncwarp();
@@ -408,21 +431,7 @@ __global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ sc
 }
 
 // ============================================================================ exact tau + PV
-// One CTA (256 threads) per (b, q-head):
-//  1. candidates {z > tau_lo = z_max - 1} in a FIXED order (fp64 sums below are then
-//     deterministic): sparse rows are read directly from the score row over the head's
-//     page list (block scan per round of 4 pages per thread); full rows come from the
-//     k_candidates chunk regions concatenated in chunk order.  Overflow -> Newton
-//     streamed over the source moves tau_lo just below tau, then an ordered re-extraction.
-//  2. Newton on g(tau) = ||(z - tau)_+||_beta - 1 from tau_lo (convex, decreasing:
-//     monotone from the left, exact in one step for one active token);
-//  3. support by R9: z > tau_N + band -> in, z < tau_N - band -> out, else F(z_j) < 1;
-//  4. tau from the support: beta = 1: (S1 - 1)/k; beta = 2: m - sqrt((1 - ss)/k);
-//     otherwise one Newton polish on sum_S (z - tau)^beta = 1;
-//  5. p_j = (z_j - tau)^beta; out = sum p_j v_j / sum p_j (R12): support tokens are
-//     compacted NT at a time, their page-table entries fetched in parallel, then warps
-//     gather the V rows (4 in flight per warp; lane = 4 dims);
-// Softmax rows (a6): p = exp(s - s_max) over every valid token (dense V).
+// The tau / support / PV kernel is k_tau_sparse (kernels_tau.cuh); the shared pieces live here.
 constexpr int kTauNT = 256;
 constexpr int kCap = 12288;         // shared-memory candidate capacity
 constexpr int kPr = 2048;           // pruned-list capacity (tau solver)
@@ -435,6 +444,7 @@ struct TauArgs {
     int Hq, G; float alpha; int transform;
     float *out; double *tau_out; int32_t *supp_out;
     int32_t *tok_list; double *p_list; int32_t *n_list; int list_cap;     // eval list
+    int no_pv;                                                            // tau/supp only (dense-V)
 };
 
 template <typename T>
@@ -459,586 +469,6 @@ __device__ __forceinline__ double lbeta_step(double F, double Fd, double beta, i
     else if (ib == 4) { root = sqrtf(sqrtf(Ff)); rm1 = dF / ((1.0f + root) * (1.0f + root * root)); }
     else { rm1 = expm1f(log1pf(dF) / (float)beta); root = 1.0f + rm1; }
     return (double)(rm1 * Ff / (root * Fdf));
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kTauNT, 1) k_tau_pv(CacheView c, TauArgs A) {
-    EKV_TRACE(6);
-    constexpr int NT = kTauNT;
-    constexpr int NW = NT / 32;
-    extern __shared__ __align__(16) unsigned char smem[];
-    unsigned long long *ck = reinterpret_cast<unsigned long long *>(smem);   // [kCap] (j << 32 | s bits)
-    uint8_t *cin = reinterpret_cast<uint8_t *>(smem + sizeof(unsigned long long) * kCap);   // [kCap]
-    int *cphys = reinterpret_cast<int *>(smem + (sizeof(unsigned long long) + 1) * kCap);    // [kCap] (direct path)
-    __shared__ double rbuf[2 * 2 * NW];
-    __shared__ double shd[2 * NW + 2];
-    __shared__ int shi[NW + 1];
-    __shared__ float red[NW][kD];
-    constexpr int kSup = 2048;
-    __shared__ int sup_j[kSup], sup_phys[kSup];
-    __shared__ float sup_p[kSup];
-    BlockRed2<NT> R{rbuf, 0};
-
-    stamp(0, 0);
-    const int row = blockIdx.x;
-    const int b = row / A.Hq, h = row % A.Hq, kvh = h / A.G;
-    const int L = c.seq_lens[b];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t mk = A.rowmax[row];
-    if (mk == 0u) {   // empty C_tok
-        if (threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = 0.0f;
-        if (threadIdx.x == 0) {
-            if (A.tau_out) A.tau_out[row] = NAN;
-            if (A.supp_out) A.supp_out[row] = 0;
-            if (A.n_list) A.n_list[row] = 0;
-        }
-        return;
-    }
-    const float smax = key2f(mk);
-    const int nlist = A.full ? n_pages_of(L) : A.n_sel[row];
-    const int32_t *plist = A.page_idx + (size_t)row * A.sel_stride;
-    const float *srow = A.scores + (size_t)row * A.ntok;
-    const T *Vb = reinterpret_cast<const T *>(c.V);
-
-    if (A.transform == 1) {
-        // ---------------- softmax over C_tok: every valid token of the page list (dense V)
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        double zs = 0.0, dz = 0.0;
-        int cnt = 0;
-        for (int e = warp; e < nlist * kP; e += NW) {
-            const int pg = A.full ? e / kP : plist[e / kP];
-            const int j = pg * kP + e % kP;
-            if (j >= L) continue;
-            const float p = expf(srow[j] - smax);
-            if (lane == 0) { zs += (double)p; ++cnt; }
-            const int phys = c.page_table[(size_t)b * c.maxp + pg];
-            float vx[4];
-            ldv4<T>(Vb + (((size_t)phys * c.Hkv + kvh) * kP + (j % kP)) * kD + 4 * lane, vx);
-#pragma unroll
-            for (int e2 = 0; e2 < 4; ++e2) acc[e2] = __fmaf_rn(p, vx[e2], acc[e2]);
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) red[warp][4 * lane + e] = acc[e];
-        R.sum(zs, dz);
-        cnt = block_sum_i<NT>(cnt, shi);
-        if (threadIdx.x < kD) {
-            float o = 0.f;
-            for (int w = 0; w < NW; ++w) o = __fadd_rn(o, red[w][threadIdx.x]);
-            A.out[(size_t)row * kD + threadIdx.x] = (float)((double)o / zs);
-        }
-        if (threadIdx.x == 0) {
-            if (A.tau_out) A.tau_out[row] = (double)smax + log(zs);
-            if (A.supp_out) A.supp_out[row] = cnt;
-        }
-        return;
-    }
-
-    // ---------------- exact alpha-entmax
-    const double a = (double)A.alpha - 1.0;
-    const double beta = 1.0 / a;
-    const int ib = (fabs(beta - rint(beta)) < 1e-12 && beta <= 4.5) ? (int)rint(beta) : 0;
-    const double zmax = a * (double)smax;
-    double tau_lo = zmax - 1.0 - 1e-12 * fmax(1.0, fabs(zmax));
-    int ncand = 0;
-    bool overflow = false;
-    bool have_phys = false;                 // cphys[] valid (direct extraction without overflow)
-
-    if (!A.full) {
-        // (direct) rounds of up to 4 list pages per thread: loads in flight, count, scan, write
-        // fp32 pre-test (conservative: a * s > tau_lo needs s > tau_lo / a; -inf never passes)
-        const float thr_c = (float)(tau_lo / a);
-        const float thr_f = thr_c - 1e-6f * fmaxf(1.0f, fabsf(thr_c));
-        for (int r0 = 0; r0 < nlist; r0 += 4 * NT) {
-            float sv[4][kP];
-            int pgs[4], phs[4];
-            int cnt = 0;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int li = r0 + threadIdx.x + u * NT;
-                pgs[u] = li < nlist ? plist[li] : -1;
-                phs[u] = 0;
-                if (pgs[u] >= 0) {
-                    phs[u] = __ldg(c.page_table + (size_t)b * c.maxp + pgs[u]);
-                    const float4 *p4 = reinterpret_cast<const float4 *>(srow + (size_t)pgs[u] * kP);
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        const float4 x = p4[v];
-                        sv[u][4 * v] = x.x; sv[u][4 * v + 1] = x.y; sv[u][4 * v + 2] = x.z; sv[u][4 * v + 3] = x.w;
-                    }
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (pgs[u] >= 0) {
-#pragma unroll
-                    for (int t = 0; t < kP; ++t)
-                        cnt += (pgs[u] * kP + t < L && sv[u][t] >= thr_f && a * (double)sv[u][t] > tau_lo);
-                }
-            int tot;
-            int pos = ncand + block_excl_scan<NT>(cnt, shi, &tot);
-            if (ncand + tot > kCap) { overflow = true; break; }   // uniform
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (pgs[u] >= 0) {
-#pragma unroll
-                    for (int t = 0; t < kP; ++t)
-                        if (pgs[u] * kP + t < L && sv[u][t] >= thr_f && a * (double)sv[u][t] > tau_lo) {
-                            cphys[pos] = phs[u];
-                            ck[pos++] = ((unsigned long long)(uint32_t)(pgs[u] * kP + t) << 32) | __float_as_uint(sv[u][t]);
-                        }
-                }
-            ncand += tot;
-        }
-        have_phys = !overflow;
-        __syncthreads();
-    } else {
-        // (full) chunk regions from k_candidates, concatenated in chunk order (nch <= NT)
-        int ccnt = 0, tot = 0;
-        bool chunk_ovf = false;
-        if (threadIdx.x < A.nch) {
-            ccnt = A.ccount[(size_t)row * A.nch + threadIdx.x];
-            chunk_ovf = ccnt > kCpc;
-        }
-        const int coff = block_excl_scan<NT>(ccnt, shi, &tot);
-        chunk_ovf = __syncthreads_or(chunk_ovf);
-        const float *gs = A.cand_s + (size_t)row * A.nch * kCpc;
-        const int32_t *gj = A.cand_j + (size_t)row * A.nch * kCpc;
-        if (!chunk_ovf && tot <= kCap) {
-            int *s_off = reinterpret_cast<int *>(cin);       // cin is free until the support pass
-            if (threadIdx.x < A.nch) s_off[threadIdx.x] = coff;
-            __syncthreads();
-#pragma unroll 4
-            for (int e = threadIdx.x; e < tot; e += NT) {
-                int lo = 0, hi = A.nch - 1;               // last chunk with offset <= e
-                while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (s_off[mid] <= e) lo = mid; else hi = mid - 1; }
-                const size_t g = (size_t)lo * kCpc + (e - s_off[lo]);
-                ck[e] = ((unsigned long long)(uint32_t)__ldg(gj + g) << 32) | __float_as_uint(__ldg(gs + g));
-            }
-            ncand = tot;
-            __syncthreads();
-        } else if (!chunk_ovf) {
-            // too many for shared memory: Newton over the chunk regions (thread t <-> chunk t)
-            double tau = tau_lo;
-            for (int it = 0; it < 200; ++it) {
-                double F = 0.0, Fd = 0.0;
-                if (threadIdx.x < A.nch) {
-                    const size_t g0 = (size_t)threadIdx.x * kCpc;
-                    for (int k = 0; k < ccnt; ++k) {
-                        const double d = a * (double)__ldg(gs + g0 + k) - tau;
-                        if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
-                    }
-                }
-                R.sum(F, Fd);
-                if (!(Fd > 0.0)) break;
-                const double step = lbeta_step(F, Fd, beta, ib);
-                tau += step;
-                if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(tau)))) break;
-            }
-            tau_lo = fmax(tau_lo, tau - 1e-7 * fmax(1.0, fabs(tau)));
-            int mine = 0;
-            if (threadIdx.x < A.nch) {
-                const size_t g0 = (size_t)threadIdx.x * kCpc;
-                for (int k = 0; k < ccnt; ++k) mine += a * (double)__ldg(gs + g0 + k) > tau_lo;
-            }
-            int tt;
-            int pos = block_excl_scan<NT>(mine, shi, &tt);
-            if (tt > kCap) overflow = true;
-            else {
-                if (threadIdx.x < A.nch) {
-                    const size_t g0 = (size_t)threadIdx.x * kCpc;
-                    for (int k = 0; k < ccnt; ++k) {
-                        const float sj = __ldg(gs + g0 + k);
-                        if (a * (double)sj > tau_lo)
-                            ck[pos++] = ((unsigned long long)(uint32_t)__ldg(gj + g0 + k) << 32) | __float_as_uint(sj);
-                    }
-                }
-                ncand = tt;
-            }
-            __syncthreads();
-        } else {
-            overflow = true;
-        }
-    }
-    if (overflow) {
-        // Newton streamed over the whole score row (coalesced, fixed thread mapping), then
-        // an ordered re-extraction by contiguous per-thread segments of the page list.
-        const int ntk = nlist * kP;
-        double tau = tau_lo;
-        for (int it = 0; it < 200; ++it) {
-            double F = 0.0, Fd = 0.0;
-            for (int e = threadIdx.x; e < ntk; e += NT) {
-                const int pg = A.full ? e / kP : plist[e / kP];
-                const int j = pg * kP + e % kP;
-                if (j >= L) continue;
-                const float sj = srow[j];
-                if (sj == -INFINITY) continue;
-                const double d = a * (double)sj - tau;
-                if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
-            }
-            R.sum(F, Fd);
-            if (!(Fd > 0.0)) break;
-            const double step = lbeta_step(F, Fd, beta, ib);
-            tau += step;
-            if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(tau)))) break;
-        }
-        tau_lo = fmax(tau_lo, tau - 1e-7 * fmax(1.0, fabs(tau)));
-        const int seg = (nlist + NT - 1) / NT;            // pages per thread, contiguous in list order
-        int mine = 0;
-        for (int li = threadIdx.x * seg; li < min(nlist, (threadIdx.x + 1) * seg); ++li) {
-            const int pg = A.full ? li : plist[li];
-            for (int t = 0; t < kP; ++t) {
-                const int j = pg * kP + t;
-                if (j < L && srow[j] != -INFINITY && a * (double)srow[j] > tau_lo) ++mine;
-            }
-        }
-        int tt;
-        int pos = block_excl_scan<NT>(mine, shi, &tt);
-        if (tt > kCap) {             // support larger than the shared-memory capacity
-            if (threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = NAN;
-            if (threadIdx.x == 0) {
-                if (A.tau_out) A.tau_out[row] = NAN;
-                if (A.supp_out) A.supp_out[row] = -tt;
-            }
-            return;
-        }
-        for (int li = threadIdx.x * seg; li < min(nlist, (threadIdx.x + 1) * seg); ++li) {
-            const int pg = A.full ? li : plist[li];
-            for (int t = 0; t < kP; ++t) {
-                const int j = pg * kP + t;
-                if (j < L && srow[j] != -INFINITY && a * (double)srow[j] > tau_lo)
-                    ck[pos++] = ((unsigned long long)(uint32_t)j << 32) | __float_as_uint(srow[j]);
-            }
-        }
-        ncand = tt;
-        __syncthreads();
-    }
-    stamp(0, 2);
-#ifdef EKV_STAMPS
-    if (blockIdx.x == 0 && threadIdx.x == 0) ekv_stamps[0][14] = (unsigned long long)ncand;
-#endif
-#define ZOF(k) (a * (double)__uint_as_float((uint32_t)(ck[k] & 0xffffffffu)))
-    // ---- tau and support by warp 0 alone (warp-shuffle sums, no block barriers; the xor
-    // butterfly leaves the same value on every lane, so every result is deterministic):
-    //  (a) fp32 Newton on the candidates (cheap; only steers),
-    //  (b) certified lower bound lo2 = tau32 - 1e-3 max(1, |tau32|) if F(lo2) >= 1 in fp64
-    //      (F decreasing -> tau >= lo2; else lo2 = tau_lo), and the list {z > lo2} in fp64
-    //      compacted into shared memory (every token outside it has F(z) >= 1: not in S),
-    //  (c) fp64 Newton on the list from lo2, R9 support, tau from the support (closed forms),
-    //  (d) the support's p_j and V addresses for the PV gather.
-    double *zp = reinterpret_cast<double *>(smem + (sizeof(unsigned long long) + 1 + 4) * kCap);   // [kPr]
-    int *ip = reinterpret_cast<int *>(smem + (sizeof(unsigned long long) + 1 + 4) * kCap + 8 * kPr); // [kPr]
-    __shared__ double s_tau, s_kk, s_psum;
-    __shared__ int s_nsup, s_mode;
-    if (warp == 0) {
-        const float af = (float)a;
-        const float betaf = (float)beta;
-        float tf = (float)tau_lo;
-        // a few fp32 Newton steps from the left: only a pruning point, not a result
-        for (int it = 0; it < 6; ++it) {
-            float F0 = 0.f, F1 = 0.f, D0 = 0.f, D1 = 0.f;
-            for (int k = lane; k < ncand; k += 64) {
-                const float d0 = af * __uint_as_float((uint32_t)ck[k]) - tf;
-                if (d0 > 0.f) { F0 += powbf(d0, betaf, ib); D0 += powbm1f(d0, betaf, ib); }
-                if (k + 32 < ncand) {
-                    const float d1 = af * __uint_as_float((uint32_t)ck[k + 32]) - tf;
-                    if (d1 > 0.f) { F1 += powbf(d1, betaf, ib); D1 += powbm1f(d1, betaf, ib); }
-                }
-            }
-            float F = F0 + F1, D = D0 + D1;
-#pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) {
-                F += __shfl_xor_sync(0xffffffffu, F, o);
-                D += __shfl_xor_sync(0xffffffffu, D, o);
-            }
-            if (!(D > 0.f)) break;
-            const float step = (float)lbeta_step((double)F, (double)D, beta, ib);
-            tf += step;
-            if (!(fabsf(step) > 1e-4f * fmaxf(1.0f, fabsf(tf)))) break;
-        }
-        stamp(6, 1);
-        auto wsum2 = [&](double &x, double &y) {
-#pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) {
-                x += __shfl_xor_sync(0xffffffffu, x, o);
-                y += __shfl_xor_sync(0xffffffffu, y, o);
-            }
-        };
-        // (b) list {z > base} with the fp64 mass F(base); an fp32 pre-test skips the
-        // fp64 work of tokens far below base (conservative margin)
-        auto build = [&](double base, double &F) -> int {
-            int np = 0;
-            double f = 0.0, dz = 0.0;
-            const float bf = (float)base;
-            const float bpre = bf - 1e-3f * fmaxf(1.0f, fabsf(bf));
-            for (int k0 = 0; k0 < ncand; k0 += 32) {
-                const int k = k0 + lane;
-                const bool pre = k < ncand && af * __uint_as_float((uint32_t)ck[k]) > bpre;
-                if (!__any_sync(0xffffffffu, pre)) continue;
-                double z = 0.0;
-                bool in = false;
-                if (pre) {
-                    z = ZOF(k);
-                    const double d = z - base;
-                    if (d > 0.0) { f += powb(d, beta, ib); in = true; }
-                }
-                const unsigned bal = __ballot_sync(0xffffffffu, in);
-                const int pos = np + __popc(bal & ((1u << lane) - 1u));
-                if (in && pos < kPr) { zp[pos] = z; ip[pos] = k; }
-                np += __popc(bal);
-            }
-            wsum2(f, dz);
-            F = f;
-            return np;
-        };
-        double base = (double)tf - 1e-4 * fmax(1.0, fabs((double)tf));
-        double Fb = 0.0;
-        int np = -1;
-        if (base > tau_lo && tf == tf) {
-            np = build(base, Fb);
-            if (!(Fb >= 1.0)) np = -1;
-        }
-        if (np < 0) { base = tau_lo; np = build(base, Fb); }
-        stamp(6, 2);
-        const bool listed = np <= kPr;      // else: work on the whole candidate array
-        const int nl = listed ? np : ncand;
-#define ZL(i) (listed ? zp[i] : ZOF(i))
-        for (int k = lane; k < ncand; k += 32) cin[k] = 0;
-        __syncwarp();
-        double tauN = base;
-        int n_it = 0, amb = 0;
-        if (listed && np <= 64) {
-            // (c1) short list: the R9 criterion itself, F(z_j) = sum_i (z_i - z_j)_+^beta < 1,
-            // for every entry (all pairs; z_i broadcast from shared memory)
-            for (int i = lane; i < nl; i += 32) {
-                const double zj = zp[i];
-                double F = 0.0;
-                for (int i2 = 0; i2 < nl; ++i2) {
-                    const double d = zp[i2] - zj;
-                    if (d > 0.0) F += powb(d, beta, ib);
-                }
-                cin[ip[i]] = (F < 1.0) ? 1 : 0;
-            }
-            __syncwarp();
-            if (ib != 1 && ib != 2) {
-                // Newton polish start for the general-beta tau below: the largest listed z
-                // outside the support (or base) has F >= 1, i.e. lies left of tau
-                double t0 = base, dz = 0.0;
-                for (int i = lane; i < nl; i += 32)
-                    if (!cin[ip[i]]) t0 = fmax(t0, zp[i]);
-#pragma unroll
-                for (int o = 16; o >= 1; o >>= 1) t0 = fmax(t0, __shfl_xor_sync(0xffffffffu, t0, o));
-                tauN = t0;
-                for (int it = 0; it < 60; ++it) {
-                    double F = 0.0, Fd = 0.0;
-                    for (int i = lane; i < nl; i += 32)
-                        if (cin[ip[i]]) { const double d = zp[i] - tauN; F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
-                    wsum2(F, Fd);
-                    if (!(Fd > 0.0)) break;
-                    const double step = lbeta_step(F, Fd, beta, ib);
-                    tauN += step;
-                    if (!(fabs(step) > 1e-15 * fmax(1.0, fabs(tauN)))) break;
-                }
-                (void)dz;
-            }
-        } else {
-            // (c2) fp64 Newton from base (monotone from the left), then R9 with a band
-            for (int it = 0; it < 200; ++it) {
-                n_it = it + 1;
-                double F = 0.0, Fd = 0.0;
-                for (int i = lane; i < nl; i += 32) {
-                    const double d = ZL(i) - tauN;
-                    if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
-                }
-                wsum2(F, Fd);
-                if (!(Fd > 0.0)) break;
-                const double step = lbeta_step(F, Fd, beta, ib);
-                tauN += step;
-                // 1e-14 relative is far inside the support band (R9) and the final tau is
-                // recomputed from the support; a tighter test can oscillate at the ulp level
-                if (!(fabs(step) > 1e-14 * fmax(1.0, fabs(tauN))) || it >= 63) break;
-            }
-            stamp(6, 3);
-            // support (R9): z > tau_N + band -> in, z < tau_N - band -> out, else F(z_j) < 1
-            // (list entries only: every other candidate has z <= base <= tau)
-            const double band = 1e-9 * fmax(1.0, fabs(tauN));
-            for (int i = lane; i < nl; i += 32) {
-                const double z = ZL(i);
-                const uint8_t f = (z > tauN + band) ? 1 : (z < tauN - band) ? 0 : 2;
-                cin[listed ? ip[i] : i] = f;
-                amb += (f == 2);
-            }
-            amb = __reduce_add_sync(0xffffffffu, amb);
-            __syncwarp();
-            if (amb > 0) {
-                for (int i0 = 0; i0 < nl; ++i0) {
-                    const int k0 = listed ? ip[i0] : i0;
-                    if (cin[k0] != 2) continue;
-                    const double zk = ZL(i0);
-                    double F = 0.0, dz = 0.0;
-                    for (int i = lane; i < nl; i += 32) {
-                        const double d = ZL(i) - zk;
-                        if (d > 0.0) F += powb(d, beta, ib);
-                    }
-                    wsum2(F, dz);
-                    __syncwarp();
-                    if (lane == 0) cin[k0] = (F < 1.0) ? 1 : 0;
-                    __syncwarp();
-                }
-            }
-        }
-#ifdef EKV_STAMPS
-        if (blockIdx.x == 0 && lane == 0) {
-            ekv_stamps[0][13] = (unsigned long long)n_it; ekv_stamps[0][12] = (unsigned long long)amb;
-            ekv_stamps[0][11] = (unsigned long long)np;
-        }
-#endif
-        stamp(6, 4);
-        // tau from the support
-        double S1 = 0.0, kk = 0.0;
-        for (int i = lane; i < nl; i += 32)
-            if (cin[listed ? ip[i] : i]) { S1 += ZL(i); kk += 1.0; }
-        wsum2(S1, kk);
-        double tau;
-        if (ib == 1) {
-            tau = (S1 - 1.0) / kk;
-        } else if (ib == 2) {
-            const double m = S1 / kk;
-            double ss = 0.0, dz = 0.0;
-            for (int i = lane; i < nl; i += 32)
-                if (cin[listed ? ip[i] : i]) { const double d = ZL(i) - m; ss += d * d; }
-            wsum2(ss, dz);
-            tau = m - sqrt(fmax(0.0, 1.0 - ss) / kk);
-        } else {
-            double F = 0.0, Fd = 0.0;
-            for (int i = lane; i < nl; i += 32)
-                if (cin[listed ? ip[i] : i]) { const double d = ZL(i) - tauN; F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
-            wsum2(F, Fd);
-            tau = tauN + (F - 1.0) / (beta * Fd);
-        }
-        stamp(6, 5);
-        // (d) support entries (list order) with p_j, if they fit the shared support arrays
-        int nsup = 0;
-        double psum = 0.0, dz = 0.0;
-        if (listed && kk <= (double)kSup) {
-            for (int i0 = 0; i0 < nl; i0 += 32) {
-                const int i = i0 + lane;
-                const int k = i < nl ? ip[i] : 0;
-                const bool in = i < nl && cin[k];
-                const unsigned bal = __ballot_sync(0xffffffffu, in);
-                const int pos = nsup + __popc(bal & ((1u << lane) - 1u));
-                if (in) {
-                    const int j = (int)(ck[k] >> 32);
-                    const double d = zp[i] - tau;
-                    const double pd = d > 0.0 ? powb(d, beta, ib) : 0.0;
-                    sup_j[pos] = j;
-                    sup_p[pos] = (float)pd;
-                    sup_phys[pos] = have_phys ? cphys[k] : __ldg(c.page_table + (size_t)b * c.maxp + j / kP);
-                    psum += pd;
-                }
-                nsup += __popc(bal);
-            }
-            wsum2(psum, dz);
-        }
-#undef ZL
-        stamp(6, 6);
-        if (lane == 0) {
-            s_tau = tau; s_kk = kk; s_psum = psum; s_nsup = nsup;
-            s_mode = (listed && kk <= (double)kSup) ? 1 : 0;
-        }
-    }
-    stamp(0, 3);
-    __syncthreads();
-    const double tau = s_tau, kk = s_kk;
-    stamp(0, 4);
-    // ---- PV: warp w gathers support entries w, w + NW, ... (4 V rows in flight per warp)
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    double psum = 0.0;
-    auto gather = [&](int nsup) {
-        for (int e0 = warp; e0 < nsup; e0 += 4 * NW) {
-            float vx[4][4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int e = e0 + u * NW;
-                if (e < nsup) {
-                    const int j = sup_j[e];
-                    ldv4<T>(Vb + (((size_t)sup_phys[e] * c.Hkv + kvh) * kP + (j % kP)) * kD + 4 * lane, vx[u]);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int e = e0 + u * NW;
-                if (e < nsup) {
-                    const float p = sup_p[e];
-#pragma unroll
-                    for (int q2 = 0; q2 < 4; ++q2) acc[q2] = __fmaf_rn(p, vx[u][q2], acc[q2]);
-                }
-            }
-        }
-    };
-    if (s_mode == 1) {
-        gather(s_nsup);
-        if (threadIdx.x == 0) psum = s_psum;
-    } else {
-        // large support: compacted in candidate order, rounds of kSup entries
-        for (int r0 = 0; r0 < ncand;) {
-            int nsup = 0, r1 = r0;
-            while (r1 < ncand) {
-                const int k = r1 + threadIdx.x;
-                const bool in = k < ncand && cin[k];
-                int tot;
-                const int pos = nsup + block_excl_scan<NT>(in ? 1 : 0, shi, &tot);
-                if (nsup + tot > kSup) break;             // uniform
-                if (in) {
-                    const int j = (int)(ck[k] >> 32);
-                    const double d = ZOF(k) - tau;
-                    const double pd = d > 0.0 ? powb(d, beta, ib) : 0.0;
-                    sup_j[pos] = j;
-                    sup_p[pos] = (float)pd;
-                    sup_phys[pos] = have_phys ? cphys[k] : __ldg(c.page_table + (size_t)b * c.maxp + j / kP);
-                    psum += pd;
-                }
-                nsup += tot;
-                r1 += NT;
-            }
-            __syncthreads();
-            gather(nsup);
-            __syncthreads();
-            r0 = r1;
-        }
-    }
-#pragma unroll
-    for (int e = 0; e < 4; ++e) red[warp][4 * lane + e] = acc[e];
-    double pz = 0.0;
-    R.sum(psum, pz);
-    if (threadIdx.x < kD) {
-        float o = 0.f;
-        for (int w = 0; w < NW; ++w) o = __fadd_rn(o, red[w][threadIdx.x]);
-        A.out[(size_t)row * kD + threadIdx.x] = (float)((double)o / psum);
-    }
-    if (threadIdx.x == 0) {
-        if (A.tau_out) A.tau_out[row] = tau;
-        if (A.supp_out) A.supp_out[row] = (int)kk;
-    }
-    stamp(0, 5);
-    // ---- eval list: support token positions and p (for exact delta / rho)
-    if (A.tok_list) {
-        int base = 0;
-        for (int r0 = 0; r0 < ncand; r0 += NT) {
-            const int k = r0 + threadIdx.x;
-            const int keep = (k < ncand && cin[k]) ? 1 : 0;
-            int tot;
-            const int pos = block_excl_scan<NT>(keep, shi, &tot);
-            if (keep && base + pos < A.list_cap) {
-                const double d = ZOF(k) - tau;
-                A.tok_list[(size_t)row * A.list_cap + base + pos] = (int32_t)(ck[k] >> 32);
-                A.p_list[(size_t)row * A.list_cap + base + pos] = d > 0.0 ? powb(d, beta, ib) : 0.0;
-            }
-            base += tot;
-        }
-        if (threadIdx.x == 0) A.n_list[row] = base;
-    }
-#undef ZOF
-    stamp(0, 6);
 }
 
 // ============================================================================ a4: certified delta_bar

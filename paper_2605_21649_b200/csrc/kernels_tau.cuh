@@ -138,15 +138,17 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
     // independent loads first (one round trip): row max, list length, sequence length and
     // this rank's first-round page list
     const uint32_t mk = __ldg(A.rowmax + row);
-    const int nlist = __ldg(A.n_sel + row);
     const int L = __ldg(c.seq_lens + b);
+    const int nlist = A.full ? n_pages_of(L) : __ldg(A.n_sel + row);
+    // logical page of list entry i (full rows: every page, in order)
+    auto page_of = [&](int i) -> int { return A.full ? i : __ldg(plist + i); };
     // rank rk extracts the items [rk S, (rk + 1) S) (item = 4 scores), S from the list capacity
     const int S = ((A.sel_stride * 4 + CL - 1) / CL + 3) & ~3;
     int pg[kTsU];
 #pragma unroll
     for (int u = 0; u < kTsU; ++u) {
         const int e = rk * S + threadIdx.x + NT * u;
-        pg[u] = (e < (rk + 1) * S && (e >> 2) < A.sel_stride) ? __ldg(plist + (e >> 2)) : -1;
+        pg[u] = (!A.full && e < (rk + 1) * S && (e >> 2) < A.sel_stride) ? __ldg(plist + (e >> 2)) : -1;
     }
     ph_stamp<6>(0);
     if (mk == 0u) {   // empty C_tok (uniform over the cluster)
@@ -179,7 +181,7 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
 #pragma unroll
                 for (int u = 0; u < kTsU; ++u) {
                     const int e = r0 + threadIdx.x + NT * u;
-                    pg[u] = e < nitems ? __ldg(plist + (e >> 2)) : -1;
+                    pg[u] = e < nitems ? page_of(e >> 2) : -1;
                 }
             }
             float4 v[kTsU];
@@ -227,7 +229,82 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
         }
         return n;
     };
-    int ncand = extract(tau_lo, true, rk * S, (rk + 1) * S);
+    int ncand;
+    if (A.full) {
+        // full rows: k_candidates' chunk regions concatenated in chunk order (nch <= NT)
+        int ccnt = 0, tot = 0;
+        bool chunk_ovf = false;
+        if (threadIdx.x < A.nch) {
+            ccnt = A.ccount[(size_t)row * A.nch + threadIdx.x];
+            chunk_ovf = ccnt > kCpc;
+        }
+        const int coff = block_excl_scan<NT>(ccnt, shi, &tot);
+        chunk_ovf = __syncthreads_or(chunk_ovf);
+        const float *gs = A.cand_s + (size_t)row * A.nch * kCpc;
+        const int32_t *gj = A.cand_j + (size_t)row * A.nch * kCpc;
+        if (!chunk_ovf && tot > kTsCap) {
+            // too many for shared memory: fp64 Newton over the chunk regions (thread t <->
+            // chunk t) moves tau_lo just below tau, then an ordered re-extraction {z > tau_lo}
+            double t = tau_lo;
+            for (int it = 0; it < 200; ++it) {
+                double F = 0.0, Fd = 0.0;
+                if (threadIdx.x < A.nch) {
+                    const size_t g0 = (size_t)threadIdx.x * kCpc;
+                    for (int k = 0; k < ccnt; ++k) {
+                        const double d = a * (double)__ldg(gs + g0 + k) - t;
+                        if (d > 0.0) { F += powB<IB>(d, beta); Fd += powBm1<IB>(d, beta); }
+                    }
+                }
+                Rd.sum(F, Fd);
+                if (!(Fd > 0.0)) break;
+                const double step = lbeta_step(F, Fd, beta, IB);
+                t += step;
+                if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(t)))) break;
+            }
+            tau_lo = fmax(tau_lo, t - 1e-7 * fmax(1.0, fabs(t)));
+            int mine = 0;
+            if (threadIdx.x < A.nch) {
+                const size_t g0 = (size_t)threadIdx.x * kCpc;
+                for (int k = 0; k < ccnt; ++k) mine += a * (double)__ldg(gs + g0 + k) > tau_lo;
+            }
+            int tt;
+            int pos = block_excl_scan<NT>(mine, shi, &tt);
+            if (tt <= kTsCap) {
+                if (threadIdx.x < A.nch) {
+                    const size_t g0 = (size_t)threadIdx.x * kCpc;
+                    for (int k = 0; k < ccnt; ++k) {
+                        const float sj = __ldg(gs + g0 + k);
+                        if (a * (double)sj > tau_lo) {
+                            const int j = __ldg(gj + g0 + k);
+                            zs[pos] = sj; cj[pos] = j; cph[pos] = __ldg(ptab + j / kP);
+                            ++pos;
+                        }
+                    }
+                }
+                ncand = tt;
+            } else {
+                ncand = -1;
+            }
+        } else if (!chunk_ovf) {
+            __shared__ int s_off[256];
+            if (threadIdx.x < A.nch) s_off[threadIdx.x] = coff;
+            __syncthreads();
+            for (int e = threadIdx.x; e < tot; e += NT) {
+                int lo = 0, hi = A.nch - 1;                // last chunk with offset <= e
+                while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (s_off[mid] <= e) lo = mid; else hi = mid - 1; }
+                const size_t g = (size_t)lo * kCpc + (e - s_off[lo]);
+                const int j = __ldg(gj + g);
+                zs[e] = __ldg(gs + g);
+                cj[e] = j;
+                cph[e] = __ldg(ptab + j / kP);
+            }
+            ncand = tot;
+        } else {
+            ncand = -1;
+        }
+    } else {
+        ncand = extract(tau_lo, true, rk * S, (rk + 1) * S);
+    }
     if (CL > 1) {
         // merge: ranks publish their counts; if everything fits, ranks >= 1 store their
         // candidates into rank 0's arrays (rank order: deterministic) and leave
@@ -262,7 +339,7 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
         for (int it = 0; it < 200; ++it) {
             double F = 0.0, Fd = 0.0;
             for (int e = threadIdx.x; e < ntk; e += NT) {
-                const int j = __ldg(plist + e / kP) * kP + e % kP;
+                const int j = page_of(e / kP) * kP + e % kP;
                 if (j >= L) continue;
                 const double d = a * (double)srow[j] - t;
                 if (d > 0.0) { F += powB<IB>(d, beta); Fd += powBm1<IB>(d, beta); }
@@ -576,6 +653,13 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
     ph_stamp<6>(4);
     const double tau = s_tau, kk = s_kk;
 
+    if (A.no_pv) {                       // dense-V baseline: V is streamed by k_softmax_partial
+        if (threadIdx.x == 0) {
+            if (A.tau_out) A.tau_out[row] = tau;
+            if (A.supp_out) A.supp_out[row] = (int)kk;
+        }
+        return;
+    }
     // ---- 5. PV
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     double psum = 0.0;
@@ -655,6 +739,23 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
         if (A.tau_out) A.tau_out[row] = tau;
         if (A.supp_out) A.supp_out[row] = (int)kk;
     }
+    // eval list: support token positions and p_j in candidate order (exact delta / rho)
+    if (A.tok_list) {
+        int base = 0;
+        for (int r0 = 0; r0 < ncand; r0 += NT) {
+            const int k = r0 + threadIdx.x;
+            const bool keep = k < ncand && cin[k];
+            int tot;
+            const int pos = base + block_excl_scan<NT>(keep ? 1 : 0, shi, &tot);
+            if (keep && pos < A.list_cap) {
+                const double d = a * (double)zs[k] - tau;
+                A.tok_list[(size_t)row * A.list_cap + pos] = cj[k];
+                A.p_list[(size_t)row * A.list_cap + pos] = d > 0.0 ? powB<IB>(d, beta) : 0.0;
+            }
+            base += tot;
+        }
+        if (threadIdx.x == 0) A.n_list[row] = base;
+    }
     ph_stamp<6>(5);
 }
 
@@ -668,13 +769,17 @@ namespace ekv {
 // p_j = exp(s_j - s_max); chunk c of kSmxPages list pages -> acc[c][dv] = sum p_j v_j (fp32),
 // l[c] = sum p_j (fp64); k_softmax_combine adds the chunks in order (deterministic).
 constexpr int kSmxPages = 32;            // list pages per CTA (512 tokens)
+// The same split dense-V pass serves the dense-V full-cache entmax baseline (the
+// reference reads all scores and V): weights p_j = ((alpha-1) s_j - tau)_+^beta in fp64 from
+// the row's exact tau (ent_tau != NULL), every V row streamed whether p_j is zero or not.
 template <typename T>
 __global__ void __launch_bounds__(256) k_softmax_partial(CacheView c, const float *__restrict__ scores, size_t ntok,
                                                          const uint32_t *__restrict__ rowmax,
                                                          const int32_t *__restrict__ page_idx,
                                                          const int32_t *__restrict__ n_sel, int stride, int full,
                                                          int Hq, int G, int nch, float *__restrict__ pacc,
-                                                         double *__restrict__ pl, int32_t *__restrict__ pcnt) {
+                                                         double *__restrict__ pl, int32_t *__restrict__ pcnt,
+                                                         const double *__restrict__ ent_tau, float alpha) {
     __shared__ float red[8][kD];
     __shared__ double wl[8];
     __shared__ int wc[8];
@@ -702,7 +807,13 @@ __global__ void __launch_bounds__(256) k_softmax_partial(CacheView c, const floa
             for (int t = 0; t < kP; ++t) {
                 const float s = __shfl_sync(0xffffffffu, sv, t);
                 if (pg * kP + t >= L || s == -INFINITY) continue;        // warp-uniform
-                const float p = expf(s - smax);
+                float p;
+                if (ent_tau) {
+                    const double a = (double)alpha - 1.0, d = a * (double)s - ent_tau[row];
+                    p = d > 0.0 ? (float)pow(d, 1.0 / a) : 0.0f;
+                } else {
+                    p = expf(s - smax);
+                }
                 float vx[4];
                 ldv4<T>(vp + (size_t)t * kD, vx);
 #pragma unroll
@@ -746,7 +857,7 @@ __global__ void __launch_bounds__(128) k_softmax_combine(const float *__restrict
         cnt += pcnt[i];
     }
     out[(size_t)row * kD + threadIdx.x] = (mk && l > 0.0) ? (float)((double)o / l) : 0.0f;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {             // (entmax dense-V: tau / supp come from the tau kernel)
         if (tau) tau[row] = mk ? (double)key2f(mk) + log(l) : NAN;
         if (supp) supp[row] = cnt;
     }

@@ -207,12 +207,14 @@ def test_sparse_softmax_same_kernels(case):
 
 @pytest.mark.parametrize("case", CASES, ids=ids)
 @pytest.mark.parametrize("alpha", [1.5, 2.0, 1.25])
-def test_full_attend(case, alpha):
+@pytest.mark.parametrize("dense_v", [False, True])
+def test_full_attend(case, alpha, dense_v):
+    """a5: full-cache entmax, support-V and dense-V (every V row streamed)."""
     B, sl, Hq, Hkv, dt = case
     wl, dc, hc = make_pair(B, sl, Hq, Hkv, dtype=dt, seed=19)
     G = Hq // Hkv
     qh = q_host(wl)
-    out, tau, supp = ekv.full_attend(dc, wl.q.cuda(), ekv.attn_params(alpha))
+    out, tau, supp = ekv.full_attend(dc, wl.q.cuda(), ekv.attn_params(alpha, dense_v=dense_v))
     torch.cuda.synchronize()
     out, tau, supp = out.cpu().numpy(), tau.cpu().numpy(), supp.cpu().numpy()
     for b in range(B):

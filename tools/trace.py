@@ -17,7 +17,7 @@ k = int(sys.argv[3]) if len(sys.argv) > 3 else max(1, -(-M // 100))
 wl = make_workload(1, n, Hq, Hkv, seed=1, device=dev, spare_tokens=200)
 c = ekv.PagedCache.allocate_meta(wl.K, wl.V, wl.page_table, wl.seq_lens)
 ekv.rebuild_page_stats(c)
-sel = ekv.select_params(policy, k)
+sel = ekv.select_params('topk' if policy == 'full' else policy, k)
 attn = ekv.attn_params(1.5)
 ws = ekv.alloc_workspace(c, Hq, sel)
 st = ekv.DecodeStats(1, Hq, dev, delta_bar=True, gauss=policy == 'gauss')
@@ -28,7 +28,17 @@ L = ekv.lib()
 L.entmaxkv_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 
 
+if policy == 'full':
+    wsf = ekv.alloc_workspace(c, Hq, None)
+    fo = torch.empty(1, Hq, 128, dtype=torch.float32, device=dev)
+    ft = torch.empty(1, Hq, dtype=torch.float64, device=dev)
+    fs = torch.empty(1, Hq, dtype=torch.int32, device=dev)
+
+
 def step():
+    if policy == 'full':
+        ekv.full_attend(c, q, attn, workspace=wsf, out=fo, tau=ft, supp=fs, stream=s)
+        return
     ekv.append_kv(c, kn, vn, stream=s)
     ekv.decode(c, q, sel, attn, ws, out=out, stats=st, stream=s)
 
