@@ -313,6 +313,26 @@ ekv_status launch_tau_sparse(const CacheView &v, const TauArgs &A, int rows, cud
     }
 }
 
+template <typename T>
+ekv_status launch_dense_group(const CacheView &v, const float *scores, size_t ntok, const uint32_t *rowmax, int Hq,
+                              int nch, float *pacc, double *pl, int32_t *pc, const double *ent_tau, float alpha,
+                              cudaStream_t st) {
+    const int G = Hq / v.Hkv;
+    int ib = 0;
+    if (ent_tau) {
+        const double beta = 1.0 / ((double)alpha - 1.0);
+        ib = (std::fabs(beta - std::rint(beta)) < 1e-12 && beta <= 4.5) ? (int)std::rint(beta) : 0;
+    }
+    dim3 g(nch, v.B * v.Hkv);
+    switch (G) {
+    case 1: k_dense_group_partial<T, 1><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, Hq, nch, pacc, pl, pc, ent_tau, alpha, ib); break;
+    case 2: k_dense_group_partial<T, 2><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, Hq, nch, pacc, pl, pc, ent_tau, alpha, ib); break;
+    case 4: k_dense_group_partial<T, 4><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, Hq, nch, pacc, pl, pc, ent_tau, alpha, ib); break;
+    default: k_dense_group_partial<T, 8><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, Hq, nch, pacc, pl, pc, ent_tau, alpha, ib); break;
+    }
+    return check_launch("k_dense_group_partial");
+}
+
 ekv_status check_attn(const ekv_attn_params *a) {
     if (!a) return fail(EKV_ERR_INVALID_ARG, "attn params NULL");
     if (a->transform != EKV_ENTMAX && a->transform != EKV_SOFTMAX) return fail(EKV_ERR_INVALID_ARG, "bad transform");
@@ -381,13 +401,19 @@ ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t 
         float *pacc = at<float>(ws, L.smx_acc);
         double *pl = at<double>(ws, L.smx_l);
         int32_t *pc = at<int32_t>(ws, L.smx_cnt);
-        if (c->dtype == EKV_BF16)
-            k_softmax_partial<__nv_bfloat16><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, pi, ns, stride, full, Hq,
-                                                                 Hq / c->n_kv_heads, nch, pacc, pl, pc, nullptr, 0.f);
-        else
-            k_softmax_partial<float><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, pi, ns, stride, full, Hq,
-                                                        Hq / c->n_kv_heads, nch, pacc, pl, pc, nullptr, 0.f);
-        EKV_TRY(check_launch("k_softmax_partial"));
+        if (full) {
+            if (c->dtype == EKV_BF16)
+                EKV_TRY(launch_dense_group<__nv_bfloat16>(v, scores, ntok, rowmax, Hq, nch, pacc, pl, pc, nullptr, 0.f, st));
+            else EKV_TRY(launch_dense_group<float>(v, scores, ntok, rowmax, Hq, nch, pacc, pl, pc, nullptr, 0.f, st));
+        } else {
+            if (c->dtype == EKV_BF16)
+                k_softmax_partial<__nv_bfloat16><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, pi, ns, stride, full, Hq,
+                                                                     Hq / c->n_kv_heads, nch, pacc, pl, pc, nullptr, 0.f);
+            else
+                k_softmax_partial<float><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, pi, ns, stride, full, Hq,
+                                                            Hq / c->n_kv_heads, nch, pacc, pl, pc, nullptr, 0.f);
+            EKV_TRY(check_launch("k_softmax_partial"));
+        }
         k_softmax_combine<<<rows, 128, 0, st>>>(pacc, pl, pc, rowmax, nch, out, tau, supp);
         return check_launch("k_softmax_combine");
     }
@@ -405,14 +431,10 @@ ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t 
     float *pacc = at<float>(ws, L.smx_acc);
     double *pl = at<double>(ws, L.smx_l);
     int32_t *pc = at<int32_t>(ws, L.smx_cnt);
+    (void)g;
     if (c->dtype == EKV_BF16)
-        k_softmax_partial<__nv_bfloat16><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, pi, ns, stride, full, Hq,
-                                                             Hq / c->n_kv_heads, dch, pacc, pl, pc, A.tau_out,
-                                                             attn->alpha);
-    else
-        k_softmax_partial<float><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, pi, ns, stride, full, Hq,
-                                                    Hq / c->n_kv_heads, dch, pacc, pl, pc, A.tau_out, attn->alpha);
-    EKV_TRY(check_launch("k_softmax_partial"));
+        EKV_TRY(launch_dense_group<__nv_bfloat16>(v, scores, ntok, rowmax, Hq, dch, pacc, pl, pc, A.tau_out, attn->alpha, st));
+    else EKV_TRY(launch_dense_group<float>(v, scores, ntok, rowmax, Hq, dch, pacc, pl, pc, A.tau_out, attn->alpha, st));
     k_softmax_combine<<<rows, 128, 0, st>>>(pacc, pl, pc, rowmax, dch, out, nullptr, nullptr);
     return check_launch("k_softmax_combine");
 }
