@@ -863,3 +863,107 @@ __global__ void __launch_bounds__(128) k_softmax_combine(const float *__restrict
     }
 }
 }  // namespace ekv
+
+namespace ekv {
+// Full rows (every page, every head of the group): one CTA per (chunk, KV unit) streams each
+// V row ONCE for the G heads of the group (weights from the G score rows): softmax p =
+// exp(s - s_max), entmax p = ((alpha-1) s - tau)_+^beta with integer beta by products.
+// Writes the same per-(row, chunk) partials as k_softmax_partial.
+template <typename T, int G>
+__global__ void __launch_bounds__(256) k_dense_group_partial(CacheView c, const float *__restrict__ scores, size_t ntok,
+                                                             const uint32_t *__restrict__ rowmax, int Hq, int nch,
+                                                             float *__restrict__ pacc, double *__restrict__ pl,
+                                                             int32_t *__restrict__ pcnt,
+                                                             const double *__restrict__ ent_tau, float alpha, int ib) {
+    __shared__ float red[8][kD];
+    __shared__ double wl[8][G];
+    __shared__ int wc[8];
+    const int unit = blockIdx.y, ch = blockIdx.x;
+    const int b = unit / c.Hkv, kvh = unit % c.Hkv;
+    const int row0 = b * Hq + kvh * G;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int L = __ldg(c.seq_lens + b);
+    const int nlist = n_pages_of(L);
+    const double a = (double)alpha - 1.0;
+    float smax[G];
+    double tau[G];
+    bool live[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const uint32_t mk = __ldg(rowmax + row0 + g);
+        live[g] = mk != 0u;
+        smax[g] = mk ? key2f(mk) : 0.f;
+        tau[g] = ent_tau ? ent_tau[row0 + g] : 0.0;
+    }
+    const T *Vb = reinterpret_cast<const T *>(c.V);
+    float acc[G][4];
+    double l[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) { l[g] = 0.0; acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f; }
+    int cnt = 0;
+    const int i0 = ch * kSmxPages;
+    for (int pg = i0 + warp; pg < min(nlist, i0 + kSmxPages); pg += 8) {
+        const int phys = __ldg(c.page_table + (size_t)b * c.maxp + pg);
+        float sv[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) sv[g] = (lane < kP) ? scores[(size_t)(row0 + g) * ntok + (size_t)pg * kP + lane] : -INFINITY;
+        const T *vp = Vb + ((size_t)phys * c.Hkv + kvh) * kP * kD + 4 * lane;
+#pragma unroll 2
+        for (int t = 0; t < kP; ++t) {
+            if (pg * kP + t >= L) break;                                   // warp-uniform
+            float vx[4];
+            ldv4<T>(vp + (size_t)t * kD, vx);                               // every V row is read
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const float s = __shfl_sync(0xffffffffu, sv[g], t);
+                if (!live[g] || s == -INFINITY) continue;
+                float p;
+                if (ent_tau) {
+                    const double d = a * (double)s - tau[g];
+                    double w = 0.0;
+                    if (d > 0.0) {
+                        if (ib == 1) w = d;
+                        else if (ib == 2) w = d * d;
+                        else if (ib == 3) w = d * d * d;
+                        else if (ib == 4) { const double d2 = d * d; w = d2 * d2; }
+                        else w = pow(d, 1.0 / a);
+                    }
+                    p = (float)w;
+                    if (lane == 0) l[g] += w;
+                } else {
+                    p = expf(s - smax[g]);
+                    if (lane == 0) l[g] += (double)p;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[g][q] = __fmaf_rn(p, vx[q], acc[g][q]);
+            }
+            if (lane == 0) ++cnt;
+        }
+    }
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) red[warp][4 * lane + q] = acc[g][q];
+        if (lane == 0) wl[warp][g] = l[g];
+        __syncthreads();
+        const size_t o = (size_t)(row0 + g) * nch + ch;
+        if (threadIdx.x < kD) {
+            float sacc = 0.f;
+            for (int w = 0; w < 8; ++w) sacc = __fadd_rn(sacc, red[w][threadIdx.x]);
+            pacc[o * kD + threadIdx.x] = sacc;
+        }
+        if (threadIdx.x == 0) {
+            double sl = 0.0;
+            for (int w = 0; w < 8; ++w) sl += wl[w][g];
+            pl[o] = sl;
+        }
+        __syncthreads();
+    }
+    if (lane == 0) wc[warp] = cnt;
+    __syncthreads();
+    if (threadIdx.x < G) {
+        int sc = 0;
+        for (int w = 0; w < 8; ++w) sc += wc[w];
+        pcnt[(size_t)(row0 + threadIdx.x) * nch + ch] = sc;
+    }
+}
+}  // namespace ekv
