@@ -408,6 +408,9 @@ def main():
             "speedup_vs_full_entmax": (full_dense_us / us_step) if full_dense_us else None,
             "full_entmax_support_v_us": full_us,
             "speedup_vs_full_entmax_support_v": (full_us / us_step) if full_us else None,
+            # the dense-V baseline's own floor: all K + all V bytes at the HBM peak
+            "full_entmax_dense_v_roofline_us": full_bytes / (peak * 1e3),
+            "speedup_vs_full_entmax_roofline": full_bytes / (peak * 1e3) / us_step,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_us, "unit": "us", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches_per_step * args.steps,

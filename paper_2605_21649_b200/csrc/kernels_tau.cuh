@@ -865,12 +865,17 @@ __global__ void __launch_bounds__(128) k_softmax_combine(const float *__restrict
 }  // namespace ekv
 
 namespace ekv {
+// 8 dims of one V row (lane chunk c) -> fp32
+template <typename T> __device__ __forceinline__ void ldv8(const T *p, float (&x)[8]) { Elem<T>::load8(p, x); }
+
 // Full rows (every page, every head of the group): one CTA per (chunk, KV unit) streams each
 // V row ONCE for the G heads of the group (weights from the G score rows): softmax p =
 // exp(s - s_max), entmax p = ((alpha-1) s - tau)_+^beta with integer beta by products.
+// Layout for memory-level parallelism: a warp takes a page; lane = (token parity h, 8-dim
+// chunk c): its 8 loads of 16 bytes (tokens 2 i + h) go out together, then the weights.
 // Writes the same per-(row, chunk) partials as k_softmax_partial.
 template <typename T, int G>
-__global__ void __launch_bounds__(256) k_dense_group_partial(CacheView c, const float *__restrict__ scores, size_t ntok,
+__global__ void __launch_bounds__(256, 2) k_dense_group_partial(CacheView c, const float *__restrict__ scores, size_t ntok,
                                                              const uint32_t *__restrict__ rowmax, int Hq, int nch,
                                                              float *__restrict__ pacc, double *__restrict__ pl,
                                                              int32_t *__restrict__ pcnt,
@@ -882,6 +887,7 @@ __global__ void __launch_bounds__(256) k_dense_group_partial(CacheView c, const 
     const int b = unit / c.Hkv, kvh = unit % c.Hkv;
     const int row0 = b * Hq + kvh * G;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int hpar = lane >> 4, cdim = lane & 15;
     const int L = __ldg(c.seq_lens + b);
     const int nlist = n_pages_of(L);
     const double a = (double)alpha - 1.0;
@@ -896,53 +902,87 @@ __global__ void __launch_bounds__(256) k_dense_group_partial(CacheView c, const 
         tau[g] = ent_tau ? ent_tau[row0 + g] : 0.0;
     }
     const T *Vb = reinterpret_cast<const T *>(c.V);
-    float acc[G][4];
+    float acc[G][8];
     double l[G];
 #pragma unroll
-    for (int g = 0; g < G; ++g) { l[g] = 0.0; acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f; }
+    for (int g = 0; g < G; ++g) {
+        l[g] = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[g][i] = 0.f;
+    }
     int cnt = 0;
     const int i0 = ch * kSmxPages;
     for (int pg = i0 + warp; pg < min(nlist, i0 + kSmxPages); pg += 8) {
         const int phys = __ldg(c.page_table + (size_t)b * c.maxp + pg);
+        const int nt = min(kP, L - pg * kP);
         float sv[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) sv[g] = (lane < kP) ? scores[(size_t)(row0 + g) * ntok + (size_t)pg * kP + lane] : -INFINITY;
-        const T *vp = Vb + ((size_t)phys * c.Hkv + kvh) * kP * kD + 4 * lane;
-#pragma unroll 2
-        for (int t = 0; t < kP; ++t) {
-            if (pg * kP + t >= L) break;                                   // warp-uniform
-            float vx[4];
-            ldv4<T>(vp + (size_t)t * kD, vx);                               // every V row is read
+        const T *vp = Vb + ((size_t)phys * c.Hkv + kvh) * kP * kD + 8 * cdim;
+        // raw 16-byte words in flight (bf16: 8 dims; fp32: 4 dims, two words per row)
+        constexpr int WPR = sizeof(T) == 2 ? 1 : 2;
+        uint4 raw[kP / 2][WPR];
+#pragma unroll
+        for (int i = 0; i < kP / 2; ++i) {                                  // every V row is read
+            const int t = 2 * i + hpar;
+#pragma unroll
+            for (int w = 0; w < WPR; ++w)
+                raw[i][w] = (t < nt) ? __ldg(reinterpret_cast<const uint4 *>(vp + (size_t)t * kD) + w) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int i = 0; i < kP / 2; ++i) {
+            const int t = 2 * i + hpar;
+            float vx[1][8];
+            if constexpr (sizeof(T) == 2) {
+                vx[0][0] = bf_lo(raw[i][0].x); vx[0][1] = bf_hi(raw[i][0].x); vx[0][2] = bf_lo(raw[i][0].y);
+                vx[0][3] = bf_hi(raw[i][0].y); vx[0][4] = bf_lo(raw[i][0].z); vx[0][5] = bf_hi(raw[i][0].z);
+                vx[0][6] = bf_lo(raw[i][0].w); vx[0][7] = bf_hi(raw[i][0].w);
+            } else {
+                const uint4 r0 = raw[i][0], r1 = raw[i][WPR - 1];
+                vx[0][0] = __uint_as_float(r0.x); vx[0][1] = __uint_as_float(r0.y); vx[0][2] = __uint_as_float(r0.z);
+                vx[0][3] = __uint_as_float(r0.w); vx[0][4] = __uint_as_float(r1.x); vx[0][5] = __uint_as_float(r1.y);
+                vx[0][6] = __uint_as_float(r1.z); vx[0][7] = __uint_as_float(r1.w);
+            }
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 const float s = __shfl_sync(0xffffffffu, sv[g], t);
-                if (!live[g] || s == -INFINITY) continue;
-                float p;
-                if (ent_tau) {
-                    const double d = a * (double)s - tau[g];
-                    double w = 0.0;
-                    if (d > 0.0) {
-                        if (ib == 1) w = d;
-                        else if (ib == 2) w = d * d;
-                        else if (ib == 3) w = d * d * d;
-                        else if (ib == 4) { const double d2 = d * d; w = d2 * d2; }
-                        else w = pow(d, 1.0 / a);
+                float p = 0.f;
+                double w = 0.0;
+                if (live[g] && t < nt && s != -INFINITY) {
+                    if (ent_tau) {
+                        const double d = a * (double)s - tau[g];
+                        if (d > 0.0) {
+                            if (ib == 1) w = d;
+                            else if (ib == 2) w = d * d;
+                            else if (ib == 3) w = d * d * d;
+                            else if (ib == 4) { const double d2 = d * d; w = d2 * d2; }
+                            else w = pow(d, 1.0 / a);
+                        }
+                        p = (float)w;
+                    } else {
+                        p = expf(s - smax[g]);
+                        w = (double)p;
                     }
-                    p = (float)w;
-                    if (lane == 0) l[g] += w;
-                } else {
-                    p = expf(s - smax[g]);
-                    if (lane == 0) l[g] += (double)p;
                 }
+                if (cdim == 0) l[g] += w;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) acc[g][q] = __fmaf_rn(p, vx[q], acc[g][q]);
+                for (int e = 0; e < 8; ++e) acc[g][e] = __fmaf_rn(p, vx[0][e], acc[g][e]);
             }
-            if (lane == 0) ++cnt;
         }
+        if (lane == 0) cnt += nt;
     }
+    // fold the two token parities (lanes c and c + 16), then the warps in fixed order
+#pragma unroll
     for (int g = 0; g < G; ++g) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) red[warp][4 * lane + q] = acc[g][q];
+        for (int e = 0; e < 8; ++e) acc[g][e] = __fadd_rn(acc[g][e], __shfl_xor_sync(0xffffffffu, acc[g][e], 16));
+        l[g] += __shfl_xor_sync(0xffffffffu, l[g], 16);
+    }
+    for (int g = 0; g < G; ++g) {
+        if (lane < 16) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) red[warp][8 * cdim + e] = acc[g][e];
+        }
         if (lane == 0) wl[warp][g] = l[g];
         __syncthreads();
         const size_t o = (size_t)(row0 + g) * nch + ch;
