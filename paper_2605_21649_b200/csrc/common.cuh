@@ -349,6 +349,22 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 }
 }  // namespace ekv
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Kernels of the decode chain are launched with programmatic stream serialisation: a kernel
+// lets its successor be scheduled early (launch_dependents) and waits for its predecessor's
+// completion and memory (wait) before touching anything the predecessor wrote.  Both are
+// no-ops when the launch carries no programmatic dependency.
+namespace ekv {
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+// zero a byte range (16-byte aligned, multiple of 16) -- replaces a memset node in the chain
+__global__ void __launch_bounds__(256) k_zero(uint4 *p, size_t n16) {
+    pdl_launch();
+    pdl_wait();
+    for (size_t i = blockIdx.x * 256 + threadIdx.x; i < n16; i += (size_t)gridDim.x * 256) p[i] = make_uint4(0, 0, 0, 0);
+}
+}  // namespace ekv
+
 // ---------------------------------------------------------------- optional in-kernel phase stamps
 // Built with -DEKV_STAMPS: block 0 / thread 0 of an instrumented kernel writes %globaltimer
 // (ns) at checkpoints into ekv_stamps[kernel_slot][i]; read with entmaxkv_debug_stamps().

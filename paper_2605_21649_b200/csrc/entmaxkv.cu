@@ -6,6 +6,8 @@
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
+#include <stdlib.h>
+#include <utility>
 
 #include "entmaxkv.h"
 #include "common.cuh"
@@ -35,6 +37,42 @@ ekv_status check_launch(const char *what) {
     if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
     ++g_launches;
     return EKV_OK;
+}
+
+// Launch with programmatic stream serialisation (PDL; EKV_NO_PDL=1 disables it) and an
+// optional thread-block cluster.  Every kernel of the decode chain starts with
+// griddepcontrol.launch_dependents / wait, so the next launch overlaps this one's tail.
+bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) { const char *e = getenv("EKV_NO_PDL"); v = (e && e[0] == '1') ? 0 : 1; }
+    return v == 1;
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, unsigned cluster,
+                      Args &&...args) {
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (cluster) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = cluster;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 #define EKV_TRY(x)                       \
@@ -186,7 +224,7 @@ void score_go(const CacheView &v, const T *q, int Hq, float *box, float *mu, flo
     long long gx = ((long long)v.B * v.maxp + 7) / 8;
     if (gx > per_sm * num_sms()) gx = per_sm * num_sms();
     if (gx < 1) gx = 1;
-    k_score<T, G, MODES><<<(unsigned)gx, 288, smem, st>>>(v, q, Hq, box, mu, s2);
+    launch_ex(k_score<T, G, MODES>, dim3((unsigned)gx), dim3(288), smem, st, 0, v, q, Hq, box, mu, s2);
 }
 template <typename T, int G>
 ekv_status launch_score_t(const CacheView &v, const void *q, int Hq, int modes, float *box, float *mu, float *s2,
@@ -218,27 +256,15 @@ ekv_status launch_topk(const float *box, int B, int Hq, int maxp, const int32_t 
     int CL = 1;
     while (CL * kTkPerCta < maxp) CL *= 2;
     if (CL > 8) return fail(EKV_ERR_UNSUPPORTED, "top-k supports at most %d pages", 8 * kTkPerCta);
-    cudaLaunchConfig_t cfg;
-    memset(&cfg, 0, sizeof(cfg));
-    cfg.gridDim = dim3((unsigned)(B * Hq * CL));
-    cfg.blockDim = dim3(kTkNT);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_topk, box, Hq, maxp, sl, k, pi, ns, stride, G, u.umask, u.W);
+    cudaError_t e = launch_ex(k_topk, dim3((unsigned)(B * Hq * CL)), dim3(kTkNT), 0, st, (unsigned)CL, box, Hq, maxp, sl, k,
+                              pi, ns, stride, G, u.umask, u.W);
     if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "k_topk: %s", cudaGetErrorString(e));
     return check_launch("k_topk");
 }
 
 ekv_status launch_mark(const ekv_cache *c, int Hq, const int32_t *pi, const int32_t *ns, int stride, uint32_t *um,
                        int W, cudaStream_t st) {
-    k_mark<<<c->batch * Hq, 256, 0, st>>>(Hq, Hq / c->n_kv_heads, pi, ns, stride, um, W);
+    launch_ex(k_mark, dim3(c->batch * Hq), dim3(256), 0, st, 0, Hq, Hq / c->n_kv_heads, pi, ns, stride, um, W);
     return check_launch("k_mark");
 }
 
@@ -255,8 +281,8 @@ ekv_status launch_scores_t(const CacheView &v, const void *q, int Hq, const uint
     long long gx = (slots + 31) / 32;                                // >= 32 work slots per CTA
     if (gx > per_sm * num_sms()) gx = per_sm * num_sms();
     if (gx < 1) gx = 1;
-    k_attend_scores<T, G><<<(unsigned)gx, 32 * (AttCfg<T>::NCW + 1), smem, st>>>(v, static_cast<const T *>(q), Hq, um, W, pi, ns, stride,
-                                                           scores, rowmax, full);
+    launch_ex(k_attend_scores<T, G>, dim3((unsigned)gx), dim3(32 * (AttCfg<T>::NCW + 1)), smem, st, 0, v,
+              static_cast<const T *>(q), Hq, um, W, pi, ns, stride, scores, rowmax, full);
     return check_launch("k_attend_scores");
 }
 template <typename T>
@@ -282,20 +308,7 @@ ekv_status launch_tau_sparse_ib(const CacheView &v, const TauArgs &A, int rows, 
     // a cluster of up to 4 CTAs per row splits the candidate extraction (page-list reads are
     // latency bound per SM); rank 0 then finishes the row
     const int CL = A.full ? 1 : A.sel_stride > 384 ? 4 : A.sel_stride > 128 ? 2 : 1;
-    cudaLaunchConfig_t cfg;
-    memset(&cfg, 0, sizeof(cfg));
-    cfg.gridDim = dim3((unsigned)(rows * CL));
-    cfg.blockDim = dim3(kTsNT);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_tau_sparse<T, IB>, v, A);
+    cudaError_t e = launch_ex(k_tau_sparse<T, IB>, dim3((unsigned)(rows * CL)), dim3(kTsNT), smem, st, (unsigned)CL, v, A);
     if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "k_tau_sparse: %s", cudaGetErrorString(e));
     return check_launch("k_tau_sparse");
 }
@@ -558,11 +571,11 @@ ekv_status entmaxkv_append_kv(const ekv_cache *cache, const void *k_new, const v
     int nt = cache->n_kv_heads * kD;
     if (nt > 1024) nt = 1024;
     if (cache->dtype == EKV_BF16)
-        k_append<__nv_bfloat16><<<cache->batch, nt, 0, st>>>(v, static_cast<const __nv_bfloat16 *>(k_new),
-                                                             static_cast<const __nv_bfloat16 *>(v_new), n_tokens);
+        launch_ex(k_append<__nv_bfloat16>, dim3(cache->batch), dim3(nt), 0, st, 0, v,
+                  static_cast<const __nv_bfloat16 *>(k_new), static_cast<const __nv_bfloat16 *>(v_new), n_tokens);
     else
-        k_append<float><<<cache->batch, nt, 0, st>>>(v, static_cast<const float *>(k_new),
-                                                     static_cast<const float *>(v_new), n_tokens);
+        launch_ex(k_append<float>, dim3(cache->batch), dim3(nt), 0, st, 0, v, static_cast<const float *>(k_new),
+                  static_cast<const float *>(v_new), n_tokens);
     return check_launch("k_append");
 }
 
@@ -676,9 +689,14 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
     int32_t *ns = at<int32_t>(workspace, L.n_sel);
     double *th = at<double>(workspace, L.tau_hat);
     const bool want_db = stats && stats->delta_bar && attn->transform == EKV_ENTMAX;
-    // zero the per-step counters / union mask once; the selection kernel merges the union
-    if (cudaMemsetAsync(at<char>(workspace, L.zero), 0, L.zero_bytes, st) != cudaSuccess)
-        return fail(EKV_ERR_CUDA, "memset: %s", cudaGetErrorString(cudaGetLastError()));
+    // zero the per-step counters / union mask once (a kernel, so the PDL chain is unbroken);
+    // the selection kernel merges the union
+    {
+        const size_t n16 = L.zero_bytes / 16;
+        launch_ex(k_zero, dim3((unsigned)std::min<size_t>(148, (n16 + 255) / 256)), dim3(256), 0, st, 0,
+                  at<uint4>(workspace, L.zero), n16);
+        EKV_TRY(check_launch("k_zero"));
+    }
     const int Gq = n_q_heads / cache->n_kv_heads;
     const UnionOut uo{at<uint32_t>(workspace, L.umask), L.W};
     // a1: page scores (box for top-k and for the certificate; mu/sigma2 for Gaussian)
@@ -695,7 +713,7 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
         const int k = sel->policy == EKV_TOPK ? sel->k_pages : maxp;
         EKV_TRY(launch_topk(box, cache->batch, n_q_heads, maxp, cache->seq_lens, k, pi, ns, L.cap, Gq, uo, st));
     } else {
-        k_gauss_select<1024><<<cache->batch * n_q_heads, 1024, 0, st>>>(mu, s2, n_q_heads, maxp, cache->seq_lens,
+        launch_ex(k_gauss_select<1024>, dim3(cache->batch * n_q_heads), dim3(1024), 0, st, 0, (const float *)mu, (const float *)s2, n_q_heads, maxp, (const int32_t *)cache->seq_lens,
                                                                       attn->alpha, sel->margin, sel->q_page, pi, ns,
                                                                       L.cap, th);
         EKV_TRY(check_launch("k_gauss_select"));
@@ -714,25 +732,14 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
         kc.beta = 1.0 / kc.a;
         kc.inv_a = kc.beta;
         kc.ib = (std::fabs(kc.beta - std::rint(kc.beta)) < 1e-12 && kc.beta <= 4.5) ? (int)std::rint(kc.beta) : 0;
-        cudaLaunchConfig_t cfg;
-        memset(&cfg, 0, sizeof(cfg));
-        cfg.gridDim = dim3((unsigned)nch, (unsigned)rows);
-        cfg.blockDim = dim3(256);
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = (unsigned)nch;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        const dim3 dg((unsigned)nch, (unsigned)rows), db(256);
         cudaError_t ce;
         switch (kc.ib) {
-        case 1: ce = cudaLaunchKernelEx(&cfg, k_delta_bar<1>, (const float *)box, maxp, (const int32_t *)cache->seq_lens, n_q_heads, Gq, (const uint32_t *)uo.umask, L.W, (const double *)tau_p, kc, stats->delta_bar); break;
-        case 2: ce = cudaLaunchKernelEx(&cfg, k_delta_bar<2>, (const float *)box, maxp, (const int32_t *)cache->seq_lens, n_q_heads, Gq, (const uint32_t *)uo.umask, L.W, (const double *)tau_p, kc, stats->delta_bar); break;
-        case 3: ce = cudaLaunchKernelEx(&cfg, k_delta_bar<3>, (const float *)box, maxp, (const int32_t *)cache->seq_lens, n_q_heads, Gq, (const uint32_t *)uo.umask, L.W, (const double *)tau_p, kc, stats->delta_bar); break;
-        case 4: ce = cudaLaunchKernelEx(&cfg, k_delta_bar<4>, (const float *)box, maxp, (const int32_t *)cache->seq_lens, n_q_heads, Gq, (const uint32_t *)uo.umask, L.W, (const double *)tau_p, kc, stats->delta_bar); break;
-        default: ce = cudaLaunchKernelEx(&cfg, k_delta_bar<0>, (const float *)box, maxp, (const int32_t *)cache->seq_lens, n_q_heads, Gq, (const uint32_t *)uo.umask, L.W, (const double *)tau_p, kc, stats->delta_bar); break;
+        case 1: ce = launch_ex(k_delta_bar<1>, dg, db, 0, st, (unsigned)nch, (const float *)box, maxp, (const int32_t *)cache->seq_lens, n_q_heads, Gq, (const uint32_t *)uo.umask, L.W, (const double *)tau_p, kc, stats->delta_bar); break;
+        case 2: ce = launch_ex(k_delta_bar<2>, dg, db, 0, st, (unsigned)nch, (const float *)box, maxp, (const int32_t *)cache->seq_lens, n_q_heads, Gq, (const uint32_t *)uo.umask, L.W, (const double *)tau_p, kc, stats->delta_bar); break;
+        case 3: ce = launch_ex(k_delta_bar<3>, dg, db, 0, st, (unsigned)nch, (const float *)box, maxp, (const int32_t *)cache->seq_lens, n_q_heads, Gq, (const uint32_t *)uo.umask, L.W, (const double *)tau_p, kc, stats->delta_bar); break;
+        case 4: ce = launch_ex(k_delta_bar<4>, dg, db, 0, st, (unsigned)nch, (const float *)box, maxp, (const int32_t *)cache->seq_lens, n_q_heads, Gq, (const uint32_t *)uo.umask, L.W, (const double *)tau_p, kc, stats->delta_bar); break;
+        default: ce = launch_ex(k_delta_bar<0>, dg, db, 0, st, (unsigned)nch, (const float *)box, maxp, (const int32_t *)cache->seq_lens, n_q_heads, Gq, (const uint32_t *)uo.umask, L.W, (const double *)tau_p, kc, stats->delta_bar); break;
         }
         if (ce != cudaSuccess) return fail(EKV_ERR_CUDA, "k_delta_bar: %s", cudaGetErrorString(ce));
         EKV_TRY(check_launch("k_delta_bar"));

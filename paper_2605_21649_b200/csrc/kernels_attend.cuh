@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
     const int32_t *__restrict__ page_idx, const int32_t *__restrict__ n_sel, int stride,
     float *__restrict__ scores, uint32_t *__restrict__ rowmax, int full) {
     EKV_TRACE(4);
+    pdl_wait();
     constexpr int SP = AttCfg<T>::SP, NS = AttCfg<T>::NS, TILE = AttCfg<T>::TILE;
     constexpr int NCW = AttCfg<T>::NCW;
     constexpr int CHK = 256;                // work slots per producer chunk (8 per lane)
@@ -342,6 +343,7 @@ __global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ sc
                                                     int *__restrict__ ccount, float *__restrict__ cand_s,
                                                     int32_t *__restrict__ cand_j) {
     EKV_TRACE(5);
+    pdl_wait();
     __shared__ int sh[9];
     const int row = blockIdx.y;
     const int b = row / Hq;
@@ -496,6 +498,7 @@ __global__ void __launch_bounds__(256) k_delta_bar(const float *__restrict__ box
                                                    const double *__restrict__ tau, DbConst k,
                                                    double *__restrict__ out) {
     EKV_TRACE(7);
+    pdl_wait();
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     constexpr int R = kDbChunk / 1024;

@@ -15,6 +15,7 @@ template <typename T>
 __global__ void __launch_bounds__(1024, 1) k_append(CacheView c, const T *__restrict__ k_new,
                                                  const T *__restrict__ v_new, int n_tokens) {
     EKV_TRACE(0);
+    pdl_wait();
     const int b = blockIdx.x;
     const int L = c.seq_lens[b];
     T *K = reinterpret_cast<T *>(c.Kw);
@@ -129,6 +130,7 @@ __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(C
                                                    float *__restrict__ box, float *__restrict__ mu,
                                                    float *__restrict__ sigma2) {
     EKV_TRACE(1);
+    pdl_wait();
     constexpr int SP = ScoreCfg<MODES>::SP, NS = ScoreCfg<MODES>::NS;
     constexpr int NCW = 8;
     extern __shared__ __align__(128) unsigned char smem[];

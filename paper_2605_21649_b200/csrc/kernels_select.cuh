@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
                                                 int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
                                                 int sel_stride, int G, uint32_t *__restrict__ umask, int W) {
     EKV_TRACE(2);
+    pdl_wait();
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     const int CL = (int)cl.num_blocks(), r = (int)cl.block_rank();
@@ -266,6 +267,7 @@ __global__ void __launch_bounds__(256) k_mark(int Hq, int G, const int32_t *__re
                                               const int32_t *__restrict__ n_sel, int sel_stride,
                                               uint32_t *__restrict__ umask, int W) {
     EKV_TRACE(3);
+    pdl_wait();
     const int row = blockIdx.x;
     const int b = row / Hq, h = row % Hq;
     const int unit = b * (Hq / G) + h / G, g = h % G;
@@ -358,6 +360,7 @@ __global__ void __launch_bounds__(NT) k_gauss_select(const float *__restrict__ m
                                                      int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
                                                      int sel_stride, double *__restrict__ tau_hat_out) {
     EKV_TRACE(8);
+    pdl_wait();
     __shared__ double shd[2 * (NT / 32) + 2];
     __shared__ int shi[NT / 32 + 1];
     __shared__ float shf[NT / 32 + 1];

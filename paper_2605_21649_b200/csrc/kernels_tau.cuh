@@ -108,6 +108,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <typename T, int IB>
 __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A) {
     EKV_TRACE(6);
+    pdl_wait();
     constexpr int NT = kTsNT, NW = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     float *zs = reinterpret_cast<float *>(smem);                           // raw scores s
@@ -780,6 +781,7 @@ __global__ void __launch_bounds__(256) k_softmax_partial(CacheView c, const floa
                                                          int Hq, int G, int nch, float *__restrict__ pacc,
                                                          double *__restrict__ pl, int32_t *__restrict__ pcnt,
                                                          const double *__restrict__ ent_tau, float alpha) {
+    pdl_wait();
     __shared__ float red[8][kD];
     __shared__ double wl[8];
     __shared__ int wc[8];
@@ -845,6 +847,7 @@ __global__ void __launch_bounds__(128) k_softmax_combine(const float *__restrict
                                                          const int32_t *__restrict__ pcnt, const uint32_t *__restrict__ rowmax,
                                                          int nch, float *__restrict__ out, double *__restrict__ tau,
                                                          int32_t *__restrict__ supp) {
+    pdl_wait();
     const int row = blockIdx.x;
     const uint32_t mk = rowmax[row];
     float o = 0.f;
@@ -880,6 +883,7 @@ __global__ void __launch_bounds__(256, 2) k_dense_group_partial(CacheView c, con
                                                              float *__restrict__ pacc, double *__restrict__ pl,
                                                              int32_t *__restrict__ pcnt,
                                                              const double *__restrict__ ent_tau, float alpha, int ib) {
+    pdl_wait();
     __shared__ float red[8][kD];
     __shared__ double wl[8][G];
     __shared__ int wc[8];
