@@ -47,6 +47,24 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic(kernel_prefix):
+    """dram__bytes_read.sum + dram__bytes_write.sum (bytes) of one launch of the kernel, from the
+    newest committed ncu --set full capture summary (profiles/r*_ncu_full_top_kernels.json)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_top_kernels.json")))
+    if not files:
+        return None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    try:
+        for k in json.load(open(files[-1])):
+            if k["Kernel Name"][0].split("(")[0].replace("void ", "").startswith(kernel_prefix):
+                rd, wr = k["dram__bytes_read.sum"], k["dram__bytes_write.sum"]
+                return float(rd[0]) * scale[rd[1]] + float(wr[0]) * scale[wr[1]]
+    except Exception:
+        return None
+    return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -397,7 +415,7 @@ def main():
                        "l2": "inputs larger than L2 (K/V 4 GiB, metadata 1.5 GiB per GPU)",
                        "parallelism": f"batch-sharded x{world} (one sequence per GPU, no collective)"},
             "roofline": {"bound": "hbm", "kernel": "score_pages (k_score)", "achieved": score_gbs, "peak": peak,
-                         "unit": "GB/s", "frac": score_gbs / peak, "traffic": None, "peak_kind": peak_kind,
+                         "unit": "GB/s", "frac": score_gbs / peak, "traffic": ncu_traffic("k_score"), "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": meta_bytes},
             "phases_us": phases,
             "step_bytes": step_bytes, "step_gbs": step_bytes / (us_step * 1e-6) / 1e9,

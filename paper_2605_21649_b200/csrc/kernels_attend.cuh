@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
                 pg[r] = 0;
                 if (cb + r * 32 + lane < f1) {
                     if (full) { pg[r] = sl; ok[r] = sl < n_pages_of(__ldg(c.seq_lens + bb)); }
-                    else if (sl < __ldg(n_sel + u)) { pg[r] = __ldg(page_idx + (size_t)u * stride + sl); ok[r] = true; }
+                    else if (bal || sl < __ldg(n_sel + u)) { pg[r] = __ldg(page_idx + (size_t)u * stride + sl); ok[r] = true; }
                 }
             }
             cs += CHK;

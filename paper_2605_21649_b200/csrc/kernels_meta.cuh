@@ -158,13 +158,16 @@ __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(C
         int si = 0;
         // (b, page) of the chunk start, advanced incrementally (no 64-bit divisions in the loop)
         int cb_b = (int)(r0 / c.maxp), cb_p = (int)(r0 % c.maxp);
-        for (long long cb = r0; cb < r1; cb += 512) {
-            const int nchk = (int)min((long long)512, r1 - cb);
+        // the first chunk is short (64 slots: the first copies go out after one round trip);
+        // page-table entry and sequence length are loaded together and masked afterwards
+        for (long long cb = r0; cb < r1;) {
+            const int nchk = (int)min((long long)(cb == r0 ? 64 : 512), r1 - cb);
 #pragma unroll 4
             for (int i = lane; i < nchk; i += 32) {
                 int bb = cb_b, p = cb_p + i;
                 while (p >= c.maxp) { p -= c.maxp; ++bb; }
-                l_phys[i] = (p < n_pages_of(__ldg(c.seq_lens + bb))) ? __ldg(c.page_table + (size_t)bb * c.maxp + p) : -1;
+                const int ph = __ldg(c.page_table + (size_t)bb * c.maxp + p);
+                l_phys[i] = (p < n_pages_of(__ldg(c.seq_lens + bb))) ? ph : -1;
             }
             __syncwarp();
             {
@@ -209,6 +212,7 @@ __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(C
                 }
             }
             __syncwarp();
+            cb += nchk;
             cb_p += nchk;
             while (cb_p >= c.maxp) { cb_p -= c.maxp; ++cb_b; }
         }
