@@ -372,17 +372,29 @@ def main():
     oh = torch.empty(1, Hq, d, dtype=torch.float32).pin_memory()
     qd, kd, vd = torch.empty_like(q), torch.empty_like(kn), torch.empty_like(vn)
     e2e_steps = max(5, args.steps // 2)
+
+    def e2e_step():
+        qd.copy_(qh, non_blocking=True)
+        kd.copy_(kh, non_blocking=True)
+        vd.copy_(vh, non_blocking=True)
+        ekv.append_kv(cache, kd, vd, stream=stream)
+        ekv.decode(cache, qd, sel, attn, ws, out=out, stats=stats, stream=stream)
+        oh.copy_(out, non_blocking=True)
+
+    # the public API is graph-capturable: the user's step (pinned-host copies in, append,
+    # decode, copy out) captured once and replayed, synchronised on the host every step
+    ge = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        e2e_step()
+    stream.synchronize()
+    with torch.cuda.graph(ge, stream=stream):
+        e2e_step()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         a.record(stream)
         for _ in range(e2e_steps):
-            qd.copy_(qh, non_blocking=True)
-            kd.copy_(kh, non_blocking=True)
-            vd.copy_(vh, non_blocking=True)
-            ekv.append_kv(cache, kd, vd, stream=stream)
-            ekv.decode(cache, qd, sel, attn, ws, out=out, stats=stats, stream=stream)
-            oh.copy_(out, non_blocking=True)
+            ge.replay()
             stream.synchronize()
         b.record(stream)
     torch.cuda.synchronize()
