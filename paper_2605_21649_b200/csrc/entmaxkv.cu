@@ -253,11 +253,17 @@ struct UnionOut {            // optional union marks done by the selection kerne
 // top-k: one cluster of CL CTAs per row, CL = pages / 8192 rounded up to a power of two
 ekv_status launch_topk(const float *box, int B, int Hq, int maxp, const int32_t *sl, int k, int32_t *pi, int32_t *ns,
                        int stride, int G, const UnionOut &u, cudaStream_t st) {
+    // short rows: 256-thread CTAs (more CTAs per SM when there are many rows)
+    const int NT = maxp <= 4096 ? 256 : 512;
+    const int per = NT * kTkKPT;
     int CL = 1;
-    while (CL * kTkPerCta < maxp) CL *= 2;
-    if (CL > 8) return fail(EKV_ERR_UNSUPPORTED, "top-k supports at most %d pages", 8 * kTkPerCta);
-    cudaError_t e = launch_ex(k_topk, dim3((unsigned)(B * Hq * CL)), dim3(kTkNT), 0, st, (unsigned)CL, box, Hq, maxp, sl, k,
-                              pi, ns, stride, G, u.umask, u.W);
+    while (CL * per < maxp) CL *= 2;
+    if (CL > 8) return fail(EKV_ERR_UNSUPPORTED, "top-k supports at most %d pages", 8 * per);
+    cudaError_t e = NT == 256
+        ? launch_ex(k_topk<256>, dim3((unsigned)(B * Hq * CL)), dim3(256), 0, st, (unsigned)CL, box, Hq, maxp, sl, k,
+                    pi, ns, stride, G, u.umask, u.W)
+        : launch_ex(k_topk<512>, dim3((unsigned)(B * Hq * CL)), dim3(512), 0, st, (unsigned)CL, box, Hq, maxp, sl, k,
+                    pi, ns, stride, G, u.umask, u.W);
     if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "k_topk: %s", cudaGetErrorString(e));
     return check_launch("k_topk");
 }
@@ -297,11 +303,14 @@ ekv_status launch_scores(const CacheView &v, const void *q, int Hq, const uint32
 }
 
 template <typename T, int IB>
-ekv_status launch_tau_sparse_ib(const CacheView &v, const TauArgs &A, int rows, cudaStream_t st) {
+ekv_status launch_tau_sparse_ib(const CacheView &v, const TauArgs &A0, int rows, cudaStream_t st) {
     static bool init = false;
-    constexpr int smem = ts_smem<T>();
+    TauArgs A = A0;
+    A.cap = A.full ? kTsCap : std::min(kTsCap, (A.sel_stride * kP + 255) & ~255);
+    A.pr = std::min(kPr, A.cap);
+    const int smem = (4 + 4 + 4 + 1) * A.cap + (8 + 4) * A.pr + kTsVpre * kD * (int)sizeof(T);
     if (!init) {
-        set_smem(k_tau_sparse<T, IB>, smem);
+        set_smem(k_tau_sparse<T, IB>, ts_smem<T>());
         cudaFuncSetAttribute(k_tau_sparse<T, IB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         init = true;
     }

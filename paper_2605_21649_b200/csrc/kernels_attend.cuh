@@ -78,18 +78,26 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
     const bool bal = !full && nrows <= kMaxRowsBal;
     long long tot = full ? (long long)c.B * c.Hkv * c.maxp : (long long)c.B * Hq * stride;
     if (bal && warp == NCW) {
-        const int per = (nrows + 31) / 32;
-        int run = 0;
-        for (int i = 0; i < per; ++i) { const int r = lane * per + i; run += r < nrows ? __ldg(n_sel + r) : 0; }
-        int incl = run;
+        // rows lane + 32 i: every n_sel load in flight at once, then a warp scan per 32 rows
+        constexpr int MAXPER = kMaxRowsBal / 32;
+        int v[MAXPER];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += y; }
-        int acc = incl - run;
-        for (int i = 0; i < per; ++i) {
-            const int r = lane * per + i;
-            if (r < nrows) { pref[r] = acc; acc += __ldg(n_sel + r); }
+        for (int i = 0; i < MAXPER; ++i) {
+            const int r = lane + 32 * i;
+            v[i] = (r < nrows) ? __ldg(n_sel + r) : 0;
         }
-        if (lane == 31) pref[nrows] = incl;
+        int carry = 0;
+#pragma unroll
+        for (int i = 0; i < MAXPER; ++i) {
+            if (32 * i >= nrows) break;
+            int incl = v[i];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += y; }
+            const int r = lane + 32 * i;
+            if (r < nrows) pref[r] = carry + incl - v[i];
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) pref[nrows] = carry;
         __syncwarp();
         tot = pref[nrows];
     }
@@ -105,7 +113,11 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
         int si = 0, fill = 0;
         int cu = (int)(f0 / ucap), cs = (int)(f0 % ucap);   // (row or unit, slot) of the chunk start
         int brow = 0;                                        // balanced: row of the chunk start
-        if (bal) { while (brow + 1 < nrows && pref[brow + 1] <= f0) ++brow; }
+        if (bal) {                                           // last row with pref <= f0 (binary search)
+            int lo = 0, hi = nrows - 1;
+            while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (pref[mid] <= f0) lo = mid; else hi = mid - 1; }
+            brow = lo;
+        }
         for (long long cb = f0; cb < f1; cb += CHK) {
             int un[CHK / 32], pg[CHK / 32], hg[CHK / 32];
             bool ok[CHK / 32];
@@ -447,6 +459,7 @@ struct TauArgs {
     float *out; double *tau_out; int32_t *supp_out;
     int32_t *tok_list; double *p_list; int32_t *n_list; int list_cap;     // eval list
     int no_pv;                                                            // tau/supp only (dense-V)
+    int cap, pr;                                                          // tau kernel capacities
 };
 
 template <typename T>

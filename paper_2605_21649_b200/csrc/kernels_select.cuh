@@ -26,9 +26,8 @@ namespace ekv {
 //  3. Selection bitmap (bit = page), one word per thread (t < 256), block scan + cluster
 //     offsets: ascending page ids, and -- if umask != NULL -- the KV-group union marks.
 //     (512 threads, 2 CTAs per SM: the 256 CTAs of a 32-row, 65536-page launch are one wave.)
-constexpr int kTkNT = 512;
-constexpr int kTkKPT = 16;
-constexpr int kTkPerCta = kTkNT * kTkKPT;   // 8192 pages per CTA, <= 8 CTAs -> 65536 pages
+constexpr int kTkKPT = 16;                  // keys per thread; NT = 512 (8192 pages per CTA,
+                                            // <= 8 CTAs -> 65536 pages) or 256 for short rows
 
 // union mark of one selected page: bit g of the page's byte (fire-and-forget atomic)
 __device__ __forceinline__ void union_mark(uint32_t *um, int p, int g) {
@@ -45,7 +44,8 @@ __device__ __forceinline__ uint32_t nibble_word(uint32_t nib, int lane) {
     return w;
 }
 
-__global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, int Hq, int maxp,
+template <int NT>
+__global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int Hq, int maxp,
                                                 const int32_t *__restrict__ seq_lens, int k,
                                                 int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
                                                 int sel_stride, int G, uint32_t *__restrict__ umask, int W) {
@@ -56,14 +56,14 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
     const int CL = (int)cl.num_blocks(), r = (int)cl.block_rank();
     const int row = blockIdx.x / CL;
     const int t = threadIdx.x, lane = t & 31;
-    constexpr int NWp = kTkNT / 32;
+    constexpr int NWp = NT / 32;
     __shared__ uint32_t whist[NWp][256];     // per-warp private histograms (no cross-warp contention)
     __shared__ uint32_t hist[2][256];        // the CTA's histogram of the current digit (published)
     __shared__ uint32_t bits[256];
     __shared__ int xch[2];                   // published to the cluster: [0] #eq, [1] #selected
-    __shared__ int sh[(kTkNT / 32 + 2)];
+    __shared__ int sh[(NT / 32 + 2)];
     const int b = row / Hq;
-    const int base = r * kTkPerCta;
+    const int base = r * (NT * kTkKPT);
     const float *x = box + (size_t)row * maxp;
     const bool vec = (maxp & 3) == 0;
     // keys and the sequence length in one round trip (masked below)
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
     float4 kv[kTkKPT / 4];
 #pragma unroll
     for (int j = 0; j < kTkKPT / 4; ++j) {
-        const int i4 = base + 4 * (t + kTkNT * j);
+        const int i4 = base + 4 * (t + NT * j);
         if (vec && i4 + 3 < maxp) kv[j] = __ldg(reinterpret_cast<const float4 *>(x + i4));
         else {
             kv[j].x = (i4 < maxp) ? __ldg(x + i4) : 0.f;
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
     stamp(1, 0);
     ph_stamp<2>(0);
     if (keff >= M) {                         // every page (uniform over the cluster)
-        for (int p = base + t; p < min(M, base + kTkPerCta); p += kTkNT) {
+        for (int p = base + t; p < min(M, base + (NT * kTkKPT)); p += NT) {
             out[p] = p;
             if (um) union_mark(um, p, gh);
         }
@@ -98,13 +98,13 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
     uint32_t key[kTkKPT];
 #pragma unroll
     for (int j = 0; j < kTkKPT / 4; ++j) {
-        const int i4 = base + 4 * (t + kTkNT * j);
+        const int i4 = base + 4 * (t + NT * j);
         key[4 * j] = (i4 < M) ? f2key(kv[j].x) : 0u;
         key[4 * j + 1] = (i4 + 1 < M) ? f2key(kv[j].y) : 0u;
         key[4 * j + 2] = (i4 + 2 < M) ? f2key(kv[j].z) : 0u;
         key[4 * j + 3] = (i4 + 3 < M) ? f2key(kv[j].w) : 0u;
     }
-    for (int i = t; i < NWp * 256; i += kTkNT) (&whist[0][0])[i] = 0u;
+    for (int i = t; i < NWp * 256; i += NT) (&whist[0][0])[i] = 0u;
     __syncthreads();
     stamp(1, 1);
     ph_stamp<2>(1);
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
         int ceq = 0;
 #pragma unroll
         for (int j = 0; j < kTkKPT; ++j) ceq += key[j] == prefix;
-        ceq = block_sum_i<kTkNT>(ceq, sh);
+        ceq = block_sum_i<NT>(ceq, sh);
         if (t == 0) xch[0] = ceq;
         cl.sync();
         int before = 0;
@@ -204,12 +204,12 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
 #pragma unroll
             for (int e = 0; e < 4; ++e) nib |= (key[4 * j + e] == prefix ? 1u : 0u) << e;
             const uint32_t w = nibble_word(nib, lane);
-            if ((lane & 7) == 0) bits[64 * j + (t >> 3)] = w;
+            if ((lane & 7) == 0) bits[(NT / 8) * j + (t >> 3)] = w;
         }
         __syncthreads();
-        uint32_t w = t < 256 ? bits[t] : 0u;
+        uint32_t w = t < NT / 2 ? bits[t] : 0u;
         int tot;
-        int rank = block_excl_scan<kTkNT>(__popc(w), sh, &tot);
+        int rank = block_excl_scan<NT>(__popc(w), sh, &tot);
         uint32_t keep = 0u;
         while (w) {
             const uint32_t lb = w & (0u - w);
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
             w ^= lb;
         }
         __syncthreads();
-        if (t < 256) bits[t] = keep;         // chosen equal keys
+        if (t < NT / 2) bits[t] = keep;      // chosen equal keys
         __syncthreads();
     }
     // 3. selection bitmap and ascending output
@@ -233,14 +233,14 @@ __global__ void __launch_bounds__(kTkNT) k_topk(const float *__restrict__ box, i
         }
         const uint32_t w = nibble_word(nib, lane);
         if ((lane & 7) == 0) {
-            const int wi = 64 * j + (t >> 3);
+            const int wi = (NT / 8) * j + (t >> 3);
             bits[wi] = whole ? w : (w | bits[wi]);
         }
     }
     __syncthreads();
-    const uint32_t w = t < 256 ? bits[t] : 0u;
+    const uint32_t w = t < NT / 2 ? bits[t] : 0u;
     int tot;
-    const int pos = block_excl_scan<kTkNT>(__popc(w), sh, &tot);
+    const int pos = block_excl_scan<NT>(__popc(w), sh, &tot);
     if (t == 0) xch[1] = tot;
     cl.sync();
     int o = pos;

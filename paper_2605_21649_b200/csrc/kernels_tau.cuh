@@ -106,18 +106,21 @@ __device__ __forceinline__ void cp_async_commit_wait_all() {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 
 template <typename T, int IB>
-__global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A) {
+__global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A) {
     EKV_TRACE(6);
     pdl_wait();
     constexpr int NT = kTsNT, NW = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
+    // capacities: cap candidates (<= kTsCap; sparse rows: the list's token count, so short
+    // lists take little shared memory and several CTAs fit an SM), pr list entries
+    const int cap = A.cap, pr = A.pr;
     float *zs = reinterpret_cast<float *>(smem);                           // raw scores s
-    int *cj = reinterpret_cast<int *>(smem + 4 * kTsCap);                  // token positions
-    int *cph = reinterpret_cast<int *>(smem + 8 * kTsCap);                 // physical pages
-    double *zp = reinterpret_cast<double *>(smem + 12 * kTsCap);           // list z (fp64)
-    int *ip = reinterpret_cast<int *>(smem + 12 * kTsCap + 8 * kPr);       // list -> candidate slot
-    T *vpre = reinterpret_cast<T *>(smem + 12 * kTsCap + 12 * kPr);        // [kTsVpre][kD] staged V rows
-    uint8_t *cin = reinterpret_cast<uint8_t *>(smem + 12 * kTsCap + 12 * kPr + kTsVpre * kD * sizeof(T));
+    int *cj = reinterpret_cast<int *>(smem + 4 * cap);                     // token positions
+    int *cph = reinterpret_cast<int *>(smem + 8 * cap);                    // physical pages
+    double *zp = reinterpret_cast<double *>(smem + 12 * cap);              // list z (fp64)
+    int *ip = reinterpret_cast<int *>(smem + 12 * cap + 8 * pr);           // list -> candidate slot
+    T *vpre = reinterpret_cast<T *>(smem + 12 * cap + 12 * pr);            // [kTsVpre][kD] staged V rows
+    uint8_t *cin = reinterpret_cast<uint8_t *>(smem + 12 * cap + 12 * pr + kTsVpre * kD * sizeof(T));
     __shared__ float red[NW][kD];
     __shared__ int sup_j[kTsSup], sup_phys[kTsSup];   // (staged path: sup_j = list index)
     __shared__ float sup_p[kTsSup];
@@ -209,7 +212,7 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
             }
             int tot;
             int pos = n + block_excl_scan<NT>(__popcll(bits), shi, &tot);
-            if (n + tot > kTsCap) return -1;
+            if (n + tot > cap) return -1;
             if (bits) {
 #pragma unroll
                 for (int u = 0; u < kTsU; ++u) {
@@ -243,7 +246,7 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
         chunk_ovf = __syncthreads_or(chunk_ovf);
         const float *gs = A.cand_s + (size_t)row * A.nch * kCpc;
         const int32_t *gj = A.cand_j + (size_t)row * A.nch * kCpc;
-        if (!chunk_ovf && tot > kTsCap) {
+        if (!chunk_ovf && tot > cap) {
             // too many for shared memory: fp64 Newton over the chunk regions (thread t <->
             // chunk t) moves tau_lo just below tau, then an ordered re-extraction {z > tau_lo}
             double t = tau_lo;
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
             }
             int tt;
             int pos = block_excl_scan<NT>(mine, shi, &tt);
-            if (tt <= kTsCap) {
+            if (tt <= cap) {
                 if (threadIdx.x < A.nch) {
                     const size_t g0 = (size_t)threadIdx.x * kCpc;
                     for (int k = 0; k < ccnt; ++k) {
@@ -320,7 +323,7 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
             if (q < rk) off += nq;
             tot += nq;
         }
-        if (tot > kTsCap) ovf = true;
+        if (tot > cap) ovf = true;
         if (!ovf && rk > 0 && ncand > 0) {
             float *zs0 = cl.map_shared_rank(zs, 0);
             int *cj0 = cl.map_shared_rank(cj, 0), *cph0 = cl.map_shared_rank(cph, 0);
@@ -398,7 +401,7 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
             }
             int tot;
             const int pos = np + block_excl_scan<NT>(in ? 1 : 0, shi, &tot);
-            if (in && pos < kPr) { zp[pos] = z; ip[pos] = k; }
+            if (in && pos < pr) { zp[pos] = z; ip[pos] = k; }
             np += tot;
         }
         Rd.sum(f, dz);
@@ -413,7 +416,7 @@ __global__ void __launch_bounds__(kTsNT, 1) k_tau_sparse(CacheView c, TauArgs A)
         if (!(Fb >= 1.0)) np = -1;
     }
     if (np < 0) { base = tau_lo; np = build(base, Fb); }
-    const bool listed = np <= kPr;
+    const bool listed = np <= pr;
     const bool staged = np <= kTsVpre;
     if (staged) {
         // V rows of the list entries -> shared memory, in flight during step 4

@@ -7,11 +7,14 @@ from paper_2605_21649_b200 import binding as ekv
 from paper_2605_21649_b200.workload import make_workload
 slot = int(sys.argv[1]) if len(sys.argv) > 1 else 3     # block-0 stage stamps: 3 K-score, 4 score_pages
 dev = torch.device('cuda')
-n = (1 << 20) - 200; Hq, Hkv = 32, 8
-wl = make_workload(1, n, Hq, Hkv, seed=1, device=dev, spare_tokens=200)
+n = int(sys.argv[2]) if len(sys.argv) > 2 else (1 << 20) - 200
+B = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+kp = int(sys.argv[4]) if len(sys.argv) > 4 else 656
+Hq, Hkv = 32, 8
+wl = make_workload(B, n, Hq, Hkv, seed=1, device=dev, spare_tokens=200)
 c = ekv.PagedCache.allocate_meta(wl.K, wl.V, wl.page_table, wl.seq_lens); ekv.rebuild_page_stats(c)
-sel = ekv.select_params('topk', 656); attn = ekv.attn_params(1.5); ws = ekv.alloc_workspace(c, Hq, sel)
-st = ekv.DecodeStats(1, Hq, dev)
+sel = ekv.select_params('topk', kp); attn = ekv.attn_params(1.5); ws = ekv.alloc_workspace(c, Hq, sel)
+st = ekv.DecodeStats(B, Hq, dev)
 L = ekv.lib(); L.entmaxkv_debug_cta.argtypes = [ctypes.c_void_p]
 L.entmaxkv_debug_stamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 buf = (ctypes.c_ulonglong * 4096)(); sb = (ctypes.c_ulonglong * 256)(); nc = ctypes.c_int()

@@ -10,19 +10,20 @@ NAMES = ['append', 'score', 'topk', 'mark', 'attend_scores', 'candidates', 'tau_
          'eval_metrics', 'rebuild']
 n = int(sys.argv[1]) if len(sys.argv) > 1 else (1 << 20) - 200
 policy = sys.argv[2] if len(sys.argv) > 2 else 'topk'
+B = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 dev = torch.device('cuda')
 Hq, Hkv = 32, 8
 M = (n + 15) // 16
 k = int(sys.argv[3]) if len(sys.argv) > 3 else max(1, -(-M // 100))
-wl = make_workload(1, n, Hq, Hkv, seed=1, device=dev, spare_tokens=200)
+wl = make_workload(B, n, Hq, Hkv, seed=1, device=dev, spare_tokens=200)
 c = ekv.PagedCache.allocate_meta(wl.K, wl.V, wl.page_table, wl.seq_lens)
 ekv.rebuild_page_stats(c)
 sel = ekv.select_params('topk' if policy == 'full' else policy, k)
 attn = ekv.attn_params(1.5)
 ws = ekv.alloc_workspace(c, Hq, sel)
-st = ekv.DecodeStats(1, Hq, dev, delta_bar=True, gauss=policy == 'gauss')
-q, kn, vn = new_tokens(1, Hq, Hkv, seed=7, device=dev)
-out = torch.empty(1, Hq, 128, dtype=torch.float32, device=dev)
+st = ekv.DecodeStats(B, Hq, dev, delta_bar=True, gauss=policy == 'gauss')
+q, kn, vn = new_tokens(B, Hq, Hkv, seed=7, device=dev)
+out = torch.empty(B, Hq, 128, dtype=torch.float32, device=dev)
 s = torch.cuda.Stream()
 L = ekv.lib()
 L.entmaxkv_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
@@ -30,9 +31,9 @@ L.entmaxkv_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 
 if policy == 'full':
     wsf = ekv.alloc_workspace(c, Hq, None)
-    fo = torch.empty(1, Hq, 128, dtype=torch.float32, device=dev)
-    ft = torch.empty(1, Hq, dtype=torch.float64, device=dev)
-    fs = torch.empty(1, Hq, dtype=torch.int32, device=dev)
+    fo = torch.empty(B, Hq, 128, dtype=torch.float32, device=dev)
+    ft = torch.empty(B, Hq, dtype=torch.float64, device=dev)
+    fs = torch.empty(B, Hq, dtype=torch.int32, device=dev)
 
 
 def step():
