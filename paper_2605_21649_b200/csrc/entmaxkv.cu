@@ -302,24 +302,29 @@ ekv_status launch_scores(const CacheView &v, const void *q, int Hq, const uint32
     }
 }
 
-template <typename T, int IB>
-ekv_status launch_tau_sparse_ib(const CacheView &v, const TauArgs &A0, int rows, cudaStream_t st) {
+template <typename T, int IB, bool FULL>
+ekv_status launch_tau_sparse_ibf(const CacheView &v, const TauArgs &A0, int rows, cudaStream_t st) {
     static bool init = false;
     TauArgs A = A0;
     A.cap = A.full ? kTsCap : std::min(kTsCap, (A.sel_stride * kP + 255) & ~255);
     A.pr = std::min(kPr, A.cap);
     const int smem = (4 + 4 + 4 + 1) * A.cap + (8 + 4) * A.pr + kTsVpre * kD * (int)sizeof(T);
     if (!init) {
-        set_smem(k_tau_sparse<T, IB>, ts_smem<T>());
-        cudaFuncSetAttribute(k_tau_sparse<T, IB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        set_smem(k_tau_sparse<T, IB, FULL>, ts_smem<T>());
+        cudaFuncSetAttribute(k_tau_sparse<T, IB, FULL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         init = true;
     }
     // a cluster of up to 4 CTAs per row splits the candidate extraction (page-list reads are
     // latency bound per SM); rank 0 then finishes the row
     const int CL = A.full ? 1 : A.sel_stride > 384 ? 4 : A.sel_stride > 128 ? 2 : 1;
-    cudaError_t e = launch_ex(k_tau_sparse<T, IB>, dim3((unsigned)(rows * CL)), dim3(kTsNT), smem, st, (unsigned)CL, v, A);
+    cudaError_t e = launch_ex(k_tau_sparse<T, IB, FULL>, dim3((unsigned)(rows * CL)), dim3(kTsNT), smem, st, (unsigned)CL, v, A);
     if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "k_tau_sparse: %s", cudaGetErrorString(e));
     return check_launch("k_tau_sparse");
+}
+template <typename T, int IB>
+ekv_status launch_tau_sparse_ib(const CacheView &v, const TauArgs &A0, int rows, cudaStream_t st) {
+    if (A0.full) return launch_tau_sparse_ibf<T, IB, true>(v, A0, rows, st);
+    return launch_tau_sparse_ibf<T, IB, false>(v, A0, rows, st);
 }
 // integer beta = 1/(alpha-1) in 1..4 is a template constant; any other alpha -> IB = 0
 template <typename T>
@@ -447,6 +452,12 @@ ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t 
     }
     if (c->dtype == EKV_BF16) EKV_TRY(launch_tau_sparse<__nv_bfloat16>(v, A, rows, st));
     else EKV_TRY(launch_tau_sparse<float>(v, A, rows, st));
+#ifdef EKV_STAMPS
+    if (getenv("EKV_TAU_TWICE")) {                 // debug: warm instruction cache experiment
+        if (c->dtype == EKV_BF16) EKV_TRY(launch_tau_sparse<__nv_bfloat16>(v, A, rows, st));
+        else EKV_TRY(launch_tau_sparse<float>(v, A, rows, st));
+    }
+#endif
     if (!dense) return EKV_OK;
     const int dch = (c->max_pages_per_seq + kSmxPages - 1) / kSmxPages;
     dim3 g(dch, rows);

@@ -92,7 +92,7 @@ constexpr int kTsNT = 256;
 constexpr int kTsCap = 10240;                                         // candidates in shared memory
 constexpr int kTsSup = 1024;                                          // support entries per gather round
 constexpr int kTsVpre = 64;                                           // V rows staged for short lists
-constexpr int kTsU = 12;                                              // float4 items per thread per round
+constexpr int kTsU = 4;                                               // float4 items per thread per round (x 4 ranks: 1024 pages)
 template <typename T> constexpr int ts_smem() {
     return (4 + 4 + 4 + 1) * kTsCap + (8 + 4) * kPr + kTsVpre * kD * (int)sizeof(T);
 }
@@ -105,7 +105,10 @@ __device__ __forceinline__ void cp_async_commit_wait_all() {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 
-template <typename T, int IB>
+// FULL: full-cache rows (candidates from k_candidates' chunk regions, eval lists); the decode
+// path instantiates FULL = false, which keeps only the sparse code (less instruction fetch:
+// the kernel runs once per step on cold instruction caches)
+template <typename T, int IB, bool FULL>
 __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A) {
     EKV_TRACE(6);
     pdl_wait();
@@ -143,16 +146,16 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
     // this rank's first-round page list
     const uint32_t mk = __ldg(A.rowmax + row);
     const int L = __ldg(c.seq_lens + b);
-    const int nlist = A.full ? n_pages_of(L) : __ldg(A.n_sel + row);
+    const int nlist = FULL ? n_pages_of(L) : __ldg(A.n_sel + row);
     // logical page of list entry i (full rows: every page, in order)
-    auto page_of = [&](int i) -> int { return A.full ? i : __ldg(plist + i); };
+    auto page_of = [&](int i) -> int { return FULL ? i : __ldg(plist + i); };
     // rank rk extracts the items [rk S, (rk + 1) S) (item = 4 scores), S from the list capacity
     const int S = ((A.sel_stride * 4 + CL - 1) / CL + 3) & ~3;
     int pg[kTsU];
 #pragma unroll
     for (int u = 0; u < kTsU; ++u) {
         const int e = rk * S + threadIdx.x + NT * u;
-        pg[u] = (!A.full && e < (rk + 1) * S && (e >> 2) < A.sel_stride) ? __ldg(plist + (e >> 2)) : -1;
+        pg[u] = (!FULL && e < (rk + 1) * S && (e >> 2) < A.sel_stride) ? __ldg(plist + (e >> 2)) : -1;
     }
     ph_stamp<6>(0);
     if (mk == 0u) {   // empty C_tok (uniform over the cluster)
@@ -233,31 +236,137 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
         }
         return n;
     };
-    int ncand;
-    if (A.full) {
-        // full rows: k_candidates' chunk regions concatenated in chunk order (nch <= NT)
-        int ccnt = 0, tot = 0;
-        bool chunk_ovf = false;
-        if (threadIdx.x < A.nch) {
-            ccnt = A.ccount[(size_t)row * A.nch + threadIdx.x];
-            chunk_ovf = ccnt > kCpc;
+    // One extraction call site (the kernel runs on cold instruction caches: code size is
+    // latency).  Attempt 0: FULL rows from the chunk regions, sparse rows from this rank's
+    // slice (merged into rank 0); later attempts (rank 0 alone): the whole list, after a
+    // cluster overflow, or after the streamed Newton raised tau_lo past an overflow.
+    int ncand = -1;
+    int xlo = rk * S, xhi = (rk + 1) * S;
+    bool have_pg = true, first = true, newton_done = false;
+    for (;;) {
+        if (FULL && first) {
+            // full rows: k_candidates' chunk regions concatenated in chunk order (nch <= NT)
+            int ccnt = 0, tot = 0;
+            bool chunk_ovf = false;
+            if (threadIdx.x < A.nch) {
+                ccnt = A.ccount[(size_t)row * A.nch + threadIdx.x];
+                chunk_ovf = ccnt > kCpc;
+            }
+            const int coff = block_excl_scan<NT>(ccnt, shi, &tot);
+            chunk_ovf = __syncthreads_or(chunk_ovf);
+            const float *gs = A.cand_s + (size_t)row * A.nch * kCpc;
+            const int32_t *gj = A.cand_j + (size_t)row * A.nch * kCpc;
+            if (!chunk_ovf && tot > cap) {
+                // too many for shared memory: fp64 Newton over the chunk regions (thread t <->
+                // chunk t) moves tau_lo just below tau, then an ordered re-extraction {z > tau_lo}
+                double t = tau_lo;
+                for (int it = 0; it < 200; ++it) {
+                    double F = 0.0, Fd = 0.0;
+                    if (threadIdx.x < A.nch) {
+                        const size_t g0 = (size_t)threadIdx.x * kCpc;
+                        for (int k = 0; k < ccnt; ++k) {
+                            const double d = a * (double)__ldg(gs + g0 + k) - t;
+                            if (d > 0.0) { F += powB<IB>(d, beta); Fd += powBm1<IB>(d, beta); }
+                        }
+                    }
+                    Rd.sum(F, Fd);
+                    if (!(Fd > 0.0)) break;
+                    const double step = lbeta_step(F, Fd, beta, IB);
+                    t += step;
+                    if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(t)))) break;
+                }
+                tau_lo = fmax(tau_lo, t - 1e-7 * fmax(1.0, fabs(t)));
+                int mine = 0;
+                if (threadIdx.x < A.nch) {
+                    const size_t g0 = (size_t)threadIdx.x * kCpc;
+                    for (int k = 0; k < ccnt; ++k) mine += a * (double)__ldg(gs + g0 + k) > tau_lo;
+                }
+                int tt;
+                int pos = block_excl_scan<NT>(mine, shi, &tt);
+                if (tt <= cap) {
+                    if (threadIdx.x < A.nch) {
+                        const size_t g0 = (size_t)threadIdx.x * kCpc;
+                        for (int k = 0; k < ccnt; ++k) {
+                            const float sj = __ldg(gs + g0 + k);
+                            if (a * (double)sj > tau_lo) {
+                                const int j = __ldg(gj + g0 + k);
+                                zs[pos] = sj; cj[pos] = j; cph[pos] = __ldg(ptab + j / kP);
+                                ++pos;
+                            }
+                        }
+                    }
+                    ncand = tt;
+                } else {
+                    ncand = -1;
+                }
+            } else if (!chunk_ovf) {
+                __shared__ int s_off[256];
+                if (threadIdx.x < A.nch) s_off[threadIdx.x] = coff;
+                __syncthreads();
+                for (int e = threadIdx.x; e < tot; e += NT) {
+                    int lo = 0, hi = A.nch - 1;                // last chunk with offset <= e
+                    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (s_off[mid] <= e) lo = mid; else hi = mid - 1; }
+                    const size_t g = (size_t)lo * kCpc + (e - s_off[lo]);
+                    const int j = __ldg(gj + g);
+                    zs[e] = __ldg(gs + g);
+                    cj[e] = j;
+                    cph[e] = __ldg(ptab + j / kP);
+                }
+                ncand = tot;
+            } else {
+                ncand = -1;
+            }
+        } else {
+            ncand = extract(tau_lo, have_pg, xlo, xhi);
         }
-        const int coff = block_excl_scan<NT>(ccnt, shi, &tot);
-        chunk_ovf = __syncthreads_or(chunk_ovf);
-        const float *gs = A.cand_s + (size_t)row * A.nch * kCpc;
-        const int32_t *gj = A.cand_j + (size_t)row * A.nch * kCpc;
-        if (!chunk_ovf && tot > cap) {
-            // too many for shared memory: fp64 Newton over the chunk regions (thread t <->
-            // chunk t) moves tau_lo just below tau, then an ordered re-extraction {z > tau_lo}
+        if (first && CL > 1) {
+            // merge: ranks publish their counts; if everything fits, ranks >= 1 store their
+            // candidates into rank 0's arrays (rank order: deterministic) and leave
+            __shared__ int s_cnt;
+            if (threadIdx.x == 0) s_cnt = ncand;
+            cl.sync();
+            int tot = 0, off = 0;
+            bool ovf = false;
+            for (int q = 0; q < CL; ++q) {
+                const int nq = *cl.map_shared_rank(&s_cnt, q);
+                if (nq < 0) ovf = true;
+                if (q < rk) off += nq;
+                tot += nq;
+            }
+            if (tot > cap) ovf = true;
+            if (!ovf && rk > 0 && ncand > 0) {
+                float *zs0 = cl.map_shared_rank(zs, 0);
+                int *cj0 = cl.map_shared_rank(cj, 0), *cph0 = cl.map_shared_rank(cph, 0);
+                for (int i = threadIdx.x; i < ncand; i += NT) {
+                    zs0[off + i] = zs[i]; cj0[off + i] = cj[i]; cph0[off + i] = cph[i];
+                }
+            }
+            cl.sync();
+            if (rk > 0) return;
+            if (!ovf) { ncand = tot; break; }
+            ncand = -1;
+        }
+        first = false;
+        if (ncand >= 0) break;
+        xlo = 0; xhi = 1 << 30; have_pg = false;
+        if (newton_done) {             // support larger than the shared-memory capacity
+            if (threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = NAN;
+            if (threadIdx.x == 0) {
+                if (A.tau_out) A.tau_out[row] = NAN;
+                if (A.supp_out) A.supp_out[row] = -1;
+            }
+            return;
+        }
+            // overflow: fp64 Newton streamed over the whole row moves tau_lo just below tau
+            const int ntk = nlist * kP;
             double t = tau_lo;
             for (int it = 0; it < 200; ++it) {
                 double F = 0.0, Fd = 0.0;
-                if (threadIdx.x < A.nch) {
-                    const size_t g0 = (size_t)threadIdx.x * kCpc;
-                    for (int k = 0; k < ccnt; ++k) {
-                        const double d = a * (double)__ldg(gs + g0 + k) - t;
-                        if (d > 0.0) { F += powB<IB>(d, beta); Fd += powBm1<IB>(d, beta); }
-                    }
+                for (int e = threadIdx.x; e < ntk; e += NT) {
+                    const int j = page_of(e / kP) * kP + e % kP;
+                    if (j >= L) continue;
+                    const double d = a * (double)srow[j] - t;
+                    if (d > 0.0) { F += powB<IB>(d, beta); Fd += powBm1<IB>(d, beta); }
                 }
                 Rd.sum(F, Fd);
                 if (!(Fd > 0.0)) break;
@@ -266,104 +375,7 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
                 if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(t)))) break;
             }
             tau_lo = fmax(tau_lo, t - 1e-7 * fmax(1.0, fabs(t)));
-            int mine = 0;
-            if (threadIdx.x < A.nch) {
-                const size_t g0 = (size_t)threadIdx.x * kCpc;
-                for (int k = 0; k < ccnt; ++k) mine += a * (double)__ldg(gs + g0 + k) > tau_lo;
-            }
-            int tt;
-            int pos = block_excl_scan<NT>(mine, shi, &tt);
-            if (tt <= cap) {
-                if (threadIdx.x < A.nch) {
-                    const size_t g0 = (size_t)threadIdx.x * kCpc;
-                    for (int k = 0; k < ccnt; ++k) {
-                        const float sj = __ldg(gs + g0 + k);
-                        if (a * (double)sj > tau_lo) {
-                            const int j = __ldg(gj + g0 + k);
-                            zs[pos] = sj; cj[pos] = j; cph[pos] = __ldg(ptab + j / kP);
-                            ++pos;
-                        }
-                    }
-                }
-                ncand = tt;
-            } else {
-                ncand = -1;
-            }
-        } else if (!chunk_ovf) {
-            __shared__ int s_off[256];
-            if (threadIdx.x < A.nch) s_off[threadIdx.x] = coff;
-            __syncthreads();
-            for (int e = threadIdx.x; e < tot; e += NT) {
-                int lo = 0, hi = A.nch - 1;                // last chunk with offset <= e
-                while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (s_off[mid] <= e) lo = mid; else hi = mid - 1; }
-                const size_t g = (size_t)lo * kCpc + (e - s_off[lo]);
-                const int j = __ldg(gj + g);
-                zs[e] = __ldg(gs + g);
-                cj[e] = j;
-                cph[e] = __ldg(ptab + j / kP);
-            }
-            ncand = tot;
-        } else {
-            ncand = -1;
-        }
-    } else {
-        ncand = extract(tau_lo, true, rk * S, (rk + 1) * S);
-    }
-    if (CL > 1) {
-        // merge: ranks publish their counts; if everything fits, ranks >= 1 store their
-        // candidates into rank 0's arrays (rank order: deterministic) and leave
-        __shared__ int s_cnt;
-        if (threadIdx.x == 0) s_cnt = ncand;
-        cl.sync();
-        int tot = 0, off = 0;
-        bool ovf = false;
-        for (int q = 0; q < CL; ++q) {
-            const int nq = *cl.map_shared_rank(&s_cnt, q);
-            if (nq < 0) ovf = true;
-            if (q < rk) off += nq;
-            tot += nq;
-        }
-        if (tot > cap) ovf = true;
-        if (!ovf && rk > 0 && ncand > 0) {
-            float *zs0 = cl.map_shared_rank(zs, 0);
-            int *cj0 = cl.map_shared_rank(cj, 0), *cph0 = cl.map_shared_rank(cph, 0);
-            for (int i = threadIdx.x; i < ncand; i += NT) {
-                zs0[off + i] = zs[i]; cj0[off + i] = cj[i]; cph0[off + i] = cph[i];
-            }
-        }
-        cl.sync();
-        if (rk > 0) return;
-        ncand = ovf ? -1 : tot;
-        if (ovf) ncand = extract(tau_lo, false, 0, 1 << 30);   // rank 0 alone (may overflow again)
-    }
-    if (ncand < 0) {
-        // overflow: fp64 Newton streamed over the whole row moves tau_lo just below tau
-        const int ntk = nlist * kP;
-        double t = tau_lo;
-        for (int it = 0; it < 200; ++it) {
-            double F = 0.0, Fd = 0.0;
-            for (int e = threadIdx.x; e < ntk; e += NT) {
-                const int j = page_of(e / kP) * kP + e % kP;
-                if (j >= L) continue;
-                const double d = a * (double)srow[j] - t;
-                if (d > 0.0) { F += powB<IB>(d, beta); Fd += powBm1<IB>(d, beta); }
-            }
-            Rd.sum(F, Fd);
-            if (!(Fd > 0.0)) break;
-            const double step = lbeta_step(F, Fd, beta, IB);
-            t += step;
-            if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(t)))) break;
-        }
-        tau_lo = fmax(tau_lo, t - 1e-7 * fmax(1.0, fabs(t)));
-        ncand = extract(tau_lo, false, 0, 1 << 30);
-        if (ncand < 0) {             // support larger than the shared-memory capacity
-            if (threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = NAN;
-            if (threadIdx.x == 0) {
-                if (A.tau_out) A.tau_out[row] = NAN;
-                if (A.supp_out) A.supp_out[row] = -1;
-            }
-            return;
-        }
+        newton_done = true;
     }
     __syncthreads();
     ph_stamp<6>(1);
@@ -389,21 +401,24 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
     auto build = [&](double base, double &Fb) -> int {
         const float bf = (float)base;
         const float bpre = bf - 1e-3f * fmaxf(1.0f, fabsf(bf));
-        int np = 0;
+        // thread t owns the contiguous candidate slots [t L, (t + 1) L): one block scan in total
+        const int per = (ncand + NT - 1) / NT;
+        const int k0 = threadIdx.x * per, k1 = min(ncand, k0 + per);
         double f = 0.0, dz = 0.0;
-        for (int r0 = 0; r0 < ncand; r0 += NT) {
-            const int k = r0 + threadIdx.x;
-            bool in = false;
-            double z = 0.0;
-            if (k < ncand && af * zs[k] > bpre) {
-                z = a * (double)zs[k];
-                if (z > base) { in = true; f += powB<IB>(z - base, beta); }
+        int mine = 0;
+        for (int k = k0; k < k1; ++k)
+            if (af * zs[k] > bpre) {
+                const double z = a * (double)zs[k];
+                if (z > base) { ++mine; f += powB<IB>(z - base, beta); }
             }
-            int tot;
-            const int pos = np + block_excl_scan<NT>(in ? 1 : 0, shi, &tot);
-            if (in && pos < pr) { zp[pos] = z; ip[pos] = k; }
-            np += tot;
-        }
+        int np;
+        int pos = block_excl_scan<NT>(mine, shi, &np);
+        if (mine)
+            for (int k = k0; k < k1; ++k)
+                if (af * zs[k] > bpre) {
+                    const double z = a * (double)zs[k];
+                    if (z > base) { if (pos < pr) { zp[pos] = z; ip[pos] = k; } ++pos; }
+                }
         Rd.sum(f, dz);
         Fb = f;
         return np;
@@ -744,7 +759,7 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
         if (A.supp_out) A.supp_out[row] = (int)kk;
     }
     // eval list: support token positions and p_j in candidate order (exact delta / rho)
-    if (A.tok_list) {
+    if (FULL && A.tok_list) {
         int base = 0;
         for (int r0 = 0; r0 < ncand; r0 += NT) {
             const int k = r0 + threadIdx.x;
