@@ -401,6 +401,13 @@ ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t 
     if (c->dtype == EKV_BF16)
         EKV_TRY(launch_scores<__nv_bfloat16>(v, q, Hq, um, L.W, pi, ns, stride, scores, rowmax, full, st));
     else EKV_TRY(launch_scores<float>(v, q, Hq, um, L.W, pi, ns, stride, scores, rowmax, full, st));
+#ifdef EKV_STAMPS
+    if (getenv("EKV_ATT_TWICE")) {                 // debug: warm instruction cache experiment
+        if (c->dtype == EKV_BF16)
+            EKV_TRY(launch_scores<__nv_bfloat16>(v, q, Hq, um, L.W, pi, ns, stride, scores, rowmax, full, st));
+        else EKV_TRY(launch_scores<float>(v, q, Hq, um, L.W, pi, ns, stride, scores, rowmax, full, st));
+    }
+#endif
     const int rows = c->batch * Hq;
     const size_t ntok = (size_t)c->max_pages_per_seq * kP;
     float *cs = at<float>(ws, L.cand_s);

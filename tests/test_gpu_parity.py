@@ -206,6 +206,26 @@ def test_sparse_softmax_same_kernels(case):
 
 
 @pytest.mark.parametrize("case", CASES, ids=ids)
+def test_full_softmax_grouped_dense_v(case):
+    """a6 on the full cache: one CTA per (chunk, KV group) reads each V row once for the
+    G heads (k_dense_group_partial) -- softmax vs the oracle's fp64 softmax."""
+    B, sl, Hq, Hkv, dt = case
+    wl, dc, hc = make_pair(B, sl, Hq, Hkv, dtype=dt, seed=29)
+    G = Hq // Hkv
+    qh = q_host(wl)
+    out, tau, supp = ekv.full_attend(dc, wl.q.cuda(), ekv.attn_params(1.5, "softmax"))
+    torch.cuda.synchronize()
+    out, tau, supp = out.cpu().numpy(), tau.cpu().numpy(), supp.cpu().numpy()
+    for b in range(B):
+        M = hc.n_pages(b)
+        for h in range(Hq):
+            ref = hc.attend(qh[b, h], b, h // G, np.arange(M, dtype=np.int32), 1.5, transform=1)
+            np.testing.assert_allclose(out[b, h], ref["o"], atol=tol_for(dt), rtol=0, err_msg=f"b={b} h={h}")
+            assert abs(tau[b, h] - ref["tau"]) < 1e-5
+            assert supp[b, h] == int(wl.seq_lens[b])
+
+
+@pytest.mark.parametrize("case", CASES, ids=ids)
 @pytest.mark.parametrize("alpha", [1.5, 2.0, 1.25])
 @pytest.mark.parametrize("dense_v", [False, True])
 def test_full_attend(case, alpha, dense_v):
