@@ -41,9 +41,12 @@ namespace ekv {
 #ifndef EKV_ATT_NS
 #define EKV_ATT_NS 3
 #endif
+#ifndef EKV_ATT_SP
+#define EKV_ATT_SP 8
+#endif
 template <typename T> struct AttCfg {
     static constexpr int NCW = EKV_ATT_NCW;                // consumer warps (16 half-warps >= items per stage, usually)
-    static constexpr int SP = 8;                           // pages per stage (item code: 3 bits)
+    static constexpr int SP = EKV_ATT_SP;                  // pages per stage (item code: 3 bits)
     static constexpr int NS = sizeof(T) == 2 ? EKV_ATT_NS : 2;   // ring stages
     static constexpr int TILE = kP * kD * (int)sizeof(T);
     static constexpr int RING = NS * SP * TILE;
