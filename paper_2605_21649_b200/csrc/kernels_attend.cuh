@@ -173,23 +173,36 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
                 nl += __popc(bal);
             }
             __syncwarp();
-            for (int i = 0; i < nl; ++i) {          // warp-uniform
+            for (int i = 0; i < nl;) {              // warp-uniform; up to SP pages per iteration
                 const int slot = si % NS;
                 if (fill == 0) {
                     if (lane == 0 && si >= NS) mbar_wait(&emptyb[slot], ((si / NS) - 1) & 1);
                     __syncwarp();
                 }
-                if (lane == 0) {
-                    d_unit[slot][fill] = l_unit[i]; d_page[slot][fill] = l_page[i];
-                    d_mask[slot][fill] = l_mask[i]; d_phys[slot][fill] = l_phys[i];
+                const int cnt = min(SP - fill, nl - i);
+                if (lane < cnt) {                       // lane-parallel stage entries
+                    d_unit[slot][fill + lane] = l_unit[i + lane]; d_page[slot][fill + lane] = l_page[i + lane];
+                    d_mask[slot][fill + lane] = l_mask[i + lane]; d_phys[slot][fill + lane] = l_phys[i + lane];
                 }
-                if (++fill == SP) {
+                i += cnt;
+                fill += cnt;
+                if (fill == SP) {
                     __syncwarp();
+                    // items (page k, head g) in page order: lane k writes its page's heads at
+                    // the prefix of the head counts (full: every (page, head), codes computed
+                    // by the consumers)
+                    int ni = SP * G;
+                    if (!full) {
+                        const unsigned m = lane < SP ? (unsigned)d_mask[slot][lane] : 0u;
+                        int incl = __popc(m);
+#pragma unroll
+                        for (int o = 1; o < 8; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += y; }
+                        int off = incl - __popc(m);
+                        for (unsigned mm = m; mm; mm &= mm - 1u) d_items[slot][off++] = (uint8_t)(lane * 8 + __ffs((int)mm) - 1);
+                        ni = __shfl_sync(0xffffffffu, incl, SP - 1);
+                    }
                     if (lane == 0) {
                         d_n[slot] = SP;
-                        int ni = 0;
-                        for (int kk = 0; kk < SP; ++kk)
-                            for (unsigned m = d_mask[slot][kk]; m; m &= m - 1u) d_items[slot][ni++] = (uint8_t)(kk * 8 + __ffs((int)m) - 1);
                         d_ni[slot] = ni;
                         mbar_expect_tx(&fullb[slot], (uint32_t)(SP * TILE));
                     }
@@ -209,9 +222,12 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
             __syncwarp();
             if (lane == 0) {
                 d_n[slot] = fill;
-                int ni = 0;
-                for (int kk = 0; kk < fill; ++kk)
-                    for (unsigned m = d_mask[slot][kk]; m; m &= m - 1u) d_items[slot][ni++] = (uint8_t)(kk * 8 + __ffs((int)m) - 1);
+                int ni = fill * G;
+                if (!full) {
+                    ni = 0;
+                    for (int kk = 0; kk < fill; ++kk)
+                        for (unsigned m = d_mask[slot][kk]; m; m &= m - 1u) d_items[slot][ni++] = (uint8_t)(kk * 8 + __ffs((int)m) - 1);
+                }
                 d_ni[slot] = ni;
                 mbar_expect_tx(&fullb[slot], (uint32_t)(fill * TILE));
             }
@@ -267,7 +283,8 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
         for (int base = 2 * warp; base < ni; base += 2 * NCW) {            // warp-uniform
             const int it = base + half;
             const bool act = it < ni;
-            const int code = d_items[slot][act ? it : base];
+            const int itc = act ? it : base;
+            const int code = full ? ((itc / G) * 8 + itc % G) : d_items[slot][itc];
             const int k = code >> 3, g = code & 7;
             const int unit = d_unit[slot][k];
             const int unitA = __shfl_sync(0xffffffffu, unit, 0), unitB = __shfl_sync(0xffffffffu, unit, 16);
