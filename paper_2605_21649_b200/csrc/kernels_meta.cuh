@@ -181,8 +181,10 @@ __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(C
                         if (++p0 == c.maxp) { p0 = 0; ++bb; }
                         continue;
                     }
-                    int n = 1;
-                    while (n < SP && i + n < nchk && l_phys[i + n] >= 0 && p0 + n < c.maxp) ++n;
+                    // run length: leading valid slots of [i, i + SP) (one ballot, not a serial scan)
+                    const bool vv = lane < SP && i + lane < nchk && l_phys[i + lane] >= 0 && p0 + lane < c.maxp;
+                    const unsigned vb = __ballot_sync(0xffffffffu, vv);
+                    const int n = min(SP, __ffs((int)~vb) - 1 < 0 ? 32 : __ffs((int)~vb) - 1);
                     const int slot = si % NS;
                     if (lane == 0) {
                         if (si >= NS) mbar_wait(&emptyb[slot], ((si / NS) - 1) & 1);
