@@ -208,7 +208,8 @@ int num_sms() {
 }
 
 template <typename T, int G, int MODES>
-void score_go(const CacheView &v, const T *q, int Hq, float *box, float *mu, float *s2, cudaStream_t st) {
+void score_go(const CacheView &v, const T *q, int Hq, float *box, float *mu, float *s2, uint4 *zero, size_t zero_n16,
+              cudaStream_t st) {
     constexpr int SP = ScoreCfg<MODES>::SP, NS = ScoreCfg<MODES>::NS;
     const int HD = v.Hkv * kD;
     const int per_page = ((MODES & 1) ? 2 * HD * (int)sizeof(T) : 0) + ((MODES & 2) ? 2 * HD * 4 : 0);
@@ -224,25 +225,27 @@ void score_go(const CacheView &v, const T *q, int Hq, float *box, float *mu, flo
     long long gx = ((long long)v.B * v.maxp + 7) / 8;
     if (gx > per_sm * num_sms()) gx = per_sm * num_sms();
     if (gx < 1) gx = 1;
-    launch_ex(k_score<T, G, MODES>, dim3((unsigned)gx), dim3(288), smem, st, 0, v, q, Hq, box, mu, s2);
+    launch_ex(k_score<T, G, MODES>, dim3((unsigned)gx), dim3(288), smem, st, 0, v, q, Hq, box, mu, s2, zero, zero_n16);
 }
 template <typename T, int G>
 ekv_status launch_score_t(const CacheView &v, const void *q, int Hq, int modes, float *box, float *mu, float *s2,
+                          uint4 *zero, size_t zero_n16,
                           cudaStream_t st) {
     const T *qq = static_cast<const T *>(q);
-    if (modes == 1) score_go<T, G, 1>(v, qq, Hq, box, mu, s2, st);
-    else if (modes == 2) score_go<T, G, 2>(v, qq, Hq, box, mu, s2, st);
-    else score_go<T, G, 3>(v, qq, Hq, box, mu, s2, st);
+    if (modes == 1) score_go<T, G, 1>(v, qq, Hq, box, mu, s2, zero, zero_n16, st);
+    else if (modes == 2) score_go<T, G, 2>(v, qq, Hq, box, mu, s2, zero, zero_n16, st);
+    else score_go<T, G, 3>(v, qq, Hq, box, mu, s2, zero, zero_n16, st);
     return check_launch("k_score");
 }
 template <typename T>
 ekv_status launch_score(const CacheView &v, const void *q, int Hq, int modes, float *box, float *mu, float *s2,
+                        uint4 *zero, size_t zero_n16,
                         cudaStream_t st) {
     switch (Hq / v.Hkv) {
-    case 1: return launch_score_t<T, 1>(v, q, Hq, modes, box, mu, s2, st);
-    case 2: return launch_score_t<T, 2>(v, q, Hq, modes, box, mu, s2, st);
-    case 4: return launch_score_t<T, 4>(v, q, Hq, modes, box, mu, s2, st);
-    default: return launch_score_t<T, 8>(v, q, Hq, modes, box, mu, s2, st);
+    case 1: return launch_score_t<T, 1>(v, q, Hq, modes, box, mu, s2, zero, zero_n16, st);
+    case 2: return launch_score_t<T, 2>(v, q, Hq, modes, box, mu, s2, zero, zero_n16, st);
+    case 4: return launch_score_t<T, 4>(v, q, Hq, modes, box, mu, s2, zero, zero_n16, st);
+    default: return launch_score_t<T, 8>(v, q, Hq, modes, box, mu, s2, zero, zero_n16, st);
     }
 }
 
@@ -634,8 +637,8 @@ ekv_status entmaxkv_score_pages(const ekv_cache *cache, const void *q, int32_t n
     g_launches = 0;
     CacheView v = view(cache);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (cache->dtype == EKV_BF16) return launch_score<__nv_bfloat16>(v, q, n_q_heads, modes, box, mu, sigma2, st);
-    return launch_score<float>(v, q, n_q_heads, modes, box, mu, sigma2, st);
+    if (cache->dtype == EKV_BF16) return launch_score<__nv_bfloat16>(v, q, n_q_heads, modes, box, mu, sigma2, nullptr, 0, st);
+    return launch_score<float>(v, q, n_q_heads, modes, box, mu, sigma2, nullptr, 0, st);
 }
 
 ekv_status entmaxkv_select(const ekv_cache *cache, int32_t n_q_heads, const float *box, const float *mu,
@@ -716,23 +719,22 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
     int32_t *ns = at<int32_t>(workspace, L.n_sel);
     double *th = at<double>(workspace, L.tau_hat);
     const bool want_db = stats && stats->delta_bar && attn->transform == EKV_ENTMAX;
-    // zero the per-step counters / union mask once (a kernel, so the PDL chain is unbroken);
-    // the selection kernel merges the union
-    {
-        const size_t n16 = L.zero_bytes / 16;
-        launch_ex(k_zero, dim3((unsigned)std::min<size_t>(148, (n16 + 255) / 256)), dim3(256), 0, st, 0,
-                  at<uint4>(workspace, L.zero), n16);
-        EKV_TRY(check_launch("k_zero"));
-    }
     const int Gq = n_q_heads / cache->n_kv_heads;
     const UnionOut uo{at<uint32_t>(workspace, L.umask), L.W};
-    // a1: page scores (box for top-k and for the certificate; mu/sigma2 for Gaussian)
+    // a1: page scores (box for top-k and for the certificate; mu/sigma2 for Gaussian); the
+    // per-step counters / union mask are zeroed by the scoring kernel (or a k_zero launch
+    // when nothing is scored) -- kernels only, so the PDL chain is unbroken
     int modes = 0;
     if (sel->policy == EKV_TOPK || want_db) modes |= EKV_SCORE_BOX;
     if (sel->policy == EKV_GAUSS) modes |= EKV_SCORE_GAUSS;
+    uint4 *zp = at<uint4>(workspace, L.zero);
+    const size_t zn16 = L.zero_bytes / 16;
     if (modes) {
-        if (cache->dtype == EKV_BF16) EKV_TRY(launch_score<__nv_bfloat16>(v, q, n_q_heads, modes, box, mu, s2, st));
-        else EKV_TRY(launch_score<float>(v, q, n_q_heads, modes, box, mu, s2, st));
+        if (cache->dtype == EKV_BF16) EKV_TRY(launch_score<__nv_bfloat16>(v, q, n_q_heads, modes, box, mu, s2, zp, zn16, st));
+        else EKV_TRY(launch_score<float>(v, q, n_q_heads, modes, box, mu, s2, zp, zn16, st));
+    } else {
+        launch_ex(k_zero, dim3((unsigned)std::min<size_t>(148, (zn16 + 255) / 256)), dim3(256), 0, st, 0, zp, zn16);
+        EKV_TRY(check_launch("k_zero"));
     }
     // a2 / a2'
     const int maxp = cache->max_pages_per_seq;
@@ -844,8 +846,8 @@ ekv_status entmaxkv_decode_sharded(const ekv_cache *cache, const int32_t *global
     if (cudaMemsetAsync(at<char>(workspace, L.zero), 0, L.zero_bytes, st) != cudaSuccess)
         return fail(EKV_ERR_CUDA, "memset: %s", cudaGetErrorString(cudaGetLastError()));
     // 1. local scores + local top-k, then the global merge
-    if (cache->dtype == EKV_BF16) EKV_TRY(launch_score<__nv_bfloat16>(v, q, n_q_heads, EKV_SCORE_BOX, box, nullptr, nullptr, st));
-    else EKV_TRY(launch_score<float>(v, q, n_q_heads, EKV_SCORE_BOX, box, nullptr, nullptr, st));
+    if (cache->dtype == EKV_BF16) EKV_TRY(launch_score<__nv_bfloat16>(v, q, n_q_heads, EKV_SCORE_BOX, box, nullptr, nullptr, nullptr, 0, st));
+    else EKV_TRY(launch_score<float>(v, q, n_q_heads, EKV_SCORE_BOX, box, nullptr, nullptr, nullptr, 0, st));
     EKV_TRY(launch_topk(box, cache->batch, n_q_heads, maxp, cache->seq_lens, sel->k_pages, pi, ns, L.cap, Gq,
                         UnionOut{nullptr, 0}, st));
     float *ps = at<float>(workspace, S.pack_s), *rs = at<float>(workspace, S.recv_s);

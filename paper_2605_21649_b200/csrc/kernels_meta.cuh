@@ -128,9 +128,14 @@ template <int MODES> struct ScoreCfg {
 template <typename T, int G, int MODES>
 __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(CacheView c, const T *__restrict__ q, int Hq,
                                                    float *__restrict__ box, float *__restrict__ mu,
-                                                   float *__restrict__ sigma2) {
+                                                   float *__restrict__ sigma2, uint4 *__restrict__ zero,
+                                                   size_t zero_n16) {
     EKV_TRACE(1);
     pdl_wait();
+    // decode's per-step counters / union mask (read by the later kernels of the step) are
+    // zeroed here, one slice per CTA -- no separate launch
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < zero_n16; i += (size_t)gridDim.x * blockDim.x)
+        zero[i] = make_uint4(0, 0, 0, 0);
     constexpr int SP = ScoreCfg<MODES>::SP, NS = ScoreCfg<MODES>::NS;
     constexpr int NCW = 8;
     extern __shared__ __align__(128) unsigned char smem[];
