@@ -135,9 +135,8 @@ int sel_cap(const ekv_cache *c, const ekv_select_params *s) {
 // One layout serves decode (incl. eval_exact), select, sparse_attend and full_attend.
 struct Layout {
     size_t box, mu, sigma2, page_idx, n_sel, tau_hat;
-    size_t zero, rowmax, ccount, tickets, ucount, umask, zero_bytes;   // zeroed per attention pass
-    size_t ulist;
-    size_t db_partial, tau_int, smx_acc, smx_l, smx_cnt;
+    size_t zero, rowmax, ccount, umask, zero_bytes;   // zeroed per step / attention pass
+    size_t tau_int, smx_acc, smx_l, smx_cnt;
     int smx_nch;
     size_t scores, cand_s, cand_j, tok_list, p_list, n_list, full_out, total;
     int cap, W, list_cap;
@@ -160,11 +159,8 @@ Layout layout(const ekv_cache *c, int Hq, const ekv_select_params *sel) {
     L.zero = o;
     L.rowmax = take(B * Hq * 4);
     L.ccount = take(B * Hq * (size_t)((maxp + 255) / 256) * 4);
-    L.tickets = take(B * Hq * 4);
-    L.ucount = take(B * Hkv * 4);
     L.umask = take(B * Hkv * (size_t)L.W * 4);
     L.zero_bytes = o - L.zero;
-    L.ulist = take(B * Hkv * maxp * 4);
     L.scores = take(B * Hq * maxp * kP * 4);
     L.cand_s = take(B * Hq * (size_t)((maxp + 255) / 256) * kCpc * 4);
     L.cand_j = take(B * Hq * (size_t)((maxp + 255) / 256) * kCpc * 4);
@@ -172,7 +168,6 @@ Layout layout(const ekv_cache *c, int Hq, const ekv_select_params *sel) {
     L.p_list = take(B * Hq * (size_t)L.list_cap * 8);
     L.n_list = take(B * Hq * 4);
     L.full_out = take(B * Hq * kD * 4);
-    L.db_partial = take(B * Hq * (size_t)((maxp + kDbChunk - 1) / kDbChunk) * 8);
     L.tau_int = take(B * Hq * 8);
     L.smx_nch = (int)((maxp + kSmxPages - 1) / kSmxPages);
     L.smx_acc = take(B * Hq * (size_t)L.smx_nch * kD * 4);
