@@ -352,6 +352,16 @@ def main():
     step_bytes = meta_bytes + kv_sparse + Hq * d * 2 + Hq * d * 4
     full_bytes = n_tok * Hkv * 2 * d * 2
 
+    # ---- the paper's approximate threshold (N1, R23: histogram init + 2 Halley steps)
+    attn_apx = ekv.attn_params(args.alpha, tau_halley=2)
+    outa = torch.empty_like(out)
+    stats_a = ekv.DecodeStats(1, Hq, dev, delta_bar=True, gauss=args.policy == "gauss")
+    approx_us = time_graph(lambda: ekv.decode(cache, q, sel, attn_apx, ws, out=outa, stats=stats_a, stream=stream), reps)
+    torch.cuda.synchronize()
+    ekv.decode(cache, q, sel, attn, ws, out=out, stats=stats, stream=stream)
+    torch.cuda.synchronize()
+    approx_maxabs = float((outa - out).abs().max().item())
+
     # ---- full-cache entmax baseline (a5)
     full_us = full_dense_us = None
     if not args.no_full:
@@ -443,6 +453,8 @@ def main():
             "speedup_vs_full_entmax_roofline": full_bytes / (peak * 1e3) / us_step,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_us, "unit": "us", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "decode_approx_tau": {"us": approx_us, "tau_halley": 2, "maxabs_vs_exact": approx_maxabs,
+                                  "note": "decode only (no append), the paper's histogram + Halley threshold"},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
             "support_per_head_mean": supp / Hq, "union_pages": union,

@@ -78,10 +78,16 @@ typedef struct {
  * outside the support), the paper's full-cache reference that reads all scores and V
  * (P:1343); without it the full path reads V of the support only.  Ignored elsewhere. */
 enum { EKV_ATTN_DENSE_V = 1 };
+/* tau_halley > 0 (entmax): the paper's approximate threshold instead of the exact one
+ * ("a histogram-based initialization followed by Halley iterations"; DESIGN R23):
+ * tau_0 from a 64-bin histogram of z over (z_max - 1, z_max] (the largest bin edge whose
+ * certified lower bound of F reaches 1), then tau_halley Halley steps on
+ * sum_{z > t} (z - t)^beta = 1; p_j = (z_j - tau)_+^beta renormalised (R12).  0 = exact. */
 typedef struct {
     float alpha;
     int32_t transform;
     int32_t flags;
+    int32_t tau_halley;
 } ekv_attn_params;
 
 /*

@@ -222,6 +222,64 @@ int orc_entmax(const double *z, int n, double alpha, double *p, double *tau_out)
     return k;
 }
 
+/* ------------------------------------------------------------------------- */
+/* Approximate tau, the paper's kernel recipe ("estimates the entmax   */
+/* threshold tau using a histogram-based initialization followed by Halley     */
+/* iterations"; DESIGN reading R23 fixes the unstated details):                */
+/*  1. 64 bins over (z_max - 1, z_max]: z in bin b iff b = min(63,            */
+/*     floor((z_max - z) * 64)), for z > z_max - 1 (tau >= z_max - 1);         */
+/*  2. tau_0 = the largest edge e_k = z_max - k/64 whose certified lower bound  */
+/*     LB_k = sum_{b<k} cnt_b ((k-1-b)/64)^beta reaches 1 (else z_max - 1);    */
+/*  3. h Halley steps on f(t) = sum_{z>t} (z-t)^beta - 1:                      */
+/*     t <- t - 2 f f' / (2 f'^2 - f f''), f' = -beta S_{beta-1},              */
+/*     f'' = beta (beta-1) S_{beta-2}, S_m = sum_{z>t} (z-t)^m;                  */
+/*  4. p_i = (z_i - tau)_+^beta (normalised by the caller, R12).               */
+/* Returns |{z > tau}|.                                                         */
+/* ------------------------------------------------------------------------- */
+int orc_entmax_approx(const double *z, int n, double alpha, int h, double *p, double *tau_out)
+{
+    const double beta = 1.0 / (alpha - 1.0);
+    if (n <= 0) { if (tau_out) *tau_out = NAN; return 0; }
+    double zmax = z[0];
+    for (int i = 1; i < n; ++i) if (z[i] > zmax) zmax = z[i];
+    double cnt[64] = {0};
+    for (int i = 0; i < n; ++i) {
+        if (!(z[i] > zmax - 1.0)) continue;
+        double fb = floor((zmax - z[i]) * 64.0);
+        int b = fb > 63.0 ? 63 : (int)fb;
+        cnt[b] += 1.0;
+    }
+    double t = zmax - 1.0;
+    for (int k = 1; k <= 64; ++k) {
+        double lb = 0.0;
+        for (int b = 0; b < k; ++b) lb += cnt[b] * powb((double)(k - 1 - b) / 64.0, beta);
+        if (lb >= 1.0) { t = zmax - (double)k / 64.0; break; }
+    }
+    for (int it = 0; it < h; ++it) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0;   /* sum w^beta, w^(beta-1), w^(beta-2), w = z - t > 0 */
+        for (int i = 0; i < n; ++i) {
+            double w = z[i] - t;
+            if (w > 0.0) {
+                s0 += powb(w, beta);
+                s1 += powb(w, beta - 1.0);
+                s2 += (beta == 1.0) ? 0.0 : powb(w, beta - 2.0);
+            }
+        }
+        double f = s0 - 1.0, fp = -beta * s1, fpp = beta * (beta - 1.0) * s2;
+        double den = 2.0 * fp * fp - f * fpp;
+        if (!(den != 0.0)) break;
+        t -= 2.0 * f * fp / den;
+    }
+    int k = 0;
+    for (int i = 0; i < n; ++i) {
+        double w = z[i] - t;
+        p[i] = w > 0.0 ? powb(w, beta) : 0.0;
+        k += w > 0.0;
+    }
+    if (tau_out) *tau_out = t;
+    return k;
+}
+
 /* softmax, fp64 with max subtraction. Returns log-normalizer. */
 double orc_softmax(const double *s, int n, double *p)
 {
@@ -247,7 +305,7 @@ int orc_attend(const float *q, const float *Kp, const float *Vp,
                const int32_t *page_row, int seq_len, int kvh, int Hkv, int P,
                int dv, const int32_t *pages, int n_pages, double alpha,
                int transform, double *o, double *tau, double *p_tok,
-               float *s_tok)
+               float *s_tok, int approx_h)
 {
     const int d = ORC_D;
     int cap = n_pages * P;
@@ -270,10 +328,16 @@ int orc_attend(const float *q, const float *Kp, const float *Vp,
     }
     int ret;
     if (n == 0) ret = 0, *tau = NAN;
+    else if (transform == 0 && approx_h > 0) ret = orc_entmax_approx(z, n, alpha, approx_h, pr, tau);
     else if (transform == 0) ret = orc_entmax(z, n, alpha, pr, tau);
     else { *tau = orc_softmax(z, n, pr); ret = n; }
     for (int i = 0; i < dv; ++i) o[i] = 0.0;
     if (p_tok) for (int j = 0; j < seq_len; ++j) p_tok[j] = 0.0;
+    if (transform == 0 && approx_h > 0 && n > 0) {       /* R12: o = sum p v / sum p */
+        double ps = 0.0;
+        for (int m = 0; m < n; ++m) ps += pr[m];
+        for (int m = 0; m < n; ++m) pr[m] /= ps;
+    }
     for (int m = 0; m < n; ++m) {
         int j = tok[m];
         if (p_tok) p_tok[j] = pr[m];

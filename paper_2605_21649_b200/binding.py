@@ -50,7 +50,8 @@ EKV_ATTN_DENSE_V = 1
 
 
 class ekv_attn_params(ctypes.Structure):
-    _fields_ = [("alpha", ctypes.c_float), ("transform", ctypes.c_int32), ("flags", ctypes.c_int32)]
+    _fields_ = [("alpha", ctypes.c_float), ("transform", ctypes.c_int32), ("flags", ctypes.c_int32),
+                ("tau_halley", ctypes.c_int32)]
 
 
 class ekv_select_params(ctypes.Structure):
@@ -194,9 +195,10 @@ def select_params(policy="topk", k_pages=64, q_page=0.99, margin=0.0) -> ekv_sel
     return ekv_select_params(pol, int(k_pages), float(q_page), float(margin))
 
 
-def attn_params(alpha=1.5, transform="entmax", dense_v=False) -> ekv_attn_params:
+def attn_params(alpha=1.5, transform="entmax", dense_v=False, tau_halley=0) -> ekv_attn_params:
+    """tau_halley > 0: the paper's approximate threshold (histogram init + that many Halley steps)."""
     return ekv_attn_params(float(alpha), {"entmax": EKV_ENTMAX, "softmax": EKV_SOFTMAX}[transform],
-                           EKV_ATTN_DENSE_V if dense_v else 0)
+                           EKV_ATTN_DENSE_V if dense_v else 0, int(tau_halley))
 
 
 def workspace_size(cache: PagedCache, n_q_heads: int, sel: ekv_select_params | None) -> int:

@@ -362,6 +362,7 @@ ekv_status check_attn(const ekv_attn_params *a) {
     if (!a) return fail(EKV_ERR_INVALID_ARG, "attn params NULL");
     if (a->transform != EKV_ENTMAX && a->transform != EKV_SOFTMAX) return fail(EKV_ERR_INVALID_ARG, "bad transform");
     if (a->transform == EKV_ENTMAX && !(a->alpha > 1.0f)) return fail(EKV_ERR_INVALID_ARG, "alpha must be > 1");
+    if (a->tau_halley < 0 || a->tau_halley > 32) return fail(EKV_ERR_INVALID_ARG, "tau_halley must be in 0..32");
     return EKV_OK;
 }
 
@@ -426,6 +427,7 @@ ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t 
     A.nch = nch; A.page_idx = pi; A.n_sel = ns; A.sel_stride = stride; A.full = full;
     A.Hq = Hq; A.G = Hq / c->n_kv_heads; A.alpha = attn->alpha; A.transform = attn->transform;
     A.out = out; A.tau_out = tau; A.supp_out = supp;
+    A.approx_h = attn->tau_halley > 0 ? attn->tau_halley : 0;
     if (attn->transform == EKV_SOFTMAX) {
         // a6: split dense-V softmax (flash-decoding chunks) + ordered combine
         const int nch = full ? (c->max_pages_per_seq + kSmxPages - 1) / kSmxPages : (stride + kSmxPages - 1) / kSmxPages;

@@ -480,6 +480,7 @@ struct TauArgs {
     int32_t *tok_list; double *p_list; int32_t *n_list; int list_cap;     // eval list
     int no_pv;                                                            // tau/supp only (dense-V)
     int cap, pr;                                                          // tau kernel capacities
+    int approx_h;                                                         // > 0: approximate tau, Halley steps
 };
 
 template <typename T>

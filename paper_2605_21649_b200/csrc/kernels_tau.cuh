@@ -381,6 +381,70 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
     ph_stamp<6>(1);
     ph_count<6>(0, ncand);
 
+    // ---- approximate tau (attn flag: the paper's kernel recipe; DESIGN R23): histogram
+    // initialisation over (z_max - 1, z_max] with the certified lower bound of F at the bin
+    // edges, then A.approx_h Halley steps; support {z > tau}; PV below (candidate rounds)
+    bool staged = false;
+    if (A.approx_h > 0) {
+        __shared__ unsigned hcnt[64];
+        __shared__ double s_t0;
+        if (threadIdx.x < 64) hcnt[threadIdx.x] = 0u;
+        __syncthreads();
+        for (int k = threadIdx.x; k < ncand; k += NT) {
+            const double z = a * (double)zs[k];
+            if (!(z > zmax - 1.0)) continue;
+            const double fb = floor((zmax - z) * 64.0);
+            atomicAdd(&hcnt[fb > 63.0 ? 63 : (int)fb], 1u);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            // lane l: edges k = l + 1 and l + 33; the same b-ascending sums as the oracle
+            double lb0 = 0.0, lb1 = 0.0;
+            const int k0 = lane + 1, k1 = lane + 33;
+            for (int bb = 0; bb < k1; ++bb) {
+                const double term1 = __dmul_rn((double)hcnt[bb], powB<IB>((double)(k1 - 1 - bb) / 64.0, beta));
+                lb1 = __dadd_rn(lb1, term1);
+                if (bb < k0) {
+                    const double term0 = __dmul_rn((double)hcnt[bb], powB<IB>((double)(k0 - 1 - bb) / 64.0, beta));
+                    lb0 = __dadd_rn(lb0, term0);
+                }
+            }
+            const unsigned m0 = __ballot_sync(0xffffffffu, lb0 >= 1.0), m1 = __ballot_sync(0xffffffffu, lb1 >= 1.0);
+            int kst = 0;
+            if (m0) kst = __ffs(m0);             // smallest k with LB_k >= 1
+            else if (m1) kst = 32 + __ffs(m1);
+            if (lane == 0) s_t0 = kst ? zmax - (double)kst / 64.0 : zmax - 1.0;
+        }
+        __syncthreads();
+        double t = s_t0;
+        for (int it = 0; it < A.approx_h; ++it) {
+            double S0 = 0.0, S1 = 0.0, S2 = 0.0, dz = 0.0;
+            for (int k = threadIdx.x; k < ncand; k += NT) {
+                const double w = a * (double)zs[k] - t;
+                if (w > 0.0) {
+                    S0 += powB<IB>(w, beta);
+                    S1 += powBm1<IB>(w, beta);
+                    S2 += (IB == 1) ? 0.0 : (IB == 2 ? 1.0 : (IB == 3 ? w : (IB == 4 ? w * w : pow(w, beta - 2.0))));
+                }
+            }
+            Rd.sum(S0, S1);
+            Rd.sum(S2, dz);
+            const double f = S0 - 1.0, fp = -beta * S1, fpp = beta * (beta - 1.0) * S2;
+            const double den = 2.0 * fp * fp - f * fpp;
+            if (!(den != 0.0)) break;
+            t -= 2.0 * f * fp / den;
+        }
+        int mine = 0;
+        for (int k = threadIdx.x; k < ncand; k += NT) {
+            const bool in = a * (double)zs[k] > t;
+            cin[k] = in ? 1 : 0;
+            mine += in;
+        }
+        mine = block_sum_i<NT>(mine, shi);
+        if (threadIdx.x == 0) { s_tau = t; s_kk = (double)mine; s_mode = 0; s_nsup = 0; s_psum = 0.0; }
+        __syncthreads();
+    } else {
+
     // ---- 2. fp32 Newton steps (pruning point only)
     float tf = (float)tau_lo;
     for (int it = 0; it < 3; ++it) {      // Newton from the left: every iterate is below tau
@@ -432,7 +496,7 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
     }
     if (np < 0) { base = tau_lo; np = build(base, Fb); }
     const bool listed = np <= pr;
-    const bool staged = np <= kTsVpre;
+    staged = np <= kTsVpre;
     if (staged) {
         // V rows of the list entries -> shared memory, in flight during step 4
         constexpr int CH = kD * (int)sizeof(T) / 16;          // 16-byte chunks per row
@@ -667,6 +731,7 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
             s_mode = one_round ? (staged ? 2 : 1) : 0;
         }
     }
+    }   // exact tau
     if (staged) cp_async_commit_wait_all();
     __syncthreads();
     ph_stamp<6>(4);

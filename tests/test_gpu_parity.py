@@ -186,6 +186,29 @@ def test_sparse_attend_oracle_pages(case, alpha):
             _check_attend(hc, qh, b, h, G, lists[b, h], alpha, 0, out[b, h], tau[b, h], supp[b, h], tol_for(dt))
 
 
+@pytest.mark.parametrize("case", CASES, ids=ids)
+@pytest.mark.parametrize("alpha,h", [(1.5, 1), (1.5, 2), (1.25, 2), (2.0, 1)])
+def test_sparse_attend_approx_tau(case, alpha, h):
+    """N1: the paper's approximate threshold (histogram init + h Halley steps) vs the
+    oracle's step-by-step version of the same recipe."""
+    B, sl, Hq, Hkv, dt = case
+    wl, dc, hc = make_pair(B, sl, Hq, Hkv, dtype=dt, seed=37, kind="planted" if B < 3 else "randn")
+    G = Hq // Hkv
+    qh = q_host(wl)
+    box, _, _ = ekv.score_pages(dc, wl.q.cuda(), modes=1)
+    pi, ns, _ = ekv.select(dc, Hq, ekv.select_params("topk", 12), box=box)
+    out, tau, supp = ekv.sparse_attend(dc, wl.q.cuda(), pi, ns, ekv.attn_params(alpha, tau_halley=h))
+    torch.cuda.synchronize()
+    out, tau, supp = out.cpu().numpy(), tau.cpu().numpy(), supp.cpu().numpy()
+    for b in range(B):
+        for h_ in range(Hq):
+            ob, _, _ = hc.score_pages(qh[b, h_], b, h_ // G, modes=1)
+            ref = hc.attend(qh[b, h_], b, h_ // G, oracle.topk(ob, 12), alpha, approx_halley=h)
+            np.testing.assert_allclose(out[b, h_], ref["o"], atol=tol_for(dt), rtol=0, err_msg=f"b={b} h={h_}")
+            assert abs(tau[b, h_] - ref["tau"]) <= 1e-6 * max(1.0, abs(ref["tau"])), (b, h_)
+            assert supp[b, h_] == ref["supp"], (b, h_)
+
+
 @pytest.mark.parametrize("case", CASES[:4], ids=ids)
 def test_sparse_softmax_same_kernels(case):
     B, sl, Hq, Hkv, dt = case

@@ -455,3 +455,36 @@ def test_gauss_select_properties():
     # q_page = 0.5, c = 1 -> sbar = mu exactly
     zq5 = oracle.zq_table(0.5, 16)
     assert abs(zq5[1]) < 1e-15
+
+
+# --------------------------------------------------------------------------- approximate tau (N1)
+@pytest.mark.parametrize("alpha", [1.25, 1.5, 1.75, 2.0])
+def test_approx_tau_converges_to_exact(alpha):
+    """The paper's kernel recipe (histogram init + Halley; DESIGN R23): with enough
+    Halley steps it reaches the exact threshold, which is itself pinned to the closed forms
+    and to brute force above."""
+    rng = np.random.default_rng(11)
+    for trial in range(20):
+        z = (alpha - 1.0) * rng.standard_normal(int(rng.integers(2, 400))) * rng.uniform(0.3, 3.0)
+        _, t_ex, k_ex = oracle.entmax(z, alpha)
+        p, t, k = oracle.entmax_approx(z, alpha, 8)
+        assert abs(t - t_ex) <= 1e-12 * max(1.0, abs(t_ex))
+        assert k == k_ex
+        assert abs(p.sum() - 1.0) <= 1e-10
+
+
+@pytest.mark.parametrize("alpha", [1.25, 1.5, 2.0])
+def test_approx_tau_initialisation_is_a_lower_bound(alpha):
+    """h = 0: tau_0 is a bin edge whose certified lower bound of F reaches 1, so F(tau_0) >= 1,
+    tau_0 <= tau and {z > tau_0} contains the exact support (nothing is dropped before the
+    Halley steps); tau_0 >= z_max - 1."""
+    beta = 1.0 / (alpha - 1.0)
+    rng = np.random.default_rng(12)
+    for trial in range(30):
+        z = (alpha - 1.0) * rng.standard_normal(int(rng.integers(1, 500)))
+        _, t_ex, k_ex = oracle.entmax(z, alpha)
+        _, t0, k0 = oracle.entmax_approx(z, alpha, 0)
+        F0 = np.sum(np.maximum(z - t0, 0.0) ** beta)
+        assert F0 >= 1.0 - 1e-12
+        assert z.max() - 1.0 - 1e-12 <= t0 <= t_ex + 1e-12
+        assert k0 >= k_ex
