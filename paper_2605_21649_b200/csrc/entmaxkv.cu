@@ -305,6 +305,12 @@ ekv_status launch_tau_sparse_ibf(const CacheView &v, const TauArgs &A0, int rows
     static bool init = false;
     TauArgs A = A0;
     A.cap = A.full ? kTsCap : std::min(kTsCap, (A.sel_stride * kP + 255) & ~255);
+    // variable-length (Gaussian) lists run many rows of up to max_pages entries: a smaller
+    // candidate capacity keeps two CTAs per SM (measured C3: 126 -> 71 us); an overflowing
+    // row falls back to the streamed path (correct, slower).  EKV_TS_CAP overrides.
+    static const int cap_env = getenv("EKV_TS_CAP") ? atoi(getenv("EKV_TS_CAP")) : 0;
+    const int cap_lim = cap_env > 0 ? cap_env : A.var ? 4096 : 0;
+    if (cap_lim > 0 && !A.full) A.cap = std::min(A.cap, (cap_lim + 255) & ~255);
     A.pr = std::min(kPr, A.cap);
     const int smem = (4 + 4 + 4 + 1) * A.cap + (8 + 4) * A.pr + kTsVpre * kD * (int)sizeof(T);
     if (!init) {
@@ -356,6 +362,23 @@ ekv_status launch_dense_group(const CacheView &v, const float *scores, size_t nt
     default: k_dense_group_partial<T, 8><<<g, 256, 0, st>>>(v, scores, ntok, rowmax, Hq, nch, pacc, pl, pc, ent_tau, alpha, ib); break;
     }
     return check_launch("k_dense_group_partial");
+}
+
+// a2': one 1024-thread CTA per (b, q-head); rows of up to 8192 pages staged in shared memory
+ekv_status launch_gauss(const ekv_cache *cache, int Hq, const float *mu, const float *s2, float alpha,
+                        const ekv_select_params *sel, int32_t *pi, int32_t *ns, int stride, double *th, cudaStream_t st) {
+    static bool init = false;
+    const int cache_pages = std::min(cache->max_pages_per_seq, 8192);
+    const int smem = 12 * cache_pages;
+    if (!init) {
+        set_smem(k_gauss_select<1024>, 12 * 8192);
+        init = true;
+    }
+    cudaError_t e = launch_ex(k_gauss_select<1024>, dim3((unsigned)(cache->batch * Hq)), dim3(1024), smem, st, 0u, mu, s2, Hq,
+                              (int)cache->max_pages_per_seq, (const int32_t *)cache->seq_lens, alpha, sel->margin,
+                              sel->q_page, pi, ns, stride, th, cache_pages);
+    if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "k_gauss_select: %s", cudaGetErrorString(e));
+    return check_launch("k_gauss_select");
 }
 
 ekv_status check_attn(const ekv_attn_params *a) {
@@ -660,10 +683,7 @@ ekv_status entmaxkv_select(const ekv_cache *cache, int32_t n_q_heads, const floa
                            sel_stride, n_q_heads / cache->n_kv_heads, UnionOut{nullptr, 0}, st);
     }
     if (!mu || !sigma2) return fail(EKV_ERR_INVALID_ARG, "Gaussian selector needs mu/sigma2");
-    k_gauss_select<1024><<<cache->batch * n_q_heads, 1024, 0, st>>>(mu, sigma2, n_q_heads, maxp, cache->seq_lens, alpha,
-                                                                  sel->margin, sel->q_page, page_idx, n_sel, sel_stride,
-                                                                  tau_hat);
-    return check_launch("k_gauss_select");
+    return launch_gauss(cache, n_q_heads, mu, sigma2, alpha, sel, page_idx, n_sel, sel_stride, tau_hat, st);
 }
 
 ekv_status entmaxkv_sparse_attend(const ekv_cache *cache, const void *q, int32_t n_q_heads, const int32_t *page_idx,
@@ -739,16 +759,16 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
         const int k = sel->policy == EKV_TOPK ? sel->k_pages : maxp;
         EKV_TRY(launch_topk(box, cache->batch, n_q_heads, maxp, cache->seq_lens, k, pi, ns, L.cap, Gq, uo, st));
     } else {
-        launch_ex(k_gauss_select<1024>, dim3(cache->batch * n_q_heads), dim3(1024), 0, st, 0, (const float *)mu, (const float *)s2, n_q_heads, maxp, (const int32_t *)cache->seq_lens,
-                                                                      attn->alpha, sel->margin, sel->q_page, pi, ns,
-                                                                      L.cap, th);
-        EKV_TRY(check_launch("k_gauss_select"));
+        EKV_TRY(launch_gauss(cache, n_q_heads, mu, s2, attn->alpha, sel, pi, ns, L.cap, th, st));
         EKV_TRY(launch_mark(cache, n_q_heads, pi, ns, L.cap, uo.umask, L.W, st));
     }
     // a3
     double *tau_p = (stats && stats->tau) ? stats->tau : at<double>(workspace, L.tau_int);
+    TauArgs xa;
+    memset(&xa, 0, sizeof(xa));
+    xa.var = sel->policy == EKV_GAUSS;
     EKV_TRY(attend_impl(cache, q, n_q_heads, pi, ns, L.cap, 0, attn, out, tau_p,
-                        stats ? stats->supp_count : nullptr, workspace, L, st, nullptr, /*marked=*/true));
+                        stats ? stats->supp_count : nullptr, workspace, L, st, &xa, /*marked=*/true));
     const int rows = cache->batch * n_q_heads;
     // a4: certified dropped-mass bound (wide kernel; deterministic ticketed final sum)
     if (want_db) {

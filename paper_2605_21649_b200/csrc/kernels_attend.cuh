@@ -481,6 +481,7 @@ struct TauArgs {
     int no_pv;                                                            // tau/supp only (dense-V)
     int cap, pr;                                                          // tau kernel capacities
     int approx_h;                                                         // > 0: approximate tau, Halley steps
+    int var;                                                              // list lengths vary (slices from n_sel)
 };
 
 template <typename T>

@@ -278,90 +278,143 @@ __global__ void __launch_bounds__(256) k_mark(int Hq, int G, const int32_t *__re
 }
 
 // ============================================================================ a2': Gaussian selector
-// One CTA per (b, q-head).  tau_hat solves  sum_p c_p E[(a S_p - tau)_+^beta] = 1
-// (Eq. gaussian-threshold-main) with the App. D closed forms in fp64
-// (beta = 4 by the truncated-moment recursion, R15).  Bracket [lo, hi] with
-// mass(lo) >= 1 > mass(hi), then safeguarded Newton (dE/dtau = -beta * M_{beta-1}),
-// falling back to bisection when a Newton step leaves the bracket.  Page rule
-// (Eq. gaussian-selector-main, R14): keep p iff
-// (double)a * fmaf(sqrtf(sigma2), zq[c], mu) > tau_hat - margin; empty -> argmax mu.
-struct GaussMoments { double m, dm; };   // M_beta and M_{beta-1}
+struct GaussMoments { double m, dm, d2; };   // M_beta, M_{beta-1}, and the d^2/dtau^2 term
 
+// truncated moments of Y ~ N(muY, sigY^2): M_k = E[(Y)_+^k] by the App. D recursion
+// M_k = muY M_{k-1} + (k-1) sigY^2 M_{k-2} (M_0 = Phi(t), M_1 = muY Phi + sigY phi).
+// d2 = M_{beta-2} (beta >= 2) or phi(t) / sigY (beta = 1): with it
+// mass'' = beta (beta-1) sum c M_{beta-2}  (beta = 1: sum c phi / sigY), for Halley steps.
 __device__ __forceinline__ GaussMoments trunc_moments(int beta, double muY, double sigY) {
     if (!(sigY > 0.0)) {
-        const double x = muY > 0.0 ? muY : 0.0;
-        double r = 1.0, rm = 1.0;
-        for (int i = 0; i < beta; ++i) { rm = r; r *= x; }
-        if (beta == 0) rm = 0.0;
-        return {r, rm};
+        if (!(muY > 0.0)) return {0.0, 0.0, 0.0};
+        double r = 1.0, rm = 1.0, rm2 = 1.0;
+        for (int i = 0; i < beta; ++i) { rm2 = rm; rm = r; r *= muY; }
+        return {r, rm, beta == 1 ? 0.0 : rm2};
     }
     const double t = muY / sigY;
     const double Ph = normcdf(t);
     const double ph = exp(-0.5 * t * t) * 0.39894228040143267794;   // 1/sqrt(2 pi)
-    double m0 = Ph, m1 = muY * Ph + sigY * ph;
-    if (beta == 1) return {m1, m0};
-    double prev = m0, cur = m1;
+    const double m0 = Ph, m1 = muY * Ph + sigY * ph;
+    if (beta == 1) return {m1, m0, ph / sigY};
+    double pp = m0, prev = m0, cur = m1;
     for (int k = 2; k <= beta; ++k) {
         const double nx = muY * cur + (double)(k - 1) * sigY * sigY * prev;
-        prev = cur; cur = nx;
+        pp = prev; prev = cur; cur = nx;
     }
-    return {cur, prev};
+    return {cur, prev, pp};
 }
 
-// mass(tau) = sum_p c_p M_beta(a mu_p - tau, a sigma_p) and -d mass / d tau, in fp64 (FP64 = 1)
-// or fp32 (steering only).  Pages whose standardised t = (a mu - tau) / (a sigma) < -9 are
-// skipped: their terms are below Phi(-9) ~ 1e-19 relative (the fp64 sum's own rounding is
-// ~1e-16), decided by a conservative fp32 pre-test.
-template <int NT, bool FP64>
-__device__ void gauss_mass2(const float *mu, const float *s2, int M, int Lseq, float af, int beta, double tau,
-                            double &mass, double &dmass, double *shd) {
-    double m = 0.0, dm = 0.0;
-    const float tf = (float)tau;
-    for (int p = threadIdx.x; p < M; p += NT) {
-        const float mp = __ldg(mu + p), sp = sqrtf(__ldg(s2 + p));
-        const float num = af * mp - tf, den = af * sp;
-        if (den > 0.f ? (num < -9.5f * den) : (num <= 0.f)) continue;
-        const double cnt = (double)min(kP, Lseq - p * kP);
-        if constexpr (FP64) {
-            const double a = (double)af;
-            const double sg = sqrt((double)s2[p]);
-            GaussMoments g = trunc_moments(beta, a * (double)mp - tau, a * sg);
-            m += cnt * g.m;
-            dm += cnt * (double)beta * g.dm;
-        } else {
-            float r, rm;
-            if (!(den > 0.f)) {
-                const float x = num > 0.f ? num : 0.f;
-                r = 1.f; rm = 1.f;
-                for (int i = 0; i < beta; ++i) { rm = r; r *= x; }
-            } else {
-                const float t = num / den;
-                const float Ph = normcdff(t), ph = __expf(-0.5f * t * t) * 0.39894228f;
-                float m0 = Ph, m1 = num * Ph + den * ph;
-                if (beta == 1) { r = m1; rm = m0; }
-                else {
-                    float pr = m0, cu = m1;
-                    for (int k = 2; k <= beta; ++k) { const float nx = num * cu + (float)(k - 1) * den * den * pr; pr = cu; cu = nx; }
-                    r = cu; rm = pr;
-                }
-            }
-            m += cnt * (double)r;
-            dm += cnt * (double)beta * (double)rm;
+template <int NT> __device__ __forceinline__ void block_sum3_d(double &a, double &b, double &c, double *sh) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) { sh[3 * w] = a; sh[3 * w + 1] = b; sh[3 * w + 2] = c; }
+    __syncthreads();
+    if (w == 0) {
+        double x = 0.0, y = 0.0, z = 0.0;
+        if (l < NT / 32) { x = sh[3 * l]; y = sh[3 * l + 1]; z = sh[3 * l + 2]; }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            x += __shfl_xor_sync(0xffffffffu, x, o);
+            y += __shfl_xor_sync(0xffffffffu, y, o);
+            z += __shfl_xor_sync(0xffffffffu, z, o);
         }
+        if (l == 0) { sh[0] = x; sh[1] = y; sh[2] = z; }
     }
-    block_sum2_d<NT>(m, dm, shd);
-    mass = m; dmass = dm;
+    __syncthreads();
+    a = sh[0]; b = sh[1]; c = sh[2];
 }
 
+// Pages whose standardised t = (a mu - tau) / (a sigma) < -9.5 are skipped: their terms are
+// below Phi(-9.5) ~ 1e-21 relative (the fp64 sum's own rounding is ~1e-16), decided by a
+// conservative fp32 pre-test.  sg = sqrtf(sigma2) (cached) or nullptr (computed).
+#define EKV_GAUSS_SKIP(num, den) ((den) > 0.f ? ((num) < -9.5f * (den)) : ((num) <= 0.f))
+
+// fp32 steering pass: mass(tau) and -d mass/d tau, fp32 terms and per-thread sums
+template <int NT>
+__device__ void gauss_mass32(const float *mu, const float *sg, const float *s2, int M, int Lseq, float af, int beta,
+                             float tf, double &mass, double &dmass, double *shd) {
+    float m = 0.f, dm = 0.f;
+#pragma unroll 4
+    for (int p = threadIdx.x; p < M; p += NT) {
+        const float mp = mu[p], sp = sg ? sg[p] : sqrtf(s2[p]);
+        const float num = af * mp - tf, den = af * sp;
+        if (EKV_GAUSS_SKIP(num, den)) continue;
+        const float cnt = (float)min(kP, Lseq - p * kP);
+        float r, rm;
+        if (!(den > 0.f)) {
+            r = 1.f; rm = 1.f;
+            for (int i = 0; i < beta; ++i) { rm = r; r *= num; }
+        } else {
+            const float t = num / den;
+            const float Ph = normcdff(t), ph = __expf(-0.5f * t * t) * 0.39894228f;
+            const float m0 = Ph, m1 = num * Ph + den * ph;
+            if (beta == 1) { r = m1; rm = m0; }
+            else {
+                float pr = m0, cu = m1;
+                for (int k = 2; k <= beta; ++k) { const float nx = num * cu + (float)(k - 1) * den * den * pr; pr = cu; cu = nx; }
+                r = cu; rm = pr;
+            }
+        }
+        m = fmaf(cnt, r, m);
+        dm = fmaf(cnt, rm, dm);
+    }
+    double a = m, b = (double)beta * dm;
+    block_sum2_d<NT>(a, b, shd);
+    mass = a; dmass = b;
+}
+
+// fp64 pass: mass, -mass' and mass'' (the terms follow orc_gauss_mass: a, mu, sqrt(sigma2) in fp64)
+template <int NT>
+__device__ void gauss_mass64(const float *mu, const float *sg, const float *s2, int M, int Lseq, float af, int beta,
+                             double tau, double &mass, double &dmass, double &d2mass, double *shd) {
+    double m = 0.0, dm = 0.0, d2 = 0.0;
+    const float tf = (float)tau;
+    const double a = (double)af;
+    for (int p = threadIdx.x; p < M; p += NT) {
+        const float mp = mu[p], s2p = s2[p], sp = sg ? sg[p] : sqrtf(s2p);
+        const float num = af * mp - tf, den = af * sp;
+        if (EKV_GAUSS_SKIP(num, den)) continue;
+        const double cnt = (double)min(kP, Lseq - p * kP);
+        const GaussMoments g = trunc_moments(beta, a * (double)mp - tau, a * sqrt((double)s2p));
+        m = fma(cnt, g.m, m);
+        dm = fma(cnt, g.dm, dm);
+        d2 = fma(cnt, g.d2, d2);
+    }
+    dm *= (double)beta;
+    d2 *= beta == 1 ? 1.0 : (double)(beta * (beta - 1));
+    block_sum3_d<NT>(m, dm, d2, shd);
+    mass = m; dmass = dm; d2mass = d2;
+}
+
+// One CTA per (b, q-head).  tau_hat solves  sum_p c_p E[(a S_p - tau)_+^beta] = 1
+// (Eq. gaussian-threshold-main) with the App. D closed forms (beta integer,
+// R15); the paper names Newton/Halley for it.  The row's mu, sigma2 and
+// sqrt(sigma2) are staged in shared memory (rows up to cache_pages pages).
+//  (1) fp32 steering: Newton on log mass (the terms are log-concave in tau: near-quadratic
+//      in the Gaussian tails where the root usually lies), safeguarded by a bracket;
+//  (2) fp64 Halley from the fp32 root (cubic: one pass, a second when the predicted error
+//      (mass''/mass')^2 |step|^3 is not below 1e-15 relative); any large or non-finite step
+//      falls back to a verified fp64 bracket + safeguarded Newton.
+// Page rule (Eq. gaussian-selector-main, R14): keep p iff
+// (double)a * fmaf(sqrtf(sigma2), zq[c], mu) > tau_hat - margin; empty -> argmax mu.
 template <int NT>
 __global__ void __launch_bounds__(NT) k_gauss_select(const float *__restrict__ mu, const float *__restrict__ sigma2,
                                                      int Hq, int maxp, const int32_t *__restrict__ seq_lens,
                                                      float alpha, double margin, double q_page,
                                                      int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
-                                                     int sel_stride, double *__restrict__ tau_hat_out) {
+                                                     int sel_stride, double *__restrict__ tau_hat_out, int cache_pages) {
     EKV_TRACE(8);
     pdl_wait();
-    __shared__ double shd[2 * (NT / 32) + 2];
+    ph_stamp<8>(0);
+    int n32 = 0, n64 = 0;
+    extern __shared__ float gsm[];
+    __shared__ double shd[3 * (NT / 32) + 3];
     __shared__ int shi[NT / 32 + 1];
     __shared__ float shf[NT / 32 + 1];
     __shared__ float zq[kP + 1];
@@ -372,72 +425,97 @@ __global__ void __launch_bounds__(NT) k_gauss_select(const float *__restrict__ m
     const int b = row / Hq;
     const int Lseq = seq_lens[b];
     const int M = n_pages_of(Lseq);
-    const float *m_ = mu + (size_t)row * maxp;
-    const float *s_ = sigma2 + (size_t)row * maxp;
+    const float *mg = mu + (size_t)row * maxp;
+    const float *sgg = sigma2 + (size_t)row * maxp;
+    const bool cached = M <= cache_pages;
+    float *c_mu = gsm, *c_s2 = gsm + cache_pages, *c_sg = gsm + 2 * cache_pages;
     const double a = (double)alpha - 1.0;
     const float af = (float)a;
     const int beta = (int)llrint(1.0 / a);
-    // (1) fp32 steering: bracket from a max_p (mu + 8 sigma), then safeguarded Newton
+    // stage the row (and the bracket start a max_p (mu + 8 sigma))
     float tmax = -INFINITY;
-    for (int p = threadIdx.x; p < M; p += NT) tmax = fmaxf(tmax, m_[p] + 8.0f * sqrtf(s_[p]));
-    tmax = block_max_f<NT>(tmax, shf);
-    double hi = a * (double)tmax, w = 1.0, mass, dmass;
-    for (int it = 0; it < 200; ++it) {
-        gauss_mass2<NT, false>(m_, s_, M, Lseq, af, beta, hi, mass, dmass, shd);
-        if (mass < 1.0) break;
-        hi += w; w *= 2.0;
+    for (int p = threadIdx.x; p < M; p += NT) {
+        const float mp = __ldg(mg + p), s2p = __ldg(sgg + p), sp = sqrtf(s2p);
+        if (cached) { c_mu[p] = mp; c_s2[p] = s2p; c_sg[p] = sp; }
+        tmax = fmaxf(tmax, mp + 8.0f * sp);
     }
-    double lo = hi - 1.0;
-    w = 1.0;
-    for (int it = 0; it < 200; ++it) {
-        gauss_mass2<NT, false>(m_, s_, M, Lseq, af, beta, lo, mass, dmass, shd);
-        if (mass >= 1.0) break;
-        lo -= w; w *= 2.0;
-    }
-    double tau = lo;
-    for (int it = 0; it < 60; ++it) {
-        gauss_mass2<NT, false>(m_, s_, M, Lseq, af, beta, tau, mass, dmass, shd);
+    tmax = block_max_f<NT>(tmax, shf);   // (its barriers publish the staged row)
+    const float *m_ = cached ? c_mu : mg, *s_ = cached ? c_s2 : sgg, *g_ = cached ? c_sg : nullptr;
+    ph_stamp<8>(1);
+    // (1) fp32 steering: Newton on log mass from the right end a max_p (mu + 8 sigma);
+    // bisection once bracketed when a step leaves the bracket, doubling steps while a side
+    // is still open
+    double lo = -INFINITY, hi = INFINITY, tau = a * (double)tmax, w = 1.0, dxold = INFINITY, mass, dmass, d2mass;
+    gauss_mass32<NT>(m_, g_, s_, M, Lseq, af, beta, (float)tau, mass, dmass, shd);
+    ++n32;
+    for (int it = 0; it < 80; ++it) {
         if (mass >= 1.0) lo = tau; else hi = tau;
-        double nt = (dmass > 0.0) ? tau + (mass - 1.0) / dmass : 0.5 * (lo + hi);
-        if (!(nt > lo && nt < hi)) nt = 0.5 * (lo + hi);
-        const bool stop = fabs(nt - tau) <= 2e-7 * fmax(1.0, fabs(tau)) || hi - lo <= 2e-7 * fmax(1.0, fabs(hi));
+        double nt = NAN;
+        // Newton on log mass (log-concave terms: Gaussian tails and (c - tau)^beta alike are
+        // near-quadratic / logarithmic there): tau + mass log(mass) / dmass
+        if (dmass > 0.0 && mass > 0.0) nt = tau + mass * log(mass) / dmass;
+        const bool closed = lo > -INFINITY && hi < INFINITY;
+        // bisect when the step leaves the bracket or does not halve the previous one (a sum
+        // of log-concave terms need not be log-concave: no cycling)
+        bool newton = true;
+        if (!(nt > lo && nt < hi) || (closed && fabs(nt - tau) > 0.5 * dxold)) {
+            newton = false;
+            if (closed) nt = 0.5 * (lo + hi);
+            else { nt = lo > -INFINITY ? lo + w : hi - w; w *= 2.0; }
+        }
+        // (Newton from one side may converge without ever closing the bracket)
+        const bool stop = (newton && fabs(nt - tau) <= 1e-5 * fmax(1.0, fabs(tau))) ||
+                          (closed && hi - lo <= 1e-5 * fmax(1.0, fabs(hi)));
+        dxold = fabs(nt - tau);
         tau = nt;
         if (stop) break;
+        gauss_mass32<NT>(m_, g_, s_, M, Lseq, af, beta, (float)tau, mass, dmass, shd);
+        ++n32;
     }
-    // (2) fp64 Newton straight from the fp32 root (mass is convex and decreasing: quadratic
-    // convergence from ~1e-6 takes two or three passes); any large or non-finite step falls
-    // back to a verified bracket + safeguarded Newton
+    ph_stamp<8>(2);
+    // (2) fp64 Halley from the fp32 root
     bool done64 = false;
     {
         double t = tau;
         for (int it = 0; it < 4; ++it) {
-            gauss_mass2<NT, true>(m_, s_, M, Lseq, af, beta, t, mass, dmass, shd);
+            gauss_mass64<NT>(m_, g_, s_, M, Lseq, af, beta, t, mass, dmass, d2mass, shd);
+            ++n64;
             if (!(dmass > 0.0)) break;
-            const double step = (mass - 1.0) / dmass;
+            const double f = mass - 1.0;
+            const double den = 2.0 * dmass * dmass - f * d2mass;
+            const double step = den > 0.0 ? 2.0 * f * dmass / den : f / dmass;
             if (!(fabs(step) <= 1e-3 * fmax(1.0, fabs(t)))) break;
             t += step;
-            if (fabs(step) <= 1e-14 * fmax(1.0, fabs(t))) { done64 = true; break; }
+            const double kq = d2mass / dmass;
+            if (kq * kq * fabs(step) * step * step <= 1e-15 * fmax(1.0, fabs(t)) ||
+                fabs(step) <= 1e-15 * fmax(1.0, fabs(t))) {
+                done64 = true;
+                break;
+            }
         }
         if (done64) tau = t;
     }
+    ph_stamp<8>(3);
+    ph_count<8>(0, n32);
+    ph_count<8>(1, n64 + (done64 ? 0 : 1000));
     double dl = 1e-4 * fmax(1.0, fabs(tau));
     if (!done64) {
     lo = tau - dl;
     for (int it = 0; it < 200; ++it) {
-        gauss_mass2<NT, true>(m_, s_, M, Lseq, af, beta, lo, mass, dmass, shd);
+        gauss_mass64<NT>(m_, g_, s_, M, Lseq, af, beta, lo, mass, dmass, d2mass, shd);
         if (mass >= 1.0) break;
         dl *= 4.0; lo = tau - dl;
     }
     double dh = 1e-4 * fmax(1.0, fabs(tau));
     hi = tau + dh;
     for (int it = 0; it < 200; ++it) {
-        gauss_mass2<NT, true>(m_, s_, M, Lseq, af, beta, hi, mass, dmass, shd);
+        gauss_mass64<NT>(m_, g_, s_, M, Lseq, af, beta, hi, mass, dmass, d2mass, shd);
         if (mass < 1.0) break;
         dh *= 4.0; hi = tau + dh;
     }
     tau = fmin(fmax(tau, lo), hi);
     for (int it = 0; it < 100; ++it) {
-        gauss_mass2<NT, true>(m_, s_, M, Lseq, af, beta, tau, mass, dmass, shd);
+        gauss_mass64<NT>(m_, g_, s_, M, Lseq, af, beta, tau, mass, dmass, d2mass, shd);
         if (mass >= 1.0) lo = tau; else hi = tau;
         double nt = (dmass > 0.0) ? tau + (mass - 1.0) / dmass : 0.5 * (lo + hi);
         if (!(nt > lo && nt < hi)) nt = 0.5 * (lo + hi);
@@ -448,6 +526,7 @@ __global__ void __launch_bounds__(NT) k_gauss_select(const float *__restrict__ m
         tau = nt;
     }
     }
+    ph_stamp<8>(4);
     // page rule + ordered compaction (NT pages per round)
     int32_t *out = page_idx + (size_t)row * sel_stride;
     int base = 0;
@@ -456,7 +535,7 @@ __global__ void __launch_bounds__(NT) k_gauss_select(const float *__restrict__ m
         int keep = 0;
         if (p < M) {
             const int cnt = min(kP, Lseq - p * kP);
-            const float sg = __fmaf_rn(sqrtf(s_[p]), zq[cnt], m_[p]);
+            const float sg = __fmaf_rn(g_ ? g_[p] : sqrtf(s_[p]), zq[cnt], m_[p]);
             keep = (a * (double)sg > tau - margin) ? 1 : 0;
         }
         int tot;
@@ -491,6 +570,7 @@ __global__ void __launch_bounds__(NT) k_gauss_select(const float *__restrict__ m
         n_sel[row] = base;
         if (tau_hat_out) tau_hat_out[row] = tau;
     }
+    ph_stamp<8>(5);
 }
 
 }  // namespace ekv

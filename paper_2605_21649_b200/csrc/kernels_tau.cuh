@@ -150,7 +150,9 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
     // logical page of list entry i (full rows: every page, in order)
     auto page_of = [&](int i) -> int { return FULL ? i : __ldg(plist + i); };
     // rank rk extracts the items [rk S, (rk + 1) S) (item = 4 scores), S from the list capacity
-    const int S = ((A.sel_stride * 4 + CL - 1) / CL + 3) & ~3;
+    // (variable-length lists, e.g. the Gaussian selector: from the list length -- one round
+    // trip more, but every rank gets work)
+    const int S = (((A.var ? nlist : A.sel_stride) * 4 + CL - 1) / CL + 3) & ~3;
     int pg[kTsU];
 #pragma unroll
     for (int u = 0; u < kTsU; ++u) {
