@@ -348,15 +348,19 @@ def test_gaussian_select(case, alpha):
             assert pi[b, h, :ns[b, h]].tolist() == ref.tolist()
 
 
-def test_decode_gauss_end_to_end():
-    B, sl, Hq, Hkv = 2, [2048, 1333], 8, 2
-    wl, dc, hc = make_pair(B, sl, Hq, Hkv, seed=31, kind="planted")
+@pytest.mark.parametrize("sl,alpha,kind", [([2048, 1333], 1.5, "planted"), ([32768], 1.25, "randn"),
+                                           ([20000], 1.5, "randn")], ids=["small", "wide-a1.25", "randn-a1.5"])
+def test_decode_gauss_end_to_end(sl, alpha, kind):
+    """Gaussian selector -> tau kernel with variable-length lists (slices from n_sel; the
+    wide case overflows the 4096-candidate capacity and takes the streamed path)."""
+    B, Hq, Hkv = len(sl), 8, 2
+    wl, dc, hc = make_pair(B, sl, Hq, Hkv, seed=31, kind=kind)
     G = Hq // Hkv
     qh = q_host(wl)
     sel = ekv.select_params("gauss", q_page=0.99, margin=0.1)
     ws = ekv.alloc_workspace(dc, Hq, sel)
     st = ekv.DecodeStats(B, Hq, "cuda", delta_bar=False, gauss=True)
-    out = ekv.decode(dc, wl.q.cuda(), sel, ekv.attn_params(1.5), ws, stats=st)
+    out = ekv.decode(dc, wl.q.cuda(), sel, ekv.attn_params(alpha), ws, stats=st)
     torch.cuda.synchronize()
     out = out.cpu().numpy()
     zq = oracle.zq_table(0.99, 16)
@@ -364,9 +368,9 @@ def test_decode_gauss_end_to_end():
         counts = hc.page_counts(b)
         for h in range(Hq):
             _, om, os2 = hc.score_pages(qh[b, h], b, h // G, modes=2)
-            pages = oracle.gauss_select(om, os2, counts, 1.5, float(st.tau_hat[b, h]), 0.1, zq)
+            pages = oracle.gauss_select(om, os2, counts, alpha, float(st.tau_hat[b, h]), 0.1, zq)
             assert int(st.n_sel[b, h]) == len(pages)
-            ref = hc.attend(qh[b, h], b, h // G, pages, 1.5)
+            ref = hc.attend(qh[b, h], b, h // G, pages, alpha)
             np.testing.assert_allclose(out[b, h], ref["o"], atol=2e-3, rtol=0)
             assert int(st.supp_count[b, h]) == ref["supp"]
 
