@@ -360,15 +360,36 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
             return;
         }
             // overflow: fp64 Newton streamed over the whole row moves tau_lo just below tau
-            const int ntk = nlist * kP;
+            // (items of 4 scores, 8 in flight per thread: the row is read from L2 once per pass)
+            const int nit = nlist * 4;
             double t = tau_lo;
             for (int it = 0; it < 200; ++it) {
                 double F = 0.0, Fd = 0.0;
-                for (int e = threadIdx.x; e < ntk; e += NT) {
-                    const int j = page_of(e / kP) * kP + e % kP;
-                    if (j >= L) continue;
-                    const double d = a * (double)srow[j] - t;
-                    if (d > 0.0) { F += powB<IB>(d, beta); Fd += powBm1<IB>(d, beta); }
+                for (int r0 = 0; r0 < nit; r0 += 8 * NT) {
+                    int pv[8];
+                    float4 v4[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int e = r0 + threadIdx.x + NT * u;
+                        pv[u] = e < nit ? page_of(e >> 2) : -1;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int e = r0 + threadIdx.x + NT * u;
+                        if (pv[u] >= 0) v4[u] = *reinterpret_cast<const float4 *>(srow + (size_t)pv[u] * kP + 4 * (e & 3));
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        if (pv[u] < 0) continue;
+                        const int e = r0 + threadIdx.x + NT * u;
+                        const int j0 = pv[u] * kP + 4 * (e & 3);
+                        const float sv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const double d = a * (double)sv[q] - t;
+                            if (j0 + q < L && d > 0.0) { F += powB<IB>(d, beta); Fd += powBm1<IB>(d, beta); }
+                        }
+                    }
                 }
                 Rd.sum(F, Fd);
                 if (!(Fd > 0.0)) break;

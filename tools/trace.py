@@ -19,7 +19,7 @@ wl = make_workload(B, n, Hq, Hkv, seed=1, device=dev, spare_tokens=200)
 c = ekv.PagedCache.allocate_meta(wl.K, wl.V, wl.page_table, wl.seq_lens)
 ekv.rebuild_page_stats(c)
 sel = ekv.select_params('topk' if policy == 'full' else policy, k)
-attn = ekv.attn_params(1.5)
+attn = ekv.attn_params(float(__import__('os').environ.get('TRACE_ALPHA', '1.5')))
 ws = ekv.alloc_workspace(c, Hq, sel)
 st = ekv.DecodeStats(B, Hq, dev, delta_bar=True, gauss=policy == 'gauss')
 q, kn, vn = new_tokens(B, Hq, Hkv, seed=7, device=dev)
