@@ -108,6 +108,51 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 // FULL: full-cache rows (candidates from k_candidates' chunk regions, eval lists); the decode
 // path instantiates FULL = false, which keeps only the sparse code (less instruction fetch:
 // the kernel runs once per step on cold instruction caches)
+// Overflow path of k_tau_sparse: fp64 Newton on ||(z - t)_+||_beta - 1 streamed over the
+// whole list
+template <int NT, int IB>
+__device__ __noinline__ double streamed_newton(const float *srow, const int32_t *plist, bool full, int nlist, int L,
+                                               double a, double beta, double t0, BlockRed2<NT> &Rd) {
+    // (items of 4 scores, 8 in flight per thread: the row is read from L2 once per pass)
+    const int nit = nlist * 4;
+    double t = t0;
+    for (int it = 0; it < 200; ++it) {
+        double F = 0.0, Fd = 0.0;
+        for (int r0 = 0; r0 < nit; r0 += 8 * NT) {
+            int pv[8];
+            float4 v4[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = r0 + threadIdx.x + NT * u;
+                pv[u] = e < nit ? (full ? (e >> 2) : __ldg(plist + (e >> 2))) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = r0 + threadIdx.x + NT * u;
+                if (pv[u] >= 0) v4[u] = *reinterpret_cast<const float4 *>(srow + (size_t)pv[u] * kP + 4 * (e & 3));
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (pv[u] < 0) continue;
+                const int e = r0 + threadIdx.x + NT * u;
+                const int j0 = pv[u] * kP + 4 * (e & 3);
+                const float sv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double d = a * (double)sv[q] - t;
+                    if (j0 + q < L && d > 0.0) { F += powB<IB>(d, beta); Fd += powBm1<IB>(d, beta); }
+                }
+            }
+        }
+        Rd.sum(F, Fd);
+        if (!(Fd > 0.0)) break;
+        const double step = lbeta_step(F, Fd, beta, IB);
+        t += step;
+        if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(t)))) break;
+    }
+    return t;
+}
+
 template <typename T, int IB, bool FULL>
 __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A) {
     EKV_TRACE(6);
@@ -360,43 +405,8 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
             return;
         }
             // overflow: fp64 Newton streamed over the whole row moves tau_lo just below tau
-            // (items of 4 scores, 8 in flight per thread: the row is read from L2 once per pass)
-            const int nit = nlist * 4;
-            double t = tau_lo;
-            for (int it = 0; it < 200; ++it) {
-                double F = 0.0, Fd = 0.0;
-                for (int r0 = 0; r0 < nit; r0 += 8 * NT) {
-                    int pv[8];
-                    float4 v4[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int e = r0 + threadIdx.x + NT * u;
-                        pv[u] = e < nit ? page_of(e >> 2) : -1;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int e = r0 + threadIdx.x + NT * u;
-                        if (pv[u] >= 0) v4[u] = *reinterpret_cast<const float4 *>(srow + (size_t)pv[u] * kP + 4 * (e & 3));
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        if (pv[u] < 0) continue;
-                        const int e = r0 + threadIdx.x + NT * u;
-                        const int j0 = pv[u] * kP + 4 * (e & 3);
-                        const float sv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const double d = a * (double)sv[q] - t;
-                            if (j0 + q < L && d > 0.0) { F += powB<IB>(d, beta); Fd += powBm1<IB>(d, beta); }
-                        }
-                    }
-                }
-                Rd.sum(F, Fd);
-                if (!(Fd > 0.0)) break;
-                const double step = lbeta_step(F, Fd, beta, IB);
-                t += step;
-                if (!(fabs(step) > 1e-12 * fmax(1.0, fabs(t)))) break;
-            }
+            // (out of line: the hot path's code stays contiguous -- cold instruction fetch)
+            const double t = streamed_newton<NT, IB>(srow, plist, FULL, nlist, L, a, beta, tau_lo, Rd);
             tau_lo = fmax(tau_lo, t - 1e-7 * fmax(1.0, fabs(t)));
         newton_done = true;
     }
