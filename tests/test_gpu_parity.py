@@ -348,6 +348,27 @@ def test_gaussian_select(case, alpha):
             assert pi[b, h, :ns[b, h]].tolist() == ref.tolist()
 
 
+def test_gaussian_select_uncached_long_row():
+    """Rows longer than the selector's 8192-page shared-memory stage read mu / sigma2 from
+    global memory (140000 tokens = 8750 pages)."""
+    B, sl, Hq, Hkv = 1, [140000], 4, 1
+    wl, dc, hc = make_pair(B, sl, Hq, Hkv, seed=37, kind="planted")
+    qh = q_host(wl)
+    _, mu, s2 = ekv.score_pages(dc, wl.q.cuda(), modes=2)
+    sel = ekv.select_params("gauss", q_page=0.99, margin=0.05)
+    pi, ns, th = ekv.select(dc, Hq, sel, alpha=1.5, mu=mu, sigma2=s2)
+    torch.cuda.synchronize()
+    pi, ns, th = pi.cpu().numpy(), ns.cpu().numpy(), th.cpu().numpy()
+    zq = oracle.zq_table(0.99, 16)
+    counts = hc.page_counts(0)
+    for h in range(Hq):
+        _, om, os2 = hc.score_pages(qh[0, h], 0, h // Hq, modes=2)
+        t_ref = oracle.gauss_tau(om, os2, counts, 1.5)
+        assert abs(th[0, h] - t_ref) <= 1e-10 * max(1.0, abs(t_ref)), (h, th[0, h], t_ref)
+        ref = oracle.gauss_select(om, os2, counts, 1.5, th[0, h], 0.05, zq)
+        assert pi[0, h, :ns[0, h]].tolist() == ref.tolist()
+
+
 @pytest.mark.parametrize("sl,alpha,kind", [([2048, 1333], 1.5, "planted"), ([32768], 1.25, "randn"),
                                            ([20000], 1.5, "randn")], ids=["small", "wide-a1.25", "randn-a1.5"])
 def test_decode_gauss_end_to_end(sl, alpha, kind):
