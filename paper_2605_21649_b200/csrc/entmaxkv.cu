@@ -364,21 +364,31 @@ ekv_status launch_dense_group(const CacheView &v, const float *scores, size_t nt
     return check_launch("k_dense_group_partial");
 }
 
-// a2': one 1024-thread CTA per (b, q-head); rows of up to 8192 pages staged in shared memory
-ekv_status launch_gauss(const ekv_cache *cache, int Hq, const float *mu, const float *s2, float alpha,
-                        const ekv_select_params *sel, int32_t *pi, int32_t *ns, int stride, double *th, cudaStream_t st) {
+// a2': one CTA per (b, q-head); rows of up to 8192 pages staged in shared memory.  Many rows
+// (>= 2 per SM): 512-thread CTAs, two per SM, so one row's reductions overlap the other's
+// passes (C3: 244 -> 212 us); few rows: 1024 threads per row.
+template <int NT>
+ekv_status launch_gauss_nt(const ekv_cache *cache, int Hq, const float *mu, const float *s2, float alpha,
+                           const ekv_select_params *sel, int32_t *pi, int32_t *ns, int stride, double *th,
+                           cudaStream_t st) {
     static bool init = false;
     const int cache_pages = std::min(cache->max_pages_per_seq, 8192);
     const int smem = 12 * cache_pages;
     if (!init) {
-        set_smem(k_gauss_select<1024>, 12 * 8192);
+        set_smem(k_gauss_select<NT>, 12 * 8192);
         init = true;
     }
-    cudaError_t e = launch_ex(k_gauss_select<1024>, dim3((unsigned)(cache->batch * Hq)), dim3(1024), smem, st, 0u, mu, s2, Hq,
+    cudaError_t e = launch_ex(k_gauss_select<NT>, dim3((unsigned)(cache->batch * Hq)), dim3(NT), smem, st, 0u, mu, s2, Hq,
                               (int)cache->max_pages_per_seq, (const int32_t *)cache->seq_lens, alpha, sel->margin,
                               sel->q_page, pi, ns, stride, th, cache_pages);
     if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "k_gauss_select: %s", cudaGetErrorString(e));
     return check_launch("k_gauss_select");
+}
+ekv_status launch_gauss(const ekv_cache *cache, int Hq, const float *mu, const float *s2, float alpha,
+                        const ekv_select_params *sel, int32_t *pi, int32_t *ns, int stride, double *th, cudaStream_t st) {
+    if (cache->batch * Hq >= 2 * 148)
+        return launch_gauss_nt<512>(cache, Hq, mu, s2, alpha, sel, pi, ns, stride, th, st);
+    return launch_gauss_nt<1024>(cache, Hq, mu, s2, alpha, sel, pi, ns, stride, th, st);
 }
 
 ekv_status check_attn(const ekv_attn_params *a) {

@@ -404,7 +404,7 @@ __device__ void gauss_mass64(const float *mu, const float *sg, const float *s2, 
 // Page rule (Eq. gaussian-selector-main, R14): keep p iff
 // (double)a * fmaf(sqrtf(sigma2), zq[c], mu) > tau_hat - margin; empty -> argmax mu.
 template <int NT>
-__global__ void __launch_bounds__(NT) k_gauss_select(const float *__restrict__ mu, const float *__restrict__ sigma2,
+__global__ void __launch_bounds__(NT, 1024 / NT) k_gauss_select(const float *__restrict__ mu, const float *__restrict__ sigma2,
                                                      int Hq, int maxp, const int32_t *__restrict__ seq_lens,
                                                      float alpha, double margin, double q_page,
                                                      int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
