@@ -181,6 +181,8 @@ def gauss_tau(mu, sigma2, counts, alpha):
     t = np.zeros(1, np.float64)
     rc = lib().orc_gauss_tau(_p(mu, ctypes.c_float), _p(sigma2, ctypes.c_float), _p(counts, ctypes.c_int32),
                              mu.shape[0], float(alpha), _p(t, ctypes.c_double))
+    if rc == -2:
+        raise ValueError(f"Gaussian tau_hat needs an integer beta = 1/(alpha-1) (alpha={alpha})")
     if rc != 0:
         raise RuntimeError("tau_hat bracket failure")
     return float(t[0])

@@ -413,7 +413,10 @@ double orc_gauss_mass(const float *mu, const float *sigma2, const int32_t *count
                       int M, double alpha, double tau)
 {
     double a = alpha - 1.0;
-    int beta = (int)lround(1.0 / a);
+    double bd = 1.0 / a;
+    int beta = (int)lround(bd);
+    /* the closed forms need an integer beta (App. D); any other alpha is rejected (NaN)  */
+    if (!(fabs(bd - (double)beta) <= 1e-12) || beta < 1) return NAN;
     double m = 0.0;
     for (int p = 0; p < M; ++p) {
         double s = sqrt((double)sigma2[p]);
@@ -426,11 +429,12 @@ double orc_gauss_mass(const float *mu, const float *sigma2, const int32_t *count
 /* non-increasing in tau and strictly decreasing where positive.       */
 /* Plain bracketing + bisection to fp64 resolution (the paper's Newton/Halley */
 /* is a faster route to the same root).  Returns 0 on success, -1 on a bracket */
-/* failure.                                                                    */
+/* failure, -2 for a non-integer beta (no closed form; see orc_gauss_mass).    */
 int orc_gauss_tau(const float *mu, const float *sigma2, const int32_t *counts,
                   int M, double alpha, double *tau_hat)
 {
     double a = alpha - 1.0, top = -INFINITY;
+    if (isnan(orc_gauss_mass(mu, sigma2, counts, 0, alpha, 0.0))) return -2;   /* non-integer beta */
     for (int p = 0; p < M; ++p) {
         double v = a * ((double)mu[p] + 8.0 * sqrt((double)sigma2[p]));
         if (v > top) top = v;

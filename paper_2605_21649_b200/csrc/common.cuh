@@ -4,24 +4,16 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include "types.cuh"
 
 namespace ekv {
 
-constexpr int kD = 128;   // head_dim = value_dim (R1)
-constexpr int kP = 16;    // page size
-constexpr float kCd = 0x1.6a09e6p-4f;   // fl32(1/sqrt(128)) (R2)
-
-struct CacheView {
-    int dtype, B, Hkv, maxp, nphys;
-    const void *K, *V;
-    void *Kw, *Vw;            // writable aliases (append)
-    void *kmin, *kmax;
-    float *ksum, *ksumsq, *kavg, *kvar;
-    const int32_t *page_table;
-    int32_t *seq_lens;
-};
-
 __device__ __forceinline__ int n_pages_of(int L) { return (L + kP - 1) / kP; }
+
+// union mark of one selected page: bit g of the page's byte (fire-and-forget atomic)
+__device__ __forceinline__ void union_mark(uint32_t *um, int p, int g) {
+    atomicOr(um + (p >> 2), 1u << ((p & 3) * 8 + g));
+}
 
 // ---------------------------------------------------------------- element access
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
@@ -357,12 +349,6 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 namespace ekv {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
-// zero a byte range (16-byte aligned, multiple of 16) -- replaces a memset node in the chain
-__global__ void __launch_bounds__(256) k_zero(uint4 *p, size_t n16) {
-    pdl_launch();
-    pdl_wait();
-    for (size_t i = blockIdx.x * 256 + threadIdx.x; i < n16; i += (size_t)gridDim.x * 256) p[i] = make_uint4(0, 0, 0, 0);
-}
 }  // namespace ekv
 
 // ---------------------------------------------------------------- optional in-kernel phase stamps
@@ -370,7 +356,7 @@ __global__ void __launch_bounds__(256) k_zero(uint4 *p, size_t n16) {
 // (ns) at checkpoints into ekv_stamps[kernel_slot][i]; read with entmaxkv_debug_stamps().
 namespace ekv {
 #ifdef EKV_STAMPS
-__device__ unsigned long long ekv_stamps[8][32];
+static __device__ unsigned long long ekv_stamps[8][32];
 __device__ __forceinline__ void stamp(int k, int i) {
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
         unsigned long long t;
@@ -391,7 +377,7 @@ __device__ __forceinline__ void stamp_if(bool cond, int k, int i) {
 #ifndef EKV_CTA_KERNEL
 #define EKV_CTA_KERNEL 1
 #endif
-__device__ unsigned long long ekv_cta[4][1024];
+static __device__ unsigned long long ekv_cta[4][1024];
 template <int KID> __device__ __forceinline__ void stamp_cta(bool cond, int which) {
     if (KID == EKV_CTA_KERNEL && cond && blockIdx.x < 1024) {
         unsigned long long t;
@@ -407,8 +393,8 @@ template <int KID> __device__ __forceinline__ void count_cta(bool cond, unsigned
 #ifndef EKV_PH_KERNEL
 #define EKV_PH_KERNEL 6
 #endif
-__device__ unsigned long long ekv_ph[8][1024];
-__device__ long long ekv_phc[2][1024];
+static __device__ unsigned long long ekv_ph[8][1024];
+static __device__ long long ekv_phc[2][1024];
 template <int KID> __device__ __forceinline__ void ph_stamp(int phase) {
     if (KID == EKV_PH_KERNEL && threadIdx.x == 0 && blockIdx.x < 1024) {
         unsigned long long t;
@@ -420,7 +406,7 @@ template <int KID> __device__ __forceinline__ void ph_count(int which, long long
     if (KID == EKV_PH_KERNEL && threadIdx.x == 0 && blockIdx.x < 1024) ekv_phc[which][blockIdx.x] = v;
 }
 // whole-kernel trace: first CTA start (min) and last CTA end (max, thread 0 of each CTA)
-__device__ unsigned long long ekv_trace[16][2];
+static __device__ unsigned long long ekv_trace[16][2];
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -436,6 +422,26 @@ struct TraceScope {
     }
 };
 #define EKV_TRACE(kid) ::ekv::TraceScope ekv_trace_scope_(kid)
+// host side: every translation unit has its own (static) stamp buffers and registers a
+// reader for them; the entmaxkv_debug_* calls merge the readers' results
+static void tu_debug_read(int what, void *out, int reset) {
+    switch (what) {
+    case 0:
+        if (reset) {
+            unsigned long long init[16][2];
+            for (int i = 0; i < 16; ++i) { init[i][0] = ~0ull; init[i][1] = 0ull; }
+            cudaMemcpyToSymbol(ekv_trace, init, sizeof(init));
+        } else {
+            cudaMemcpyFromSymbol(out, ekv_trace, sizeof(ekv_trace));
+        }
+        break;
+    case 1: cudaMemcpyFromSymbol(out, ekv_cta, sizeof(ekv_cta)); break;
+    case 2: cudaMemcpyFromSymbol(out, ekv_ph, sizeof(ekv_ph)); break;
+    case 3: cudaMemcpyFromSymbol(out, ekv_phc, sizeof(ekv_phc)); break;
+    default: cudaMemcpyFromSymbol(out, ekv_stamps, sizeof(ekv_stamps)); break;
+    }
+}
+static struct TuDebugReg { TuDebugReg() { debug_register(&tu_debug_read); } } tu_debug_reg;
 #else
 #define EKV_TRACE(kid) do {} while (0)
 template <int KID> __device__ __forceinline__ void ph_stamp(int) {}

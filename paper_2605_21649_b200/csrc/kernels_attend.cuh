@@ -365,8 +365,7 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
 // region cand[row][chunk][0..kCpc) and its count into ccount[row][chunk]; the tau
 // kernel concatenates the chunks in order, so the candidate order is deterministic.
 // (max_pages <= 65536 -> at most 256 chunks per row.)
-constexpr int kCpc = 1024;          // candidates per chunk region
-__global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ scores, size_t ntok,
+static __global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ scores, size_t ntok,
                                                     const uint32_t *__restrict__ rowmax,
                                                     const int32_t *__restrict__ page_idx,
                                                     const int32_t *__restrict__ n_sel, int sel_stride,
@@ -466,24 +465,6 @@ __global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ sc
 
 // ============================================================================ exact tau + PV
 // The tau / support / PV kernel is k_tau_sparse (kernels_tau.cuh); the shared pieces live here.
-constexpr int kTauNT = 256;
-constexpr int kCap = 12288;         // shared-memory candidate capacity
-constexpr int kPr = 2048;           // pruned-list capacity (tau solver)
-constexpr int kTauSmem = (8 + 1 + 4) * kCap + (8 + 4) * kPr;
-
-struct TauArgs {
-    const float *scores; size_t ntok;
-    const uint32_t *rowmax; const int *ccount; const float *cand_s; const int32_t *cand_j; int nch;
-    const int32_t *page_idx; const int32_t *n_sel; int sel_stride; int full;
-    int Hq, G; float alpha; int transform;
-    float *out; double *tau_out; int32_t *supp_out;
-    int32_t *tok_list; double *p_list; int32_t *n_list; int list_cap;     // eval list
-    int no_pv;                                                            // tau/supp only (dense-V)
-    int cap, pr;                                                          // tau kernel capacities
-    int approx_h;                                                         // > 0: approximate tau, Halley steps
-    int var;                                                              // list lengths vary (slices from n_sel)
-};
-
 template <typename T>
 __device__ __forceinline__ void ldv4(const T *vr, float (&vx)[4]) {
     if constexpr (sizeof(T) == 2) {
@@ -514,11 +495,6 @@ __device__ __forceinline__ double lbeta_step(double F, double Fd, double beta, i
 // marks its row's selected pages of the chunk in a shared bitmap, sums its chunk
 // (deterministic block tree) into partial[row][chunk]; the last CTA of a row (ticket
 // counter) adds the partials in chunk order, so the result is deterministic.
-constexpr int kDbChunk = 8192;   // pages per CTA: 256 threads x 8 groups of 4 pages
-struct DbConst {                 // per-call constants of alpha (host-computed)
-    double a, beta, inv_a;       // a = alpha - 1, beta = 1/a
-    int ib;                      // integer beta in 1..4, else 0
-};
 // delta_bar (R16, P:409-420 certificate): per (b, q-head) row, sum over the UNSELECTED
 // valid pages p of n_p * ((alpha-1) * box_p - tau)_+^beta.  Grid (chunks, rows), the
 // chunks of a row form one thread-block cluster (<= 8).  Every thread issues its 8 float4
@@ -603,7 +579,7 @@ __global__ void __launch_bounds__(256) k_delta_bar(const float *__restrict__ box
 // against the sparse selection (ascending page list of head h): delta = sum of p_j
 // whose page is not selected (Eq. delta), recovered = |S cap C_tok|,
 // full_supp = |S| (Eq. rho).
-__global__ void __launch_bounds__(256) k_eval_metrics(const int32_t *__restrict__ tok_list, const double *__restrict__ p_list,
+static __global__ void __launch_bounds__(256) k_eval_metrics(const int32_t *__restrict__ tok_list, const double *__restrict__ p_list,
                                                       const int32_t *__restrict__ n_list, int list_cap,
                                                       const int32_t *__restrict__ page_idx, const int32_t *__restrict__ n_sel,
                                                       int sel_stride, double *delta, int32_t *recovered, int32_t *full_supp) {

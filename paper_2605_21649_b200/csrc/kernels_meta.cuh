@@ -4,6 +4,13 @@
 
 namespace ekv {
 
+// zero a byte range (16-byte aligned, multiple of 16) -- replaces a memset node in the chain
+static __global__ void __launch_bounds__(256) k_zero(uint4 *p, size_t n16) {
+    pdl_launch();
+    pdl_wait();
+    for (size_t i = blockIdx.x * 256 + threadIdx.x; i < n16; i += (size_t)gridDim.x * 256) p[i] = make_uint4(0, 0, 0, 0);
+}
+
 // ============================================================================ a0: append_kv
 // One CTA per sequence; thread (h, i) owns dimension i of kv head h (loops when
 // Hkv*D > blockDim).  Token t of the call goes to position L + t.  Statistics are

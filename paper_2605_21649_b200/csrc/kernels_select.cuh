@@ -26,13 +26,6 @@ namespace ekv {
 //  3. Selection bitmap (bit = page), one word per thread (t < 256), block scan + cluster
 //     offsets: ascending page ids, and -- if umask != NULL -- the KV-group union marks.
 //     (512 threads, 2 CTAs per SM: the 256 CTAs of a 32-row, 65536-page launch are one wave.)
-constexpr int kTkKPT = 16;                  // keys per thread; NT = 512 (8192 pages per CTA,
-                                            // <= 8 CTAs -> 65536 pages) or 256 for short rows
-
-// union mark of one selected page: bit g of the page's byte (fire-and-forget atomic)
-__device__ __forceinline__ void union_mark(uint32_t *um, int p, int g) {
-    atomicOr(um + (p >> 2), 1u << ((p & 3) * 8 + g));
-}
 
 // bitmap word of the CTA-local pages 2048 j + 4 t + e (e < 4) of a 4-bit nibble per thread:
 // 8 consecutive lanes share a word (index 64 j + t / 8); lane t % 8 == 0 returns it
@@ -263,7 +256,7 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
 // u32, bit g = selected by query head g of the group), zeroed by the host and filled
 // with atomicOr from the page lists.  The K-score kernel walks the G page lists of a
 // group and keeps a page only from its lowest selecting head (one read per union page).
-__global__ void __launch_bounds__(256) k_mark(int Hq, int G, const int32_t *__restrict__ page_idx,
+static __global__ void __launch_bounds__(256) k_mark(int Hq, int G, const int32_t *__restrict__ page_idx,
                                               const int32_t *__restrict__ n_sel, int sel_stride,
                                               uint32_t *__restrict__ umask, int W) {
     EKV_TRACE(3);

@@ -29,13 +29,9 @@
 
 namespace ekv {
 
-constexpr int kShT = 62;                 // interior probes per multisection round (6 bits)
-constexpr int kShP = kShT + 2;           // probe points incl. the bracket ends
-constexpr int kShCap = 8192;             // local candidates per row
-constexpr int kShSums = 5;               // S_0 .. S_4
 
 // 1a. (score, global page) of the rank's selected pages; padding: -inf / -1
-__global__ void __launch_bounds__(256) k_shard_pack(const float *__restrict__ box, int maxp,
+static __global__ void __launch_bounds__(256) k_shard_pack(const float *__restrict__ box, int maxp,
                                                     const int32_t *__restrict__ page_idx,
                                                     const int32_t *__restrict__ n_sel, int stride, int kc,
                                                     int rank, int world, float *__restrict__ cs,
@@ -57,9 +53,7 @@ __global__ void __launch_bounds__(256) k_shard_pack(const float *__restrict__ bo
 
 // 1b. global top-k among the W gathered lists (recv_s / recv_g: [W][rows][kc]); this rank's
 // selected entries come from its own (ascending) segment, so the output stays ascending.
-constexpr int kShMergeNT = 1024;
-constexpr int kShMergeKPT = 16;          // W * kc <= 16384
-__global__ void __launch_bounds__(kShMergeNT) k_shard_merge(const float *__restrict__ recv_s,
+static __global__ void __launch_bounds__(kShMergeNT) k_shard_merge(const float *__restrict__ recv_s,
                                                             const int32_t *__restrict__ recv_g, int rows,
                                                             int kc, int k, int rank, int world,
                                                             const int32_t *__restrict__ gseq,
@@ -134,20 +128,15 @@ __global__ void __launch_bounds__(kShMergeNT) k_shard_merge(const float *__restr
 }
 
 // 2. local row max (ordered key, 0 = empty) -> fp32 (-inf when empty)
-__global__ void k_shard_zmax(const uint32_t *__restrict__ rowmax, int rows, float *__restrict__ zmax) {
+static __global__ void k_shard_zmax(const uint32_t *__restrict__ rowmax, int rows, float *__restrict__ zmax) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < rows) zmax[i] = rowmax[i] ? key2f(rowmax[i]) : -INFINITY;
 }
 
-struct ShardRow {                        // per-row multisection state (device)
-    double lo, hi;                       // F(lo) >= 1 > F(hi)
-    double cgt_lo, cge_hi;               // #{z > lo}, #{z >= hi} (global)
-    int done, rounds;
-};
 
 // 3. local candidates {z > z_max - 1} of the row's score list (list-ordered reads);
 //    initialises the bracket [a z_max - 1 - eps, a z_max]
-__global__ void __launch_bounds__(256) k_shard_cand(const float *__restrict__ scores, size_t ntok,
+static __global__ void __launch_bounds__(256) k_shard_cand(const float *__restrict__ scores, size_t ntok,
                                                     const int32_t *__restrict__ page_idx,
                                                     const int32_t *__restrict__ n_sel, int stride,
                                                     const int32_t *__restrict__ seq_lens, const int32_t *__restrict__ ptab,
@@ -268,7 +257,7 @@ __global__ void __launch_bounds__(256) k_shard_probe(const double *__restrict__ 
 }
 
 // host-visible convergence summary: number of rows still open
-__global__ void k_shard_open(const ShardRow *__restrict__ st, int rows, int *__restrict__ open) {
+static __global__ void k_shard_open(const ShardRow *__restrict__ st, int rows, int *__restrict__ open) {
     __shared__ int sh[9];
     int c = 0;
     for (int i = threadIdx.x; i < rows; i += 256) c += st[i].done == 0;
@@ -277,7 +266,7 @@ __global__ void k_shard_open(const ShardRow *__restrict__ st, int rows, int *__r
 }
 
 // 5a. power sums of w = z - lo over the local support
-__global__ void __launch_bounds__(256) k_shard_sums(const double *__restrict__ cz, const int32_t *__restrict__ ncand,
+static __global__ void __launch_bounds__(256) k_shard_sums(const double *__restrict__ cz, const int32_t *__restrict__ ncand,
                                                     const ShardRow *__restrict__ st, double *__restrict__ sums) {
     __shared__ double wp[8][kShSums];
     const int row = blockIdx.x;
@@ -305,7 +294,7 @@ __global__ void __launch_bounds__(256) k_shard_sums(const double *__restrict__ c
 }
 
 // 5b. tau from the all-reduced power sums: sum_m C(beta, m) (-delta)^(beta - m) S_m = 1
-__global__ void k_shard_tau(const double *__restrict__ sums, int ib, ShardRow *__restrict__ st, int rows,
+static __global__ void k_shard_tau(const double *__restrict__ sums, int ib, ShardRow *__restrict__ st, int rows,
                             double *__restrict__ tau, int32_t *__restrict__ supp) {
     const int row = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= rows) return;
@@ -398,7 +387,7 @@ __global__ void __launch_bounds__(256) k_shard_pv(CacheView c, const double *__r
 }
 
 // 6b. out = num / den; NaN rows (overflow / unconverged) stay NaN
-__global__ void k_shard_out(const float *__restrict__ num, const double *__restrict__ den,
+static __global__ void k_shard_out(const float *__restrict__ num, const double *__restrict__ den,
                             const double *__restrict__ tau, int rows, float *__restrict__ out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= rows * kD) return;
@@ -411,7 +400,7 @@ __global__ void k_shard_out(const float *__restrict__ num, const double *__restr
 
 namespace ekv {
 // global |C_page| = min(k, global pages) per row
-__global__ void k_shard_nsel(const int32_t *__restrict__ gseq, int Hq, int rows, int k, int32_t *__restrict__ n_sel) {
+static __global__ void k_shard_nsel(const int32_t *__restrict__ gseq, int Hq, int rows, int k, int32_t *__restrict__ n_sel) {
     const int row = blockIdx.x * blockDim.x + threadIdx.x;
     if (row < rows) n_sel[row] = min(k, n_pages_of(gseq[row / Hq]));
 }

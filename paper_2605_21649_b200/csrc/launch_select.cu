@@ -1,0 +1,58 @@
+// launch_select.cu -- launches of the a2 (top-k), a2' (Gaussian selector) and union-mark kernels.
+#include <algorithm>
+#include "host.h"
+#include "kernels_select.cuh"
+
+namespace ekvh {
+
+// top-k: one cluster of CL CTAs per row, CL = pages / 8192 rounded up to a power of two
+ekv_status launch_topk(const float *box, int B, int Hq, int maxp, const int32_t *sl, int k, int32_t *pi, int32_t *ns,
+                       int stride, int G, const UnionOut &u, cudaStream_t st) {
+    // short rows: 256-thread CTAs (more CTAs per SM when there are many rows)
+    const int NT = maxp <= 4096 ? 256 : 512;
+    const int per = NT * kTkKPT;
+    int CL = 1;
+    while (CL * per < maxp) CL *= 2;
+    if (CL > 8) return fail(EKV_ERR_UNSUPPORTED, "top-k supports at most %d pages", 8 * per);
+    cudaError_t e = NT == 256
+        ? launch_ex(k_topk<256>, dim3((unsigned)(B * Hq * CL)), dim3(256), 0, st, (unsigned)CL, box, Hq, maxp, sl, k,
+                    pi, ns, stride, G, u.umask, u.W)
+        : launch_ex(k_topk<512>, dim3((unsigned)(B * Hq * CL)), dim3(512), 0, st, (unsigned)CL, box, Hq, maxp, sl, k,
+                    pi, ns, stride, G, u.umask, u.W);
+    if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "k_topk: %s", cudaGetErrorString(e));
+    return check_launch("k_topk");
+}
+
+ekv_status launch_mark(int B, int Hq, int G, const int32_t *pi, const int32_t *ns, int stride, uint32_t *um, int W,
+                       cudaStream_t st) {
+    launch_ex(k_mark, dim3(B * Hq), dim3(256), 0, st, 0, Hq, G, pi, ns, stride, um, W);
+    return check_launch("k_mark");
+}
+
+// a2': one CTA per (b, q-head); rows of up to 8192 pages staged in shared memory.  Many rows
+// (>= 2 per SM): 512-thread CTAs, two per SM, so one row's reductions overlap the other's
+// passes (C3: 244 -> 212 us); few rows: 1024 threads per row.
+template <int NT>
+static ekv_status launch_gauss_nt(const ekv_cache *cache, int Hq, const float *mu, const float *s2, float alpha,
+                                  const ekv_select_params *sel, int32_t *pi, int32_t *ns, int stride, double *th,
+                                  cudaStream_t st) {
+    const int cache_pages = std::min(cache->max_pages_per_seq, 8192);
+    const int smem = 12 * cache_pages;
+    set_smem(k_gauss_select<NT>, 12 * 8192);
+    cudaError_t e = launch_ex(k_gauss_select<NT>, dim3((unsigned)(cache->batch * Hq)), dim3(NT), smem, st, 0u, mu, s2, Hq,
+                              (int)cache->max_pages_per_seq, (const int32_t *)cache->seq_lens, alpha, sel->margin,
+                              sel->q_page, pi, ns, stride, th, cache_pages);
+    if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "k_gauss_select: %s", cudaGetErrorString(e));
+    return check_launch("k_gauss_select");
+}
+ekv_status launch_gauss(const ekv_cache *cache, int Hq, const float *mu, const float *s2, float alpha,
+                        const ekv_select_params *sel, int32_t *pi, int32_t *ns, int stride, double *th, cudaStream_t st) {
+    // the block size (and so the fp64 reduction order of tau_hat) depends on the number of rows:
+    // tau_hat is reproducible per (batch, heads) configuration, and within 1e-10 relative of the
+    // oracle either way (R14)
+    if (cache->batch * Hq >= 2 * num_sms())
+        return launch_gauss_nt<512>(cache, Hq, mu, s2, alpha, sel, pi, ns, stride, th, st);
+    return launch_gauss_nt<1024>(cache, Hq, mu, s2, alpha, sel, pi, ns, stride, th, st);
+}
+
+}  // namespace ekvh
