@@ -115,6 +115,9 @@ typedef struct {
  *   delta f64 exact dropped mass (Eq. delta),
  *   recovered i32 |S cap C_tok|, full_supp i32 |S| (Eq. rho),
  *   tau_full f64.
+ * supp_tok (may be NULL): [batch][n_q_heads][supp_cap] i32, the token positions of S~ (the
+ *   support within C_tok, R9) in ascending order; a row with more than supp_cap support tokens
+ *   gets its first supp_cap (supp_count holds the total).  Entmax only.
  */
 typedef struct {
     double *tau;
@@ -127,6 +130,8 @@ typedef struct {
     int32_t *recovered;
     int32_t *full_supp;
     double *tau_full;
+    int32_t *supp_tok;
+    int32_t supp_cap;
 } ekv_decode_stats;
 
 /* Last error message of the calling thread ("" if none). */

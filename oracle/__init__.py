@@ -52,6 +52,7 @@ def lib():
         L.orc_token_score.argtypes = [f32p, f32p]
         L.orc_token_score.restype = ctypes.c_float
         L.orc_page_stats.argtypes = [f32p, c_int, c_int] + [f32p] * 6
+        L.orc_build_stats.argtypes = [f32p, c_int, c_int, c_int, i32p, i32p, c_int, c_int] + [f32p] * 6
         L.orc_score_pages.argtypes = [f32p, c_int, c_int, f32p, f32p, f32p, f32p,
                                       i32p, c_int, c_int, f32p, f32p, f32p]
         L.orc_topk.argtypes = [f32p, c_int, c_int, i32p]
@@ -254,14 +255,10 @@ class HostCache:
         self.kmin, self.kmax = np.zeros(shp, np.float32), np.zeros(shp, np.float32)
         self.ksum, self.ksumsq = np.zeros(shp, np.float32), np.zeros(shp, np.float32)
         self.kavg, self.kvar = np.zeros(shp, np.float32), np.zeros(shp, np.float32)
-        for b in range(self.page_table.shape[0]):
-            counts = self.page_counts(b)
-            for lp in range(self.n_pages(b)):
-                ph = int(self.page_table[b, lp])
-                for g in range(self.Hkv):
-                    st = page_stats(self.K[ph, g, : counts[lp]])
-                    for n in ("kmin", "kmax", "ksum", "ksumsq", "kavg", "kvar"):
-                        getattr(self, n)[ph, g] = st[n]
+        lib().orc_build_stats(_p(self.K, ctypes.c_float), self.Hkv, self.P, self.d, _p(self.page_table, ctypes.c_int32),
+                              _p(self.seq_lens, ctypes.c_int32), self.page_table.shape[0], self.page_table.shape[1],
+                              *[_p(getattr(self, n), ctypes.c_float)
+                                for n in ("kmin", "kmax", "ksum", "ksumsq", "kavg", "kvar")])
 
     def score_pages(self, q, b, kvh, modes=1):
         q = _f32(q)

@@ -90,6 +90,27 @@ void orc_page_stats(const float *keys, int c, int d, float *kmin, float *kmax,
     }
 }
 
+/* Every valid page of a paged cache (composition of orc_page_stats, no new     */
+/* arithmetic): K [n_phys][Hkv][P][d]; page_table [B][maxp]; seq_lens [B];      */
+/* outputs [n_phys][Hkv][d].  The last page of a sequence holds c <= P tokens.  */
+void orc_build_stats(const float *K, int Hkv, int P, int d, const int32_t *page_table,
+                     const int32_t *seq_lens, int B, int maxp, float *kmin, float *kmax,
+                     float *ksum, float *ksumsq, float *kavg, float *kvar)
+{
+    for (int b = 0; b < B; ++b) {
+        int n = seq_lens[b], M = (n + P - 1) / P;
+        for (int lp = 0; lp < M; ++lp) {
+            int c = (lp == M - 1) ? n - lp * P : P;
+            size_t ph = (size_t)page_table[(size_t)b * maxp + lp];
+            for (int g = 0; g < Hkv; ++g) {
+                size_t o = (ph * Hkv + g) * d;
+                orc_page_stats(K + (ph * Hkv + g) * P * d, c, d, kmin + o, kmax + o,
+                               ksum + o, ksumsq + o, kavg + o, kvar + o);
+            }
+        }
+    }
+}
+
 /* ------------------------------------------------------------------------- */
 /* Query-aware page scoring for ONE query head (kv head kvh) of one sequence. */
 /*  box  = (1/sqrt d) sum_i max(q_i kmin_i, q_i kmax_i)  Eq. box-page-bound    */

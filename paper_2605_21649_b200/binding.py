@@ -63,7 +63,7 @@ class ekv_decode_stats(ctypes.Structure):
     _fields_ = [("tau", ctypes.c_void_p), ("supp_count", ctypes.c_void_p), ("n_sel", ctypes.c_void_p),
                 ("delta_bar", ctypes.c_void_p), ("tau_hat", ctypes.c_void_p), ("eval_exact", ctypes.c_int32),
                 ("delta", ctypes.c_void_p), ("recovered", ctypes.c_void_p), ("full_supp", ctypes.c_void_p),
-                ("tau_full", ctypes.c_void_p)]
+                ("tau_full", ctypes.c_void_p), ("supp_tok", ctypes.c_void_p), ("supp_cap", ctypes.c_int32)]
 
 
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32, ctypes.c_int32,
@@ -294,7 +294,7 @@ def full_attend(cache: PagedCache, q, attn: ekv_attn_params, workspace=None, out
 class DecodeStats:
     """Device buffers for ekv_decode_stats ([B][Hq] each)."""
 
-    def __init__(self, B, Hq, device, delta_bar=True, eval_exact=False, gauss=False):
+    def __init__(self, B, Hq, device, delta_bar=True, eval_exact=False, gauss=False, supp_cap=0):
         f64 = lambda: torch.zeros(B, Hq, dtype=torch.float64, device=device)
         i32 = lambda: torch.zeros(B, Hq, dtype=torch.int32, device=device)
         self.tau, self.supp_count, self.n_sel = f64(), i32(), i32()
@@ -305,11 +305,19 @@ class DecodeStats:
         self.recovered = i32() if eval_exact else None
         self.full_supp = i32() if eval_exact else None
         self.tau_full = f64() if eval_exact else None
+        self.supp_cap = int(supp_cap)
+        self.supp_tok = (torch.full((B, Hq, self.supp_cap), -1, dtype=torch.int32, device=device)
+                         if self.supp_cap > 0 else None)
 
     def c_struct(self):
         return ekv_decode_stats(_ptr(self.tau), _ptr(self.supp_count), _ptr(self.n_sel), _ptr(self.delta_bar),
                                 _ptr(self.tau_hat), int(self.eval_exact), _ptr(self.delta), _ptr(self.recovered),
-                                _ptr(self.full_supp), _ptr(self.tau_full))
+                                _ptr(self.full_supp), _ptr(self.tau_full), _ptr(self.supp_tok), self.supp_cap)
+
+    def support(self, b, h):
+        """Support token positions of row (b, h) (ascending; needs supp_cap > 0)."""
+        n = min(int(self.supp_count[b, h]), self.supp_cap)
+        return self.supp_tok[b, h, :n]
 
 
 def decode(cache: PagedCache, q, sel: ekv_select_params, attn: ekv_attn_params, workspace, out=None,

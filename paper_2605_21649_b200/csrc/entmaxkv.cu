@@ -509,6 +509,10 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
     TauArgs xa;
     memset(&xa, 0, sizeof(xa));
     xa.var = sel->policy == EKV_GAUSS;
+    if (stats && stats->supp_tok && stats->supp_cap > 0 && attn->transform == EKV_ENTMAX) {
+        xa.supp_tok = stats->supp_tok;
+        xa.supp_cap = stats->supp_cap;
+    }
     EKV_TRY(attend_impl(cache, q, n_q_heads, pi, ns, L.cap, 0, attn, out, tau_p,
                         stats ? stats->supp_count : nullptr, workspace, L, st, &xa, /*marked=*/true));
     const int rows = cache->batch * n_q_heads;

@@ -847,6 +847,18 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
         if (A.tau_out) A.tau_out[row] = tau;
         if (A.supp_out) A.supp_out[row] = (int)kk;
     }
+    // support token positions, ascending (candidates are extracted in list order = token order)
+    if (!FULL && A.supp_tok) {
+        int base = 0;
+        for (int r0 = 0; r0 < ncand; r0 += NT) {
+            const int k = r0 + threadIdx.x;
+            const bool keep = k < ncand && cin[k];
+            int tot;
+            const int pos = base + block_excl_scan<NT>(keep ? 1 : 0, shi, &tot);
+            if (keep && pos < A.supp_cap) A.supp_tok[(size_t)row * A.supp_cap + pos] = cj[k];
+            base += tot;
+        }
+    }
     // eval list: support token positions and p_j in candidate order (exact delta / rho)
     if (FULL && A.tok_list) {
         int base = 0;

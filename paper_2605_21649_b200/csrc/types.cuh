@@ -39,6 +39,7 @@ struct TauArgs {
     int cap, pr;                                                          // tau kernel capacities
     int approx_h;                                                         // > 0: approximate tau, Halley steps
     int var;                                                              // list lengths vary (slices from n_sel)
+    int32_t *supp_tok; int supp_cap;                                      // support token list (decode stats)
 };
 
 constexpr int kTsNT = 256;

@@ -277,7 +277,7 @@ def test_decode_topk_end_to_end(case, alpha, k):
     qh = q_host(wl)
     sel = ekv.select_params("topk", k)
     ws = ekv.alloc_workspace(dc, Hq, sel, eval_exact=True)
-    st = ekv.DecodeStats(B, Hq, "cuda", delta_bar=True, eval_exact=True)
+    st = ekv.DecodeStats(B, Hq, "cuda", delta_bar=True, eval_exact=True, supp_cap=4096)
     out = ekv.decode(dc, wl.q.cuda(), sel, ekv.attn_params(alpha), ws, stats=st)
     torch.cuda.synchronize()
     out = out.cpu().numpy()
@@ -287,6 +287,8 @@ def test_decode_topk_end_to_end(case, alpha, k):
             np.testing.assert_allclose(out[b, h], ref["o"], atol=tol_for(dt), rtol=0)
             assert int(st.n_sel[b, h]) == len(ref["pages"])
             assert int(st.supp_count[b, h]) == ref["supp"]
+            # the support set itself, element by element (R9)
+            assert st.support(b, h).cpu().tolist() == np.nonzero(ref["p"])[0].tolist(), (b, h)
             assert abs(float(st.tau[b, h]) - ref["tau"]) <= 1e-6 * max(1, abs(ref["tau"]))
             m = ref["metrics"]
             assert int(st.full_supp[b, h]) == m["full_supp"]
@@ -310,16 +312,17 @@ def test_decode_large_budgets(k, alpha):
     qh = q_host(wl)
     sel = ekv.select_params("topk", k)
     ws = ekv.alloc_workspace(dc, Hq, sel)
-    st = ekv.DecodeStats(B, Hq, "cuda", delta_bar=True)
+    st = ekv.DecodeStats(B, Hq, "cuda", delta_bar=True, supp_cap=12000)
     out = ekv.decode(dc, wl.q.cuda(), sel, ekv.attn_params(alpha), ws, stats=st)
     torch.cuda.synchronize()
     out = out.cpu().numpy()
     for b in range(B):
         for h in range(Hq):
-            ref = oracle.decode_head(hc, qh[b, h], b, h // G, alpha, k_pages=k)
+            ref = oracle.decode_head(hc, qh[b, h], b, h // G, alpha, k_pages=k, eval_exact=True)
             np.testing.assert_allclose(out[b, h], ref["o"], atol=2e-3, rtol=0, err_msg=f"b={b} h={h}")
             assert int(st.n_sel[b, h]) == len(ref["pages"])
             assert int(st.supp_count[b, h]) == ref["supp"], (b, h)
+            assert st.support(b, h).cpu().tolist() == np.nonzero(ref["p"])[0].tolist(), (b, h)
             assert abs(float(st.tau[b, h]) - ref["tau"]) <= 1e-6 * max(1, abs(ref["tau"]))
 
 
@@ -380,7 +383,7 @@ def test_decode_gauss_end_to_end(sl, alpha, kind):
     qh = q_host(wl)
     sel = ekv.select_params("gauss", q_page=0.99, margin=0.1)
     ws = ekv.alloc_workspace(dc, Hq, sel)
-    st = ekv.DecodeStats(B, Hq, "cuda", delta_bar=False, gauss=True)
+    st = ekv.DecodeStats(B, Hq, "cuda", delta_bar=False, gauss=True, supp_cap=40000)
     out = ekv.decode(dc, wl.q.cuda(), sel, ekv.attn_params(alpha), ws, stats=st)
     torch.cuda.synchronize()
     out = out.cpu().numpy()
@@ -391,9 +394,11 @@ def test_decode_gauss_end_to_end(sl, alpha, kind):
             _, om, os2 = hc.score_pages(qh[b, h], b, h // G, modes=2)
             pages = oracle.gauss_select(om, os2, counts, alpha, float(st.tau_hat[b, h]), 0.1, zq)
             assert int(st.n_sel[b, h]) == len(pages)
-            ref = hc.attend(qh[b, h], b, h // G, pages, alpha)
+            ref = hc.attend(qh[b, h], b, h // G, pages, alpha, want_p=True)
             np.testing.assert_allclose(out[b, h], ref["o"], atol=2e-3, rtol=0)
             assert int(st.supp_count[b, h]) == ref["supp"]
+            if ref["supp"] <= st.supp_cap:
+                assert st.support(b, h).cpu().tolist() == np.nonzero(ref["p"])[0].tolist(), (b, h)
 
 
 def test_prop2_exactness_on_gpu():
