@@ -189,11 +189,13 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
     // (variable-length lists, e.g. the Gaussian selector: from the list length -- one round
     // trip more, but every rank gets work)
     const int S = (((A.var ? nlist : A.sel_stride) * 4 + CL - 1) / CL + 3) & ~3;
-    int pg[kTsU];
-#pragma unroll
-    for (int u = 0; u < kTsU; ++u) {
-        const int e = rk * S + threadIdx.x + NT * u;
-        pg[u] = (!FULL && e < (rk + 1) * S && (e >> 2) < A.sel_stride) ? __ldg(plist + (e >> 2)) : -1;
+    // thread t owns list page (item r0 / 4 + t) of each round: its kTsU = 4 items are that
+    // page's 4 quads, so the block scan compacts candidates in list order = token order
+    static_assert(kTsU == 4, "one page (4 quads of 4 scores) per thread and round");
+    int pg;
+    {
+        const int i = (rk * S >> 2) + threadIdx.x;
+        pg = (!FULL && 4 * i < (rk + 1) * S && i < A.sel_stride) ? __ldg(plist + i) : -1;
     }
     ph_stamp<6>(0);
     if (mk == 0u) {   // empty C_tok (uniform over the cluster)
@@ -221,51 +223,42 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
         const float thr_f = thr_c - 1e-6f * fmaxf(1.0f, fabsf(thr_c));   // conservative fp32 pre-test
         const int nitems = min(nlist * 4, hi);
         int n = 0;
-        for (int r0 = lo; r0 < nitems; r0 += kTsU * NT) {
-            if (r0 > lo || !have_pg) {
+        for (int r0 = lo; r0 < nitems; r0 += kTsU * NT) {       // lo, r0, nitems: multiples of 4
+            const int e0 = r0 + 4 * threadIdx.x;                     // this thread's page's first item
+            if (r0 > lo || !have_pg) pg = e0 < nitems ? page_of(e0 >> 2) : -1;
+            if (e0 >= nitems) pg = -1;
+            float4 v[kTsU];
+            int ph = 0;
+            if (pg >= 0) {
+#pragma unroll
+                for (int u = 0; u < kTsU; ++u) v[u] = *reinterpret_cast<const float4 *>(srow + (size_t)pg * kP + 4 * u);
+                ph = __ldg(ptab + pg);
+            }
+            uint32_t bits = 0u;
+            if (pg >= 0) {
+                const int j0 = pg * kP;
 #pragma unroll
                 for (int u = 0; u < kTsU; ++u) {
-                    const int e = r0 + threadIdx.x + NT * u;
-                    pg[u] = e < nitems ? page_of(e >> 2) : -1;
+                    const float sv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (j0 + 4 * u + q < L && sv[q] >= thr_f && a * (double)sv[q] > tlo) bits |= 1u << (4 * u + q);
                 }
-            }
-            float4 v[kTsU];
-            int ph[kTsU];
-#pragma unroll
-            for (int u = 0; u < kTsU; ++u) {
-                const int e = r0 + threadIdx.x + NT * u;
-                if (e >= nitems) pg[u] = -1;
-                if (pg[u] >= 0) {
-                    v[u] = *reinterpret_cast<const float4 *>(srow + (size_t)pg[u] * kP + 4 * (e & 3));
-                    ph[u] = __ldg(ptab + pg[u]);
-                }
-            }
-            uint64_t bits = 0ull;
-#pragma unroll
-            for (int u = 0; u < kTsU; ++u) {
-                if (pg[u] < 0) continue;
-                const int e = r0 + threadIdx.x + NT * u;
-                const int j0 = pg[u] * kP + 4 * (e & 3);
-                const float sv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (j0 + q < L && sv[q] >= thr_f && a * (double)sv[q] > tlo) bits |= 1ull << (4 * u + q);
             }
             int tot;
-            int pos = n + block_excl_scan<NT>(__popcll(bits), shi, &tot);
+            int pos = n + block_excl_scan<NT>(__popc(bits), shi, &tot);
             if (n + tot > cap) return -1;
             if (bits) {
 #pragma unroll
                 for (int u = 0; u < kTsU; ++u) {
-                    if (!((bits >> (4 * u)) & 15ull)) continue;
-                    const int e = r0 + threadIdx.x + NT * u;
+                    if (!((bits >> (4 * u)) & 15u)) continue;
                     const float sv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
-                        if ((bits >> (4 * u + q)) & 1ull) {
+                        if ((bits >> (4 * u + q)) & 1u) {
                             zs[pos] = sv[q];
-                            cj[pos] = pg[u] * kP + 4 * (e & 3) + q;
-                            cph[pos] = ph[u];
+                            cj[pos] = pg * kP + 4 * u + q;
+                            cph[pos] = ph;
                             ++pos;
                         }
                 }
