@@ -237,8 +237,7 @@ namespace {
 // zero(rowmax, ccount, umask) -> [mark] -> K scores -> candidates -> tau/PV
 ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t *pi, const int32_t *ns, int stride,
                        int full, const ekv_attn_params *attn, float *out, double *tau, int32_t *supp, void *ws,
-                       const Layout &L, cudaStream_t st, const TauArgs *extra, bool marked = false,
-                       bool scored = false) {
+                       const Layout &L, cudaStream_t st, const TauArgs *extra, bool marked = false) {
     const CacheView v = view(c);
     uint32_t *rowmax = at<uint32_t>(ws, L.rowmax);
     int *ccount = at<int>(ws, L.ccount);
@@ -246,7 +245,7 @@ ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t 
     float *scores = at<float>(ws, L.scores);
     if (!marked) EKV_TRY(launch_zero(at<uint4>(ws, L.zero), L.zero_bytes / 16, st));
     if (!full && !marked) EKV_TRY(launch_mark(c->batch, Hq, Hq / c->n_kv_heads, pi, ns, stride, um, L.W, st));
-    if (!scored) EKV_TRY(launch_scores(v, q, Hq, um, L.W, pi, ns, stride, scores, rowmax, full, st));
+    EKV_TRY(launch_scores(v, q, Hq, um, L.W, pi, ns, stride, scores, rowmax, full, st));
     const int rows = c->batch * Hq;
     const size_t ntok = (size_t)c->max_pages_per_seq * kP;
     float *cs = at<float>(ws, L.cand_s);
@@ -498,17 +497,9 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
     else EKV_TRY(launch_zero(zp, zn16, st));
     // a2 / a2'
     const int maxp = cache->max_pages_per_seq;
-    const bool fused = sel->policy == EKV_TOPK || sel->policy == EKV_ALL;
-    if (fused) {
-        // top-k with the K scores of the selected pages fused in (no separate K-score pass)
+    if (sel->policy == EKV_TOPK || sel->policy == EKV_ALL) {
         const int k = sel->policy == EKV_TOPK ? sel->k_pages : maxp;
-        TopkScoreArgs fz;
-        fz.c = v;
-        fz.q = q;
-        fz.scores = at<float>(workspace, L.scores);
-        fz.rowmax = at<uint32_t>(workspace, L.rowmax);
-        EKV_TRY(launch_topk(modes & EKV_SCORE_BOX ? box : nullptr, cache->batch, n_q_heads, maxp, cache->seq_lens, k, pi,
-                            ns, L.cap, Gq, uo, st, &fz));
+        EKV_TRY(launch_topk(box, cache->batch, n_q_heads, maxp, cache->seq_lens, k, pi, ns, L.cap, Gq, uo, st));
     } else {
         EKV_TRY(launch_gauss(cache, n_q_heads, mu, s2, attn->alpha, sel, pi, ns, L.cap, th, st));
         EKV_TRY(launch_mark(cache->batch, n_q_heads, Gq, pi, ns, L.cap, uo.umask, L.W, st));
@@ -522,16 +513,13 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
         xa.supp_tok = stats->supp_tok;
         xa.supp_cap = stats->supp_cap;
     }
-    if (want_db) {             // a4: the certified dropped-mass bound, folded into the tau kernel
-        xa.box = box;
-        xa.umask = uo.umask;
-        xa.W = L.W;
-        xa.db_out = stats->delta_bar;
-    }
     EKV_TRY(attend_impl(cache, q, n_q_heads, pi, ns, L.cap, 0, attn, out, tau_p,
-                        stats ? stats->supp_count : nullptr, workspace, L, st, &xa, /*marked=*/true,
-                        /*scored=*/fused));
+                        stats ? stats->supp_count : nullptr, workspace, L, st, &xa, /*marked=*/true));
     const int rows = cache->batch * n_q_heads;
+    // a4: certified dropped-mass bound
+    if (want_db)
+        EKV_TRY(launch_delta_bar(box, maxp, cache->seq_lens, rows, n_q_heads, Gq, uo.umask, L.W, tau_p, attn->alpha,
+                                 stats->delta_bar, st));
     if (stats) {
         if (stats->n_sel)
             EKV_TRY(check_err(cudaMemcpyAsync(stats->n_sel, ns, rows * sizeof(int32_t), cudaMemcpyDeviceToDevice, st),

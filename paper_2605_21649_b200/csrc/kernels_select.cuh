@@ -37,30 +37,18 @@ __device__ __forceinline__ uint32_t nibble_word(uint32_t nib, int lane) {
     return w;
 }
 
-// Fused K scores (the decode path, SCORE = true; R17 variant without the union dedup): after
-// the selection, each CTA streams the K tiles of ITS selected pages (about k / CL of them)
-// and scores them for its own query head -- no separate K-score launch, no page-list walk:
-// the pages are already in shared memory.  Each warp owns one ring slot (one 16-token page
-// tile, a 1-D bulk copy completing on the warp's own mbarrier) and loops over the CTA's
-// list: copy -> wait -> score -> next.  Lane = (token t, chunk half hh): it runs the 8
-// canonical fma chains of chunks hh*8 + (cc ^ (t & 7)) (the XOR relabel keeps the reads
-// conflict-free and maps R1's tree pairs onto themselves), the c + (c + 8) level is one
-// shuffle, the rest of R1's tree is local: bit-identical to dot16x8.  s = fl32(dot * c_d)
-// (R2), -inf past seq_len; the CTA's row maximum goes out in one atomicMax.
-
-template <int NT, typename T, bool SCORE>
+template <int NT>
 __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int Hq, int maxp,
                                                 const int32_t *__restrict__ seq_lens, int k,
                                                 int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
-                                                int sel_stride, int G, uint32_t *__restrict__ umask, int W,
-                                                TopkScoreArgs SA) {
+                                                int sel_stride, int G, uint32_t *__restrict__ umask, int W) {
     EKV_TRACE(2);
     pdl_wait();
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     const int CL = (int)cl.num_blocks(), r = (int)cl.block_rank();
     const int row = blockIdx.x / CL;
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int t = threadIdx.x, lane = t & 31;
     constexpr int NWp = NT / 32;
     __shared__ uint32_t whist[NWp][256];     // per-warp private histograms (no cross-warp contention)
     __shared__ uint32_t hist[2][256];        // the CTA's histogram of the current digit (published)
@@ -77,8 +65,7 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
 #pragma unroll
     for (int j = 0; j < kTkKPT / 4; ++j) {
         const int i4 = base + 4 * (t + NT * j);
-        if (!box) kv[j] = make_float4(1.f, 1.f, 1.f, 1.f);          // no scores: policy ALL
-        else if (vec && i4 + 3 < maxp) kv[j] = __ldg(reinterpret_cast<const float4 *>(x + i4));
+        if (vec && i4 + 3 < maxp) kv[j] = __ldg(reinterpret_cast<const float4 *>(x + i4));
         else {
             kv[j].x = (i4 < maxp) ? __ldg(x + i4) : 0.f;
             kv[j].y = (i4 + 1 < maxp) ? __ldg(x + i4 + 1) : 0.f;
@@ -93,6 +80,14 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
     uint32_t *um = umask ? umask + (size_t)unit * W : nullptr;
     stamp(1, 0);
     ph_stamp<2>(0);
+    if (keff >= M) {                         // every page (uniform over the cluster)
+        for (int p = base + t; p < min(M, base + (NT * kTkKPT)); p += NT) {
+            out[p] = p;
+            if (um) union_mark(um, p, gh);
+        }
+        if (r == 0 && t == 0) n_sel[row] = M;
+        return;
+    }
     uint32_t key[kTkKPT];
 #pragma unroll
     for (int j = 0; j < kTkKPT / 4; ++j) {
@@ -102,15 +97,14 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
         key[4 * j + 2] = (i4 + 2 < M) ? f2key(kv[j].z) : 0u;
         key[4 * j + 3] = (i4 + 3 < M) ? f2key(kv[j].w) : 0u;
     }
-    uint32_t prefix = 0u, pmask = 0u;
-    int kk = keff;                           // keys still to take among those matching prefix
-    bool whole = keff >= M;                  // every page (uniform over the cluster): no search
-    if (!whole) {
     for (int i = t; i < NWp * 256; i += NT) (&whist[0][0])[i] = 0u;
     __syncthreads();
     stamp(1, 1);
     ph_stamp<2>(1);
     // 1. radix select over the cluster
+    uint32_t prefix = 0u, pmask = 0u;
+    int kk = keff;                           // keys still to take among those matching prefix
+    bool whole = false;                      // the last digit's bin is taken entirely
 #pragma unroll 1
     for (int pass = 0; pass < 4; ++pass) {
         const int shift = 24 - 8 * pass;
@@ -181,11 +175,11 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
         const int cnt = sh[2];
         if (kk == cnt) { whole = true; break; }
     }
-    }
     stamp(1, 2);
     ph_stamp<2>(6);
-    // selected: key != 0 and ((key & pmask) > prefix, or (key & pmask) == prefix and (whole, or
-    // one of the first kk equal keys in page order))
+    // selected: (key & pmask) > prefix, or (key & pmask) == prefix and (whole, or one of the
+    // first kk equal keys in page order)
+    int take = 0;
     if (!whole) {
         int ceq = 0;
 #pragma unroll
@@ -195,7 +189,7 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
         cl.sync();
         int before = 0;
         for (int q = 0; q < r; ++q) before += *cl.map_shared_rank(&xch[0], q);
-        const int take = min(max(kk - before, 0), ceq);
+        take = min(max(kk - before, 0), ceq);
         // equal keys of this CTA in page order: bitmap, word w = pages 32 w .. 32 w + 31
 #pragma unroll
         for (int j = 0; j < kTkKPT / 4; ++j) {
@@ -227,7 +221,7 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const uint32_t v = key[4 * j + e] & pmask;
-            const bool s = key[4 * j + e] != 0u && (v > prefix || (whole && v == prefix));
+            const bool s = v > prefix || (whole && v == prefix);
             nib |= (s ? 1u : 0u) << e;
         }
         const uint32_t w = nibble_word(nib, lane);
@@ -244,118 +238,17 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
     cl.sync();
     int o = pos;
     for (int q = 0; q < r; ++q) o += *cl.map_shared_rank(&xch[1], q);
-    {
-        uint32_t v = w;
-        while (v) {
-            const int p = base + 32 * t + __ffs(v) - 1;
-            v &= v - 1;
-            out[o++] = p;
-            if (um) union_mark(um, p, gh);
-        }
+    uint32_t v = w;
+    while (v) {
+        const int p = base + 32 * t + __ffs(v) - 1;
+        v &= v - 1;
+        out[o++] = p;
+        if (um) union_mark(um, p, gh);
     }
     if (r == 0 && t == 0) n_sel[row] = keff;
     stamp(1, 6);
     ph_stamp<2>(7);
     cl.sync();                               // keep shared memory alive for remote readers
-    if constexpr (SCORE) {
-        // ---- K scores of this CTA's selected pages (its own query head)
-        extern __shared__ __align__(128) unsigned char tsm[];
-        constexpr int TILE = kP * kD * (int)sizeof(T);
-        unsigned char *ring = tsm;                                           // [NWp][TILE]
-        int *lpage = reinterpret_cast<int *>(tsm + NWp * TILE);              // [kTkListCap]
-        int *lphys = lpage + kTkListCap;                                     // [kTkListCap]
-        __shared__ __align__(16) T qs[kD];
-        __shared__ uint64_t wbar[NWp];
-        __shared__ float wmax[NWp];
-        const CacheView &c = SA.c;
-        const int h = row % Hq, kvh = h / G;
-        if (t < kD) qs[t] = reinterpret_cast<const T *>(SA.q)[(size_t)row * kD + t];
-        if (lane == 0) mbar_init(&wbar[warp], 1);
-        fence_mbar_init();
-        const size_t ntok = (size_t)maxp * kP;
-        float *srow = SA.scores + (size_t)row * ntok;
-        const int32_t *ptab = c.page_table + (size_t)b * c.maxp;
-        const unsigned char *Kb = reinterpret_cast<const unsigned char *>(c.K);
-        const int tt = lane & 15, hh = lane >> 4, sw = tt & 7;
-        float mx = -INFINITY;
-        uint32_t ph = 0u;                                                    // this warp's barrier phase
-        for (int r0 = 0; r0 < tot; r0 += kTkListCap) {
-            // the list window [r0, r0 + cap): page ids in order, physical pages looked up in parallel
-            __syncthreads();
-            {
-                uint32_t v = w;
-                int i = pos;
-                while (v) {
-                    const int p = base + 32 * t + __ffs(v) - 1;
-                    v &= v - 1;
-                    if (i >= r0 && i < r0 + kTkListCap) { lpage[i - r0] = p; lphys[i - r0] = __ldg(ptab + p); }
-                    ++i;
-                }
-            }
-            __syncthreads();
-            const int nl = min(tot - r0, kTkListCap);
-            unsigned char *slot = ring + (size_t)warp * TILE;
-            for (int i = warp; i < nl; i += NWp) {                          // warp-uniform
-                if (lane == 0) {
-                    mbar_expect_tx(&wbar[warp], (uint32_t)TILE);
-                    bulk_g2s(slot, Kb + ((size_t)lphys[i] * c.Hkv + kvh) * TILE, (uint32_t)TILE, &wbar[warp]);
-                }
-                mbar_wait(&wbar[warp], ph);
-                ph ^= 1u;
-                float acc[8];
-                if constexpr (sizeof(T) == 2) {
-                    const uint4 *krow = reinterpret_cast<const uint4 *>(slot) + tt * (kD / 8);
-                    const uint4 *qrow = reinterpret_cast<const uint4 *>(qs);
-#pragma unroll
-                    for (int cc = 0; cc < 8; ++cc) {
-                        const int ch = 8 * hh + (cc ^ sw);
-                        const uint4 kw = krow[ch], qw = qrow[ch];
-                        float a = 0.0f;
-                        a = fma_bf16lo(qw.x, kw.x, a); a = fma_bf16hi(qw.x, kw.x, a);
-                        a = fma_bf16lo(qw.y, kw.y, a); a = fma_bf16hi(qw.y, kw.y, a);
-                        a = fma_bf16lo(qw.z, kw.z, a); a = fma_bf16hi(qw.z, kw.z, a);
-                        a = fma_bf16lo(qw.w, kw.w, a); a = fma_bf16hi(qw.w, kw.w, a);
-                        acc[cc] = a;
-                    }
-                } else {
-                    const float4 *krow = reinterpret_cast<const float4 *>(slot) + tt * (kD / 4);
-                    const float4 *qrow = reinterpret_cast<const float4 *>(qs);
-#pragma unroll
-                    for (int cc = 0; cc < 8; ++cc) {
-                        const int ch = 8 * hh + (cc ^ sw);
-                        const float4 k0 = krow[2 * ch], k1 = krow[2 * ch + 1], q0 = qrow[2 * ch], q1 = qrow[2 * ch + 1];
-                        float a = 0.0f;
-                        a = fmaf(q0.x, k0.x, a); a = fmaf(q0.y, k0.y, a); a = fmaf(q0.z, k0.z, a); a = fmaf(q0.w, k0.w, a);
-                        a = fmaf(q1.x, k1.x, a); a = fmaf(q1.y, k1.y, a); a = fmaf(q1.z, k1.z, a); a = fmaf(q1.w, k1.w, a);
-                        acc[cc] = a;
-                    }
-                }
-                __syncwarp();                                               // slot reads done before reuse
-                // R1 tree: chunk c (lane half 0) + chunk c + 8 (lane half 1), then local levels
-#pragma unroll
-                for (int cc = 0; cc < 8; ++cc) acc[cc] = __fadd_rn(acc[cc], __shfl_xor_sync(0xffffffffu, acc[cc], 16));
-#pragma unroll
-                for (int cc = 0; cc < 4; ++cc) acc[cc] = __fadd_rn(acc[cc], acc[cc + 4]);
-                acc[0] = __fadd_rn(acc[0], acc[2]);
-                acc[1] = __fadd_rn(acc[1], acc[3]);
-                const float sv = __fmul_rn(__fadd_rn(acc[0], acc[1]), kCd);
-                const int tok = lpage[i] * kP + tt;
-                const float v = tok < Lb ? sv : -INFINITY;
-                if (hh == 0) srow[tok] = v;
-                mx = fmaxf(mx, v);
-            }
-        }
-        // the CTA's row maximum (ordered key, 0 = nothing scored)
-#pragma unroll
-        for (int o2 = 16; o2 >= 1; o2 >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o2));
-        if (lane == 0) wmax[warp] = mx;
-        __syncthreads();
-        if (t == 0) {
-            float m = -INFINITY;
-            for (int q = 0; q < NWp; ++q) m = fmaxf(m, wmax[q]);
-            if (m > -INFINITY) atomicMax(SA.rowmax + row, f2key(m));
-        }
-    }
 }
 
 // ============================================================================ union per KV group

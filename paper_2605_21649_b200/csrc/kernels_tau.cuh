@@ -144,41 +144,6 @@ __device__ __noinline__ double streamed_newton(const float *srow, const int32_t 
     return t;
 }
 
-// a4 folded into the tau kernel (R16, App. B.4): the certified dropped-mass bound
-//   delta_bar = sum_{p not in C_page(h)} c_p [(alpha-1) box_p - tau~]_+^beta
-// over this rank's share [p0, p1) of the row's pages (p0 a multiple of 4), fp64 terms in page
-// order per thread, a fixed-order block sum (all threads get it).  Selected pages: bit g of
-// the union-mask byte of the page (head g of the KV group).  Out of line: the decode's hot
-// code stays contiguous.
-template <int NT, int IB>
-__device__ __noinline__ double db_partial(const float *__restrict__ bx, const uint32_t *__restrict__ um, int g, int M,
-                                          int L, int p0, int p1, bool vec, double a, double beta, double t,
-                                          BlockRed2<NT> &Rd) {
-    double db = 0.0, dz = 0.0;
-    const float tf = (float)(t / a);
-    const float thr = tf - 1e-3f * fmaxf(1.0f, fabsf(tf));    // fp32 pre-test, rounded well below t / a
-    for (int p4 = p0 + 4 * threadIdx.x; p4 < p1; p4 += 4 * NT) {
-        float bv[4];
-        if (vec && p4 + 3 < p1) {
-            const float4 v = __ldg(reinterpret_cast<const float4 *>(bx + p4));
-            bv[0] = v.x; bv[1] = v.y; bv[2] = v.z; bv[3] = v.w;
-        } else {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) bv[e] = (p4 + e < p1) ? __ldg(bx + p4 + e) : -INFINITY;
-        }
-        const uint32_t mw = __ldg(um + (p4 >> 2));
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int p = p4 + e;
-            if (p >= p1 || ((mw >> (8 * e + g)) & 1u) || !(bv[e] > thr)) continue;
-            const double d = a * (double)bv[e] - t;
-            if (d > 0.0) db += (p == M - 1 ? (double)(L - p * kP) : (double)kP) * powB<IB>(d, beta);
-        }
-    }
-    Rd.sum(db, dz);
-    return db;
-}
-
 template <typename T, int IB, bool FULL>
 __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A) {
     EKV_TRACE(6);
@@ -238,7 +203,6 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
         if (rk == 0 && threadIdx.x == 0) {
             if (A.tau_out) A.tau_out[row] = NAN;
             if (A.supp_out) A.supp_out[row] = 0;
-            if (!FULL && A.db_out) A.db_out[row] = NAN;
         }
         return;
     }
@@ -251,35 +215,6 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
     const float af = (float)a, betaf = (float)beta;
     const double zmax = a * (double)smax;
     double tau_lo = zmax - 1.0 - 1e-12 * fmax(1.0, fabs(zmax));
-
-    // ---- a4: delta_bar over the row's pages, split over the cluster's ranks (every rank calls
-    // this exactly once, after the candidate merge; rank 0 with the row's tau)
-    __shared__ double s_dbt, s_dbp;
-    auto finish_db = [&](double t_row) {
-        if constexpr (!FULL) {
-            if (!A.db_out) return;
-            if (rk == 0 && threadIdx.x == 0) s_dbt = t_row;
-            cl.sync();
-            const double t = *cl.map_shared_rank(&s_dbt, 0);
-            const int Mr = n_pages_of(L);
-            const int chunk = ((Mr + CL - 1) / CL + 3) & ~3;
-            const int p0 = min(Mr, rk * chunk), p1 = min(Mr, p0 + chunk);
-            double part = 0.0;
-            if (t == t) {
-                const int G = A.G, unit = b * (A.Hq / G) + h / G;
-                part = db_partial<NT, IB>(A.box + (size_t)row * c.maxp, A.umask + (size_t)unit * A.W, h % G, Mr, L,
-                                          p0, p1, (c.maxp & 3) == 0, a, beta, t, Rd);
-            }
-            if (threadIdx.x == 0) s_dbp = part;
-            cl.sync();
-            if (rk == 0 && threadIdx.x == 0) {
-                double sum = 0.0;
-                for (int q = 0; q < CL; ++q) sum += *cl.map_shared_rank(&s_dbp, q);
-                A.db_out[row] = (t == t) ? sum : NAN;
-            }
-            cl.sync();                       // rank 0's shared memory stays alive for the reads
-        }
-    };
 
     // ---- 1. candidates {z > tau_lo} (returns -1 on overflow; uniform)
     // items [lo, min(hi, 4 nlist)) in rounds of U * NT; candidates compacted in item order
@@ -438,7 +373,7 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
                 }
             }
             cl.sync();
-            if (rk > 0) { finish_db(0.0); return; }
+            if (rk > 0) return;
             if (!ovf) { ncand = tot; break; }
             ncand = -1;
         }
@@ -451,7 +386,6 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
                 if (A.tau_out) A.tau_out[row] = NAN;
                 if (A.supp_out) A.supp_out[row] = -1;
             }
-            finish_db(NAN);
             return;
         }
             // overflow: fp64 Newton streamed over the whole row moves tau_lo just below tau
@@ -935,7 +869,6 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
         }
         if (threadIdx.x == 0) A.n_list[row] = base;
     }
-    finish_db(tau);
     ph_stamp<6>(5);
 }
 

@@ -5,44 +5,20 @@
 
 namespace ekvh {
 
-// top-k: one cluster of CL CTAs per row, CL = pages / 8192 rounded up to a power of two;
-// fz != NULL: the decode path, K scores of the selected pages fused in (kernels_select.cuh)
-namespace {
-template <int NT, typename T, bool SCORE>
-cudaError_t topk_go(int CL, const float *box, int B, int Hq, int maxp, const int32_t *sl, int k, int32_t *pi,
-                    int32_t *ns, int stride, int G, const UnionOut &u, cudaStream_t st, const TopkScoreArgs &sa) {
-    int smem = 0;
-    if (SCORE) {
-        smem = topk_score_smem<T>(NT);
-        set_smem(k_topk<NT, T, SCORE>, smem);
-    }
-    return launch_ex(k_topk<NT, T, SCORE>, dim3((unsigned)(B * Hq * CL)), dim3(NT), (size_t)smem, st, (unsigned)CL, box,
-                     Hq, maxp, sl, k, pi, ns, stride, G, u.umask, u.W, sa);
-}
-}  // namespace
-
+// top-k: one cluster of CL CTAs per row, CL = pages / 8192 rounded up to a power of two
 ekv_status launch_topk(const float *box, int B, int Hq, int maxp, const int32_t *sl, int k, int32_t *pi, int32_t *ns,
-                       int stride, int G, const UnionOut &u, cudaStream_t st, const TopkScoreArgs *fz) {
+                       int stride, int G, const UnionOut &u, cudaStream_t st) {
     // short rows: 256-thread CTAs (more CTAs per SM when there are many rows)
     const int NT = maxp <= 4096 ? 256 : 512;
     const int per = NT * kTkKPT;
     int CL = 1;
     while (CL * per < maxp) CL *= 2;
     if (CL > 8) return fail(EKV_ERR_UNSUPPORTED, "top-k supports at most %d pages", 8 * per);
-    TopkScoreArgs sa;
-    memset(&sa, 0, sizeof(sa));
-    if (fz) sa = *fz;
-    cudaError_t e;
-    const bool bf = fz && fz->c.dtype == EKV_BF16;
-    if (NT == 256) {
-        e = !fz ? topk_go<256, __nv_bfloat16, false>(CL, box, B, Hq, maxp, sl, k, pi, ns, stride, G, u, st, sa)
-            : bf ? topk_go<256, __nv_bfloat16, true>(CL, box, B, Hq, maxp, sl, k, pi, ns, stride, G, u, st, sa)
-                 : topk_go<256, float, true>(CL, box, B, Hq, maxp, sl, k, pi, ns, stride, G, u, st, sa);
-    } else {
-        e = !fz ? topk_go<512, __nv_bfloat16, false>(CL, box, B, Hq, maxp, sl, k, pi, ns, stride, G, u, st, sa)
-            : bf ? topk_go<512, __nv_bfloat16, true>(CL, box, B, Hq, maxp, sl, k, pi, ns, stride, G, u, st, sa)
-                 : topk_go<512, float, true>(CL, box, B, Hq, maxp, sl, k, pi, ns, stride, G, u, st, sa);
-    }
+    cudaError_t e = NT == 256
+        ? launch_ex(k_topk<256>, dim3((unsigned)(B * Hq * CL)), dim3(256), 0, st, (unsigned)CL, box, Hq, maxp, sl, k,
+                    pi, ns, stride, G, u.umask, u.W)
+        : launch_ex(k_topk<512>, dim3((unsigned)(B * Hq * CL)), dim3(512), 0, st, (unsigned)CL, box, Hq, maxp, sl, k,
+                    pi, ns, stride, G, u.umask, u.W);
     if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "k_topk: %s", cudaGetErrorString(e));
     return check_launch("k_topk");
 }

@@ -29,9 +29,7 @@ ekv_status tau_ibf(const CacheView &v, const TauArgs &A0, int rows, cudaStream_t
     set_smem(k_tau_sparse<T, IB, FULL>, ts_smem<T>(), /*nonportable_cluster=*/true);
     // a cluster of up to 4 CTAs per row splits the candidate extraction (page-list reads are
     // latency bound per SM); rank 0 then finishes the row
-    int CL = A.full ? 1 : A.sel_stride > 384 ? 4 : A.sel_stride > 128 ? 2 : 1;
-    // the folded delta_bar scans every page of the row: long rows take more ranks
-    if (!A.full && A.db_out) CL = std::max(CL, v.maxp > 16384 ? 4 : v.maxp > 4096 ? 2 : 1);
+    const int CL = A.full ? 1 : A.sel_stride > 384 ? 4 : A.sel_stride > 128 ? 2 : 1;
     cudaError_t e = launch_ex(k_tau_sparse<T, IB, FULL>, dim3((unsigned)(rows * CL)), dim3(kTsNT), smem, st, (unsigned)CL, v, A);
     if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "k_tau_sparse: %s", cudaGetErrorString(e));
     return check_launch("k_tau_sparse");

@@ -23,18 +23,6 @@ struct CacheView {
 // ---------------------------------------------------------------- a2 top-k
 constexpr int kTkKPT = 16;          // keys per thread; NT = 512 (8192 pages per CTA, <= 8 CTAs)
 
-// top-k fused with the K scores of the selected pages (decode path)
-struct TopkScoreArgs {
-    CacheView c;
-    const void *q;          // [B][Hq][d] (KV dtype)
-    float *scores;          // [B][Hq][maxp * P]
-    uint32_t *rowmax;       // [B][Hq] ordered keys (zeroed before the step)
-};
-constexpr int kTkListCap = 2048;    // selected pages per K-score round (shared list)
-template <typename T> constexpr int topk_score_smem(int NT) {
-    return (NT / 32) * kP * kD * (int)sizeof(T) + kTkListCap * 8;
-}
-
 // ---------------------------------------------------------------- a3 / a5 candidates and tau
 constexpr int kCpc = 1024;          // candidates per chunk region (k_candidates)
 constexpr int kCap = 12288;         // eval-list capacity per row
@@ -52,7 +40,6 @@ struct TauArgs {
     int approx_h;                                                         // > 0: approximate tau, Halley steps
     int var;                                                              // list lengths vary (slices from n_sel)
     int32_t *supp_tok; int supp_cap;                                      // support token list (decode stats)
-    const float *box; const uint32_t *umask; int W; double *db_out;       // folded delta_bar (a4)
 };
 
 constexpr int kTsNT = 256;
