@@ -377,7 +377,10 @@ def main():
     attn = ekv.attn_params(args.alpha)
     ws = ekv.alloc_workspace(cache, HQ, sel)
     stats = ekv.DecodeStats(1, HQ, dev, delta_bar=True, gauss=args.policy == "gauss")
-    q, kn, vn = new_tokens(1, HQ, HKV, seed=7 + rank, device=dev)
+    # the query the heavy hitters were planted for (planted workload; randn: q ~ N(0, I) either
+    # way); the appended token's k/v are fresh draws
+    _, kn, vn = new_tokens(1, HQ, HKV, seed=7 + rank, device=dev)
+    q = wl.q.contiguous()
     out = torch.empty(1, HQ, D, dtype=torch.float32, device=dev)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.synchronize()
