@@ -53,7 +53,10 @@ def parse():
     ap.add_argument("--budget", type=float, default=0.01)
     ap.add_argument("--alpha", type=float, default=1.5)
     ap.add_argument("--policy", default="topk", choices=["topk", "gauss"])
-    ap.add_argument("--workload", default="planted", choices=["planted", "randn"])
+    ap.add_argument("--workload", default="llama", choices=["llama", "planted", "randn"])
+    ap.add_argument("--bounds", default="kv", choices=["kv", "e4m3"],
+                    help="stored page bounds: KV dtype (exact) or outward-rounded fp8 e4m3 (N3, R24)")
+    ap.add_argument("--stats", default="f32", choices=["f32", "bf16"], help="stored kavg/kvar dtype")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="headline + roofline only (profiling runs)")
@@ -158,7 +161,7 @@ def k_pages_for(args):
 
 
 # ----------------------------------------------------------------------------- CPU oracle
-def host_group_caches(K, V, page_table, seq_len):
+def host_group_caches(K, V, page_table, seq_len, bound="kv", stat="f32"):
     """One oracle cache per KV group of sequence 0 (pages gathered in logical order; the oracle
     computes its own metadata).  Cache state, not per-step work."""
     import numpy as np
@@ -172,7 +175,7 @@ def host_group_caches(K, V, page_table, seq_len):
         Kh = K[phys, kv].float().cpu().numpy()[:, None]
         Vh = V[phys, kv].float().cpu().numpy()[:, None]
         hc = oracle.HostCache(Kh, Vh, np.arange(M, dtype=np.int32)[None], np.array([seq_len], np.int32))
-        hc.build_stats()
+        hc.build_stats(bound=bound, stat=stat)
         caches.append(hc)
         del Kh, Vh
         torch.cuda.empty_cache() if torch.cuda.is_available() else None
@@ -214,7 +217,7 @@ def run_reference(args, rank, world):
     dev = torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu")
     k_pages = k_pages_for(args)
     wl = workload_for(args, 0, dev)
-    caches = host_group_caches(wl.K, wl.V, wl.page_table, int(wl.seq_lens[0]))
+    caches = host_group_caches(wl.K, wl.V, wl.page_table, int(wl.seq_lens[0]), args.bounds, args.stats)
     qh = wl.q.float().cpu().numpy()
     del wl
     cores = os.cpu_count() or 1
@@ -231,7 +234,8 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"C4: 1 seq x {args.n} ctx, 32q/8kv, d=128, P=16, alpha={args.alpha}, top-k "
-                                   f"{args.budget:.0%} (k={k_pages}), {args.workload}"},
+                                   f"{args.budget:.0%} (k={k_pages}), {args.workload}, page bounds {args.bounds}, "
+                                   f"stats {args.stats}"},
             "cpu_baseline": {"value": us, "unit": "us", "cores": threads, "kind": "oracle",
                              "sample": f"the whole step (32 query heads: score all {len(caches[0].page_table[0])} pages, "
                                        f"top-k, exact sparse entmax), one head per thread on {threads} of {cores} "
@@ -371,7 +375,7 @@ def main():
     spare = args.steps + args.warmup + 64 + max(5, args.steps // 2) + 16
     n0 = n - spare if (n + spare + P - 1) // P > 65536 else n
     wl = workload_for(args, rank, dev, n_tokens=n0, spare=n - n0 if n0 < n else spare)
-    cache = ekv.PagedCache.allocate_meta(wl.K, wl.V, wl.page_table, wl.seq_lens)
+    cache = ekv.PagedCache.allocate_meta(wl.K, wl.V, wl.page_table, wl.seq_lens, bound=args.bounds, stat=args.stats)
     ekv.rebuild_page_stats(cache)
     sel = ekv.select_params(args.policy, k_pages, 0.99, 0.0)
     attn = ekv.attn_params(args.alpha)
@@ -440,7 +444,7 @@ def main():
             lambda: ekv.sparse_attend(cache, q, pi, ns, attn, workspace=ws, stream=stream), reps)
     torch.cuda.synchronize()
     n_tok = int(cache.seq_lens[0].item())
-    meta_bytes = M * HKV * 2 * D * 2                      # kmin + kmax, bf16, every page
+    meta_bytes = M * HKV * 2 * D * (1 if args.bounds == "e4m3" else 2)   # kmin + kmax of every page
     score_gbs = meta_bytes / (phases["score_pages"] * 1e-6) / 1e9
     peak, peak_kind = peaks()
 
@@ -583,7 +587,7 @@ def main():
                                            box=ekv.score_pages(cache, q, modes=1, stream=stream)[0], stream=stream)
             torch.cuda.synchronize()
             seq_len = int(cache.seq_lens[0].item())
-            caches = host_group_caches(cache.K, cache.V, cache.page_table, seq_len)
+            caches = host_group_caches(cache.K, cache.V, cache.page_table, seq_len, args.bounds, args.stats)
             qh = q.float().cpu().numpy()
             cores = os.cpu_count() or 1
             threads = min(cores, HQ)
@@ -626,7 +630,7 @@ def main():
             "vs_baseline": None, "dtype": "bf16", "data": f"synthetic ({args.workload})",
             "config": {"workload": f"C4: 1 seq x {args.n} ctx per GPU, 32q/8kv heads, d=128, P=16, bf16, "
                                    f"alpha={args.alpha}, {args.policy} {args.budget:.0%} (k={k_pages} pages), "
-                                   f"{args.workload}; step = append + score + select + sparse entmax + delta_bar; "
+                                   f"{args.workload}, page bounds {args.bounds}, stats {args.stats}; step = append + score + select + sparse entmax + delta_bar; "
                                    f"CUDA-graph replay",
                        "l2": "inputs larger than L2 (K/V 4 GiB, metadata 1.5 GiB per GPU): no flush",
                        "parallelism": f"batch-sharded x{world} (one sequence per GPU, no collective)"},

@@ -51,12 +51,25 @@ enum { EKV_SCORE_BOX = 1, EKV_SCORE_GAUSS = 2 };
  * Paged KV cache (PagedAttention layout).  Caller-owned device buffers.
  *   k_pages  [n_phys_pages][n_kv_heads][page_size][head_dim]   dtype
  *   v_pages  [n_phys_pages][n_kv_heads][page_size][value_dim]  dtype
- *   kmin,kmax[n_phys_pages][n_kv_heads][head_dim]              dtype (exact copies)
- *   ksum, ksumsq, kavg, kvar [n_phys_pages][n_kv_heads][head_dim]  fp32 (R5)
+ *   kmin,kmax[n_phys_pages][n_kv_heads][head_dim]   bound_dtype:
+ *       EKV_BOUND_KV   -- the KV dtype, exact copies of the coordinate-wise min / max;
+ *       EKV_BOUND_E4M3 -- one byte each, fp8 e4m3 (OCP FN: bias 7, no infinities, max 448),
+ *                         kmin rounded DOWN and kmax rounded UP to the e4m3 grid (outward
+ *                         rounding: kmin8 <= kmin, kmax8 >= kmax, so the box bound of
+ *                         Prop. B.1 stays an upper bound of every token score;
+ *                         DESIGN R24).  Precondition: |k| <= 448 (beyond it the bound
+ *                         saturates to +-448 and is no longer certified).
+ *   ksum, ksumsq [n_phys_pages][n_kv_heads][head_dim]  fp32 append accumulators (R5)
+ *   kavg, kvar   [n_phys_pages][n_kv_heads][head_dim]  stat_dtype:
+ *       EKV_STAT_F32 -- fp32 (R5);  EKV_STAT_BF16 -- the fp32 values rounded to nearest-even
+ *       bf16 (half the bytes the Gaussian scorer reads; R24).
  *   page_table [batch][max_pages_per_seq] int32: logical page -> physical page
  *   seq_lens   [batch] int32 (device; append_kv increments it)
  * Token j of sequence b lives in physical page page_table[b][j / P], slot j % P.
+ * A zero-initialised bound_dtype / stat_dtype is the exact layout (KV dtype bounds, fp32 stats).
  */
+enum { EKV_BOUND_KV = 0, EKV_BOUND_E4M3 = 1 };
+enum { EKV_STAT_F32 = 0, EKV_STAT_BF16 = 1 };
 typedef struct {
     int32_t dtype;             /* ekv_dtype of K, V, kmin, kmax */
     int32_t batch;
@@ -67,10 +80,13 @@ typedef struct {
     int32_t max_pages_per_seq;
     int32_t n_phys_pages;
     void *k_pages, *v_pages;
-    void *kmin, *kmax;
-    float *ksum, *ksumsq, *kavg, *kvar;
+    void *kmin, *kmax;         /* bound_dtype */
+    float *ksum, *ksumsq;
+    void *kavg, *kvar;         /* stat_dtype */
     const int32_t *page_table;
     int32_t *seq_lens;
+    int32_t bound_dtype;       /* EKV_BOUND_KV | EKV_BOUND_E4M3 */
+    int32_t stat_dtype;        /* EKV_STAT_F32 | EKV_STAT_BF16 */
 } ekv_cache;
 
 /* alpha > 1; transform = ekv_transform (softmax ignores alpha).

@@ -81,6 +81,13 @@ def lib():
         L.orc_gauss_select.restype = c_int
         L.orc_delta_bar.argtypes = [f32p, i32p, u8p, c_int, c_double, c_double]
         L.orc_delta_bar.restype = c_double
+        L.orc_e4m3_round_down.argtypes = [ctypes.c_float]
+        L.orc_e4m3_round_down.restype = ctypes.c_float
+        L.orc_e4m3_round_up.argtypes = [ctypes.c_float]
+        L.orc_e4m3_round_up.restype = ctypes.c_float
+        L.orc_bf16_round.argtypes = [ctypes.c_float]
+        L.orc_bf16_round.restype = ctypes.c_float
+        L.orc_store_meta.argtypes = [f32p, f32p, f32p, f32p, ctypes.c_size_t, c_int, c_int]
         _lib = L
     return _lib
 
@@ -211,6 +218,18 @@ def gauss_select(mu, sigma2, counts, alpha, tau_hat, margin, zq):
     return out[:n].copy()
 
 
+def e4m3_round_down(x) -> np.float32:
+    return np.float32(lib().orc_e4m3_round_down(float(x)))
+
+
+def e4m3_round_up(x) -> np.float32:
+    return np.float32(lib().orc_e4m3_round_up(float(x)))
+
+
+def bf16_round(x) -> np.float32:
+    return np.float32(lib().orc_bf16_round(float(x)))
+
+
 def delta_bar(box, counts, selected_pages, alpha, tau_sparse):
     box, counts = _f32(box), _i32(counts)
     sel = np.zeros(box.shape[0], np.uint8)
@@ -249,8 +268,10 @@ class HostCache:
             c[-1] = n - (M - 1) * self.P
         return c
 
-    def build_stats(self):
-        """Recompute every page's metadata from its tokens (orc_page_stats)."""
+    def build_stats(self, bound="kv", stat="f32"):
+        """Recompute every page's metadata from its tokens (orc_page_stats), then round it to the
+        stored form (orc_store_meta): bound "e4m3" = outward-rounded fp8 kmin/kmax, stat "bf16" =
+        nearest-even bf16 kavg/kvar (DESIGN R24)."""
         shp = (self.n_phys, self.Hkv, self.d)
         self.kmin, self.kmax = np.zeros(shp, np.float32), np.zeros(shp, np.float32)
         self.ksum, self.ksumsq = np.zeros(shp, np.float32), np.zeros(shp, np.float32)
@@ -259,6 +280,10 @@ class HostCache:
                               _p(self.seq_lens, ctypes.c_int32), self.page_table.shape[0], self.page_table.shape[1],
                               *[_p(getattr(self, n), ctypes.c_float)
                                 for n in ("kmin", "kmax", "ksum", "ksumsq", "kavg", "kvar")])
+        if bound != "kv" or stat != "f32":
+            lib().orc_store_meta(_p(self.kmin, ctypes.c_float), _p(self.kmax, ctypes.c_float),
+                                 _p(self.kavg, ctypes.c_float), _p(self.kvar, ctypes.c_float), self.kmin.size,
+                                 1 if bound == "e4m3" else 0, 1 if stat == "bf16" else 0)
 
     def score_pages(self, q, b, kvh, modes=1):
         q = _f32(q)

@@ -112,6 +112,92 @@ void orc_build_stats(const float *K, int Hkv, int P, int d, const int32_t *page_
 }
 
 /* ------------------------------------------------------------------------- */
+/* Compressed stored metadata (DESIGN R24).                   */
+/* The box bound of Prop. B.1 needs only kmin_i <= k_{t,i} <=      */
+/* kmax_i; any stored lower bound of kmin and upper bound of kmax keeps it an  */
+/* upper bound of every token score.  Stored forms:                           */
+/*   e4m3 (OCP fp8 "FN": 1 sign, 4 exponent bits with bias 7, 3 mantissa bits,*/
+/*   no infinities, largest finite 448):                                       */
+/*     kmin8 = largest e4m3 value <= kmin, kmax8 = smallest e4m3 value >= kmax */
+/*   bf16 (kavg, kvar): the fp32 value rounded to nearest, ties to even.       */
+/* The e4m3 set is written out from its definition (no bit tricks); rounding  */
+/* is a plain search over it.                                                  */
+/* ------------------------------------------------------------------------- */
+static double e4m3_vals[256];
+static int e4m3_n = 0;
+
+static void e4m3_init(void)
+{
+    if (e4m3_n) return;
+    double pos[127];
+    int np = 0;
+    for (int m = 0; m < 8; ++m) pos[np++] = ldexp((double)m / 8.0, -6);          /* e = 0: subnormals (and 0) */
+    for (int e = 1; e <= 15; ++e)
+        for (int m = 0; m < 8; ++m) {
+            if (e == 15 && m == 7) continue;                                      /* NaN encoding */
+            pos[np++] = ldexp(1.0 + (double)m / 8.0, e - 7);
+        }
+    /* ascending: the negatives (largest magnitude first), then 0, then the positives */
+    int n = 0;
+    for (int i = np - 1; i >= 1; --i) e4m3_vals[n++] = -pos[i];
+    for (int i = 0; i < np; ++i) e4m3_vals[n++] = pos[i];
+    e4m3_n = n;
+}
+
+/* largest e4m3 value <= x (x >= -448: the precondition of the stored form) */
+float orc_e4m3_round_down(float x)
+{
+    e4m3_init();
+    double best = e4m3_vals[0];
+    for (int i = 0; i < e4m3_n; ++i)
+        if (e4m3_vals[i] <= (double)x) best = e4m3_vals[i];
+    return (float)best;
+}
+
+/* smallest e4m3 value >= x (x <= 448) */
+float orc_e4m3_round_up(float x)
+{
+    e4m3_init();
+    double best = e4m3_vals[e4m3_n - 1];
+    for (int i = e4m3_n - 1; i >= 0; --i)
+        if (e4m3_vals[i] >= (double)x) best = e4m3_vals[i];
+    return (float)best;
+}
+
+/* fp32 -> nearest bf16 value (8 significant bits), ties to the even significand.
+ * lo = x truncated to 8 significant bits, hi = the next bf16 value away from zero. */
+float orc_bf16_round(float x)
+{
+    if (x == 0.0f || x != x) return x;
+    uint32_t b;
+    memcpy(&b, &x, 4);
+    uint32_t lob = b & 0xffff0000u, hib = lob + 0x10000u;
+    float lo, hi;
+    memcpy(&lo, &lob, 4);
+    memcpy(&hi, &hib, 4);
+    double dlo = fabs((double)x - (double)lo), dhi = fabs((double)hi - (double)x);
+    if (dlo < dhi) return lo;
+    if (dhi < dlo) return hi;
+    return ((lob >> 16) & 1u) ? hi : lo;                 /* tie: even last significand bit */
+}
+
+/* Replace freshly built fp32 metadata (orc_build_stats) by its stored form, in place.
+ * bound: 0 = KV dtype (unchanged), 1 = e4m3 outward; stat: 0 = fp32, 1 = bf16.     */
+void orc_store_meta(float *kmin, float *kmax, float *kavg, float *kvar, size_t n, int bound, int stat)
+{
+    for (size_t i = 0; i < n; ++i) {
+        if (bound == 1) {
+            kmin[i] = orc_e4m3_round_down(kmin[i]);
+            kmax[i] = orc_e4m3_round_up(kmax[i]);
+        }
+        if (stat == 1) {
+            kavg[i] = orc_bf16_round(kavg[i]);
+            kvar[i] = orc_bf16_round(kvar[i]);
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------- */
 /* Query-aware page scoring for ONE query head (kv head kvh) of one sequence. */
 /*  box  = (1/sqrt d) sum_i max(q_i kmin_i, q_i kmax_i)  Eq. box-page-bound    */
 /*         (P:321-333); evaluated as dot16x8(q, kext), kext_i = q_i>=0 ? kmax  */

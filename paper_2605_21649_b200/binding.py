@@ -43,7 +43,12 @@ class ekv_cache(ctypes.Structure):
                 ("k_pages", ctypes.c_void_p), ("v_pages", ctypes.c_void_p),
                 ("kmin", ctypes.c_void_p), ("kmax", ctypes.c_void_p),
                 ("ksum", ctypes.c_void_p), ("ksumsq", ctypes.c_void_p), ("kavg", ctypes.c_void_p),
-                ("kvar", ctypes.c_void_p), ("page_table", ctypes.c_void_p), ("seq_lens", ctypes.c_void_p)]
+                ("kvar", ctypes.c_void_p), ("page_table", ctypes.c_void_p), ("seq_lens", ctypes.c_void_p),
+                ("bound_dtype", ctypes.c_int32), ("stat_dtype", ctypes.c_int32)]
+
+
+EKV_BOUND_KV, EKV_BOUND_E4M3 = 0, 1
+EKV_STAT_F32, EKV_STAT_BF16 = 0, 1
 
 
 EKV_ATTN_DENSE_V = 1
@@ -154,15 +159,26 @@ class PagedCache:
     ksumsq: torch.Tensor
     kavg: torch.Tensor
     kvar: torch.Tensor
+    bound: str = "kv"        # "kv": kmin/kmax in the KV dtype; "e4m3": outward-rounded fp8 bytes (R24)
+    stat: str = "f32"        # "f32" | "bf16": kavg / kvar storage
 
     @classmethod
-    def allocate_meta(cls, K, V, page_table, seq_lens):
+    def allocate_meta(cls, K, V, page_table, seq_lens, bound="kv", stat="f32"):
         n_phys, Hkv, P, d = K.shape
         dev = K.device
+        if bound not in ("kv", "e4m3") or stat not in ("f32", "bf16"):
+            raise ValueError(f"bound {bound!r} / stat {stat!r}")
         mk = lambda dt: torch.zeros(n_phys, Hkv, d, dtype=dt, device=dev)
+        bdt = torch.uint8 if bound == "e4m3" else K.dtype
+        sdt = torch.bfloat16 if stat == "bf16" else torch.float32
         return cls(K, V, page_table.to(torch.int32).contiguous(), seq_lens.to(torch.int32).contiguous(),
-                   mk(K.dtype), mk(K.dtype), mk(torch.float32), mk(torch.float32), mk(torch.float32),
-                   mk(torch.float32))
+                   mk(bdt), mk(bdt), mk(torch.float32), mk(torch.float32), mk(sdt), mk(sdt), bound, stat)
+
+    def bounds_f32(self):
+        """kmin, kmax as fp32 values (decodes the e4m3 bytes)."""
+        if self.bound == "e4m3":
+            return (self.kmin.view(torch.float8_e4m3fn).float(), self.kmax.view(torch.float8_e4m3fn).float())
+        return self.kmin.float(), self.kmax.float()
 
     @property
     def batch(self):
@@ -187,7 +203,9 @@ class PagedCache:
         return ekv_cache(_DT[self.K.dtype], self.batch, Hkv, d, self.V.shape[3], P, self.max_pages, n_phys,
                          self.K.data_ptr(), self.V.data_ptr(), self.kmin.data_ptr(), self.kmax.data_ptr(),
                          self.ksum.data_ptr(), self.ksumsq.data_ptr(), self.kavg.data_ptr(), self.kvar.data_ptr(),
-                         self.page_table.data_ptr(), self.seq_lens.data_ptr())
+                         self.page_table.data_ptr(), self.seq_lens.data_ptr(),
+                         EKV_BOUND_E4M3 if self.bound == "e4m3" else EKV_BOUND_KV,
+                         EKV_STAT_BF16 if self.stat == "bf16" else EKV_STAT_F32)
 
 
 def select_params(policy="topk", k_pages=64, q_page=0.99, margin=0.0) -> ekv_select_params:

@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 #include "types.cuh"
 
@@ -576,5 +577,60 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
     float2 d;
     asm("mov.b64 {%0,%1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
     return d;
+}
+}  // namespace ekv
+
+namespace ekv {
+// ---------------------------------------------------------------- fp8 e4m3 page bounds (R24, §8(f) N3)
+// OCP e4m3 "FN": sign-magnitude byte, bias 7, no infinities, 0x7f/0xff NaN, max finite 448.
+// Positive codes 0x00..0x7e are ordered by value, negative codes 0x80..0xfe by magnitude.
+__device__ __forceinline__ float e4m3_to_f(uint32_t code) {
+    uint32_t h2;
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"((unsigned short)(code & 0xffu)));
+    return __half2float(__ushort_as_half((unsigned short)(h2 & 0xffffu)));
+}
+// round to nearest (saturating to +-448)
+__device__ __forceinline__ uint32_t e4m3_rn(float x) {
+    unsigned short r;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(0.0f), "f"(x));
+    return (uint32_t)r & 0xffu;
+}
+// largest e4m3 value <= x (kmin, rounded down); |x| <= 448 (precondition)
+__device__ __forceinline__ uint32_t e4m3_rd(float x) {
+    uint32_t c = e4m3_rn(x);
+    if (e4m3_to_f(c) > x) {
+        const uint32_t mag = c & 0x7fu;
+        if (!(c & 0x80u)) c = mag ? c - 1u : 0x81u;     // positive: one step down; +0 -> -2^-9
+        else if (mag == 0u) c = 0x81u;                  // -0 -> -2^-9
+        else if (mag < 0x7eu) c = c + 1u;               // negative: magnitude one step up
+    }
+    return c;
+}
+// smallest e4m3 value >= x (kmax, rounded up); |x| <= 448 (precondition)
+__device__ __forceinline__ uint32_t e4m3_ru(float x) {
+    uint32_t c = e4m3_rn(x);
+    if (e4m3_to_f(c) < x) {
+        const uint32_t mag = c & 0x7fu;
+        if (c & 0x80u) c = mag > 1u ? c - 1u : 0x00u;   // negative: magnitude one step down (-2^-9 -> 0)
+        else if (mag < 0x7eu) c = c + 1u;               // positive / +0: one step up
+    }
+    return c;
+}
+// 8 consecutive e4m3 bytes (8-byte aligned, shared memory) -> 8 exact fp32 values
+__device__ __forceinline__ void load8_e4m3(const unsigned char *p, float (&x)[8]) {
+    const uint2 w = *reinterpret_cast<const uint2 *>(p);
+    const uint32_t ws[2] = {w.x, w.y};
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint32_t h2;
+            asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"((unsigned short)(ws[j] >> (16 * h))));
+            const __half2 hh = *reinterpret_cast<const __half2 *>(&h2);
+            const float2 f = __half22float2(hh);
+            x[4 * j + 2 * h] = f.x;
+            x[4 * j + 2 * h + 1] = f.y;
+        }
+    }
 }
 }  // namespace ekv

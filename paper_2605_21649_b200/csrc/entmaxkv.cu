@@ -129,6 +129,10 @@ ekv_status check_cache(const ekv_cache *c, int Hq) {
     }
     if (!c->k_pages || !c->v_pages || !c->page_table || !c->seq_lens)
         return fail(EKV_ERR_INVALID_ARG, "NULL cache buffer");
+    if (c->bound_dtype != EKV_BOUND_KV && c->bound_dtype != EKV_BOUND_E4M3)
+        return fail(EKV_ERR_INVALID_ARG, "bad bound_dtype %d", c->bound_dtype);
+    if (c->stat_dtype != EKV_STAT_F32 && c->stat_dtype != EKV_STAT_BF16)
+        return fail(EKV_ERR_INVALID_ARG, "bad stat_dtype %d", c->stat_dtype);
     if (((uintptr_t)c->k_pages | (uintptr_t)c->v_pages) & 15)
         return fail(EKV_ERR_INVALID_ARG, "k_pages/v_pages must be 16-byte aligned");
     return EKV_OK;
@@ -174,6 +178,7 @@ CacheView view(const ekv_cache *c) {
     v.kmin = c->kmin; v.kmax = c->kmax;
     v.ksum = c->ksum; v.ksumsq = c->ksumsq; v.kavg = c->kavg; v.kvar = c->kvar;
     v.page_table = c->page_table; v.seq_lens = c->seq_lens;
+    v.bound = c->bound_dtype; v.stat = c->stat_dtype;
     return v;
 }
 

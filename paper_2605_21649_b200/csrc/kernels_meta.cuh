@@ -1,6 +1,7 @@
 // kernels_meta.cuh -- a0 (append + page statistics) and a1 (page scoring).
 #pragma once
 #include "common.cuh"
+#include <type_traits>
 
 namespace ekv {
 
@@ -9,6 +10,35 @@ static __global__ void __launch_bounds__(256) k_zero(uint4 *p, size_t n16) {
     pdl_launch();
     pdl_wait();
     for (size_t i = blockIdx.x * 256 + threadIdx.x; i < n16; i += (size_t)gridDim.x * 256) p[i] = make_uint4(0, 0, 0, 0);
+}
+
+// Stored page metadata (R5, R24): bounds in the KV dtype (exact) or e4m3 rounded outward
+// (kmin down, kmax up: rd(min_t k_t) = min_t rd(k_t), so incremental and bulk builds agree
+// bit for bit); kavg / kvar in fp32 or rounded to nearest-even bf16.
+template <typename T>
+__device__ __forceinline__ float load_kmin(const CacheView &c, size_t m) {
+    return c.bound ? e4m3_to_f(reinterpret_cast<const uint8_t *>(c.kmin)[m]) : Elem<T>::to_f(reinterpret_cast<const T *>(c.kmin)[m]);
+}
+template <typename T>
+__device__ __forceinline__ float load_kmax(const CacheView &c, size_t m) {
+    return c.bound ? e4m3_to_f(reinterpret_cast<const uint8_t *>(c.kmax)[m]) : Elem<T>::to_f(reinterpret_cast<const T *>(c.kmax)[m]);
+}
+template <typename T>
+__device__ __forceinline__ void store_meta(const CacheView &c, size_t m, float mn, float mx, float avg, float var) {
+    if (c.bound) {
+        reinterpret_cast<uint8_t *>(c.kmin)[m] = (uint8_t)e4m3_rd(mn);
+        reinterpret_cast<uint8_t *>(c.kmax)[m] = (uint8_t)e4m3_ru(mx);
+    } else {
+        reinterpret_cast<T *>(c.kmin)[m] = Elem<T>::from_f(mn);
+        reinterpret_cast<T *>(c.kmax)[m] = Elem<T>::from_f(mx);
+    }
+    if (c.stat) {
+        reinterpret_cast<__nv_bfloat16 *>(c.kavg)[m] = __float2bfloat16_rn(avg);
+        reinterpret_cast<__nv_bfloat16 *>(c.kvar)[m] = __float2bfloat16_rn(var);
+    } else {
+        reinterpret_cast<float *>(c.kavg)[m] = avg;
+        reinterpret_cast<float *>(c.kvar)[m] = var;
+    }
 }
 
 // ============================================================================ a0: append_kv
@@ -27,8 +57,6 @@ __global__ void __launch_bounds__(1024, 1) k_append(CacheView c, const T *__rest
     const int L = c.seq_lens[b];
     T *K = reinterpret_cast<T *>(c.Kw);
     T *V = reinterpret_cast<T *>(c.Vw);
-    T *kmin = reinterpret_cast<T *>(c.kmin);
-    T *kmax = reinterpret_cast<T *>(c.kmax);
     const int HD = c.Hkv * kD;
     for (int t = 0; t < n_tokens; ++t) {
         const int pos = L + t;
@@ -47,7 +75,7 @@ __global__ void __launch_bounds__(1024, 1) k_append(CacheView c, const T *__rest
             if (slot == 0) {
                 mn = kf; mx = kf; s = __fadd_rn(0.0f, kf); ss = __fmaf_rn(kf, kf, 0.0f);
             } else {
-                mn = Elem<T>::to_f(kmin[m]); mx = Elem<T>::to_f(kmax[m]);
+                mn = load_kmin<T>(c, m); mx = load_kmax<T>(c, m);    // (e4m3: the rounded bound)
                 if (kf < mn) mn = kf;
                 if (kf > mx) mx = kf;
                 s = __fadd_rn(c.ksum[m], kf);
@@ -58,8 +86,8 @@ __global__ void __launch_bounds__(1024, 1) k_append(CacheView c, const T *__rest
             const float m2 = __fdiv_rn(ss, cf);
             float var = __fsub_rn(m2, __fmul_rn(avg, avg));
             if (!(var > 0.0f)) var = 0.0f;
-            kmin[m] = Elem<T>::from_f(mn); kmax[m] = Elem<T>::from_f(mx);
-            c.ksum[m] = s; c.ksumsq[m] = ss; c.kavg[m] = avg; c.kvar[m] = var;
+            store_meta<T>(c, m, mn, mx, avg, var);
+            c.ksum[m] = s; c.ksumsq[m] = ss;
         }
         __syncthreads();
     }
@@ -98,9 +126,8 @@ __global__ void __launch_bounds__(256) k_rebuild(CacheView c) {
     float var = __fsub_rn(m2, __fmul_rn(avg, avg));
     if (!(var > 0.0f)) var = 0.0f;
     const size_t m = ((size_t)page * c.Hkv + h) * kD + i;
-    reinterpret_cast<T *>(c.kmin)[m] = Elem<T>::from_f(mn);
-    reinterpret_cast<T *>(c.kmax)[m] = Elem<T>::from_f(mx);
-    c.ksum[m] = s; c.ksumsq[m] = ss; c.kavg[m] = avg; c.kvar[m] = var;
+    store_meta<T>(c, m, mn, mx, avg, var);
+    c.ksum[m] = s; c.ksumsq[m] = ss;
 }
 
 // ============================================================================ a1: score_pages
@@ -132,7 +159,7 @@ template <int MODES> struct ScoreCfg {
 // flattened (b, page) space is split into equal contiguous ranges, one per CTA; the
 // producer streams the range's metadata through an NS-deep ring of SP-page stages
 // (full/empty mbarriers, no CTA-wide barrier in the loop).
-template <typename T, int G, int MODES>
+template <typename T, int G, int MODES, int FMT>
 __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(CacheView c, const T *__restrict__ q, int Hq,
                                                    float *__restrict__ box, float *__restrict__ mu,
                                                    float *__restrict__ sigma2, uint4 *__restrict__ zero,
@@ -154,8 +181,10 @@ __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(C
     const long long r0 = total * blockIdx.x / gridDim.x, r1 = total * (blockIdx.x + 1) / gridDim.x;
     stamp_cta<2>(threadIdx.x == 0, 0);
     const int HD = c.Hkv * kD;
-    const uint32_t bmm = (uint32_t)(HD * sizeof(T));          // kmin / kmax block bytes
-    const uint32_t bgs = (uint32_t)(HD * sizeof(float));      // kavg / kvar block bytes
+    constexpr bool BE = (FMT & 1) != 0;                       // e4m3 bounds (R24)
+    constexpr bool SB = (FMT & 2) != 0;                       // bf16 kavg / kvar
+    const uint32_t bmm = (uint32_t)(HD * (BE ? 1 : sizeof(T)));   // kmin / kmax block bytes
+    const uint32_t bgs = (uint32_t)(HD * (SB ? 2 : 4));           // kavg / kvar block bytes
     const uint32_t per_page = ((MODES & 1) ? 2 * bmm : 0) + ((MODES & 2) ? 2 * bgs : 0);
     if (threadIdx.x == 0) {
         for (int i = 0; i < NS; ++i) { mbar_init(&fullb[i], 1); mbar_init(&emptyb[i], NCW); }
@@ -209,14 +238,14 @@ __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(C
                         const size_t phys = (size_t)l_phys[i + k];
                         unsigned char *dst = smem + ((size_t)slot * SP + k) * per_page;
                         if (MODES & 1) {
-                            if (w == 0) bulk_g2s(dst, reinterpret_cast<const T *>(c.kmin) + phys * HD, bmm, &fullb[slot]);
-                            if (w == 1) bulk_g2s(dst + bmm, reinterpret_cast<const T *>(c.kmax) + phys * HD, bmm, &fullb[slot]);
+                            if (w == 0) bulk_g2s(dst, reinterpret_cast<const unsigned char *>(c.kmin) + phys * bmm, bmm, &fullb[slot]);
+                            if (w == 1) bulk_g2s(dst + bmm, reinterpret_cast<const unsigned char *>(c.kmax) + phys * bmm, bmm, &fullb[slot]);
                             dst += 2 * bmm;
                         }
                         if (MODES & 2) {
                             const int w2 = w - ((MODES & 1) ? 2 : 0);
-                            if (w2 == 0) bulk_g2s(dst, c.kavg + phys * HD, bgs, &fullb[slot]);
-                            if (w2 == 1) bulk_g2s(dst + bgs, c.kvar + phys * HD, bgs, &fullb[slot]);
+                            if (w2 == 0) bulk_g2s(dst, reinterpret_cast<const unsigned char *>(c.kavg) + phys * bgs, bgs, &fullb[slot]);
+                            if (w2 == 1) bulk_g2s(dst + bgs, reinterpret_cast<const unsigned char *>(c.kvar) + phys * bgs, bgs, &fullb[slot]);
                         }
                     }
                     ++si;
@@ -244,7 +273,7 @@ __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(C
     const int hwpk = 16 / c.Hkv;
     const int kvh = hw / hwpk, sub = hw % hwpk;
     const int hq0 = kvh * G;
-    if constexpr (MODES == 1 && sizeof(T) == 2) {
+    if constexpr (MODES == 1 && sizeof(T) == 2 && !BE) {
         // Box, bf16: lane c keeps q's 4 bf16x2 words of its chunk per head and the PRMT
         // selectors picking kext_i = (q_i >= 0 ? kmax_i : kmin_i) bytewise from the packed
         // kmax/kmin words (R1's kext exactly, -0 counted as >= 0); the chain is FHFMA.BF16
@@ -368,10 +397,17 @@ __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(C
             const unsigned char *pg1 = smem + ((size_t)slot * SP + (v1 ? i1 : 0)) * per_page;
             if (MODES & 1) {
                 float mn0[8], mx0[8], mn1[8], mx1[8];
-                Elem<T>::load8(reinterpret_cast<const T *>(pg0) + kvh * kD + 8 * l16, mn0);
-                Elem<T>::load8(reinterpret_cast<const T *>(pg0 + bmm) + kvh * kD + 8 * l16, mx0);
-                Elem<T>::load8(reinterpret_cast<const T *>(pg1) + kvh * kD + 8 * l16, mn1);
-                Elem<T>::load8(reinterpret_cast<const T *>(pg1 + bmm) + kvh * kD + 8 * l16, mx1);
+                if constexpr (BE) {                           // e4m3 -> fp32 (exact; F2FP unpack)
+                    load8_e4m3(pg0 + kvh * kD + 8 * l16, mn0);
+                    load8_e4m3(pg0 + bmm + kvh * kD + 8 * l16, mx0);
+                    load8_e4m3(pg1 + kvh * kD + 8 * l16, mn1);
+                    load8_e4m3(pg1 + bmm + kvh * kD + 8 * l16, mx1);
+                } else {
+                    Elem<T>::load8(reinterpret_cast<const T *>(pg0) + kvh * kD + 8 * l16, mn0);
+                    Elem<T>::load8(reinterpret_cast<const T *>(pg0 + bmm) + kvh * kD + 8 * l16, mx0);
+                    Elem<T>::load8(reinterpret_cast<const T *>(pg1) + kvh * kD + 8 * l16, mn1);
+                    Elem<T>::load8(reinterpret_cast<const T *>(pg1 + bmm) + kvh * kD + 8 * l16, mx1);
+                }
                 float acc[2 * G];
 #pragma unroll
                 for (int g = 0; g < GP; ++g) {
@@ -396,10 +432,11 @@ __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(C
                 const unsigned char *ps0 = pg0 + ((MODES & 1) ? 2 * bmm : 0);
                 const unsigned char *ps1 = pg1 + ((MODES & 1) ? 2 * bmm : 0);
                 float av0[8], vr0[8], av1[8], vr1[8];
-                Elem<float>::load8(reinterpret_cast<const float *>(ps0) + kvh * kD + 8 * l16, av0);
-                Elem<float>::load8(reinterpret_cast<const float *>(ps0 + bgs) + kvh * kD + 8 * l16, vr0);
-                Elem<float>::load8(reinterpret_cast<const float *>(ps1) + kvh * kD + 8 * l16, av1);
-                Elem<float>::load8(reinterpret_cast<const float *>(ps1 + bgs) + kvh * kD + 8 * l16, vr1);
+                using ST = typename std::conditional<SB, __nv_bfloat16, float>::type;   // exact widening
+                Elem<ST>::load8(reinterpret_cast<const ST *>(ps0) + kvh * kD + 8 * l16, av0);
+                Elem<ST>::load8(reinterpret_cast<const ST *>(ps0 + bgs) + kvh * kD + 8 * l16, vr0);
+                Elem<ST>::load8(reinterpret_cast<const ST *>(ps1) + kvh * kD + 8 * l16, av1);
+                Elem<ST>::load8(reinterpret_cast<const ST *>(ps1 + bgs) + kvh * kD + 8 * l16, vr1);
                 float am[2 * G], as[2 * G];
 #pragma unroll
                 for (int g = 0; g < GP; ++g) {

@@ -30,28 +30,42 @@ ekv_status launch_zero(uint4 *p, size_t n16, cudaStream_t st) {
 }
 
 namespace {
-template <typename T, int G, int MODES>
+template <typename T, int G, int MODES, int FMT>
 void score_go(const CacheView &v, const T *q, int Hq, float *box, float *mu, float *s2, uint4 *zero, size_t zero_n16,
               cudaStream_t st) {
     constexpr int SP = ScoreCfg<MODES>::SP, NS = ScoreCfg<MODES>::NS;
     const int HD = v.Hkv * kD;
-    const int per_page = ((MODES & 1) ? 2 * HD * (int)sizeof(T) : 0) + ((MODES & 2) ? 2 * HD * 4 : 0);
+    const int per_page = ((MODES & 1) ? 2 * HD * ((FMT & 1) ? 1 : (int)sizeof(T)) : 0) +
+                         ((MODES & 2) ? 2 * HD * ((FMT & 2) ? 2 : 4) : 0);
     const int smem = NS * SP * per_page;
-    set_smem(k_score<T, G, MODES>, smem);
-    const int per_sm = resident_per_sm(k_score<T, G, MODES>, 288, smem);
+    set_smem(k_score<T, G, MODES, FMT>, smem);
+    const int per_sm = resident_per_sm(k_score<T, G, MODES, FMT>, 288, smem);
     // persistent: one wave of resident CTAs over the flattened (b, page) space, >= 8 pages per CTA
     long long gx = ((long long)v.B * v.maxp + 7) / 8;
     if (gx > (long long)per_sm * num_sms()) gx = (long long)per_sm * num_sms();
     if (gx < 1) gx = 1;
-    launch_ex(k_score<T, G, MODES>, dim3((unsigned)gx), dim3(288), smem, st, 0, v, q, Hq, box, mu, s2, zero, zero_n16);
+    launch_ex(k_score<T, G, MODES, FMT>, dim3((unsigned)gx), dim3(288), smem, st, 0, v, q, Hq, box, mu, s2, zero, zero_n16);
 }
 template <typename T, int G>
 void score_t(const CacheView &v, const void *q, int Hq, int modes, float *box, float *mu, float *s2, uint4 *zero,
              size_t zero_n16, cudaStream_t st) {
     const T *qq = static_cast<const T *>(q);
-    if (modes == 1) score_go<T, G, 1>(v, qq, Hq, box, mu, s2, zero, zero_n16, st);
-    else if (modes == 2) score_go<T, G, 2>(v, qq, Hq, box, mu, s2, zero, zero_n16, st);
-    else score_go<T, G, 3>(v, qq, Hq, box, mu, s2, zero, zero_n16, st);
+    // FMT: bit 0 = e4m3 bounds (box), bit 1 = bf16 kavg / kvar (Gaussian)
+    const int be = v.bound ? 1 : 0, sb = v.stat ? 2 : 0;
+    if (modes == 1) {
+        if (be) score_go<T, G, 1, 1>(v, qq, Hq, box, mu, s2, zero, zero_n16, st);
+        else score_go<T, G, 1, 0>(v, qq, Hq, box, mu, s2, zero, zero_n16, st);
+    } else if (modes == 2) {
+        if (sb) score_go<T, G, 2, 2>(v, qq, Hq, box, mu, s2, zero, zero_n16, st);
+        else score_go<T, G, 2, 0>(v, qq, Hq, box, mu, s2, zero, zero_n16, st);
+    } else {
+        switch (be | sb) {
+        case 0: score_go<T, G, 3, 0>(v, qq, Hq, box, mu, s2, zero, zero_n16, st); break;
+        case 1: score_go<T, G, 3, 1>(v, qq, Hq, box, mu, s2, zero, zero_n16, st); break;
+        case 2: score_go<T, G, 3, 2>(v, qq, Hq, box, mu, s2, zero, zero_n16, st); break;
+        default: score_go<T, G, 3, 3>(v, qq, Hq, box, mu, s2, zero, zero_n16, st); break;
+        }
+    }
 }
 template <typename T>
 void score_dt(const CacheView &v, const void *q, int Hq, int modes, float *box, float *mu, float *s2, uint4 *zero,

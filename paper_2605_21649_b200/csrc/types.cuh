@@ -14,10 +14,12 @@ struct CacheView {
     int dtype, B, Hkv, maxp, nphys;
     const void *K, *V;
     void *Kw, *Vw;            // writable aliases (append)
-    void *kmin, *kmax;
-    float *ksum, *ksumsq, *kavg, *kvar;
+    void *kmin, *kmax;        // bound: 0 = KV dtype, 1 = e4m3 outward-rounded (uint8)
+    float *ksum, *ksumsq;
+    void *kavg, *kvar;        // stat: 0 = fp32, 1 = bf16 (RNE)
     const int32_t *page_table;
     int32_t *seq_lens;
+    int bound, stat;
 };
 
 // ---------------------------------------------------------------- a2 top-k

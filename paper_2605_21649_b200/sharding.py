@@ -26,7 +26,7 @@ def local_pages(n_tokens: int, rank: int, world: int, P: int = 16):
     return pages, L
 
 
-def shard_cache(K, V, page_table, seq_lens, rank: int, world: int, spare_pages: int = 0):
+def shard_cache(K, V, page_table, seq_lens, rank: int, world: int, spare_pages: int = 0, bound="kv", stat="f32"):
     """Rank `rank`'s local cache of a global paged cache (K/V [n_phys][Hkv][P][d], page_table
     [B][maxp], seq_lens [B]; host or device tensors): its pages gathered into a local pool
     (local page i -> local physical page), metadata rebuilt by the library on the device."""
@@ -56,7 +56,7 @@ def shard_cache(K, V, page_table, seq_lens, rank: int, world: int, spare_pages: 
         Kl, Vl = torch.cat([Kl, z]), torch.cat([Vl, z.clone()])
         table[table < 0] = torch.arange(n_used, n_used + extra, dtype=torch.int32)
     cache = ekv.PagedCache.allocate_meta(Kl, Vl, table.to(dev), torch.tensor([L for _, L in per_b], dtype=torch.int32,
-                                                                             device=dev))
+                                                                             device=dev), bound=bound, stat=stat)
     ekv.rebuild_page_stats(cache)
     return cache
 

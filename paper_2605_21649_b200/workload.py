@@ -12,7 +12,15 @@ Workloads (recipes restated in DESIGN.md "Input recipe"):
   star's "synthetic Llama-shaped paged KV caches with planted heavy-hitter
   keys"): anisotropic channel scales, 64 planted spans of 4 tokens per
   (sequence, kv head) aligned to one query head of the group, plus a sink at
-  token 0.  Used for quality (recall) claims.
+  token 0.  Used for quality (recall) claims.  Background keys are i.i.d. over token
+  positions: the worst case for page-level bounds (every page's box is the envelope of 16
+  independent draws).
+* ``llama``   -- ``planted`` on a background with token locality: the background key
+  sequence of each (sequence, kv head) is an AR(1) process along token positions,
+  k_t = phi k_{t-1} + sqrt(1 - phi^2) e_t (phi = 0.9, truncated to 64 taps), scaled per
+  channel as in ``planted``.  Adjacent keys of real LLM caches are similar -- the premise
+  of page-level (Quest-style) bounds the paper builds on -- so this is
+  the north star's "Llama-shaped" cache; ``planted`` stays as the locality-free stress case.
 
 Physical pages are a random permutation of the page pool (no locality), as in a
 vLLM-style paged allocator.
@@ -76,9 +84,9 @@ def make_workload(B, seq_lens, Hq, Hkv, d=128, dv=128, P=16, dtype=torch.bfloat1
     V32 = torch.randn(n_phys, Hkv, P, dv, generator=g, device=device)
     q32 = torch.randn(B, Hq, d, generator=g, device=device)
     planted = {}
-    if kind == "planted":
+    if kind in ("planted", "llama"):
         K32, planted = _plant(K32, q32, page_table, seq_lens, Hq, Hkv, P, d, g, device,
-                              n_spans, span_len, kappa)
+                              n_spans, span_len, kappa, phi=0.9 if kind == "llama" else 0.0)
     elif kind != "randn":
         raise ValueError(f"unknown workload {kind!r}")
     sl = torch.tensor(seq_lens, dtype=torch.int32, device=device)
@@ -87,11 +95,23 @@ def make_workload(B, seq_lens, Hq, Hkv, d=128, dv=128, P=16, dtype=torch.bfloat1
                     planted=planted)
 
 
-def _plant(K32, q32, page_table, seq_lens, Hq, Hkv, P, d, g, device, n_spans, span_len, kappa):
+def _ar_filter(x, phi, taps=64):
+    """x [N][d] i.i.d. N(0, 1) rows -> AR(1) rows along N: y_t = sqrt(1 - phi^2) *
+    sum_{j <= taps} phi^j x_{t-j} (unit variance up to phi^(2 taps + 2) ~ 1e-6)."""
+    N, d = x.shape
+    w = (math.sqrt(1.0 - phi * phi) * phi ** torch.arange(taps, -1, -1, dtype=torch.float32,
+                                                            device=x.device))
+    y = torch.nn.functional.conv1d(torch.nn.functional.pad(x.t().unsqueeze(0), (taps, 0)),
+                                   w.view(1, 1, -1).expand(d, 1, taps + 1).contiguous(), groups=d)
+    return y[0].t()
+
+
+def _plant(K32, q32, page_table, seq_lens, Hq, Hkv, P, d, g, device, n_spans, span_len, kappa,
+           phi=0.0):
     """Planted heavy hitters (DESIGN.md "Input recipe" W-llama-planted).
 
     Per (b, kv head): channel scales sigma_ch ~ logU[0.25, 4]; background keys
-    k = sigma_ch * N(0, I); n_spans spans of span_len consecutive tokens at uniform
+    k = sigma_ch * N(0, I) (phi > 0: k = sigma_ch * AR(1) along token positions, ``llama``); n_spans spans of span_len consecutive tokens at uniform
     positions plus a sink at token 0.  A planted key for query head h becomes
         k <- 0.6 k + kappa * sigma_bg,h * sqrt(d) * q_h / ||q_h||^2,
     so its score against q_h is raised by kappa * sigma_bg,h, where
@@ -110,7 +130,11 @@ def _plant(K32, q32, page_table, seq_lens, Hq, Hkv, P, d, g, device, n_spans, sp
             # background for all tokens of this (b, kv)
             M = (n + P - 1) // P
             phys = page_table[b, :M].long()
-            K32[phys, kv] = K32[phys, kv] * sig_ch
+            if phi > 0.0:
+                bg = _ar_filter(K32[phys, kv].reshape(M * P, d), phi)
+                K32[phys, kv] = bg.view(M, P, d) * sig_ch
+            else:
+                K32[phys, kv] = K32[phys, kv] * sig_ch
             starts = torch.randint(1, max(2, n - span_len), (n_spans,), generator=g, device=device)
             kap = kappa[0] + (kappa[1] - kappa[0]) * torch.rand(n_spans, span_len, generator=g, device=device)
             kap_sink = kappa[0] + (kappa[1] - kappa[0]) * torch.rand(G, generator=g, device=device)
