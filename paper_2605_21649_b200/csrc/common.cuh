@@ -350,6 +350,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 namespace ekv {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+// Every kernel of the decode chain starts with pdl_enter(): it waits for its predecessor (the
+// successor is scheduled when this kernel's CTAs exit -- an explicit early trigger was measured
+// slower: the successor's resident CTAs took SM slots from this kernel, C4 step 119.7 -> 129.7 us).
+// Invariant: a CTA of kernel n starts only after every CTA of kernel n-1 has exited, and n-1
+// passed its own wait only after n-2 completed, so a prologue placed BEFORE pdl_enter() may read
+// data written two or more launches back (not n-1's).
+__device__ __forceinline__ void pdl_enter() { pdl_wait(); }
 }  // namespace ekv
 
 // ---------------------------------------------------------------- optional in-kernel phase stamps
@@ -632,5 +639,39 @@ __device__ __forceinline__ void load8_e4m3(const unsigned char *p, float (&x)[8]
             x[4 * j + 2 * h + 1] = f.y;
         }
     }
+}
+}  // namespace ekv
+
+namespace ekv {
+// two e4m3 bytes (low 16 bits) -> f16x2 (exact: every e4m3 value is an f16 value; F2FP unpack)
+__device__ __forceinline__ uint32_t e4m3x2_to_h2(uint32_t two) {
+    uint32_t h2;
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"((unsigned short)(two & 0xffffu)));
+    return h2;
+}
+// fp32 accumulate of an f16 x f16 product (FHFMA, half selectors folded): the operands widen
+// exactly and the product is exact in fp32, so this is fmaf(float(a), float(b), c) -- the R1
+// chain step.  Used for the e4m3 box path with q converted to f16 when that is exact.
+__device__ __forceinline__ float fma_h_lo(uint32_t a, uint32_t b, float c) {
+    unsigned short al, ah, bl, bh;
+    asm("mov.b32 {%0,%1}, %2;" : "=h"(al), "=h"(ah) : "r"(a));
+    asm("mov.b32 {%0,%1}, %2;" : "=h"(bl), "=h"(bh) : "r"(b));
+    asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(c) : "h"(al), "h"(bl));
+    return c;
+}
+__device__ __forceinline__ float fma_h_hi(uint32_t a, uint32_t b, float c) {
+    unsigned short al, ah, bl, bh;
+    asm("mov.b32 {%0,%1}, %2;" : "=h"(al), "=h"(ah) : "r"(a));
+    asm("mov.b32 {%0,%1}, %2;" : "=h"(bl), "=h"(bh) : "r"(b));
+    asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(c) : "h"(ah), "h"(bh));
+    return c;
+}
+// bf16x2 word -> f16x2 word; *exact = both values representable in f16 (|v| in [2^-17, 65504] or 0)
+__device__ __forceinline__ uint32_t bf2_to_h2(uint32_t w, bool &exact) {
+    const float lo = __uint_as_float(w << 16), hi = __uint_as_float(w & 0xffff0000u);
+    const __half2 h = __floats2half2_rn(lo, hi);
+    const float2 back = __half22float2(h);
+    exact = exact && back.x == lo && back.y == hi;
+    return *reinterpret_cast<const uint32_t *>(&h);
 }
 }  // namespace ekv

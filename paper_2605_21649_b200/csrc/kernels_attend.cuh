@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
     const int32_t *__restrict__ page_idx, const int32_t *__restrict__ n_sel, int stride,
     float *__restrict__ scores, uint32_t *__restrict__ rowmax, int full) {
     EKV_TRACE(4);
-    pdl_wait();
+    pdl_enter();
     constexpr int SP = AttCfg<T>::SP, NS = AttCfg<T>::NS, TILE = AttCfg<T>::TILE;
     constexpr int NCW = AttCfg<T>::NCW;
     constexpr int CHK = 256;                // work slots per producer chunk (8 per lane)
@@ -374,7 +374,7 @@ static __global__ void __launch_bounds__(256) k_candidates(const float *__restri
                                                     int *__restrict__ ccount, float *__restrict__ cand_s,
                                                     int32_t *__restrict__ cand_j) {
     EKV_TRACE(5);
-    pdl_wait();
+    pdl_enter();
     __shared__ int sh[9];
     const int row = blockIdx.y;
     const int b = row / Hq;
@@ -509,7 +509,6 @@ __global__ void __launch_bounds__(256) k_delta_bar(const float *__restrict__ box
                                                    const double *__restrict__ tau, DbConst k,
                                                    double *__restrict__ out) {
     EKV_TRACE(7);
-    pdl_wait();
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     constexpr int R = kDbChunk / 1024;
@@ -523,7 +522,6 @@ __global__ void __launch_bounds__(256) k_delta_bar(const float *__restrict__ box
     const uint32_t *um = umask + (size_t)unit * W;
     const bool vec = (maxp & 3) == 0;
     const int L = __ldg(seq_lens + b);
-    const double t = __ldg(tau + row);
     float bv[4 * R];
     uint32_t mw[R];
 #pragma unroll
@@ -538,6 +536,10 @@ __global__ void __launch_bounds__(256) k_delta_bar(const float *__restrict__ box
         }
         mw[r] = (p < maxp) ? __ldg(um + (p >> 2)) : 0u;
     }
+    // box (page scoring), the union marks (top-k) and seq_lens (append) are two or more launches
+    // back: loaded above, before the wait; tau comes from the immediately preceding kernel
+    pdl_enter();
+    const double t = tau[row];
     const int M = n_pages_of(L);
     double db = 0.0, dz = 0.0;
     if (t == t) {   // tau is NaN for an empty row

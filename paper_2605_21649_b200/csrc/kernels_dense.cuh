@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(256) k_softmax_partial(CacheView c, const floa
                                                          int Hq, int G, int nch, float *__restrict__ pacc,
                                                          double *__restrict__ pl, int32_t *__restrict__ pcnt,
                                                          const double *__restrict__ ent_tau, float alpha) {
-    pdl_wait();
+    pdl_enter();
     __shared__ float red[8][kD];
     __shared__ double wl[8];
     __shared__ int wc[8];
@@ -87,7 +87,7 @@ static __global__ void __launch_bounds__(128) k_softmax_combine(const float *__r
                                                          const int32_t *__restrict__ pcnt, const uint32_t *__restrict__ rowmax,
                                                          int nch, float *__restrict__ out, double *__restrict__ tau,
                                                          int32_t *__restrict__ supp) {
-    pdl_wait();
+    pdl_enter();
     const int row = blockIdx.x;
     const uint32_t mk = rowmax[row];
     float o = 0.f;
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(256, 2) k_dense_group_partial(CacheView c, con
                                                              float *__restrict__ pacc, double *__restrict__ pl,
                                                              int32_t *__restrict__ pcnt,
                                                              const double *__restrict__ ent_tau, float alpha, int ib) {
-    pdl_wait();
+    pdl_enter();
     __shared__ float red[8][kD];
     __shared__ double wl[8][G];
     __shared__ int wc[8];

@@ -7,8 +7,7 @@ namespace ekv {
 
 // zero a byte range (16-byte aligned, multiple of 16) -- replaces a memset node in the chain
 static __global__ void __launch_bounds__(256) k_zero(uint4 *p, size_t n16) {
-    pdl_launch();
-    pdl_wait();
+    pdl_enter();
     for (size_t i = blockIdx.x * 256 + threadIdx.x; i < n16; i += (size_t)gridDim.x * 256) p[i] = make_uint4(0, 0, 0, 0);
 }
 
@@ -52,7 +51,7 @@ template <typename T>
 __global__ void __launch_bounds__(1024, 1) k_append(CacheView c, const T *__restrict__ k_new,
                                                  const T *__restrict__ v_new, int n_tokens) {
     EKV_TRACE(0);
-    pdl_wait();
+    pdl_enter();
     const int b = blockIdx.x;
     const int L = c.seq_lens[b];
     T *K = reinterpret_cast<T *>(c.Kw);
@@ -150,8 +149,17 @@ __global__ void __launch_bounds__(256) k_rebuild(CacheView c) {
 #ifndef EKV_SCORE_NS
 #define EKV_SCORE_NS 3
 #endif
-template <int MODES> struct ScoreCfg {
-    static constexpr int SP = (MODES == 1) ? EKV_SCORE_SP : 4;   // pages per stage
+#ifndef EKV_SCORE_E4M3_CTAS
+#define EKV_SCORE_E4M3_CTAS 2
+#endif
+#ifndef EKV_SCORE_E4M3_SP
+#define EKV_SCORE_E4M3_SP 16
+#endif
+template <int MODES, int FMT = 0> struct ScoreCfg {
+    // pages per stage: a stage carries about the same bytes whatever the stored form (the
+    // ring's bytes in flight, not the page count, set the stream rate): e4m3 bounds = 2x pages
+    static constexpr int SP = (MODES == 1) ? ((FMT & 1) ? EKV_SCORE_E4M3_SP : EKV_SCORE_SP)
+                                           : ((FMT & 2) ? 8 : 4);
     static constexpr int NS = EKV_SCORE_NS;                      // ring stages
 };
 
@@ -160,17 +168,19 @@ template <int MODES> struct ScoreCfg {
 // producer streams the range's metadata through an NS-deep ring of SP-page stages
 // (full/empty mbarriers, no CTA-wide barrier in the loop).
 template <typename T, int G, int MODES, int FMT>
-__global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(CacheView c, const T *__restrict__ q, int Hq,
+__global__ void __launch_bounds__(288, (MODES == 1 && (FMT & 1) && G <= 4 && sizeof(T) == 2) ? EKV_SCORE_E4M3_CTAS
+                                       : (G <= 4 && MODES != 3) ? 2 : 1) k_score(CacheView c, const T *__restrict__ q, int Hq,
                                                    float *__restrict__ box, float *__restrict__ mu,
                                                    float *__restrict__ sigma2, uint4 *__restrict__ zero,
                                                    size_t zero_n16) {
     EKV_TRACE(1);
-    pdl_wait();
     // decode's per-step counters / union mask (read by the later kernels of the step) are
-    // zeroed here, one slice per CTA -- no separate launch
+    // zeroed here, one slice per CTA -- no separate launch.  Their last readers ran two or more
+    // launches back (pdl_enter invariant), so this runs before the wait.
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < zero_n16; i += (size_t)gridDim.x * blockDim.x)
         zero[i] = make_uint4(0, 0, 0, 0);
-    constexpr int SP = ScoreCfg<MODES>::SP, NS = ScoreCfg<MODES>::NS;
+    pdl_enter();
+    constexpr int SP = ScoreCfg<MODES, FMT>::SP, NS = ScoreCfg<MODES, FMT>::NS;
     constexpr int NCW = 8;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t fullb[NS], emptyb[NS];
@@ -347,6 +357,114 @@ __global__ void __launch_bounds__(288, (G <= 4 && MODES != 3) ? 2 : 1) k_score(C
                     box[((size_t)bb * Hq + hq0 + hh) * c.maxp + q0 + it] = r;
             }
             if (!released) {                                 // no group (n <= sub): release now
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&emptyb[slot]);
+            }
+            stamp_if(threadIdx.x == 0 && si < 16, 4, 16 + si);
+        }
+        return;
+    }
+    if constexpr (MODES == 1 && sizeof(T) == 2 && BE) {
+        // Box, e4m3 bounds (R24), bf16 q: lane c unpacks its chunk's 8 kmin and 8 kmax bytes to
+        // f16x2 (F2FP, exact) and runs R1's chain as FHFMA with f16 operands on the PRMT-selected
+        // kext -- exact products, so bit-identical to fmaf(q_i, kext_i, acc).  q is converted to
+        // f16 once per sequence; a lane whose q chunk is not exactly representable in f16
+        // (|q_i| < 2^-17 or > 65504) runs the same chain in fp32 instead (same bits).
+        constexpr int IPR = (16 / G) < 2 ? 16 / G : 2;
+        constexpr int V = IPR * G;
+        uint32_t qh[G][4], sel[G][4];
+        bool qexact = true;
+        int cur_b = -1;
+        for (int si = 0;; ++si) {
+            const int slot = si % NS;
+            mbar_wait(&fullb[slot], (si / NS) & 1);
+            const int n = d_n[slot];
+            stamp_cta<2>(threadIdx.x == 0 && si == 0, 1);
+            stamp_if(threadIdx.x == 0 && si < 16, 4, si);
+            if (n < 0) { stamp_cta<2>(threadIdx.x == 0, 2); count_cta<2>(threadIdx.x == 0, si); break; }
+            const int bb = d_b[slot], q0 = d_p0[slot];
+            if (bb != cur_b) {
+                cur_b = bb;
+                qexact = true;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const uint4 w = __ldg(reinterpret_cast<const uint4 *>(q + ((size_t)bb * Hq + hq0 + g) * kD + 8 * l16));
+                    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        qh[g][j] = bf2_to_h2(ws[j], qexact);
+                        const bool plo = __uint_as_float(ws[j] << 16) >= 0.0f;
+                        const bool phi = __uint_as_float(ws[j] & 0xffff0000u) >= 0.0f;
+                        sel[g][j] = (plo ? 0x10u : 0x54u) | ((phi ? 0x32u : 0x76u) << 8);
+                    }
+                }
+            }
+            bool released = false;
+            for (int ib = 0; ib < n; ib += IPR * hwpk) {
+                uint32_t wn[IPR][4], wx[IPR][4];
+#pragma unroll
+                for (int j = 0; j < IPR; ++j) {
+                    const int it = ib + sub + j * hwpk;
+                    const unsigned char *pg = smem + ((size_t)slot * SP + (it < n ? it : 0)) * per_page;
+                    const uint2 mn = *reinterpret_cast<const uint2 *>(pg + kvh * kD + 8 * l16);
+                    const uint2 mx = *reinterpret_cast<const uint2 *>(pg + bmm + kvh * kD + 8 * l16);
+                    wn[j][0] = mn.x; wn[j][1] = mn.y; wx[j][0] = mx.x; wx[j][1] = mx.y;
+                }
+                if (ib + IPR * hwpk >= n) {                  // warp-uniform
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&emptyb[slot]);
+                    released = true;
+                }
+#pragma unroll
+                for (int j = 0; j < IPR; ++j) {              // 8 bytes -> 4 f16x2 words per bound
+                    const uint32_t a0 = wn[j][0], a1 = wn[j][1], b0 = wx[j][0], b1 = wx[j][1];
+                    wn[j][0] = e4m3x2_to_h2(a0); wn[j][1] = e4m3x2_to_h2(a0 >> 16);
+                    wn[j][2] = e4m3x2_to_h2(a1); wn[j][3] = e4m3x2_to_h2(a1 >> 16);
+                    wx[j][0] = e4m3x2_to_h2(b0); wx[j][1] = e4m3x2_to_h2(b0 >> 16);
+                    wx[j][2] = e4m3x2_to_h2(b1); wx[j][3] = e4m3x2_to_h2(b1 >> 16);
+                }
+                float acc[V];
+                if (qexact) {
+#pragma unroll
+                    for (int j = 0; j < IPR; ++j) {
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            float a = 0.0f;
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const uint32_t ke = prmt(wx[j][e], wn[j][e], sel[g][e]);
+                                a = fma_h_lo(qh[g][e], ke, a);
+                                a = fma_h_hi(qh[g][e], ke, a);
+                            }
+                            acc[j * G + g] = a;
+                        }
+                    }
+                } else {                                     // rare: the fp32 chain (q re-read from L1)
+#pragma unroll
+                    for (int j = 0; j < IPR; ++j) {
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            const uint4 qq = __ldg(reinterpret_cast<const uint4 *>(q + ((size_t)bb * Hq + hq0 + g) * kD + 8 * l16));
+                            const uint32_t qb[4] = {qq.x, qq.y, qq.z, qq.w};
+                            float a = 0.0f;
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const uint32_t ke = prmt(wx[j][e], wn[j][e], sel[g][e]);
+                                const float2 kf = __half22float2(*reinterpret_cast<const __half2 *>(&ke));
+                                a = __fmaf_rn(__uint_as_float(qb[e] << 16), kf.x, a);
+                                a = __fmaf_rn(__uint_as_float(qb[e] & 0xffff0000u), kf.y, a);
+                            }
+                            acc[j * G + g] = a;
+                        }
+                    }
+                }
+                const float r = __fmul_rn(rs_reduce16<V>(acc, lane), kCd);
+                const int vv = rs_head<V>(lane);
+                const int it = ib + sub + (vv / G) * hwpk, hh = vv % G;
+                if (rs_writer<V>(lane) && it < n)
+                    box[((size_t)bb * Hq + hq0 + hh) * c.maxp + q0 + it] = r;
+            }
+            if (!released) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&emptyb[slot]);
             }

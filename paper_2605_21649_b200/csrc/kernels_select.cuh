@@ -37,13 +37,140 @@ __device__ __forceinline__ uint32_t nibble_word(uint32_t nib, int lane) {
     return w;
 }
 
+// One histogram increment per active lane, aggregated to one shared atomic when all active
+// lanes of the warp hit the same bin (the usual case for leading digits).  (__match_any_sync
+// was measured at ~12 us for a 4-pass select over 4096 keys: far slower than this.)
+__device__ __forceinline__ void hist_add_agg(uint32_t *hist, uint32_t d, bool act, int lane) {
+    const unsigned bal = __ballot_sync(0xffffffffu, act);
+    if (bal == 0u) return;
+    const int leader = __ffs(bal) - 1;
+    const uint32_t dl = __shfl_sync(0xffffffffu, d, leader);
+    const unsigned same = __ballot_sync(0xffffffffu, act && d == dl);
+    if (same == bal) {
+        if (lane == leader) atomicAdd(&hist[dl], (uint32_t)__popc(bal));
+    } else if (act) {
+        atomicAdd(&hist[d], 1u);
+    }
+}
+
+// Block-wide k-th largest of per-thread uint32 keys (CPT per thread, 0 = no key; 1 <= k <= #keys):
+// MSB-first radix select, 8-bit digits, one shared 256-bin histogram per digit.
+// Per-warp private histograms whist[NT/32][256] (zero on entry, left zero on exit): no
+// cross-warp contention on the leading digits' single hot bin.
 template <int NT>
-__global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int Hq, int maxp,
+__device__ __forceinline__ void hist_merge(uint32_t (*whist)[256], uint32_t *hist) {
+    for (int i = threadIdx.x; i < 256; i += NT) {
+        uint32_t g = 0u;
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w) { g += whist[w][i]; whist[w][i] = 0u; }
+        hist[i] = g;
+    }
+}
+template <int NT, int CPT>
+__device__ uint32_t block_kth_largest_agg(const uint32_t (&key)[CPT], int k, uint32_t (*whist)[256], uint32_t *hist,
+                                          int *sh) {
+    uint32_t prefix = 0u, pmask = 0u;
+    int kk = k;
+    const int t = threadIdx.x, lane = t & 31;
+#pragma unroll 1
+    for (int shift = 24; shift >= 0; shift -= 8) {
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+            const bool act = key[j] != 0u && (key[j] & pmask) == prefix;
+            hist_add_agg(whist[t >> 5], (key[j] >> shift) & 255u, act, lane);
+        }
+        __syncthreads();
+        hist_merge<NT>(whist, hist);
+        __syncthreads();
+        if (t < 32) {
+            int v[8], s = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) { v[e] = (int)hist[255 - 8 * lane - e]; s += v[e]; }
+            int incl = s;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int excl = incl - s;
+            int D = -1, cab = 0, cum = excl;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                if (D < 0 && cum + v[e] >= kk) { D = 255 - 8 * lane - e; cab = cum; }
+                cum += v[e];
+            }
+            const unsigned bm = __ballot_sync(0xffffffffu, D >= 0 && excl < kk);
+            const int src = __ffs(bm) - 1;
+            D = __shfl_sync(0xffffffffu, D, src);
+            cab = __shfl_sync(0xffffffffu, cab, src);
+            if (lane == 0) { sh[0] = D; sh[1] = cab; }
+        }
+        __syncthreads();
+        prefix |= (uint32_t)sh[0] << shift;
+        pmask |= 255u << shift;
+        kk -= sh[1];
+        __syncthreads();
+    }
+    return prefix;
+}
+
+
+// ---- value-domain (linear) histogram helpers of the sample-pivot top-k
+constexpr int kLinNB = 1024;
+template <int NT> __device__ __forceinline__ uint32_t block_max_u32(uint32_t v, uint32_t *shu) {
+    v = __reduce_max_sync(0xffffffffu, v);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) shu[threadIdx.x >> 5] = v;
+    __syncthreads();
+    uint32_t r = 0u;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) r = max(r, shu[w]);
+    return r;
+}
+template <int NT> __device__ __forceinline__ uint32_t block_min_u32(uint32_t v, uint32_t *shu) {
+    v = __reduce_min_sync(0xffffffffu, v);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) shu[threadIdx.x >> 5] = v;
+    __syncthreads();
+    uint32_t r = 0xffffffffu;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) r = min(r, shu[w]);
+    return r;
+}
+// bin of an ordered key in [klo, khi]: floor((v - vlo) * sc), monotone non-decreasing in the key
+__device__ __forceinline__ int lin_bin(uint32_t key, float vlo, float sc) {
+    return min(kLinNB - 1, max(0, (int)((key2f(key) - vlo) * sc)));
+}
+// Locate the bin holding the r-th largest element of a kLinNB-bin histogram: out[0] = bin,
+// out[1] = #elements in higher bins, out[2] = the bin's count.  1 <= r <= total.
+template <int NT> __device__ __forceinline__ void lin_find(const uint32_t *lin, int r, int *sh, int *out) {
+    constexpr int PER = kLinNB / NT;                  // bins per thread, from the top down
+    const int t = threadIdx.x;
+    int loc = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) loc += (int)lin[kLinNB - 1 - (t * PER + i)];
+    int tot;
+    const int ex = block_excl_scan<NT>(loc, sh, &tot);
+    if (ex < r && r <= ex + loc) {
+        int cum = ex;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int bn = kLinNB - 1 - (t * PER + i);
+            const int c = (int)lin[bn];
+            if (cum + c >= r) { out[0] = bn; out[1] = cum; out[2] = c; break; }
+            cum += c;
+        }
+    }
+    __syncthreads();
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict__ box, int Hq, int maxp,
                                                 const int32_t *__restrict__ seq_lens, int k,
                                                 int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
                                                 int sel_stride, int G, uint32_t *__restrict__ umask, int W) {
     EKV_TRACE(2);
-    pdl_wait();
+    pdl_enter();
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     const int CL = (int)cl.num_blocks(), r = (int)cl.block_rank();
@@ -97,14 +224,237 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
         key[4 * j + 2] = (i4 + 2 < M) ? f2key(kv[j].z) : 0u;
         key[4 * j + 3] = (i4 + 3 < M) ? f2key(kv[j].w) : 0u;
     }
-    for (int i = t; i < NWp * 256; i += NT) (&whist[0][0])[i] = 0u;
-    __syncthreads();
+    // 1a. Sample pivot (exact; the cluster radix select below is the fallback).  Every CTA
+    //     publishes NT sampled keys (one per thread, spread over its range); every CTA gathers
+    //     the cluster's samples and takes, by a block radix select, the pivot T_p = the r_p-th
+    //     largest sample, r_p ~ 1.25 k / M of the samples + 16 (so that about 1.25 k keys and
+    //     always at least k, barring a 4-sigma sampling event, are >= T_p).  The candidates
+    //     key >= T_p are collected as unique composites (key << 32 | ~page: larger key first,
+    //     then the lower page, R3) -- if there are between k and kTkCap of them, every CTA
+    //     gathers them all and finds T* = the k-th largest composite (MSB-first radix select
+    //     with 8-bit digits, stopping when a digit's bin is taken whole); the selection is
+    //     composite >= T*.  Two cluster barriers instead of one per digit and a tie round.
+    bool fast = false;
+    unsigned long long tcomp = 0ull;
+    uint32_t tpiv = 0xffffffffu;
+    {
+        extern __shared__ __align__(16) unsigned long long tk_dyn[];
+        unsigned long long *lc = tk_dyn;               // [kTkCap] this CTA's candidates
+        unsigned long long *gc = tk_dyn + kTkCap;      // [kTkCap] the cluster's candidates
+        __shared__ uint32_t samp[NT];
+        __shared__ uint32_t lin[kLinNB];
+        __shared__ uint32_t linmin;
+        __shared__ int lincnt, linres[3];
+        __shared__ unsigned long long tcomp_sh;
+        __shared__ int qoff[8], qcnt[8];
+        {
+            const int si = (t & 3) * 4 + ((t >> 2) & 3);      // (keeps key[] in registers)
+            uint32_t sv0 = 0u;
+#pragma unroll
+            for (int j = 0; j < kTkKPT; ++j) sv0 = (j == si) ? key[j] : sv0;
+            samp[t] = sv0;
+        }
+        for (int i = t; i < NWp * 256; i += NT) (&whist[0][0])[i] = 0u;
+        cl.sync();                                     // (1) samples published (and whist zero)
+        ph_stamp<2>(2);
+        uint32_t sk[8];
+        int sv = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            sk[i] = (i < CL) ? cl.map_shared_rank(samp, i)[t] : 0u;
+            sv += sk[i] != 0u;
+        }
+        const int Sv = block_sum_i<NT>(sv, sh);
+        const int rp = min(Sv, (int)ceil(1.25 * (double)keff * (double)Sv / (double)M) + 16);
+        // pivot: a sample key tp with #{samples >= tp} >= rp -- the smallest sample of the
+        // linear-histogram bin (1024 bins over the samples' value range) holding the rp-th largest
+        uint32_t tp = 0xffffffffu;
+        if (rp >= 1) {
+            uint32_t smax = 0u, smin = 0xffffffffu;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (sk[i]) { smax = max(smax, sk[i]); smin = min(smin, sk[i]); }
+            {
+                const uint32_t a = __reduce_max_sync(0xffffffffu, smax), b2 = __reduce_min_sync(0xffffffffu, smin);
+                if (lane == 0) { bits[t >> 5] = a; bits[32 + (t >> 5)] = b2; }
+                __syncthreads();
+#pragma unroll
+                for (int w = 0; w < NWp; ++w) { smax = max(smax, bits[w]); smin = min(smin, bits[32 + w]); }
+            }
+            const float vlo = key2f(smin), sc = (float)kLinNB / (key2f(smax) - vlo);
+            if (smax == smin) {
+                tp = smax;
+            } else if (!(sc > 0.0f && sc < INFINITY)) {
+                tp = block_kth_largest_agg<NT, 8>(sk, rp, whist, hist[0], sh);
+            } else {
+                for (int i = t; i < kLinNB; i += NT) lin[i] = 0u;
+                if (t == 0) linmin = 0xffffffffu;
+                __syncthreads();
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (sk[i]) atomicAdd(&lin[lin_bin(sk[i], vlo, sc)], 1u);
+                __syncthreads();
+                lin_find<NT>(lin, rp, sh, linres);
+                const int B = linres[0];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (sk[i] && lin_bin(sk[i], vlo, sc) == B) atomicMin(&linmin, sk[i]);
+                __syncthreads();
+                tp = linmin;
+            }
+        }
+        tpiv = tp;
+        ph_stamp<2>(3);
+        int nc = 0;
+#pragma unroll
+        for (int j = 0; j < kTkKPT; ++j) nc += (key[j] != 0u && key[j] >= tp) ? 1 : 0;
+        int ntot;
+        int pos = block_excl_scan<NT>(nc, sh, &ntot);
+#pragma unroll
+        for (int j = 0; j < kTkKPT; ++j) {
+            if (key[j] != 0u && key[j] >= tp) {
+                if (pos < kTkCap) {
+                    const uint32_t page = (uint32_t)(base + 4 * (t + NT * (j >> 2)) + (j & 3));
+                    lc[pos] = ((unsigned long long)key[j] << 32) | (unsigned long long)(0xffffffffu - page);
+                }
+                ++pos;
+            }
+        }
+        if (t == 0) xch[0] = ntot;
+        cl.sync();                                     // (2) candidate lists published
+        ph_stamp<2>(4);
+        // the CTAs' counts in one round of parallel remote loads (lane q reads CTA q)
+        if (t < 32) {
+            const int nq = t < CL ? *cl.map_shared_rank(&xch[0], t) : 0;
+            int inc = nq;
+#pragma unroll
+            for (int o2 = 1; o2 < 8; o2 <<= 1) { const int y = __shfl_up_sync(0xffffffffu, inc, o2); if (t >= o2) inc += y; }
+            if (t < 8) { qoff[t] = inc - nq; qcnt[t] = nq; }
+        }
+        __syncthreads();
+        const int C = qoff[CL - 1] + qcnt[CL - 1];
+        fast = rp >= 1 && C >= keff && C <= kTkCap;    // uniform over the cluster
+        ph_count<2>(0, C);
+        ph_count<2>(1, (long long)rp * 10 + (fast ? 1 : 0));
+        if (fast) {
+            // gather: element i comes from the CTA q with qoff[q] <= i < qoff[q] + qcnt[q]; all of a
+            // thread's remote loads are issued before any is used
+            constexpr int GPT = kTkCap / NT;
+            unsigned long long tmp[GPT];
+#pragma unroll
+            for (int u = 0; u < GPT; ++u) {
+                const int i = t + NT * u;
+                int q = 0;
+#pragma unroll
+                for (int z = 1; z < 8; ++z) q += (z < CL && qoff[z] <= i) ? 1 : 0;
+                tmp[u] = i < C ? cl.map_shared_rank(lc, q)[i - qoff[q]] : 0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < GPT; ++u) {
+                const int i = t + NT * u;
+                if (i < C) gc[i] = tmp[u];
+            }
+            __syncthreads();                           // gc complete before the passes read it
+            // T* = the keff-th largest composite: linear histogram of the candidates' values over
+            // [tp, max], then a brute-force rank among the (few) composites of the boundary bin
+            bool done = false;
+            {
+                uint32_t cmax = 0u;
+                for (int i = t; i < C; i += NT) cmax = max(cmax, (uint32_t)(gc[i] >> 32));
+                cmax = block_max_u32<NT>(cmax, bits);
+                const float vlo = key2f(tp), sc = (float)kLinNB / (key2f(cmax) - vlo);
+                if (cmax != tp && sc > 0.0f && sc < INFINITY) {
+                    for (int i = t; i < kLinNB; i += NT) lin[i] = 0u;
+                    if (t == 0) { linmin = 0u; lincnt = 0; }
+                    __syncthreads();
+                    for (int i = t; i < C; i += NT) atomicAdd(&lin[lin_bin((uint32_t)(gc[i] >> 32), vlo, sc)], 1u);
+                    __syncthreads();
+                    lin_find<NT>(lin, keff, sh, linres);
+                    const int B = linres[0], need = keff - linres[1], cB = linres[2];
+                    unsigned long long *bb = reinterpret_cast<unsigned long long *>(&whist[0][0]);
+                    constexpr int BBCAP = NWp * 256 / 2;
+                    if (cB <= BBCAP) {
+                        for (int i = t; i < C; i += NT)
+                            if (lin_bin((uint32_t)(gc[i] >> 32), vlo, sc) == B) bb[atomicAdd(&lincnt, 1)] = gc[i];
+                        __syncthreads();
+                        for (int i = t; i < cB; i += NT) {
+                            int rk = 0;
+                            const unsigned long long me = bb[i];
+                            for (int j2 = 0; j2 < cB; ++j2) rk += bb[j2] > me;
+                            if (rk == need - 1) tcomp_sh = me;
+                        }
+                        __syncthreads();
+                        tcomp = tcomp_sh;
+                        done = true;
+                    }
+                }
+            }
+            unsigned long long pre = 0ull, pm = 0ull;
+            int kk = keff;
+            if (!done) {
+#pragma unroll 1
+            for (int pass = 0; pass < 8; ++pass) {
+                const int shift = 56 - 8 * pass;
+                for (int i0 = 0; i0 < C; i0 += NT) {   // uniform trip count (warp votes below)
+                    const int i = i0 + t;
+                    const unsigned long long xv = i < C ? gc[i] : 0ull;
+                    const bool act = i < C && (xv & pm) == pre;
+                    hist_add_agg(whist[t >> 5], (uint32_t)((xv >> shift) & 255ull), act, lane);
+                }
+                __syncthreads();
+                hist_merge<NT>(whist, hist[0]);
+                __syncthreads();
+                if (t < 32) {
+                    int v[8], s8 = 0;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) { v[e] = (int)hist[0][255 - 8 * lane - e]; s8 += v[e]; }
+                    int incl = s8;
+#pragma unroll
+                    for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, o2);
+                        if (lane >= o2) incl += y;
+                    }
+                    const int excl = incl - s8;
+                    int D = -1, cab = 0, cum = excl, cnt = 0;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        if (D < 0 && cum + v[e] >= kk) { D = 255 - 8 * lane - e; cab = cum; cnt = v[e]; }
+                        cum += v[e];
+                    }
+                    const unsigned bm = __ballot_sync(0xffffffffu, D >= 0 && excl < kk);
+                    const int src = __ffs(bm) - 1;
+                    D = __shfl_sync(0xffffffffu, D, src);
+                    cab = __shfl_sync(0xffffffffu, cab, src);
+                    cnt = __shfl_sync(0xffffffffu, cnt, src);
+                    if (lane == 0) { sh[0] = D; sh[1] = cab; sh[2] = cnt; }
+                }
+                __syncthreads();
+                pre |= (unsigned long long)sh[0] << shift;
+                pm |= 255ull << shift;
+                kk -= sh[1];
+                const int cnt = sh[2];
+                __syncthreads();
+                if (kk == cnt) break;                  // the bin is taken whole (composites are unique)
+            }
+            tcomp = pre;
+            }
+        }
+#ifdef EKV_DBG_TOPK
+        if (t == 0 && row == EKV_DBG_TOPK)
+            printf("row %d r %d CL %d M %d keff %d Sv %d rp %d tp %08x C %d nloc %d fast %d tcomp %016llx\n", row, r, CL, M,
+                   keff, Sv, rp, tp, C, xch[0], (int)fast, tcomp);
+#endif
+        ph_stamp<2>(5);
+    }
     stamp(1, 1);
     ph_stamp<2>(1);
-    // 1. radix select over the cluster
+    // 1. radix select over the cluster (fallback)
     uint32_t prefix = 0u, pmask = 0u;
     int kk = keff;                           // keys still to take among those matching prefix
-    bool whole = false;                      // the last digit's bin is taken entirely
+    bool whole = fast;                       // the last digit's bin is taken entirely
+    if (!fast) {
+    for (int i = t; i < NWp * 256; i += NT) (&whist[0][0])[i] = 0u;
+    __syncthreads();
 #pragma unroll 1
     for (int pass = 0; pass < 4; ++pass) {
         const int shift = 24 - 8 * pass;
@@ -175,6 +525,7 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
         const int cnt = sh[2];
         if (kk == cnt) { whole = true; break; }
     }
+    }
     stamp(1, 2);
     ph_stamp<2>(6);
     // selected: (key & pmask) > prefix, or (key & pmask) == prefix and (whole, or one of the
@@ -220,8 +571,15 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
         uint32_t nib = 0u;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const uint32_t v = key[4 * j + e] & pmask;
-            const bool s = v > prefix || (whole && v == prefix);
+            bool s;
+            if (fast) {
+                const uint32_t page = (uint32_t)(base + 4 * (t + NT * j) + e);
+                s = key[4 * j + e] != 0u && key[4 * j + e] >= tpiv &&          // a candidate, and
+                    (((unsigned long long)key[4 * j + e] << 32) | (unsigned long long)(0xffffffffu - page)) >= tcomp;
+            } else {
+                const uint32_t v = key[4 * j + e] & pmask;
+                s = v > prefix || (whole && v == prefix);
+            }
             nib |= (s ? 1u : 0u) << e;
         }
         const uint32_t w = nibble_word(nib, lane);
@@ -237,7 +595,11 @@ __global__ void __launch_bounds__(NT) k_topk(const float *__restrict__ box, int 
     if (t == 0) xch[1] = tot;
     cl.sync();
     int o = pos;
-    for (int q = 0; q < r; ++q) o += *cl.map_shared_rank(&xch[1], q);
+    if (r > 0) {                                             // sum of the lower ranks' counts
+        int c = (lane < r) ? *cl.map_shared_rank(&xch[1], lane) : 0;
+        c = __reduce_add_sync(0xffffffffu, c);
+        o += c;
+    }
     uint32_t v = w;
     while (v) {
         const int p = base + 32 * t + __ffs(v) - 1;
@@ -260,7 +622,7 @@ static __global__ void __launch_bounds__(256) k_mark(int Hq, int G, const int32_
                                               const int32_t *__restrict__ n_sel, int sel_stride,
                                               uint32_t *__restrict__ umask, int W) {
     EKV_TRACE(3);
-    pdl_wait();
+    pdl_enter();
     const int row = blockIdx.x;
     const int b = row / Hq, h = row % Hq;
     const int unit = b * (Hq / G) + h / G, g = h % G;
@@ -403,7 +765,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gauss_select(const float *__r
                                                      int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
                                                      int sel_stride, double *__restrict__ tau_hat_out, int cache_pages) {
     EKV_TRACE(8);
-    pdl_wait();
+    pdl_enter();
     ph_stamp<8>(0);
     int n32 = 0, n64 = 0;
     extern __shared__ float gsm[];

@@ -33,7 +33,7 @@ namespace {
 template <typename T, int G, int MODES, int FMT>
 void score_go(const CacheView &v, const T *q, int Hq, float *box, float *mu, float *s2, uint4 *zero, size_t zero_n16,
               cudaStream_t st) {
-    constexpr int SP = ScoreCfg<MODES>::SP, NS = ScoreCfg<MODES>::NS;
+    constexpr int SP = ScoreCfg<MODES, FMT>::SP, NS = ScoreCfg<MODES, FMT>::NS;
     const int HD = v.Hkv * kD;
     const int per_page = ((MODES & 1) ? 2 * HD * ((FMT & 1) ? 1 : (int)sizeof(T)) : 0) +
                          ((MODES & 2) ? 2 * HD * ((FMT & 2) ? 2 : 4) : 0);

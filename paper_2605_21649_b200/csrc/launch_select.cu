@@ -14,10 +14,13 @@ ekv_status launch_topk(const float *box, int B, int Hq, int maxp, const int32_t 
     int CL = 1;
     while (CL * per < maxp) CL *= 2;
     if (CL > 8) return fail(EKV_ERR_UNSUPPORTED, "top-k supports at most %d pages", 8 * per);
+    const int smem = 2 * kTkCap * 8;      // sample-pivot candidate lists
+    set_smem(k_topk<256>, smem);
+    set_smem(k_topk<512>, smem);
     cudaError_t e = NT == 256
-        ? launch_ex(k_topk<256>, dim3((unsigned)(B * Hq * CL)), dim3(256), 0, st, (unsigned)CL, box, Hq, maxp, sl, k,
+        ? launch_ex(k_topk<256>, dim3((unsigned)(B * Hq * CL)), dim3(256), smem, st, (unsigned)CL, box, Hq, maxp, sl, k,
                     pi, ns, stride, G, u.umask, u.W)
-        : launch_ex(k_topk<512>, dim3((unsigned)(B * Hq * CL)), dim3(512), 0, st, (unsigned)CL, box, Hq, maxp, sl, k,
+        : launch_ex(k_topk<512>, dim3((unsigned)(B * Hq * CL)), dim3(512), smem, st, (unsigned)CL, box, Hq, maxp, sl, k,
                     pi, ns, stride, G, u.umask, u.W);
     if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "k_topk: %s", cudaGetErrorString(e));
     return check_launch("k_topk");

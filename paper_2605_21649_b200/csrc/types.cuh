@@ -24,6 +24,7 @@ struct CacheView {
 
 // ---------------------------------------------------------------- a2 top-k
 constexpr int kTkKPT = 16;          // keys per thread; NT = 512 (8192 pages per CTA, <= 8 CTAs)
+constexpr int kTkCap = 4096;        // sample-pivot candidates per row (u64 composites, x2 in smem)
 
 // ---------------------------------------------------------------- a3 / a5 candidates and tau
 constexpr int kCpc = 1024;          // candidates per chunk region (k_candidates)

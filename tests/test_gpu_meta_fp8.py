@@ -163,3 +163,24 @@ def test_c4_one_million_tokens_e4m3(kind):
     for g in range(G):
         h = kv * G + g
         check_row(hc, qh[0, h], alpha, k, out, st, box[0, h], pi[0, h], ns[0, h], 0, h, M)
+
+
+def test_score_e4m3_query_not_f16_exact():
+    """The e4m3 box path runs FHFMA on q converted to f16; query chunks that f16 cannot hold
+    exactly (|q_i| < 2^-17, |q_i| > 65504) take the fp32 chain -- the box stays bit-exact."""
+    B, sl, Hq, Hkv = 2, [900, 1300], 8, 2
+    wl, dc, hc = make_pair(B, sl, Hq, Hkv, seed=12, kind="llama", bound="e4m3", stat="bf16")
+    q = wl.q.clone()
+    q[0, 1, 5] = 3e-7          # below the f16 subnormal grid for 8 significant bits
+    q[1, 6, 100] = -1.1e-6
+    q[1, 2, 64] = 7.0e4         # above f16's largest finite value
+    q = q.to(torch.bfloat16)
+    box, _, _ = ekv.score_pages(dc, q.cuda(), modes=1)
+    torch.cuda.synchronize()
+    qh = q.float().numpy()
+    G = Hq // Hkv
+    for b in range(B):
+        M = hc.n_pages(b)
+        for h in range(Hq):
+            ob, _, _ = hc.score_pages(qh[b, h], b, h // G, modes=1)
+            np.testing.assert_array_equal(box[b, h, :M].cpu().numpy(), ob, err_msg=f"b={b} h={h}")

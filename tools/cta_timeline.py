@@ -12,7 +12,9 @@ B = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 kp = int(sys.argv[4]) if len(sys.argv) > 4 else 656
 Hq, Hkv = 32, 8
 wl = make_workload(B, n, Hq, Hkv, seed=1, device=dev, spare_tokens=200)
-c = ekv.PagedCache.allocate_meta(wl.K, wl.V, wl.page_table, wl.seq_lens); ekv.rebuild_page_stats(c)
+import os
+c = ekv.PagedCache.allocate_meta(wl.K, wl.V, wl.page_table, wl.seq_lens, bound=os.environ.get('BOUNDS', 'kv'),
+                                 stat=os.environ.get('STATS', 'f32')); ekv.rebuild_page_stats(c)
 sel = ekv.select_params('topk', kp); attn = ekv.attn_params(1.5); ws = ekv.alloc_workspace(c, Hq, sel)
 st = ekv.DecodeStats(B, Hq, dev)
 L = ekv.lib(); L.entmaxkv_debug_cta.argtypes = [ctypes.c_void_p]

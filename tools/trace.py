@@ -15,14 +15,17 @@ dev = torch.device('cuda')
 Hq, Hkv = 32, 8
 M = (n + 15) // 16
 k = int(sys.argv[3]) if len(sys.argv) > 3 else max(1, -(-M // 100))
-wl = make_workload(B, n, Hq, Hkv, seed=1, device=dev, spare_tokens=200)
-c = ekv.PagedCache.allocate_meta(wl.K, wl.V, wl.page_table, wl.seq_lens)
+import os
+wl = make_workload(B, n, Hq, Hkv, seed=1, device=dev, spare_tokens=200, kind=os.environ.get('WORKLOAD', 'llama'))
+c = ekv.PagedCache.allocate_meta(wl.K, wl.V, wl.page_table, wl.seq_lens, bound=os.environ.get('BOUNDS', 'kv'),
+                                 stat=os.environ.get('STATS', 'f32'))
 ekv.rebuild_page_stats(c)
 sel = ekv.select_params('topk' if policy == 'full' else policy, k)
 attn = ekv.attn_params(float(__import__('os').environ.get('TRACE_ALPHA', '1.5')))
 ws = ekv.alloc_workspace(c, Hq, sel)
 st = ekv.DecodeStats(B, Hq, dev, delta_bar=True, gauss=policy == 'gauss')
-q, kn, vn = new_tokens(B, Hq, Hkv, seed=7, device=dev)
+_, kn, vn = new_tokens(B, Hq, Hkv, seed=7, device=dev)
+q = wl.q.contiguous()
 out = torch.empty(B, Hq, 128, dtype=torch.float32, device=dev)
 s = torch.cuda.Stream()
 L = ekv.lib()
