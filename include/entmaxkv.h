@@ -266,6 +266,10 @@ typedef struct {
     int32_t (*allreduce)(void *buf, size_t count, int32_t dtype, int32_t op, void *user, void *stream);
     int32_t (*allgather)(const void *send, void *recv, size_t bytes, void *user, void *stream);
     void *user;
+    /* 0: adaptive multisection (stops when every row converged; one small synchronous device->host
+     * read per round).  R > 0: exactly R rounds with no host read -- the step is then CUDA-graph
+     * capturable if the callbacks are (NCCL on the same stream is); R >= 12 always converges (R20). */
+    int32_t fixed_rounds;
 } ekv_comm;
 
 /* Workspace bytes for entmaxkv_decode_sharded on this local cache shape. */
@@ -287,14 +291,30 @@ size_t entmaxkv_shard_workspace_size(const ekv_cache *local, int32_t n_q_heads, 
  *   6. all-reduce(sum) of the numerator sum p_j v_j and denominator sum p_j -> out.
  * global_seq_lens: device [batch] int32, the unsharded sequence lengths.
  * Supported: policy TOPK, transform ENTMAX, integer beta = 1/(alpha-1) in {1,2,3,4}, world * k
- * <= 16384, <= 8192 candidates per row and rank (else the row's tau/out are NaN).
+ * <= 16384.  A row with more than 8192 candidates on some rank is marked on every rank in the same
+ * round (NaN out / tau, supp_count -1, EKV_STATUS_CAPACITY in the workspace status word); the
+ * adaptive mode also returns EKV_ERR_CAPACITY after the step's collectives complete.
  * stats may be NULL; fills tau, supp_count (global |S~|) and n_sel (global |C_page|).
- * Not graph-capturable (one small synchronous read per multisection round).
+ * Graph-capturable with comm->fixed_rounds > 0 (see ekv_comm).
  */
 ekv_status entmaxkv_decode_sharded(const ekv_cache *local, const int32_t *global_seq_lens, const void *q,
                                    int32_t n_q_heads, const ekv_select_params *sel, const ekv_attn_params *attn,
                                    const ekv_comm *comm, float *out, ekv_decode_stats *stats, void *workspace,
                                    void *stream);
+
+/*
+ * Device status of the last score/select/attend/decode step that used `workspace` (the word is
+ * cleared at the start of every such call, in its first kernel): bit 0 (EKV_STATUS_CAPACITY) =
+ * some row's candidate set exceeded a kernel capacity -- the exact support did not fit the tau
+ * kernel's shared-memory list (more than ~10k support tokens) or, sequence-sharded, more than
+ * 8192 candidates per row and rank; such rows get out = NaN, tau = NaN, supp_count = -1.
+ * Copies the word to *flags, synchronising `stream` (the one call that does), and returns
+ * EKV_ERR_CAPACITY when bit 0 is set, else EKV_OK.  cache / n_q_heads / sel as for
+ * entmaxkv_workspace_size.
+ */
+enum { EKV_STATUS_CAPACITY = 1 };
+ekv_status entmaxkv_workspace_status(const ekv_cache *cache, int32_t n_q_heads, const ekv_select_params *sel,
+                                     const void *workspace, int32_t *flags, void *stream);
 
 /* Number of kernels the last successful entmaxkv_decode / full_attend call on this
  * thread enqueued (for launch accounting). */

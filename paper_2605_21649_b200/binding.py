@@ -24,6 +24,7 @@ EKV_SCORE_BOX, EKV_SCORE_GAUSS = 1, 2
 
 EXPORTED = [
     "entmaxkv_last_error", "entmaxkv_version", "entmaxkv_workspace_size", "entmaxkv_select_capacity",
+    "entmaxkv_workspace_status",
     "entmaxkv_append_kv", "entmaxkv_rebuild_page_stats", "entmaxkv_score_pages", "entmaxkv_select",
     "entmaxkv_sparse_attend", "entmaxkv_full_attend", "entmaxkv_decode", "entmaxkv_last_launch_count",
     "entmaxkv_shard_workspace_size", "entmaxkv_decode_sharded",
@@ -79,7 +80,7 @@ ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p
 
 class ekv_comm(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("allreduce", ALLREDUCE_FN),
-                ("allgather", ALLGATHER_FN), ("user", ctypes.c_void_p)]
+                ("allgather", ALLGATHER_FN), ("user", ctypes.c_void_p), ("fixed_rounds", ctypes.c_int32)]
 
 
 _lib = None
@@ -109,6 +110,8 @@ def lib():
         L.entmaxkv_decode.argtypes = [P(ekv_cache), vp, i32, P(ekv_select_params), P(ekv_attn_params), vp,
                                       P(ekv_decode_stats), vp, vp]
         L.entmaxkv_last_launch_count.restype = i32
+        L.entmaxkv_workspace_status.argtypes = [P(ekv_cache), i32, P(ekv_select_params), vp, P(i32), vp]
+        L.entmaxkv_workspace_status.restype = ctypes.c_int
         L.entmaxkv_shard_workspace_size.argtypes = [P(ekv_cache), i32, P(ekv_select_params), i32]
         L.entmaxkv_shard_workspace_size.restype = ctypes.c_size_t
         L.entmaxkv_decode_sharded.argtypes = [P(ekv_cache), vp, vp, i32, P(ekv_select_params), P(ekv_attn_params),
@@ -225,6 +228,20 @@ def workspace_size(cache: PagedCache, n_q_heads: int, sel: ekv_select_params | N
     if n == 0:
         raise EkvError(EKV_ERR_INVALID_ARG, lib().entmaxkv_last_error().decode())
     return int(n)
+
+
+def workspace_status(cache: PagedCache, n_q_heads, sel, workspace, stream=None, raise_on_capacity=False) -> int:
+    """Device status word of the last call on `workspace` (EKV_STATUS_* bits; synchronises the stream)."""
+    cs = cache.c_struct()
+    f = ctypes.c_int32(0)
+    st = lib().entmaxkv_workspace_status(ctypes.byref(cs), int(n_q_heads), None if sel is None else ctypes.byref(sel),
+                                         _ptr(workspace), ctypes.byref(f), _stream(stream))
+    if st != EKV_OK and (st != EKV_ERR_CAPACITY or raise_on_capacity):
+        _check(st)
+    return int(f.value)
+
+
+EKV_STATUS_CAPACITY = 1
 
 
 def select_capacity(cache: PagedCache, sel: ekv_select_params) -> int:
@@ -377,7 +394,7 @@ def shard_workspace(cache: PagedCache, n_q_heads, sel: ekv_select_params, world:
 
 
 def decode_sharded(cache: PagedCache, global_seq_lens, q, sel: ekv_select_params, attn: ekv_attn_params, comm,
-                   workspace, out=None, stats: DecodeStats | None = None, stream=None):
+                   workspace, out=None, stats: DecodeStats | None = None, stream=None, fixed_rounds=0):
     """One sequence-sharded decode step on this rank's local cache (include/entmaxkv.h).
     `comm` provides rank, world and the collectives (see paper_2605_21649_b200.sharding); the
     library calls them back between its kernels.  Returns out [B][Hq][dv] fp32 (replicated)."""
@@ -386,7 +403,7 @@ def decode_sharded(cache: PagedCache, global_seq_lens, q, sel: ekv_select_params
         out = torch.empty(B, Hq, cache.V.shape[3], dtype=torch.float32, device=q.device)
     s = stream if stream is not None else torch.cuda.current_stream(q.device)
     comm.bind(workspace, s)
-    cm = ekv_comm(int(comm.rank), int(comm.world), comm.c_allreduce, comm.c_allgather, None)
+    cm = ekv_comm(int(comm.rank), int(comm.world), comm.c_allreduce, comm.c_allgather, None, int(fixed_rounds))
     cs = cache.c_struct()
     st = stats.c_struct() if stats is not None else None
     try:

@@ -202,6 +202,8 @@ Layout layout(const ekv_cache *c, int Hq, const ekv_select_params *sel) {
     L.n_sel = take(B * Hq * 4);
     L.tau_hat = take(B * Hq * 8);
     L.zero = o;
+    L.status = take(16);
+    L.retry = take(B * Hq * 4);
     L.rowmax = take(B * Hq * 4);
     L.ccount = take(B * Hq * (size_t)((maxp + 255) / 256) * 4);
     L.umask = take(B * Hkv * (size_t)L.W * 4);
@@ -248,7 +250,10 @@ ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t 
     int *ccount = at<int>(ws, L.ccount);
     uint32_t *um = at<uint32_t>(ws, L.umask);
     float *scores = at<float>(ws, L.scores);
-    if (!marked) EKV_TRY(launch_zero(at<uint4>(ws, L.zero), L.zero_bytes / 16, st));
+    if (!marked) {   // (the eval pass keeps the sparse pass's status word)
+        const size_t z0 = (extra && extra->tok_list) ? L.rowmax : L.zero;
+        EKV_TRY(launch_zero(at<uint4>(ws, z0), (L.zero_bytes - (z0 - L.zero)) / 16, st));
+    }
     if (!full && !marked) EKV_TRY(launch_mark(c->batch, Hq, Hq / c->n_kv_heads, pi, ns, stride, um, L.W, st));
     EKV_TRY(launch_scores(v, q, Hq, um, L.W, pi, ns, stride, scores, rowmax, full, st));
     const int rows = c->batch * Hq;
@@ -269,6 +274,8 @@ ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t 
     A.Hq = Hq; A.G = Hq / c->n_kv_heads; A.alpha = attn->alpha; A.transform = attn->transform;
     A.out = out; A.tau_out = tau; A.supp_out = supp;
     A.approx_h = attn->tau_halley > 0 ? attn->tau_halley : 0;
+    A.status = at<uint32_t>(ws, L.status);
+    A.retry = at<int32_t>(ws, L.retry);
     float *pacc = at<float>(ws, L.smx_acc);
     double *pl = at<double>(ws, L.smx_l);
     int32_t *pc = at<int32_t>(ws, L.smx_cnt);
@@ -373,6 +380,23 @@ int entmaxkv_debug_stamps(unsigned long long *out /*[8*32]*/, int *nc) {
     (void)out; (void)nc;
     return 0;
 #endif
+}
+
+ekv_status entmaxkv_workspace_status(const ekv_cache *cache, int32_t n_q_heads, const ekv_select_params *sel,
+                                     const void *workspace, int32_t *flags, void *stream) {
+    begin_call();
+    EKV_TRY(check_cache(cache, n_q_heads));
+    if (!workspace || !flags) return fail(EKV_ERR_INVALID_ARG, "NULL argument");
+    const Layout L = layout(cache, n_q_heads, sel);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint32_t f = 0u;
+    EKV_TRY(check_err(cudaMemcpyAsync(&f, static_cast<const char *>(workspace) + L.status, sizeof(f),
+                                      cudaMemcpyDeviceToHost, st), "status read"));
+    EKV_TRY(check_err(cudaStreamSynchronize(st), "status sync"));
+    *flags = (int32_t)f;
+    if (f & kStatusCapacity)
+        return fail(EKV_ERR_CAPACITY, "a row's candidate set exceeded the kernel capacity (its out/tau are NaN, supp -1)");
+    return EKV_OK;
 }
 
 size_t entmaxkv_workspace_size(const ekv_cache *cache, int32_t n_q_heads, const ekv_select_params *sel) {

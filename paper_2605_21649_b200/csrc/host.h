@@ -84,7 +84,7 @@ CacheView view(const ekv_cache *c);
 // One layout serves decode (incl. eval_exact), select, sparse_attend and full_attend.
 struct Layout {
     size_t box, mu, sigma2, page_idx, n_sel, tau_hat;
-    size_t zero, rowmax, ccount, umask, zero_bytes;   // zeroed per step / attention pass
+    size_t zero, status, retry, rowmax, ccount, umask, zero_bytes;   // zeroed per step / attention pass
     size_t tau_int, smx_acc, smx_l, smx_cnt;
     int smx_nch;
     size_t scores, cand_s, cand_j, tok_list, p_list, n_list, full_out, total;

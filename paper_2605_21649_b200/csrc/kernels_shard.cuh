@@ -202,16 +202,25 @@ __device__ __forceinline__ double probe_x(double lo, double hi, int t) {
 
 // 4. one multisection round.  red (nullable) = the previous round's all-reduced partials
 //    [rows][kShP][3] (F, #>, #>=): narrow the bracket first.  part = this round's partials.
+//    Capacity: a rank holding more than kShCap candidates of a row marks the row's first
+//    partial F(lo) = +inf; the all-reduce carries it to every rank, which all mark the row
+//    done = 4 (NaN out / tau, supp -1, EKV_STATUS_CAPACITY) in the same round -- the ranks'
+//    control flow and collectives stay in lockstep.
 template <int IB>
 __global__ void __launch_bounds__(256) k_shard_probe(const double *__restrict__ cz, const int32_t *__restrict__ ncand,
                                                      double beta, ShardRow *__restrict__ st,
-                                                     const double *__restrict__ red, double *__restrict__ part) {
+                                                     const double *__restrict__ red, double *__restrict__ part,
+                                                     uint32_t *__restrict__ status) {
     __shared__ ShardRow s;
     __shared__ double acc[kShP][3];
     const int row = blockIdx.x;
     if (threadIdx.x == 0) {
         s = st[row];
-        if (red && !s.done) {
+        if (red && !s.done && red[(size_t)row * kShP * 3] == INFINITY) {
+            s.done = 4;                                           // some rank overflowed
+            st[row] = s;
+            if (status) atomicOr(status, kStatusCapacity);
+        } else if (red && !s.done) {
             const double *r = red + (size_t)row * kShP * 3;
             // F decreasing: last probe with F >= 1 and the next one
             int t1 = 0;
@@ -253,16 +262,20 @@ __global__ void __launch_bounds__(256) k_shard_probe(const double *__restrict__ 
         if (lane == 0) { acc[t][0] = f; acc[t][1] = cg; acc[t][2] = ce; }
     }
     __syncthreads();
+    if (threadIdx.x == 0 && !red && ncand[row] > kShCap) acc[0][0] = INFINITY;   // capacity overflow marker
+    __syncthreads();
     for (int i = threadIdx.x; i < kShP * 3; i += 256) part[(size_t)row * kShP * 3 + i] = (&acc[0][0])[i];
 }
 
 // host-visible convergence summary: number of rows still open
+// (open[0] = rows still open, open[1] = rows marked capacity-overflowed)
 static __global__ void k_shard_open(const ShardRow *__restrict__ st, int rows, int *__restrict__ open) {
     __shared__ int sh[9];
-    int c = 0;
-    for (int i = threadIdx.x; i < rows; i += 256) c += st[i].done == 0;
+    int c = 0, o = 0;
+    for (int i = threadIdx.x; i < rows; i += 256) { c += st[i].done == 0; o += st[i].done == 4; }
     c = block_sum_i<256>(c, sh);
-    if (threadIdx.x == 0) *open = c;
+    o = block_sum_i<256>(o, sh);
+    if (threadIdx.x == 0) { open[0] = c; open[1] = o; }
 }
 
 // 5a. power sums of w = z - lo over the local support

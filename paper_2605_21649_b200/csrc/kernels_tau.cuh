@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
     cg::cluster_group cl = cg::this_cluster();
     const int CL = (int)cl.num_blocks(), rk = (int)cl.block_rank();
     const int row = blockIdx.x / CL;
+    if (A.retry_pass && A.retry[row] == 0) return;           // (uniform over the cluster)
     const int b = row / A.Hq, h = row % A.Hq, kvh = h / A.G;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int32_t *plist = A.page_idx + (size_t)row * A.sel_stride;
@@ -381,10 +382,15 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
         if (ncand >= 0) break;
         xlo = 0; xhi = 1 << 30; have_pg = false;
         if (newton_done) {             // support larger than the shared-memory capacity
+            if (A.retry && !A.retry_pass && cap < kTsCap) {  // reduced capacity: re-run at kTsCap
+                if (threadIdx.x == 0) A.retry[row] = 1;
+                return;
+            }
             if (threadIdx.x < kD) A.out[(size_t)row * kD + threadIdx.x] = NAN;
             if (threadIdx.x == 0) {
                 if (A.tau_out) A.tau_out[row] = NAN;
                 if (A.supp_out) A.supp_out[row] = -1;
+                if (A.status) atomicOr(A.status, kStatusCapacity);    // EKV_ERR_CAPACITY on request
             }
             return;
         }

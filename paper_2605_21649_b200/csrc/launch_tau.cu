@@ -18,12 +18,13 @@ template <typename T, int IB, bool FULL>
 ekv_status tau_ibf(const CacheView &v, const TauArgs &A0, int rows, cudaStream_t st) {
     TauArgs A = A0;
     A.cap = A.full ? kTsCap : std::min(kTsCap, (A.sel_stride * kP + 255) & ~255);
+    if (A.retry_pass) A.cap = kTsCap;
     // variable-length (Gaussian) lists run many rows of up to max_pages entries: a smaller
     // candidate capacity keeps two CTAs per SM (measured C3: 126 -> 71 us); an overflowing
     // row falls back to the streamed path.  EKV_TS_CAP overrides.
     static const int cap_env = getenv("EKV_TS_CAP") ? atoi(getenv("EKV_TS_CAP")) : 0;
     const int cap_lim = cap_env > 0 ? cap_env : A.var ? 4096 : 0;
-    if (cap_lim > 0 && !A.full) A.cap = std::min(A.cap, (cap_lim + 255) & ~255);
+    if (cap_lim > 0 && !A.full && !A.retry_pass) A.cap = std::min(A.cap, (cap_lim + 255) & ~255);
     A.pr = std::min(kPr, A.cap);
     const int smem = (4 + 4 + 4 + 1) * A.cap + (8 + 4) * A.pr + kTsVpre * kD * (int)sizeof(T);
     set_smem(k_tau_sparse<T, IB, FULL>, ts_smem<T>(), /*nonportable_cluster=*/true);
@@ -43,7 +44,7 @@ ekv_status tau_ib(const CacheView &v, const TauArgs &A0, int rows, cudaStream_t 
 
 // integer beta = 1/(alpha-1) in 1..4 is a template constant; any other alpha -> IB = 0
 template <typename T>
-ekv_status launch_tau_sparse(const CacheView &v, const TauArgs &A, int rows, cudaStream_t st) {
+ekv_status tau_dispatch(const CacheView &v, const TauArgs &A, int rows, cudaStream_t st) {
     switch (int_beta(A.alpha)) {
     case 1: return tau_ib<T, 1>(v, A, rows, st);
     case 2: return tau_ib<T, 2>(v, A, rows, st);
@@ -51,6 +52,17 @@ ekv_status launch_tau_sparse(const CacheView &v, const TauArgs &A, int rows, cud
     case 4: return tau_ib<T, 4>(v, A, rows, st);
     default: return tau_ib<T, 0>(v, A, rows, st);
     }
+}
+template <typename T>
+ekv_status launch_tau_sparse(const CacheView &v, const TauArgs &A, int rows, cudaStream_t st) {
+    EKV_TRY(tau_dispatch<T>(v, A, rows, st));
+    // variable-length lists run at a reduced candidate capacity: rows whose support did not fit
+    // are re-run at the full capacity (CTAs of the other rows exit at once)
+    const bool reduced = !A.full && A.var && A.retry;
+    if (!reduced) return EKV_OK;
+    TauArgs B = A;
+    B.retry_pass = 1;
+    return tau_dispatch<T>(v, B, rows, st);
 }
 template ekv_status launch_tau_sparse<EKV_TAU_T>(const CacheView &, const TauArgs &, int, cudaStream_t);
 

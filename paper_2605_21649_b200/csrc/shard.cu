@@ -33,7 +33,7 @@ ShardLayout shard_layout(const ekv_cache *c, int Hq, const ekv_select_params *se
     S.tau = take(rows * 8);
     S.num = take(rows * kD * 4);
     S.den = take(rows * 8);
-    S.open = take(4);
+    S.open = take(8);
     S.total = o;
     return S;
 }
@@ -125,27 +125,35 @@ ekv_status entmaxkv_decode_sharded(const ekv_cache *cache, const int32_t *global
     // 4. multisection rounds (host loop; one small device->host read per round)
     double *part = at<double>(workspace, S.part);
     int *openp = at<int>(workspace, S.open);
+    uint32_t *status = at<uint32_t>(workspace, L.status);
     auto probe = [&](const double *red) -> ekv_status {
         switch (ib) {
-        case 1: k_shard_probe<1><<<rows, 256, 0, st>>>(cz, nc, beta, rst, red, part); break;
-        case 2: k_shard_probe<2><<<rows, 256, 0, st>>>(cz, nc, beta, rst, red, part); break;
-        case 3: k_shard_probe<3><<<rows, 256, 0, st>>>(cz, nc, beta, rst, red, part); break;
-        default: k_shard_probe<4><<<rows, 256, 0, st>>>(cz, nc, beta, rst, red, part); break;
+        case 1: k_shard_probe<1><<<rows, 256, 0, st>>>(cz, nc, beta, rst, red, part, status); break;
+        case 2: k_shard_probe<2><<<rows, 256, 0, st>>>(cz, nc, beta, rst, red, part, status); break;
+        case 3: k_shard_probe<3><<<rows, 256, 0, st>>>(cz, nc, beta, rst, red, part, status); break;
+        default: k_shard_probe<4><<<rows, 256, 0, st>>>(cz, nc, beta, rst, red, part, status); break;
         }
         return check_launch("k_shard_probe");
     };
     EKV_TRY(probe(nullptr));
-    for (int round = 0; round < 13; ++round) {
+    // adaptive (fixed_rounds = 0): stop once every row has converged, one small device->host read
+    // per round from the second on; fixed_rounds = R: exactly R rounds, no host read (rows that
+    // converge early idle), so the whole step can be captured in a CUDA graph.  12 rounds of
+    // 63-way multisection exhaust fp64 (R20), so R >= 12 always converges.
+    const int fixed = comm->fixed_rounds;
+    int overflow = 0;
+    for (int round = 0; round < (fixed > 0 ? fixed : 13); ++round) {
         EKV_TRY(comm_allreduce(comm, part, (size_t)rows * kShP * 3, 1, 0, st));
         EKV_TRY(probe(part));
-        if (round < 1) continue;              // two rounds (12 bits) before the first check
+        if (fixed > 0 || round < 1) continue;   // two rounds (12 bits) before the first check
         k_shard_open<<<1, 256, 0, st>>>(rst, rows, openp);
         EKV_TRY(check_launch("k_shard_open"));
-        int open = 0;
-        if (cudaMemcpyAsync(&open, openp, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        int open[2] = {0, 0};
+        if (cudaMemcpyAsync(open, openp, 2 * sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
             cudaStreamSynchronize(st) != cudaSuccess)
             return fail(EKV_ERR_CUDA, "round sync: %s", cudaGetErrorString(cudaGetLastError()));
-        if (open == 0) break;
+        overflow = open[1];
+        if (open[0] == 0) break;
     }
     // 5. power sums -> tau
     double *sums = at<double>(workspace, S.sums);
@@ -179,6 +187,8 @@ ekv_status entmaxkv_decode_sharded(const ekv_cache *cache, const int32_t *global
         k_shard_nsel<<<(rows + 127) / 128, 128, 0, st>>>(global_seq_lens, n_q_heads, rows, sel->k_pages, stats->n_sel);
         EKV_TRY(check_launch("k_shard_nsel"));
     }
+    if (overflow > 0)   // every rank finished the step's collectives; the rows are NaN on all of them
+        return fail(EKV_ERR_CAPACITY, "%d row(s) exceed %d candidates per rank (NaN out/tau, supp -1)", overflow, kShCap);
     return EKV_OK;
 }
 

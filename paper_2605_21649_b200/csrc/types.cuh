@@ -43,7 +43,10 @@ struct TauArgs {
     int approx_h;                                                         // > 0: approximate tau, Halley steps
     int var;                                                              // list lengths vary (slices from n_sel)
     int32_t *supp_tok; int supp_cap;                                      // support token list (decode stats)
+    uint32_t *status;                                                     // workspace status word (EKV_STATUS_*)
+    int32_t *retry; int retry_pass;   // reduced-capacity rows that overflowed -> re-run at kTsCap (pass 1)
 };
+constexpr uint32_t kStatusCapacity = 1u;   // a row's candidates overflowed a kernel capacity (row NaN)
 
 constexpr int kTsNT = 256;
 constexpr int kTsCap = 10240;       // candidates in shared memory
