@@ -474,6 +474,7 @@ def main():
 
     # ---- full-cache entmax baselines (a5) on the same cache
     full_us = full_dense_us = None
+    full_out = None
     if not args.no_full:
         wsf = ekv.alloc_workspace(cache, HQ, None)
         fo = torch.empty(1, HQ, D, dtype=torch.float32, device=dev)
@@ -484,6 +485,8 @@ def main():
         attn_d = ekv.attn_params(args.alpha, dense_v=True)
         full_dense_us = time_graph(lambda: ekv.full_attend(cache, q, attn_d, workspace=wsf, out=fo, tau=ft,
                                                            supp=fsu, stream=stream), max(5, reps // 5))
+        torch.cuda.synchronize()
+        full_out = fo.clone()
         del wsf
 
     if not args.no_extras:
@@ -524,6 +527,20 @@ def main():
             qg = quality(ekv, cache, q, sg, attn, dev)
             qg.update(decode_us=g_us, q_page=0.99, margin=0.0,
                       speedup_vs_full_dense_v=(full_dense_us / g_us) if full_dense_us else None)
+            # the paper's Gaussian kernel: tau_hat passed to the decode kernel + one Halley
+            # refinement on the selected scores (R25) instead of the exact threshold
+            a1 = ekv.attn_params(args.alpha, tau_halley=1)
+            og1 = torch.empty_like(out)
+            g1_us = time_graph(lambda: ekv.decode(cache, q, sg, a1, wsg, out=og1, stats=stg, stream=stream),
+                               max(5, reps // 5))
+            ekv.decode(cache, q, sg, attn, wsg, out=og, stats=stg, stream=stream)
+            ekv.decode(cache, q, sg, a1, wsg, out=og1, stats=stg, stream=stream)
+            torch.cuda.synchronize()
+            rel = lambda x, y: float(((x - y).norm(dim=-1) / y.norm(dim=-1).clamp_min(1e-30)).mean().item())
+            qg["tau_hat_halley1"] = {"decode_us": g1_us, "R_vs_exact_sparse_mean": rel(og1, og)}
+            if full_out is not None:
+                qg["R_vs_full_mean"] = rel(og, full_out)
+                qg["tau_hat_halley1"]["R_vs_full_mean"] = rel(og1, full_out)
             line_extra["gaussian_selector"] = qg
             del wsg
         except Exception as e:  # reported, the headline stands

@@ -218,6 +218,13 @@ ekv_status entmaxkv_select(const ekv_cache *cache, int32_t n_q_heads, const floa
  * C_tok = tokens of page_idx[b][h][0..n_sel) below seq_len; p~ = alpha-entmax (exact
  * tau, R8/R9) or softmax of {s_j : j in C_tok}; out = sum p~_j v_j / sum p~_j (R12).
  * K of the KV-group union is read once (R17); V only for support tokens.
+ * tau_init (nullable, device [batch][n_q_heads] f64): with attn->tau_halley > 0, the start of
+ *   the Halley refinement instead of the histogram initialisation -- the paper's Gaussian variant,
+ *   "the selected page indices and estimated threshold are then passed to the decode kernel.
+ *   Inside the kernel, we perform one additional Halley refinement using the actual selected
+ *   scores"; a start outside [z_max - 1, z_max) is replaced by z_max - 1 (DESIGN R25).
+ *   Ignored for the exact threshold (tau_halley = 0).  entmaxkv_decode passes the Gaussian
+ *   selector's tau_hat itself when policy = GAUSS and tau_halley > 0.
  *   out  [batch][n_q_heads][value_dim] fp32
  *   tau  [batch][n_q_heads] f64 (softmax: log-normaliser)   (may be NULL)
  *   supp [batch][n_q_heads] int32                            (may be NULL)
@@ -225,7 +232,8 @@ ekv_status entmaxkv_select(const ekv_cache *cache, int32_t n_q_heads, const floa
  */
 ekv_status entmaxkv_sparse_attend(const ekv_cache *cache, const void *q, int32_t n_q_heads,
                                   const int32_t *page_idx, const int32_t *n_sel,
-                                  int32_t sel_stride, const ekv_attn_params *attn,
+                                  int32_t sel_stride, const double *tau_init,
+                                  const ekv_attn_params *attn,
                                   float *out, double *tau, int32_t *supp,
                                   void *workspace, void *stream);
 

@@ -63,7 +63,9 @@ def lib():
         L.orc_softmax.restype = c_double
         L.orc_attend.argtypes = [f32p, f32p, f32p, i32p, c_int, c_int, c_int, c_int,
                                  c_int, i32p, c_int, c_double, c_int, f64p, f64p,
-                                 f64p, f32p, c_int]
+                                 f64p, f32p, c_int, c_double]
+        L.orc_entmax_approx_init.argtypes = [f64p, c_int, c_double, c_double, c_int, f64p, f64p]
+        L.orc_entmax_approx_init.restype = c_int
         L.orc_entmax_approx.argtypes = [f64p, c_int, c_double, c_int, f64p, f64p]
         L.orc_entmax_approx.restype = c_int
         L.orc_attend.restype = c_int
@@ -151,6 +153,18 @@ def entmax_approx(z, alpha: float, halley: int):
     tau = np.zeros(1, np.float64)
     k = lib().orc_entmax_approx(_p(z, ctypes.c_double), n, float(alpha), int(halley), _p(p, ctypes.c_double),
                                 _p(tau, ctypes.c_double))
+    return p[:n], float(tau[0]), int(k)
+
+
+def entmax_approx_init(z, alpha: float, tau0: float, halley: int):
+    """The Gaussian variant's approximate threshold (tau_hat start + Halley steps; R25) on
+    already-scaled z.  Returns (unnormalised p, tau, |{z > tau}|)."""
+    z = _f64(z)
+    n = z.shape[0]
+    p = np.zeros(max(n, 1), np.float64)
+    tau = np.zeros(1, np.float64)
+    k = lib().orc_entmax_approx_init(_p(z, ctypes.c_double), n, float(alpha), float(tau0), int(halley),
+                                     _p(p, ctypes.c_double), _p(tau, ctypes.c_double))
     return p[:n], float(tau[0]), int(k)
 
 
@@ -301,7 +315,8 @@ class HostCache:
                           _p(box, ctypes.c_float), _p(mu, ctypes.c_float), _p(s2, ctypes.c_float))
         return box[:M], mu[:M], s2[:M]
 
-    def attend(self, q, b, kvh, pages, alpha, transform=0, want_p=False, want_s=False, approx_halley=0):
+    def attend(self, q, b, kvh, pages, alpha, transform=0, want_p=False, want_s=False, approx_halley=0,
+               tau_init=None):
         """Attention of one query head over the given logical pages of sequence b."""
         q = _f32(q)
         pages = _i32(pages)
@@ -316,7 +331,8 @@ class HostCache:
                              _p(pages, ctypes.c_int32), pages.shape[0], float(alpha), int(transform),
                              _p(o, ctypes.c_double), _p(tau, ctypes.c_double),
                              None if p_tok is None else _p(p_tok, ctypes.c_double),
-                             None if s_tok is None else _p(s_tok, ctypes.c_float), int(approx_halley))
+                             None if s_tok is None else _p(s_tok, ctypes.c_float), int(approx_halley),
+                             float("nan") if tau_init is None else float(tau_init))
         return {"o": o, "tau": float(tau[0]), "supp": int(k), "p": p_tok, "s": s_tok}
 
 

@@ -343,6 +343,9 @@ int orc_entmax(const double *z, int n, double alpha, double *p, double *tau_out)
 /*  4. p_i = (z_i - tau)_+^beta (normalised by the caller, R12).               */
 /* Returns |{z > tau}|.                                                         */
 /* ------------------------------------------------------------------------- */
+static int entmax_halley_from(const double *z, int n, double beta, double zmax, double t, int h, double *p,
+                              double *tau_out);
+
 int orc_entmax_approx(const double *z, int n, double alpha, int h, double *p, double *tau_out)
 {
     const double beta = 1.0 / (alpha - 1.0);
@@ -362,6 +365,33 @@ int orc_entmax_approx(const double *z, int n, double alpha, int h, double *p, do
         for (int b = 0; b < k; ++b) lb += cnt[b] * powb((double)(k - 1 - b) / 64.0, beta);
         if (lb >= 1.0) { t = zmax - (double)k / 64.0; break; }
     }
+    return entmax_halley_from(z, n, beta, zmax, t, h, p, tau_out);
+}
+
+/* ------------------------------------------------------------------------- */
+/* The Gaussian variant's approximate tau ("The selected page indices  */
+/* and estimated threshold are then passed to the decode kernel. Inside the   */
+/* kernel, we perform one additional Halley refinement using the actual       */
+/* selected scores"): start at the selector's tau_hat, then h Halley steps     */
+/* (step 3 above).  DESIGN R25: tau_hat outside [z_max - 1, z_max) -- where    */
+/* the exact tau always lies (F(z_max - 1) >= 1 > F(z_max) = 0) -- is replaced */
+/* by z_max - 1.                                                              */
+/* ------------------------------------------------------------------------- */
+int orc_entmax_approx_init(const double *z, int n, double alpha, double tau0, int h, double *p, double *tau_out)
+{
+    const double beta = 1.0 / (alpha - 1.0);
+    if (n <= 0) { if (tau_out) *tau_out = NAN; return 0; }
+    double zmax = z[0];
+    for (int i = 1; i < n; ++i) if (z[i] > zmax) zmax = z[i];
+    double t = (tau0 >= zmax - 1.0 && tau0 < zmax) ? tau0 : zmax - 1.0;
+    return entmax_halley_from(z, n, beta, zmax, t, h, p, tau_out);
+}
+
+/* h Halley steps from t (step 3); R25: an iterate below z_max - 1 (the exact tau's lower bound)
+ * is raised to z_max - 1. */
+static int entmax_halley_from(const double *z, int n, double beta, double zmax, double t, int h, double *p,
+                              double *tau_out)
+{
     for (int it = 0; it < h; ++it) {
         double s0 = 0.0, s1 = 0.0, s2 = 0.0;   /* sum w^beta, w^(beta-1), w^(beta-2), w = z - t > 0 */
         for (int i = 0; i < n; ++i) {
@@ -376,6 +406,7 @@ int orc_entmax_approx(const double *z, int n, double alpha, int h, double *p, do
         double den = 2.0 * fp * fp - f * fpp;
         if (!(den != 0.0)) break;
         t -= 2.0 * f * fp / den;
+        if (t < zmax - 1.0) t = zmax - 1.0;
     }
     int k = 0;
     for (int i = 0; i < n; ++i) {
@@ -412,7 +443,7 @@ int orc_attend(const float *q, const float *Kp, const float *Vp,
                const int32_t *page_row, int seq_len, int kvh, int Hkv, int P,
                int dv, const int32_t *pages, int n_pages, double alpha,
                int transform, double *o, double *tau, double *p_tok,
-               float *s_tok, int approx_h)
+               float *s_tok, int approx_h, double tau0)
 {
     const int d = ORC_D;
     int cap = n_pages * P;
@@ -435,6 +466,8 @@ int orc_attend(const float *q, const float *Kp, const float *Vp,
     }
     int ret;
     if (n == 0) ret = 0, *tau = NAN;
+    else if (transform == 0 && approx_h > 0 && tau0 == tau0)     /* tau0 given (not NaN): P:488 */
+        ret = orc_entmax_approx_init(z, n, alpha, tau0, approx_h, pr, tau);
     else if (transform == 0 && approx_h > 0) ret = orc_entmax_approx(z, n, alpha, approx_h, pr, tau);
     else if (transform == 0) ret = orc_entmax(z, n, alpha, pr, tau);
     else { *tau = orc_softmax(z, n, pr); ret = n; }

@@ -105,7 +105,8 @@ def lib():
         L.entmaxkv_rebuild_page_stats.argtypes = [P(ekv_cache), vp]
         L.entmaxkv_score_pages.argtypes = [P(ekv_cache), vp, i32, i32, vp, vp, vp, vp, vp]
         L.entmaxkv_select.argtypes = [P(ekv_cache), i32, vp, vp, vp, P(ekv_select_params), f32, vp, vp, i32, vp, vp, vp]
-        L.entmaxkv_sparse_attend.argtypes = [P(ekv_cache), vp, i32, vp, vp, i32, P(ekv_attn_params), vp, vp, vp, vp, vp]
+        L.entmaxkv_sparse_attend.argtypes = [P(ekv_cache), vp, i32, vp, vp, i32, vp, P(ekv_attn_params), vp, vp, vp, vp,
+                                             vp]
         L.entmaxkv_full_attend.argtypes = [P(ekv_cache), vp, i32, P(ekv_attn_params), vp, vp, vp, vp, vp]
         L.entmaxkv_decode.argtypes = [P(ekv_cache), vp, i32, P(ekv_select_params), P(ekv_attn_params), vp,
                                       P(ekv_decode_stats), vp, vp]
@@ -295,7 +296,8 @@ def select(cache: PagedCache, n_q_heads, sel: ekv_select_params, alpha=1.5, box=
     return page_idx, n_sel, tau_hat
 
 
-def sparse_attend(cache: PagedCache, q, page_idx, n_sel, attn: ekv_attn_params, workspace=None, stream=None):
+def sparse_attend(cache: PagedCache, q, page_idx, n_sel, attn: ekv_attn_params, workspace=None, stream=None,
+                  tau_init=None):
     B, Hq, _ = q.shape
     dev = q.device
     stride = page_idx.shape[2]
@@ -306,7 +308,9 @@ def sparse_attend(cache: PagedCache, q, page_idx, n_sel, attn: ekv_attn_params, 
     supp = torch.empty(B, Hq, dtype=torch.int32, device=dev)
     cs = cache.c_struct()
     _check(lib().entmaxkv_sparse_attend(ctypes.byref(cs), _ptr(q.contiguous()), Hq, _ptr(page_idx.contiguous()),
-                                        _ptr(n_sel.contiguous()), stride, ctypes.byref(attn), _ptr(out), _ptr(tau),
+                                        _ptr(n_sel.contiguous()), stride,
+                                        _ptr(None if tau_init is None else tau_init.contiguous()),
+                                        ctypes.byref(attn), _ptr(out), _ptr(tau),
                                         _ptr(supp), _ptr(workspace), _stream(stream)))
     return out, tau, supp
 

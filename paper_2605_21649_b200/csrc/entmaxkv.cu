@@ -465,8 +465,9 @@ ekv_status entmaxkv_select(const ekv_cache *cache, int32_t n_q_heads, const floa
 }
 
 ekv_status entmaxkv_sparse_attend(const ekv_cache *cache, const void *q, int32_t n_q_heads, const int32_t *page_idx,
-                                  const int32_t *n_sel, int32_t sel_stride, const ekv_attn_params *attn, float *out,
-                                  double *tau, int32_t *supp, void *workspace, void *stream) {
+                                  const int32_t *n_sel, int32_t sel_stride, const double *tau_init,
+                                  const ekv_attn_params *attn, float *out, double *tau, int32_t *supp, void *workspace,
+                                  void *stream) {
     begin_call();
     EKV_TRY(check_cache(cache, n_q_heads));
     EKV_TRY(check_attn(attn));
@@ -474,8 +475,11 @@ ekv_status entmaxkv_sparse_attend(const ekv_cache *cache, const void *q, int32_t
     EKV_TRY(check_q(q));
     if (sel_stride < 1) return fail(EKV_ERR_INVALID_ARG, "sel_stride < 1");
     Layout L = layout(cache, n_q_heads, nullptr);
+    TauArgs xa;
+    memset(&xa, 0, sizeof(xa));
+    xa.tau_init = tau_init;
     return attend_impl(cache, q, n_q_heads, page_idx, n_sel, sel_stride, 0, attn, out, tau, supp, workspace, L,
-                       static_cast<cudaStream_t>(stream), nullptr);
+                       static_cast<cudaStream_t>(stream), &xa);
 }
 
 ekv_status entmaxkv_full_attend(const ekv_cache *cache, const void *q, int32_t n_q_heads, const ekv_attn_params *attn,
@@ -538,6 +542,7 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
     TauArgs xa;
     memset(&xa, 0, sizeof(xa));
     xa.var = sel->policy == EKV_GAUSS;
+    if (sel->policy == EKV_GAUSS && attn->tau_halley > 0) xa.tau_init = th;   // tau_hat + Halley
     if (stats && stats->supp_tok && stats->supp_cap > 0 && attn->transform == EKV_ENTMAX) {
         xa.supp_tok = stats->supp_tok;
         xa.supp_cap = stats->supp_cap;

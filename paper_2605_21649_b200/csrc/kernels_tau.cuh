@@ -411,6 +411,12 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
     if (A.approx_h > 0) {
         __shared__ unsigned hcnt[64];
         __shared__ double s_t0;
+        if (A.tau_init) {
+            // the Gaussian variant: start at the selector's tau_hat; outside
+            // [z_max - 1, z_max) (where the exact tau lies) the start is z_max - 1 (R25)
+            const double t0 = A.tau_init[row];
+            if (threadIdx.x == 0) s_t0 = (t0 >= zmax - 1.0 && t0 < zmax) ? t0 : zmax - 1.0;
+        } else {
         if (threadIdx.x < 64) hcnt[threadIdx.x] = 0u;
         __syncthreads();
         for (int k = threadIdx.x; k < ncand; k += NT) {
@@ -438,6 +444,7 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
             else if (m1) kst = 32 + __ffs(m1);
             if (lane == 0) s_t0 = kst ? zmax - (double)kst / 64.0 : zmax - 1.0;
         }
+        }
         __syncthreads();
         double t = s_t0;
         for (int it = 0; it < A.approx_h; ++it) {
@@ -456,6 +463,7 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
             const double den = 2.0 * fp * fp - f * fpp;
             if (!(den != 0.0)) break;
             t -= 2.0 * f * fp / den;
+            t = fmax(t, zmax - 1.0);       // R25: never below the exact tau's lower bound
         }
         int mine = 0;
         for (int k = threadIdx.x; k < ncand; k += NT) {

@@ -41,6 +41,7 @@ struct TauArgs {
     int no_pv;                                                            // tau/supp only (dense-V)
     int cap, pr;                                                          // tau kernel capacities
     int approx_h;                                                         // > 0: approximate tau, Halley steps
+    const double *tau_init;                                               // approx: start, else histogram
     int var;                                                              // list lengths vary (slices from n_sel)
     int32_t *supp_tok; int supp_cap;                                      // support token list (decode stats)
     uint32_t *status;                                                     // workspace status word (EKV_STATUS_*)

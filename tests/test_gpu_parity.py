@@ -432,3 +432,48 @@ def test_errors_fail_loudly():
     box, mu, s2 = ekv.score_pages(dc, wl.q.cuda(), modes=3)
     with pytest.raises(ekv.EkvError):
         ekv.select(dc, 4, ekv.select_params("gauss"), alpha=1.7, mu=mu, sigma2=s2)   # non-integer beta
+
+
+@pytest.mark.parametrize("alpha", [1.5, 2.0, 1.25])
+@pytest.mark.parametrize("h", [1, 2])
+def test_decode_gaussian_tau_hat_halley(alpha, h):
+    """N1, the paper's Gaussian variant: the selector's tau_hat is passed to the decode
+    kernel, which performs h Halley refinements on the selected scores (R25).  Against the oracle
+    from the same tau_hat (the GPU's, within 1e-10 of the oracle's, R14) and the same pages."""
+    B, sl, Hq, Hkv = 2, [3000, 1777], 8, 2
+    wl, dc, hc = make_pair(B, sl, Hq, Hkv, seed=29, kind="llama")
+    G = Hq // Hkv
+    sel = ekv.select_params("gauss", 0, 0.99, 0.0)
+    ws = ekv.alloc_workspace(dc, Hq, sel)
+    st = ekv.DecodeStats(B, Hq, torch.device("cuda"), delta_bar=False, gauss=True)
+    out = ekv.decode(dc, wl.q.cuda(), sel, ekv.attn_params(alpha, tau_halley=h), ws, stats=st).cpu().numpy()
+    torch.cuda.synchronize()
+    qh = q_host(wl)
+    zq = oracle.zq_table(0.99, 16)
+    for b in range(B):
+        counts = hc.page_counts(b)
+        for hh in range(Hq):
+            ref = oracle.decode_head(hc, qh[b, hh], b, hh // G, alpha, policy="gauss")
+            tg = float(st.tau_hat[b, hh])
+            assert abs(tg - ref["tau_hat"]) <= 1e-10 * max(1.0, abs(ref["tau_hat"]))
+            pages = oracle.gauss_select(ref["mu"], ref["sigma2"], counts, alpha, tg, 0.0, zq)
+            att = hc.attend(qh[b, hh], b, hh // G, pages, alpha, approx_halley=h, tau_init=tg)
+            np.testing.assert_allclose(out[b, hh], att["o"], atol=2e-3, rtol=0, err_msg=f"b={b} h={hh}")
+            assert abs(float(st.tau[b, hh]) - att["tau"]) <= 1e-6 * max(1.0, abs(att["tau"])), (b, hh)
+            assert int(st.supp_count[b, hh]) == att["supp"], (b, hh)
+
+
+def test_sparse_attend_tau_init_api():
+    """entmaxkv_sparse_attend's tau_init: the exact tau as the start is a fixed point (one Halley
+    step leaves it in place), so the approximate output equals the exact one."""
+    B, sl, Hq, Hkv, alpha = 2, [2000, 1500], 8, 2, 1.5
+    wl, dc, hc = make_pair(B, sl, Hq, Hkv, seed=31, kind="planted")
+    box, _, _ = ekv.score_pages(dc, wl.q.cuda(), modes=1)
+    pi, ns, _ = ekv.select(dc, Hq, ekv.select_params("topk", 20), box=box)
+    o_ex, t_ex, s_ex = ekv.sparse_attend(dc, wl.q.cuda(), pi, ns, ekv.attn_params(alpha))
+    o_ap, t_ap, s_ap = ekv.sparse_attend(dc, wl.q.cuda(), pi, ns, ekv.attn_params(alpha, tau_halley=1),
+                                         tau_init=t_ex.clone())
+    torch.cuda.synchronize()
+    assert torch.allclose(t_ap, t_ex, rtol=1e-12, atol=1e-12)
+    assert torch.equal(s_ap, s_ex)
+    assert (o_ap - o_ex).abs().max().item() <= 1e-6

@@ -188,3 +188,50 @@ def test_gaussian_moments_equal_token_score_moments_on_orthogonal_design():
         var_s = float(np.mean((s - s.mean()) ** 2))
         assert abs(float(s2[0]) - var_s) <= 2e-6 * max(1e-3, var_s), (trial, float(s2[0]), var_s)
         assert abs(float(mu[0]) - s.mean()) <= 1e-5 * max(1.0, abs(s.mean()))
+
+
+# ------------------------------------------------------------------ tau_hat-initialised Halley (R25)
+@pytest.mark.parametrize("alpha", [1.25, 1.5, 2.0, 4.0 / 3.0])
+def test_approx_init_one_halley_step_decimal(alpha):
+    """P:488 (Gaussian variant): tau_1 = one Halley step from the given tau_hat, the same update
+    as P:485's, here recomputed in 50-digit decimal from an arbitrary start inside
+    [z_max - 1, z_max) (DESIGN R25)."""
+    getcontext().prec = 50
+    beta = round(1.0 / (alpha - 1.0))
+    rng = np.random.default_rng(15)
+    for trial in range(6):
+        z = (alpha - 1.0) * rng.standard_normal(int(rng.integers(20, 300))) * 2.0
+        zmax = float(z.max())
+        _, tex, _ = oracle.entmax(z, alpha)
+        t0 = tex - rng.uniform(0.05, 0.9) * (tex - (zmax - 1.0))        # left of the root, in range
+        _, t1, _ = oracle.entmax_approx_init(z, alpha, t0, 1)
+        T = Decimal(repr(t0))
+        w = [Decimal(repr(float(v))) - T for v in z]
+        w = [x for x in w if x > 0]
+        S = lambda m: sum(x ** m for x in w) if m > 0 else (Decimal(len(w)) if m == 0 else Decimal(0))
+        f, fp, fpp = S(beta) - 1, -beta * S(beta - 1), beta * (beta - 1) * S(beta - 2)
+        ref = T - 2 * f * fp / (2 * fp * fp - f * fpp)
+        assert abs(t1 - float(ref)) <= 1e-13 * max(1.0, abs(float(ref))), (alpha, trial)
+
+
+@pytest.mark.parametrize("alpha", [1.25, 1.5, 2.0])
+def test_approx_init_fixed_point_range_and_convergence(alpha):
+    """The exact tau is a fixed point of the refinement; a start outside [z_max - 1, z_max) is
+    replaced by z_max - 1 (R25); iterates never fall below z_max - 1; many steps reach the exact
+    tau (pinned to the closed forms / brute force in test_oracle_pins.py)."""
+    rng = np.random.default_rng(16)
+    for trial in range(8):
+        z = (alpha - 1.0) * rng.standard_normal(int(rng.integers(10, 400))) * 3.0
+        zmax = float(z.max())
+        p_ex, tex, kex = oracle.entmax(z, alpha)
+        _, t1, k1 = oracle.entmax_approx_init(z, alpha, tex, 1)
+        assert abs(t1 - tex) <= 1e-12 * max(1.0, abs(tex)) and k1 == kex
+        for bad in (zmax, zmax + 3.0, zmax - 1.5, float("inf")):
+            _, tb, _ = oracle.entmax_approx_init(z, alpha, bad, 2)
+            _, tr, _ = oracle.entmax_approx_init(z, alpha, zmax - 1.0, 2)
+            assert tb == tr
+        for h in (1, 2, 3):
+            _, th, _ = oracle.entmax_approx_init(z, alpha, zmax - 0.999, h)
+            assert th >= zmax - 1.0
+        _, t12, k12 = oracle.entmax_approx_init(z, alpha, zmax - 0.5, 12)
+        assert abs(t12 - tex) <= 1e-10 * max(1.0, abs(tex)) and k12 == kex
