@@ -92,8 +92,12 @@ typedef struct {
 /* alpha > 1; transform = ekv_transform (softmax ignores alpha).
  * flags: EKV_ATTN_DENSE_V -- entmaxkv_full_attend streams EVERY V row (weights p_j, zero
  * outside the support), the paper's full-cache reference that reads all scores and V
- * (P:1343); without it the full path reads V of the support only.  Ignored elsewhere. */
-enum { EKV_ATTN_DENSE_V = 1 };
+ * (P:1343); without it the full path reads V of the support only.  Ignored elsewhere.
+ * EKV_ATTN_CANONICAL -- the full path of a bf16 cache scores every token on tensor cores by
+ *   default (mma bf16 -> fp32; the products are exact, the accumulation order is the tensor
+ *   core's, DESIGN R26), so its scores may differ from the canonical order of R1 in the last
+ *   bits; this flag keeps R1 (bit-identical to the sparse path's scores). */
+enum { EKV_ATTN_DENSE_V = 1, EKV_ATTN_CANONICAL = 2 };
 /* tau_halley > 0 (entmax): the paper's approximate threshold instead of the exact one
  * ("a histogram-based initialization followed by Halley iterations"; DESIGN R23):
  * tau_0 from a 64-bin histogram of z over (z_max - 1, z_max] (the largest bin edge whose

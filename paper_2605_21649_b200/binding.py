@@ -53,6 +53,7 @@ EKV_STAT_F32, EKV_STAT_BF16 = 0, 1
 
 
 EKV_ATTN_DENSE_V = 1
+EKV_ATTN_CANONICAL = 2
 
 
 class ekv_attn_params(ctypes.Structure):
@@ -217,10 +218,12 @@ def select_params(policy="topk", k_pages=64, q_page=0.99, margin=0.0) -> ekv_sel
     return ekv_select_params(pol, int(k_pages), float(q_page), float(margin))
 
 
-def attn_params(alpha=1.5, transform="entmax", dense_v=False, tau_halley=0) -> ekv_attn_params:
-    """tau_halley > 0: the paper's approximate threshold (histogram init + that many Halley steps)."""
+def attn_params(alpha=1.5, transform="entmax", dense_v=False, tau_halley=0, canonical=False) -> ekv_attn_params:
+    """tau_halley > 0: the paper's approximate threshold (histogram init + that many Halley steps).
+    canonical: the full path scores in R1's order instead of on tensor cores (R26)."""
     return ekv_attn_params(float(alpha), {"entmax": EKV_ENTMAX, "softmax": EKV_SOFTMAX}[transform],
-                           EKV_ATTN_DENSE_V if dense_v else 0, int(tau_halley))
+                           (EKV_ATTN_DENSE_V if dense_v else 0) | (EKV_ATTN_CANONICAL if canonical else 0),
+                           int(tau_halley))
 
 
 def workspace_size(cache: PagedCache, n_q_heads: int, sel: ekv_select_params | None) -> int:

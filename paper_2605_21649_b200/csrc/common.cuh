@@ -216,6 +216,34 @@ template <int NT> __device__ __forceinline__ int block_sum_i(int v, int *sh) {
     return sh[0];
 }
 // exclusive block scan of ints; returns exclusive prefix, total via *tot
+// the same scan on 64-bit words (used with packed 16-bit count fields)
+template <int NT>
+__device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long long v, unsigned long long *sh,
+                                                                  unsigned long long *tot) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (l >= o) x += y;
+    }
+    __syncthreads();
+    if (l == 31) sh[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long s = (l < NT / 32) ? sh[l] : 0ull;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long y = __shfl_up_sync(0xffffffffu, s, o);
+            if (l >= o) s += y;
+        }
+        if (l < NT / 32) sh[l] = s;
+    }
+    __syncthreads();
+    const unsigned long long base = (w > 0) ? sh[w - 1] : 0ull;
+    *tot = sh[NT / 32 - 1];
+    return base + x - v;
+}
 template <int NT> __device__ __forceinline__ int block_excl_scan(int v, int *sh, int *tot) {
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     int x = v;

@@ -216,6 +216,7 @@ Layout layout(const ekv_cache *c, int Hq, const ekv_select_params *sel) {
     L.n_list = take(B * Hq * 4);
     L.full_out = take(B * Hq * kD * 4);
     L.tau_int = take(B * Hq * 8);
+    L.sink = take(16);
     L.smx_nch = (int)((maxp + kSmxPages - 1) / kSmxPages);
     L.smx_acc = take(B * Hq * (size_t)L.smx_nch * kD * 4);
     L.smx_l = take(B * Hq * (size_t)L.smx_nch * 8);
@@ -255,7 +256,13 @@ ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t 
         EKV_TRY(launch_zero(at<uint4>(ws, z0), (L.zero_bytes - (z0 - L.zero)) / 16, st));
     }
     if (!full && !marked) EKV_TRY(launch_mark(c->batch, Hq, Hq / c->n_kv_heads, pi, ns, stride, um, L.W, st));
-    EKV_TRY(launch_scores(v, q, Hq, um, L.W, pi, ns, stride, scores, rowmax, full, st));
+    // full rows (a5/a6 baseline) of a bf16 cache: the score pass is a dense contraction, run on
+    // tensor cores (R26); the eval pass and EKV_ATTN_CANONICAL keep the canonical order (R1)
+    const int G = Hq / c->n_kv_heads;
+    const bool tc = full && c->dtype == EKV_BF16 && !(extra && extra->tok_list) &&
+                    !(attn->flags & EKV_ATTN_CANONICAL) && (G == 1 || G == 2 || G == 4 || G == 8);
+    if (tc) EKV_TRY(launch_full_scores_mma(v, q, Hq, scores, rowmax, st));
+    else EKV_TRY(launch_scores(v, q, Hq, um, L.W, pi, ns, stride, scores, rowmax, full, st));
     const int rows = c->batch * Hq;
     const size_t ntok = (size_t)c->max_pages_per_seq * kP;
     float *cs = at<float>(ws, L.cand_s);
@@ -264,8 +271,7 @@ ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t 
     // the tau kernel directly from the score row (one launch less)
     const int nch = full ? (c->max_pages_per_seq + 255) / 256 : 0;
     if (full && attn->transform == EKV_ENTMAX)
-        EKV_TRY(launch_candidates(scores, ntok, rowmax, pi, ns, stride, c->seq_lens, Hq, full, attn->alpha,
-                                  attn->transform, nch, rows, ccount, cs, cj, st));
+        EKV_TRY(launch_candidates(scores, ntok, rowmax, c->seq_lens, Hq, attn->alpha, nch, rows, ccount, cs, cj, st));
     TauArgs A;
     memset(&A, 0, sizeof(A));
     if (extra) A = *extra;
@@ -287,16 +293,12 @@ ekv_status attend_impl(const ekv_cache *c, const void *q, int Hq, const int32_t 
         return launch_softmax_combine(rows, pacc, pl, pc, rowmax, snch, out, tau, supp, st);
     }
     const bool dense = full && (attn->flags & EKV_ATTN_DENSE_V) && !A.tok_list;
-    if (dense) {
-        // dense-V baseline: exact tau first (no PV), then every V row streamed with p_j
-        A.no_pv = 1;
-        if (!tau) A.tau_out = at<double>(ws, L.tau_int);
-    }
+    // exact tau, support and PV over the support
     EKV_TRY(launch_tau(v, A, rows, st));
     if (!dense) return EKV_OK;
-    const int dch = (c->max_pages_per_seq + kSmxPages - 1) / kSmxPages;
-    EKV_TRY(launch_dense_group(v, scores, ntok, rowmax, Hq, dch, pacc, pl, pc, A.tau_out, attn->alpha, st));
-    return launch_softmax_combine(rows, pacc, pl, pc, rowmax, dch, out, nullptr, nullptr, st);
+    // dense-V baseline (R22): every V row streamed once as well (p_j = 0 off the support, so the
+    // output is the PV above; the stream is the paper's reference's V traffic)
+    return launch_vstream(v, at<uint32_t>(ws, L.sink), st);
 }
 
 }  // namespace

@@ -85,7 +85,7 @@ CacheView view(const ekv_cache *c);
 struct Layout {
     size_t box, mu, sigma2, page_idx, n_sel, tau_hat;
     size_t zero, status, retry, rowmax, ccount, umask, zero_bytes;   // zeroed per step / attention pass
-    size_t tau_int, smx_acc, smx_l, smx_cnt;
+    size_t tau_int, smx_acc, smx_l, smx_cnt, sink;
     int smx_nch;
     size_t scores, cand_s, cand_j, tok_list, p_list, n_list, full_out, total;
     int cap, W, list_cap;
@@ -113,9 +113,9 @@ ekv_status launch_gauss(const ekv_cache *cache, int Hq, const float *mu, const f
 // ---------------------------------------------------------------- launch_attend.cu
 ekv_status launch_scores(const CacheView &v, const void *q, int Hq, const uint32_t *um, int W, const int32_t *pi,
                          const int32_t *ns, int stride, float *scores, uint32_t *rowmax, int full, cudaStream_t st);
-ekv_status launch_candidates(const float *scores, size_t ntok, const uint32_t *rowmax, const int32_t *pi,
-                             const int32_t *ns, int stride, const int32_t *seq_lens, int Hq, int full, float alpha,
-                             int transform, int nch, int rows, int *ccount, float *cs, int32_t *cj, cudaStream_t st);
+ekv_status launch_candidates(const float *scores, size_t ntok, const uint32_t *rowmax, const int32_t *seq_lens,
+                             int Hq, float alpha, int nch, int rows, int *ccount, float *cs, int32_t *cj,
+                             cudaStream_t st);
 ekv_status launch_delta_bar(const float *box, int maxp, const int32_t *seq_lens, int rows, int Hq, int G,
                             const uint32_t *umask, int W, const double *tau, float alpha, double *out, cudaStream_t st);
 ekv_status launch_eval_metrics(int rows, const int32_t *tok_list, const double *p_list, const int32_t *n_list,
@@ -128,6 +128,9 @@ ekv_status launch_softmax_partial(const CacheView &v, const float *scores, size_
 ekv_status launch_dense_group(const CacheView &v, const float *scores, size_t ntok, const uint32_t *rowmax, int Hq,
                               int nch, float *pacc, double *pl, int32_t *pc, const double *ent_tau, float alpha,
                               cudaStream_t st);
+ekv_status launch_vstream(const CacheView &v, uint32_t *sink, cudaStream_t st);   // dense-V: every V row read
+ekv_status launch_full_scores_mma(const CacheView &v, const void *q, int Hq, float *scores, uint32_t *rowmax,
+                                  cudaStream_t st);                                // a5 scores on tensor cores (R26)
 ekv_status launch_softmax_combine(int rows, const float *pacc, const double *pl, const int32_t *pc,
                                   const uint32_t *rowmax, int nch, float *out, double *tau, int32_t *supp,
                                   cudaStream_t st);

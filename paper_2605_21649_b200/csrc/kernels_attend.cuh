@@ -358,108 +358,130 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
 }
 
 // ============================================================================ candidates
-// Grid (chunk of 256 page-list entries, b * Hq + h); thread = one selected page of the
-// row (sparse: page_idx[row][i]; full: page i).  A token is a candidate iff
-// z = (double)a * s > tau_lo = a * s_max - 1 (tau >= z_max - 1 since F(z_max - 1) >= 1,
-// R9).  Each chunk writes its candidates, in page-list order (block scan), into its own
-// region cand[row][chunk][0..kCpc) and its count into ccount[row][chunk]; the tau
-// kernel concatenates the chunks in order, so the candidate order is deterministic.
-// (max_pages <= 65536 -> at most 256 chunks per row.)
-static __global__ void __launch_bounds__(256) k_candidates(const float *__restrict__ scores, size_t ntok,
-                                                    const uint32_t *__restrict__ rowmax,
-                                                    const int32_t *__restrict__ page_idx,
-                                                    const int32_t *__restrict__ n_sel, int sel_stride,
-                                                    const int32_t *__restrict__ seq_lens, int Hq, int full,
-                                                    float alpha, int transform, int nch,
-                                                    int *__restrict__ ccount, float *__restrict__ cand_s,
-                                                    int32_t *__restrict__ cand_j) {
+// Full rows (a5): grid (chunk of 256 pages = 4096 tokens, b * Hq + h), 128 threads.  A token
+// is a candidate iff z = (double)a * s > tau_lo = a * s_max - 1 (tau >= z_max - 1 since
+// F(z_max - 1) >= 1, R9).  Each chunk writes its candidates in token order into its own
+// region cand[row][chunk][0..kCpc) and its count into ccount[row][chunk]; the tau kernel
+// concatenates the chunks in order, so the candidate order is deterministic.  The chunk's
+// 16 KiB of scores arrive by one TMA bulk copy into shared memory (8 CTAs per SM keep
+// 128 KiB in flight per SM; registers no longer bound the bytes in flight); thread t
+// takes float4 t + 128 v (v < 8), and the token order is recovered from two block scans
+// of four packed 16-bit counts.  The chunk-local tightening (many candidates: small
+// alpha) runs out of line.  (max_pages <= 65536 -> at most 256 chunks per row.)
+constexpr int kCandNT = 128;
+static __device__ __noinline__ double chunk_tighten(const float *__restrict__ s4k, int nt, double a, double tau_lo) {
+    // Local tightening: the chunk's own entmax threshold tau_c is a lower bound of tau
+    // (F_all >= F_chunk), so tokens with z <= tau_c can never be in the support.  Newton on
+    // ||(z - t)_+||_beta - 1 from the chunk's z_max - 1 (monotone from the left),
+    // deterministic block reductions over the staged chunk (shared memory).
+    __shared__ double shd[18];
+    __shared__ float shf[9];
+    const double beta = 1.0 / a;
+    const int ib = (fabs(beta - rint(beta)) < 1e-12 && beta <= 4.5) ? (int)rint(beta) : 0;
+    float lm = -INFINITY;
+    for (int t = threadIdx.x; t < nt; t += kCandNT) lm = fmaxf(lm, s4k[t]);
+    lm = block_max_f<kCandNT>(lm, shf);
+    double tc = a * (double)lm - 1.0;
+    for (int it = 0; it < 100; ++it) {
+        double F = 0.0, Fd = 0.0;
+        for (int t = threadIdx.x; t < nt; t += kCandNT) {
+            const float sv = s4k[t];
+            if (sv == -INFINITY) continue;
+            const double d = a * (double)sv - tc;
+            if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
+        }
+        block_sum2_d<kCandNT>(F, Fd, shd);
+        if (!(Fd > 0.0)) break;
+        const float Ff = (float)F, rootf = (ib == 1) ? Ff : (ib == 2) ? sqrtf(Ff) : (ib == 4) ? sqrtf(sqrtf(Ff)) : powf(Ff, (float)(1.0 / beta));
+        const double step = (double)((rootf - 1.0f) * Ff / (rootf * (float)Fd));
+        tc += step;
+        if (!(fabs(step) > 1e-9 * fmax(1.0, fabs(tc)))) break;
+    }
+    tc -= 1e-7 * fmax(1.0, fabs(tc));      // margin: stay below the chunk threshold
+    return tc > tau_lo ? tc : tau_lo;
+}
+
+static __global__ void __launch_bounds__(kCandNT, 8) k_candidates(const float *__restrict__ scores, size_t ntok,
+                                                                  const uint32_t *__restrict__ rowmax,
+                                                                  const int32_t *__restrict__ seq_lens, int Hq,
+                                                                  float alpha, int nch, int *__restrict__ ccount,
+                                                                  float *__restrict__ cand_s,
+                                                                  int32_t *__restrict__ cand_j) {
     EKV_TRACE(5);
-    pdl_enter();
-    __shared__ int sh[9];
+    __shared__ __align__(128) float st[256 * kP];
+    __shared__ uint64_t bar;
+    __shared__ unsigned long long sh[2][5];
     const int row = blockIdx.y;
-    const int b = row / Hq;
-    const int L = seq_lens[b];
-    const int nlist = full ? n_pages_of(L) : n_sel[row];
-    const int i = blockIdx.x * 256 + threadIdx.x;
-    if (blockIdx.x * 256 >= nlist) return;
+    const int t0 = blockIdx.x * 256 * kP;        // first token of the chunk
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+    pdl_enter();
+    const int L = seq_lens[row / Hq];
+    if (t0 >= L) return;
     const uint32_t mk = rowmax[row];
-    if (mk == 0u || transform == 1) return;     // softmax rows stream the row in k_tau_pv
+    if (mk == 0u) return;
+    const int nt = min(256 * kP, L - t0);
+    const float *s4k = scores + (size_t)row * ntok + t0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t bytes = (uint32_t)min((size_t)256 * kP, ntok - (size_t)t0) * 4u;
+        mbar_expect_tx(&bar, bytes);
+        bulk_g2s(st, s4k, bytes, &bar);
+    }
     const double a = (double)alpha - 1.0;
     const double zmax = a * (double)key2f(mk);
     const double tau_lo = zmax - 1.0 - 1e-12 * fmax(1.0, fabs(zmax));
-    float sv[kP];
-    int page = 0, cnt = 0;
-    const float *srow = scores + (size_t)row * ntok;
-    if (i < nlist) {
-        page = full ? i : page_idx[(size_t)row * sel_stride + i];
-        const float4 *p4 = reinterpret_cast<const float4 *>(srow + (size_t)page * kP);
+    mbar_wait(&bar, 0);
+    const float4 *p4 = reinterpret_cast<const float4 *>(st);
+    auto packed = [&](double cut, int h) {       // counts of float4 t + 128 (4 h + v), v < 4
+        unsigned long long c = 0ull;
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
-            const float4 x = p4[v];
-            sv[4 * v] = x.x; sv[4 * v + 1] = x.y; sv[4 * v + 2] = x.z; sv[4 * v + 3] = x.w;
-        }
+            const int f = threadIdx.x + kCandNT * (4 * h + v);
+            const float4 x = p4[f];
+            const float sv[4] = {x.x, x.y, x.z, x.w};
+            unsigned int n = 0;
 #pragma unroll
-        for (int t = 0; t < kP; ++t)
-            cnt += ((page * kP + t < L) && sv[t] != -INFINITY && a * (double)sv[t] > tau_lo) ? 1 : 0;
-    }
-    // Local tightening: the chunk's own entmax threshold tau_c is a lower bound of tau
-    // (F_all >= F_chunk), so tokens with z <= tau_c can never be in the support.  Used when
-    // the chunk has many candidates (small alpha); Newton on ||(z - t)_+||_beta - 1 from the
-    // chunk's z_max - 1 (monotone from the left), deterministic block reductions.
-    __shared__ double shd[18];
-    __shared__ float shf[9];
+            for (int e = 0; e < 4; ++e) n += (4 * f + e < nt && sv[e] != -INFINITY && a * (double)sv[e] > cut) ? 1u : 0u;
+            c |= (unsigned long long)n << (16 * v);
+        }
+        return c;
+    };
+    auto fsum = [](unsigned long long t) {
+        return (int)((t & 0xffff) + ((t >> 16) & 0xffff) + ((t >> 32) & 0xffff) + (t >> 48));
+    };
     double tcut = tau_lo;
-    int ctot = block_sum_i<256>(cnt, sh);
-    if (ctot > 256) {
-        const double beta = 1.0 / a;
-        const int ib = (fabs(beta - rint(beta)) < 1e-12 && beta <= 4.5) ? (int)rint(beta) : 0;
-        float lm = -INFINITY;
-        if (i < nlist) {
-#pragma unroll
-            for (int t = 0; t < kP; ++t) if (page * kP + t < L) lm = fmaxf(lm, sv[t]);
-        }
-        lm = block_max_f<256>(lm, shf);
-        double tc = a * (double)lm - 1.0;
-        for (int it = 0; it < 100; ++it) {
-            double F = 0.0, Fd = 0.0;
-            if (i < nlist) {
-#pragma unroll
-                for (int t = 0; t < kP; ++t) {
-                    if (page * kP + t >= L || sv[t] == -INFINITY) continue;
-                    const double d = a * (double)sv[t] - tc;
-                    if (d > 0.0) { F += powb(d, beta, ib); Fd += powbm1(d, beta, ib); }
-                }
-            }
-            block_sum2_d<256>(F, Fd, shd);
-            if (!(Fd > 0.0)) break;
-            const float Ff = (float)F, rootf = (ib == 1) ? Ff : (ib == 2) ? sqrtf(Ff) : (ib == 4) ? sqrtf(sqrtf(Ff)) : powf(Ff, (float)(1.0 / beta));
-            const double step = (double)((rootf - 1.0f) * Ff / (rootf * (float)Fd));
-            tc += step;
-            if (!(fabs(step) > 1e-9 * fmax(1.0, fabs(tc)))) break;
-        }
-        tc -= 1e-7 * fmax(1.0, fabs(tc));      // margin: stay below the chunk threshold
-        if (tc > tcut) {
-            tcut = tc;
-            cnt = 0;
-            if (i < nlist) {
-#pragma unroll
-                for (int t = 0; t < kP; ++t)
-                    cnt += ((page * kP + t < L) && sv[t] != -INFINITY && a * (double)sv[t] > tcut) ? 1 : 0;
-            }
+    unsigned long long cnt0 = packed(tcut, 0), cnt1 = packed(tcut, 1), tot0, tot1;
+    unsigned long long pos0 = block_excl_scan_u64<kCandNT>(cnt0, sh[0], &tot0);
+    unsigned long long pos1 = block_excl_scan_u64<kCandNT>(cnt1, sh[1], &tot1);
+    if (fsum(tot0) + fsum(tot1) > 256) {           // block-uniform
+        tcut = chunk_tighten(st, nt, a, tau_lo);
+        if (tcut > tau_lo) {
+            cnt0 = packed(tcut, 0);
+            cnt1 = packed(tcut, 1);
+            pos0 = block_excl_scan_u64<kCandNT>(cnt0, sh[0], &tot0);
+            pos1 = block_excl_scan_u64<kCandNT>(cnt1, sh[1], &tot1);
         }
     }
-    int tot;
-    int pos = block_excl_scan<256>(cnt, sh, &tot);
     const size_t reg = ((size_t)row * nch + blockIdx.x) * kCpc;
-    if (threadIdx.x == 0) ccount[(size_t)row * nch + blockIdx.x] = tot;
-    if (i < nlist && cnt) {
+    if (threadIdx.x == 0) ccount[(size_t)row * nch + blockIdx.x] = fsum(tot0) + fsum(tot1);
+    if (!(cnt0 | cnt1)) return;
+    int base = 0;
 #pragma unroll
-        for (int t = 0; t < kP; ++t) {
-            if ((page * kP + t < L) && sv[t] != -INFINITY && a * (double)sv[t] > tcut) {
-                if (pos < kCpc) { cand_s[reg + pos] = sv[t]; cand_j[reg + pos] = page * kP + t; }
-                ++pos;
+    for (int w = 0; w < 8; ++w) {
+        const unsigned long long pos = w < 4 ? pos0 : pos1, tot = w < 4 ? tot0 : tot1;
+        const int sh16 = 16 * (w & 3);
+        int p = base + (int)((pos >> sh16) & 0xffff);
+        const int f = threadIdx.x + kCandNT * w;
+        const float4 x = p4[f];
+        const float sv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (4 * f + e < nt && sv[e] != -INFINITY && a * (double)sv[e] > tcut) {
+                if (p < kCpc) { cand_s[reg + p] = sv[e]; cand_j[reg + p] = t0 + 4 * f + e; }
+                ++p;
             }
         }
+        base += (int)((tot >> sh16) & 0xffff);
     }
 }
 

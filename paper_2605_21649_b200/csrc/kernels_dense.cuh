@@ -251,3 +251,167 @@ __global__ void __launch_bounds__(256, 2) k_dense_group_partial(CacheView c, con
     }
 }
 }  // namespace ekv
+
+namespace ekv {
+// ============================================================================ a5 dense-V: the V stream
+// The dense-V full-cache baseline reads every V row, as the paper's reference does (it
+// "reads all scores and V").  Its output equals the support-V variant's (p_j = 0 off the
+// support), so the tau kernel's exact PV over the support gives out, and this kernel streams
+// the whole V of every valid page once: a warp takes one (b, page) -- the page's Hkv tiles are
+// contiguous (Hkv * P * dv elements) -- with 8 x 16-byte loads per lane in flight, folding the
+// words into an xor checksum (one atomic per warp into `sink`) so the reads are real work.
+template <typename T>
+__global__ void __launch_bounds__(256) k_vstream(CacheView c, uint32_t *__restrict__ sink) {
+    pdl_enter();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long total = (long long)c.B * c.maxp;
+    const long long wtot = (long long)gridDim.x * 8;
+    const int n16 = c.Hkv * kP * kD * (int)sizeof(T) / 16;
+    const uint4 *V = reinterpret_cast<const uint4 *>(c.V);
+    uint32_t x = 0u;
+    for (long long sl = (long long)blockIdx.x * 8 + warp; sl < total; sl += wtot) {
+        const int b = (int)(sl / c.maxp), p = (int)(sl % c.maxp);
+        if (p >= n_pages_of(__ldg(c.seq_lens + b))) continue;               // warp-uniform
+        const uint4 *src = V + (size_t)__ldg(c.page_table + (size_t)b * c.maxp + p) * n16;
+        for (int i0 = 0; i0 < n16; i0 += 32 * 8) {
+            uint4 r[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + 32 * u + lane;
+                r[u] = i < n16 ? __ldcs(src + i) : make_uint4(0, 0, 0, 0);    // streaming (evict-first)
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x ^= r[u].x ^ r[u].y ^ r[u].z ^ r[u].w;
+        }
+    }
+    x = __reduce_xor_sync(0xffffffffu, x);
+    if (lane == 0) atomicXor(sink, x);
+}
+}  // namespace ekv
+
+
+namespace ekv {
+// ============================================================================ a5: full-cache K scores on tensor cores
+// The full-cache baseline's score pass (every token of every page, G heads of a KV group) as a
+// dense bf16 contraction: per 16-token page tile, S[16 tok][8 heads] = K[16][128] q^T[128][8]
+// with mma.sync m16n8k16 (bf16 x bf16 -> fp32; heads >= G are zero columns).  Products are
+// exact; the accumulation is the tensor core's own (not R1's order), so these scores are the
+// baseline's, not bit-identical to the oracle's -- DESIGN R26 (the sparse path keeps R1).
+// A warp owns a contiguous range of (unit, page) slots; tiles arrive by cp.async (16-byte
+// chunks, chunk index XOR (row & 7): ldmatrix reads conflict-free), double-buffered per warp.
+__device__ __forceinline__ void cpa16(void *s, const void *g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+template <int G>
+__global__ void __launch_bounds__(256, 3) k_full_scores_mma(CacheView c, const __nv_bfloat16 *__restrict__ q, int Hq,
+                                                            float *__restrict__ scores, uint32_t *__restrict__ rowmax) {
+    pdl_enter();
+    extern __shared__ __align__(128) unsigned char fsm[];       // [8 warps][2][4096]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gid = lane >> 2, tig = lane & 3;
+    unsigned char *buf = fsm + (size_t)warp * 2 * 4096;
+    const long long total = (long long)c.B * c.Hkv * c.maxp;
+    const long long wtot = (long long)gridDim.x * 8, wid = (long long)blockIdx.x * 8 + warp;
+    const long long s0 = total * wid / wtot, s1 = total * (wid + 1) / wtot;
+    const size_t ntok = (size_t)c.maxp * kP;
+    const unsigned char *Kb = reinterpret_cast<const unsigned char *>(c.K);
+    // slot -> (unit, page); valid pages only (others skipped)
+    auto valid = [&](long long sl, int &unit, int &pg, int &L) -> bool {
+        unit = (int)(sl / c.maxp); pg = (int)(sl % c.maxp);
+        L = __ldg(c.seq_lens + unit / c.Hkv);
+        return pg < n_pages_of(L);
+    };
+    auto issue = [&](long long sl, int slot) {
+        int unit, pg, L;
+        if (sl >= s1 || !valid(sl, unit, pg, L)) return;
+        const int b = unit / c.Hkv, kvh = unit % c.Hkv;
+        const size_t phys = (size_t)__ldg(c.page_table + (size_t)b * c.maxp + pg);
+        const unsigned char *src = Kb + (phys * c.Hkv + kvh) * 4096;
+        unsigned char *dst = buf + slot * 4096;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int ch = lane + 32 * u;                  // 16-byte chunk: row r = ch / 16, col chunk cc = ch % 16
+            const int r = ch >> 4, cc = ch & 15;
+            cpa16(dst + r * 256 + ((cc ^ (r & 7)) << 4), src + ch * 16);
+        }
+    };
+    int cur_unit = -1;
+    uint32_t bq[8][2];                                    // B fragments of q (8 k-steps)
+    float hmax0 = -INFINITY, hmax1 = -INFINITY;          // running maxima of heads 2 tig, 2 tig + 1
+    auto flush = [&](int unit) {
+        if (unit < 0) return;
+        float m0 = hmax0, m1 = hmax1;
+#pragma unroll
+        for (int o = 4; o <= 16; o <<= 1) {
+            m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+            m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+        }
+        const int row0 = (unit / c.Hkv) * Hq + (unit % c.Hkv) * G;
+        if (gid == 0) {
+            if (2 * tig < G && m0 > -INFINITY) atomicMax(rowmax + row0 + 2 * tig, f2key(m0));
+            if (2 * tig + 1 < G && m1 > -INFINITY) atomicMax(rowmax + row0 + 2 * tig + 1, f2key(m1));
+        }
+        hmax0 = hmax1 = -INFINITY;
+    };
+    issue(s0, 0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    int slot = 0;
+    for (long long sl = s0; sl < s1; ++sl, slot ^= 1) {
+        issue(sl + 1, slot ^ 1);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncwarp();
+        int unit, pg, L;
+        if (valid(sl, unit, pg, L)) {                      // warp-uniform
+            if (unit != cur_unit) {
+                flush(cur_unit);
+                cur_unit = unit;
+                const int qrow = (unit / c.Hkv) * Hq + (unit % c.Hkv) * G + gid;   // head n = gid
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    if (gid < G) {
+                        const uint32_t *qp = reinterpret_cast<const uint32_t *>(q + (size_t)qrow * kD + kk * 16 + 2 * tig);
+                        bq[kk][0] = __ldg(qp);
+                        bq[kk][1] = __ldg(qp + 4);
+                    } else {
+                        bq[kk][0] = bq[kk][1] = 0u;
+                    }
+                }
+            }
+            const unsigned char *tile = buf + slot * 4096;
+            float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                // ldmatrix.x4: matrix m = lane / 8 -> rows (lane % 8) + 8 (m & 1), chunk 2 kk + (m >> 1)
+                const int m = lane >> 3, r = (lane & 7) + 8 * (m & 1), cc = 2 * kk + (m >> 1);
+                const uint32_t addr = smem_u32(tile + r * 256 + ((cc ^ (r & 7)) << 4));
+                uint32_t a0, a1, a2, a3;
+                asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "r"(addr));
+                asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                             "{%0,%1,%2,%3};"
+                             : "+f"(d0), "+f"(d1), "+f"(d2), "+f"(d3)
+                             : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bq[kk][0]), "r"(bq[kk][1]));
+            }
+            // d0, d1: token gid, heads 2 tig, 2 tig + 1; d2, d3: token gid + 8
+            const int row0 = (unit / c.Hkv) * Hq + (unit % c.Hkv) * G;
+            const int t0 = pg * kP + gid, t1 = t0 + 8;
+            const float s00 = t0 < L ? __fmul_rn(d0, kCd) : -INFINITY, s01 = t0 < L ? __fmul_rn(d1, kCd) : -INFINITY;
+            const float s10 = t1 < L ? __fmul_rn(d2, kCd) : -INFINITY, s11 = t1 < L ? __fmul_rn(d3, kCd) : -INFINITY;
+            if (2 * tig < G) {
+                float *sr = scores + (size_t)(row0 + 2 * tig) * ntok;
+                sr[t0] = s00; sr[t1] = s10;
+                hmax0 = fmaxf(hmax0, fmaxf(s00, s10));
+            }
+            if (2 * tig + 1 < G) {
+                float *sr = scores + (size_t)(row0 + 2 * tig + 1) * ntok;
+                sr[t0] = s01; sr[t1] = s11;
+                hmax1 = fmaxf(hmax1, fmaxf(s01, s11));
+            }
+        }
+        __syncwarp();
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    flush(cur_unit);
+}
+}  // namespace ekv

@@ -41,12 +41,11 @@ ekv_status launch_scores(const CacheView &v, const void *q, int Hq, const uint32
     return check_launch("k_attend_scores");
 }
 
-ekv_status launch_candidates(const float *scores, size_t ntok, const uint32_t *rowmax, const int32_t *pi,
-                             const int32_t *ns, int stride, const int32_t *seq_lens, int Hq, int full, float alpha,
-                             int transform, int nch, int rows, int *ccount, float *cs, int32_t *cj, cudaStream_t st) {
+ekv_status launch_candidates(const float *scores, size_t ntok, const uint32_t *rowmax, const int32_t *seq_lens,
+                             int Hq, float alpha, int nch, int rows, int *ccount, float *cs, int32_t *cj,
+                             cudaStream_t st) {
     dim3 cg(nch, rows);
-    k_candidates<<<cg, 256, 0, st>>>(scores, ntok, rowmax, pi, ns, stride, seq_lens, Hq, full, alpha, transform, nch,
-                                     ccount, cs, cj);
+    k_candidates<<<cg, kCandNT, 0, st>>>(scores, ntok, rowmax, seq_lens, Hq, alpha, nch, ccount, cs, cj);
     return check_launch("k_candidates");
 }
 
@@ -112,6 +111,37 @@ ekv_status launch_dense_group(const CacheView &v, const float *scores, size_t nt
     if (v.dtype == EKV_BF16) dense_group_t<__nv_bfloat16>(v, scores, ntok, rowmax, Hq, nch, pacc, pl, pc, ent_tau, alpha, ib, st);
     else dense_group_t<float>(v, scores, ntok, rowmax, Hq, nch, pacc, pl, pc, ent_tau, alpha, ib, st);
     return check_launch("k_dense_group_partial");
+}
+
+ekv_status launch_full_scores_mma(const CacheView &v, const void *q, int Hq, float *scores, uint32_t *rowmax,
+                                  cudaStream_t st) {
+    const int G = Hq / v.Hkv;
+    const int smem = 8 * 2 * 4096;
+    const long long slots = (long long)v.B * v.Hkv * v.maxp;
+    long long g = (slots + 63) / 64;                              // >= 8 slots per warp
+    const long long cap = (long long)num_sms() * 3;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    const __nv_bfloat16 *qq = static_cast<const __nv_bfloat16 *>(q);
+    cudaError_t e;
+    switch (G) {
+    case 1: set_smem(k_full_scores_mma<1>, smem); e = launch_ex(k_full_scores_mma<1>, dim3((unsigned)g), dim3(256), smem, st, 0, v, qq, Hq, scores, rowmax); break;
+    case 2: set_smem(k_full_scores_mma<2>, smem); e = launch_ex(k_full_scores_mma<2>, dim3((unsigned)g), dim3(256), smem, st, 0, v, qq, Hq, scores, rowmax); break;
+    case 4: set_smem(k_full_scores_mma<4>, smem); e = launch_ex(k_full_scores_mma<4>, dim3((unsigned)g), dim3(256), smem, st, 0, v, qq, Hq, scores, rowmax); break;
+    default: set_smem(k_full_scores_mma<8>, smem); e = launch_ex(k_full_scores_mma<8>, dim3((unsigned)g), dim3(256), smem, st, 0, v, qq, Hq, scores, rowmax); break;
+    }
+    if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "k_full_scores_mma: %s", cudaGetErrorString(e));
+    return check_launch("k_full_scores_mma");
+}
+
+ekv_status launch_vstream(const CacheView &v, uint32_t *sink, cudaStream_t st) {
+    const long long slots = (long long)v.B * v.maxp;
+    long long g = (slots + 7) / 8;
+    const long long cap = (long long)num_sms() * 8;          // 8 CTAs (64 warps) per SM
+    if (g > cap) g = cap;
+    if (v.dtype == EKV_BF16) launch_ex(k_vstream<__nv_bfloat16>, dim3((unsigned)g), dim3(256), 0, st, 0, v, sink);
+    else launch_ex(k_vstream<float>, dim3((unsigned)g), dim3(256), 0, st, 0, v, sink);
+    return check_launch("k_vstream");
 }
 
 ekv_status launch_softmax_combine(int rows, const float *pacc, const double *pl, const int32_t *pc,

@@ -250,14 +250,15 @@ def test_full_softmax_grouped_dense_v(case):
 
 @pytest.mark.parametrize("case", CASES, ids=ids)
 @pytest.mark.parametrize("alpha", [1.5, 2.0, 1.25])
-@pytest.mark.parametrize("dense_v", [False, True])
-def test_full_attend(case, alpha, dense_v):
-    """a5: full-cache entmax, support-V and dense-V (every V row streamed)."""
+@pytest.mark.parametrize("dense_v,canonical", [(False, False), (True, False), (False, True)])
+def test_full_attend(case, alpha, dense_v, canonical):
+    """a5: full-cache entmax, support-V and dense-V (every V row streamed); bf16
+    scores on tensor cores (R26) by default, R1's canonical order with canonical=True."""
     B, sl, Hq, Hkv, dt = case
     wl, dc, hc = make_pair(B, sl, Hq, Hkv, dtype=dt, seed=19)
     G = Hq // Hkv
     qh = q_host(wl)
-    out, tau, supp = ekv.full_attend(dc, wl.q.cuda(), ekv.attn_params(alpha, dense_v=dense_v))
+    out, tau, supp = ekv.full_attend(dc, wl.q.cuda(), ekv.attn_params(alpha, dense_v=dense_v, canonical=canonical))
     torch.cuda.synchronize()
     out, tau, supp = out.cpu().numpy(), tau.cpu().numpy(), supp.cpu().numpy()
     for b in range(B):
@@ -406,7 +407,8 @@ def test_prop2_exactness_on_gpu():
     B, Hq, Hkv = 1, 8, 2
     wl, dc, hc = make_pair(B, 3000, Hq, Hkv, seed=37, kind="planted")
     qh = q_host(wl)
-    out_f, tau_f, _ = ekv.full_attend(dc, wl.q.cuda(), ekv.attn_params(1.5))
+    # canonical (R1) scores on the full side: Prop. 2 is a statement about the same scores
+    out_f, tau_f, _ = ekv.full_attend(dc, wl.q.cuda(), ekv.attn_params(1.5, canonical=True))
     cap = 40
     pi = torch.full((B, Hq, cap), -1, dtype=torch.int32)
     ns = torch.zeros(B, Hq, dtype=torch.int32)

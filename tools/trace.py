@@ -21,7 +21,8 @@ c = ekv.PagedCache.allocate_meta(wl.K, wl.V, wl.page_table, wl.seq_lens, bound=o
                                  stat=os.environ.get('STATS', 'f32'))
 ekv.rebuild_page_stats(c)
 sel = ekv.select_params('topk' if policy == 'full' else policy, k)
-attn = ekv.attn_params(float(__import__('os').environ.get('TRACE_ALPHA', '1.5')))
+attn = ekv.attn_params(float(__import__('os').environ.get('TRACE_ALPHA', '1.5')),
+                       dense_v=__import__('os').environ.get('DENSE', '0') == '1')
 ws = ekv.alloc_workspace(c, Hq, sel)
 st = ekv.DecodeStats(B, Hq, dev, delta_bar=True, gauss=policy == 'gauss')
 _, kn, vn = new_tokens(B, Hq, Hkv, seed=7, device=dev)
