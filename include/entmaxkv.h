@@ -282,7 +282,28 @@ typedef struct {
      * read per round).  R > 0: exactly R rounds with no host read -- the step is then CUDA-graph
      * capturable if the callbacks are (NCCL on the same stream is); R >= 12 always converges (R20). */
     int32_t fixed_rounds;
+    /* In-kernel collectives: when peers[0] != NULL the step exchanges its data
+     * inside its own kernels over peer memory and the callbacks / fixed_rounds are ignored.
+     * peers[q] (q < world <= 8) = rank q's exchange buffer as mapped in this process: device
+     * memory of entmaxkv_peer_buffer_size() bytes per rank, ZEROED once before the first step,
+     * reachable from this device (CUDA IPC with peer access over NVLink / NVSwitch across GPUs;
+     * plain device pointers for virtual ranks sharing one GPU).  Each exchange: every rank stores
+     * its payload into every rank's buffer and raises a flag there (release, system scope); a
+     * rank waits on its own buffer's flags (acquire) and reduces the W payloads in rank order, so
+     * every rank computes identical bits and the multisection rounds stop on every rank at the
+     * same round with no host read.  The top-k lists, z_max, the round partials, the power sums
+     * and numerator / denominator all go this way (2 + rounds + 2 exchanges per row and step).
+     * The step is then CUDA-graph capturable (the exchange counters live in the buffers).  All
+     * ranks' steps must run concurrently; a flag missing for ~2 s marks the row failed
+     * (EKV_STATUS_TIMEOUT: NaN out/tau, supp -1) instead of hanging, after which the buffers
+     * must be re-zeroed on every rank.  The buffer memory stays owned by the caller. */
+    void *peers[8];
 } ekv_comm;
+
+/* Bytes of one rank's exchange buffer for the in-kernel collective mode (ekv_comm.peers);
+ * 0 on invalid arguments (world must be 1..8). */
+size_t entmaxkv_peer_buffer_size(const ekv_cache *local, int32_t n_q_heads, const ekv_select_params *sel,
+                                 int32_t world);
 
 /* Workspace bytes for entmaxkv_decode_sharded on this local cache shape. */
 size_t entmaxkv_shard_workspace_size(const ekv_cache *local, int32_t n_q_heads, const ekv_select_params *sel,
@@ -320,11 +341,13 @@ ekv_status entmaxkv_decode_sharded(const ekv_cache *local, const int32_t *global
  * some row's candidate set exceeded a kernel capacity -- the exact support did not fit the tau
  * kernel's shared-memory list (more than ~10k support tokens) or, sequence-sharded, more than
  * 8192 candidates per row and rank; such rows get out = NaN, tau = NaN, supp_count = -1.
+ * Bit 1 (EKV_STATUS_TIMEOUT): in-kernel collectives (ekv_comm.peers) -- a peer's exchange did
+ * not arrive within ~2 s; those rows are NaN and the exchange buffers must be re-zeroed.
  * Copies the word to *flags, synchronising `stream` (the one call that does), and returns
- * EKV_ERR_CAPACITY when bit 0 is set, else EKV_OK.  cache / n_q_heads / sel as for
+ * EKV_ERR_COMM when bit 1 is set, else EKV_ERR_CAPACITY when bit 0 is set, else EKV_OK.  cache / n_q_heads / sel as for
  * entmaxkv_workspace_size.
  */
-enum { EKV_STATUS_CAPACITY = 1 };
+enum { EKV_STATUS_CAPACITY = 1, EKV_STATUS_TIMEOUT = 2 };
 ekv_status entmaxkv_workspace_status(const ekv_cache *cache, int32_t n_q_heads, const ekv_select_params *sel,
                                      const void *workspace, int32_t *flags, void *stream);
 

@@ -27,7 +27,7 @@ EXPORTED = [
     "entmaxkv_workspace_status",
     "entmaxkv_append_kv", "entmaxkv_rebuild_page_stats", "entmaxkv_score_pages", "entmaxkv_select",
     "entmaxkv_sparse_attend", "entmaxkv_full_attend", "entmaxkv_decode", "entmaxkv_last_launch_count",
-    "entmaxkv_shard_workspace_size", "entmaxkv_decode_sharded",
+    "entmaxkv_shard_workspace_size", "entmaxkv_decode_sharded", "entmaxkv_peer_buffer_size",
 ]
 
 
@@ -81,7 +81,8 @@ ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p
 
 class ekv_comm(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("allreduce", ALLREDUCE_FN),
-                ("allgather", ALLGATHER_FN), ("user", ctypes.c_void_p), ("fixed_rounds", ctypes.c_int32)]
+                ("allgather", ALLGATHER_FN), ("user", ctypes.c_void_p), ("fixed_rounds", ctypes.c_int32),
+                ("peers", ctypes.c_void_p * 8)]
 
 
 _lib = None
@@ -116,6 +117,8 @@ def lib():
         L.entmaxkv_workspace_status.restype = ctypes.c_int
         L.entmaxkv_shard_workspace_size.argtypes = [P(ekv_cache), i32, P(ekv_select_params), i32]
         L.entmaxkv_shard_workspace_size.restype = ctypes.c_size_t
+        L.entmaxkv_peer_buffer_size.argtypes = [P(ekv_cache), i32, P(ekv_select_params), i32]
+        L.entmaxkv_peer_buffer_size.restype = ctypes.c_size_t
         L.entmaxkv_decode_sharded.argtypes = [P(ekv_cache), vp, vp, i32, P(ekv_select_params), P(ekv_attn_params),
                                               P(ekv_comm), vp, P(ekv_decode_stats), vp, vp]
         for name in ("entmaxkv_decode_sharded", "entmaxkv_append_kv", "entmaxkv_rebuild_page_stats", "entmaxkv_score_pages", "entmaxkv_select",
@@ -246,6 +249,7 @@ def workspace_status(cache: PagedCache, n_q_heads, sel, workspace, stream=None, 
 
 
 EKV_STATUS_CAPACITY = 1
+EKV_STATUS_TIMEOUT = 2
 
 
 def select_capacity(cache: PagedCache, sel: ekv_select_params) -> int:
@@ -400,17 +404,27 @@ def shard_workspace(cache: PagedCache, n_q_heads, sel: ekv_select_params, world:
     return torch.empty(int(n), dtype=torch.uint8, device=cache.K.device)
 
 
+def peer_buffer_size(cache: PagedCache, n_q_heads, sel: ekv_select_params, world: int) -> int:
+    n = lib().entmaxkv_peer_buffer_size(ctypes.byref(cache.c_struct()), int(n_q_heads), ctypes.byref(sel), int(world))
+    if n == 0:
+        raise EkvError(EKV_ERR_INVALID_ARG, lib().entmaxkv_last_error().decode())
+    return int(n)
+
+
 def decode_sharded(cache: PagedCache, global_seq_lens, q, sel: ekv_select_params, attn: ekv_attn_params, comm,
                    workspace, out=None, stats: DecodeStats | None = None, stream=None, fixed_rounds=0):
     """One sequence-sharded decode step on this rank's local cache (include/entmaxkv.h).
-    `comm` provides rank, world and the collectives (see paper_2605_21649_b200.sharding); the
-    library calls them back between its kernels.  Returns out [B][Hq][dv] fp32 (replicated)."""
+    `comm` provides rank, world and either the collectives (callback mode: the library calls
+    them back between its kernels) or `peers`, the W exchange-buffer pointers of the in-kernel
+    collective mode (see paper_2605_21649_b200.sharding).  Returns out [B][Hq][dv] fp32 (replicated)."""
     B, Hq, _ = q.shape
     if out is None:
         out = torch.empty(B, Hq, cache.V.shape[3], dtype=torch.float32, device=q.device)
     s = stream if stream is not None else torch.cuda.current_stream(q.device)
     comm.bind(workspace, s)
     cm = ekv_comm(int(comm.rank), int(comm.world), comm.c_allreduce, comm.c_allgather, None, int(fixed_rounds))
+    for i, p in enumerate(getattr(comm, "peers", None) or []):
+        cm.peers[i] = int(p)
     cs = cache.c_struct()
     st = stats.c_struct() if stats is not None else None
     try:

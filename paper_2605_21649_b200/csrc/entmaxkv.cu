@@ -396,6 +396,8 @@ ekv_status entmaxkv_workspace_status(const ekv_cache *cache, int32_t n_q_heads, 
                                       cudaMemcpyDeviceToHost, st), "status read"));
     EKV_TRY(check_err(cudaStreamSynchronize(st), "status sync"));
     *flags = (int32_t)f;
+    if (f & kStatusTimeout)
+        return fail(EKV_ERR_COMM, "in-kernel collectives: a peer's exchange did not arrive (rows NaN; re-zero the exchange buffers)");
     if (f & kStatusCapacity)
         return fail(EKV_ERR_CAPACITY, "a row's candidate set exceeded the kernel capacity (its out/tau are NaN, supp -1)");
     return EKV_OK;

@@ -1,5 +1,6 @@
 // shard.cu -- sequence-sharded decode: host orchestration of the
 // kernels_shard.cuh kernels and the caller's collectives.
+#include <algorithm>
 #include <cmath>
 #include "host.h"
 #include "kernels_shard.cuh"
@@ -38,14 +39,77 @@ ShardLayout shard_layout(const ekv_cache *c, int Hq, const ekv_select_params *se
     return S;
 }
 
+// in-kernel collectives (N2): payload bytes per (parity, sender, row) and buffer bytes
+uint32_t peer_pay(int kc) {
+    size_t p = std::max<size_t>({(size_t)8 * kc, (size_t)kShP * 3 * 8, (size_t)kD * 4 + 16, 64});
+    return (uint32_t)((p + 15) & ~(size_t)15);
+}
+size_t peer_bytes(int rows, int world, int kc) {
+    const size_t hdr = ((size_t)8 * rows * (1 + world) + 255) & ~(size_t)255;
+    return hdr + (size_t)2 * world * rows * peer_pay(kc);
+}
+
 ekv_status comm_allreduce(const ekv_comm *cm, void *buf, size_t count, int dtype, int op, cudaStream_t st) {
     if (cm->world <= 1) return EKV_OK;
     if (cm->allreduce(buf, count, dtype, op, cm->user, st) != 0) return fail(EKV_ERR_COMM, "allreduce callback failed");
     return EKV_OK;
 }
+// the step with in-kernel collectives (N2): no callback, no host synchronisation
+ekv_status decode_sharded_dev(const ekv_cache *cache, const CacheView &v, const Layout &L, const ShardLayout &S,
+                              const PeerSet &P, const int32_t *global_seq_lens, const void *q, int Hq,
+                              const ekv_select_params *sel, const ekv_attn_params *attn, int ib, double beta,
+                              float *out, ekv_decode_stats *stats, void *workspace, cudaStream_t st) {
+    const int rows = P.rows, Gq = Hq / cache->n_kv_heads, maxp = cache->max_pages_per_seq;
+    float *box = at<float>(workspace, L.box);
+    int32_t *pi = at<int32_t>(workspace, L.page_idx);
+    int32_t *ns = at<int32_t>(workspace, L.n_sel);
+    uint32_t *um = at<uint32_t>(workspace, L.umask);
+    uint32_t *status = at<uint32_t>(workspace, L.status);
+    // (local box scores and local top-k already enqueued by the caller)
+    k_shard_pack_push<<<rows, 256, 0, st>>>(box, maxp, pi, ns, L.cap, S.kc, P);
+    EKV_TRY(check_launch("k_shard_pack_push"));
+    k_shard_merge<<<rows, kShMergeNT, 0, st>>>(nullptr, nullptr, rows, S.kc, sel->k_pages, P.rk, P.W, global_seq_lens,
+                                               pi, ns, L.cap, Hq, Gq, um, L.W, P, status);
+    EKV_TRY(check_launch("k_shard_merge"));
+    float *scores = at<float>(workspace, L.scores);
+    uint32_t *rowmax = at<uint32_t>(workspace, L.rowmax);
+    EKV_TRY(launch_scores(v, q, Hq, um, L.W, pi, ns, L.cap, scores, rowmax, 0, st));
+    double *cz = at<double>(workspace, S.cz);
+    int32_t *cj = at<int32_t>(workspace, S.cj), *cph = at<int32_t>(workspace, S.cph), *nc = at<int32_t>(workspace, S.ncand);
+    ShardRow *rst = at<ShardRow>(workspace, S.rowst);
+    double *tau = (stats && stats->tau) ? stats->tau : at<double>(workspace, S.tau);
+    int32_t *supp = stats ? stats->supp_count : nullptr;
+    auto solve = [&](auto tag) {
+        using T = decltype(tag);
+#define EKV_DSOLVE(IB) k_shard_dsolve<T, IB><<<rows, 256, 0, st>>>(v, P, scores, (size_t)maxp * kP, pi, ns, L.cap, rowmax, \
+                                                                    Hq, Gq, attn->alpha, beta, cz, cj, cph, nc, rst, tau, \
+                                                                    supp, out, status)
+        switch (ib) {
+        case 1: EKV_DSOLVE(1); break;
+        case 2: EKV_DSOLVE(2); break;
+        case 3: EKV_DSOLVE(3); break;
+        default: EKV_DSOLVE(4); break;
+        }
+#undef EKV_DSOLVE
+    };
+    if (cache->dtype == EKV_BF16) solve(__nv_bfloat16());
+    else solve(0.0f);
+    EKV_TRY(check_launch("k_shard_dsolve"));
+    if (stats && stats->n_sel) {
+        k_shard_nsel<<<(rows + 127) / 128, 128, 0, st>>>(global_seq_lens, Hq, rows, sel->k_pages, stats->n_sel);
+        EKV_TRY(check_launch("k_shard_nsel"));
+    }
+    return EKV_OK;
+}
 }  // namespace
 
 extern "C" {
+
+size_t entmaxkv_peer_buffer_size(const ekv_cache *local, int32_t n_q_heads, const ekv_select_params *sel,
+                                 int32_t world) {
+    if (check_cache(local, n_q_heads) != EKV_OK || world < 1 || world > kMaxPeers) return 0;
+    return peer_bytes(local->batch * n_q_heads, world, sel_cap(local, sel));
+}
 
 size_t entmaxkv_shard_workspace_size(const ekv_cache *local, int32_t n_q_heads, const ekv_select_params *sel,
                                      int32_t world) {
@@ -64,8 +128,15 @@ ekv_status entmaxkv_decode_sharded(const ekv_cache *cache, const int32_t *global
     EKV_TRY(check_sel(sel, attn->alpha));
     if (!q || !out || !workspace || !comm || !global_seq_lens) return fail(EKV_ERR_INVALID_ARG, "NULL argument");
     EKV_TRY(check_q(q));
-    if (comm->world < 1 || comm->rank < 0 || comm->rank >= comm->world || (comm->world > 1 && (!comm->allreduce || !comm->allgather)))
+    const bool dev = comm->peers[0] != nullptr;     // in-kernel collectives (N2)
+    if (comm->world < 1 || comm->rank < 0 || comm->rank >= comm->world ||
+        (!dev && comm->world > 1 && (!comm->allreduce || !comm->allgather)))
         return fail(EKV_ERR_INVALID_ARG, "bad communicator (rank %d, world %d)", comm->rank, comm->world);
+    if (dev) {
+        if (comm->world > kMaxPeers) return fail(EKV_ERR_UNSUPPORTED, "in-kernel collectives: world %d > %d", comm->world, kMaxPeers);
+        for (int q = 0; q < comm->world; ++q)
+            if (!comm->peers[q]) return fail(EKV_ERR_INVALID_ARG, "in-kernel collectives: peers[%d] is NULL", q);
+    }
     if (sel->policy != EKV_TOPK || attn->transform != EKV_ENTMAX)
         return fail(EKV_ERR_UNSUPPORTED, "sharded decode supports top-k selection with entmax");
     const double beta = 1.0 / ((double)attn->alpha - 1.0);
@@ -92,6 +163,14 @@ ekv_status entmaxkv_decode_sharded(const ekv_cache *cache, const int32_t *global
     EKV_TRY(launch_score(v, q, n_q_heads, EKV_SCORE_BOX, box, nullptr, nullptr, nullptr, 0, st));
     EKV_TRY(launch_topk(box, cache->batch, n_q_heads, maxp, cache->seq_lens, sel->k_pages, pi, ns, L.cap, Gq,
                         UnionOut{nullptr, 0}, st));
+    PeerSet P;
+    memset(&P, 0, sizeof(P));
+    if (dev) {
+        for (int q = 0; q < W; ++q) P.buf[q] = static_cast<unsigned char *>(comm->peers[q]);
+        P.W = W; P.rk = rk; P.rows = rows; P.pay = peer_pay(S.kc);
+        return decode_sharded_dev(cache, v, L, S, P, global_seq_lens, q, n_q_heads, sel, attn, ib, beta, out, stats,
+                                  workspace, st);
+    }
     float *ps = at<float>(workspace, S.pack_s), *rs = at<float>(workspace, S.recv_s);
     int32_t *pg = at<int32_t>(workspace, S.pack_g), *rg = at<int32_t>(workspace, S.recv_g);
     k_shard_pack<<<rows, 256, 0, st>>>(box, maxp, pi, ns, L.cap, S.kc, rk, W, ps, pg);
@@ -105,7 +184,7 @@ ekv_status entmaxkv_decode_sharded(const ekv_cache *cache, const int32_t *global
         cudaMemcpyAsync(rg, pg, pbytes, cudaMemcpyDeviceToDevice, st);
     }
     k_shard_merge<<<rows, kShMergeNT, 0, st>>>(rs, rg, rows, S.kc, sel->k_pages, rk, W, global_seq_lens, pi, ns, L.cap,
-                                               n_q_heads, Gq, um, L.W);
+                                               n_q_heads, Gq, um, L.W, P, at<uint32_t>(workspace, L.status));
     EKV_TRY(check_launch("k_shard_merge"));
     // 2. K scores of the local share, global z_max
     float *scores = at<float>(workspace, L.scores);

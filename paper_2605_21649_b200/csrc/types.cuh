@@ -73,6 +73,15 @@ constexpr int kShCap = 8192;        // local candidates per row
 constexpr int kShSums = 5;          // S_0 .. S_4
 constexpr int kShMergeNT = 1024;
 constexpr int kShMergeKPT = 16;     // W * kc <= 16384
+constexpr int kMaxPeers = 8;        // in-kernel collectives (N2): ranks per exchange
+constexpr uint32_t kStatusTimeout = 2u;    // a peer's flag did not arrive in time (row NaN)
+// Rank q's exchange buffer (entmaxkv_peer_buffer_size): [ctr: rows x u64][flag: W x rows x u64]
+// (padded to 256 B) then [data: 2 parities x W senders x rows x pay bytes].
+struct PeerSet {
+    unsigned char *buf[kMaxPeers];   // every rank's exchange buffer, as mapped in this process
+    int W, rk, rows;
+    uint32_t pay;                    // payload bytes per (parity, sender, row), multiple of 16
+};
 struct ShardRow {                   // per-row multisection state (device)
     double lo, hi;                  // F(lo) >= 1 > F(hi)
     double cgt_lo, cge_hi;          // #{z > lo}, #{z >= hi} (global)

@@ -180,3 +180,62 @@ class LoopbackComm(_CommBase):
         vals = self._exchange(send)
         recv.copy_(torch.cat(vals))
         torch.cuda.synchronize()
+
+
+# ----------------------------------------------------------------------------- in-kernel collectives (N2)
+class PeerComm(_CommBase):
+    """Rank `rank` of an in-kernel collective group: `peers` = every rank's exchange buffer
+    (device pointers as mapped in this process).  The library exchanges its partials inside
+    its kernels (include/entmaxkv.h, ekv_comm.peers); no callback is ever made."""
+
+    def __init__(self, rank: int, world: int, peers, keep=None):
+        super().__init__(rank, world)
+        self.peers = [int(p) for p in peers]
+        self._keep = keep          # keeps the buffers (and any IPC mappings) alive
+
+    def all_reduce(self, t, op):   # pragma: no cover - never called in peer mode
+        raise RuntimeError("in-kernel collective mode makes no callbacks")
+
+    all_gather = all_reduce
+
+
+class LocalPeerGroup:
+    """W virtual ranks sharing one GPU (tests): the W exchange buffers are plain zeroed device
+    buffers of this process; each rank's step must run on its own stream so that the ranks'
+    kernels run concurrently."""
+
+    def __init__(self, world: int, nbytes: int, device=None):
+        self.world = world
+        self.bufs = [torch.zeros(int(nbytes), dtype=torch.uint8, device=device or "cuda") for _ in range(world)]
+
+    def comm(self, rank: int) -> PeerComm:
+        return PeerComm(rank, self.world, [b.data_ptr() for b in self.bufs], keep=self.bufs)
+
+    def reset(self):
+        for b in self.bufs:
+            b.zero_()
+
+
+def ipc_peer_comm(nbytes: int, group=None) -> PeerComm:
+    """One rank per process (one GPU each, or several sharing a GPU): allocate this rank's
+    zeroed exchange buffer, share its CUDA IPC handle through torch.distributed (any backend)
+    and open every peer's buffer in this process (peer access over NVLink / NVSwitch is
+    enabled by the IPC mapping).  Collective over `group`."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    buf = torch.zeros(int(nbytes), dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    handle = buf.untyped_storage()._share_cuda_()
+    off = int(handle[3])
+    handles = [None] * world
+    dist.all_gather_object(handles, (handle, off, buf.data_ptr() - buf.untyped_storage().data_ptr()), group=group)
+    keep, peers = [buf], []
+    for r, (h, off_r, view_off) in enumerate(handles):
+        if r == rank:
+            peers.append(buf.data_ptr())
+            continue
+        st = torch.UntypedStorage._new_shared_cuda(*h)
+        keep.append(st)
+        peers.append(st.data_ptr() + view_off)
+    dist.barrier(group=group)
+    return PeerComm(rank, world, peers, keep=keep)

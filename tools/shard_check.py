@@ -29,7 +29,10 @@ cache = sharding.shard_cache(wl.K, wl.V, wl.page_table, wl.seq_lens, rank, world
 sel, attn = ekv.select_params("topk", k), ekv.attn_params(alpha)
 ws = ekv.shard_workspace(cache, Hq, sel, world)
 st = ekv.DecodeStats(1, Hq, dev, delta_bar=False)
-comm = sharding.TorchComm()
+if os.environ.get("EKV_PEER") == "1":        # in-kernel collectives over CUDA IPC buffers (N2)
+    comm = sharding.ipc_peer_comm(ekv.peer_buffer_size(cache, Hq, sel, world))
+else:
+    comm = sharding.TorchComm()
 out = None
 for _ in range(3):
     out = ekv.decode_sharded(cache, wl.seq_lens.to(torch.int32).to(dev), wl.q.to(dev), sel, attn, comm, ws, stats=st)
