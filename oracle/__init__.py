@@ -83,6 +83,8 @@ def lib():
         L.orc_gauss_select.restype = c_int
         L.orc_delta_bar.argtypes = [f32p, i32p, u8p, c_int, c_double, c_double]
         L.orc_delta_bar.restype = c_double
+        L.orc_box_certified.argtypes = [f32p, c_int, c_double, c_double, i32p]
+        L.orc_box_certified.restype = c_int
         L.orc_e4m3_round_down.argtypes = [ctypes.c_float]
         L.orc_e4m3_round_down.restype = ctypes.c_float
         L.orc_e4m3_round_up.argtypes = [ctypes.c_float]
@@ -232,6 +234,15 @@ def gauss_select(mu, sigma2, counts, alpha, tau_hat, margin, zq):
     return out[:n].copy()
 
 
+def box_certified(box, alpha, tau_hat):
+    """Prop. B.2 (P:838-893): pages with (alpha-1) box > tau_hat, ascending."""
+    box = _f32(box)
+    out = np.zeros(max(box.shape[0], 1), np.int32)
+    n = lib().orc_box_certified(_p(box, ctypes.c_float), box.shape[0], float(alpha), float(tau_hat),
+                                _p(out, ctypes.c_int32))
+    return out[:n].copy()
+
+
 def e4m3_round_down(x) -> np.float32:
     return np.float32(lib().orc_e4m3_round_down(float(x)))
 
@@ -360,6 +371,14 @@ def decode_head(cache: HostCache, q, b, kvh, alpha, k_pages=None, policy="topk",
         res["box"] = box
     elif policy == "all":
         pages = np.arange(M, dtype=np.int32)
+    elif policy == "certified":
+        # N4 (Prop. B.2; DESIGN R27): a top-k pass gives the exact sparse threshold
+        # tau~ <= tau (R13); every page with (alpha-1) box > tau~ is then selected
+        box, _, _ = cache.score_pages(q, b, kvh, modes=1)
+        first = cache.attend(q, b, kvh, topk(box, k_pages), alpha, transform)
+        tau_lo = first["tau"]
+        pages = box_certified(box, alpha, tau_lo)
+        res.update(box=box, tau_lo=tau_lo)
     else:
         _, mu, s2 = cache.score_pages(q, b, kvh, modes=2)
         tau_hat = gauss_tau(mu, s2, counts, alpha)

@@ -655,3 +655,18 @@ double orc_delta_bar(const float *box, const int32_t *counts, const uint8_t *sel
     }
     return s;
 }
+
+/* Support-superset (certified conservative) page selection, SURVEY 8(f) N4 --   */
+/* Prop. B.2 "No false negatives from deterministic page bounds":     */
+/* C_page = {p : (alpha-1) * sbar_box(p) > tau_hat}, for any tau_hat <= tau.       */
+/* The decision is taken in fp64 (R9's precision for z): (double)a * box[p].      */
+/* Ascending page ids; returns |C_page|.  DESIGN R27: tau_hat is the exact         */
+/* threshold of a first top-k pass (a lower bound of tau by R13).                  */
+int orc_box_certified(const float *box, int M, double alpha, double tau_hat, int32_t *out)
+{
+    double a = alpha - 1.0;
+    int n = 0;
+    for (int p = 0; p < M; ++p)
+        if (a * (double)box[p] > tau_hat) out[n++] = p;
+    return n;
+}
