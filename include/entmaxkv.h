@@ -44,7 +44,7 @@ typedef enum {
 
 typedef enum { EKV_BF16 = 0, EKV_F32 = 1 } ekv_dtype;
 typedef enum { EKV_ENTMAX = 0, EKV_SOFTMAX = 1 } ekv_transform;     /* P:128-136 / P:121-124 */
-typedef enum { EKV_TOPK = 0, EKV_GAUSS = 1, EKV_ALL = 2 } ekv_policy;
+typedef enum { EKV_TOPK = 0, EKV_GAUSS = 1, EKV_ALL = 2, EKV_CERTIFIED = 3 } ekv_policy;
 enum { EKV_SCORE_BOX = 1, EKV_SCORE_GAUSS = 2 };
 
 /*
@@ -116,6 +116,14 @@ typedef struct {
  *   (Eq. gaussian-selector-main); needs integer beta = 1/(alpha-1) in
  *   {1,2,3,4} (App. D, R15), else EKV_ERR_UNSUPPORTED.
  * policy ALL: every page (the full cache).
+ * policy CERTIFIED (Prop. B.2 "no false negatives from deterministic page
+ *   bounds"): entmaxkv_decode only.  A first top-k pass (k_pages) gives the exact
+ *   sparse threshold tau~, a lower bound of the full-cache tau (DESIGN R13); then every page
+ *   with (alpha-1) * box(p) > tau~ (fp64 decision) is selected and attended.  That selection
+ *   contains every support token's page, so the output IS full-cache entmax (Prop. 2,
+ *   P:213-216) and delta_bar = 0.  stats->tau_hat receives tau~, n_sel the final |C_page|;
+ *   the workspace holds full-length page lists.  With loose box bounds the selection can
+ *   cover most pages (App. C) -- an exactness mode, not a fast one.  Entmax only.
  */
 typedef struct {
     int32_t policy;

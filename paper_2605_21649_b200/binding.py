@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libentmaxkv.so")
 EKV_OK, EKV_ERR_INVALID_ARG, EKV_ERR_UNSUPPORTED, EKV_ERR_CAPACITY, EKV_ERR_EMPTY, EKV_ERR_CUDA, EKV_ERR_COMM = range(7)
 EKV_BF16, EKV_F32 = 0, 1
 EKV_ENTMAX, EKV_SOFTMAX = 0, 1
-EKV_TOPK, EKV_GAUSS, EKV_ALL = 0, 1, 2
+EKV_TOPK, EKV_GAUSS, EKV_ALL, EKV_CERTIFIED = 0, 1, 2, 3
 EKV_SCORE_BOX, EKV_SCORE_GAUSS = 1, 2
 
 EXPORTED = [
@@ -217,7 +217,7 @@ class PagedCache:
 
 
 def select_params(policy="topk", k_pages=64, q_page=0.99, margin=0.0) -> ekv_select_params:
-    pol = {"topk": EKV_TOPK, "gauss": EKV_GAUSS, "all": EKV_ALL}[policy]
+    pol = {"topk": EKV_TOPK, "gauss": EKV_GAUSS, "all": EKV_ALL, "certified": EKV_CERTIFIED}[policy]
     return ekv_select_params(pol, int(k_pages), float(q_page), float(margin))
 
 

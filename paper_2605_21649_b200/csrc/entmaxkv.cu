@@ -164,6 +164,8 @@ ekv_status check_sel(const ekv_select_params *s, float alpha) {
         if (!(alpha > 1.0f) || fabs(beta - rb) > 1e-9 || rb < 1 || rb > 4)
             return fail(EKV_ERR_UNSUPPORTED, "Gaussian selector needs integer beta=1/(alpha-1) in {1,2,3,4} (alpha=%g)",
                         (double)alpha);
+    } else if (s->policy == EKV_CERTIFIED) {
+        if (s->k_pages < 1) return fail(EKV_ERR_INVALID_ARG, "k_pages (first pass) must be >= 1");
     } else if (s->policy != EKV_ALL) {
         return fail(EKV_ERR_INVALID_ARG, "bad policy %d", s->policy);
     }
@@ -508,8 +510,8 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
     EKV_TRY(check_sel(sel, attn->alpha));
     if (!q || !out || !workspace) return fail(EKV_ERR_INVALID_ARG, "NULL argument");
     EKV_TRY(check_q(q));
-    if (sel->policy == EKV_GAUSS && attn->transform != EKV_ENTMAX)
-        return fail(EKV_ERR_INVALID_ARG, "Gaussian selector is entmax-specific");
+    if ((sel->policy == EKV_GAUSS || sel->policy == EKV_CERTIFIED) && attn->transform != EKV_ENTMAX)
+        return fail(EKV_ERR_INVALID_ARG, "Gaussian / certified selection is entmax-specific");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const CacheView v = view(cache);
     Layout L = layout(cache, n_q_heads, sel);
@@ -526,7 +528,8 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
     // per-step counters / union mask are zeroed by the scoring kernel (or a k_zero launch
     // when nothing is scored) -- kernels only, so the PDL chain is unbroken
     int modes = 0;
-    if (sel->policy == EKV_TOPK || want_db) modes |= EKV_SCORE_BOX;
+    const bool cert = sel->policy == EKV_CERTIFIED;
+    if (sel->policy == EKV_TOPK || cert || want_db) modes |= EKV_SCORE_BOX;
     if (sel->policy == EKV_GAUSS) modes |= EKV_SCORE_GAUSS;
     uint4 *zp = at<uint4>(workspace, L.zero);
     const size_t zn16 = L.zero_bytes / 16;
@@ -534,8 +537,8 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
     else EKV_TRY(launch_zero(zp, zn16, st));
     // a2 / a2'
     const int maxp = cache->max_pages_per_seq;
-    if (sel->policy == EKV_TOPK || sel->policy == EKV_ALL) {
-        const int k = sel->policy == EKV_TOPK ? sel->k_pages : maxp;
+    if (sel->policy == EKV_TOPK || sel->policy == EKV_ALL || cert) {
+        const int k = sel->policy == EKV_ALL ? maxp : sel->k_pages;
         EKV_TRY(launch_topk(box, cache->batch, n_q_heads, maxp, cache->seq_lens, k, pi, ns, L.cap, Gq, uo, st));
     } else {
         EKV_TRY(launch_gauss(cache, n_q_heads, mu, s2, attn->alpha, sel, pi, ns, L.cap, th, st));
@@ -551,9 +554,21 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
         xa.supp_tok = stats->supp_tok;
         xa.supp_cap = stats->supp_cap;
     }
+    const int rows = cache->batch * n_q_heads;
+    if (cert) {
+        // N4 (Prop. B.2): the top-k pass's exact tau~ <= tau certifies {p : a box(p) > tau~};
+        // the second pass attends that superset of the support's pages (exact, Prop. 2)
+        TauArgs x1;
+        memset(&x1, 0, sizeof(x1));
+        EKV_TRY(attend_impl(cache, q, n_q_heads, pi, ns, L.cap, 0, attn, out, th, nullptr, workspace, L, st, &x1,
+                            /*marked=*/true));
+        EKV_TRY(launch_zero(at<uint4>(workspace, L.retry), (L.zero_bytes - (L.retry - L.zero)) / 16, st));
+        EKV_TRY(launch_box_certified(box, cache->batch, n_q_heads, Gq, maxp, cache->seq_lens, th, attn->alpha, pi, ns,
+                                     L.cap, uo.umask, L.W, st));
+        xa.var = 1;
+    }
     EKV_TRY(attend_impl(cache, q, n_q_heads, pi, ns, L.cap, 0, attn, out, tau_p,
                         stats ? stats->supp_count : nullptr, workspace, L, st, &xa, /*marked=*/true));
-    const int rows = cache->batch * n_q_heads;
     // a4: certified dropped-mass bound
     if (want_db)
         EKV_TRY(launch_delta_bar(box, maxp, cache->seq_lens, rows, n_q_heads, Gq, uo.umask, L.W, tau_p, attn->alpha,
@@ -562,7 +577,7 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
         if (stats->n_sel)
             EKV_TRY(check_err(cudaMemcpyAsync(stats->n_sel, ns, rows * sizeof(int32_t), cudaMemcpyDeviceToDevice, st),
                               "n_sel copy"));
-        if (stats->tau_hat && sel->policy == EKV_GAUSS)
+        if (stats->tau_hat && (sel->policy == EKV_GAUSS || cert))
             EKV_TRY(check_err(cudaMemcpyAsync(stats->tau_hat, th, rows * sizeof(double), cudaMemcpyDeviceToDevice, st),
                               "tau_hat copy"));
         if (stats->eval_exact && attn->transform == EKV_ENTMAX) {

@@ -105,6 +105,9 @@ struct UnionOut {            // optional union marks done by the selection kerne
 };
 ekv_status launch_topk(const float *box, int B, int Hq, int maxp, const int32_t *sl, int k, int32_t *pi, int32_t *ns,
                        int stride, int G, const UnionOut &u, cudaStream_t st);
+ekv_status launch_box_certified(const float *box, int B, int Hq, int G, int maxp, const int32_t *seq_lens,
+                                const double *tau_hat, float alpha, int32_t *pi, int32_t *ns, int stride,
+                                uint32_t *um, int W, cudaStream_t st);
 ekv_status launch_mark(int B, int Hq, int G, const int32_t *pi, const int32_t *ns, int stride, uint32_t *um, int W,
                        cudaStream_t st);
 ekv_status launch_gauss(const ekv_cache *cache, int Hq, const float *mu, const float *s2, float alpha,

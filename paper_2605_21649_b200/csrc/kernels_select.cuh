@@ -632,6 +632,50 @@ static __global__ void __launch_bounds__(256) k_mark(int Hq, int G, const int32_
     for (int i = threadIdx.x; i < n; i += 256) union_mark(um, pl[i], g);
 }
 
+// ============================================================================ N4: certified selection
+// Prop. B.2: C_page = {p : (alpha-1) sbar_box(p) > tau_hat} with tau_hat <= tau
+// (here the exact threshold of a first top-k pass, R13 / R27); the fp64 decision of R9.
+// One CTA per (b, q-head), 512 threads x 4 consecutive pages per chunk, ascending output by
+// block scan, union marks for the group (umask zeroed by the host).  A NaN tau_hat (the
+// first pass overflowed) selects every page -- still a superset.
+static __global__ void __launch_bounds__(512) k_box_certified(const float *__restrict__ box, int Hq, int G, int maxp,
+                                                              const int32_t *__restrict__ seq_lens,
+                                                              const double *__restrict__ tau_hat, float alpha,
+                                                              int32_t *__restrict__ page_idx,
+                                                              int32_t *__restrict__ n_sel, int stride,
+                                                              uint32_t *__restrict__ umask, int W) {
+    pdl_enter();
+    __shared__ int sh[18];
+    const int row = blockIdx.x, b = row / Hq;
+    const int M = n_pages_of(seq_lens[b]);
+    const double a = (double)alpha - 1.0, t = tau_hat[row];
+    const bool all = !(t == t);
+    const float *x = box + (size_t)row * maxp;
+    int32_t *out = page_idx + (size_t)row * stride;
+    uint32_t *um = umask + (size_t)(b * (Hq / G) + (row % Hq) / G) * W;
+    const int g = (row % Hq) % G;
+    int base = 0;
+    for (int p0 = 0; p0 < M; p0 += 512 * 4) {
+        uint32_t bits = 0u;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int p = p0 + 4 * threadIdx.x + e;
+            if (p < M && (all || a * (double)__ldg(x + p) > t)) bits |= 1u << e;
+        }
+        int tot;
+        int pos = base + block_excl_scan<512>(__popc(bits), sh, &tot);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if ((bits >> e) & 1u) {
+                const int p = p0 + 4 * threadIdx.x + e;
+                out[pos++] = p;
+                union_mark(um, p, g);
+            }
+        base += tot;
+    }
+    if (threadIdx.x == 0) n_sel[row] = base;
+}
+
 // ============================================================================ a2': Gaussian selector
 struct GaussMoments { double m, dm, d2; };   // M_beta, M_{beta-1}, and the d^2/dtau^2 term
 

@@ -32,6 +32,14 @@ ekv_status launch_mark(int B, int Hq, int G, const int32_t *pi, const int32_t *n
     return check_launch("k_mark");
 }
 
+ekv_status launch_box_certified(const float *box, int B, int Hq, int G, int maxp, const int32_t *seq_lens,
+                                const double *tau_hat, float alpha, int32_t *pi, int32_t *ns, int stride,
+                                uint32_t *um, int W, cudaStream_t st) {
+    launch_ex(k_box_certified, dim3(B * Hq), dim3(512), 0, st, 0, box, Hq, G, maxp, seq_lens, tau_hat, alpha, pi, ns,
+              stride, um, W);
+    return check_launch("k_box_certified");
+}
+
 // a2': one CTA per (b, q-head); rows of up to 8192 pages staged in shared memory.  Many rows
 // (>= 2 per SM): 512-thread CTAs, two per SM, so one row's reductions overlap the other's
 // passes (C3: 244 -> 212 us); few rows: 1024 threads per row.
