@@ -294,6 +294,29 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 #ifndef EKV_MBAR_HINT
 #define EKV_MBAR_HINT 0
 #endif
+// streaming bulk copy: the source lines are marked evict-first in L2 (data read once per step
+// -- page metadata, K tiles -- must not push out what the next kernels re-read: box scores,
+// page tables, score rows).  EKV_EF=0 builds plain copies (A/B).
+#ifndef EKV_EF
+#define EKV_EF 1
+#endif
+__device__ __forceinline__ void bulk_g2s_stream(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+#if EKV_EF
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+#else
+    bulk_g2s(dst, src, bytes, bar);
+#endif
+}
+// bulk L2 prefetch (no shared memory, no completion): warms L2 for a later TMA read
+__device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
 #if EKV_MBAR_HINT
     // try_wait with a suspend-time hint (ns): the warp may sleep until the phase completes

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
                     }
                     __syncwarp();
                     if (lane < SP)
-                        bulk_g2s(smem + ((size_t)slot * SP + lane) * TILE,
+                        bulk_g2s_stream(smem + ((size_t)slot * SP + lane) * TILE,
                                  Kb + ((size_t)d_phys[slot][lane] * c.Hkv + d_unit[slot][lane] % c.Hkv) * TILE,
                                  TILE, &fullb[slot]);
                     ++si;
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
             }
             __syncwarp();
             if (lane < fill)
-                bulk_g2s(smem + ((size_t)slot * SP + lane) * TILE,
+                bulk_g2s_stream(smem + ((size_t)slot * SP + lane) * TILE,
                          Kb + ((size_t)d_phys[slot][lane] * c.Hkv + d_unit[slot][lane] % c.Hkv) * TILE,
                          TILE, &fullb[slot]);
             ++si;

@@ -248,14 +248,14 @@ __global__ void __launch_bounds__(288, (MODES == 1 && (FMT & 1) && G <= 4 && siz
                         const size_t phys = (size_t)l_phys[i + k];
                         unsigned char *dst = smem + ((size_t)slot * SP + k) * per_page;
                         if (MODES & 1) {
-                            if (w == 0) bulk_g2s(dst, reinterpret_cast<const unsigned char *>(c.kmin) + phys * bmm, bmm, &fullb[slot]);
-                            if (w == 1) bulk_g2s(dst + bmm, reinterpret_cast<const unsigned char *>(c.kmax) + phys * bmm, bmm, &fullb[slot]);
+                            if (w == 0) bulk_g2s_stream(dst, reinterpret_cast<const unsigned char *>(c.kmin) + phys * bmm, bmm, &fullb[slot]);
+                            if (w == 1) bulk_g2s_stream(dst + bmm, reinterpret_cast<const unsigned char *>(c.kmax) + phys * bmm, bmm, &fullb[slot]);
                             dst += 2 * bmm;
                         }
                         if (MODES & 2) {
                             const int w2 = w - ((MODES & 1) ? 2 : 0);
-                            if (w2 == 0) bulk_g2s(dst, reinterpret_cast<const unsigned char *>(c.kavg) + phys * bgs, bgs, &fullb[slot]);
-                            if (w2 == 1) bulk_g2s(dst + bgs, reinterpret_cast<const unsigned char *>(c.kvar) + phys * bgs, bgs, &fullb[slot]);
+                            if (w2 == 0) bulk_g2s_stream(dst, reinterpret_cast<const unsigned char *>(c.kavg) + phys * bgs, bgs, &fullb[slot]);
+                            if (w2 == 1) bulk_g2s_stream(dst + bgs, reinterpret_cast<const unsigned char *>(c.kvar) + phys * bgs, bgs, &fullb[slot]);
                         }
                     }
                     ++si;

@@ -84,7 +84,7 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ uint64_t gtimer() {
+__device__ __forceinline__ uint64_t px_now() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
@@ -109,9 +109,9 @@ __device__ __forceinline__ bool px_wait(const PeerSet &P, int row, uint64_t e) {
     bool ok = true;
     if (threadIdx.x < P.W) {
         const uint64_t *f = px_flag(P, P.rk, threadIdx.x, row);
-        const uint64_t t0 = gtimer();
+        const uint64_t t0 = px_now();
         while (ld_acquire_sys(f) < e) {
-            if (gtimer() - t0 > 2000000000ull) { ok = false; break; }
+            if (px_now() - t0 > 2000000000ull) { ok = false; break; }
         }
     }
     return __syncthreads_and(ok) != 0;

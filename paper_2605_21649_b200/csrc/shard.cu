@@ -134,8 +134,8 @@ ekv_status entmaxkv_decode_sharded(const ekv_cache *cache, const int32_t *global
         return fail(EKV_ERR_INVALID_ARG, "bad communicator (rank %d, world %d)", comm->rank, comm->world);
     if (dev) {
         if (comm->world > kMaxPeers) return fail(EKV_ERR_UNSUPPORTED, "in-kernel collectives: world %d > %d", comm->world, kMaxPeers);
-        for (int q = 0; q < comm->world; ++q)
-            if (!comm->peers[q]) return fail(EKV_ERR_INVALID_ARG, "in-kernel collectives: peers[%d] is NULL", q);
+        for (int r = 0; r < comm->world; ++r)
+            if (!comm->peers[r]) return fail(EKV_ERR_INVALID_ARG, "in-kernel collectives: peers[%d] is NULL", r);
     }
     if (sel->policy != EKV_TOPK || attn->transform != EKV_ENTMAX)
         return fail(EKV_ERR_UNSUPPORTED, "sharded decode supports top-k selection with entmax");
@@ -166,7 +166,7 @@ ekv_status entmaxkv_decode_sharded(const ekv_cache *cache, const int32_t *global
     PeerSet P;
     memset(&P, 0, sizeof(P));
     if (dev) {
-        for (int q = 0; q < W; ++q) P.buf[q] = static_cast<unsigned char *>(comm->peers[q]);
+        for (int r = 0; r < W; ++r) P.buf[r] = static_cast<unsigned char *>(comm->peers[r]);
         P.W = W; P.rk = rk; P.rows = rows; P.pay = peer_pay(S.kc);
         return decode_sharded_dev(cache, v, L, S, P, global_seq_lens, q, n_q_heads, sel, attn, ib, beta, out, stats,
                                   workspace, st);
