@@ -408,6 +408,15 @@ __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.laun
 // passed its own wait only after n-2 completed, so a prologue placed BEFORE pdl_enter() may read
 // data written two or more launches back (not n-1's).
 __device__ __forceinline__ void pdl_enter() { pdl_wait(); }
+// Per-kernel early trigger (bit KID of EKV_PDL_TRIG; trace ids): kernels whose grid is one
+// partial wave let their successor be launched right away, so its CTAs are resident (waiting
+// in pdl_enter) when this grid completes -- the launch latency leaves the critical path.
+#ifndef EKV_PDL_TRIG
+#define EKV_PDL_TRIG 65   /* append (0) and tau (6): measured 112.3 -> 111.7 us; other kernels slower */
+#endif
+template <int KID> __device__ __forceinline__ void pdl_trigger() {
+    if constexpr (((EKV_PDL_TRIG) >> KID) & 1) pdl_launch();
+}
 }  // namespace ekv
 
 // ---------------------------------------------------------------- optional in-kernel phase stamps

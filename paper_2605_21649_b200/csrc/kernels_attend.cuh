@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
     float *__restrict__ scores, uint32_t *__restrict__ rowmax, int full) {
     EKV_TRACE(4);
     pdl_enter();
+    pdl_trigger<4>();
     constexpr int SP = AttCfg<T>::SP, NS = AttCfg<T>::NS, TILE = AttCfg<T>::TILE;
     constexpr int NCW = AttCfg<T>::NCW;
     constexpr int CHK = 256;                // work slots per producer chunk (8 per lane)

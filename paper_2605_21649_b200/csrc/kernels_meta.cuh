@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(1024, 1) k_append(CacheView c, const T *__rest
                                                  const T *__restrict__ v_new, int n_tokens) {
     EKV_TRACE(0);
     pdl_enter();
+    pdl_trigger<0>();
     const int b = blockIdx.x;
     const int L = c.seq_lens[b];
     T *K = reinterpret_cast<T *>(c.Kw);
@@ -180,6 +181,7 @@ __global__ void __launch_bounds__(288, (MODES == 1 && (FMT & 1) && G <= 4 && siz
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < zero_n16; i += (size_t)gridDim.x * blockDim.x)
         zero[i] = make_uint4(0, 0, 0, 0);
     pdl_enter();
+    pdl_trigger<1>();
     constexpr int SP = ScoreCfg<MODES, FMT>::SP, NS = ScoreCfg<MODES, FMT>::NS;
     constexpr int NCW = 8;
     extern __shared__ __align__(128) unsigned char smem[];

@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict_
                                                 int sel_stride, int G, uint32_t *__restrict__ umask, int W) {
     EKV_TRACE(2);
     pdl_enter();
+    pdl_trigger<2>();
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     const int CL = (int)cl.num_blocks(), r = (int)cl.block_rank();

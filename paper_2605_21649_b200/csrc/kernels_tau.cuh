@@ -148,6 +148,7 @@ template <typename T, int IB, bool FULL>
 __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A) {
     EKV_TRACE(6);
     pdl_enter();
+    pdl_trigger<6>();
     constexpr int NT = kTsNT, NW = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     // capacities: cap candidates (<= kTsCap; sparse rows: the list's token count, so short
