@@ -235,11 +235,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict_
     //     gathers them all and finds T* = the k-th largest composite (MSB-first radix select
     //     with 8-bit digits, stopping when a digit's bin is taken whole); the selection is
     //     composite >= T*.  Two cluster barriers instead of one per digit and a tie round.
+    extern __shared__ __align__(16) unsigned long long tk_dyn[];
     bool fast = false;
+    int nfast = 0;
     unsigned long long tcomp = 0ull;
     uint32_t tpiv = 0xffffffffu;
     {
-        extern __shared__ __align__(16) unsigned long long tk_dyn[];
         unsigned long long *lc = tk_dyn;               // [kTkCap] this CTA's candidates
         unsigned long long *gc = tk_dyn + kTkCap;      // [kTkCap] the cluster's candidates
         __shared__ uint32_t samp[NT];
@@ -335,6 +336,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict_
         __syncthreads();
         const int C = qoff[CL - 1] + qcnt[CL - 1];
         fast = rp >= 1 && C >= keff && C <= kTkCap;    // uniform over the cluster
+        nfast = C;
         ph_count<2>(0, C);
         ph_count<2>(1, (long long)rp * 10 + (fast ? 1 : 0));
         if (fast) {
@@ -356,6 +358,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict_
                 if (i < C) gc[i] = tmp[u];
             }
             __syncthreads();                           // gc complete before the passes read it
+            // this CTA's remote reads are done: arrive on the cluster barrier now, wait only at
+            // exit (the other CTAs' lists stay alive until every CTA has gathered)
+            asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
             // T* = the keff-th largest composite: linear histogram of the candidates' values over
             // [tp, max], then a brute-force rank among the (few) composites of the boundary bin
             bool done = false;
@@ -593,13 +598,28 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict_
     const uint32_t w = t < NT / 2 ? bits[t] : 0u;
     int tot;
     const int pos = block_excl_scan<NT>(__popc(w), sh, &tot);
-    if (t == 0) xch[1] = tot;
-    cl.sync();
     int o = pos;
-    if (r > 0) {                                             // sum of the lower ranks' counts
-        int c = (lane < r) ? *cl.map_shared_rank(&xch[1], lane) : 0;
-        c = __reduce_add_sync(0xffffffffu, c);
-        o += c;
+    if (fast) {
+        // the lower ranks' selected pages, counted from this CTA's copy of the candidate list
+        // (every selected page is a candidate): no cluster exchange
+        if (r > 0) {
+            const unsigned long long *gc = tk_dyn + kTkCap;
+            const uint32_t inv_base = 0xffffffffu - (uint32_t)base;   // page < base <=> low word > inv_base
+            int c = 0;
+            for (int i = t; i < nfast; i += NT) {
+                const unsigned long long x = gc[i];
+                c += (x >= tcomp && (uint32_t)(x & 0xffffffffu) > inv_base) ? 1 : 0;
+            }
+            o += block_sum_i<NT>(c, sh);
+        }
+    } else {
+        if (t == 0) xch[1] = tot;
+        cl.sync();
+        if (r > 0) {                                         // sum of the lower ranks' counts
+            int c = (lane < r) ? *cl.map_shared_rank(&xch[1], lane) : 0;
+            c = __reduce_add_sync(0xffffffffu, c);
+            o += c;
+        }
     }
     uint32_t v = w;
     while (v) {
@@ -611,7 +631,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict_
     if (r == 0 && t == 0) n_sel[row] = keff;
     stamp(1, 6);
     ph_stamp<2>(7);
-    cl.sync();                               // keep shared memory alive for remote readers
+    if (fast) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");   // (arrived after the gather)
+    else cl.sync();                          // keep shared memory alive for remote readers
 }
 
 // ============================================================================ union per KV group
