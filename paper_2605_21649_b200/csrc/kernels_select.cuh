@@ -756,21 +756,51 @@ template <int NT> __device__ __forceinline__ void block_sum3_d(double &a, double
 // conservative fp32 pre-test.  sg = sqrtf(sigma2) (cached) or nullptr (computed).
 #define EKV_GAUSS_SKIP(num, den) ((den) > 0.f ? ((num) < -9.5f * (den)) : ((num) <= 0.f))
 
+// Cluster-split rows (CL > 1 CTAs per row, page slice [p0, p1) each): the CTA's partial sums
+// are published in a double-buffered shared slot and every CTA adds the CL slots in rank order
+// -- identical totals (and so identical Newton / Halley control flow) in every CTA, one
+// cluster barrier per reduction.
+struct GaussRed {
+    double *slot;      // [2][4] this CTA's published partials (double-buffered)
+    double *gath;      // [8][4] the CL CTAs' partials, gathered
+    int CL, par;
+};
+__device__ __forceinline__ void gauss_cluster_sum(GaussRed &R, double *v, int n) {
+    if (R.CL <= 1) return;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    double *my = R.slot + 4 * R.par;
+    if (threadIdx.x < (unsigned)n) my[threadIdx.x] = threadIdx.x == 0 ? v[0] : threadIdx.x == 1 ? v[1] : v[2];
+    cl.sync();
+    if (threadIdx.x < (unsigned)(R.CL * n)) {
+        const int q = threadIdx.x / n, i = threadIdx.x - q * n;
+        R.gath[4 * q + i] = cl.map_shared_rank(my, q)[i];
+    }
+    __syncthreads();
+    for (int i = 0; i < n; ++i) {
+        double acc = 0.0;
+        for (int q = 0; q < R.CL; ++q) acc += R.gath[4 * q + i];
+        v[i] = acc;
+    }
+    R.par ^= 1;
+}
+
 // fp32 steering pass: mass(tau) and -d mass/d tau, fp32 terms and per-thread sums
 template <int NT>
-__device__ void gauss_mass32(const float *mu, const float *sg, const float *s2, int M, int Lseq, float af, int beta,
-                             float tf, double &mass, double &dmass, double *shd) {
+__device__ void gauss_mass32(const float *mu, const float *sg, const float *s2, int p0, int p1, int Lseq, float af,
+                             int beta, float tf, double &mass, double &dmass, double *shd, GaussRed &R) {
     float m = 0.f, dm = 0.f;
 #pragma unroll 4
-    for (int p = threadIdx.x; p < M; p += NT) {
-        const float mp = mu[p], sp = sg ? sg[p] : sqrtf(s2[p]);
+    for (int p = p0 + threadIdx.x; p < p1; p += NT) {
+        const int i = p - p0;
+        const float mp = mu[i], sp = sg ? sg[i] : sqrtf(s2[i]);
         const float num = af * mp - tf, den = af * sp;
         if (EKV_GAUSS_SKIP(num, den)) continue;
         const float cnt = (float)min(kP, Lseq - p * kP);
         float r, rm;
         if (!(den > 0.f)) {
             r = 1.f; rm = 1.f;
-            for (int i = 0; i < beta; ++i) { rm = r; r *= num; }
+            for (int i2 = 0; i2 < beta; ++i2) { rm = r; r *= num; }
         } else {
             const float t = num / den;
             const float Ph = normcdff(t), ph = __expf(-0.5f * t * t) * 0.39894228f;
@@ -787,18 +817,22 @@ __device__ void gauss_mass32(const float *mu, const float *sg, const float *s2, 
     }
     double a = m, b = (double)beta * dm;
     block_sum2_d<NT>(a, b, shd);
-    mass = a; dmass = b;
+    double v[3] = {a, b, 0.0};
+    gauss_cluster_sum(R, v, 2);
+    mass = v[0]; dmass = v[1];
 }
 
 // fp64 pass: mass, -mass' and mass'' (the terms follow orc_gauss_mass: a, mu, sqrt(sigma2) in fp64)
 template <int NT>
-__device__ void gauss_mass64(const float *mu, const float *sg, const float *s2, int M, int Lseq, float af, int beta,
-                             double tau, double &mass, double &dmass, double &d2mass, double *shd) {
+__device__ void gauss_mass64(const float *mu, const float *sg, const float *s2, int p0, int p1, int Lseq, float af,
+                             int beta, double tau, double &mass, double &dmass, double &d2mass, double *shd,
+                             GaussRed &R) {
     double m = 0.0, dm = 0.0, d2 = 0.0;
     const float tf = (float)tau;
     const double a = (double)af;
-    for (int p = threadIdx.x; p < M; p += NT) {
-        const float mp = mu[p], s2p = s2[p], sp = sg ? sg[p] : sqrtf(s2p);
+    for (int p = p0 + threadIdx.x; p < p1; p += NT) {
+        const int i = p - p0;
+        const float mp = mu[i], s2p = s2[i], sp = sg ? sg[i] : sqrtf(s2p);
         const float num = af * mp - tf, den = af * sp;
         if (EKV_GAUSS_SKIP(num, den)) continue;
         const double cnt = (double)min(kP, Lseq - p * kP);
@@ -810,7 +844,9 @@ __device__ void gauss_mass64(const float *mu, const float *sg, const float *s2, 
     dm *= (double)beta;
     d2 *= beta == 1 ? 1.0 : (double)(beta * (beta - 1));
     block_sum3_d<NT>(m, dm, d2, shd);
-    mass = m; dmass = dm; d2mass = d2;
+    double v[3] = {m, dm, d2};
+    gauss_cluster_sum(R, v, 3);
+    mass = v[0]; dmass = v[1]; d2mass = v[2];
 }
 
 // One CTA per (b, q-head).  tau_hat solves  sum_p c_p E[(a S_p - tau)_+^beta] = 1
@@ -842,32 +878,52 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gauss_select(const float *__r
     // zq[c] = Phi^{-1}(q_page^{1/c}), fp64 normcdfinv rounded to fp32 (R14)
     if (threadIdx.x >= 1 && threadIdx.x <= kP)
         zq[threadIdx.x] = (float)normcdfinv(pow(q_page, 1.0 / (double)threadIdx.x));
-    const int row = blockIdx.x;
+    // a row is split over the CL CTAs of a cluster (rows longer than the shared-memory stage):
+    // CTA r owns pages [p0, p1) of the row
+    namespace cg = cooperative_groups;
+    const int CL = (int)cg::this_cluster().num_blocks(), rk = (int)cg::this_cluster().block_rank();
+    __shared__ double red_slot[8], red_gath[32];
+    GaussRed R{red_slot, red_gath, CL, 0};
+    const int row = blockIdx.x / CL;
     const int b = row / Hq;
     const int Lseq = seq_lens[b];
     const int M = n_pages_of(Lseq);
-    const float *mg = mu + (size_t)row * maxp;
-    const float *sgg = sigma2 + (size_t)row * maxp;
-    const bool cached = M <= cache_pages;
+    const int S = (maxp + CL - 1) / CL;
+    const int p0 = min(M, rk * S), p1 = min(M, (rk + 1) * S);
+    const float *mg = mu + (size_t)row * maxp + p0;
+    const float *sgg = sigma2 + (size_t)row * maxp + p0;
+    const bool cached = p1 - p0 <= cache_pages;
     float *c_mu = gsm, *c_s2 = gsm + cache_pages, *c_sg = gsm + 2 * cache_pages;
     const double a = (double)alpha - 1.0;
     const float af = (float)a;
     const int beta = (int)llrint(1.0 / a);
-    // stage the row (and the bracket start a max_p (mu + 8 sigma))
+    // stage the slice (and the bracket start a max_p (mu + 8 sigma))
     float tmax = -INFINITY;
-    for (int p = threadIdx.x; p < M; p += NT) {
-        const float mp = __ldg(mg + p), s2p = __ldg(sgg + p), sp = sqrtf(s2p);
-        if (cached) { c_mu[p] = mp; c_s2[p] = s2p; c_sg[p] = sp; }
+    for (int i = threadIdx.x; i < p1 - p0; i += NT) {
+        const float mp = __ldg(mg + i), s2p = __ldg(sgg + i), sp = sqrtf(s2p);
+        if (cached) { c_mu[i] = mp; c_s2[i] = s2p; c_sg[i] = sp; }
         tmax = fmaxf(tmax, mp + 8.0f * sp);
     }
-    tmax = block_max_f<NT>(tmax, shf);   // (its barriers publish the staged row)
+    tmax = block_max_f<NT>(tmax, shf);   // (its barriers publish the staged slice)
+    if (CL > 1) {
+        double v[3] = {(double)tmax, 0.0, 0.0};
+        // (max via the sum machinery is wrong; exchange the CTA maxima explicitly)
+        cg::cluster_group cl = cg::this_cluster();
+        if (threadIdx.x == 0) red_slot[4] = (double)tmax;
+        cl.sync();
+        double mx = -INFINITY;
+        for (int q = 0; q < CL; ++q) mx = fmax(mx, *cl.map_shared_rank(&red_slot[4], q));
+        tmax = (float)mx;
+        (void)v;
+        cl.sync();                        // (red_slot[4] is reused by the first reduction)
+    }
     const float *m_ = cached ? c_mu : mg, *s_ = cached ? c_s2 : sgg, *g_ = cached ? c_sg : nullptr;
     ph_stamp<8>(1);
     // (1) fp32 steering: Newton on log mass from the right end a max_p (mu + 8 sigma);
     // bisection once bracketed when a step leaves the bracket, doubling steps while a side
     // is still open
     double lo = -INFINITY, hi = INFINITY, tau = a * (double)tmax, w = 1.0, dxold = INFINITY, mass, dmass, d2mass;
-    gauss_mass32<NT>(m_, g_, s_, M, Lseq, af, beta, (float)tau, mass, dmass, shd);
+    gauss_mass32<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, (float)tau, mass, dmass, shd, R);
     ++n32;
     for (int it = 0; it < 80; ++it) {
         if (mass >= 1.0) lo = tau; else hi = tau;
@@ -890,7 +946,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gauss_select(const float *__r
         dxold = fabs(nt - tau);
         tau = nt;
         if (stop) break;
-        gauss_mass32<NT>(m_, g_, s_, M, Lseq, af, beta, (float)tau, mass, dmass, shd);
+        gauss_mass32<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, (float)tau, mass, dmass, shd, R);
         ++n32;
     }
     ph_stamp<8>(2);
@@ -899,7 +955,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gauss_select(const float *__r
     {
         double t = tau;
         for (int it = 0; it < 4; ++it) {
-            gauss_mass64<NT>(m_, g_, s_, M, Lseq, af, beta, t, mass, dmass, d2mass, shd);
+            gauss_mass64<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, t, mass, dmass, d2mass, shd, R);
             ++n64;
             if (!(dmass > 0.0)) break;
             const double f = mass - 1.0;
@@ -923,20 +979,20 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gauss_select(const float *__r
     if (!done64) {
     lo = tau - dl;
     for (int it = 0; it < 200; ++it) {
-        gauss_mass64<NT>(m_, g_, s_, M, Lseq, af, beta, lo, mass, dmass, d2mass, shd);
+        gauss_mass64<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, lo, mass, dmass, d2mass, shd, R);
         if (mass >= 1.0) break;
         dl *= 4.0; lo = tau - dl;
     }
     double dh = 1e-4 * fmax(1.0, fabs(tau));
     hi = tau + dh;
     for (int it = 0; it < 200; ++it) {
-        gauss_mass64<NT>(m_, g_, s_, M, Lseq, af, beta, hi, mass, dmass, d2mass, shd);
+        gauss_mass64<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, hi, mass, dmass, d2mass, shd, R);
         if (mass < 1.0) break;
         dh *= 4.0; hi = tau + dh;
     }
     tau = fmin(fmax(tau, lo), hi);
     for (int it = 0; it < 100; ++it) {
-        gauss_mass64<NT>(m_, g_, s_, M, Lseq, af, beta, tau, mass, dmass, d2mass, shd);
+        gauss_mass64<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, tau, mass, dmass, d2mass, shd, R);
         if (mass >= 1.0) lo = tau; else hi = tau;
         double nt = (dmass > 0.0) ? tau + (mass - 1.0) / dmass : 0.5 * (lo + hi);
         if (!(nt > lo && nt < hi)) nt = 0.5 * (lo + hi);
@@ -948,15 +1004,43 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gauss_select(const float *__r
     }
     }
     ph_stamp<8>(4);
-    // page rule + ordered compaction (NT pages per round)
+    // page rule + ordered compaction (NT pages per round) over the slice; the slices' counts
+    // are exchanged for the output offsets (rank order = page order)
     int32_t *out = page_idx + (size_t)row * sel_stride;
-    int base = 0;
-    for (int r0 = 0; r0 < M; r0 += NT) {
+    __shared__ int x_cnt;
+    __shared__ unsigned long long x_best;
+    int cnt_local = 0;
+    for (int r0 = p0; r0 < p1; r0 += NT) {
         const int p = r0 + threadIdx.x;
         int keep = 0;
-        if (p < M) {
+        if (p < p1) {
             const int cnt = min(kP, Lseq - p * kP);
-            const float sg = __fmaf_rn(g_ ? g_[p] : sqrtf(s_[p]), zq[cnt], m_[p]);
+            const float sg = __fmaf_rn(g_ ? g_[p - p0] : sqrtf(s_[p - p0]), zq[cnt], m_[p - p0]);
+            keep = (a * (double)sg > tau - margin) ? 1 : 0;
+        }
+        int tot;
+        block_excl_scan<NT>(keep, shi, &tot);
+        cnt_local += tot;
+    }
+    int off = 0, total = cnt_local;
+    if (CL > 1) {
+        cg::cluster_group cl = cg::this_cluster();
+        if (threadIdx.x == 0) x_cnt = cnt_local;
+        cl.sync();
+        total = 0;
+        for (int q = 0; q < CL; ++q) {
+            const int c = *cl.map_shared_rank(&x_cnt, q);
+            if (q < rk) off += c;
+            total += c;
+        }
+    }
+    int base = off;
+    for (int r0 = p0; r0 < p1; r0 += NT) {
+        const int p = r0 + threadIdx.x;
+        int keep = 0;
+        if (p < p1) {
+            const int cnt = min(kP, Lseq - p * kP);
+            const float sg = __fmaf_rn(g_ ? g_[p - p0] : sqrtf(s_[p - p0]), zq[cnt], m_[p - p0]);
             keep = (a * (double)sg > tau - margin) ? 1 : 0;
         }
         int tot;
@@ -964,14 +1048,13 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gauss_select(const float *__r
         if (keep) out[base + pos] = p;
         base += tot;
     }
-    if (base == 0 && M > 0) {
-        // argmax mu, lower index on ties (R6)
+    if (total == 0 && M > 0) {
+        // argmax mu, lower index on ties (R6), over the whole row
         uint64_t best = 0;
-        for (int p = threadIdx.x; p < M; p += NT) {
-            const uint64_t k = ((uint64_t)f2key(m_[p]) << 32) | (uint32_t)(0xffffffffu - (uint32_t)p);
+        for (int p = p0 + threadIdx.x; p < p1; p += NT) {
+            const uint64_t k = ((uint64_t)f2key(m_[p - p0]) << 32) | (uint32_t)(0xffffffffu - (uint32_t)p);
             best = best > k ? best : k;
         }
-        // block max of u64 via two passes on shared memory
         __shared__ unsigned long long shb[NT / 32];
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) {
@@ -983,14 +1066,26 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gauss_select(const float *__r
         if (threadIdx.x == 0) {
             uint64_t r = 0;
             for (int i = 0; i < NT / 32; ++i) r = r > shb[i] ? r : shb[i];
-            out[0] = (int)(0xffffffffu - (uint32_t)(r & 0xffffffffu));
+            x_best = r;
         }
-        base = 1;
+        __syncthreads();
+        uint64_t r = x_best;
+        if (CL > 1) {
+            cg::cluster_group cl = cg::this_cluster();
+            cl.sync();
+            for (int q = 0; q < CL; ++q) {
+                const uint64_t y = *cl.map_shared_rank(&x_best, q);
+                r = r > y ? r : y;
+            }
+        }
+        if (rk == 0 && threadIdx.x == 0) out[0] = (int)(0xffffffffu - (uint32_t)(r & 0xffffffffu));
+        total = 1;
     }
-    if (threadIdx.x == 0) {
-        n_sel[row] = base;
+    if (rk == 0 && threadIdx.x == 0) {
+        n_sel[row] = total;
         if (tau_hat_out) tau_hat_out[row] = tau;
     }
+    if (CL > 1) cg::this_cluster().sync();   // keep shared memory alive for remote readers
     ph_stamp<8>(5);
 }
 

@@ -46,24 +46,29 @@ ekv_status launch_box_certified(const float *box, int B, int Hq, int G, int maxp
 template <int NT>
 static ekv_status launch_gauss_nt(const ekv_cache *cache, int Hq, const float *mu, const float *s2, float alpha,
                                   const ekv_select_params *sel, int32_t *pi, int32_t *ns, int stride, double *th,
-                                  cudaStream_t st) {
-    const int cache_pages = std::min(cache->max_pages_per_seq, 8192);
+                                  int CL, cudaStream_t st) {
+    const int maxp = cache->max_pages_per_seq;
+    const int cache_pages = std::min((maxp + CL - 1) / CL, 8192);
     const int smem = 12 * cache_pages;
     set_smem(k_gauss_select<NT>, 12 * 8192);
-    cudaError_t e = launch_ex(k_gauss_select<NT>, dim3((unsigned)(cache->batch * Hq)), dim3(NT), smem, st, 0u, mu, s2, Hq,
-                              (int)cache->max_pages_per_seq, (const int32_t *)cache->seq_lens, alpha, sel->margin,
-                              sel->q_page, pi, ns, stride, th, cache_pages);
+    cudaError_t e = launch_ex(k_gauss_select<NT>, dim3((unsigned)(cache->batch * Hq * CL)), dim3(NT), smem, st,
+                              (unsigned)(CL > 1 ? CL : 0), mu, s2, Hq, maxp, (const int32_t *)cache->seq_lens, alpha,
+                              sel->margin, sel->q_page, pi, ns, stride, th, cache_pages);
     if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "k_gauss_select: %s", cudaGetErrorString(e));
     return check_launch("k_gauss_select");
 }
 ekv_status launch_gauss(const ekv_cache *cache, int Hq, const float *mu, const float *s2, float alpha,
                         const ekv_select_params *sel, int32_t *pi, int32_t *ns, int stride, double *th, cudaStream_t st) {
-    // the block size (and so the fp64 reduction order of tau_hat) depends on the number of rows:
-    // tau_hat is reproducible per (batch, heads) configuration, and within 1e-10 relative of the
-    // oracle either way (R14)
-    if (cache->batch * Hq >= 2 * num_sms())
-        return launch_gauss_nt<512>(cache, Hq, mu, s2, alpha, sel, pi, ns, stride, th, st);
-    return launch_gauss_nt<1024>(cache, Hq, mu, s2, alpha, sel, pi, ns, stride, th, st);
+    // rows longer than the 8192-page shared-memory stage are split over a cluster of CL CTAs
+    // (C4: 65536 pages -> 8 CTAs per row, each row's slices staged in shared memory).  The
+    // block size and CL (and so the fp64 reduction order of tau_hat) depend on the shape:
+    // tau_hat is reproducible per configuration, and within 1e-10 relative of the oracle (R14)
+    int CL = 1;
+    while (CL < 8 && (cache->max_pages_per_seq + CL - 1) / CL > 8192) CL *= 2;
+    const long long ctas = (long long)cache->batch * Hq * CL;
+    if (ctas > num_sms())
+        return launch_gauss_nt<512>(cache, Hq, mu, s2, alpha, sel, pi, ns, stride, th, CL, st);
+    return launch_gauss_nt<1024>(cache, Hq, mu, s2, alpha, sel, pi, ns, stride, th, CL, st);
 }
 
 }  // namespace ekvh
