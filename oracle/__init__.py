@@ -83,6 +83,8 @@ def lib():
         L.orc_gauss_select.restype = c_int
         L.orc_delta_bar.argtypes = [f32p, i32p, u8p, c_int, c_double, c_double]
         L.orc_delta_bar.restype = c_double
+        L.orc_trunc_moment_num.argtypes = [c_double, c_double, c_double]
+        L.orc_trunc_moment_num.restype = c_double
         L.orc_box_certified.argtypes = [f32p, c_int, c_double, c_double, i32p]
         L.orc_box_certified.restype = c_int
         L.orc_e4m3_round_down.argtypes = [ctypes.c_float]
@@ -194,6 +196,11 @@ def trunc_moment(beta: int, muY: float, sigY: float) -> float:
     return float(lib().orc_trunc_moment(int(beta), float(muY), float(sigY)))
 
 
+def trunc_moment_num(beta: float, muY: float, sigY: float) -> float:
+    """E[(Y)_+^beta], Y ~ N(muY, sigY^2), any real beta > 0, by quadrature (R28)."""
+    return float(lib().orc_trunc_moment_num(float(beta), float(muY), float(sigY)))
+
+
 def gauss_mass(mu, sigma2, counts, alpha, tau):
     mu, sigma2, counts = _f32(mu), _f32(sigma2), _i32(counts)
     return float(lib().orc_gauss_mass(_p(mu, ctypes.c_float), _p(sigma2, ctypes.c_float),
@@ -206,7 +213,7 @@ def gauss_tau(mu, sigma2, counts, alpha):
     rc = lib().orc_gauss_tau(_p(mu, ctypes.c_float), _p(sigma2, ctypes.c_float), _p(counts, ctypes.c_int32),
                              mu.shape[0], float(alpha), _p(t, ctypes.c_double))
     if rc == -2:
-        raise ValueError(f"Gaussian tau_hat needs an integer beta = 1/(alpha-1) (alpha={alpha})")
+        raise ValueError(f"Gaussian tau_hat needs alpha > 1 (alpha={alpha})")
     if rc != 0:
         raise RuntimeError("tau_hat bracket failure")
     return float(t[0])

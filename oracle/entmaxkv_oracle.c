@@ -546,6 +546,45 @@ double orc_trunc_moment(int beta, double muY, double sigY)
     }
 }
 
+/* E[(Y)_+^beta] for a real beta > 0 ("for generic alpha > 1  */
+/* with non-integer beta ... the expectation can be evaluated numerically").          */
+/* E = sigY^beta h(m), m = muY / sigY, h(m) = int_0^inf u^beta phi(u - m) du, by       */
+/* tanh-sinh (double-exponential) quadrature on [L, U] = [max(0, m - 12),             */
+/* max(m, 0) + 12] (phi(12) < 3e-32: the cut tails are below fp64 resolution), the    */
+/* step halved from 1/8 until two successive sums agree to 1e-15 relative.  The       */
+/* substitution u = c + w tanh(pi/2 sinh t) clusters the nodes at the ends, which     */
+/* absorbs the u^beta endpoint singularity at u = 0 (DESIGN R28).  sigY = 0: the     */
+/* point mass [muY]_+^beta.                                                           */
+double orc_trunc_moment_num(double beta, double muY, double sigY)
+{
+    if (!(sigY > 0.0)) return muY > 0.0 ? pow(muY, beta) : 0.0;
+    double m = muY / sigY;
+    double L = m - 12.0 > 0.0 ? m - 12.0 : 0.0;
+    double U = (m > 0.0 ? m : 0.0) + 12.0;
+    double hw = 0.5 * (U - L);
+    double prev = NAN, s = 0.0;
+    for (double h = 0.125; h > 1e-5; h *= 0.5) {
+        s = 0.0;
+        int K = (int)ceil(4.5 / h);
+        for (int k = -K; k <= K; ++k) {
+            double t = k * h;
+            double y = 0.5 * M_PI * sinh(t);
+            double e = exp(-2.0 * fabs(y));
+            /* distance from the nearer end: w (1 - tanh|y|) = 2 w e / (1 + e) (no cancellation) */
+            double dnear = 2.0 * hw * e / (1.0 + e);
+            double u = (t < 0.0) ? L + dnear : U - dnear;
+            double ch = cosh(y);
+            double wgt = hw * 0.5 * M_PI * cosh(t) / (ch * ch);
+            if (!(wgt > 0.0) || !(u > 0.0)) continue;
+            s += wgt * pow(u, beta) * exp(-0.5 * (u - m) * (u - m));
+        }
+        s *= h / sqrt(2.0 * M_PI);
+        if (fabs(s - prev) <= 1e-15 * fabs(s)) break;
+        prev = s;
+    }
+    return pow(sigY, beta) * s;
+}
+
 /* Approximate normalization mass  sum_p |P_p| E[g_alpha(S^(p); tau)]          */
 /* (Eq. gaussian-threshold-main), S^(p) ~ N(mu_p, sigma_p^2),        */
 /* Y = a S - tau: muY = a mu - tau, sigY = a sigma.              */
@@ -555,12 +594,16 @@ double orc_gauss_mass(const float *mu, const float *sigma2, const int32_t *count
     double a = alpha - 1.0;
     double bd = 1.0 / a;
     int beta = (int)lround(bd);
-    /* the closed forms need an integer beta (App. D); any other alpha is rejected (NaN)  */
-    if (!(fabs(bd - (double)beta) <= 1e-12) || beta < 1) return NAN;
+    /* integer beta: App. D's closed forms; any other beta > 0: the numerical expectation  */
+    /* (orc_trunc_moment_num) -- never a rounded beta                   */
+    int closed = fabs(bd - (double)beta) <= 1e-12 && beta >= 1;
+    if (!(a > 0.0)) return NAN;
     double m = 0.0;
     for (int p = 0; p < M; ++p) {
         double s = sqrt((double)sigma2[p]);
-        m += (double)counts[p] * orc_trunc_moment(beta, a * (double)mu[p] - tau, a * s);
+        double muY = a * (double)mu[p] - tau, sigY = a * s;
+        m += (double)counts[p] * (closed ? orc_trunc_moment(beta, muY, sigY)
+                                         : orc_trunc_moment_num(bd, muY, sigY));
     }
     return m;
 }
@@ -569,12 +612,12 @@ double orc_gauss_mass(const float *mu, const float *sigma2, const int32_t *count
 /* non-increasing in tau and strictly decreasing where positive.       */
 /* Plain bracketing + bisection to fp64 resolution (the paper's Newton/Halley */
 /* is a faster route to the same root).  Returns 0 on success, -1 on a bracket */
-/* failure, -2 for a non-integer beta (no closed form; see orc_gauss_mass).    */
+/* failure, -2 for alpha <= 1.  Non-integer beta: the numerical expectation.    */
 int orc_gauss_tau(const float *mu, const float *sigma2, const int32_t *counts,
                   int M, double alpha, double *tau_hat)
 {
     double a = alpha - 1.0, top = -INFINITY;
-    if (isnan(orc_gauss_mass(mu, sigma2, counts, 0, alpha, 0.0))) return -2;   /* non-integer beta */
+    if (isnan(orc_gauss_mass(mu, sigma2, counts, 0, alpha, 0.0))) return -2;   /* alpha <= 1 */
     for (int p = 0; p < M; ++p) {
         double v = a * ((double)mu[p] + 8.0 * sqrt((double)sigma2[p]));
         if (v > top) top = v;

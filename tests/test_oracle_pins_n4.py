@@ -1,6 +1,10 @@
-"""Pins for SURVEY 8(f) N4 in the oracle: the certified conservative box selection of
+"""Pins for SURVEY 8(f) N4 in the oracle: (1) the certified conservative box selection of
 Prop. B.2, C_page = {p : (alpha-1) sbar_box(p) > tau_hat} for tau_hat <= tau, with
-tau_hat = the exact threshold of a first top-k pass (DESIGN R27; tau~ <= tau by R13).
+tau_hat = the exact threshold of a first top-k pass (DESIGN R27; tau~ <= tau by R13); (2) the
+Gaussian selector's truncated moment E[(Y)_+^beta] for non-integer beta, "evaluated
+numerically" (DESIGN R28), pinned against arbitrary-precision quadrature (mpmath),
+the parabolic-cylinder closed form (scipy), App. D's closed forms at integer beta and the
+point-mass limit.
 
 Citations: P:L = PAPER.md line L; R<n> = DESIGN.md reading n."""
 import numpy as np
@@ -70,3 +74,57 @@ def test_certified_with_too_high_tau_can_miss():
     assert t_bad > full["tau"]
     sel = set(oracle.box_certified(box, 1.5, t_bad).tolist())
     assert not sup_pages <= sel
+
+
+# ------------------------------------------------------------------ numerical truncated moment
+import math  # noqa: E402
+
+BETAS = [0.5, 1.0 / (float(np.float32(1.7)) - 1.0), 2.5, 0.75, 3.3, 6.5]
+POINTS = [(-3.0, 1.0), (-1.0, 0.5), (0.0, 1.0), (0.3, 2.0), (2.0, 1.0), (5.0, 0.7), (40.0, 1.5), (-8.0, 1.0)]
+
+
+@pytest.mark.parametrize("beta", BETAS)
+def test_trunc_moment_num_vs_mpmath(beta):
+    """E[(Y)_+^beta] = sigY^beta int_0^inf u^beta phi(u - muY/sigY) du, 40-digit mpmath quadrature
+    (split at the mode) as the reference: 1e-13 relative.  A dropped sigY^beta, a wrong
+    standardisation (m = muY sigY) or integrating from -inf fails."""
+    mpmath = pytest.importorskip("mpmath")
+    mpmath.mp.dps = 40
+    for muY, sig in POINTS:
+        m = mpmath.mpf(muY) / sig
+        ref = float(mpmath.mpf(sig) ** beta * mpmath.quad(lambda u: u ** beta * mpmath.npdf(u - m),
+                                                          [0, max(m, 0), max(m, 0) + 40]))
+        got = oracle.trunc_moment_num(beta, muY, sig)
+        assert abs(got - ref) <= 1e-13 * abs(ref), (beta, muY, sig, got, ref)
+
+
+@pytest.mark.parametrize("nu", [0.5, 1.4285714, 2.5])
+def test_trunc_moment_num_vs_parabolic_cylinder(nu):
+    """Closed form through the parabolic cylinder function D (a textbook identity):
+    int_0^inf u^nu phi(u - m) du = Gamma(nu+1) e^{-m^2/4} D_{-nu-1}(-m) / sqrt(2 pi)."""
+    sp = pytest.importorskip("scipy.special")
+    for m in (-3.0, -1.0, 0.0, 0.5, 2.0, 5.0):
+        ref = math.gamma(nu + 1) * math.exp(-m * m / 4) * sp.pbdv(-nu - 1, -m)[0] / math.sqrt(2 * math.pi)
+        got = oracle.trunc_moment_num(nu, m, 1.0)
+        assert abs(got - ref) <= 1e-12 * abs(ref), (nu, m, got, ref)
+
+
+@pytest.mark.parametrize("beta", [1, 2, 3, 4])
+def test_trunc_moment_num_matches_app_d_closed_forms(beta):
+    """At integer beta the quadrature reproduces App. D's closed forms (R15).  (Deep
+    in the lower tail the closed forms themselves cancel -- muY Phi + sigY phi with muY < 0 --
+    and lose up to ~1e-11 relative at m = -3 (beta = 4) and more at m = -8; the quadrature
+    matches 40-digit mpmath there, above.  So: 1e-13 for m >= 0, 2e-11 for -5 < m < 0.)"""
+    for muY, sig in [x for x in POINTS if x[0] / x[1] > -5]:
+        ref = oracle.trunc_moment(beta, muY, sig)
+        got = oracle.trunc_moment_num(float(beta), muY, sig)
+        tol = 1e-13 if muY >= 0 else 2e-11
+        assert abs(got - ref) <= tol * max(abs(ref), 1e-300), (beta, muY, sig, got, ref)
+
+
+def test_trunc_moment_num_point_mass_limit():
+    """sigY -> 0: E[(Y)_+^beta] -> [muY]_+^beta; sigY = 0 is the point mass itself."""
+    b = BETAS[1]
+    assert oracle.trunc_moment_num(b, 1.3, 0.0) == 1.3 ** b
+    assert oracle.trunc_moment_num(b, -0.2, 0.0) == 0.0
+    assert abs(oracle.trunc_moment_num(b, 1.3, 1e-4) - 1.3 ** b) <= 1e-6

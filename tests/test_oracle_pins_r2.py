@@ -54,16 +54,27 @@ def test_gauss_select_empty_fallback_ties():
     assert sel.tolist() == [1]
 
 
-def test_gauss_mass_rejects_non_integer_beta():
+def test_gauss_mass_non_integer_beta_is_numerical():
     """App. D's closed forms need an integer beta; alpha = 1.7 (beta = 1.4286) must not be
-    silently rounded: NaN mass, ValueError for tau_hat."""
+    silently rounded.  Since N4 (DESIGN R28) the oracle evaluates the
+    expectation numerically instead: the mass is the counts-weighted sum of the numerical
+    truncated moments (pinned against mpmath in test_oracle_pins_n4.py), not the beta = 1
+    (rounded) closed form, and tau_hat is its root."""
     mu = np.array([0.5, 1.0], np.float32)
     s2 = np.array([0.1, 0.2], np.float32)
     cnt = np.array([16, 16], np.int32)
-    assert math.isnan(oracle.gauss_mass(mu, s2, cnt, 1.7, 0.0))
-    with pytest.raises(ValueError):
-        oracle.gauss_tau(mu, s2, cnt, 1.7)
+    a = float(np.float32(1.7)) - 1.0
+    beta = 1.0 / a
+    want = sum(16 * oracle.trunc_moment_num(beta, a * float(m), a * math.sqrt(float(v))) for m, v in zip(mu, s2))
+    got = oracle.gauss_mass(mu, s2, cnt, float(np.float32(1.7)), 0.0)
+    assert abs(got - want) <= 1e-14 * want
+    rounded = sum(16 * oracle.trunc_moment(1, a * float(m), a * math.sqrt(float(v))) for m, v in zip(mu, s2))
+    assert abs(got - rounded) > 1e-3 * want                     # not the rounded beta
+    t = oracle.gauss_tau(mu, s2, cnt, float(np.float32(1.7)))
+    assert abs(oracle.gauss_mass(mu, s2, cnt, float(np.float32(1.7)), t) - 1.0) < 1e-12
     assert not math.isnan(oracle.gauss_mass(mu, s2, cnt, 1.5, 0.0))
+    with pytest.raises(ValueError):
+        oracle.gauss_tau(mu, s2, cnt, 1.0)                      # alpha <= 1
 
 
 # ------------------------------------------------------------------ certified delta_bar
