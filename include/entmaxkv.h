@@ -113,8 +113,12 @@ typedef struct {
 /*
  * policy TOPK: k_pages >= 1 pages per query head (R3 tie-break).
  * policy GAUSS: q_page in (0,1) page-max confidence, margin = Delta >= 0
- *   (Eq. gaussian-selector-main); needs integer beta = 1/(alpha-1) in
- *   {1,2,3,4} (App. D, R15), else EKV_ERR_UNSUPPORTED.
+ *   (Eq. gaussian-selector-main).  beta = 1/(alpha-1) in {1,2,3,4}: App. D's closed
+ *   forms (R15); any other beta <= 32 (alpha > 1 + 1/32): the expectation evaluated numerically
+ *   (DESIGN R28) -- a per-call table of log E[(m + Z)_+^beta]
+ *   (Chebyshev series from tanh-sinh quadrature, one extra launch) in the workspace, so
+ *   entmaxkv_select then needs a workspace.  Rows longer than 8192 pages run on a cluster of
+ *   CTAs.  Else EKV_ERR_UNSUPPORTED.
  * policy ALL: every page (the full cache).
  * policy CERTIFIED (Prop. B.2 "no false negatives from deterministic page
  *   bounds"): entmaxkv_decode only.  A first top-k pass (k_pages) gives the exact

@@ -291,15 +291,20 @@ def score_pages(cache: PagedCache, q, modes=EKV_SCORE_BOX, stream=None):
 
 
 def select(cache: PagedCache, n_q_heads, sel: ekv_select_params, alpha=1.5, box=None, mu=None, sigma2=None,
-           stream=None):
+           stream=None, workspace=None):
+    """workspace: needed by the Gaussian selector for a non-integer beta (its moment table);
+    allocated here when None."""
     cap = select_capacity(cache, sel)
+    if workspace is None and sel.policy == EKV_GAUSS:
+        workspace = alloc_workspace(cache, n_q_heads, sel)
     dev = cache.K.device
     page_idx = torch.full((cache.batch, n_q_heads, cap), -1, dtype=torch.int32, device=dev)
     n_sel = torch.zeros(cache.batch, n_q_heads, dtype=torch.int32, device=dev)
     tau_hat = torch.zeros(cache.batch, n_q_heads, dtype=torch.float64, device=dev)
     cs = cache.c_struct()
     _check(lib().entmaxkv_select(ctypes.byref(cs), int(n_q_heads), _ptr(box), _ptr(mu), _ptr(sigma2), ctypes.byref(sel),
-                                 float(alpha), _ptr(page_idx), _ptr(n_sel), cap, _ptr(tau_hat), None, _stream(stream)))
+                                 float(alpha), _ptr(page_idx), _ptr(n_sel), cap, _ptr(tau_hat), _ptr(workspace),
+                                 _stream(stream)))
     return page_idx, n_sel, tau_hat
 
 

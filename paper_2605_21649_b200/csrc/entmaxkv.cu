@@ -159,11 +159,11 @@ ekv_status check_sel(const ekv_select_params *s, float alpha) {
     } else if (s->policy == EKV_GAUSS) {
         if (!(s->q_page > 0.0 && s->q_page < 1.0)) return fail(EKV_ERR_INVALID_ARG, "q_page must be in (0,1)");
         if (!(s->margin >= 0.0)) return fail(EKV_ERR_INVALID_ARG, "margin must be >= 0");
+        // integer beta in 1..4: App. D's closed forms; any other beta <= 32: the numerical
+        // expectation (N4)
         const double beta = 1.0 / ((double)alpha - 1.0);
-        const double rb = (double)(long long)(beta + 0.5);
-        if (!(alpha > 1.0f) || fabs(beta - rb) > 1e-9 || rb < 1 || rb > 4)
-            return fail(EKV_ERR_UNSUPPORTED, "Gaussian selector needs integer beta=1/(alpha-1) in {1,2,3,4} (alpha=%g)",
-                        (double)alpha);
+        if (!(alpha > 1.0f) || !(beta <= 32.0))
+            return fail(EKV_ERR_UNSUPPORTED, "Gaussian selector needs alpha > 1 + 1/32 (alpha=%g)", (double)alpha);
     } else if (s->policy == EKV_CERTIFIED) {
         if (s->k_pages < 1) return fail(EKV_ERR_INVALID_ARG, "k_pages (first pass) must be >= 1");
     } else if (s->policy != EKV_ALL) {
@@ -203,6 +203,7 @@ Layout layout(const ekv_cache *c, int Hq, const ekv_select_params *sel) {
     L.page_idx = take(B * Hq * maxp * 4);          // capacity max_pages: also serves the eval pass
     L.n_sel = take(B * Hq * 4);
     L.tau_hat = take(B * Hq * 8);
+    L.gtab = take(64 * 48 * 8);           // non-integer-beta moment table (N4)
     L.zero = o;
     L.status = take(16);
     L.retry = take(B * Hq * 4);
@@ -467,7 +468,8 @@ ekv_status entmaxkv_select(const ekv_cache *cache, int32_t n_q_heads, const floa
                            sel_stride, n_q_heads / cache->n_kv_heads, UnionOut{nullptr, 0}, st);
     }
     if (!mu || !sigma2) return fail(EKV_ERR_INVALID_ARG, "Gaussian selector needs mu/sigma2");
-    return launch_gauss(cache, n_q_heads, mu, sigma2, alpha, sel, page_idx, n_sel, sel_stride, tau_hat, st);
+    double *gtab = workspace ? at<double>(workspace, layout(cache, n_q_heads, sel).gtab) : nullptr;
+    return launch_gauss(cache, n_q_heads, mu, sigma2, alpha, sel, page_idx, n_sel, sel_stride, tau_hat, gtab, st);
 }
 
 ekv_status entmaxkv_sparse_attend(const ekv_cache *cache, const void *q, int32_t n_q_heads, const int32_t *page_idx,
@@ -541,7 +543,7 @@ ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_he
         const int k = sel->policy == EKV_ALL ? maxp : sel->k_pages;
         EKV_TRY(launch_topk(box, cache->batch, n_q_heads, maxp, cache->seq_lens, k, pi, ns, L.cap, Gq, uo, st));
     } else {
-        EKV_TRY(launch_gauss(cache, n_q_heads, mu, s2, attn->alpha, sel, pi, ns, L.cap, th, st));
+        EKV_TRY(launch_gauss(cache, n_q_heads, mu, s2, attn->alpha, sel, pi, ns, L.cap, th, at<double>(workspace, L.gtab), st));
         EKV_TRY(launch_mark(cache->batch, n_q_heads, Gq, pi, ns, L.cap, uo.umask, L.W, st));
     }
     // a3

@@ -83,7 +83,7 @@ CacheView view(const ekv_cache *c);
 // ---------------------------------------------------------------- workspace layout
 // One layout serves decode (incl. eval_exact), select, sparse_attend and full_attend.
 struct Layout {
-    size_t box, mu, sigma2, page_idx, n_sel, tau_hat;
+    size_t box, mu, sigma2, page_idx, n_sel, tau_hat, gtab;
     size_t zero, status, retry, rowmax, ccount, umask, zero_bytes;   // zeroed per step / attention pass
     size_t tau_int, smx_acc, smx_l, smx_cnt, sink;
     int smx_nch;
@@ -111,7 +111,8 @@ ekv_status launch_box_certified(const float *box, int B, int Hq, int G, int maxp
 ekv_status launch_mark(int B, int Hq, int G, const int32_t *pi, const int32_t *ns, int stride, uint32_t *um, int W,
                        cudaStream_t st);
 ekv_status launch_gauss(const ekv_cache *cache, int Hq, const float *mu, const float *s2, float alpha,
-                        const ekv_select_params *sel, int32_t *pi, int32_t *ns, int stride, double *th, cudaStream_t st);
+                        const ekv_select_params *sel, int32_t *pi, int32_t *ns, int stride, double *th, double *gtab,
+                        cudaStream_t st);
 
 // ---------------------------------------------------------------- launch_attend.cu
 ekv_status launch_scores(const CacheView &v, const void *q, int Hq, const uint32_t *um, int W, const int32_t *pi,

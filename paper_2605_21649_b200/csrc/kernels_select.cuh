@@ -725,6 +725,113 @@ __device__ __forceinline__ GaussMoments trunc_moments(int beta, double muY, doub
     return {cur, prev, pp};
 }
 
+// ---------------------------------------------------------------- non-integer beta (N4, R28)
+// E[(Y)_+^beta] = sigY^beta h(m), m = muY / sigY, h(m) = int_0^inf u^beta phi(u - m) du ("the
+// expectation can be evaluated numerically").  Per call, k_gauss_table fills a table
+// of g = log h on [-10, 22) -- 64 intervals of width 1/2, a degree-15 Chebyshev series each,
+// from tanh-sinh quadrature at the Chebyshev nodes -- plus the series of g' and g''; pages
+// then get h = e^g, h' = g' h (= beta h_{beta-1}), h'' = (g'' + g'^2) h (= beta (beta-1)
+// h_{beta-2}) from three Clenshaw sums.  m < -10: 0 (such pages are skipped, t < -9.5);
+// m >= 22: the asymptotic series E[(m + Z)^b] = m^b sum_k C(b, 2k) (2k-1)!! m^-2k.
+constexpr int kGtN = 16, kGtI = 64, kGtStride = 48;
+constexpr double kGtLo = -10.0, kGtW = 0.5;
+__device__ double gt_quad(double beta, double m) {
+    const double L = fmax(0.0, m - 12.0), U = fmax(m, 0.0) + 12.0, hw = 0.5 * (U - L);
+    double prev = NAN, s = 0.0;
+    for (double h = 0.125; h > 0.0009; h *= 0.5) {
+        s = 0.0;
+        const int K = (int)ceil(4.5 / h);
+        for (int k = -K; k <= K; ++k) {
+            const double t = k * h, y = 1.5707963267948966 * sinh(t);
+            const double e = exp(-2.0 * fabs(y));
+            const double dn = 2.0 * hw * e / (1.0 + e);
+            const double u = t < 0.0 ? L + dn : U - dn;
+            const double ch = cosh(y);
+            const double w = hw * 1.5707963267948966 * cosh(t) / (ch * ch);
+            if (!(w > 0.0) || !(u > 0.0)) continue;
+            s += w * pow(u, beta) * exp(-0.5 * (u - m) * (u - m));
+        }
+        s *= h * 0.39894228040143267794;
+        if (fabs(s - prev) <= 1e-13 * fabs(s)) break;   // (the DE rule's error ~squares per halving)
+        prev = s;
+    }
+    return s;
+}
+// one CTA per interval, kGtN threads (one Chebyshev node each)
+static __global__ void __launch_bounds__(kGtN) k_gauss_table(double beta, double *__restrict__ tab) {
+    pdl_enter();
+    __shared__ double gv[kGtN], cf[kGtN];
+    const int iv = blockIdx.x, j = threadIdx.x;
+    const double a0 = kGtLo + kGtW * iv, c = a0 + 0.5 * kGtW, r = 0.5 * kGtW;
+    const double x = cos(3.141592653589793 * (j + 0.5) / kGtN);
+    gv[j] = log(gt_quad(beta, c + r * x));
+    __syncthreads();
+    double sum = 0.0;
+    for (int k = 0; k < kGtN; ++k) sum += gv[k] * cos(3.141592653589793 * j * (k + 0.5) / kGtN);
+    cf[j] = sum * (2.0 / kGtN);
+    __syncthreads();
+    if (j == 0) {
+        // derivative series (Chebyshev recurrence), scaled by 1 / r per derivative
+        double *t = tab + (size_t)iv * kGtStride;
+        double d1[kGtN], d2[kGtN];
+        for (int k = 0; k < kGtN; ++k) t[k] = cf[k];
+        d1[kGtN - 1] = 0.0;
+        d1[kGtN - 2] = 2.0 * (kGtN - 1) * cf[kGtN - 1];
+        for (int k = kGtN - 3; k >= 0; --k) d1[k] = d1[k + 2] + 2.0 * (k + 1) * cf[k + 1];
+        d2[kGtN - 1] = 0.0;
+        d2[kGtN - 2] = 2.0 * (kGtN - 1) * d1[kGtN - 1];
+        for (int k = kGtN - 3; k >= 0; --k) d2[k] = d2[k + 2] + 2.0 * (k + 1) * d1[k + 1];
+        for (int k = 0; k < kGtN; ++k) { t[kGtN + k] = d1[k] / r; t[2 * kGtN + k] = d2[k] / (r * r); }
+    }
+}
+// Chebyshev sum sum_k c_k T_k(y) - c_0 / 2 (Clenshaw)
+__device__ __forceinline__ double gt_cheb(const double *c, double y) {
+    double b1 = 0.0, b2 = 0.0;
+    for (int k = kGtN - 1; k >= 1; --k) { const double t = 2.0 * y * b1 - b2 + __ldg(c + k); b2 = b1; b1 = t; }
+    return y * b1 - b2 + 0.5 * __ldg(c);
+}
+// E[(m + Z)_+^b] for large m (asymptotic series; the cut lower tail is below phi(22))
+__device__ __forceinline__ double gt_asym(double b, double m) {
+    double term = 1.0, s = 1.0;
+    const double im2 = 1.0 / (m * m);
+    for (int k = 0; k < 40; ++k) {
+        term *= (b - 2 * k) * (b - 2 * k - 1) * im2 / (2.0 * (k + 1));   // C(b,2k+2)(2k+1)!!/(C(b,2k)(2k-1)!!)
+        s += term;
+        if (fabs(term) <= 1e-17 * fabs(s)) break;
+    }
+    return pow(m, b) * s;
+}
+// h, h', h'' at m (h' = dh/dm, h'' = d2h/dm2)
+__device__ __forceinline__ void gt_eval(const double *tab, double beta, double m, double &h, double &h1, double &h2) {
+    if (m < kGtLo) { h = h1 = h2 = 0.0; return; }
+    if (m >= kGtLo + kGtI * kGtW) {
+        h = gt_asym(beta, m);
+        h1 = beta * gt_asym(beta - 1.0, m);
+        h2 = beta * (beta - 1.0) * gt_asym(beta - 2.0, m);
+        return;
+    }
+    const int iv = min(kGtI - 1, (int)((m - kGtLo) / kGtW));
+    const double c = kGtLo + kGtW * iv + 0.5 * kGtW;
+    const double y = (m - c) / (0.5 * kGtW);
+    const double *t = tab + (size_t)iv * kGtStride;
+    const double g = gt_cheb(t, y), g1 = gt_cheb(t + kGtN, y), g2 = gt_cheb(t + 2 * kGtN, y);
+    h = exp(g);
+    h1 = g1 * h;
+    h2 = (g2 + g1 * g1) * h;
+}
+// the moments of trunc_moments for a non-integer beta, already multiplied as the mass needs:
+// m = E[Y_+^b], dm = -dE/dtau = b E[Y_+^(b-1)], d2 = d2E/dtau2 = b (b-1) E[Y_+^(b-2)]
+__device__ __forceinline__ GaussMoments trunc_moments_tab(const double *tab, double beta, double muY, double sigY) {
+    if (!(sigY > 0.0)) {
+        if (!(muY > 0.0)) return {0.0, 0.0, 0.0};
+        return {pow(muY, beta), beta * pow(muY, beta - 1.0), beta * (beta - 1.0) * pow(muY, beta - 2.0)};
+    }
+    double h, h1, h2;
+    gt_eval(tab, beta, muY / sigY, h, h1, h2);
+    const double sb = pow(sigY, beta);
+    return {sb * h, sb / sigY * h1, sb / (sigY * sigY) * h2};
+}
+
 template <int NT> __device__ __forceinline__ void block_sum3_d(double &a, double &b, double &c, double *sh) {
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
@@ -788,7 +895,8 @@ __device__ __forceinline__ void gauss_cluster_sum(GaussRed &R, double *v, int n)
 // fp32 steering pass: mass(tau) and -d mass/d tau, fp32 terms and per-thread sums
 template <int NT>
 __device__ void gauss_mass32(const float *mu, const float *sg, const float *s2, int p0, int p1, int Lseq, float af,
-                             int beta, float tf, double &mass, double &dmass, double *shd, GaussRed &R) {
+                             int beta, float tf, double &mass, double &dmass, double *shd, GaussRed &R,
+                             const double *gtab, double betaf) {
     float m = 0.f, dm = 0.f;
 #pragma unroll 4
     for (int p = p0 + threadIdx.x; p < p1; p += NT) {
@@ -798,7 +906,10 @@ __device__ void gauss_mass32(const float *mu, const float *sg, const float *s2, 
         if (EKV_GAUSS_SKIP(num, den)) continue;
         const float cnt = (float)min(kP, Lseq - p * kP);
         float r, rm;
-        if (!(den > 0.f)) {
+        if (beta == 0) {                          // non-integer beta: the table (fp64 terms)
+            const GaussMoments g = trunc_moments_tab(gtab, betaf, (double)num, (double)den);
+            r = (float)g.m; rm = (float)g.dm;
+        } else if (!(den > 0.f)) {
             r = 1.f; rm = 1.f;
             for (int i2 = 0; i2 < beta; ++i2) { rm = r; r *= num; }
         } else {
@@ -815,7 +926,7 @@ __device__ void gauss_mass32(const float *mu, const float *sg, const float *s2, 
         m = fmaf(cnt, r, m);
         dm = fmaf(cnt, rm, dm);
     }
-    double a = m, b = (double)beta * dm;
+    double a = m, b = beta == 0 ? (double)dm : (double)beta * dm;
     block_sum2_d<NT>(a, b, shd);
     double v[3] = {a, b, 0.0};
     gauss_cluster_sum(R, v, 2);
@@ -826,7 +937,7 @@ __device__ void gauss_mass32(const float *mu, const float *sg, const float *s2, 
 template <int NT>
 __device__ void gauss_mass64(const float *mu, const float *sg, const float *s2, int p0, int p1, int Lseq, float af,
                              int beta, double tau, double &mass, double &dmass, double &d2mass, double *shd,
-                             GaussRed &R) {
+                             GaussRed &R, const double *gtab, double betaf) {
     double m = 0.0, dm = 0.0, d2 = 0.0;
     const float tf = (float)tau;
     const double a = (double)af;
@@ -836,13 +947,16 @@ __device__ void gauss_mass64(const float *mu, const float *sg, const float *s2, 
         const float num = af * mp - tf, den = af * sp;
         if (EKV_GAUSS_SKIP(num, den)) continue;
         const double cnt = (double)min(kP, Lseq - p * kP);
-        const GaussMoments g = trunc_moments(beta, a * (double)mp - tau, a * sqrt((double)s2p));
+        const GaussMoments g = beta == 0 ? trunc_moments_tab(gtab, betaf, a * (double)mp - tau, a * sqrt((double)s2p))
+                                         : trunc_moments(beta, a * (double)mp - tau, a * sqrt((double)s2p));
         m = fma(cnt, g.m, m);
         dm = fma(cnt, g.dm, dm);
         d2 = fma(cnt, g.d2, d2);
     }
-    dm *= (double)beta;
-    d2 *= beta == 1 ? 1.0 : (double)(beta * (beta - 1));
+    if (beta > 0) {                               // (the table path returns them multiplied)
+        dm *= (double)beta;
+        d2 *= beta == 1 ? 1.0 : (double)(beta * (beta - 1));
+    }
     block_sum3_d<NT>(m, dm, d2, shd);
     double v[3] = {m, dm, d2};
     gauss_cluster_sum(R, v, 3);
@@ -865,7 +979,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gauss_select(const float *__r
                                                      int Hq, int maxp, const int32_t *__restrict__ seq_lens,
                                                      float alpha, double margin, double q_page,
                                                      int32_t *__restrict__ page_idx, int32_t *__restrict__ n_sel,
-                                                     int sel_stride, double *__restrict__ tau_hat_out, int cache_pages) {
+                                                     int sel_stride, double *__restrict__ tau_hat_out, int cache_pages,
+                                                     const double *__restrict__ gtab) {
     EKV_TRACE(8);
     pdl_enter();
     ph_stamp<8>(0);
@@ -896,7 +1011,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gauss_select(const float *__r
     float *c_mu = gsm, *c_s2 = gsm + cache_pages, *c_sg = gsm + 2 * cache_pages;
     const double a = (double)alpha - 1.0;
     const float af = (float)a;
-    const int beta = (int)llrint(1.0 / a);
+    // integer beta in 1..4: App. D's closed forms (R15); any other beta: the table (N4, R28)
+    const double betaf = 1.0 / a;
+    const int beta = (fabs(betaf - rint(betaf)) < 1e-9 && rint(betaf) >= 1.0 && rint(betaf) <= 4.0) ? (int)rint(betaf) : 0;
     // stage the slice (and the bracket start a max_p (mu + 8 sigma))
     float tmax = -INFINITY;
     for (int i = threadIdx.x; i < p1 - p0; i += NT) {
@@ -923,7 +1040,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gauss_select(const float *__r
     // bisection once bracketed when a step leaves the bracket, doubling steps while a side
     // is still open
     double lo = -INFINITY, hi = INFINITY, tau = a * (double)tmax, w = 1.0, dxold = INFINITY, mass, dmass, d2mass;
-    gauss_mass32<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, (float)tau, mass, dmass, shd, R);
+    gauss_mass32<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, (float)tau, mass, dmass, shd, R, gtab, betaf);
     ++n32;
     for (int it = 0; it < 80; ++it) {
         if (mass >= 1.0) lo = tau; else hi = tau;
@@ -946,7 +1063,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gauss_select(const float *__r
         dxold = fabs(nt - tau);
         tau = nt;
         if (stop) break;
-        gauss_mass32<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, (float)tau, mass, dmass, shd, R);
+        gauss_mass32<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, (float)tau, mass, dmass, shd, R, gtab, betaf);
         ++n32;
     }
     ph_stamp<8>(2);
@@ -955,7 +1072,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gauss_select(const float *__r
     {
         double t = tau;
         for (int it = 0; it < 4; ++it) {
-            gauss_mass64<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, t, mass, dmass, d2mass, shd, R);
+            gauss_mass64<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, t, mass, dmass, d2mass, shd, R, gtab, betaf);
             ++n64;
             if (!(dmass > 0.0)) break;
             const double f = mass - 1.0;
@@ -979,20 +1096,20 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gauss_select(const float *__r
     if (!done64) {
     lo = tau - dl;
     for (int it = 0; it < 200; ++it) {
-        gauss_mass64<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, lo, mass, dmass, d2mass, shd, R);
+        gauss_mass64<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, lo, mass, dmass, d2mass, shd, R, gtab, betaf);
         if (mass >= 1.0) break;
         dl *= 4.0; lo = tau - dl;
     }
     double dh = 1e-4 * fmax(1.0, fabs(tau));
     hi = tau + dh;
     for (int it = 0; it < 200; ++it) {
-        gauss_mass64<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, hi, mass, dmass, d2mass, shd, R);
+        gauss_mass64<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, hi, mass, dmass, d2mass, shd, R, gtab, betaf);
         if (mass < 1.0) break;
         dh *= 4.0; hi = tau + dh;
     }
     tau = fmin(fmax(tau, lo), hi);
     for (int it = 0; it < 100; ++it) {
-        gauss_mass64<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, tau, mass, dmass, d2mass, shd, R);
+        gauss_mass64<NT>(m_, g_, s_, p0, p1, Lseq, af, beta, tau, mass, dmass, d2mass, shd, R, gtab, betaf);
         if (mass >= 1.0) lo = tau; else hi = tau;
         double nt = (dmass > 0.0) ? tau + (mass - 1.0) / dmass : 0.5 * (lo + hi);
         if (!(nt > lo && nt < hi)) nt = 0.5 * (lo + hi);

@@ -1,5 +1,6 @@
 // launch_select.cu -- launches of the a2 (top-k), a2' (Gaussian selector) and union-mark kernels.
 #include <algorithm>
+#include <cmath>
 #include "host.h"
 #include "kernels_select.cuh"
 
@@ -46,19 +47,28 @@ ekv_status launch_box_certified(const float *box, int B, int Hq, int G, int maxp
 template <int NT>
 static ekv_status launch_gauss_nt(const ekv_cache *cache, int Hq, const float *mu, const float *s2, float alpha,
                                   const ekv_select_params *sel, int32_t *pi, int32_t *ns, int stride, double *th,
-                                  int CL, cudaStream_t st) {
+                                  const double *gtab, int CL, cudaStream_t st) {
     const int maxp = cache->max_pages_per_seq;
     const int cache_pages = std::min((maxp + CL - 1) / CL, 8192);
     const int smem = 12 * cache_pages;
     set_smem(k_gauss_select<NT>, 12 * 8192);
     cudaError_t e = launch_ex(k_gauss_select<NT>, dim3((unsigned)(cache->batch * Hq * CL)), dim3(NT), smem, st,
                               (unsigned)(CL > 1 ? CL : 0), mu, s2, Hq, maxp, (const int32_t *)cache->seq_lens, alpha,
-                              sel->margin, sel->q_page, pi, ns, stride, th, cache_pages);
+                              sel->margin, sel->q_page, pi, ns, stride, th, cache_pages, gtab);
     if (e != cudaSuccess) return fail(EKV_ERR_CUDA, "k_gauss_select: %s", cudaGetErrorString(e));
     return check_launch("k_gauss_select");
 }
 ekv_status launch_gauss(const ekv_cache *cache, int Hq, const float *mu, const float *s2, float alpha,
-                        const ekv_select_params *sel, int32_t *pi, int32_t *ns, int stride, double *th, cudaStream_t st) {
+                        const ekv_select_params *sel, int32_t *pi, int32_t *ns, int stride, double *th, double *gtab,
+                        cudaStream_t st) {
+    // non-integer beta (or beta > 4): the per-call moment table first (N4, R28)
+    const double bf = 1.0 / ((double)alpha - 1.0);
+    const bool closed = std::fabs(bf - std::rint(bf)) < 1e-9 && std::rint(bf) >= 1.0 && std::rint(bf) <= 4.0;
+    if (!closed) {
+        if (!gtab) return fail(EKV_ERR_INVALID_ARG, "non-integer beta: the Gaussian selector needs the workspace");
+        launch_ex(k_gauss_table, dim3(kGtI), dim3(kGtN), 0, st, 0u, bf, gtab);
+        EKV_TRY(check_launch("k_gauss_table"));
+    }
     // rows longer than the 8192-page shared-memory stage are split over a cluster of CL CTAs
     // (C4: 65536 pages -> 8 CTAs per row, each row's slices staged in shared memory).  The
     // block size and CL (and so the fp64 reduction order of tau_hat) depend on the shape:
@@ -67,8 +77,8 @@ ekv_status launch_gauss(const ekv_cache *cache, int Hq, const float *mu, const f
     while (CL < 8 && (cache->max_pages_per_seq + CL - 1) / CL > 8192) CL *= 2;
     const long long ctas = (long long)cache->batch * Hq * CL;
     if (ctas > num_sms())
-        return launch_gauss_nt<512>(cache, Hq, mu, s2, alpha, sel, pi, ns, stride, th, CL, st);
-    return launch_gauss_nt<1024>(cache, Hq, mu, s2, alpha, sel, pi, ns, stride, th, CL, st);
+        return launch_gauss_nt<512>(cache, Hq, mu, s2, alpha, sel, pi, ns, stride, th, gtab, CL, st);
+    return launch_gauss_nt<1024>(cache, Hq, mu, s2, alpha, sel, pi, ns, stride, th, gtab, CL, st);
 }
 
 }  // namespace ekvh

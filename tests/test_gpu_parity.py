@@ -352,6 +352,37 @@ def test_gaussian_select(case, alpha):
             assert pi[b, h, :ns[b, h]].tolist() == ref.tolist()
 
 
+@pytest.mark.parametrize("alpha", [1.7, 1.4, 2.5, 1.2])
+def test_gaussian_select_non_integer_beta(alpha):
+    """N4 (DESIGN R28): beta = 1/(alpha-1) not in {1,2,3,4} -- the GPU's per-call table of
+    log E[(m+Z)_+^beta] (Chebyshev series from tanh-sinh quadrature) against the oracle's direct
+    quadrature: tau_hat within 1e-10 relative, page set at tau_hat_gpu bit-exact; plus the C4
+    row length (65536 pages, cluster-split rows) on a head subsample."""
+    alpha = float(np.float32(alpha))
+    for (B, sl, Hq, Hkv), seed in [((2, [3000, 1777], 8, 2), 31), ((1, (1 << 20) - 77, 4, 1), 32)]:
+        wl, dc, hc = make_pair(B, sl, Hq, Hkv, seed=seed, kind="planted")
+        G = Hq // Hkv
+        qh = q_host(wl)
+        _, mu, s2 = ekv.score_pages(dc, wl.q.cuda(), modes=2)
+        sel = ekv.select_params("gauss", q_page=0.99, margin=0.0)
+        pi, ns, th = ekv.select(dc, Hq, sel, alpha=alpha, mu=mu, sigma2=s2)
+        torch.cuda.synchronize()
+        pi, ns, th = pi.cpu().numpy(), ns.cpu().numpy(), th.cpu().numpy()
+        zq = oracle.zq_table(0.99, 16)
+        rows = [(b, h) for b in range(B) for h in range(Hq)][: (2 if B == 1 else None)]
+        for b, h in rows:
+            counts = hc.page_counts(b)
+            _, om, os2 = hc.score_pages(qh[b, h], b, h // G, modes=2)
+            if B > 1:
+                t_ref = oracle.gauss_tau(om, os2, counts, alpha)
+                assert abs(th[b, h] - t_ref) <= 1e-10 * max(1.0, abs(t_ref)), (b, h, th[b, h], t_ref)
+            else:
+                # long row: the oracle's quadrature mass (one evaluation per page) AT tau_hat_gpu
+                assert abs(oracle.gauss_mass(om, os2, counts, alpha, th[b, h]) - 1.0) <= 1e-9, (b, h)
+            ref = oracle.gauss_select(om, os2, counts, alpha, th[b, h], 0.0, zq)
+            assert pi[b, h, :ns[b, h]].tolist() == ref.tolist()
+
+
 def test_gaussian_select_uncached_long_row():
     """Rows longer than the selector's 8192-page shared-memory stage read mu / sigma2 from
     global memory (140000 tokens = 8750 pages)."""
