@@ -463,8 +463,10 @@ def test_errors_fail_loudly():
     with pytest.raises(ekv.EkvError):
         ekv.select(dc, 4, ekv.select_params("topk", 0), box=torch.zeros(1, 4, dc.max_pages, device="cuda"))
     box, mu, s2 = ekv.score_pages(dc, wl.q.cuda(), modes=3)
+    with pytest.raises(ekv.EkvError):                                  # beta > 32 (N4 covers beta <= 32)
+        ekv.select(dc, 4, ekv.select_params("gauss"), alpha=1.01, mu=mu, sigma2=s2)
     with pytest.raises(ekv.EkvError):
-        ekv.select(dc, 4, ekv.select_params("gauss"), alpha=1.7, mu=mu, sigma2=s2)   # non-integer beta
+        ekv.select(dc, 4, ekv.select_params("gauss", q_page=1.5), alpha=1.5, mu=mu, sigma2=s2)   # q_page
 
 
 @pytest.mark.parametrize("alpha", [1.5, 2.0, 1.25])
