@@ -1,6 +1,7 @@
 // entmaxkv.cu -- the C ABI of libentmaxkv.so (include/entmaxkv.h): argument validation,
 // workspace carve-out and the orchestration of the kernel launches (launch_*.cu) on the
 // caller's stream; no allocation, no synchronisation.
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdarg.h>
@@ -24,6 +25,9 @@ namespace {
 thread_local char g_err[512] = "";
 thread_local int g_launches = 0;
 }  // namespace
+
+NvtxRange::NvtxRange(const char *name) { nvtxRangePushA(name); }
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
 
 void begin_call() {
     g_err[0] = 0;
@@ -389,7 +393,7 @@ int entmaxkv_debug_stamps(unsigned long long *out /*[8*32]*/, int *nc) {
 
 ekv_status entmaxkv_workspace_status(const ekv_cache *cache, int32_t n_q_heads, const ekv_select_params *sel,
                                      const void *workspace, int32_t *flags, void *stream) {
-    begin_call();
+    EKV_CALL("entmaxkv_workspace_status");
     EKV_TRY(check_cache(cache, n_q_heads));
     if (!workspace || !flags) return fail(EKV_ERR_INVALID_ARG, "NULL argument");
     const Layout L = layout(cache, n_q_heads, sel);
@@ -418,7 +422,7 @@ int32_t entmaxkv_select_capacity(const ekv_cache *cache, const ekv_select_params
 
 ekv_status entmaxkv_append_kv(const ekv_cache *cache, const void *k_new, const void *v_new, int32_t n_tokens,
                               void *stream) {
-    begin_call();
+    EKV_CALL("entmaxkv_append_kv");
     EKV_TRY(check_cache(cache, 0));
     if (!k_new || !v_new || n_tokens < 1) return fail(EKV_ERR_INVALID_ARG, "append: bad k/v or n_tokens");
     if (!cache->kmin || !cache->kmax || !cache->ksum || !cache->ksumsq || !cache->kavg || !cache->kvar)
@@ -427,7 +431,7 @@ ekv_status entmaxkv_append_kv(const ekv_cache *cache, const void *k_new, const v
 }
 
 ekv_status entmaxkv_rebuild_page_stats(const ekv_cache *cache, void *stream) {
-    begin_call();
+    EKV_CALL("entmaxkv_rebuild_page_stats");
     EKV_TRY(check_cache(cache, 0));
     if (!cache->kmin || !cache->kmax || !cache->ksum || !cache->ksumsq || !cache->kavg || !cache->kvar)
         return fail(EKV_ERR_INVALID_ARG, "rebuild: metadata buffers NULL");
@@ -437,7 +441,7 @@ ekv_status entmaxkv_rebuild_page_stats(const ekv_cache *cache, void *stream) {
 ekv_status entmaxkv_score_pages(const ekv_cache *cache, const void *q, int32_t n_q_heads, int32_t modes, float *box,
                                 float *mu, float *sigma2, void *workspace, void *stream) {
     (void)workspace;
-    begin_call();
+    EKV_CALL("entmaxkv_score_pages");
     EKV_TRY(check_cache(cache, n_q_heads));
     EKV_TRY(check_q(q));
     if (modes < 1 || modes > 3) return fail(EKV_ERR_INVALID_ARG, "modes must be 1..3");
@@ -451,7 +455,7 @@ ekv_status entmaxkv_select(const ekv_cache *cache, int32_t n_q_heads, const floa
                            const float *sigma2, const ekv_select_params *sel, float alpha, int32_t *page_idx,
                            int32_t *n_sel, int32_t sel_stride, double *tau_hat, void *workspace, void *stream) {
     (void)workspace;
-    begin_call();
+    EKV_CALL("entmaxkv_select");
     EKV_TRY(check_cache(cache, n_q_heads));
     EKV_TRY(check_sel(sel, alpha));
     if (!page_idx || !n_sel) return fail(EKV_ERR_INVALID_ARG, "page_idx/n_sel NULL");
@@ -476,7 +480,7 @@ ekv_status entmaxkv_sparse_attend(const ekv_cache *cache, const void *q, int32_t
                                   const int32_t *n_sel, int32_t sel_stride, const double *tau_init,
                                   const ekv_attn_params *attn, float *out, double *tau, int32_t *supp, void *workspace,
                                   void *stream) {
-    begin_call();
+    EKV_CALL("entmaxkv_sparse_attend");
     EKV_TRY(check_cache(cache, n_q_heads));
     EKV_TRY(check_attn(attn));
     if (!q || !page_idx || !n_sel || !out || !workspace) return fail(EKV_ERR_INVALID_ARG, "NULL argument");
@@ -492,7 +496,7 @@ ekv_status entmaxkv_sparse_attend(const ekv_cache *cache, const void *q, int32_t
 
 ekv_status entmaxkv_full_attend(const ekv_cache *cache, const void *q, int32_t n_q_heads, const ekv_attn_params *attn,
                                 float *out, double *tau, int32_t *supp, void *workspace, void *stream) {
-    begin_call();
+    EKV_CALL("entmaxkv_full_attend");
     EKV_TRY(check_cache(cache, n_q_heads));
     EKV_TRY(check_attn(attn));
     if (!q || !out || !workspace) return fail(EKV_ERR_INVALID_ARG, "NULL argument");
@@ -506,7 +510,7 @@ ekv_status entmaxkv_full_attend(const ekv_cache *cache, const void *q, int32_t n
 ekv_status entmaxkv_decode(const ekv_cache *cache, const void *q, int32_t n_q_heads, const ekv_select_params *sel,
                            const ekv_attn_params *attn, float *out, ekv_decode_stats *stats, void *workspace,
                            void *stream) {
-    begin_call();
+    EKV_CALL("entmaxkv_decode");
     EKV_TRY(check_cache(cache, n_q_heads));
     EKV_TRY(check_attn(attn));
     EKV_TRY(check_sel(sel, attn->alpha));

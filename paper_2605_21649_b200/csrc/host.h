@@ -74,6 +74,13 @@ template <typename P> P *at(void *ws, size_t off) { return reinterpret_cast<P *>
 
 int sel_cap(const ekv_cache *c, const ekv_select_params *s);
 void begin_call();                                  // clears the thread's error and launch count
+// NVTX range per C-ABI call (nvtx3, header-only: no cost unless a tool such as nsys / ncu
+// --nvtx is attached); EKV_CALL(name) = begin_call() + a range scoped to the entry point
+struct NvtxRange {
+    explicit NvtxRange(const char *name);
+    ~NvtxRange();
+};
+#define EKV_CALL(name) ::ekvh::NvtxRange ekv_nvtx_range_(name); ::ekvh::begin_call()
 ekv_status check_cache(const ekv_cache *c, int Hq);
 ekv_status check_q(const void *q);
 ekv_status check_attn(const ekv_attn_params *a);

@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
                         int off = incl - __popc(m);
                         for (unsigned mm = m; mm; mm &= mm - 1u) d_items[slot][off++] = (uint8_t)(lane * 8 + __ffs((int)mm) - 1);
                         ni = __shfl_sync(0xffffffffu, incl, SP - 1);
+                        __syncwarp();                  // the lanes' d_items stores before lane 0's release
                     }
                     if (lane == 0) {
                         d_n[slot] = SP;

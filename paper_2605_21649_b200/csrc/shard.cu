@@ -122,7 +122,7 @@ ekv_status entmaxkv_decode_sharded(const ekv_cache *cache, const int32_t *global
                                    int32_t n_q_heads, const ekv_select_params *sel, const ekv_attn_params *attn,
                                    const ekv_comm *comm, float *out, ekv_decode_stats *stats, void *workspace,
                                    void *stream) {
-    begin_call();
+    EKV_CALL("entmaxkv_decode_sharded");
     EKV_TRY(check_cache(cache, n_q_heads));
     EKV_TRY(check_attn(attn));
     EKV_TRY(check_sel(sel, attn->alpha));
