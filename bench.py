@@ -591,6 +591,44 @@ def main():
             del wsg
         except Exception as e:  # reported, the headline stands
             line_extra["gaussian_selector"] = {"error": f"{type(e).__name__}: {e}"}
+        # ---- N4: certified conservative box selection (Prop. B.2) -- exact full-cache entmax
+        try:
+            sc = ekv.select_params("certified", k_pages)
+            wsc = ekv.alloc_workspace(cache, HQ, sc)
+            stc = ekv.DecodeStats(1, HQ, dev, delta_bar=True, gauss=True)
+            oc = torch.empty_like(out)
+            c_us = time_graph(lambda: ekv.decode(cache, q, sc, attn, wsc, out=oc, stats=stc, stream=stream),
+                              max(3, reps // 10))
+            ekv.decode(cache, q, sc, attn, wsc, out=oc, stats=stc, stream=stream)
+            torch.cuda.synchronize()
+            line_extra["certified_selection"] = {
+                "decode_us": c_us, "first_pass_k_pages": k_pages,
+                "coverage": float(stc.n_sel.float().mean().item()) / M,
+                "delta_bar_max": float(stc.delta_bar.max().item()),
+                "maxabs_vs_full": float((oc - full_out).abs().max().item()) if full_out is not None else None,
+                "speedup_vs_full_dense_v": (full_dense_us / c_us) if full_dense_us else None,
+                "note": "Prop. B.2: pages with (alpha-1) box > tau~ of a top-k pass; output = full-cache entmax"}
+            del wsc
+        except Exception as e:
+            line_extra["certified_selection"] = {"error": f"{type(e).__name__}: {e}"}
+        # ---- N4: Gaussian selector at a non-integer beta (alpha = 1.7: beta = 1.43, numerical expectation)
+        try:
+            a17 = ekv.attn_params(1.7)
+            sg = ekv.select_params("gauss", 0, 0.99, 0.0)
+            wsn = ekv.alloc_workspace(cache, HQ, sg)
+            stn = ekv.DecodeStats(1, HQ, dev, delta_bar=False, gauss=True)
+            on = torch.empty_like(out)
+            n_us = time_graph(lambda: ekv.decode(cache, q, sg, a17, wsn, out=on, stats=stn, stream=stream),
+                              max(3, reps // 10))
+            ekv.decode(cache, q, sg, a17, wsn, out=on, stats=stn, stream=stream)
+            torch.cuda.synchronize()
+            line_extra["gaussian_non_integer_beta"] = {
+                "alpha": 1.7, "beta": 1.0 / (float(np.float32(1.7)) - 1.0), "decode_us": n_us,
+                "coverage": float(stn.n_sel.float().mean().item()) / M,
+                "outputs_finite": bool(torch.isfinite(on).all().item())}
+            del wsn
+        except Exception as e:
+            line_extra["gaussian_non_integer_beta"] = {"error": f"{type(e).__name__}: {e}"}
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
     qh_p = q.cpu().pin_memory()
