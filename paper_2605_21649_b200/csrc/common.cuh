@@ -399,6 +399,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // completion and memory (wait) before touching anything the predecessor wrote.  Both are
 // no-ops when the launch carries no programmatic dependency.
 namespace ekv {
+// floor(n / d) for 0 <= n < 2^22, 1 <= d < 2^10 from a precomputed fp32 reciprocal (one
+// correction step each way): no integer-division sequence on latency-critical paths
+__device__ __forceinline__ int qdiv_small(int n, int d, float inv) {
+    int q = __float2int_rz((float)n * inv);
+    q += ((q + 1) * d <= n) ? 1 : 0;
+    q -= (q * d > n) ? 1 : 0;
+    return q;
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 // Every kernel of the decode chain starts with pdl_enter(): it waits for its predecessor (the
@@ -462,7 +470,7 @@ template <int KID> __device__ __forceinline__ void count_cta(bool cond, unsigned
 #define EKV_PH_KERNEL 6
 #endif
 static __device__ unsigned long long ekv_ph[8][1024];
-static __device__ long long ekv_phc[2][1024];
+static __device__ long long ekv_phc[8][1024];
 template <int KID> __device__ __forceinline__ void ph_stamp(int phase) {
     if (KID == EKV_PH_KERNEL && threadIdx.x == 0 && blockIdx.x < 1024) {
         unsigned long long t;
@@ -470,8 +478,15 @@ template <int KID> __device__ __forceinline__ void ph_stamp(int phase) {
         ekv_ph[phase][blockIdx.x] = t;
     }
 }
+template <int KID> __device__ __forceinline__ void ph_stamp_if(bool cond, int phase) {
+    if (KID == EKV_PH_KERNEL && cond && blockIdx.x < 1024) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        ekv_ph[phase][blockIdx.x] = t;
+    }
+}
 template <int KID> __device__ __forceinline__ void ph_count(int which, long long v) {
-    if (KID == EKV_PH_KERNEL && threadIdx.x == 0 && blockIdx.x < 1024) ekv_phc[which][blockIdx.x] = v;
+    if (KID == EKV_PH_KERNEL && (threadIdx.x & 31) == 0 && blockIdx.x < 1024) ekv_phc[which][blockIdx.x] = v;
 }
 // whole-kernel trace: first CTA start (min) and last CTA end (max, thread 0 of each CTA)
 static __device__ unsigned long long ekv_trace[16][2];
@@ -513,6 +528,7 @@ static struct TuDebugReg { TuDebugReg() { debug_register(&tu_debug_read); } } tu
 #else
 #define EKV_TRACE(kid) do {} while (0)
 template <int KID> __device__ __forceinline__ void ph_stamp(int) {}
+template <int KID> __device__ __forceinline__ void ph_stamp_if(bool, int) {}
 template <int KID> __device__ __forceinline__ void ph_count(int, long long) {}
 __device__ __forceinline__ void stamp(int, int) {}
 __device__ __forceinline__ void stamp_if(bool, int, int) {}

@@ -356,18 +356,18 @@ int entmaxkv_debug_trace(unsigned long long *out, int reset) {
     return 0;
 #endif
 }
-/* Debug: per-CTA phase stamps [8][1024] ns and counters [2][1024]. */
+/* Debug: per-CTA phase stamps [8][1024] ns and counters [8][1024]. */
 int entmaxkv_debug_phases(unsigned long long *ph, long long *cnt) {
 #ifdef EKV_STAMPS
     std::vector<unsigned long long> b1(8 * 1024);
-    std::vector<long long> b2(2 * 1024);
+    std::vector<long long> b2(8 * 1024);
     memset(ph, 0, sizeof(unsigned long long) * 8 * 1024);
-    memset(cnt, 0, sizeof(long long) * 2 * 1024);
+    memset(cnt, 0, sizeof(long long) * 8 * 1024);
     for (auto r : debug_readers()) {
         r(2, b1.data(), 0);
         r(3, b2.data(), 0);
         for (int i = 0; i < 8 * 1024; ++i) ph[i] = std::max(ph[i], b1[i]);
-        for (int i = 0; i < 2 * 1024; ++i) cnt[i] = std::max(cnt[i], b2[i]);
+        for (int i = 0; i < 8 * 1024; ++i) cnt[i] = std::max(cnt[i], b2[i]);
     }
     return 1;
 #else

@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
     EKV_TRACE(4);
     pdl_enter();
     pdl_trigger<4>();
+    ph_stamp<4>(0);
     constexpr int SP = AttCfg<T>::SP, NS = AttCfg<T>::NS, TILE = AttCfg<T>::TILE;
     constexpr int NCW = AttCfg<T>::NCW;
     constexpr int CHK = 256;                // work slots per producer chunk (8 per lane)
@@ -104,6 +105,7 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
         if (lane == 0) pref[nrows] = carry;
         __syncwarp();
         tot = pref[nrows];
+        ph_stamp_if<4>(lane == 0, 1);
     }
     const long long f0 = tot * blockIdx.x / gridDim.x, f1 = tot * (blockIdx.x + 1) / gridDim.x;
     if (threadIdx.x == 0) {
@@ -113,53 +115,80 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
     __syncthreads();
     if (warp == NCW) {
         // ------------------------------------------------ producer
+        ph_stamp_if<4>(lane == 0, 7);
         const unsigned char *Kb = reinterpret_cast<const unsigned char *>(c.K);
         int si = 0, fill = 0;
-        int cu = (int)(f0 / ucap), cs = (int)(f0 % ucap);   // (row or unit, slot) of the chunk start
-        int brow = 0;                                        // balanced: row of the chunk start
-        if (bal) {                                           // last row with pref <= f0 (binary search)
-            int lo = 0, hi = nrows - 1;
-            while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (pref[mid] <= f0) lo = mid; else hi = mid - 1; }
-            brow = lo;
+        const int hkv = c.Hkv;
+        const float inv_hq = 1.0f / (float)Hq, inv_hkv = 1.0f / (float)hkv;
+        // The producer is one warp: its index arithmetic is latency, not throughput -- no integer
+        // divisions by runtime values (27 of them, and a per-element row search, cost ~7500
+        // cycles before the first copy) and every round of loads in flight at once.
+        int cu = 0, cs = 0, urow = 0;        // unbalanced: (row or unit, slot) of the chunk start; balanced: lane's row
+        if (bal) {                           // row of the range start: fixed-depth search (warp-uniform)
+            int lo = 0;
+#pragma unroll
+            for (int stp = kMaxRowsBal / 2; stp > 0; stp >>= 1) {
+                const int m = lo + stp;
+                lo = (m < nrows && pref[m] <= f0) ? m : lo;
+            }
+            urow = lo;
+        } else {
+            cu = (int)(f0 / ucap);
+            cs = (int)(f0 - (long long)cu * ucap);
         }
         for (long long cb = f0; cb < f1; cb += CHK) {
-            int un[CHK / 32], pg[CHK / 32], hg[CHK / 32];
+            const int nr = (int)min((long long)CHK, f1 - cb);      // elements of this chunk
+            int un[CHK / 32], pg[CHK / 32], hg[CHK / 32], rw[CHK / 32], pb[CHK / 32];
             bool ok[CHK / 32];
-            if (bal) { while (brow + 1 < nrows && pref[brow + 1] <= cb) ++brow; }
 #pragma unroll
             for (int r = 0; r < CHK / 32; ++r) {
-                int u = cu, sl = cs + r * 32 + lane;
-                if (bal) {
-                    const int e = (int)(cb + r * 32 + lane);
-                    u = brow;
-                    while (u + 1 < nrows && pref[u + 1] <= e) ++u;
-                    sl = e - pref[u];
-                } else {
-                    while (sl >= ucap) { sl -= ucap; ++u; }
+                int u = 0, sl = 0;
+                ok[r] = r * 32 + lane < nr;
+                if (r * 32 < nr) {                                  // warp-uniform
+                    if (bal) {
+                        const int e = (int)cb + r * 32 + lane;
+                        while (urow + 1 < nrows && pref[urow + 1] <= e) ++urow;   // (rows are long: ~never)
+                        u = urow;
+                        sl = e - pref[u];
+                    } else {
+                        u = cu;
+                        sl = cs + r * 32 + lane;
+                        while (sl >= ucap) { sl -= ucap; ++u; }
+                    }
                 }
-                const int bb = full ? u / c.Hkv : u / Hq;      // u: full -> unit; sparse -> row
-                un[r] = full ? u : bb * c.Hkv + (u % Hq) / G;
-                hg[r] = full ? 0 : (u % Hq) % G;
-                ok[r] = false;
-                pg[r] = 0;
-                if (cb + r * 32 + lane < f1) {
-                    if (full) { pg[r] = sl; ok[r] = sl < n_pages_of(__ldg(c.seq_lens + bb)); }
-                    else if (bal || sl < __ldg(n_sel + u)) { pg[r] = __ldg(page_idx + (size_t)u * stride + sl); ok[r] = true; }
-                }
+                const int bb = qdiv_small(u, full ? hkv : Hq, full ? inv_hkv : inv_hq);   // u: full -> unit; sparse -> row
+                const int hr = u - bb * Hq;
+                rw[r] = u;
+                pb[r] = bb;
+                un[r] = full ? u : bb * hkv + hr / G;
+                hg[r] = full ? 0 : hr % G;
+                pg[r] = sl;
             }
-            cs += CHK;
-            while (cs >= ucap) { cs -= ucap; ++cu; }
+            if (!bal) {
+                cs += CHK;
+                while (cs >= ucap) { cs -= ucap; ++cu; }
+                int lim[CHK / 32];                       // unbalanced rows / full: the row bound first
+#pragma unroll
+                for (int r = 0; r < CHK / 32; ++r)
+                    lim[r] = ok[r] ? __ldg(full ? c.seq_lens + pb[r] : n_sel + rw[r]) : 0;
+#pragma unroll
+                for (int r = 0; r < CHK / 32; ++r) ok[r] = ok[r] && pg[r] < (full ? n_pages_of(lim[r]) : lim[r]);
+            }
+            if (!full) {
+#pragma unroll
+                for (int r = 0; r < CHK / 32; ++r) pg[r] = ok[r] ? __ldg(page_idx + (size_t)rw[r] * stride + pg[r]) : 0;
+            }
+            ph_stamp_if<4>(lane == 0 && cb == f0 && pg[0] >= 0, 2);
             int ph[CHK / 32];
             uint8_t mk[CHK / 32];
 #pragma unroll
             for (int r = 0; r < CHK / 32; ++r) {
-                ph[r] = 0; mk[r] = 0;
-                if (ok[r]) {
-                    ph[r] = __ldg(c.page_table + (size_t)(un[r] / c.Hkv) * c.maxp + pg[r]);
-                    mk[r] = full ? (uint8_t)((1u << G) - 1u)
-                                 : (uint8_t)((__ldg(umask + (size_t)un[r] * W + (pg[r] >> 2)) >> ((pg[r] & 3) * 8)) & 0xffu);
-                }
+                ph[r] = ok[r] ? __ldg(c.page_table + (size_t)pb[r] * c.maxp + pg[r]) : 0;
+                mk[r] = full ? (uint8_t)((1u << G) - 1u)
+                             : ok[r] ? (uint8_t)((__ldg(umask + (size_t)un[r] * W + (pg[r] >> 2)) >> ((pg[r] & 3) * 8)) & 0xffu)
+                                     : (uint8_t)0;
             }
+            ph_stamp_if<4>(lane == 0 && cb == f0 && ph[0] >= 0 && mk[0] < 255, 3);
 #pragma unroll
             for (int r = 0; r < CHK / 32; ++r)      // keep each union page once: lowest selecting head
                 if (ok[r] && !full && (__ffs((int)mk[r]) - 1) != hg[r]) ok[r] = false;
@@ -211,8 +240,9 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
                     __syncwarp();
                     if (lane < SP)
                         bulk_g2s_stream(smem + ((size_t)slot * SP + lane) * TILE,
-                                 Kb + ((size_t)d_phys[slot][lane] * c.Hkv + d_unit[slot][lane] % c.Hkv) * TILE,
+                                 Kb + ((size_t)d_phys[slot][lane] * hkv + (d_unit[slot][lane] - qdiv_small(d_unit[slot][lane], hkv, inv_hkv) * hkv)) * TILE,
                                  TILE, &fullb[slot]);
+                    ph_stamp_if<4>(lane == 0 && si == 0, 4);
                     ++si;
                     fill = 0;
                 }
@@ -236,7 +266,7 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
             __syncwarp();
             if (lane < fill)
                 bulk_g2s_stream(smem + ((size_t)slot * SP + lane) * TILE,
-                         Kb + ((size_t)d_phys[slot][lane] * c.Hkv + d_unit[slot][lane] % c.Hkv) * TILE,
+                         Kb + ((size_t)d_phys[slot][lane] * hkv + (d_unit[slot][lane] - qdiv_small(d_unit[slot][lane], hkv, inv_hkv) * hkv)) * TILE,
                          TILE, &fullb[slot]);
             ++si;
         }
@@ -276,8 +306,10 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
         const int n = d_n[slot];
         stamp_cta<1>(threadIdx.x == 0 && si == 0, 1);
         stamp_if(threadIdx.x == 0 && si < 16, 3, si);
+        ph_stamp_if<4>(threadIdx.x == 0 && si == 0, 5);
         if (n < 0) {
             flush(cu);
+            ph_stamp_if<4>(threadIdx.x == 0, 6);
             stamp_cta<1>(threadIdx.x == 0, 2); count_cta<1>(threadIdx.x == 0, si);
             break;
         }

@@ -1,0 +1,3 @@
+PK=${PK:-4}
+make -j16 EXTRA="-DEKV_STAMPS -DEKV_PH_KERNEL=$PK" all > gpurun_out/build_st.log 2>&1 || tail -20 gpurun_out/build_st.log
+timeout 300 python tools/trace.py 2>&1 | tail -16

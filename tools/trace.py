@@ -83,7 +83,7 @@ for rep in range(3):
 import numpy as np
 L.entmaxkv_debug_phases.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 ph = np.zeros((8, 1024), dtype=np.uint64)
-cn = np.zeros((2, 1024), dtype=np.int64)
+cn = np.zeros((8, 1024), dtype=np.int64)
 L.entmaxkv_debug_phases(ph.ctypes.data, cn.ctypes.data)
 used = [i for i in range(8) if ph[i].any()]
 if used:
@@ -96,4 +96,5 @@ if used:
     last = int(np.argmax(ph[max(used)] * m))
     print('slowest CTA', last, 'phases', [round((int(ph[i][last]) - int(ph[0][last])) / 1e3, 2) for i in used],
           'counters', cn[0][last], cn[1][last])
-    print('counters p50/max', np.percentile(cn[0][m], [50, 100]), np.percentile(cn[1][m], [50, 100]))
+    for i in range(8):
+        if cn[i].any(): print(f'  counter {i}: p50 {np.percentile(cn[i][m], 50):.0f} max {cn[i][m].max()}')
