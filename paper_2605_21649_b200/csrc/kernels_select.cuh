@@ -143,6 +143,30 @@ __device__ __forceinline__ int lin_bin(uint32_t key, float vlo, float sc) {
 }
 // Locate the bin holding the r-th largest element of a kLinNB-bin histogram: out[0] = bin,
 // out[1] = #elements in higher bins, out[2] = the bin's count.  1 <= r <= total.
+// Sample-pivot variant: r is derived from the histogram's total (the valid samples Sv):
+// r = min(Sv, ceil(1.25 k Sv / M) + 16); out[3] = r (0: no valid sample, out[0] = -1).
+template <int NT> __device__ __forceinline__ void lin_find_rp(const uint32_t *lin, int keff, int M, int *sh, int *out) {
+    constexpr int PER = kLinNB / NT;
+    const int t = threadIdx.x;
+    int loc = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) loc += (int)lin[kLinNB - 1 - (t * PER + i)];
+    int tot;
+    const int ex = block_excl_scan<NT>(loc, sh, &tot);
+    const int r = min(tot, (int)ceil(1.25 * (double)keff * (double)tot / (double)M) + 16);
+    if (t == 0) { out[0] = -1; out[3] = r; }
+    if (r >= 1 && ex < r && r <= ex + loc) {
+        int cum = ex;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int bn = kLinNB - 1 - (t * PER + i);
+            const int c = (int)lin[bn];
+            if (cum + c >= r) { out[0] = bn; out[1] = cum; out[2] = c; break; }
+            cum += c;
+        }
+    }
+    __syncthreads();
+}
 template <int NT> __device__ __forceinline__ void lin_find(const uint32_t *lin, int r, int *sh, int *out) {
     constexpr int PER = kLinNB / NT;                  // bins per thread, from the top down
     const int t = threadIdx.x;
@@ -245,8 +269,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict_
         unsigned long long *gc = tk_dyn + kTkCap;      // [kTkCap] the cluster's candidates
         __shared__ uint32_t samp[NT];
         __shared__ uint32_t lin[kLinNB];
-        __shared__ uint32_t linmin;
-        __shared__ int lincnt, linres[3];
+        __shared__ int lincnt, linres[4];
+        __shared__ uint32_t xmax, cmax_sh;           // published: max candidate key of the CTA
         __shared__ unsigned long long tcomp_sh;
         __shared__ int qoff[8], qcnt[8];
         {
@@ -257,21 +281,19 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict_
             samp[t] = sv0;
         }
         for (int i = t; i < NWp * 256; i += NT) (&whist[0][0])[i] = 0u;
-        cl.sync();                                     // (1) samples published (and whist zero)
+        for (int i = t; i < kLinNB; i += NT) lin[i] = 0u;
+        if (t == 0) { xmax = 0u; lincnt = 0; }
+        cl.sync();                                     // (1) samples published (and whist, lin zero)
         ph_stamp<2>(2);
         uint32_t sk[8];
-        int sv = 0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            sk[i] = (i < CL) ? cl.map_shared_rank(samp, i)[t] : 0u;
-            sv += sk[i] != 0u;
-        }
-        const int Sv = block_sum_i<NT>(sv, sh);
-        const int rp = min(Sv, (int)ceil(1.25 * (double)keff * (double)Sv / (double)M) + 16);
-        // pivot: a sample key tp with #{samples >= tp} >= rp -- the smallest sample of the
-        // linear-histogram bin (1024 bins over the samples' value range) holding the rp-th largest
+        for (int i = 0; i < 8; ++i) sk[i] = (i < CL) ? cl.map_shared_rank(samp, i)[t] : 0u;
+        // pivot: tp with #{samples >= tp} >= rp -- the lower edge of the linear-histogram bin
+        // (1024 bins over the samples' value range) holding the rp-th largest sample; rp from
+        // the valid-sample count the histogram's scan yields
         uint32_t tp = 0xffffffffu;
-        if (rp >= 1) {
+        int rp = 0;
+        {
             uint32_t smax = 0u, smin = 0xffffffffu;
 #pragma unroll
             for (int i = 0; i < 8; ++i)
@@ -284,32 +306,48 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict_
                 for (int w = 0; w < NWp; ++w) { smax = max(smax, bits[w]); smin = min(smin, bits[32 + w]); }
             }
             const float vlo = key2f(smin), sc = (float)kLinNB / (key2f(smax) - vlo);
-            if (smax == smin) {
+            if (smin == 0xffffffffu) {
+                // no valid sample: no pivot (radix fallback)
+            } else if (smax == smin) {
                 tp = smax;
+                rp = 1;
             } else if (!(sc > 0.0f && sc < INFINITY)) {
+                int sv = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) sv += sk[i] != 0u;
+                const int Sv = block_sum_i<NT>(sv, sh);
+                rp = min(Sv, (int)ceil(1.25 * (double)keff * (double)Sv / (double)M) + 16);
                 tp = block_kth_largest_agg<NT, 8>(sk, rp, whist, hist[0], sh);
             } else {
-                for (int i = t; i < kLinNB; i += NT) lin[i] = 0u;
-                if (t == 0) linmin = 0xffffffffu;
-                __syncthreads();
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
                     if (sk[i]) atomicAdd(&lin[lin_bin(sk[i], vlo, sc)], 1u);
                 __syncthreads();
-                lin_find<NT>(lin, rp, sh, linres);
+                lin_find_rp<NT>(lin, keff, M, sh, linres);
                 const int B = linres[0];
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    if (sk[i] && lin_bin(sk[i], vlo, sc) == B) atomicMin(&linmin, sk[i]);
-                __syncthreads();
-                tp = linmin;
+                rp = linres[3];
+                if (B == 0) tp = smin;
+                else if (B > 0) {
+                    // every sample of bins >= B is >= the bin's lower edge, less a relative margin
+                    // for lin_bin's two roundings
+                    const float e = vlo + (float)B / sc;
+                    tp = max(f2key(e - (fabsf(e) + fabsf(vlo)) * 1.0e-5f), smin);
+                }
+                for (int i = t; i < kLinNB; i += NT) lin[i] = 0u;     // (read before lin_find's barrier)
             }
         }
         tpiv = tp;
         ph_stamp<2>(3);
         int nc = 0;
+        uint32_t kmx = 0u;
 #pragma unroll
-        for (int j = 0; j < kTkKPT; ++j) nc += (key[j] != 0u && key[j] >= tp) ? 1 : 0;
+        for (int j = 0; j < kTkKPT; ++j) {
+            const bool cnd = key[j] != 0u && key[j] >= tp;
+            nc += cnd ? 1 : 0;
+            kmx = cnd ? max(kmx, key[j]) : kmx;
+        }
+        kmx = __reduce_max_sync(0xffffffffu, kmx);
+        if (lane == 0 && kmx) atomicMax(&xmax, kmx);
         int ntot;
         int pos = block_excl_scan<NT>(nc, sh, &ntot);
 #pragma unroll
@@ -328,10 +366,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict_
         // the CTAs' counts in one round of parallel remote loads (lane q reads CTA q)
         if (t < 32) {
             const int nq = t < CL ? *cl.map_shared_rank(&xch[0], t) : 0;
+            const uint32_t mq = __reduce_max_sync(0xffffffffu, t < CL ? *cl.map_shared_rank(&xmax, t) : 0u);
             int inc = nq;
 #pragma unroll
             for (int o2 = 1; o2 < 8; o2 <<= 1) { const int y = __shfl_up_sync(0xffffffffu, inc, o2); if (t >= o2) inc += y; }
             if (t < 8) { qoff[t] = inc - nq; qcnt[t] = nq; }
+            if (t == 0) cmax_sh = mq;
         }
         __syncthreads();
         const int C = qoff[CL - 1] + qcnt[CL - 1];
@@ -365,14 +405,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict_
             // [tp, max], then a brute-force rank among the (few) composites of the boundary bin
             bool done = false;
             {
-                uint32_t cmax = 0u;
-                for (int i = t; i < C; i += NT) cmax = max(cmax, (uint32_t)(gc[i] >> 32));
-                cmax = block_max_u32<NT>(cmax, bits);
+                const uint32_t cmax = cmax_sh;       // (lin and lincnt were zeroed before barrier (2))
                 const float vlo = key2f(tp), sc = (float)kLinNB / (key2f(cmax) - vlo);
                 if (cmax != tp && sc > 0.0f && sc < INFINITY) {
-                    for (int i = t; i < kLinNB; i += NT) lin[i] = 0u;
-                    if (t == 0) { linmin = 0u; lincnt = 0; }
-                    __syncthreads();
                     for (int i = t; i < C; i += NT) atomicAdd(&lin[lin_bin((uint32_t)(gc[i] >> 32), vlo, sc)], 1u);
                     __syncthreads();
                     lin_find<NT>(lin, keff, sh, linres);
@@ -447,8 +482,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict_
         }
 #ifdef EKV_DBG_TOPK
         if (t == 0 && row == EKV_DBG_TOPK)
-            printf("row %d r %d CL %d M %d keff %d Sv %d rp %d tp %08x C %d nloc %d fast %d tcomp %016llx\n", row, r, CL, M,
-                   keff, Sv, rp, tp, C, xch[0], (int)fast, tcomp);
+            printf("row %d r %d CL %d M %d keff %d rp %d tp %08x C %d nloc %d fast %d tcomp %016llx\n", row, r, CL, M,
+                   keff, rp, tp, C, xch[0], (int)fast, tcomp);
 #endif
         ph_stamp<2>(5);
     }
