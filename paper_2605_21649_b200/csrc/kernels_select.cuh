@@ -151,10 +151,11 @@ template <int NT> __device__ __forceinline__ void lin_find_rp(const uint32_t *li
     int loc = 0;
 #pragma unroll
     for (int i = 0; i < PER; ++i) loc += (int)lin[kLinNB - 1 - (t * PER + i)];
+    if (t == 0) out[0] = -1;                 // (ordered before the finder's write by the scan's barriers)
     int tot;
     const int ex = block_excl_scan<NT>(loc, sh, &tot);
     const int r = min(tot, (int)ceil(1.25 * (double)keff * (double)tot / (double)M) + 16);
-    if (t == 0) { out[0] = -1; out[3] = r; }
+    if (t == 0) out[3] = r;
     if (r >= 1 && ex < r && r <= ex + loc) {
         int cum = ex;
 #pragma unroll
@@ -207,6 +208,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict_
     __shared__ uint32_t bits[256];
     __shared__ int xch[2];                   // published to the cluster: [0] #eq, [1] #selected
     __shared__ int sh[(NT / 32 + 2)];
+    __shared__ int wsc2[2][NT / 32];
     const int b = row / Hq;
     const int base = r * (NT * kTkKPT);
     const float *x = box + (size_t)row * maxp;
@@ -629,25 +631,33 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict_
             bits[wi] = whole ? w : (w | bits[wi]);
         }
     }
+    // the lower ranks' selected pages (fast: counted from this CTA's copy of the candidate list --
+    // every selected page is a candidate -- no cluster exchange), folded into the one-barrier scan
+    int clow = 0;
+    if (fast && r > 0) {
+        const unsigned long long *gc = tk_dyn + kTkCap;
+        const uint32_t inv_base = 0xffffffffu - (uint32_t)base;   // page < base <=> low word > inv_base
+        for (int i = t; i < nfast; i += NT) {
+            const unsigned long long x = gc[i];
+            clow += (x >= tcomp && (uint32_t)(x & 0xffffffffu) > inv_base) ? 1 : 0;
+        }
+    }
     __syncthreads();
     const uint32_t w = t < NT / 2 ? bits[t] : 0u;
-    int tot;
-    const int pos = block_excl_scan<NT>(__popc(w), sh, &tot);
-    int o = pos;
-    if (fast) {
-        // the lower ranks' selected pages, counted from this CTA's copy of the candidate list
-        // (every selected page is a candidate): no cluster exchange
-        if (r > 0) {
-            const unsigned long long *gc = tk_dyn + kTkCap;
-            const uint32_t inv_base = 0xffffffffu - (uint32_t)base;   // page < base <=> low word > inv_base
-            int c = 0;
-            for (int i = t; i < nfast; i += NT) {
-                const unsigned long long x = gc[i];
-                c += (x >= tcomp && (uint32_t)(x & 0xffffffffu) > inv_base) ? 1 : 0;
-            }
-            o += block_sum_i<NT>(c, sh);
-        }
-    } else {
+    int tot, o;
+    {
+        const int pc = __popc(w);
+        int x = pc;
+#pragma unroll
+        for (int o2 = 1; o2 < 32; o2 <<= 1) { const int y = __shfl_up_sync(0xffffffffu, x, o2); if (lane >= o2) x += y; }
+        const int cw = __reduce_add_sync(0xffffffffu, clow);
+        if (lane == 31) { wsc2[0][t >> 5] = x; wsc2[1][t >> 5] = cw; }
+        __syncthreads();
+        const int wv = lane < NWp ? wsc2[0][lane] : 0, cv = lane < NWp ? wsc2[1][lane] : 0;
+        tot = __reduce_add_sync(0xffffffffu, wv);
+        o = __reduce_add_sync(0xffffffffu, lane < (t >> 5) ? wv : 0) + x - pc + __reduce_add_sync(0xffffffffu, cv);
+    }
+    if (!fast) {
         if (t == 0) xch[1] = tot;
         cl.sync();
         if (r > 0) {                                         // sum of the lower ranks' counts
