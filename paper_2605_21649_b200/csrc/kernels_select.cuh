@@ -115,6 +115,21 @@ __device__ uint32_t block_kth_largest_agg(const uint32_t (&key)[CPT], int k, uin
 }
 
 
+// Exclusive block scan with one barrier: warp scans, warp totals published to wb[NT/32], every
+// warp sums the lower warps' totals itself.  The caller keeps a barrier between a scan's reads of
+// wb and the next write of the same buffer.
+template <int NT> __device__ __forceinline__ int block_excl_scan1(int v, int *wb, int *tot) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
+    if (lane == 31) wb[w] = x;
+    __syncthreads();
+    const int wv = lane < NT / 32 ? wb[lane] : 0;
+    *tot = __reduce_add_sync(0xffffffffu, wv);
+    return __reduce_add_sync(0xffffffffu, lane < w ? wv : 0) + x - v;
+}
+
 // ---- value-domain (linear) histogram helpers of the sample-pivot top-k
 constexpr int kLinNB = 1024;
 template <int NT> __device__ __forceinline__ uint32_t block_max_u32(uint32_t v, uint32_t *shu) {
@@ -151,9 +166,9 @@ template <int NT> __device__ __forceinline__ void lin_find_rp(const uint32_t *li
     int loc = 0;
 #pragma unroll
     for (int i = 0; i < PER; ++i) loc += (int)lin[kLinNB - 1 - (t * PER + i)];
-    if (t == 0) out[0] = -1;                 // (ordered before the finder's write by the scan's barriers)
+    if (t == 0) out[0] = -1;                 // (ordered before the finder's write by the scan's barrier)
     int tot;
-    const int ex = block_excl_scan<NT>(loc, sh, &tot);
+    const int ex = block_excl_scan1<NT>(loc, sh, &tot);
     const int r = min(tot, (int)ceil(1.25 * (double)keff * (double)tot / (double)M) + 16);
     if (t == 0) out[3] = r;
     if (r >= 1 && ex < r && r <= ex + loc) {
@@ -175,7 +190,7 @@ template <int NT> __device__ __forceinline__ void lin_find(const uint32_t *lin, 
 #pragma unroll
     for (int i = 0; i < PER; ++i) loc += (int)lin[kLinNB - 1 - (t * PER + i)];
     int tot;
-    const int ex = block_excl_scan<NT>(loc, sh, &tot);
+    const int ex = block_excl_scan1<NT>(loc, sh, &tot);
     if (ex < r && r <= ex + loc) {
         int cum = ex;
 #pragma unroll
@@ -351,7 +366,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict_
         kmx = __reduce_max_sync(0xffffffffu, kmx);
         if (lane == 0 && kmx) atomicMax(&xmax, kmx);
         int ntot;
-        int pos = block_excl_scan<NT>(nc, sh, &ntot);
+        int pos = block_excl_scan1<NT>(nc, sh, &ntot);
 #pragma unroll
         for (int j = 0; j < kTkKPT; ++j) {
             if (key[j] != 0u && key[j] >= tp) {
