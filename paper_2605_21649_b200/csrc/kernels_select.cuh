@@ -409,23 +409,27 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_topk(const float *__restrict_
                 for (int z = 1; z < 8; ++z) q += (z < CL && qoff[z] <= i) ? 1 : 0;
                 tmp[u] = i < C ? cl.map_shared_rank(lc, q)[i - qoff[q]] : 0ull;
             }
+            // T* = the keff-th largest composite: linear histogram of the candidates' values over
+            // [tp, max] (built from the gathered registers), then a brute-force rank among the
+            // (few) composites of the boundary bin.  Every later pass over gc reads only the
+            // thread's own entries i = t + NT u: no barrier for gc itself.
+            const uint32_t cmax = cmax_sh;           // (lin and lincnt were zeroed before barrier (2))
+            const float vlo = key2f(tp), sc = (float)kLinNB / (key2f(cmax) - vlo);
+            const bool linok = cmax != tp && sc > 0.0f && sc < INFINITY;
 #pragma unroll
             for (int u = 0; u < GPT; ++u) {
                 const int i = t + NT * u;
-                if (i < C) gc[i] = tmp[u];
+                if (i < C) {
+                    gc[i] = tmp[u];
+                    if (linok) atomicAdd(&lin[lin_bin((uint32_t)(tmp[u] >> 32), vlo, sc)], 1u);
+                }
             }
-            __syncthreads();                           // gc complete before the passes read it
-            // this CTA's remote reads are done: arrive on the cluster barrier now, wait only at
+            // this thread's remote reads are done: arrive on the cluster barrier now, wait only at
             // exit (the other CTAs' lists stay alive until every CTA has gathered)
             asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-            // T* = the keff-th largest composite: linear histogram of the candidates' values over
-            // [tp, max], then a brute-force rank among the (few) composites of the boundary bin
             bool done = false;
             {
-                const uint32_t cmax = cmax_sh;       // (lin and lincnt were zeroed before barrier (2))
-                const float vlo = key2f(tp), sc = (float)kLinNB / (key2f(cmax) - vlo);
-                if (cmax != tp && sc > 0.0f && sc < INFINITY) {
-                    for (int i = t; i < C; i += NT) atomicAdd(&lin[lin_bin((uint32_t)(gc[i] >> 32), vlo, sc)], 1u);
+                if (linok) {
                     __syncthreads();
                     lin_find<NT>(lin, keff, sh, linres);
                     const int B = linres[0], need = keff - linres[1], cB = linres[2];
