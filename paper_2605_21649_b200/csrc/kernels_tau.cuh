@@ -477,6 +477,78 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
         __syncthreads();
     } else {
 
+    // ---- small candidate sets (<= 32, the usual top-k decode row: z_max - 1 prunes to a few
+    // tokens): one warp does R9 by all pairs, tau and the support list with shuffles -- no
+    // block barrier until PV (each barrier step of the general path below costs ~1000 cycles);
+    // the candidates' V rows are staged in shared memory meanwhile
+    if (ncand >= 1 && ncand <= 32) {
+        if (warp == 0) {
+            const bool have = lane < ncand;
+            const double zl = have ? a * (double)zs[lane] : -INFINITY;
+            if (have) {
+                constexpr int CH = kD * (int)sizeof(T) / 16;          // 16-byte chunks per row
+                const int j = cj[lane];
+                const T *src = Vb + (((size_t)cph[lane] * c.Hkv + kvh) * kP + (j % kP)) * kD;
+                for (int ch = 0; ch < CH; ++ch)
+                    cp_async16(reinterpret_cast<char *>(vpre + (size_t)lane * kD) + 16 * ch,
+                               reinterpret_cast<const char *>(src) + 16 * ch);
+            }
+            cp_async_commit();
+            auto wsum = [&](double x) {
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                return x;
+            };
+            double F = 0.0;                          // R9: F(z_j) = sum_i (z_i - z_j)_+^beta
+            for (int i = 0; i < ncand; ++i) {
+                const double d = __shfl_sync(0xffffffffu, zl, i) - zl;
+                if (d > 0.0) F += powB<IB>(d, beta);
+            }
+            const bool in = have && F < 1.0;
+            const double S1 = wsum(in ? zl : 0.0), kk = wsum(in ? 1.0 : 0.0);
+            double tau;
+            if constexpr (IB == 1) {
+                tau = (S1 - 1.0) / kk;
+            } else if constexpr (IB == 2) {
+                const double m = S1 / kk;
+                const double ss = wsum(in ? (zl - m) * (zl - m) : 0.0);
+                tau = m - sqrt(fmax(0.0, 1.0 - ss) / kk);
+            } else {
+                // Newton on sum_S (z - t)^beta = 1 from the largest z outside S (or tau_lo): F >= 1
+                // there, so the iteration is monotone from the left
+                double t0 = (have && !in) ? zl : tau_lo;
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) t0 = fmax(t0, __shfl_xor_sync(0xffffffffu, t0, o));
+                tau = t0;
+                for (int it = 0; it < 60; ++it) {
+                    const double dd = zl - tau;
+                    const double Fs = wsum(in ? powB<IB>(dd, beta) : 0.0), Fd = wsum(in ? powBm1<IB>(dd, beta) : 0.0);
+                    if (!(Fd > 0.0)) break;
+                    const double step = lbeta_step(Fs, Fd, beta, IB);
+                    tau += step;
+                    if (!(fabs(step) > 1e-15 * fmax(1.0, fabs(tau)))) break;
+                }
+                const double dd = zl - tau;
+                const double Fs = wsum(in ? powB<IB>(dd, beta) : 0.0), Fd = wsum(in ? powBm1<IB>(dd, beta) : 0.0);
+                if (Fd > 0.0) tau += (Fs - 1.0) / (beta * Fd);
+            }
+            // support entries in candidate order (= token order), V rows staged (mode 2)
+            const unsigned bal = __ballot_sync(0xffffffffu, in);
+            const int pos = __popc(bal & ((1u << lane) - 1u));
+            double pd = 0.0;
+            if (in) {
+                const double d = zl - tau;
+                pd = d > 0.0 ? powB<IB>(d, beta) : 0.0;
+                sup_j[pos] = lane;
+                sup_phys[pos] = cph[lane];
+                sup_p[pos] = (float)pd;
+            }
+            if (have) cin[lane] = in ? 1 : 0;
+            const double psum = wsum(pd);
+            if (lane == 0) { s_tau = tau; s_kk = kk; s_nsup = __popc(bal); s_mode = 2; s_psum = psum; }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+        }
+    } else {
     // ---- 2. fp32 Newton steps (pruning point only)
     float tf = (float)tau_lo;
     for (int it = 0; it < 3; ++it) {      // Newton from the left: every iterate is below tau
@@ -763,6 +835,7 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
             s_mode = one_round ? (staged ? 2 : 1) : 0;
         }
     }
+    }   // general path
     }   // exact tau
     if (staged) cp_async_commit_wait_all();
     __syncthreads();
