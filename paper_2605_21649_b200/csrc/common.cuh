@@ -244,6 +244,21 @@ __device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long 
     *tot = sh[NT / 32 - 1];
     return base + x - v;
 }
+// Exclusive block scan with one barrier: warp scans, warp totals published to wb[NT/32], every
+// warp sums the lower warps' totals itself.  The caller keeps a barrier between a scan's reads of
+// wb and the next write of the same buffer.
+template <int NT> __device__ __forceinline__ int block_excl_scan1(int v, int *wb, int *tot) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
+    if (lane == 31) wb[w] = x;
+    __syncthreads();
+    const int wv = lane < NT / 32 ? wb[lane] : 0;
+    *tot = __reduce_add_sync(0xffffffffu, wv);
+    return __reduce_add_sync(0xffffffffu, lane < w ? wv : 0) + x - v;
+}
+
 template <int NT> __device__ __forceinline__ int block_excl_scan(int v, int *sh, int *tot) {
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     int x = v;

@@ -115,21 +115,6 @@ __device__ uint32_t block_kth_largest_agg(const uint32_t (&key)[CPT], int k, uin
 }
 
 
-// Exclusive block scan with one barrier: warp scans, warp totals published to wb[NT/32], every
-// warp sums the lower warps' totals itself.  The caller keeps a barrier between a scan's reads of
-// wb and the next write of the same buffer.
-template <int NT> __device__ __forceinline__ int block_excl_scan1(int v, int *wb, int *tot) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    int x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
-    if (lane == 31) wb[w] = x;
-    __syncthreads();
-    const int wv = lane < NT / 32 ? wb[lane] : 0;
-    *tot = __reduce_add_sync(0xffffffffu, wv);
-    return __reduce_add_sync(0xffffffffu, lane < w ? wv : 0) + x - v;
-}
-
 // ---- value-domain (linear) histogram helpers of the sample-pivot top-k
 constexpr int kLinNB = 1024;
 template <int NT> __device__ __forceinline__ uint32_t block_max_u32(uint32_t v, uint32_t *shu) {

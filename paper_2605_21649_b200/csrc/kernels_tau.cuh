@@ -220,6 +220,8 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
 
     // ---- 1. candidates {z > tau_lo} (returns -1 on overflow; uniform)
     // items [lo, min(hi, 4 nlist)) in rounds of U * NT; candidates compacted in item order
+    __shared__ int s_xw[2][NW];              // extraction scans: warp totals, alternating rounds
+    int xr = 0;
     auto extract = [&](double tlo, bool have_pg, int lo, int hi) -> int {
         const float thr_c = (float)(tlo / a);
         const float thr_f = thr_c - 1e-6f * fmaxf(1.0f, fabsf(thr_c));   // conservative fp32 pre-test
@@ -248,7 +250,8 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
                 }
             }
             int tot;
-            int pos = n + block_excl_scan<NT>(__popc(bits), shi, &tot);
+            int pos = n + block_excl_scan1<NT>(__popc(bits), s_xw[xr & 1], &tot);   // (alternating buffers)
+            ++xr;
             if (n + tot > cap) return -1;
             if (bits) {
 #pragma unroll
@@ -358,14 +361,11 @@ __global__ void __launch_bounds__(kTsNT, 2) k_tau_sparse(CacheView c, TauArgs A)
             __shared__ int s_cnt;
             if (threadIdx.x == 0) s_cnt = ncand;
             cl.sync();
-            int tot = 0, off = 0;
-            bool ovf = false;
-            for (int q = 0; q < CL; ++q) {
-                const int nq = *cl.map_shared_rank(&s_cnt, q);
-                if (nq < 0) ovf = true;
-                if (q < rk) off += nq;
-                tot += nq;
-            }
+            // the ranks' counts: lane q reads rank q (one round of remote loads, not CL in a row)
+            const int nq = lane < CL ? *cl.map_shared_rank(&s_cnt, lane) : 0;
+            const int tot = __reduce_add_sync(0xffffffffu, nq);
+            const int off = __reduce_add_sync(0xffffffffu, lane < rk ? nq : 0);
+            bool ovf = __any_sync(0xffffffffu, nq < 0);
             if (tot > cap) ovf = true;
             if (!ovf && rk > 0 && ncand > 0) {
                 float *zs0 = cl.map_shared_rank(zs, 0);
