@@ -115,3 +115,49 @@ def test_entmax_ties_at_support_boundary(alpha, where, dtype):
         assert all(ins) or not any(ins), (h, ins)
         np.testing.assert_allclose(out[0, h], ref["o"], atol=tol_for(dtype), rtol=0)
         assert abs(float(st.tau[0, h]) - ref["tau"]) <= 1e-6 * max(1.0, abs(ref["tau"]))
+
+
+@pytest.mark.parametrize("alpha", [1.5, 2.0, 1.25, 1.7])
+@pytest.mark.parametrize("ncand", [1, 31, 32, 33, 64])
+def test_tau_candidate_count_boundary(alpha, ncand):
+    """The tau kernel solves rows with <= 32 candidates (z > z_max - 1) in one warp and larger
+    ones on the block path: exactly ncand tokens are placed within 1 / (alpha - 1) of the
+    maximum score (the rest far below), so both paths and the switch between them are hit;
+    output, tau and the support set against the oracle."""
+    B, n, Hq, Hkv = 1, 700, 2, 1
+    wl = make_workload(B, n, Hq, Hkv, dtype=torch.float32, seed=91)
+    g = torch.Generator().manual_seed(ncand)
+    a = alpha - 1.0
+    K = torch.zeros_like(wl.K)
+    pt = wl.page_table[0]
+    near = torch.randperm(n, generator=g)[:ncand].tolist()
+    for j in range(n):
+        # head 0 scores ~ key[0]: the near tokens spread over (z_max - 0.9 / a, z_max], the rest
+        # 5 / a below (z = a s); head 1 sees key[1] (random, unconstrained)
+        v = (4.0 - 0.9 * torch.rand(1, generator=g).item() / a) if j in near else (4.0 - 5.0 / a)
+        K[int(pt[j // 16]), 0, j % 16, 0] = v
+        K[int(pt[j // 16]), 0, j % 16, 1] = torch.randn(1, generator=g).item()
+    K[int(pt[near[0] // 16]), 0, near[0] % 16, 0] = 4.0            # the maximum
+    wl.K = K.contiguous()
+    cd = float(np.float32(1.0 / np.sqrt(128.0)))
+    q = torch.zeros(B, Hq, 128, dtype=torch.float32)
+    q[0, 0, 0] = 1.0 / cd
+    q[0, 1, 1] = 1.0 / cd
+    wl.q = q
+    dc, hc = device_cache(wl), host_cache(wl)
+    qh = q_host(wl)
+    M = hc.n_pages(0)
+    sel = ekv.select_params("topk", M)
+    ws = ekv.alloc_workspace(dc, Hq, sel)
+    st = ekv.DecodeStats(B, Hq, "cuda", supp_cap=4096)
+    out = ekv.decode(dc, wl.q.cuda(), sel, ekv.attn_params(alpha), ws, stats=st)
+    torch.cuda.synchronize()
+    out = out.cpu().numpy()
+    for h in range(Hq):
+        ref = hc.attend(qh[0, h], 0, 0, np.arange(M, dtype=np.int32), alpha, want_p=True, want_s=True)
+        if h == 0:
+            z = a * ref["s"].astype(np.float64)
+            assert int(np.sum(z > z.max() - 1.0)) == ncand             # the premise: ncand candidates
+        assert st.support(0, h).cpu().tolist() == np.nonzero(ref["p"])[0].tolist(), (h, ncand)
+        np.testing.assert_allclose(out[0, h], ref["o"], atol=1e-5, rtol=0)
+        assert abs(float(st.tau[0, h]) - ref["tau"]) <= 1e-6 * max(1.0, abs(ref["tau"]))
