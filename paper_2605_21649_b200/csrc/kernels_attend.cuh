@@ -107,7 +107,17 @@ __global__ void __launch_bounds__(32 * (AttCfg<T>::NCW + 1), sizeof(T) == 2 ? 2 
         tot = pref[nrows];
         ph_stamp_if<4>(lane == 0, 1);
     }
-    const long long f0 = tot * blockIdx.x / gridDim.x, f1 = tot * (blockIdx.x + 1) / gridDim.x;
+    // the CTA's range of the flattened work space (32-bit arithmetic when it fits: the 64-bit
+    // division sequence sits on the producer's critical path)
+    long long f0, f1;
+    if (tot * ((long long)gridDim.x + 1) < (1ll << 32)) {
+        const unsigned t32 = (unsigned)tot;
+        f0 = (long long)(t32 * blockIdx.x / gridDim.x);
+        f1 = (long long)(t32 * (blockIdx.x + 1) / gridDim.x);
+    } else {
+        f0 = tot * blockIdx.x / gridDim.x;
+        f1 = tot * (blockIdx.x + 1) / gridDim.x;
+    }
     if (threadIdx.x == 0) {
         for (int i = 0; i < NS; ++i) { mbar_init(&fullb[i], 1); mbar_init(&emptyb[i], NCW); }
         fence_mbar_init();
