@@ -159,9 +159,34 @@ __global__ void __launch_bounds__(256, 2) k_dense_group_partial(CacheView c, con
     for (int pg = i0 + warp; pg < min(nlist, i0 + kSmxPages); pg += 8) {
         const int phys = __ldg(c.page_table + (size_t)b * c.maxp + pg);
         const int nt = min(kP, L - pg * kP);
-        float sv[G];
+        // the page's weights once per (token, head): lane l computes token l % 16 for every head
+        // (both lane halves: no shuffle to fill the upper half), the token loop broadcasts them
+        const int tw = lane & (kP - 1);
+        float pw[G];
 #pragma unroll
-        for (int g = 0; g < G; ++g) sv[g] = (lane < kP) ? scores[(size_t)(row0 + g) * ntok + (size_t)pg * kP + lane] : -INFINITY;
+        for (int g = 0; g < G; ++g) {
+            const float s = scores[(size_t)(row0 + g) * ntok + (size_t)pg * kP + tw];
+            float p = 0.f;
+            if (live[g] && tw < nt && s != -INFINITY) {
+                if (ent_tau) {
+                    const double d = a * (double)s - tau[g];
+                    double w = 0.0;
+                    if (d > 0.0) {
+                        if (ib == 1) w = d;
+                        else if (ib == 2) w = d * d;
+                        else if (ib == 3) w = d * d * d;
+                        else if (ib == 4) { const double d2 = d * d; w = d2 * d2; }
+                        else w = pow(d, 1.0 / a);
+                    }
+                    p = (float)w;
+                    if (lane < kP) l[g] += w;
+                } else {
+                    p = expf(s - smax[g]);
+                    if (lane < kP) l[g] += (double)p;
+                }
+            }
+            pw[g] = p;
+        }
         const T *vp = Vb + ((size_t)phys * c.Hkv + kvh) * kP * kD + 8 * cdim;
         // raw 16-byte words in flight (bf16: 8 dims; fp32: 4 dims, two words per row)
         constexpr int WPR = sizeof(T) == 2 ? 1 : 2;
@@ -189,26 +214,7 @@ __global__ void __launch_bounds__(256, 2) k_dense_group_partial(CacheView c, con
             }
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                const float s = __shfl_sync(0xffffffffu, sv[g], t);
-                float p = 0.f;
-                double w = 0.0;
-                if (live[g] && t < nt && s != -INFINITY) {
-                    if (ent_tau) {
-                        const double d = a * (double)s - tau[g];
-                        if (d > 0.0) {
-                            if (ib == 1) w = d;
-                            else if (ib == 2) w = d * d;
-                            else if (ib == 3) w = d * d * d;
-                            else if (ib == 4) { const double d2 = d * d; w = d2 * d2; }
-                            else w = pow(d, 1.0 / a);
-                        }
-                        p = (float)w;
-                    } else {
-                        p = expf(s - smax[g]);
-                        w = (double)p;
-                    }
-                }
-                if (cdim == 0) l[g] += w;
+                const float p = __shfl_sync(0xffffffffu, pw[g], t);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) acc[g][e] = __fmaf_rn(p, vx[0][e], acc[g][e]);
             }
@@ -220,7 +226,8 @@ __global__ void __launch_bounds__(256, 2) k_dense_group_partial(CacheView c, con
     for (int g = 0; g < G; ++g) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[g][e] = __fadd_rn(acc[g][e], __shfl_xor_sync(0xffffffffu, acc[g][e], 16));
-        l[g] += __shfl_xor_sync(0xffffffffu, l[g], 16);
+#pragma unroll
+        for (int o = 8; o >= 1; o >>= 1) l[g] += __shfl_xor_sync(0xffffffffu, l[g], o);   // lanes 0..15: a token each
     }
     for (int g = 0; g < G; ++g) {
         if (lane < 16) {
