@@ -117,8 +117,11 @@ template <typename T> __device__ __forceinline__ void ldv8(const T *p, float (&x
 // Layout for memory-level parallelism: a warp takes a page; lane = (token parity h, 8-dim
 // chunk c): its 8 loads of 16 bytes (tokens 2 i + h) go out together, then the weights.
 // Writes the same per-(row, chunk) partials as k_softmax_partial.
+#ifndef EKV_DG_CTAS
+#define EKV_DG_CTAS 2
+#endif
 template <typename T, int G>
-__global__ void __launch_bounds__(256, 2) k_dense_group_partial(CacheView c, const float *__restrict__ scores, size_t ntok,
+__global__ void __launch_bounds__(256, EKV_DG_CTAS) k_dense_group_partial(CacheView c, const float *__restrict__ scores, size_t ntok,
                                                              const uint32_t *__restrict__ rowmax, int Hq, int nch,
                                                              float *__restrict__ pacc, double *__restrict__ pl,
                                                              int32_t *__restrict__ pcnt,
