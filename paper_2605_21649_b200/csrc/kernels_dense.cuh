@@ -1,6 +1,7 @@
 // kernels_dense.cuh -- a6 (softmax over the same kernels) and the dense-V pass of the a5
 // full-cache baseline: split flash-decoding style partials + an ordered combine.
 #pragma once
+#include <type_traits>
 #include "kernels_attend.cuh"
 
 namespace ekv {
@@ -39,31 +40,51 @@ __global__ void __launch_bounds__(256) k_softmax_partial(CacheView c, const floa
     int cnt = 0;
     const int i0 = ch * kSmxPages;
     if (mk && i0 < nlist) {
-        // warp w: list pages i0 + w, i0 + w + 8, ...; the 16 tokens of a page, 4 V rows in flight
+        // warp w: list pages i0 + w, i0 + w + 8, ...; per page the 16 tokens' weights are
+        // computed once (lane t: token t) and broadcast, and all 16 V rows are in flight at once
         for (int ii = i0 + warp; ii < min(nlist, i0 + kSmxPages); ii += 8) {
             const int pg = full ? ii : __ldg(page_idx + (size_t)row * stride + ii);
             const int phys = __ldg(c.page_table + (size_t)b * c.maxp + pg);
-            const float sv = (lane < kP) ? srow[(size_t)pg * kP + lane] : -INFINITY;
-            const T *vp = Vb + ((size_t)phys * c.Hkv + kvh) * kP * kD + 4 * lane;
-#pragma unroll 4
-            for (int t = 0; t < kP; ++t) {
-                const float s = __shfl_sync(0xffffffffu, sv, t);
-                if (pg * kP + t >= L || s == -INFINITY) continue;        // warp-uniform
-                float p;
+            const int tl = lane & (kP - 1);
+            const float sv = srow[(size_t)pg * kP + tl];
+            const bool tv = lane < kP && pg * kP + tl < L && sv != -INFINITY;
+            float pw = 0.f;
+            if (tv) {
                 if (ent_tau) {
-                    const double a = (double)alpha - 1.0, d = a * (double)s - ent_tau[row];
-                    p = d > 0.0 ? (float)pow(d, 1.0 / a) : 0.0f;
+                    const double a = (double)alpha - 1.0, d = a * (double)sv - ent_tau[row];
+                    pw = d > 0.0 ? (float)pow(d, 1.0 / a) : 0.0f;
                 } else {
-                    p = expf(s - smax);
+                    pw = expf(sv - smax);
                 }
-                float vx[4];
-                ldv4<T>(vp + (size_t)t * kD, vx);
+                l += (double)pw;
+                ++cnt;
+            }
+            const T *vp = Vb + ((size_t)phys * c.Hkv + kvh) * kP * kD + 4 * lane;
+            const int nt = min(kP, L - pg * kP);
+            using W = typename std::conditional<sizeof(T) == 2, uint2, float4>::type;
+            W raw[kP];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) acc[q] = __fmaf_rn(p, vx[q], acc[q]);
-                if (lane == 0) { l += (double)p; ++cnt; }
+            for (int t = 0; t < kP; ++t)
+                if (t < nt) raw[t] = *reinterpret_cast<const W *>(vp + (size_t)t * kD);
+#pragma unroll
+            for (int t = 0; t < kP; ++t) {
+                const float p = __shfl_sync(0xffffffffu, pw, t);
+                if (t < nt && p != 0.f) {
+                    float vx[4];
+                    if constexpr (sizeof(T) == 2) {
+                        vx[0] = bf_lo(raw[t].x); vx[1] = bf_hi(raw[t].x); vx[2] = bf_lo(raw[t].y); vx[3] = bf_hi(raw[t].y);
+                    } else {
+                        vx[0] = raw[t].x; vx[1] = raw[t].y; vx[2] = raw[t].z; vx[3] = raw[t].w;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[q] = __fmaf_rn(p, vx[q], acc[q]);
+                }
             }
         }
     }
+    // per-token weights and counts were taken by lanes 0..15
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) { l += __shfl_xor_sync(0xffffffffu, l, o); cnt += __shfl_xor_sync(0xffffffffu, cnt, o); }
 #pragma unroll
     for (int q = 0; q < 4; ++q) red[warp][4 * lane + q] = acc[q];
     if (lane == 0) { wl[warp] = l; wc[warp] = cnt; }
