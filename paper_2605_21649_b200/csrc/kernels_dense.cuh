@@ -104,26 +104,43 @@ __global__ void __launch_bounds__(256) k_softmax_partial(CacheView c, const floa
     }
 }
 
-static __global__ void __launch_bounds__(128) k_softmax_combine(const float *__restrict__ pacc, const double *__restrict__ pl,
+// Ordered combine of the chunk partials: kCombSeg segments of the chunk range per row, one
+// thread per (segment, dim); the segment sums are added in segment order (deterministic).
+constexpr int kCombSeg = 8;
+static __global__ void __launch_bounds__(128 * kCombSeg) k_softmax_combine(const float *__restrict__ pacc, const double *__restrict__ pl,
                                                          const int32_t *__restrict__ pcnt, const uint32_t *__restrict__ rowmax,
                                                          int nch, float *__restrict__ out, double *__restrict__ tau,
                                                          int32_t *__restrict__ supp) {
     pdl_enter();
+    __shared__ float so[kCombSeg][kD];
+    __shared__ double sl[kCombSeg];
+    __shared__ int sc[kCombSeg];
     const int row = blockIdx.x;
-    const uint32_t mk = rowmax[row];
+    const int d = threadIdx.x % kD, seg = threadIdx.x / kD;
+    const int c0 = nch * seg / kCombSeg, c1 = nch * (seg + 1) / kCombSeg;
     float o = 0.f;
     double l = 0.0;
     int cnt = 0;
-    for (int ch = 0; ch < nch; ++ch) {
+#pragma unroll 8
+    for (int ch = c0; ch < c1; ++ch) {
         const size_t i = (size_t)row * nch + ch;
-        o = __fadd_rn(o, pacc[i * kD + threadIdx.x]);
-        l += pl[i];
-        cnt += pcnt[i];
+        o = __fadd_rn(o, pacc[i * kD + d]);
+        if (d == 0) { l += pl[i]; cnt += pcnt[i]; }
     }
-    out[(size_t)row * kD + threadIdx.x] = (mk && l > 0.0) ? (float)((double)o / l) : 0.0f;
-    if (threadIdx.x == 0) {             // (entmax dense-V: tau / supp come from the tau kernel)
-        if (tau) tau[row] = mk ? (double)key2f(mk) + log(l) : NAN;
-        if (supp) supp[row] = cnt;
+    so[seg][d] = o;
+    if (d == 0) { sl[seg] = l; sc[seg] = cnt; }
+    __syncthreads();
+    if (seg == 0) {
+        const uint32_t mk = rowmax[row];
+        float ot = 0.f;
+        double lt = 0.0;
+        int ct = 0;
+        for (int q = 0; q < kCombSeg; ++q) { ot = __fadd_rn(ot, so[q][d]); lt += sl[q]; ct += sc[q]; }
+        out[(size_t)row * kD + d] = (mk && lt > 0.0) ? (float)((double)ot / lt) : 0.0f;
+        if (d == 0) {                     // (entmax dense-V: tau / supp come from the tau kernel)
+            if (tau) tau[row] = mk ? (double)key2f(mk) + log(lt) : NAN;
+            if (supp) supp[row] = ct;
+        }
     }
 }
 }  // namespace ekv

@@ -147,7 +147,7 @@ ekv_status launch_vstream(const CacheView &v, uint32_t *sink, cudaStream_t st) {
 ekv_status launch_softmax_combine(int rows, const float *pacc, const double *pl, const int32_t *pc,
                                   const uint32_t *rowmax, int nch, float *out, double *tau, int32_t *supp,
                                   cudaStream_t st) {
-    k_softmax_combine<<<rows, 128, 0, st>>>(pacc, pl, pc, rowmax, nch, out, tau, supp);
+    k_softmax_combine<<<rows, 128 * kCombSeg, 0, st>>>(pacc, pl, pc, rowmax, nch, out, tau, supp);
     return check_launch("k_softmax_combine");
 }
 
